@@ -1,0 +1,155 @@
+"""Pins of the oracle's replay + schedule (or_run: O2, O8-O12) against hand-built
+serial loops over the individually pinned primitives.
+
+The primitives (sampler, targets, gradient, RMSProp) are pinned in
+test_oracle_pins.py; here the loops re-derive Alg. 1 / Alg. 2 step by step so a
+wrong fetch/push/refresh order, a wrong accumulation or a wrong replay slot in
+or_run fails.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+import synth
+from tests.test_oracle_pins import TINY, he_theta
+
+CAP = 40
+
+
+def make_replays(n_rep, n_push_each, seed, net=TINY):
+    out = []
+    for k in range(n_rep):
+        s, a, r, sn, t = synth.g_uniform(n_push_each, net.frames, net.height, net.width, net.n_actions, seed + k)
+        out.append(O.Replay(s, a, r.astype(np.float64), sn, t))
+    return out
+
+
+def ring_view(rp, cap):
+    """last-N ring contents: push i -> slot i mod cap."""
+    n = len(rp.a)
+    slot_of = {}
+    for i in range(n):
+        slot_of[i % cap] = i
+    size = min(n, cap)
+    return [slot_of[sl] for sl in range(size)]
+
+
+def serial_reference(cfg, replays, theta0, steps, cap, net=TINY):
+    """Alg. 1 x N + Alg. 2 written out: fetch every n_fetch, refresh when n-l >= C,
+    accumulate, mean over N*n_push, one RMSProp per round."""
+    N, b = cfg.n_replicas, cfg.minibatch
+    theta = theta0.copy()
+    r = np.zeros_like(theta)
+    n = 0
+    th_local = [theta0.copy() for _ in range(N)]
+    th_hat = [theta0.copy() for _ in range(N)]
+    n_loc = [0] * N
+    ell = [0] * N
+    acc = [np.zeros_like(theta) for _ in range(N)]
+    views = [ring_view(rp, cap) for rp in replays]
+    for T in range(steps):
+        for k in range(N):
+            if T % cfg.n_fetch == 0:
+                th_local[k] = theta.copy()
+                n_loc[k] = n
+                if n_loc[k] - ell[k] >= cfg.target_sync:
+                    th_hat[k] = th_local[k].copy()
+                    ell[k] = n_loc[k]
+            rp, view = replays[k], views[k]
+            idx = [view[O.sample_index(cfg.seed, k, T, j, len(view))] for j in range(b)]
+            y, _ = O.targets(net, th_hat[k], rp.s_next[idx], rp.r[idx], rp.term[idx], cfg.gamma)
+            _, g = O.loss_grad(net, th_local[k], rp.s[idx], rp.a[idx], y, cfg.err_clip)
+            acc[k] += g
+        if (T + 1) % cfg.n_push == 0:
+            gbar = sum(acc) / (N * cfg.n_push)
+            theta, r = O.rmsprop(theta, r, gbar, cfg.lr, cfg.rms_decay, cfg.rms_eps)
+            n += 1
+            acc = [np.zeros_like(theta) for _ in range(N)]
+    return theta, r, n
+
+
+@pytest.mark.parametrize("N,n_push,n_fetch,C", [
+    (1, 1, 1, 10**9),   # serial DQN (Alg. 1 with a fixed target)
+    (1, 1, 1, 1),       # C = 1: standard Q-learning targets
+    (1, 1, 1, 2),
+    (2, 1, 1, 3),       # Downpour deterministic, N = 2
+    (3, 2, 1, 2),       # accumulate over 2 steps
+    (2, 1, 3, 1),       # stale local model between fetches
+    (2, 3, 2, 2),
+])
+def test_run_equals_serial_loop(N, n_push, n_fetch, C):
+    cfg = O.TrainCfg(n_replicas=N, minibatch=3, n_push=n_push, n_fetch=n_fetch, target_sync=C, lr=1e-2,
+                     gamma=0.9)
+    replays = make_replays(N, 50, 100)  # 50 pushes into a 40-slot ring: wraps
+    theta0 = he_theta(TINY, 3)
+    steps = 6
+    out = O.run(TINY, cfg, CAP, replays, theta0, steps)
+    assert out["rc"] == 0
+    th, r, n = serial_reference(cfg, replays, theta0, steps, CAP)
+    assert out["n"] == n == steps // n_push
+    np.testing.assert_allclose(out["theta"], th, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(out["r"], r, rtol=1e-12, atol=1e-18)
+
+
+def test_n_replicas_equal_one_batch_of_N_b():
+    # A7: with n_push = n_fetch = 1, N replicas == serial DQN with batch N*b on the
+    # concatenation of the replicas' minibatches (to fp64 summation order)
+    N, b = 3, 2
+    cfg = O.TrainCfg(n_replicas=N, minibatch=b, lr=5e-3, gamma=0.95, target_sync=10**9)
+    replays = make_replays(N, 30, 7)
+    theta0 = he_theta(TINY, 5)
+    out = O.run(TINY, cfg, CAP, replays, theta0, 2)
+    theta, r = theta0.copy(), np.zeros_like(theta0)
+    for T in range(2):
+        S, A, Y = [], [], []
+        for k in range(N):
+            rp = replays[k]
+            idx = [O.sample_index(cfg.seed, k, T, j, 30) for j in range(b)]
+            y, _ = O.targets(TINY, theta0, rp.s_next[idx], rp.r[idx], rp.term[idx], cfg.gamma)
+            S.append(rp.s[idx]); A.append(rp.a[idx]); Y.append(y)
+        _, g = O.loss_grad(TINY, theta, np.concatenate(S), np.concatenate(A), np.concatenate(Y))
+        theta, r = O.rmsprop(theta, r, g, cfg.lr)
+    np.testing.assert_allclose(out["theta"], theta, rtol=0, atol=1e-12)
+
+
+def test_targets_fixed_between_refreshes():
+    # targets do not move with the live theta while theta^ is held; with
+    # gamma = 0 the live-theta path cannot leak into y, so loss reveals r only.
+    net = O.Net(frames=1, height=2, width=2, convs=(), fcs=(), n_actions=2)
+    P = O.param_count(net)
+    s = np.zeros((3, 1, 2, 2), np.uint8)
+    rp = O.Replay(s, np.zeros(3, np.int32), np.array([1.0, 2.0, 3.0]), s, np.zeros(3, np.uint8))
+    cfg = O.TrainCfg(minibatch=1, gamma=0.0, lr=0.0)
+    out = O.run(net, cfg, 2, [rp], np.zeros(P), 8)
+    # FIFO with capacity 2: slot 0 holds push 2 (r=3), slot 1 holds push 1 (r=2)
+    r_of_slot = {0: 3.0, 1: 2.0}
+    for T in range(8):
+        sl = out["idx"][0, T, 0]
+        assert out["loss"][0, T] == 0.5 * r_of_slot[sl] ** 2
+
+
+def test_sampled_idx_follow_O3_and_ring_size():
+    cfg = O.TrainCfg(n_replicas=2, minibatch=5, seed=77)
+    replays = make_replays(2, 13, 3)
+    out = O.run(TINY, cfg, CAP, replays, he_theta(TINY, 1), 3)
+    for k in range(2):
+        for T in range(3):
+            assert list(out["idx"][k, T]) == [O.sample_index(77, k, T, j, 13) for j in range(5)]
+
+
+def test_empty_replay_is_an_error():
+    rp = O.Replay(np.zeros((0, 4, 12, 12), np.uint8), np.zeros(0, np.int32), np.zeros(0), np.zeros((0, 4, 12, 12),
+                  np.uint8), np.zeros(0, np.uint8))
+    out = O.run(TINY, O.TrainCfg(minibatch=2), CAP, [rp], he_theta(TINY, 1), 1)
+    assert out["rc"] == -2
+
+
+def test_nonfinite_reward_is_flagged_and_not_applied():
+    replays = make_replays(1, 5, 9)
+    replays[0].r[:] = np.inf
+    theta0 = he_theta(TINY, 2)
+    out = O.run(TINY, O.TrainCfg(minibatch=2), CAP, replays, theta0, 1)
+    assert out["rc"] == -3
+    moved = out["theta"] != theta0
+    # every element whose mean gradient is non-finite keeps its value (A24)
+    assert np.all(np.isfinite(out["theta"])) and not np.all(moved)
