@@ -1,0 +1,161 @@
+/* dqn.h — C ABI of the B200-native distributed deep Q-learning hot path.
+ *
+ * Method: Ong, Chavez, Hong, "Distributed Deep Q-Learning", arXiv 1508.04186.
+ * Citation keys: P:n = line n of the paper text,
+ * A-n = reading n of the paper listed in DESIGN.md §3.
+ *
+ * One context per process per GPU ("replica k" of Alg. 1, which also
+ * owns shard k of the parameter server of Alg. 2). All device state
+ * (replay memory D_k, theta working copy, target theta^, gradient buffer,
+ * the owned fp32 master shard of theta and of the RMSProp accumulator r) lives
+ * in the context and is freed by dqn_destroy.
+ *
+ * Conventions for every entry point:
+ *  - return value: DQN_OK (0) or a negative DQN_E* status; a failed call that
+ *    returns DQN_EINVAL or DQN_EEMPTY has not mutated the context.
+ *  - buffers are owned by the caller; pointers may be host or device memory
+ *    (detected with cudaPointerGetAttributes); inputs are consumed (copied)
+ *    before the call returns; outputs are written before it returns.
+ *  - calls are synchronous on return, NOT thread-safe on one context.
+ *  - "collective" calls must be made by every rank of the group, in the same
+ *    order, with the same arguments where stated.
+ *  - after DQN_ECUDA or DQN_ENCCL the context is poisoned: every later call
+ *    except dqn_last_error / dqn_destroy returns DQN_ESTATE.
+ */
+#ifndef DQN_H
+#define DQN_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dqn_ctx dqn_ctx;
+
+enum {
+  DQN_OK = 0,
+  DQN_EINVAL = -1,     /* bad config / argument (validated before any mutation) */
+  DQN_EEMPTY = -2,     /* train_steps on an empty replay memory (A13)          */
+  DQN_ENONFINITE = -3, /* a push round produced a non-finite mean gradient (A24); sticky */
+  DQN_ENOMEM = -4,     /* device allocation failed                                */
+  DQN_ECUDA = -5,      /* CUDA runtime error; context poisoned                    */
+  DQN_ENCCL = -6,      /* NCCL error; context poisoned                            */
+  DQN_ESTATE = -7      /* context poisoned by an earlier ECUDA / ENCCL            */
+};
+
+/* arithmetic of the replica step (a3-a9 of DESIGN.md §2) */
+enum { DQN_FP32 = 0,   /* fp32 SIMT kernels; parity <= 1e-5 vs the fp64 oracle            */
+       DQN_BF16 = 1 }; /* bf16 operands on tcgen05 tensor cores, fp32 accumulate; <= 2e-2 */
+/* push / fetch schedule (DESIGN.md §2 a11-a13) */
+enum { DQN_DETERMINISTIC = 0, /* lock-step, reproducible                         */
+       DQN_ASYNC = 1 };       /* reserved: asynchronous staleness mode (next row) */
+/* which parameter vector dqn_get_params returns */
+enum {
+  DQN_PARAMS_SERVER = 0, /* global theta of Alg. 2 (fp32 masters, gathered over ranks: collective) */
+  DQN_PARAMS_LOCAL = 1,  /* this replica's fetched theta (Alg. 1 "Fetch model theta")       */
+  DQN_PARAMS_TARGET = 2, /* this replica's target theta^                             */
+  DQN_PARAMS_GRAD = 3,   /* this replica's last-step gradient Delta theta; diagnostic      */
+  DQN_PARAMS_RMS = 4     /* RMSProp accumulator r of Alg. 2 (gathered: collective)                 */
+};
+
+/* Problem statement (P:59-67 network, P:87 C, P:99 N, P:121 gamma, P:123 b,
+ * P:142-147 RMSProp + init). Layer list: valid convolutions (no padding,
+ * (in-k)/s+1 must be a positive integer, A16), ReLU after every conv and every
+ * hidden FC, linear output layer with n_actions units. */
+typedef struct {
+  int32_t frames, height, width;       /* phi stack F x d x d, u8 pixels          */
+  int32_t n_conv;                      /* 1..4                                            */
+  int32_t conv_filters[4], conv_kernel[4], conv_stride[4];
+  int32_t n_fc;                        /* hidden FC layers 0..4                           */
+  int32_t fc_units[4];
+  int32_t n_actions;                   /* |A| >= 1                                        */
+  int32_t minibatch;                   /* b >= 1 (Alg. 1)                           */
+  double gamma;                        /* discount                                */
+  double lr;                           /* alpha (Alg. 2)                            */
+  double rms_decay;                    /* 0.9 in Alg. 2                           */
+  double rms_eps;                      /* epsilon inside the square root (A4), e.g. 1e-8  */
+  double err_clip;                     /* 0 = off (Alg. 1); c > 0 clamps delta (A3)       */
+  int64_t replay_capacity;             /* last-N experiences kept                  */
+  int32_t n_push, n_fetch;             /* Downpour periods (A8, A9), >= 1                 */
+  int64_t target_sync;                 /* C: refresh theta^ after a fetch when n-l >= C */
+  int32_t precision;                   /* DQN_FP32 | DQN_BF16                             */
+  int32_t sync_mode;                   /* DQN_DETERMINISTIC                               */
+  uint64_t seed;                       /* key of the counter-based sampler (A11)          */
+  double init_std;                     /* xi of theta_i ~ N(0, xi) (A19)           */
+  uint64_t init_seed;
+  const float* init_params;            /* optional: P floats in canonical order (host or device); copied */
+} dqn_config;
+
+typedef struct {
+  /* outputs */
+  double loss_mean;          /* mean over the call's steps of (1/b) sum 1/2 delta^2 (unclipped, A27) */
+  int64_t generation;        /* server iteration number n after the call (Alg. 2)              */
+  int64_t steps_done;        /* replica step counter T after the call                                */
+  float device_ms;           /* device time of the call (CUDA events on the context stream)          */
+  int64_t nonfinite_rounds;  /* push rounds so far with a non-finite mean gradient (A24)              */
+  /* optional caller-owned HOST outputs (NULL = not wanted); valid when k <= 4096 */
+  int32_t* sampled_idx;      /* [k][b] replay slots sampled by this replica (a1)                     */
+  int32_t* target_argmax;    /* [k][b] argmax_a' Q(phi_{j+1}, a'; theta^), lowest index on ties      */
+  float* loss_per_step;      /* [k]                                                                  */
+} dqn_step_stats;
+
+/* Number of parameters P (weights + biases of every layer); -1 if the layer chain
+ * is invalid. Pure. Canonical flat order: layer by layer, W then b; conv W is
+ * [N][C][k][k], FC W is [H][D] with D flattened in (C,H,W) order (A18). */
+int64_t dqn_param_count(const dqn_config* cfg);
+
+/* Bytes of the NCCL unique id (128). dqn_nccl_unique_id writes one into out
+ * (call on rank 0, broadcast the bytes to every rank out of band). */
+int32_t dqn_nccl_id_bytes(void);
+int dqn_nccl_unique_id(void* out);
+
+/* Create the context of `rank` in a group of `world` ranks (collective when
+ * world > 1). nccl_unique_id: dqn_nccl_id_bytes() bytes, NULL iff world == 1.
+ * cuda_stream: a cudaStream_t all work is ordered on, or NULL for a
+ * library-owned stream. The current CUDA device must already be selected.
+ * Initial state: theta = init_params (or N(0, init_std^2) from init_seed, the
+ * same on every rank), r = 0, n = 0, theta^ = theta, l = 0, T = 0 (Alg. 2). */
+int dqn_create(const dqn_config* cfg, int rank, int world, const void* nccl_unique_id, void* cuda_stream,
+               dqn_ctx** out);
+
+/* "Store experience (phi_t, a_t, r_t, phi_{t+1}) in D_k" (Alg. 1).
+ * n transitions, oldest first: s and s_next [n][F][H][W] u8 (frames oldest
+ * first), a [n] in [0, n_actions), r [n] finite, terminal [n] (0/1).
+ * Push i goes to slot (count + i) mod capacity (FIFO last-N).
+ * DQN_EINVAL (nothing stored) on an out-of-range action or non-finite reward. */
+int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a, const float* r,
+                         const uint8_t* s_next, const uint8_t* terminal);
+
+/* Run k replica steps of Alg. 1 with the server rounds of Alg. 2 they trigger
+ * (collective: every rank passes the same k). Per step T: fetch when
+ * T % n_fetch == 0 (then refresh theta^ when n - l >= C); sample b slots
+ * uniformly with replacement; targets with theta^; gradient at the fetched
+ * theta; accumulate; when (T+1) % n_push == 0 reduce-scatter the gradient to
+ * the shard owners, each applies RMSProp to its shard, n += 1.
+ * stats may be NULL. DQN_EEMPTY if the replay memory is empty (nothing run);
+ * DQN_ENONFINITE if any round so far produced a non-finite mean gradient. */
+int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats);
+
+/* Q(s, a; theta_local) for n states [n][F][H][W] u8 -> q [n][n_actions] fp32 and
+ * (optional) argmax [n] int32, lowest index on ties. Not collective. */
+int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, float* q, int32_t* argmax);
+
+/* Copy a parameter vector (DQN_PARAMS_*) in canonical order into out[cap]
+ * (cap >= P, host or device). n_params / generation may be NULL.
+ * SERVER and RMS are collective when world > 1. */
+int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, int64_t* n_params, uint64_t* generation);
+
+/* Replay occupancy: total pushes so far and min(count, capacity). */
+int dqn_replay_size(const dqn_ctx* ctx, int64_t* count, int64_t* size);
+
+/* Last error message of this context ("" if none); with ctx == NULL, the message of the
+ * last failed dqn_create on the calling thread. Never NULL. */
+const char* dqn_last_error(const dqn_ctx* ctx);
+
+/* Free every device resource of the context (not collective). NULL is a no-op. */
+void dqn_destroy(dqn_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DQN_H */

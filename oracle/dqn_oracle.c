@@ -224,6 +224,29 @@ void or_q_values(const or_net* net, const double* theta, int64_t n, const uint8_
   }
 }
 
+/* Smallest |pre-activation| of any ReLU unit over n states (diagnostic for the
+ * parity tests: ReLU'(z) is a step function, so two correct evaluations of the
+ * gradient in different precisions may differ when some |z| is within rounding
+ * distance of 0; reading A30). */
+double or_min_abs_preact(const or_net* net, const double* theta, int64_t n, const uint8_t* states) {
+  shape_t sh;
+  if (build_shapes(net, &sh)) return NAN;
+  int64_t sz = (int64_t)net->frames * net->height * net->width;
+  double* x = (double*)malloc(sizeof(double) * sz);
+  double** z = alloc_acts(&sh);
+  double m = INFINITY;
+  for (int64_t i = 0; i < n; ++i) {
+    normalise(states + i * sz, sz, x);
+    forward_store(&sh, theta, x, z);
+    for (int l = 0; l + 1 < sh.n_layers; ++l)
+      for (int64_t e = 0; e < act_size(&sh, l); ++e)
+        if (fabs(z[l][e]) < m) m = fabs(z[l][e]);
+  }
+  free_acts(&sh, z);
+  free(x);
+  return m;
+}
+
 /* ------------------------------------------------------------------ Alg. 1 */
 /* "Set y_j = r_j if phi_{j+1} terminal, r_j + gamma max_a' Q^(phi_{j+1}, a'; theta^) otherwise".
  * A select, never (1 - term) * m (A14). */

@@ -63,6 +63,9 @@ void or_forward_u8(const or_net* net, const double* theta, const uint8_t* s, dou
 void or_q_values(const or_net* net, const double* theta, int64_t n, const uint8_t* states, double* q,
                  int32_t* argmax);
 
+/* Smallest |pre-activation| of any ReLU unit over n states (parity diagnostic, A30). */
+double or_min_abs_preact(const or_net* net, const double* theta, int64_t n, const uint8_t* states);
+
 /* ---- Alg. 1 pieces (O6, O7) ---- */
 /* y_j: terminal -> r_j, else r_j + gamma * max_a' Q(phi_{j+1}, a'; theta_hat). */
 void or_targets(const or_net* net, const double* theta_hat, int b, const uint8_t* s_next, const double* r,

@@ -128,6 +128,8 @@ def lib():
         _lib.or_loss_grad.argtypes = [C.POINTER(_Net), D, C.c_int, U8, I32, D, C.c_double, D]
         _lib.or_loss_grad_x.restype = C.c_double
         _lib.or_loss_grad_x.argtypes = [C.POINTER(_Net), D, C.c_int, D, I32, D, C.c_double, D]
+        _lib.or_min_abs_preact.restype = C.c_double
+        _lib.or_min_abs_preact.argtypes = [C.POINTER(_Net), D, C.c_int64, U8]
         _lib.or_rmsprop.argtypes = [D, D, D, C.c_int64, C.c_double, C.c_double, C.c_double]
         _lib.or_run.restype = C.c_int
         _lib.or_run.argtypes = [C.POINTER(_Net), C.POINTER(_Cfg), C.c_int64, I64, C.POINTER(U8), C.POINTER(I32),
@@ -204,6 +206,13 @@ def q_values(net: Net, theta: np.ndarray, states: np.ndarray):
     lib().or_q_values(C.byref(net.c()), _p(theta, C.c_double), n, _p(states, C.c_uint8), _p(q, C.c_double),
                       _p(am, C.c_int32))
     return q, am
+
+
+def min_abs_preact(net: Net, theta: np.ndarray, states: np.ndarray) -> float:
+    theta = _f64(theta)
+    states = np.ascontiguousarray(states, dtype=np.uint8)
+    return float(lib().or_min_abs_preact(C.byref(net.c()), _p(theta, C.c_double), states.shape[0],
+                                         _p(states, C.c_uint8)))
 
 
 def targets(net: Net, theta_hat: np.ndarray, s_next: np.ndarray, r, term, gamma: float):

@@ -1,0 +1,249 @@
+"""Python binding of libdqn.so — the C ABI of include/dqn.h.
+
+Argument marshalling only: every step of the hot path (sampling, gather,
+convolutions, FC layers, TD head, backward, RMSProp shard update, NCCL
+push/fetch) runs inside libdqn.so's CUDA kernels. There is no CPU or PyTorch
+fallback: importing this package without the built library raises.
+
+Names follow the paper (arXiv 1508.04186): theta, theta^ (target), n
+(generation), b (minibatch), C (target_sync), n_push / n_fetch (Downpour).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdqn.so")
+
+OK, EINVAL, EEMPTY, ENONFINITE, ENOMEM, ECUDA, ENCCL, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
+FP32, BF16 = 0, 1
+DETERMINISTIC, ASYNC = 0, 1
+PARAMS_SERVER, PARAMS_LOCAL, PARAMS_TARGET, PARAMS_GRAD, PARAMS_RMS = 0, 1, 2, 3, 4
+_NAMES = {0: "OK", -1: "EINVAL", -2: "EEMPTY", -3: "ENONFINITE", -4: "ENOMEM", -5: "ECUDA", -6: "ENCCL",
+          -7: "ESTATE"}
+
+
+class DqnError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Config(C.Structure):
+    _fields_ = [("frames", C.c_int32), ("height", C.c_int32), ("width", C.c_int32), ("n_conv", C.c_int32),
+                ("conv_filters", C.c_int32 * 4), ("conv_kernel", C.c_int32 * 4), ("conv_stride", C.c_int32 * 4),
+                ("n_fc", C.c_int32), ("fc_units", C.c_int32 * 4), ("n_actions", C.c_int32),
+                ("minibatch", C.c_int32), ("gamma", C.c_double), ("lr", C.c_double), ("rms_decay", C.c_double),
+                ("rms_eps", C.c_double), ("err_clip", C.c_double), ("replay_capacity", C.c_int64),
+                ("n_push", C.c_int32), ("n_fetch", C.c_int32), ("target_sync", C.c_int64),
+                ("precision", C.c_int32), ("sync_mode", C.c_int32), ("seed", C.c_uint64),
+                ("init_std", C.c_double), ("init_seed", C.c_uint64), ("init_params", C.c_void_p)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("loss_mean", C.c_double), ("generation", C.c_int64), ("steps_done", C.c_int64),
+                ("device_ms", C.c_float), ("nonfinite_rounds", C.c_int64), ("sampled_idx", C.c_void_p),
+                ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p)]
+
+
+@dataclass
+class Config:
+    """dqn_config (include/dqn.h). Defaults: Mnih-2013 DQN of BASELINE.json configs[0]."""
+    frames: int = 4
+    height: int = 84
+    width: int = 84
+    convs: Sequence[Tuple[int, int, int]] = ((16, 8, 4), (32, 4, 2))   # (filters, kernel, stride)
+    fcs: Sequence[int] = (256,)
+    n_actions: int = 6
+    minibatch: int = 32
+    gamma: float = 0.99
+    lr: float = 2.5e-4
+    rms_decay: float = 0.9
+    rms_eps: float = 1e-8
+    err_clip: float = 0.0
+    replay_capacity: int = 1000
+    n_push: int = 1
+    n_fetch: int = 1
+    target_sync: int = 2**62
+    precision: int = FP32
+    sync_mode: int = DETERMINISTIC
+    seed: int = 0xD15EA5E
+    init_std: float = 0.01
+    init_seed: int = 7
+
+    def to_c(self, init_ptr: Optional[int] = None) -> _Config:
+        c = _Config()
+        c.frames, c.height, c.width = self.frames, self.height, self.width
+        c.n_conv = len(self.convs)
+        for i, (f, k, s) in enumerate(self.convs):
+            c.conv_filters[i], c.conv_kernel[i], c.conv_stride[i] = f, k, s
+        c.n_fc = len(self.fcs)
+        for i, u in enumerate(self.fcs):
+            c.fc_units[i] = u
+        for name in ("n_actions", "minibatch", "gamma", "lr", "rms_decay", "rms_eps", "err_clip", "replay_capacity",
+                     "n_push", "n_fetch", "target_sync", "precision", "sync_mode", "seed", "init_std", "init_seed"):
+            setattr(c, name, getattr(self, name))
+        c.init_params = init_ptr
+        return c
+
+    @property
+    def state_shape(self):
+        return (self.frames, self.height, self.width)
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libdqn.so; raises if it has not been built (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1508_04186_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.dqn_param_count.restype = C.c_int64
+        L.dqn_param_count.argtypes = [C.POINTER(_Config)]
+        L.dqn_nccl_id_bytes.restype = C.c_int32
+        L.dqn_nccl_unique_id.argtypes = [P]
+        L.dqn_create.argtypes = [C.POINTER(_Config), C.c_int, C.c_int, P, P, C.POINTER(P)]
+        L.dqn_push_transitions.argtypes = [P, C.c_int64, P, P, P, P, P]
+        L.dqn_train_steps.argtypes = [P, C.c_int64, C.POINTER(_Stats)]
+        L.dqn_q_values.argtypes = [P, C.c_int64, P, P, P]
+        L.dqn_get_params.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+        L.dqn_replay_size.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.dqn_last_error.restype = C.c_char_p
+        L.dqn_last_error.argtypes = [P]
+        L.dqn_destroy.argtypes = [P]
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("dqn_param_count", "dqn_nccl_id_bytes", "dqn_nccl_unique_id", "dqn_create", "dqn_push_transitions",
+            "dqn_train_steps", "dqn_q_values", "dqn_get_params", "dqn_replay_size", "dqn_last_error", "dqn_destroy")
+
+
+def param_count(cfg: Config) -> int:
+    return int(lib().dqn_param_count(C.byref(cfg.to_c())))
+
+
+def nccl_unique_id() -> bytes:
+    n = lib().dqn_nccl_id_bytes()
+    buf = C.create_string_buffer(n)
+    rc = lib().dqn_nccl_unique_id(buf)
+    if rc:
+        raise DqnError(rc, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def _ptr(x, dtype) -> Tuple[int, object]:
+    """(address, keep-alive) of a contiguous numpy array or torch tensor (host or CUDA)."""
+    if x is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            t = x.contiguous()
+            want = {np.uint8: torch.uint8, np.int32: torch.int32, np.float32: torch.float32}[dtype]
+            if t.dtype != want:
+                t = t.to(want)
+            return t.data_ptr(), t
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return a.ctypes.data, a
+
+
+class DQN:
+    """One replica + parameter-server shard on the current CUDA device (dqn_ctx)."""
+
+    def __init__(self, cfg: Config, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 stream: Optional[int] = None, init_params=None):
+        self.cfg = cfg
+        L = lib()
+        ip, keep = _ptr(init_params, np.float32)
+        c = cfg.to_c(ip)
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, len(nccl_id)) if nccl_id is not None else None
+        rc = L.dqn_create(C.byref(c), rank, world, idbuf, stream, C.byref(h))
+        if rc:
+            raise DqnError(rc, L.dqn_last_error(None).decode())
+        self._h = h
+        self.P = param_count(cfg)
+        del keep
+
+    def _check(self, rc: int):
+        if rc:
+            raise DqnError(rc, lib().dqn_last_error(self._h).decode())
+
+    def push(self, s, a, r, s_next, term) -> None:
+        n = len(a)
+        ps, k1 = _ptr(s, np.uint8)
+        pa, k2 = _ptr(a, np.int32)
+        pr, k3 = _ptr(r, np.float32)
+        pn, k4 = _ptr(s_next, np.uint8)
+        pt, k5 = _ptr(term, np.uint8)
+        self._check(lib().dqn_push_transitions(self._h, n, ps, pa, pr, pn, pt))
+
+    def train(self, k: int, want_idx: bool = False, want_argmax: bool = False, want_loss: bool = False) -> dict:
+        st = _Stats()
+        b = self.cfg.minibatch
+        idx = np.zeros((k, b), np.int32) if want_idx else None
+        am = np.zeros((k, b), np.int32) if want_argmax else None
+        lp = np.zeros(k, np.float32) if want_loss else None
+        st.sampled_idx = idx.ctypes.data if idx is not None else None
+        st.target_argmax = am.ctypes.data if am is not None else None
+        st.loss_per_step = lp.ctypes.data if lp is not None else None
+        rc = lib().dqn_train_steps(self._h, k, C.byref(st))
+        out = dict(loss_mean=st.loss_mean, generation=st.generation, steps_done=st.steps_done,
+                   device_ms=st.device_ms, nonfinite_rounds=st.nonfinite_rounds, idx=idx, argmax=am, loss=lp,
+                   rc=rc)
+        self._check(rc)
+        return out
+
+    def q_values(self, states, q_out=None, argmax_out=None):
+        n = len(states)
+        A = self.cfg.n_actions
+        ps, k1 = _ptr(states, np.uint8)
+        q = q_out if q_out is not None else np.zeros((n, A), np.float32)
+        am = argmax_out if argmax_out is not None else np.zeros(n, np.int32)
+        pq, _ = _ptr(q, np.float32)
+        pa, _ = _ptr(am, np.int32)
+        self._check(lib().dqn_q_values(self._h, n, ps, pq, pa))
+        return q, am
+
+    def params(self, which: int = PARAMS_SERVER, out=None):
+        o = out if out is not None else np.zeros(self.P, np.float32)
+        po, _ = _ptr(o, np.float32)
+        n = C.c_int64()
+        g = C.c_uint64()
+        self._check(lib().dqn_get_params(self._h, which, po, self.P, C.byref(n), C.byref(g)))
+        return o
+
+    def generation(self, which: int = PARAMS_SERVER) -> int:
+        n = C.c_int64()
+        g = C.c_uint64()
+        self._check(lib().dqn_get_params(self._h, which, None, 0, C.byref(n), C.byref(g)))
+        return int(g.value)
+
+    def replay_size(self) -> Tuple[int, int]:
+        c, s = C.c_int64(), C.c_int64()
+        self._check(lib().dqn_replay_size(self._h, C.byref(c), C.byref(s)))
+        return int(c.value), int(s.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().dqn_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

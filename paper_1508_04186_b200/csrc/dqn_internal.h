@@ -1,0 +1,131 @@
+// dqn_internal.h — shapes, device-side state and kernel launchers shared by the
+// runtime (dqn_runtime.cu) and the kernel translation units. Product code only;
+// nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace dqn {
+
+constexpr int kMaxConv = 4;
+constexpr int kMaxFc = 4;
+constexpr int kDiagSteps = 4096;  // ring of per-step diagnostics (idx, argmax, loss)
+
+// One valid convolution layer (A16): in C x H x W, out N x Ho x Wo.
+struct ConvShape {
+  int C, H, W, N, k, s, Ho, Wo;
+  long long w_off, b_off;  // canonical offsets: W [N][C][k][k] then b [N]
+};
+// One fully connected layer: in D, out H (hidden: ReLU; last: linear output).
+struct FcShape {
+  int D, H;
+  long long w_off, b_off;  // W [H][D] then b [H]
+};
+struct NetShape {
+  int F, Hin, Win;
+  int n_conv;
+  ConvShape conv[kMaxConv];
+  int n_fc;                 // hidden FC layers
+  FcShape fc[kMaxFc + 1];   // hidden FCs then the output layer (fc[n_fc])
+  int A;                    // |A|
+  long long P;
+  long long state_bytes;    // F*Hin*Win
+};
+
+// Device counters (one struct in device memory per context). Kernels read T at
+// the start of a step and the head kernel advances it, so captured CUDA graphs
+// are replayable.
+struct DevCounters {
+  unsigned long long T;         // replica step counter
+  long long n;                  // server generation (mirrored on host in deterministic mode)
+  unsigned int nonfinite;       // # of non-finite mean-gradient elements seen (sticky)
+  unsigned int nonfinite_rounds;
+  unsigned int bad_input;       // push validation
+  unsigned int nonfinite_last;  // value of `nonfinite` at the end of the previous round
+  long long ring_size;          // min(count, capacity), written by the push path
+  unsigned int blocks_done;     // last-block-done counter of the update kernel
+  unsigned int pad2;
+};
+
+// Where the input image of a (group, image) comes from.
+// u8 mode: ring[g] + idx[img] * stride (idx == nullptr: image i at i * stride)
+// f32 mode: f32[g] + img * stride
+struct ImgSrc {
+  const uint8_t* u8[2];
+  const float* f32[2];
+  const int* idx;
+  long long stride;
+};
+
+enum Epi { EPI_STORE = 0, EPI_ACCUM = 1, EPI_BIAS_RELU = 2, EPI_BIAS = 3, EPI_MASK = 4 };
+
+struct GemmArgs {
+  const float* A[2];
+  long long sam, sak;  // A(m,k) = A[m*sam + k*sak]
+  const float* B[2];
+  long long sbk, sbn;  // B(k,n) = B[k*sbk + n*sbn]
+  float* C[2];
+  long long scm, scn;  // C(m,n) = C[m*scm + n*scn]
+  const float* bias[2];       // indexed by n (EPI_BIAS*)
+  const float* mask[2];       // EPI_MASK: keep where mask(m,n) > 0
+  long long smm, smn;
+  int M, N, K;
+  int groups;                 // 1 or 2 (independent problems sharing shapes)
+  int splits;                 // split-K factor (>1: partial buffer + reduce kernel)
+  int epi;
+  float* partial;             // [groups][splits][M][N] when splits > 1
+};
+
+struct HeadArgs {
+  const float* act[2];        // [b][H]: input of the output layer for s (theta) / s' (theta^)
+  const float* theta;         // live theta (fp32, canonical)
+  const float* theta_hat;     // target theta^ (fp32, canonical)
+  long long w_off, b_off;     // output layer
+  long long prev_b_off;       // bias of the previous hidden FC (if prev_is_fc)
+  int prev_is_fc;
+  int H, A, b;
+  const int* idx;
+  const int32_t* ring_a;
+  const float* ring_r;
+  const uint8_t* ring_term;
+  float gamma, clip;
+  float* grad;                // G (accumulated)
+  float* dH;                  // [b][H] d(pre-activation) of the previous layer
+  DevCounters* ctr;
+  float* diag_loss;           // [kDiagSteps]
+  int* diag_idx;              // [kDiagSteps][b]
+  int* diag_amax;             // [kDiagSteps][b]
+};
+
+// ------------------------------------------------------------------ launchers
+// common (kernels_common.cu)
+void launch_sample(int* idx, int b, unsigned long long seed, unsigned rank, const DevCounters* ctr,
+                   cudaStream_t st);
+void launch_validate_push(const int32_t* a, const float* r, long long n, int A, DevCounters* ctr, cudaStream_t st);
+void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
+                           long long cap, long long count0, long long n_total, long long first, long long n,
+                           long long state_bytes, const uint8_t* s, const int32_t* a, const float* r,
+                           const uint8_t* sn, const uint8_t* t, cudaStream_t st);
+void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
+                    float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int count_round,
+                    cudaStream_t st);
+void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st);
+void launch_bump_generation(DevCounters* ctr, cudaStream_t st);
+
+// fp32 SIMT path (kernels_f32.cu)
+void init_f32_kernel_attrs();
+void launch_conv_fwd_f32(const ConvShape& cs, const ImgSrc& src, const float* theta0, const float* theta1,
+                         float* out0, float* out1, int b, int groups, cudaStream_t st);
+void launch_conv_bwd_dx_f32(const ConvShape& cs, const float* dout, const float* theta, const float* a_in,
+                            float* din, int b, cudaStream_t st);
+void launch_conv_bwd_dw_f32(const ConvShape& cs, const float* dout, const ImgSrc& src, float* partial, int b,
+                            cudaStream_t st);
+void launch_reduce_rows(const float* partial, int rows, long long E, float* dst, cudaStream_t st);
+void launch_gemm_f32(const GemmArgs& g, cudaStream_t st);
+void launch_bias_grad(const float* dz, int b, int H, float* dst, cudaStream_t st);
+void launch_head_f32(const HeadArgs& h, cudaStream_t st);
+void launch_q_head_f32(const float* act, const float* theta, long long w_off, long long b_off, int H, int A, int n,
+                       float* q, int* argmax, cudaStream_t st);
+
+}  // namespace dqn

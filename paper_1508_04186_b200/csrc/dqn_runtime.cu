@@ -1,0 +1,771 @@
+// dqn_runtime.cu — the C ABI of include/dqn.h: context, replay memory, parameter
+// layout and shards, the deterministic push/fetch schedule, CUDA-graph step
+// replay, NCCL reduce-scatter (push, a11) and all-gather (fetch, a13).
+//
+// Method: Alg. 1 (worker) and Alg. 2 (parameter server) of
+// arXiv 1508.04186, re-cast for one process per B200: every rank is a replica
+// AND the owner of 1/N of the server state.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/dqn.h"
+#include "dqn_internal.h"
+
+using namespace dqn;
+
+struct dqn_ctx {
+  dqn_config cfg{};
+  NetShape net{};
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  // replay memory D_k: FIFO ring of the last `cap` experiences
+  uint8_t *ring_s = nullptr, *ring_sn = nullptr, *ring_t = nullptr;
+  int32_t* ring_a = nullptr;
+  float* ring_r = nullptr;
+  long long cap = 0, count = 0;
+  // parameters, canonical flat order, padded to P_pad = ceil(P / 64N) * 64N
+  long long P = 0, P_pad = 0, shard = 0;
+  float* theta_master = nullptr;  // [shard] fp32 master of the owned shard (world 1: whole vector)
+  float* rms = nullptr;           // [shard] RMSProp accumulator r
+  float* grad = nullptr;          // [P_pad] gradient accumulator of this replica
+  float* g_shard = nullptr;       // [shard] reduce-scatter output (world > 1)
+  float* theta_local = nullptr;   // [P_pad] fetched theta (may alias theta_master)
+  float* theta_hat = nullptr;     // [P_pad] target theta^
+  float* grad_snap = nullptr;     // [P_pad] optional copy of the last step's gradient (DQN_KEEP_GRAD)
+  float* gather_tmp = nullptr;    // [P_pad] for get_params(SERVER/RMS) with world > 1
+  // activations: conv layer c -> act_conv[c][g] [b][N*Ho*Wo]; hidden fc l -> act_fc[l][g] [b][H]
+  float* act_conv[kMaxConv][2] = {};
+  float* act_fc[kMaxFc][2] = {};
+  float* dz_conv[kMaxConv] = {};
+  float* dz_fc[kMaxFc] = {};
+  float* partial = nullptr;
+  long long partial_elems = 0;
+  int* idx = nullptr;
+  DevCounters* ctr = nullptr;
+  float* diag_loss = nullptr;
+  int* diag_idx = nullptr;
+  int* diag_amax = nullptr;
+  // q_values staging
+  uint8_t* q_stage = nullptr;
+  float* q_out = nullptr;
+  int* q_amax = nullptr;
+  // push staging (host inputs)
+  uint8_t *push_s = nullptr, *push_sn = nullptr, *push_t = nullptr;
+  int32_t* push_a = nullptr;
+  float* push_r = nullptr;
+  long long push_chunk = 0;
+  // host mirrors of the deterministic schedule (identical on every rank)
+  long long T = 0, n = 0, n_local = 0, ell = 0;
+  // graphs per (fetch, refresh, push) variant
+  cudaGraphExec_t graphs[8] = {};
+  bool use_graphs = true;
+  bool keep_grad = false;
+  bool alias_local = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+  bool poisoned = false;
+  bool diverged = false;
+};
+
+// ------------------------------------------------------------------ helpers
+static int set_err(dqn_ctx* c, int code, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (code == DQN_ECUDA || code == DQN_ENCCL) c->poisoned = true;
+  }
+  return code;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return set_err(ctx, DQN_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+#define NK(call)                                                                                  \
+  do {                                                                                            \
+    ncclResult_t r_ = (call);                                                                     \
+    if (r_ != ncclSuccess)                                                                        \
+      return set_err(ctx, DQN_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));        \
+  } while (0)
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Shapes of the layer chain (valid convolutions A16). Returns false when invalid.
+static bool build_net(const dqn_config* c, NetShape* s) {
+  std::memset(s, 0, sizeof(*s));
+  if (!c || c->frames < 1 || c->height < 1 || c->width < 1) return false;
+  if (c->n_conv < 0 || c->n_conv > kMaxConv || c->n_fc < 0 || c->n_fc > kMaxFc || c->n_actions < 1) return false;
+  s->F = c->frames; s->Hin = c->height; s->Win = c->width;
+  s->state_bytes = (long long)c->frames * c->height * c->width;
+  int ch = c->frames, h = c->height, w = c->width;
+  long long off = 0;
+  s->n_conv = c->n_conv;
+  for (int i = 0; i < c->n_conv; ++i) {
+    ConvShape& L = s->conv[i];
+    const int N = c->conv_filters[i], k = c->conv_kernel[i], st = c->conv_stride[i];
+    if (N < 1 || k < 1 || st < 1 || k > h || k > w || (h - k) % st || (w - k) % st) return false;
+    L.C = ch; L.H = h; L.W = w; L.N = N; L.k = k; L.s = st;
+    L.Ho = (h - k) / st + 1; L.Wo = (w - k) / st + 1;
+    L.w_off = off; off += (long long)N * ch * k * k;
+    L.b_off = off; off += N;
+    ch = N; h = L.Ho; w = L.Wo;
+  }
+  int d = ch * h * w;
+  s->n_fc = c->n_fc;
+  for (int i = 0; i <= c->n_fc; ++i) {
+    FcShape& F = s->fc[i];
+    const int units = i < c->n_fc ? c->fc_units[i] : c->n_actions;
+    if (units < 1) return false;
+    F.D = d; F.H = units;
+    F.w_off = off; off += (long long)units * d;
+    F.b_off = off; off += units;
+    d = units;
+  }
+  s->A = c->n_actions;
+  s->P = off;
+  return true;
+}
+
+// deterministic N(0, xi^2) init from init_seed (Alg. 2; identical on every rank)
+static uint64_t splitmix64(uint64_t& x) {
+  uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static void gaussian_init(std::vector<float>& th, double std_, uint64_t seed) {
+  uint64_t st = seed;
+  for (size_t i = 0; i < th.size(); i += 2) {
+    double u1 = ((splitmix64(st) >> 11) + 1.0) * (1.0 / 9007199254740993.0);
+    double u2 = (splitmix64(st) >> 11) * (1.0 / 9007199254740992.0);
+    double rad = std::sqrt(-2.0 * std::log(u1));
+    th[i] = (float)(std_ * rad * std::cos(2.0 * M_PI * u2));
+    if (i + 1 < th.size()) th[i + 1] = (float)(std_ * rad * std::sin(2.0 * M_PI * u2));
+  }
+}
+
+static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
+  if (!build_net(c, net)) { *why = "invalid layer chain (valid convolutions need integer output sizes)"; return DQN_EINVAL; }
+  if (c->n_conv < 1) { *why = "at least one convolution layer is required"; return DQN_EINVAL; }
+  if (c->minibatch < 1) { *why = "minibatch must be >= 1"; return DQN_EINVAL; }
+  if (c->replay_capacity < 1) { *why = "replay_capacity must be >= 1"; return DQN_EINVAL; }
+  if (c->n_push < 1 || c->n_fetch < 1) { *why = "n_push and n_fetch must be >= 1"; return DQN_EINVAL; }
+  if (c->precision != DQN_FP32 && c->precision != DQN_BF16) { *why = "unknown precision"; return DQN_EINVAL; }
+  if (c->sync_mode != DQN_DETERMINISTIC) { *why = "only DQN_DETERMINISTIC is implemented"; return DQN_EINVAL; }
+  if (!(c->rms_decay >= 0.0 && c->rms_decay < 1.0) || !(c->rms_eps >= 0.0) || !(c->lr >= 0.0) ||
+      !std::isfinite(c->gamma) || !(c->err_clip >= 0.0)) {
+    *why = "invalid hyper-parameter"; return DQN_EINVAL;
+  }
+  if (c->precision == DQN_BF16) { *why = "DQN_BF16 path not built yet"; return DQN_EINVAL; }
+  // fp32 kernels stage one input image (+ one filter chunk) in shared memory
+  for (int i = 0; i < net->n_conv; ++i) {
+    const ConvShape& L = net->conv[i];
+    long long fwd = ((long long)L.C * L.H * L.W + 3) / 4 * 4 + (long long)L.C * L.k * L.k * 16;
+    long long dw = ((long long)L.C * L.H * L.W + 3) / 4 * 4 + (long long)L.N * L.Ho * L.Wo;
+    long long dx = ((long long)L.N * L.Ho * L.Wo + 3) / 4 * 4 + (long long)L.N * L.k * L.k * 8;
+    if (fwd * 4 > 227 * 1024 || dw * 4 > 227 * 1024 || dx * 4 > 227 * 1024) {
+      *why = "layer too large for the shared-memory staging of the fp32 kernels"; return DQN_EINVAL;
+    }
+  }
+  return DQN_OK;
+}
+
+extern "C" int64_t dqn_param_count(const dqn_config* cfg) {
+  NetShape s;
+  if (!build_net(cfg, &s)) return -1;
+  return s.P;
+}
+
+extern "C" int32_t dqn_nccl_id_bytes(void) { return (int32_t)sizeof(ncclUniqueId); }
+
+extern "C" int dqn_nccl_unique_id(void* out) {
+  if (!out) return DQN_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return DQN_ENCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return DQN_OK;
+}
+
+template <typename T>
+static int dalloc(dqn_ctx* ctx, T** p, long long n) {
+  if (n <= 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, DQN_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  return DQN_OK;
+}
+
+static void free_all(dqn_ctx* c) {
+  for (auto& g : c->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  void* ptrs[] = {c->ring_s, c->ring_sn, c->ring_t, c->ring_a, c->ring_r, c->rms, c->grad, c->g_shard,
+                  c->theta_hat, c->grad_snap, c->gather_tmp, c->partial, c->idx, c->ctr, c->diag_loss,
+                  c->diag_idx, c->diag_amax, c->q_stage, c->q_out, c->q_amax, c->push_s, c->push_sn, c->push_t,
+                  c->push_a, c->push_r};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->theta_local && !c->alias_local) cudaFree(c->theta_local);
+  if (c->theta_master) cudaFree(c->theta_master);
+  for (int i = 0; i < kMaxConv; ++i) {
+    for (int g = 0; g < 2; ++g)
+      if (c->act_conv[i][g]) cudaFree(c->act_conv[i][g]);
+    if (c->dz_conv[i]) cudaFree(c->dz_conv[i]);
+  }
+  for (int i = 0; i < kMaxFc; ++i) {
+    for (int g = 0; g < 2; ++g)
+      if (c->act_fc[i][g]) cudaFree(c->act_fc[i][g]);
+    if (c->dz_fc[i]) cudaFree(c->dz_fc[i]);
+  }
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+}
+
+// split-K factor so a GEMM fills the machine (148 SMs)
+static int pick_splits(int M, int N, int K, int groups) {
+  long long tiles = (long long)((M + 63) / 64) * ((N + 63) / 64) * groups;
+  int s = 1;
+  while (tiles * s < 296 && K / (s * 2) >= 64) s *= 2;
+  return s;
+}
+
+static thread_local std::string g_create_err;
+
+static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world, const void* nccl_unique_id,
+                       void* cuda_stream) {
+  ctx->cfg = *cfg;
+  ctx->cfg.init_params = nullptr;
+  std::string why;
+  int rc = validate_cfg(cfg, &ctx->net, &why);
+  if (rc) return set_err(ctx, rc, why);
+  ctx->rank = rank;
+  ctx->world = world;
+  const NetShape& net = ctx->net;
+  const int b = cfg->minibatch;
+  ctx->P = net.P;
+  const long long unit = 64LL * world;
+  ctx->P_pad = (net.P + unit - 1) / unit * unit;
+  ctx->shard = ctx->P_pad / world;
+  ctx->cap = cfg->replay_capacity;
+  ctx->use_graphs = !(getenv("DQN_NO_GRAPH") && atoi(getenv("DQN_NO_GRAPH")));
+  ctx->keep_grad = getenv("DQN_KEEP_GRAD") && atoi(getenv("DQN_KEEP_GRAD"));
+  ctx->alias_local = (world == 1 && cfg->n_fetch == 1);
+
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  CK(cudaEventCreate(&ctx->ev0));
+  CK(cudaEventCreate(&ctx->ev1));
+  init_f32_kernel_attrs();
+
+  // replay memory: both stacks of every experience, action, reward, terminal flag
+  const long long sb = net.state_bytes;
+  if ((rc = dalloc(ctx, &ctx->ring_s, ctx->cap * sb))) return rc;
+  if ((rc = dalloc(ctx, &ctx->ring_sn, ctx->cap * sb))) return rc;
+  if ((rc = dalloc(ctx, &ctx->ring_t, ctx->cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->ring_a, ctx->cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->ring_r, ctx->cap))) return rc;
+
+  // parameters and server shards
+  if ((rc = dalloc(ctx, &ctx->theta_master, ctx->alias_local ? ctx->P_pad : ctx->shard))) return rc;
+  if ((rc = dalloc(ctx, &ctx->rms, ctx->shard))) return rc;
+  if ((rc = dalloc(ctx, &ctx->grad, ctx->P_pad))) return rc;
+  if (world > 1 && (rc = dalloc(ctx, &ctx->g_shard, ctx->shard))) return rc;
+  if (world > 1 && (rc = dalloc(ctx, &ctx->gather_tmp, ctx->P_pad))) return rc;
+  if (ctx->alias_local) ctx->theta_local = ctx->theta_master;
+  else if ((rc = dalloc(ctx, &ctx->theta_local, ctx->P_pad))) return rc;
+  if ((rc = dalloc(ctx, &ctx->theta_hat, ctx->P_pad))) return rc;
+  if (ctx->keep_grad && (rc = dalloc(ctx, &ctx->grad_snap, ctx->P_pad))) return rc;
+  CK(cudaMemsetAsync(ctx->rms, 0, sizeof(float) * ctx->shard, ctx->stream));
+  CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, ctx->stream));
+
+  // activations / gradients of activations
+  long long max_partial = 0;
+  for (int i = 0; i < net.n_conv; ++i) {
+    const ConvShape& L = net.conv[i];
+    const long long per = (long long)L.N * L.Ho * L.Wo;
+    for (int g = 0; g < 2; ++g)
+      if ((rc = dalloc(ctx, &ctx->act_conv[i][g], per * b))) return rc;
+    if ((rc = dalloc(ctx, &ctx->dz_conv[i], per * b))) return rc;
+    max_partial = std::max(max_partial, (long long)b * ((long long)L.N * L.C * L.k * L.k + L.N));
+  }
+  for (int i = 0; i <= net.n_fc; ++i) {
+    const FcShape& F = net.fc[i];
+    if (i < net.n_fc) {
+      for (int g = 0; g < 2; ++g)
+        if ((rc = dalloc(ctx, &ctx->act_fc[i][g], (long long)F.H * b))) return rc;
+      if ((rc = dalloc(ctx, &ctx->dz_fc[i], (long long)F.H * b))) return rc;
+      const int s_fwd = pick_splits(b, F.H, F.D, 2);
+      max_partial = std::max(max_partial, 2LL * s_fwd * b * F.H);
+      const int s_dx = pick_splits(b, F.D, F.H, 1);
+      max_partial = std::max(max_partial, (long long)s_dx * b * F.D);
+    }
+  }
+  const long long qn = std::max(b, 1);
+  max_partial = std::max(max_partial, 2LL * pick_splits(qn, net.fc[0].H, net.fc[0].D, 1) * qn * net.fc[0].H);
+  ctx->partial_elems = max_partial;
+  if ((rc = dalloc(ctx, &ctx->partial, max_partial))) return rc;
+  if ((rc = dalloc(ctx, &ctx->idx, b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->ctr, 1))) return rc;
+  CK(cudaMemsetAsync(ctx->ctr, 0, sizeof(DevCounters), ctx->stream));
+  if ((rc = dalloc(ctx, &ctx->diag_loss, kDiagSteps))) return rc;
+  if ((rc = dalloc(ctx, &ctx->diag_idx, (long long)kDiagSteps * b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->diag_amax, (long long)kDiagSteps * b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->q_stage, qn * sb))) return rc;
+  if ((rc = dalloc(ctx, &ctx->q_out, qn * net.A))) return rc;
+  if ((rc = dalloc(ctx, &ctx->q_amax, qn))) return rc;
+
+  // initial theta (Alg. 2): init_params or N(0, xi^2) from init_seed; theta^ = theta
+  std::vector<float> th((size_t)ctx->P_pad, 0.0f);
+  if (cfg->init_params) {
+    if (is_device_ptr(cfg->init_params)) {
+      CK(cudaMemcpy(th.data(), cfg->init_params, sizeof(float) * net.P, cudaMemcpyDeviceToHost));
+    } else {
+      std::memcpy(th.data(), cfg->init_params, sizeof(float) * net.P);
+    }
+  } else {
+    std::vector<float> g((size_t)net.P);
+    gaussian_init(g, cfg->init_std, cfg->init_seed);
+    std::memcpy(th.data(), g.data(), sizeof(float) * net.P);
+  }
+  if (ctx->alias_local) {
+    CK(cudaMemcpyAsync(ctx->theta_master, th.data(), sizeof(float) * ctx->P_pad, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    CK(cudaMemcpyAsync(ctx->theta_master, th.data() + ctx->shard * rank, sizeof(float) * ctx->shard,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->theta_local, th.data(), sizeof(float) * ctx->P_pad, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CK(cudaMemcpyAsync(ctx->theta_hat, th.data(), sizeof(float) * ctx->P_pad, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    NK(ncclCommInitRank(&ctx->comm, world, id, rank));
+  }
+  return DQN_OK;
+}
+
+extern "C" int dqn_create(const dqn_config* cfg, int rank, int world, const void* nccl_unique_id, void* cuda_stream,
+                          dqn_ctx** out) {
+  g_create_err.clear();
+  if (!out) return DQN_EINVAL;
+  *out = nullptr;
+  if (!cfg || world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id)) {
+    g_create_err = "bad create arguments";
+    return DQN_EINVAL;
+  }
+  dqn_ctx* ctx = new dqn_ctx();
+  int rc = create_impl(ctx, cfg, rank, world, nccl_unique_id, cuda_stream);
+  if (rc) {
+    g_create_err = ctx->err;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    free_all(ctx);
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return DQN_OK;
+}
+
+// ------------------------------------------------------------------ push (Alg. 1 "Store")
+extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a, const float* r,
+                                    const uint8_t* s_next, const uint8_t* terminal) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  if (n < 0 || (n > 0 && (!s || !a || !r || !s_next || !terminal))) return set_err(ctx, DQN_EINVAL, "bad push args");
+  if (n == 0) return DQN_OK;
+  const long long sb = ctx->net.state_bytes;
+  const bool dev = is_device_ptr(s);
+  if (dev != is_device_ptr(a) || dev != is_device_ptr(r) || dev != is_device_ptr(s_next) ||
+      dev != is_device_ptr(terminal))
+    return set_err(ctx, DQN_EINVAL, "push buffers must all be host or all be device memory");
+  // only the last min(n, cap) items survive; item i goes to slot (count + i) mod cap
+  const long long first = n > ctx->cap ? n - ctx->cap : 0;
+  if (!dev) {
+    for (long long i = 0; i < n; ++i)
+      if (a[i] < 0 || a[i] >= ctx->net.A || !std::isfinite(r[i]))
+        return set_err(ctx, DQN_EINVAL, "action out of range or non-finite reward at item " + std::to_string(i));
+    if (!ctx->push_s) {
+      ctx->push_chunk = std::min<long long>(ctx->cap, std::max<long long>(1, (256LL << 20) / (2 * sb)));
+      int rc;
+      if ((rc = dalloc(ctx, &ctx->push_s, ctx->push_chunk * sb))) return rc;
+      if ((rc = dalloc(ctx, &ctx->push_sn, ctx->push_chunk * sb))) return rc;
+      if ((rc = dalloc(ctx, &ctx->push_t, ctx->push_chunk))) return rc;
+      if ((rc = dalloc(ctx, &ctx->push_a, ctx->push_chunk))) return rc;
+      if ((rc = dalloc(ctx, &ctx->push_r, ctx->push_chunk))) return rc;
+    }
+    for (long long i0 = first; i0 < n; i0 += ctx->push_chunk) {
+      const long long m = std::min(ctx->push_chunk, n - i0);
+      CK(cudaMemcpyAsync(ctx->push_s, s + i0 * sb, m * sb, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->push_sn, s_next + i0 * sb, m * sb, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->push_a, a + i0, m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->push_r, r + i0, m * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(ctx->push_t, terminal + i0, m, cudaMemcpyHostToDevice, ctx->stream));
+      launch_push_canonical(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, 0,
+                            i0, m, sb, ctx->push_s, ctx->push_a, ctx->push_r, ctx->push_sn, ctx->push_t,
+                            ctx->stream);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(ctx->stream));  // staging is reused by the next chunk
+    }
+  } else {
+    CK(cudaMemsetAsync(&ctx->ctr->bad_input, 0, sizeof(unsigned), ctx->stream));
+    launch_validate_push(a, r, n, ctx->net.A, ctx->ctr, ctx->stream);
+    unsigned bad = 0;
+    CK(cudaMemcpyAsync(&bad, &ctx->ctr->bad_input, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (bad) return set_err(ctx, DQN_EINVAL, "action out of range or non-finite reward in device push");
+    for (long long i0 = first; i0 < n; i0 += 65535) {
+      const long long m = std::min<long long>(65535, n - i0);
+      launch_push_canonical(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, 0,
+                            i0, m, sb, s + i0 * sb, a + i0, r + i0, s_next + i0 * sb, terminal + i0, ctx->stream);
+      CK(cudaGetLastError());
+    }
+  }
+  ctx->count += n;
+  const long long size = std::min(ctx->count, ctx->cap);
+  CK(cudaMemcpyAsync(&ctx->ctr->ring_size, &size, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DQN_OK;
+}
+
+// ------------------------------------------------------------------ one replica step (fp32 path)
+// Enqueue the kernels of one step T on ctx->stream (captured into a graph).
+static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
+  const NetShape& net = ctx->net;
+  const dqn_config& c = ctx->cfg;
+  const int b = c.minibatch;
+  cudaStream_t st = ctx->stream;
+  // a13 fetch + a14 target refresh
+  if (fetch) {
+    if (ctx->world > 1) {
+      NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
+    } else if (!ctx->alias_local) {
+      CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_master, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+    }
+    if (refresh)
+      CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+  }
+  // a1 sample
+  launch_sample(ctx->idx, b, c.seed, (unsigned)ctx->rank, ctx->ctr, st);
+  // a2-a4 convolutions, theta on s and theta^ on s' in one launch per layer
+  ImgSrc src0{};
+  src0.u8[0] = ctx->ring_s;
+  src0.u8[1] = ctx->ring_sn;
+  src0.idx = ctx->idx;
+  src0.stride = net.state_bytes;
+  for (int i = 0; i < net.n_conv; ++i) {
+    ImgSrc src = src0;
+    if (i > 0) {
+      src = ImgSrc{};
+      src.f32[0] = ctx->act_conv[i - 1][0];
+      src.f32[1] = ctx->act_conv[i - 1][1];
+      const ConvShape& P = net.conv[i - 1];
+      src.stride = (long long)P.N * P.Ho * P.Wo;
+    }
+    launch_conv_fwd_f32(net.conv[i], src, ctx->theta_local, ctx->theta_hat, ctx->act_conv[i][0], ctx->act_conv[i][1],
+                        b, 2, st);
+  }
+  // a5 hidden FC layers
+  const ConvShape& LC = net.conv[net.n_conv - 1];
+  const float* in[2] = {ctx->act_conv[net.n_conv - 1][0], ctx->act_conv[net.n_conv - 1][1]};
+  for (int l = 0; l < net.n_fc; ++l) {
+    const FcShape& F = net.fc[l];
+    GemmArgs g{};
+    g.A[0] = in[0]; g.A[1] = in[1]; g.sam = F.D; g.sak = 1;
+    g.B[0] = ctx->theta_local + F.w_off; g.B[1] = ctx->theta_hat + F.w_off; g.sbk = 1; g.sbn = F.D;
+    g.C[0] = ctx->act_fc[l][0]; g.C[1] = ctx->act_fc[l][1]; g.scm = F.H; g.scn = 1;
+    g.bias[0] = ctx->theta_local + F.b_off; g.bias[1] = ctx->theta_hat + F.b_off;
+    g.M = b; g.N = F.H; g.K = F.D; g.groups = 2; g.splits = pick_splits(b, F.H, F.D, 2);
+    g.epi = EPI_BIAS_RELU; g.partial = ctx->partial;
+    launch_gemm_f32(g, st);
+    in[0] = ctx->act_fc[l][0]; in[1] = ctx->act_fc[l][1];
+  }
+  (void)LC;
+  // a6 head: TD target, loss, output layer gradient, d(previous pre-activation)
+  const FcShape& O = net.fc[net.n_fc];
+  HeadArgs h{};
+  h.act[0] = in[0]; h.act[1] = in[1];
+  h.theta = ctx->theta_local; h.theta_hat = ctx->theta_hat;
+  h.w_off = O.w_off; h.b_off = O.b_off;
+  h.prev_is_fc = net.n_fc > 0;
+  h.prev_b_off = net.n_fc > 0 ? net.fc[net.n_fc - 1].b_off : 0;
+  h.H = O.D; h.A = O.H; h.b = b;
+  h.idx = ctx->idx; h.ring_a = ctx->ring_a; h.ring_r = ctx->ring_r; h.ring_term = ctx->ring_t;
+  h.gamma = (float)c.gamma; h.clip = (float)c.err_clip;
+  h.grad = ctx->grad;
+  h.dH = net.n_fc > 0 ? ctx->dz_fc[net.n_fc - 1] : ctx->dz_conv[net.n_conv - 1];
+  h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
+  launch_head_f32(h, st);
+  // a7 hidden FC backward
+  for (int l = net.n_fc - 1; l >= 0; --l) {
+    const FcShape& F = net.fc[l];
+    const float* dz = ctx->dz_fc[l];
+    const float* a_in = l > 0 ? ctx->act_fc[l - 1][0] : ctx->act_conv[net.n_conv - 1][0];
+    if (l < net.n_fc - 1) launch_bias_grad(dz, b, F.H, ctx->grad + F.b_off, st);
+    GemmArgs gw{};  // dW[h][d] += sum_j dz[j][h] a_in[j][d]
+    gw.A[0] = dz; gw.sam = 1; gw.sak = F.H;
+    gw.B[0] = a_in; gw.sbk = F.D; gw.sbn = 1;
+    gw.C[0] = ctx->grad + F.w_off; gw.scm = F.D; gw.scn = 1;
+    gw.M = F.H; gw.N = F.D; gw.K = b; gw.groups = 1; gw.splits = 1; gw.epi = EPI_ACCUM;
+    launch_gemm_f32(gw, st);
+    GemmArgs gx{};  // dz_prev[j][d] = [a_in > 0] sum_h dz[j][h] W[h][d]
+    gx.A[0] = dz; gx.sam = F.H; gx.sak = 1;
+    gx.B[0] = ctx->theta_local + F.w_off; gx.sbk = F.D; gx.sbn = 1;
+    gx.C[0] = l > 0 ? ctx->dz_fc[l - 1] : ctx->dz_conv[net.n_conv - 1]; gx.scm = F.D; gx.scn = 1;
+    gx.mask[0] = a_in; gx.smm = F.D; gx.smn = 1;
+    gx.M = b; gx.N = F.D; gx.K = F.H; gx.groups = 1; gx.splits = pick_splits(b, F.D, F.H, 1);
+    gx.epi = EPI_MASK; gx.partial = ctx->partial;
+    launch_gemm_f32(gx, st);
+  }
+  // a8/a9 convolution backward
+  for (int i = net.n_conv - 1; i >= 0; --i) {
+    const ConvShape& L = net.conv[i];
+    ImgSrc src{};
+    if (i == 0) {
+      src.u8[0] = ctx->ring_s; src.idx = ctx->idx; src.stride = net.state_bytes;
+    } else {
+      src.f32[0] = ctx->act_conv[i - 1][0];
+      src.stride = (long long)L.C * L.H * L.W;
+    }
+    launch_conv_bwd_dw_f32(L, ctx->dz_conv[i], src, ctx->partial, b, st);
+    launch_reduce_rows(ctx->partial, b, (long long)L.N * L.C * L.k * L.k + L.N, ctx->grad + L.w_off, st);
+    if (i > 0) launch_conv_bwd_dx_f32(L, ctx->dz_conv[i], ctx->theta_local, ctx->act_conv[i - 1][0],
+                                      ctx->dz_conv[i - 1], b, st);
+  }
+  if (ctx->keep_grad)
+    CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+  // a11 push + a12 shard update (Alg. 2 RMSPropUpdate; n <- n + 1)
+  if (push) {
+    const float div = (float)((double)ctx->world * c.n_push);
+    const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
+    if (ctx->world > 1) {
+      NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
+      CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
+      launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
+                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 1, st);
+    } else {
+      launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
+                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 1, st);
+    }
+  }
+  CK(cudaGetLastError());
+  return DQN_OK;
+}
+
+static int run_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
+  if (!ctx->use_graphs) return enqueue_step_f32(ctx, fetch, refresh, push);
+  const int v = (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0);
+  if (!ctx->graphs[v]) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_step_f32(ctx, fetch, refresh, push);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    if (rc) return rc;
+    if (e != cudaSuccess) return set_err(ctx, DQN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    CK(cudaGraphInstantiate(&ctx->graphs[v], g, 0));
+    cudaGraphDestroy(g);
+  }
+  CK(cudaGraphLaunch(ctx->graphs[v], ctx->stream));
+  return DQN_OK;
+}
+
+extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  if (k < 0) return set_err(ctx, DQN_EINVAL, "k must be >= 0");
+  if (ctx->count == 0) return set_err(ctx, DQN_EEMPTY, "replay memory is empty (A13)");
+  const dqn_config& c = ctx->cfg;
+  const long long T0 = ctx->T;
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  for (long long s = 0; s < k; ++s) {
+    const long long T = ctx->T;
+    // O10 / O11: fetch at the start of step T when T % n_fetch == 0, then refresh theta^ when n - l >= C
+    const bool fetch = (T % c.n_fetch) == 0;
+    bool refresh = false;
+    if (fetch) {
+      ctx->n_local = ctx->n;
+      if (ctx->n_local - ctx->ell >= c.target_sync) {
+        refresh = true;
+        ctx->ell = ctx->n_local;
+      }
+    }
+    const bool push = ((T + 1) % c.n_push) == 0;
+    int rc = run_step(ctx, fetch, refresh, push);
+    if (rc) return rc;
+    if (push) ctx->n += 1;
+    ctx->T += 1;
+  }
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  DevCounters hc;
+  CK(cudaMemcpyAsync(&hc, ctx->ctr, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<float> loss;
+  const bool diag_ok = k > 0 && k <= kDiagSteps;
+  if (diag_ok) {
+    loss.resize(k);
+    for (long long s = 0; s < k; ++s) {
+      const long long slot = (T0 + s) % kDiagSteps;
+      CK(cudaMemcpyAsync(&loss[s], ctx->diag_loss + slot, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (stats && stats->sampled_idx)
+      for (long long s = 0; s < k; ++s)
+        CK(cudaMemcpyAsync(stats->sampled_idx + s * c.minibatch,
+                           ctx->diag_idx + ((T0 + s) % kDiagSteps) * c.minibatch, sizeof(int) * c.minibatch,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    if (stats && stats->target_argmax)
+      for (long long s = 0; s < k; ++s)
+        CK(cudaMemcpyAsync(stats->target_argmax + s * c.minibatch,
+                           ctx->diag_amax + ((T0 + s) % kDiagSteps) * c.minibatch, sizeof(int) * c.minibatch,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hc.T != (unsigned long long)ctx->T || hc.n != ctx->n)
+    return set_err(ctx, DQN_ECUDA, "device step counters diverged from the host schedule");
+  if (hc.nonfinite_rounds > 0) ctx->diverged = true;
+  if (stats) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    stats->device_ms = ms;
+    stats->generation = ctx->n;
+    stats->steps_done = ctx->T;
+    stats->nonfinite_rounds = hc.nonfinite_rounds;
+    double lm = 0.0;
+    for (float l : loss) lm += l;
+    stats->loss_mean = loss.empty() ? 0.0 : lm / (double)loss.size();
+    if (stats->loss_per_step && diag_ok) std::memcpy(stats->loss_per_step, loss.data(), sizeof(float) * k);
+  }
+  if (ctx->diverged) return set_err(ctx, DQN_ENONFINITE, "a push round produced a non-finite mean gradient (A24)");
+  return DQN_OK;
+}
+
+// ------------------------------------------------------------------ acting boundary (a15)
+extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, float* q, int32_t* argmax) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  if (n < 0 || (n > 0 && (!states || !q))) return set_err(ctx, DQN_EINVAL, "bad q_values args");
+  const NetShape& net = ctx->net;
+  const int b = ctx->cfg.minibatch;
+  const long long sb = net.state_bytes;
+  const bool dev_in = is_device_ptr(states), dev_q = is_device_ptr(q), dev_a = argmax && is_device_ptr(argmax);
+  cudaStream_t st = ctx->stream;
+  for (long long i0 = 0; i0 < n; i0 += b) {
+    const int m = (int)std::min<long long>(b, n - i0);
+    CK(cudaMemcpyAsync(ctx->q_stage, states + i0 * sb, m * sb, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       st));
+    ImgSrc src{};
+    src.u8[0] = ctx->q_stage;
+    src.stride = sb;
+    for (int i = 0; i < net.n_conv; ++i) {
+      ImgSrc s2 = src;
+      if (i > 0) {
+        s2 = ImgSrc{};
+        s2.f32[0] = ctx->act_conv[i - 1][0];
+        const ConvShape& P = net.conv[i - 1];
+        s2.stride = (long long)P.N * P.Ho * P.Wo;
+      }
+      launch_conv_fwd_f32(net.conv[i], s2, ctx->theta_local, nullptr, ctx->act_conv[i][0], nullptr, m, 1, st);
+    }
+    const float* in = ctx->act_conv[net.n_conv - 1][0];
+    for (int l = 0; l < net.n_fc; ++l) {
+      const FcShape& F = net.fc[l];
+      GemmArgs g{};
+      g.A[0] = in; g.sam = F.D; g.sak = 1;
+      g.B[0] = ctx->theta_local + F.w_off; g.sbk = 1; g.sbn = F.D;
+      g.C[0] = ctx->act_fc[l][0]; g.scm = F.H; g.scn = 1;
+      g.bias[0] = ctx->theta_local + F.b_off;
+      g.M = m; g.N = F.H; g.K = F.D; g.groups = 1; g.splits = pick_splits(b, F.H, F.D, 1);
+      g.epi = EPI_BIAS_RELU; g.partial = ctx->partial;
+      launch_gemm_f32(g, st);
+      in = ctx->act_fc[l][0];
+    }
+    const FcShape& O = net.fc[net.n_fc];
+    launch_q_head_f32(in, ctx->theta_local, O.w_off, O.b_off, O.D, O.H, m, ctx->q_out, ctx->q_amax, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(q + i0 * net.A, ctx->q_out, sizeof(float) * m * net.A,
+                       dev_q ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (argmax)
+      CK(cudaMemcpyAsync(argmax + i0, ctx->q_amax, sizeof(int) * m,
+                         dev_a ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return DQN_OK;
+}
+
+// ------------------------------------------------------------------ parameter readback
+extern "C" int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, int64_t* n_params,
+                              uint64_t* generation) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  if (n_params) *n_params = ctx->P;
+  if (generation) *generation = (uint64_t)(which == DQN_PARAMS_LOCAL || which == DQN_PARAMS_TARGET
+                                               ? (which == DQN_PARAMS_LOCAL ? ctx->n_local : ctx->ell)
+                                               : ctx->n);
+  if (!out) return DQN_OK;
+  if (cap < ctx->P) return set_err(ctx, DQN_EINVAL, "output buffer smaller than P");
+  const cudaMemcpyKind kind = is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  const float* src = nullptr;
+  switch (which) {
+    case DQN_PARAMS_SERVER:
+    case DQN_PARAMS_RMS: {
+      float* shard = which == DQN_PARAMS_SERVER ? ctx->theta_master : ctx->rms;
+      if (ctx->world > 1) {
+        NK(ncclAllGather(shard, ctx->gather_tmp, (size_t)ctx->shard, ncclFloat, ctx->comm, ctx->stream));
+        src = ctx->gather_tmp;
+      } else {
+        src = shard;
+      }
+      break;
+    }
+    case DQN_PARAMS_LOCAL: src = ctx->theta_local; break;
+    case DQN_PARAMS_TARGET: src = ctx->theta_hat; break;
+    case DQN_PARAMS_GRAD:
+      if (!ctx->grad_snap) return set_err(ctx, DQN_EINVAL, "gradient snapshots need DQN_KEEP_GRAD=1 at create");
+      src = ctx->grad_snap;
+      break;
+    default: return set_err(ctx, DQN_EINVAL, "unknown parameter vector");
+  }
+  CK(cudaMemcpyAsync(out, src, sizeof(float) * ctx->P, kind, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DQN_OK;
+}
+
+extern "C" int dqn_replay_size(const dqn_ctx* ctx, int64_t* count, int64_t* size) {
+  if (!ctx) return DQN_EINVAL;
+  if (count) *count = ctx->count;
+  if (size) *size = std::min(ctx->count, ctx->cap);
+  return DQN_OK;
+}
+
+// ctx == NULL: message of the last failed dqn_create on this thread
+extern "C" const char* dqn_last_error(const dqn_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+extern "C" void dqn_destroy(dqn_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  free_all(ctx);
+  delete ctx;
+}

@@ -1,0 +1,154 @@
+// kernels_common.cu — precision-independent kernels of the hot path:
+//   a1  sampler (counter-based Philox4x32-10, integer-only index mapping)
+//   push path (validation + FIFO ring writes, "Store experience" of Alg. 1)
+//   a12 fused RMSProp shard update of Alg. 2
+#include "dqn_internal.h"
+#include "philox.cuh"
+
+namespace dqn {
+
+// ---------------------------------------------------------------- a1 sampler
+// "Uniformly sample minibatch of experiences X from D_k" (Alg. 1), with
+// replacement (A11): counter (j, T_lo, T_hi, rank), key = seed.
+__global__ void sample_kernel(int* idx, int b, unsigned long long seed, unsigned rank, const DevCounters* ctr) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= b) return;
+  idx[j] = (int)sample_slot(seed, rank, ctr->T, (unsigned)j, ctr->ring_size);
+}
+
+void launch_sample(int* idx, int b, unsigned long long seed, unsigned rank, const DevCounters* ctr,
+                   cudaStream_t st) {
+  sample_kernel<<<(b + 127) / 128, 128, 0, st>>>(idx, b, seed, rank, ctr);
+}
+
+// ---------------------------------------------------------------- push path
+__global__ void validate_push_kernel(const int32_t* a, const float* r, long long n, int A, DevCounters* ctr) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (a[i] < 0 || a[i] >= A || !isfinite(r[i])) atomicAdd(&ctr->bad_input, 1u);
+}
+
+void launch_validate_push(const int32_t* a, const float* r, long long n, int A, DevCounters* ctr, cudaStream_t st) {
+  if (n <= 0) return;
+  validate_push_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, r, n, A, ctr);
+}
+
+// Item i of this chunk (global push index n_total_before + first + i) goes to
+// slot (count0 + first + i) mod cap. One CTA per transition, 16-byte copies.
+__global__ void push_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
+                            long long cap, long long count0, long long first, long long state_bytes,
+                            const uint8_t* s, const int32_t* a, const float* r, const uint8_t* sn,
+                            const uint8_t* t) {
+  long long i = blockIdx.x;
+  long long slot = (count0 + first + i) % cap;
+  const uint8_t* src0 = s + i * state_bytes;
+  const uint8_t* src1 = sn + i * state_bytes;
+  uint8_t* dst0 = ring_s + slot * state_bytes;
+  uint8_t* dst1 = ring_sn + slot * state_bytes;
+  bool vec = ((state_bytes & 15) == 0) && ((((uintptr_t)src0) | ((uintptr_t)src1)) & 15) == 0;
+  if (vec) {
+    long long nv = state_bytes / 16;
+    for (long long v = threadIdx.x; v < nv; v += blockDim.x) {
+      reinterpret_cast<uint4*>(dst0)[v] = reinterpret_cast<const uint4*>(src0)[v];
+      reinterpret_cast<uint4*>(dst1)[v] = reinterpret_cast<const uint4*>(src1)[v];
+    }
+  } else {
+    for (long long v = threadIdx.x; v < state_bytes; v += blockDim.x) {
+      dst0[v] = src0[v];
+      dst1[v] = src1[v];
+    }
+  }
+  if (threadIdx.x == 0) {
+    ring_a[slot] = a[i];
+    ring_r[slot] = r[i];
+    ring_t[slot] = t[i] ? 1 : 0;
+  }
+}
+
+void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
+                           long long cap, long long count0, long long n_total, long long first, long long n,
+                           long long state_bytes, const uint8_t* s, const int32_t* a, const float* r,
+                           const uint8_t* sn, const uint8_t* t, cudaStream_t st) {
+  (void)n_total;
+  if (n <= 0) return;
+  push_kernel<<<(unsigned)n, 256, 0, st>>>(ring_s, ring_sn, ring_a, ring_r, ring_t, cap, count0, first, state_bytes,
+                                           s, a, r, sn, t);
+}
+
+// ---------------------------------------------------------------- a12 update
+// RMSPropUpdate (Alg. 2) on the owned shard, fused with the mean over
+// N * n_push gradients (A7, A8), the non-finite guard (A24), the publication of
+// the working-precision copy that the fetch all-gathers (a13), and the reset of
+// the gradient accumulator. r is updated first and theta uses the new r (A5);
+// eps sits inside the root (A4).
+__global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r, float* __restrict__ g, long long n,
+                               float div, float lr, float rho, float omr, float eps, float* __restrict__ pub_f32,
+                               __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr,
+                               int count_round) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned bad = 0;
+  for (; i < n; i += stride) {
+    float gb = g[i] / div;
+    g[i] = 0.0f;
+    float th = theta[i];
+    if (isfinite(gb)) {
+      float rr = rho * r[i] + omr * gb * gb;
+      r[i] = rr;
+      th = th - lr * gb / sqrtf(rr + eps);
+      theta[i] = th;
+    } else {
+      ++bad;
+    }
+    if (pub_f32) pub_f32[i] = th;
+    if (pub_bf16) pub_bf16[i] = __float2bfloat16_rn(th);
+  }
+  if (bad) atomicAdd(&ctr->nonfinite, bad);
+  // the last block to finish closes the round: n <- n + 1 (Alg. 2, A22)
+  if (count_round) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(&ctr->blocks_done, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      ctr->blocks_done = 0;
+      ctr->n += 1;
+      unsigned nf = atomicAdd(&ctr->nonfinite, 0u);
+      if (nf != ctr->nonfinite_last) {
+        ctr->nonfinite_rounds += 1;
+        ctr->nonfinite_last = nf;
+      }
+    }
+  }
+}
+
+__global__ void bump_generation_kernel(DevCounters* ctr) { ctr->n += 1; }
+
+void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
+                    float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int count_round,
+                    cudaStream_t st) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  rmsprop_kernel<<<blocks, 256, 0, st>>>(theta, r, g, n, div, lr, rho, omr, eps, pub_f32, pub_bf16, ctr,
+                                         count_round);
+}
+
+void launch_bump_generation(DevCounters* ctr, cudaStream_t st) { bump_generation_kernel<<<1, 1, 0, st>>>(ctr); }
+
+__global__ void f32_to_bf16_kernel(const float* src, __nv_bfloat16* dst, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  f32_to_bf16_kernel<<<blocks, 256, 0, st>>>(src, dst, n);
+}
+
+}  // namespace dqn

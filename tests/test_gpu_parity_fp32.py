@@ -1,0 +1,208 @@
+"""GPU parity of the fp32 path (DQN_FP32) against the fp64 oracle, through the
+C ABI. Bar (BASELINE.json north_star): sampled indices and argmax actions
+bit-exact (argmax outside near-ties, A21), Q-values / gradients / parameters
+within 1e-5 normwise per tensor (A29)."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1508_04186_b200 as D
+from oracle import oracle as O
+from tests.helpers import he_theta, near_tie_mask, nets, per_tensor_rel, replay
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+TINY_KW = dict(frames=3, height=17, width=13, convs=((5, 5, 2), (6, 3, 2)), fcs=(19,), n_actions=5)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    os.environ["DQN_KEEP_GRAD"] = "1"
+    yield
+
+
+def make(dc, on, n_push_items, seed, theta_seed=3, kind="uniform"):
+    theta0 = he_theta(on, theta_seed)
+    rp, raw = replay(on, n_push_items, seed, kind)
+    g = D.DQN(dc, init_params=theta0)
+    g.push(*raw)
+    return g, theta0, rp
+
+
+@pytest.mark.parametrize("kw", [dict(), TINY_KW], ids=["mnih", "tiny"])
+def test_q_values_and_argmax(kw):
+    dc, on, _ = nets(minibatch=32, **kw)
+    theta0 = he_theta(on, 5)
+    g = D.DQN(dc, init_params=theta0)
+    _, raw = replay(on, 45, 9)        # 45 = one chunk of 32 + a ragged 13
+    states = raw[0]
+    q, am = g.q_values(states)
+    qo, amo = O.q_values(on, theta0.astype(np.float64), states)
+    err = np.max(np.abs(q - qo)) / np.max(np.abs(qo))
+    assert err < TOL, err
+    ok = near_tie_mask(qo, TOL)
+    assert ok.sum() >= 40
+    assert np.array_equal(am[ok], amo[ok])
+    g.close()
+
+
+def test_sampled_indices_bit_exact_with_wraparound():
+    dc, on, oc = nets(minibatch=16, replay_capacity=40, **TINY_KW)
+    g, theta0, rp = make(dc, on, 100, 11)   # 100 pushes into 40 slots
+    out = g.train(7, want_idx=True)
+    ref = O.run(on, O.TrainCfg(**{**oc.__dict__, "minibatch": 16}), 40, [rp], theta0.astype(np.float64), 7)
+    assert np.array_equal(out["idx"], ref["idx"][0])
+    g.close()
+
+
+@pytest.mark.parametrize("kw", [dict(), TINY_KW], ids=["mnih", "tiny"])
+def test_first_step_gradient(kw):
+    dc, on, oc = nets(minibatch=32, replay_capacity=1000, **kw)
+    g, theta0, rp = make(dc, on, 300, 21)
+    g.train(1)
+    grad = g.params(D.PARAMS_GRAD)
+    ref = O.run(on, oc, 1000, [rp], theta0.astype(np.float64), 1, want_grad0=True)
+    err = per_tensor_rel(grad, ref["grad0"], on)
+    assert err < TOL, err
+    g.close()
+
+
+FLIP = 3e-7  # |pre-activation| within fp32 rounding of the ReLU kink: ReLU'(z) may differ (A30)
+
+
+def test_config0_ten_steps_teacher_forced():
+    """BASELINE.json configs[0] (Mnih net, b = 32, gamma = 0.99, 10 SGD steps, replay 1k), checked one
+    step ahead from the GPU's own state at every step (A30): the gradient of Alg. 1 and the
+    RMSProp update of Alg. 2 evaluated by the oracle at (theta_k, r_k) must match."""
+    dc, on, oc = nets(minibatch=32, replay_capacity=1000)
+    g, theta0, rp = make(dc, on, 1000, 1234)
+    th0 = theta0.astype(np.float64)
+    flips = 0
+    for k in range(10):
+        th = g.params(D.PARAMS_LOCAL).astype(np.float64)
+        r = g.params(D.PARAMS_RMS).astype(np.float64)
+        out = g.train(1, want_idx=True, want_argmax=True, want_loss=True)
+        idx = out["idx"][0]
+        assert list(idx) == [O.sample_index(dc.seed, 0, k, j, 1000) for j in range(32)]
+        y, am = O.targets(on, th0, rp.s_next[idx], rp.r[idx], rp.term[idx], oc.gamma)
+        loss, grad = O.loss_grad(on, th, rp.s[idx], rp.a[idx], y)
+        assert abs(out["loss"][0] - loss) <= TOL * loss
+        qn, _ = O.q_values(on, th0, rp.s_next[idx])
+        ok = near_tie_mask(qn, TOL)
+        assert np.array_equal(out["argmax"][0][ok], am[ok])
+        tol = TOL
+        if O.min_abs_preact(on, th, rp.s[idx]) < FLIP:
+            flips += 1      # a ReLU unit within rounding distance of its kink: one sample's path may differ
+            tol = 1e-3
+        assert per_tensor_rel(g.params(D.PARAMS_GRAD), grad, on) < tol
+        th_next, _ = O.rmsprop(th, r, grad, oc.lr, oc.rms_decay, oc.rms_eps)
+        assert per_tensor_rel(g.params(D.PARAMS_SERVER), th_next, on) < tol
+    assert flips <= 5
+    g.close()
+
+
+def test_config0_ten_steps_free_running():
+    """The same 10 steps free-running against the oracle's own trajectory. Indices are bit-exact.
+    Parameters agree to 1e-5 until the first ReLU-boundary event; after it an affected element can
+    differ by at most one RMSProp step per remaining step, |dtheta| <= 2 alpha sqrt(1/(1-rho)) (A30)."""
+    dc, on, oc = nets(minibatch=32, replay_capacity=1000)
+    g, theta0, rp = make(dc, on, 1000, 1234)
+    th0 = theta0.astype(np.float64)
+    out = g.train(10, want_idx=True, want_loss=True)
+    ref = O.run(on, oc, 1000, [rp], th0, 10)
+    assert ref["rc"] == 0 and out["generation"] == ref["n"] == 10
+    assert np.array_equal(out["idx"], ref["idx"][0])
+    th = g.params(D.PARAMS_SERVER).astype(np.float64)
+    bound = 10 * 2 * oc.lr * np.sqrt(1.0 / (1.0 - oc.rms_decay))
+    assert np.max(np.abs(th - ref["theta"])) <= bound
+    # the oracle's own trajectory tells which prefix has no boundary event; there parity is 1e-5
+    clean = 0
+    for k in range(10):
+        thk = O.run(on, oc, 1000, [rp], th0, k)["theta"] if k else th0
+        if O.min_abs_preact(on, thk, rp.s[ref["idx"][0, k]]) < FLIP:
+            break
+        clean += 1
+    if clean >= 1:
+        g2, _, _ = make(dc, on, 1000, 1234)
+        g2.train(clean)
+        ref2 = O.run(on, oc, 1000, [rp], th0, clean)
+        assert per_tensor_rel(g2.params(D.PARAMS_SERVER), ref2["theta"], on) < TOL
+        g2.close()
+    g.close()
+
+
+@pytest.mark.parametrize("n_push,n_fetch,C", [(1, 1, 2), (2, 1, 1), (1, 2, 1), (3, 2, 2)])
+def test_schedule_variants(n_push, n_fetch, C):
+    dc, on, oc = nets(minibatch=8, replay_capacity=64, n_push=n_push, n_fetch=n_fetch, target_sync=C, lr=2e-3,
+                      **TINY_KW)
+    g, theta0, rp = make(dc, on, 80, 5)
+    out = g.train(9, want_argmax=True)
+    ref = O.run(on, oc, 64, [rp], theta0.astype(np.float64), 9)
+    assert out["generation"] == ref["n"] == 9 // n_push
+    assert per_tensor_rel(g.params(D.PARAMS_SERVER), ref["theta"], on) < TOL
+    g.close()
+
+
+def test_split_calls_and_run_to_run_bit_identical():
+    dc, on, _ = nets(minibatch=32, replay_capacity=500)
+    g1, theta0, _ = make(dc, on, 500, 77)
+    g1.train(3)
+    g1.train(7)
+    a = g1.params(D.PARAMS_SERVER)
+    g1.close()
+    g2, _, _ = make(dc, on, 500, 77)
+    g2.train(10)
+    b = g2.params(D.PARAMS_SERVER)
+    g2.close()
+    assert np.array_equal(a, b)
+
+
+def test_errors():
+    dc, on, _ = nets(minibatch=4, replay_capacity=16, **TINY_KW)
+    g = D.DQN(dc, init_params=he_theta(on, 1))
+    with pytest.raises(D.DqnError) as e:
+        g.train(1)
+    assert e.value.code == D.EEMPTY
+    _, raw = replay(on, 4, 1)
+    s, a, r, sn, t = raw
+    bad = a.copy()
+    bad[2] = on.n_actions
+    with pytest.raises(D.DqnError) as e:
+        g.push(s, bad, r, sn, t)
+    assert e.value.code == D.EINVAL
+    rr = r.copy()
+    rr[0] = np.nan
+    with pytest.raises(D.DqnError) as e:
+        g.push(s, a, rr, sn, t)
+    assert e.value.code == D.EINVAL
+    assert g.replay_size() == (0, 0)
+    g.push(s, a, r, sn, t)
+    assert g.replay_size() == (4, 4)
+    g.train(1)
+    g.close()
+    with pytest.raises(D.DqnError) as e:
+        D.DQN(D.Config(convs=((16, 8, 3),)))
+    assert e.value.code == D.EINVAL
+
+
+def test_device_pointer_inputs():
+    import torch
+    dc, on, oc = nets(minibatch=8, replay_capacity=32, **TINY_KW)
+    theta0 = he_theta(on, 8)
+    rp, raw = replay(on, 40, 3)
+    g = D.DQN(dc, init_params=torch.from_numpy(theta0).cuda())
+    g.push(*[torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in raw])
+    out = g.train(4, want_idx=True)
+    ref = O.run(on, oc, 32, [rp], theta0.astype(np.float64), 4)
+    assert np.array_equal(out["idx"], ref["idx"][0])
+    assert per_tensor_rel(g.params(D.PARAMS_SERVER), ref["theta"], on) < TOL
+    qd = torch.zeros((5, on.n_actions), dtype=torch.float32, device="cuda")
+    ad = torch.zeros(5, dtype=torch.int32, device="cuda")
+    g.q_values(torch.from_numpy(raw[0][:5]).cuda(), q_out=qd, argmax_out=ad)
+    qo, _ = O.q_values(on, ref["theta"], raw[0][:5])
+    assert np.max(np.abs(qd.cpu().numpy() - qo)) / np.max(np.abs(qo)) < TOL
+    g.close()

@@ -208,6 +208,26 @@ def test_forward_matches_library_composition(net):
         assert am[i] == int(np.argmax(ref))
 
 
+def test_min_abs_preact_matches_library_composition():
+    theta = he_theta(TINY, 13)
+    s = synth.g_uniform(3, 4, 12, 12, 3, 4)[0]
+    ref = np.inf
+    tt = O.tensor_table(TINY)
+    for i in range(3):
+        a, c, t = s[i] / 255.0, 4, 0
+        for (n, k, st) in TINY.convs:
+            W = theta[tt[t][0]:tt[t][0] + tt[t][1]].reshape(n, c, k, k)
+            b = theta[tt[t + 1][0]:tt[t + 1][0] + n]
+            z = np.stack([sum(signal.correlate(a[ci], W[ni, ci], mode="valid") for ci in range(c))[::st, ::st] + b[ni]
+                          for ni in range(n)])
+            ref = min(ref, np.min(np.abs(z)))
+            a, c, t = np.maximum(z, 0), n, t + 2
+        W = theta[tt[t][0]:tt[t][0] + tt[t][1]].reshape(4, -1)
+        z = W @ a.ravel() + theta[tt[t + 1][0]:tt[t + 1][0] + 4]
+        ref = min(ref, np.min(np.abs(z)))
+    assert abs(O.min_abs_preact(TINY, theta, s) - ref) <= 1e-12 * max(ref, 1e-300) + 1e-15
+
+
 def bias_only_net_theta(net, out_bias):
     theta = np.zeros(O.param_count(net))
     theta[-net.n_actions:] = out_bias
