@@ -1,0 +1,362 @@
+"""bench.py — DQN transitions/sec trained on B200 (BASELINE.json metric).
+
+One "step" = one replica step of Alg. 1 (sample b transitions from the on-GPU
+replay, forward s with theta and s' with theta^, TD target, backward) plus the
+parameter-server round of Alg. 2 it triggers (push = reduce-scatter, RMSProp
+shard update, fetch = all-gather), i.e. every row of SURVEY.md §8(a).
+
+N = 1 : BASELINE.json configs[1] — 1 replica, Mnih-2013 net, b = 32, replay of
+        1M transitions on the GPU, target net refreshed every C = 1000 steps.
+N > 1 : configs[2] — Downpour with the sharded parameter server, b = 32 per
+        replica, n_push = n_fetch = 1 deterministic schedule (weak scaling).
+
+usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+       (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MNIH = dict(convs=((16, 8, 4), (32, 4, 2)), fcs=(256,), n_actions=6)
+METRIC = "DQN transitions/sec trained (device-timed, max over ranks) at 1/2/4/8 B200"
+UNIT = "transitions/s"
+FP32_ALU_PEAK_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # FFMA lanes x SMs x clocks.max.sm
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm=d.get("hbm_gbs", 6650.0), bf16=d.get("bf16_tflops", 1590.0),
+                    bf16_sus=d.get("bf16_tflops_sustained", 1400.0), src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+def region_work(name: str, b: int):
+    """Algorithmic FLOPs and bytes of one step region of the Mnih net."""
+    F, H, W = 4, 84, 84
+    c1 = dict(C=4, N=16, k=8, HoWo=400)
+    c2 = dict(C=16, N=32, k=4, HoWo=81)
+    D, Hfc, A = 2592, 256, 6
+    macs = lambda L: L["HoWo"] * L["N"] * L["C"] * L["k"] ** 2  # noqa: E731
+    state = F * H * W
+    w = {
+        "conv1_fwd": (2 * 2 * b * macs(c1), 2 * b * state + 2 * b * c1["N"] * c1["HoWo"] * 4),
+        "conv2_fwd": (2 * 2 * b * macs(c2), 2 * b * c1["N"] * c1["HoWo"] * 4 + 2 * b * c2["N"] * c2["HoWo"] * 4),
+        "fc1_fwd": (2 * 2 * b * D * Hfc, 2 * b * D * 4 + 2 * D * Hfc * 4 + 2 * b * Hfc * 4),
+        "head_td": (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 * 2),
+        "fc1_bwd": (4 * b * D * Hfc, b * Hfc * 4 + b * D * 4 * 2 + D * Hfc * 4 * 3),
+        "conv2_bwd": (2 * 2 * b * macs(c2), b * c2["N"] * c2["HoWo"] * 4 + 3 * b * c1["N"] * c1["HoWo"] * 4),
+        "conv1_bwd": (2 * b * macs(c1), b * state + b * c1["N"] * c1["HoWo"] * 4),
+        "rmsprop_update": (0, 677686 * 4 * 6),
+        "sample": (0, b * 4),
+    }
+    return w.get(name, (0, 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(budget_s: float = 15.0, b: int = 32):
+    """The oracle as it stands (single-threaded fp64), on a bounded sample of the workload."""
+    import numpy as np
+
+    import synth
+    from oracle import oracle as O
+
+    net = O.Net(**MNIH)
+    s, a, r, sn, t = synth.g_pong(1000, 4, 84, 84, 6, 0x5EED)
+    rp = O.Replay(s, a, r.astype(np.float64), sn, t)
+    theta0 = synth.init_theta(O.tensor_table(net), [0.01] * 8, 7).astype(np.float64)
+    cfg = O.TrainCfg(minibatch=b, target_sync=1000)
+    t0 = time.perf_counter()
+    O.run(net, cfg, 1000, [rp], theta0, 1)
+    one = time.perf_counter() - t0
+    steps = max(1, int(budget_s / max(one, 1e-3)))
+    t0 = time.perf_counter()
+    O.run(net, cfg, 1000, [rp], theta0, steps)
+    dt = time.perf_counter() - t0
+    return {"value": steps * b / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} replica steps of b={b} (Mnih net, replay 1k G-pong instead of 1M), fp64 single thread"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the fp64 oracle timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import synth
+    from oracle import oracle as O
+
+    net = O.Net(**MNIH)
+    b_full = 32
+    s, a, r, sn, t = synth.g_pong(1000, 4, 84, 84, 6, 0x5EED)
+    rp = O.Replay(s, a, r.astype(np.float64), sn, t)
+    theta0 = synth.init_theta(O.tensor_table(net), [0.01] * 8, 7).astype(np.float64)
+    # each step: a bounded sample of the replica step (b_s of the 32 transitions) so K + W steps take ~2 min
+    t0 = time.perf_counter()
+    O.run(net, O.TrainCfg(minibatch=1, target_sync=1000), 1000, [rp], theta0, 1)
+    per_tr = time.perf_counter() - t0
+    total = max(1, args.steps + args.warmup)
+    b_s = int(max(1, min(b_full, 120.0 / (per_tr * total))))
+    cfg = O.TrainCfg(minibatch=b_s, target_sync=1000)
+    O.run(net, cfg, 1000, [rp], theta0, args.warmup)
+    t0 = time.perf_counter()
+    O.run(net, cfg, 1000, [rp], theta0, args.steps)
+    dt = time.perf_counter() - t0
+    v = args.steps * b_s / dt
+    sample = (f"{args.steps} oracle replica steps of b={b_s} (of b={b_full}), Mnih net, replay 1k G-pong "
+              f"(of 1M), fp64 single thread")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "BASELINE.json configs[1]" if world == 1 else "BASELINE.json configs[2]",
+                       "minibatch": b_full, "replay": 1_000_000, "net": "Mnih-2013"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "bf16"])
+    ap.add_argument("--replay", type=int, default=1_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--profile-steps", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import numpy as np
+    import torch
+
+    import paper_1508_04186_b200 as D
+    import synth
+
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()  # the context's stream: data generation, the library and the events share it
+    torch.cuda.set_stream(stream)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [D.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    else:
+        dist = None
+        nccl_id = None
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    prec = {"fp32": D.FP32, "bf16": D.BF16}.get(args.precision)
+    b = 32
+    cfg = None
+    for p in ([prec] if prec is not None else [D.BF16, D.FP32]):
+        cfg = D.Config(**MNIH, minibatch=b, replay_capacity=args.replay, target_sync=1000, precision=p,
+                       lr=2.5e-4, gamma=0.99, n_push=1, n_fetch=1)
+        try:
+            dqn = D.DQN(cfg, rank=rank, world=world, nccl_id=nccl_id, stream=stream.cuda_stream)
+            break
+        except D.DqnError as e:
+            if prec is not None or p == D.FP32 or e.code != D.EINVAL:
+                raise
+    dtype = "bf16" if cfg.precision == D.BF16 else "f32"
+
+    # ---- prefill the replay memory with G-pong transitions generated on the GPU
+    t0 = time.time()
+    chunk = 8192
+    done = 0
+    while done < args.replay:
+        n = min(chunk, args.replay - done)
+        s, a, r, sn, t = synth.g_pong_torch(n, 4, 84, 84, 6, 0x5EED + 1000 * rank + done, "cuda")
+        dqn.push(s, a, r, sn, t)
+        done += n
+    del s, a, r, sn, t
+    torch.cuda.synchronize()
+    prefill_s = time.time() - t0
+
+    # ---- warm-up (captures the step graphs)
+    dqn.train(args.warmup)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region: K steps in one dqn_train_steps call, CUDA events on the context stream
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        out = dqn.train(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = out["kernel_launches"]
+    if dist is not None:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = world * b * args.steps / (ms / 1e3)
+
+    # ---- e2e: through the public API with host buffers; per step push the step's new experience
+    # (Alg. 1: one Store per iteration) from pinned host memory, run the step, read the loss back
+    ne = args.e2e_steps
+    hs = torch.from_numpy(synth.g_pong(ne, 4, 84, 84, 6, 99 + rank)[0]).pin_memory()
+    hsn = torch.from_numpy(synth.g_pong(ne, 4, 84, 84, 6, 98 + rank)[0]).pin_memory()
+    ha = torch.zeros(ne, dtype=torch.int32).pin_memory()
+    hr = torch.zeros(ne, dtype=torch.float32).pin_memory()
+    ht = torch.zeros(ne, dtype=torch.uint8).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(ne):
+        dqn.push(hs[i:i + 1], ha[i:i + 1], hr[i:i + 1], hsn[i:i + 1], ht[i:i + 1])
+        dqn.train(1, want_loss=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if dist is not None:
+        tt = torch.tensor([ems], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ems = float(tt.item())
+    e2e = {"value": world * b * ne / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * 4 * 84 * 84 + 4 + 4 + 1,
+           "d2h_bytes_per_step": 4 + 48, "steps": ne,
+           "what": "per step: dqn_push_transitions of 1 new experience from pinned host memory + "
+                   "dqn_train_steps(1) + loss/counters D2H"}
+
+    # ---- per-region device times (CUDA events inside the replayed step graph)
+    regions = dqn.profile(args.profile_steps) if args.profile_steps > 0 else []
+    pk = peaks()
+    roof = None
+    if regions:
+        step_us = sum(r["avg_us"] for r in regions if r["steps"] >= args.profile_steps // 2)
+        top = max(regions, key=lambda r: r["avg_us"])
+        flops, byts = region_work(top["name"], b)
+        if dtype == "bf16" and flops:
+            roof = {"bound": "tensor", "achieved": flops / (top["avg_us"] * 1e-6) / 1e12, "peak": pk["bf16_sus"],
+                    "unit": "TFLOP/s"}
+        elif flops:
+            roof = {"bound": "alu", "achieved": flops / (top["avg_us"] * 1e-6) / 1e12,
+                    "peak": FP32_ALU_PEAK_TFLOPS, "unit": "TFLOP/s"}
+        else:
+            roof = {"bound": "hbm", "achieved": byts / (top["avg_us"] * 1e-6) / 1e9, "peak": pk["hbm"],
+                    "unit": "GB/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["kernel"] = top["name"]
+        roof["avg_us"] = top["avg_us"]
+        roof["share_of_step"] = top["avg_us"] / step_us if step_us else None
+        roof["peak_source"] = (pk["src"] + " MEASURED_PEAKS.json bf16_tflops_sustained" if roof["bound"] == "tensor"
+                               else "derived: 148 SMs x 128 FFMA lanes x 2 x 1.965 GHz" if roof["bound"] == "alu"
+                               else pk["src"] + " MEASURED_PEAKS.json hbm_gbs")
+
+    if rank != 0:
+        dqn.close()
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": "BASELINE.json configs[1]" if world == 1 else "BASELINE.json configs[2]",
+                   "net": "Mnih-2013 (conv16 8x8/4, conv32 4x4/2, fc256, 6 actions)", "minibatch_per_replica": b,
+                   "replay_per_replica": args.replay, "target_sync_C": 1000, "n_push": 1, "n_fetch": 1,
+                   "parallelism": f"dp{world} + sharded parameter server", "gamma": 0.99,
+                   "l2": "inputs larger than L2: each step gathers 32 random slots of a "
+                         f"{args.replay * 56454 / 1e9:.1f} GB replay",
+                   "prefill_s": round(prefill_s, 1)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "roofline": roof,
+        "regions_us": {r["name"]: round(r["avg_us"], 2) for r in regions},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+    dqn.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -97,7 +97,17 @@ typedef struct {
   int32_t* sampled_idx;      /* [k][b] replay slots sampled by this replica (a1)                     */
   int32_t* target_argmax;    /* [k][b] argmax_a' Q(phi_{j+1}, a'; theta^), lowest index on ties      */
   float* loss_per_step;      /* [k]                                                                  */
+  /* output */
+  int64_t kernel_launches;   /* kernels of this library launched by the call (graph kernel nodes)     */
 } dqn_step_stats;
+
+/* Per-region device time of the replica step (diagnostic; dqn_profile_steps). */
+typedef struct {
+  char name[48];             /* step region, e.g. "conv1_fwd", "head_td", "rmsprop_update"            */
+  double avg_us;             /* mean device time per step, CUDA events around the region in the graph */
+  int32_t kernels;           /* kernels in the region                                                */
+  int32_t steps;             /* steps in which the region ran                                        */
+} dqn_region_time;
 
 /* Number of parameters P (weights + biases of every layer); -1 if the layer chain
  * is invalid. Pure. Canonical flat order: layer by layer, W then b; conv W is
@@ -135,6 +145,12 @@ int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_
  * stats may be NULL. DQN_EEMPTY if the replay memory is empty (nothing run);
  * DQN_ENONFINITE if any round so far produced a non-finite mean gradient. */
 int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats);
+
+/* Diagnostic twin of dqn_train_steps (collective, same semantics: it advances the
+ * run by k real steps): the step graphs are captured with CUDA event records
+ * around every region, each step is replayed and synchronised, and the mean
+ * device time per region is written to out[cap]; *n_regions = regions found. */
+int dqn_profile_steps(dqn_ctx* ctx, int64_t k, dqn_region_time* out, int32_t cap, int32_t* n_regions);
 
 /* Q(s, a; theta_local) for n states [n][F][H][W] u8 -> q [n][n_actions] fp32 and
  * (optional) argmax [n] int32, lowest index on ties. Not collective. */

@@ -48,7 +48,11 @@ class _Config(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("loss_mean", C.c_double), ("generation", C.c_int64), ("steps_done", C.c_int64),
                 ("device_ms", C.c_float), ("nonfinite_rounds", C.c_int64), ("sampled_idx", C.c_void_p),
-                ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p)]
+                ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p), ("kernel_launches", C.c_int64)]
+
+
+class _RegionTime(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("avg_us", C.c_double), ("kernels", C.c_int32), ("steps", C.c_int32)]
 
 
 @dataclass
@@ -116,6 +120,7 @@ def lib() -> C.CDLL:
         L.dqn_push_transitions.argtypes = [P, C.c_int64, P, P, P, P, P]
         L.dqn_train_steps.argtypes = [P, C.c_int64, C.POINTER(_Stats)]
         L.dqn_q_values.argtypes = [P, C.c_int64, P, P, P]
+        L.dqn_profile_steps.argtypes = [P, C.c_int64, C.POINTER(_RegionTime), C.c_int32, C.POINTER(C.c_int32)]
         L.dqn_get_params.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
         L.dqn_replay_size.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.dqn_last_error.restype = C.c_char_p
@@ -126,7 +131,7 @@ def lib() -> C.CDLL:
 
 
 EXPORTED = ("dqn_param_count", "dqn_nccl_id_bytes", "dqn_nccl_unique_id", "dqn_create", "dqn_push_transitions",
-            "dqn_train_steps", "dqn_q_values", "dqn_get_params", "dqn_replay_size", "dqn_last_error", "dqn_destroy")
+            "dqn_train_steps", "dqn_profile_steps", "dqn_q_values", "dqn_get_params", "dqn_replay_size", "dqn_last_error", "dqn_destroy")
 
 
 def param_count(cfg: Config) -> int:
@@ -203,9 +208,17 @@ class DQN:
         rc = lib().dqn_train_steps(self._h, k, C.byref(st))
         out = dict(loss_mean=st.loss_mean, generation=st.generation, steps_done=st.steps_done,
                    device_ms=st.device_ms, nonfinite_rounds=st.nonfinite_rounds, idx=idx, argmax=am, loss=lp,
-                   rc=rc)
+                   kernel_launches=st.kernel_launches, rc=rc)
         self._check(rc)
         return out
+
+    def profile(self, k: int) -> list:
+        """k real steps with CUDA events around every region of the step graph -> per-region mean us."""
+        buf = (_RegionTime * 64)()
+        n = C.c_int32()
+        self._check(lib().dqn_profile_steps(self._h, k, buf, 64, C.byref(n)))
+        return [dict(name=buf[i].name.decode(), avg_us=buf[i].avg_us, kernels=buf[i].kernels, steps=buf[i].steps)
+                for i in range(min(n.value, 64))]
 
     def q_values(self, states, q_out=None, argmax_out=None):
         n = len(states)

@@ -65,8 +65,17 @@ struct dqn_ctx {
   long long push_chunk = 0;
   // host mirrors of the deterministic schedule (identical on every rank)
   long long T = 0, n = 0, n_local = 0, ell = 0;
-  // graphs per (fetch, refresh, push) variant
-  cudaGraphExec_t graphs[8] = {};
+  // graphs per (fetch, refresh, push) variant; [8..15]: the same with profiling event records
+  cudaGraphExec_t graphs[16] = {};
+  long long graph_kernels[16] = {};
+  // profiling (dqn_profile_steps): event pairs around each step region, per graph variant
+  struct ProfMark {
+    std::string name;
+    cudaEvent_t a, b;
+    int kernels;
+  };
+  std::vector<ProfMark> marks[16];
+  int capture_variant = -1;  // >= 8 while capturing a profiling graph
   bool use_graphs = true;
   bool keep_grad = false;
   bool alias_local = false;
@@ -218,6 +227,11 @@ static int dalloc(dqn_ctx* ctx, T** p, long long n) {
 static void free_all(dqn_ctx* c) {
   for (auto& g : c->graphs)
     if (g) cudaGraphExecDestroy(g);
+  for (auto& v : c->marks)
+    for (auto& m : v) {
+      cudaEventDestroy(m.a);
+      cudaEventDestroy(m.b);
+    }
   void* ptrs[] = {c->ring_s, c->ring_sn, c->ring_t, c->ring_a, c->ring_r, c->rms, c->grad, c->g_shard,
                   c->theta_hat, c->grad_snap, c->gather_tmp, c->partial, c->idx, c->ctr, c->diag_loss,
                   c->diag_idx, c->diag_amax, c->q_stage, c->q_out, c->q_amax, c->push_s, c->push_sn, c->push_t,
@@ -275,7 +289,7 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   if (cuda_stream) {
     ctx->stream = (cudaStream_t)cuda_stream;
   } else {
-    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault));  // blocking: ordered after legacy-stream producers
     ctx->own_stream = true;
   }
   CK(cudaEventCreate(&ctx->ev0));
@@ -453,6 +467,22 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
   return DQN_OK;
 }
 
+// ------------------------------------------------------------------ profiling marks
+static void prof_begin(dqn_ctx* ctx, const std::string& name, int kernels) {
+  if (ctx->capture_variant < 8) return;
+  dqn_ctx::ProfMark m{name, nullptr, nullptr, kernels};
+  cudaEventCreate(&m.a);
+  cudaEventCreate(&m.b);
+  cudaEventRecordWithFlags(m.a, ctx->stream, cudaEventRecordExternal);  // a real event node in the graph
+  ctx->marks[ctx->capture_variant].push_back(m);
+}
+static void prof_end(dqn_ctx* ctx) {
+  if (ctx->capture_variant < 8) return;
+  cudaEventRecordWithFlags(ctx->marks[ctx->capture_variant].back().b, ctx->stream, cudaEventRecordExternal);
+}
+#define PB(name, k) prof_begin(ctx, name, k)
+#define PE() prof_end(ctx)
+
 // ------------------------------------------------------------------ one replica step (fp32 path)
 // Enqueue the kernels of one step T on ctx->stream (captured into a graph).
 static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
@@ -463,15 +493,24 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   // a13 fetch + a14 target refresh
   if (fetch) {
     if (ctx->world > 1) {
+      PB("fetch_all_gather", 0);
       NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
+      PE();
     } else if (!ctx->alias_local) {
+      PB("fetch_copy", 0);
       CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_master, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+      PE();
     }
-    if (refresh)
+    if (refresh) {
+      PB("target_refresh", 0);
       CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+      PE();
+    }
   }
   // a1 sample
+  PB("sample", 1);
   launch_sample(ctx->idx, b, c.seed, (unsigned)ctx->rank, ctx->ctr, st);
+  PE();
   // a2-a4 convolutions, theta on s and theta^ on s' in one launch per layer
   ImgSrc src0{};
   src0.u8[0] = ctx->ring_s;
@@ -487,8 +526,10 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
       const ConvShape& P = net.conv[i - 1];
       src.stride = (long long)P.N * P.Ho * P.Wo;
     }
+    PB("conv" + std::to_string(i + 1) + "_fwd", 1);
     launch_conv_fwd_f32(net.conv[i], src, ctx->theta_local, ctx->theta_hat, ctx->act_conv[i][0], ctx->act_conv[i][1],
                         b, 2, st);
+    PE();
   }
   // a5 hidden FC layers
   const ConvShape& LC = net.conv[net.n_conv - 1];
@@ -502,7 +543,9 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
     g.bias[0] = ctx->theta_local + F.b_off; g.bias[1] = ctx->theta_hat + F.b_off;
     g.M = b; g.N = F.H; g.K = F.D; g.groups = 2; g.splits = pick_splits(b, F.H, F.D, 2);
     g.epi = EPI_BIAS_RELU; g.partial = ctx->partial;
+    PB("fc" + std::to_string(l + 1) + "_fwd", g.splits > 1 ? 2 : 1);
     launch_gemm_f32(g, st);
+    PE();
     in[0] = ctx->act_fc[l][0]; in[1] = ctx->act_fc[l][1];
   }
   (void)LC;
@@ -520,12 +563,15 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   h.grad = ctx->grad;
   h.dH = net.n_fc > 0 ? ctx->dz_fc[net.n_fc - 1] : ctx->dz_conv[net.n_conv - 1];
   h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
+  PB("head_td", 1);
   launch_head_f32(h, st);
+  PE();
   // a7 hidden FC backward
   for (int l = net.n_fc - 1; l >= 0; --l) {
     const FcShape& F = net.fc[l];
     const float* dz = ctx->dz_fc[l];
     const float* a_in = l > 0 ? ctx->act_fc[l - 1][0] : ctx->act_conv[net.n_conv - 1][0];
+    PB("fc" + std::to_string(l + 1) + "_bwd", (l < net.n_fc - 1 ? 1 : 0) + 1 + (pick_splits(b, F.D, F.H, 1) > 1 ? 2 : 1));
     if (l < net.n_fc - 1) launch_bias_grad(dz, b, F.H, ctx->grad + F.b_off, st);
     GemmArgs gw{};  // dW[h][d] += sum_j dz[j][h] a_in[j][d]
     gw.A[0] = dz; gw.sam = 1; gw.sak = F.H;
@@ -541,6 +587,7 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
     gx.M = b; gx.N = F.D; gx.K = F.H; gx.groups = 1; gx.splits = pick_splits(b, F.D, F.H, 1);
     gx.epi = EPI_MASK; gx.partial = ctx->partial;
     launch_gemm_f32(gx, st);
+    PE();
   }
   // a8/a9 convolution backward
   for (int i = net.n_conv - 1; i >= 0; --i) {
@@ -552,10 +599,12 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
       src.f32[0] = ctx->act_conv[i - 1][0];
       src.stride = (long long)L.C * L.H * L.W;
     }
+    PB("conv" + std::to_string(i + 1) + "_bwd", i > 0 ? 3 : 2);
     launch_conv_bwd_dw_f32(L, ctx->dz_conv[i], src, ctx->partial, b, st);
     launch_reduce_rows(ctx->partial, b, (long long)L.N * L.C * L.k * L.k + L.N, ctx->grad + L.w_off, st);
     if (i > 0) launch_conv_bwd_dx_f32(L, ctx->dz_conv[i], ctx->theta_local, ctx->act_conv[i - 1][0],
                                       ctx->dz_conv[i - 1], b, st);
+    PE();
   }
   if (ctx->keep_grad)
     CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
@@ -564,33 +613,114 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
     const float div = (float)((double)ctx->world * c.n_push);
     const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
     if (ctx->world > 1) {
+      PB("push_reduce_scatter", 0);
       NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
       CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
+      PE();
+      PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
                      (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 1, st);
+      PE();
     } else {
+      PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
                      (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 1, st);
+      PE();
     }
   }
   CK(cudaGetLastError());
   return DQN_OK;
 }
 
-static int run_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
-  if (!ctx->use_graphs) return enqueue_step_f32(ctx, fetch, refresh, push);
-  const int v = (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0);
+// Replay the graph of one step variant (captured on first use). profile: the
+// variant with event records around each region. *kernels += kernel nodes run.
+static int run_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push, bool profile, long long* kernels) {
+  if (!ctx->use_graphs && !profile) return enqueue_step_f32(ctx, fetch, refresh, push);
+  const int v = (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0) | (profile ? 8 : 0);
   if (!ctx->graphs[v]) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    ctx->capture_variant = v;
     int rc = enqueue_step_f32(ctx, fetch, refresh, push);
+    ctx->capture_variant = -1;
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
     if (rc) return rc;
     if (e != cudaSuccess) return set_err(ctx, DQN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    size_t n = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(g, nodes.data(), &n));
+    long long nk = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      CK(cudaGraphNodeGetType(nd, &t));
+      if (t == cudaGraphNodeTypeKernel) ++nk;
+    }
+    ctx->graph_kernels[v] = nk;
     CK(cudaGraphInstantiate(&ctx->graphs[v], g, 0));
     cudaGraphDestroy(g);
   }
   CK(cudaGraphLaunch(ctx->graphs[v], ctx->stream));
+  if (kernels) *kernels += ctx->graph_kernels[v];
+  return DQN_OK;
+}
+
+// O10 / O11 / O9 schedule of step T (host mirror; identical on every rank)
+static void schedule(dqn_ctx* ctx, bool* fetch, bool* refresh, bool* push) {
+  const dqn_config& c = ctx->cfg;
+  const long long T = ctx->T;
+  *fetch = (T % c.n_fetch) == 0;
+  *refresh = false;
+  if (*fetch) {
+    ctx->n_local = ctx->n;
+    if (ctx->n_local - ctx->ell >= c.target_sync) {
+      *refresh = true;
+      ctx->ell = ctx->n_local;
+    }
+  }
+  *push = ((T + 1) % c.n_push) == 0;
+}
+
+extern "C" int dqn_profile_steps(dqn_ctx* ctx, int64_t k, dqn_region_time* out, int32_t cap, int32_t* n_regions) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  if (k < 0) return set_err(ctx, DQN_EINVAL, "k must be >= 0");
+  if (ctx->count == 0) return set_err(ctx, DQN_EEMPTY, "replay memory is empty (A13)");
+  std::vector<std::string> names;
+  std::vector<double> tot;
+  std::vector<int> cnt, kern;
+  for (long long s = 0; s < k; ++s) {
+    bool fetch, refresh, push;
+    schedule(ctx, &fetch, &refresh, &push);
+    int rc = run_step(ctx, fetch, refresh, push, true, nullptr);
+    if (rc) return rc;
+    if (push) ctx->n += 1;
+    ctx->T += 1;
+    CK(cudaStreamSynchronize(ctx->stream));
+    const int v = (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0) | 8;
+    for (auto& m : ctx->marks[v]) {
+      float ms = 0.0f;
+      CK(cudaEventElapsedTime(&ms, m.a, m.b));
+      size_t i = 0;
+      while (i < names.size() && names[i] != m.name) ++i;
+      if (i == names.size()) {
+        names.push_back(m.name);
+        tot.push_back(0.0);
+        cnt.push_back(0);
+        kern.push_back(m.kernels);
+      }
+      tot[i] += ms * 1000.0;
+      cnt[i] += 1;
+    }
+  }
+  if (n_regions) *n_regions = (int32_t)names.size();
+  for (size_t i = 0; i < names.size() && out && (int32_t)i < cap; ++i) {
+    std::memset(out[i].name, 0, sizeof(out[i].name));
+    std::strncpy(out[i].name, names[i].c_str(), sizeof(out[i].name) - 1);
+    out[i].avg_us = tot[i] / cnt[i];
+    out[i].kernels = kern[i];
+    out[i].steps = cnt[i];
+  }
   return DQN_OK;
 }
 
@@ -602,20 +732,12 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
   const dqn_config& c = ctx->cfg;
   const long long T0 = ctx->T;
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  long long kernels = 0;
   for (long long s = 0; s < k; ++s) {
-    const long long T = ctx->T;
     // O10 / O11: fetch at the start of step T when T % n_fetch == 0, then refresh theta^ when n - l >= C
-    const bool fetch = (T % c.n_fetch) == 0;
-    bool refresh = false;
-    if (fetch) {
-      ctx->n_local = ctx->n;
-      if (ctx->n_local - ctx->ell >= c.target_sync) {
-        refresh = true;
-        ctx->ell = ctx->n_local;
-      }
-    }
-    const bool push = ((T + 1) % c.n_push) == 0;
-    int rc = run_step(ctx, fetch, refresh, push);
+    bool fetch, refresh, push;
+    schedule(ctx, &fetch, &refresh, &push);
+    int rc = run_step(ctx, fetch, refresh, push, false, &kernels);
     if (rc) return rc;
     if (push) ctx->n += 1;
     ctx->T += 1;
@@ -653,6 +775,7 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
     stats->generation = ctx->n;
     stats->steps_done = ctx->T;
     stats->nonfinite_rounds = hc.nonfinite_rounds;
+    stats->kernel_launches = kernels;
     double lm = 0.0;
     for (float l : loss) lm += l;
     stats->loss_mean = loss.empty() ? 0.0 : lm / (double)loss.size();
