@@ -62,6 +62,9 @@ def region_work(name: str, b: int):
         "rmsprop_update": (0, 677686 * 4 * 6),
         "sample": (0, b * 4),
     }
+    # fused regions of the bf16 tensor-core path
+    w["conv_fwd"] = tuple(x + y for x, y in zip(w["conv1_fwd"], w["conv2_fwd"]))
+    w["conv_bwd"] = tuple(x + y for x, y in zip(w["conv1_bwd"], w["conv2_bwd"]))
     return w.get(name, (0, 0))
 
 

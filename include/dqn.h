@@ -92,7 +92,7 @@ typedef struct {
   int64_t generation;        /* server iteration number n after the call (Alg. 2)              */
   int64_t steps_done;        /* replica step counter T after the call                                */
   float device_ms;           /* device time of the call (CUDA events on the context stream)          */
-  int64_t nonfinite_rounds;  /* push rounds so far with a non-finite mean gradient (A24)              */
+  int64_t nonfinite_elems;   /* mean-gradient elements so far that were non-finite and skipped (A24) */
   /* optional caller-owned HOST outputs (NULL = not wanted); valid when k <= 4096 */
   int32_t* sampled_idx;      /* [k][b] replay slots sampled by this replica (a1)                     */
   int32_t* target_argmax;    /* [k][b] argmax_a' Q(phi_{j+1}, a'; theta^), lowest index on ties      */

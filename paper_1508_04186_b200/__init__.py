@@ -47,7 +47,7 @@ class _Config(C.Structure):
 
 class _Stats(C.Structure):
     _fields_ = [("loss_mean", C.c_double), ("generation", C.c_int64), ("steps_done", C.c_int64),
-                ("device_ms", C.c_float), ("nonfinite_rounds", C.c_int64), ("sampled_idx", C.c_void_p),
+                ("device_ms", C.c_float), ("nonfinite_elems", C.c_int64), ("sampled_idx", C.c_void_p),
                 ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p), ("kernel_launches", C.c_int64)]
 
 
@@ -207,7 +207,7 @@ class DQN:
         st.loss_per_step = lp.ctypes.data if lp is not None else None
         rc = lib().dqn_train_steps(self._h, k, C.byref(st))
         out = dict(loss_mean=st.loss_mean, generation=st.generation, steps_done=st.steps_done,
-                   device_ms=st.device_ms, nonfinite_rounds=st.nonfinite_rounds, idx=idx, argmax=am, loss=lp,
+                   device_ms=st.device_ms, nonfinite_elems=st.nonfinite_elems, idx=idx, argmax=am, loss=lp,
                    kernel_launches=st.kernel_launches, rc=rc)
         self._check(rc)
         return out

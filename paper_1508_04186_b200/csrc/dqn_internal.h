@@ -79,6 +79,16 @@ struct GemmArgs {
 
 struct HeadArgs {
   const float* act[2];        // [b][H]: input of the output layer for s (theta) / s' (theta^)
+  // bf16 path: act[] is produced here from the FC split-K partials [g][split][b_row][H]
+  const float* fc_partial;    // nullptr: act[] given
+  int fc_splits;
+  long long fc_split_stride;  // floats between splits
+  const float* fc_bias[2];
+  float* act_out[2];          // where the reduced activations are stored (h of s is reused by the finish)
+  // per-sample scratch written by head_sample, read by head_finish
+  float* s_dq;                // [b]
+  int* s_act;                 // [b]
+  float* s_loss;              // [b]
   const float* theta;         // live theta (fp32, canonical)
   const float* theta_hat;     // target theta^ (fp32, canonical)
   long long w_off, b_off;     // output layer
@@ -92,6 +102,7 @@ struct HeadArgs {
   float gamma, clip;
   float* grad;                // G (accumulated)
   float* dH;                  // [b][H] d(pre-activation) of the previous layer
+  __nv_bfloat16* dH_bf16;     // optional bf16 copy of dH (tensor-core backward operand)
   DevCounters* ctr;
   float* diag_loss;           // [kDiagSteps]
   int* diag_idx;              // [kDiagSteps][b]
@@ -108,10 +119,9 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
                            long long state_bytes, const uint8_t* s, const int32_t* a, const float* r,
                            const uint8_t* sn, const uint8_t* t, cudaStream_t st);
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
-                    float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int count_round,
+                    float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
                     cudaStream_t st);
 void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st);
-void launch_bump_generation(DevCounters* ctr, cudaStream_t st);
 
 // fp32 SIMT path (kernels_f32.cu)
 void init_f32_kernel_attrs();
@@ -125,7 +135,67 @@ void launch_reduce_rows(const float* partial, int rows, long long E, float* dst,
 void launch_gemm_f32(const GemmArgs& g, cudaStream_t st);
 void launch_bias_grad(const float* dz, int b, int H, float* dst, cudaStream_t st);
 void launch_head_f32(const HeadArgs& h, cudaStream_t st);
+size_t head_smem_bytes(int A, int H, int b);
 void launch_q_head_f32(const float* act, const float* theta, long long w_off, long long b_off, int H, int A, int n,
                        float* q, int* argmax, cudaStream_t st);
+
+// bf16 tensor-core path, Mnih-2013 net (kernels_bf16.cu)
+struct FwdConvArgs {
+  const uint8_t* ring[2];          // s / s' rings (s2d) or a staging buffer (ctr == nullptr: image j = slot j)
+  const __nv_bfloat16* theta[2];   // canonical bf16 parameters (theta, theta^)
+  const float* theta_f32[2];       // canonical fp32 parameters (biases)
+  long long w1_off, b1_off, w2_off, b2_off;
+  int* idx;                        // out (group 0) [n]
+  const DevCounters* ctr;
+  unsigned long long seed;
+  unsigned rank;
+  int n;
+  __nv_bfloat16* a2;               // [groups*n][2592]
+  uint8_t* a1_save;                // [n][8][144][16] or nullptr
+};
+struct TcGemmArgs {
+  const __nv_bfloat16* A[2];
+  long long lda;  // A(m,k) = a_mn ? A[k*lda + m] : A[m*lda + k]
+  const __nv_bfloat16* B[2];
+  long long ldb;  // B(n,k) = b_mn ? B[k*ldb + n] : B[n*ldb + k]
+  int a_mn, b_mn;
+  int M, N, K;
+  int BN;         // n-tile (multiple of 16, <= 256)
+  int kper;       // K per split (multiple of 16)
+  int splits;
+  int epi;        // TC_EPI_*
+  float* C[2];    // TC_EPI_ACCUM: C[g][m*ldc + n] += D
+  long long ldc;
+  float* partial;           // TC_EPI_FC_FWD: partial[g][split][m][n]
+  unsigned* counters;       // [groups * m_tiles], self-resetting
+  const float* bias[2];
+  float* h_out[2];          // [N][M] = relu(sum + bias[m])
+  __nv_bfloat16* out_bf16;  // TC_EPI_MASK_T: out[n*ldo + m] = mask[n*ldo + m] > 0 ? D : 0
+  const __nv_bfloat16* mask;
+  long long ldo;
+};
+enum { TC_EPI_ACCUM = 0, TC_EPI_FC_FWD = 1, TC_EPI_MASK_T = 2 };
+struct BwdConvArgs {
+  const uint8_t* ring_s;
+  const int* idx;
+  const uint8_t* a1_save;
+  const __nv_bfloat16* dz2;        // [n][2592]
+  const __nv_bfloat16* theta;      // bf16 canonical
+  long long w1_off, b1_off, w2_off, b2_off;
+  int n;
+  float* partial;                  // [n][kBwdPart]
+  unsigned* counter;
+  float* grad;
+};
+constexpr int kMnihSlot = 28224;
+constexpr int kA1Bytes = 8 * 144 * 16;
+constexpr int kBwdPart = 256 * 16 + 256 * 32 + 16 + 32;
+void init_bf16_kernel_attrs();
+void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t, long long cap,
+                     long long count0, long long first, long long n, const uint8_t* s, const int32_t* a,
+                     const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st);
+void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st);
+void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st);
+void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st);
 
 }  // namespace dqn

@@ -48,12 +48,28 @@ struct dqn_ctx {
   float* dz_conv[kMaxConv] = {};
   float* dz_fc[kMaxFc] = {};
   float* partial = nullptr;
+  float* head_dq = nullptr;   // [b] per-sample scratch of the TD head
+  int* head_act = nullptr;    // [b]
+  float* head_loss = nullptr; // [b]
   long long partial_elems = 0;
   int* idx = nullptr;
   DevCounters* ctr = nullptr;
   float* diag_loss = nullptr;
   int* diag_idx = nullptr;
   int* diag_amax = nullptr;
+  // bf16 tensor-core path (precision == DQN_BF16)
+  bool bf16 = false;
+  __nv_bfloat16* theta_local_bf16 = nullptr;  // [P_pad] working copy the tensor cores read
+  __nv_bfloat16* theta_hat_bf16 = nullptr;    // [P_pad]
+  __nv_bfloat16* a2_bf16 = nullptr;           // [2b][2592] conv2 activations (s: theta, s': theta^)
+  uint8_t* a1_save = nullptr;                 // [b][8][144][16] conv1 activations (s2d planes)
+  __nv_bfloat16* dh_bf16 = nullptr;           // [b][H]
+  __nv_bfloat16* dz2_bf16 = nullptr;          // [b][2592]
+  float* fc_partial = nullptr;                // [2][splits][H][b]
+  unsigned* tc_counters = nullptr;            // last-CTA counters (self-resetting)
+  float* bwd_partial = nullptr;               // [b][kBwdPart]
+  uint8_t* q_stage_s2d = nullptr;             // [b][28224]
+  int fc_splits = 1;
   // q_values staging
   uint8_t* q_stage = nullptr;
   float* q_out = nullptr;
@@ -183,7 +199,22 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
       !std::isfinite(c->gamma) || !(c->err_clip >= 0.0)) {
     *why = "invalid hyper-parameter"; return DQN_EINVAL;
   }
-  if (c->precision == DQN_BF16) { *why = "DQN_BF16 path not built yet"; return DQN_EINVAL; }
+  {  // the TD head keeps the output layers and 32 samples' activations in shared memory
+    const FcShape& O = net->fc[net->n_fc];
+    if (O.H > 32 || head_smem_bytes(O.H, O.D, c->minibatch) > 227 * 1024) {
+      *why = "output layer too large for the TD-head kernel (|A| <= 32)"; return DQN_EINVAL;
+    }
+  }
+  if (c->precision == DQN_BF16) {
+    // the tensor-core kernels are specialised to the Mnih-2013 convolution stack (BASELINE.json configs[0..3])
+    const bool mnih = c->frames == 4 && c->height == 84 && c->width == 84 && c->n_conv == 2 &&
+                      c->conv_filters[0] == 16 && c->conv_kernel[0] == 8 && c->conv_stride[0] == 4 &&
+                      c->conv_filters[1] == 32 && c->conv_kernel[1] == 4 && c->conv_stride[1] == 2 && c->n_fc == 1;
+    if (!mnih) { *why = "DQN_BF16 supports the Mnih-2013 conv stack (conv16 8x8/4, conv32 4x4/2, one FC)"; return DQN_EINVAL; }
+    if (c->minibatch % 16 != 0 || c->minibatch > 256) { *why = "DQN_BF16 needs minibatch % 16 == 0 and <= 256"; return DQN_EINVAL; }
+    if (c->fc_units[0] % 16 != 0 || c->fc_units[0] > 1024) { *why = "DQN_BF16 needs fc units % 16 == 0"; return DQN_EINVAL; }
+    return DQN_OK;
+  }
   // fp32 kernels stage one input image (+ one filter chunk) in shared memory
   for (int i = 0; i < net->n_conv; ++i) {
     const ConvShape& L = net->conv[i];
@@ -234,8 +265,9 @@ static void free_all(dqn_ctx* c) {
     }
   void* ptrs[] = {c->ring_s, c->ring_sn, c->ring_t, c->ring_a, c->ring_r, c->rms, c->grad, c->g_shard,
                   c->theta_hat, c->grad_snap, c->gather_tmp, c->partial, c->idx, c->ctr, c->diag_loss,
-                  c->diag_idx, c->diag_amax, c->q_stage, c->q_out, c->q_amax, c->push_s, c->push_sn, c->push_t,
-                  c->push_a, c->push_r};
+                  c->diag_idx, c->diag_amax, c->head_dq, c->head_act, c->head_loss, c->q_stage, c->q_out, c->q_amax, c->push_s, c->push_sn, c->push_t,
+                  c->push_a, c->push_r, c->theta_local_bf16, c->theta_hat_bf16, c->a2_bf16, c->a1_save,
+                  c->dh_bf16, c->dz2_bf16, c->fc_partial, c->tc_counters, c->bwd_partial, c->q_stage_s2d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->theta_local && !c->alias_local) cudaFree(c->theta_local);
@@ -285,6 +317,7 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   ctx->use_graphs = !(getenv("DQN_NO_GRAPH") && atoi(getenv("DQN_NO_GRAPH")));
   ctx->keep_grad = getenv("DQN_KEEP_GRAD") && atoi(getenv("DQN_KEEP_GRAD"));
   ctx->alias_local = (world == 1 && cfg->n_fetch == 1);
+  ctx->bf16 = cfg->precision == DQN_BF16;
 
   if (cuda_stream) {
     ctx->stream = (cudaStream_t)cuda_stream;
@@ -344,6 +377,9 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   ctx->partial_elems = max_partial;
   if ((rc = dalloc(ctx, &ctx->partial, max_partial))) return rc;
   if ((rc = dalloc(ctx, &ctx->idx, b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->head_dq, b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->head_act, b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->head_loss, b))) return rc;
   if ((rc = dalloc(ctx, &ctx->ctr, 1))) return rc;
   CK(cudaMemsetAsync(ctx->ctr, 0, sizeof(DevCounters), ctx->stream));
   if ((rc = dalloc(ctx, &ctx->diag_loss, kDiagSteps))) return rc;
@@ -352,6 +388,22 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   if ((rc = dalloc(ctx, &ctx->q_stage, qn * sb))) return rc;
   if ((rc = dalloc(ctx, &ctx->q_out, qn * net.A))) return rc;
   if ((rc = dalloc(ctx, &ctx->q_amax, qn))) return rc;
+  if (ctx->bf16) {
+    init_bf16_kernel_attrs();
+    const int H = net.fc[0].H;
+    ctx->fc_splits = 18;  // K = 2592 = 18 x 144
+    if ((rc = dalloc(ctx, &ctx->theta_local_bf16, ctx->P_pad))) return rc;
+    if ((rc = dalloc(ctx, &ctx->theta_hat_bf16, ctx->P_pad))) return rc;
+    if ((rc = dalloc(ctx, &ctx->a2_bf16, 2LL * b * 2592))) return rc;
+    if ((rc = dalloc(ctx, &ctx->a1_save, (long long)b * kA1Bytes))) return rc;
+    if ((rc = dalloc(ctx, &ctx->dh_bf16, (long long)b * H))) return rc;
+    if ((rc = dalloc(ctx, &ctx->dz2_bf16, (long long)b * 2592))) return rc;
+    if ((rc = dalloc(ctx, &ctx->fc_partial, 2LL * ctx->fc_splits * H * b))) return rc;
+    if ((rc = dalloc(ctx, &ctx->tc_counters, 64))) return rc;
+    CK(cudaMemsetAsync(ctx->tc_counters, 0, 64 * sizeof(unsigned), ctx->stream));
+    if ((rc = dalloc(ctx, &ctx->bwd_partial, (long long)b * kBwdPart))) return rc;
+    if ((rc = dalloc(ctx, &ctx->q_stage_s2d, (long long)b * kMnihSlot))) return rc;
+  }
 
   // initial theta (Alg. 2): init_params or N(0, xi^2) from init_seed; theta^ = theta
   std::vector<float> th((size_t)ctx->P_pad, 0.0f);
@@ -374,6 +426,11 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     CK(cudaMemcpyAsync(ctx->theta_local, th.data(), sizeof(float) * ctx->P_pad, cudaMemcpyHostToDevice, ctx->stream));
   }
   CK(cudaMemcpyAsync(ctx->theta_hat, th.data(), sizeof(float) * ctx->P_pad, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->bf16) {
+    launch_f32_to_bf16(ctx->theta_hat, ctx->theta_local_bf16, ctx->P_pad, ctx->stream);
+    launch_f32_to_bf16(ctx->theta_hat, ctx->theta_hat_bf16, ctx->P_pad, ctx->stream);
+    CK(cudaGetLastError());
+  }
   CK(cudaStreamSynchronize(ctx->stream));
 
   if (world > 1) {
@@ -407,6 +464,17 @@ extern "C" int dqn_create(const dqn_config* cfg, int rank, int world, const void
 }
 
 // ------------------------------------------------------------------ push (Alg. 1 "Store")
+// Items [i0, i0+m) of the call (device pointers to their first element) go to slots
+// (count + i0 + i) mod cap; the bf16 path stores conv1's space-to-depth layout.
+static void push_ring(dqn_ctx* ctx, long long i0, long long m, const uint8_t* s, const int32_t* a, const float* r,
+                      const uint8_t* sn, const uint8_t* t) {
+  if (ctx->bf16)
+    launch_push_s2d(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, i0, m, s,
+                    a, r, sn, t, ctx->stream);
+  else
+    launch_push_canonical(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, 0,
+                          i0, m, ctx->net.state_bytes, s, a, r, sn, t, ctx->stream);
+}
 extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a, const float* r,
                                     const uint8_t* s_next, const uint8_t* terminal) {
   if (!ctx) return DQN_EINVAL;
@@ -440,9 +508,7 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
       CK(cudaMemcpyAsync(ctx->push_a, a + i0, m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
       CK(cudaMemcpyAsync(ctx->push_r, r + i0, m * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
       CK(cudaMemcpyAsync(ctx->push_t, terminal + i0, m, cudaMemcpyHostToDevice, ctx->stream));
-      launch_push_canonical(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, 0,
-                            i0, m, sb, ctx->push_s, ctx->push_a, ctx->push_r, ctx->push_sn, ctx->push_t,
-                            ctx->stream);
+      push_ring(ctx, i0, m, ctx->push_s, ctx->push_a, ctx->push_r, ctx->push_sn, ctx->push_t);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(ctx->stream));  // staging is reused by the next chunk
     }
@@ -455,8 +521,7 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
     if (bad) return set_err(ctx, DQN_EINVAL, "action out of range or non-finite reward in device push");
     for (long long i0 = first; i0 < n; i0 += 65535) {
       const long long m = std::min<long long>(65535, n - i0);
-      launch_push_canonical(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, 0,
-                            i0, m, sb, s + i0 * sb, a + i0, r + i0, s_next + i0 * sb, terminal + i0, ctx->stream);
+      push_ring(ctx, i0, m, s + i0 * sb, a + i0, r + i0, s_next + i0 * sb, terminal + i0);
       CK(cudaGetLastError());
     }
   }
@@ -563,7 +628,8 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   h.grad = ctx->grad;
   h.dH = net.n_fc > 0 ? ctx->dz_fc[net.n_fc - 1] : ctx->dz_conv[net.n_conv - 1];
   h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
-  PB("head_td", 1);
+  h.s_dq = ctx->head_dq; h.s_act = ctx->head_act; h.s_loss = ctx->head_loss;
+  PB("head_td", 2);
   launch_head_f32(h, st);
   PE();
   // a7 hidden FC backward
@@ -619,7 +685,7 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
       PE();
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
-                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 1, st);
+                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, st);
       PE();
     } else {
       PB("rmsprop_update", 1);
@@ -632,16 +698,143 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   return DQN_OK;
 }
 
+// ------------------------------------------------------------------ one replica step (bf16 tensor-core path)
+// 7 kernels: conv fwd (sample+gather+conv1+conv2, s and s'), FC fwd (split-K, last CTA
+// reduces + bias + ReLU), TD head, FC dW, FC dX (+ReLU mask), conv bwd (conv2 dW/dX,
+// conv1 dW, biases), RMSProp update (+ bf16 publication).
+static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
+  const NetShape& net = ctx->net;
+  const dqn_config& c = ctx->cfg;
+  const int b = c.minibatch;
+  const FcShape& F = net.fc[0];
+  const FcShape& O = net.fc[1];
+  const ConvShape& L1 = net.conv[0];
+  const ConvShape& L2 = net.conv[1];
+  cudaStream_t st = ctx->stream;
+  if (fetch) {  // a13 + a14
+    if (ctx->world > 1) {
+      PB("fetch_all_gather", 1);
+      NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
+      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
+      PE();
+    } else if (!ctx->alias_local) {
+      PB("fetch_copy", 1);
+      CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_master, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
+      PE();
+    }
+    if (refresh) {
+      PB("target_refresh", 0);
+      CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ctx->theta_hat_bf16, ctx->theta_local_bf16, sizeof(__nv_bfloat16) * ctx->P_pad,
+                         cudaMemcpyDeviceToDevice, st));
+      PE();
+    }
+  }
+  // a1-a4: sample + gather + conv1 + conv2 for s (theta) and s' (theta^), tcgen05
+  FwdConvArgs fa{};
+  fa.ring[0] = ctx->ring_s; fa.ring[1] = ctx->ring_sn;
+  fa.theta[0] = ctx->theta_local_bf16; fa.theta[1] = ctx->theta_hat_bf16;
+  fa.theta_f32[0] = ctx->theta_local; fa.theta_f32[1] = ctx->theta_hat;
+  fa.w1_off = L1.w_off; fa.b1_off = L1.b_off; fa.w2_off = L2.w_off; fa.b2_off = L2.b_off;
+  fa.idx = ctx->idx; fa.ctr = ctx->ctr; fa.seed = c.seed; fa.rank = (unsigned)ctx->rank; fa.n = b;
+  fa.a2 = ctx->a2_bf16; fa.a1_save = ctx->a1_save;
+  PB("conv_fwd", 1);
+  launch_fwd_conv_bf16(fa, 2, st);
+  PE();
+  // a5: FC fwd, swap-AB: h^T[H][b] = W[H][2592] a2^T, split-K 18 x 144, last CTA adds bias + ReLU
+  TcGemmArgs gf{};
+  gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.A[1] = ctx->theta_hat_bf16 + F.w_off; gf.lda = F.D; gf.a_mn = 0;
+  gf.B[0] = ctx->a2_bf16; gf.B[1] = ctx->a2_bf16 + (long long)b * F.D; gf.ldb = F.D; gf.b_mn = 0;
+  gf.M = F.H; gf.N = b; gf.K = F.D; gf.BN = b; gf.kper = F.D / ctx->fc_splits; gf.splits = ctx->fc_splits;
+  gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial; gf.counters = ctx->tc_counters;
+  gf.bias[0] = ctx->theta_local + F.b_off; gf.bias[1] = ctx->theta_hat + F.b_off;
+  // (h_out left null: the TD head reduces the split-K partials, adds the bias and applies ReLU)
+  PB("fc1_fwd", 1);
+  launch_tc_gemm(gf, 2, st);
+  PE();
+  // a6 head (TD target, loss, output layer, dH)
+  HeadArgs h{};
+  h.act[0] = ctx->act_fc[0][0]; h.act[1] = ctx->act_fc[0][1];
+  h.theta = ctx->theta_local; h.theta_hat = ctx->theta_hat;
+  h.w_off = O.w_off; h.b_off = O.b_off;
+  h.prev_is_fc = 1; h.prev_b_off = F.b_off;
+  h.H = O.D; h.A = O.H; h.b = b;
+  h.idx = ctx->idx; h.ring_a = ctx->ring_a; h.ring_r = ctx->ring_r; h.ring_term = ctx->ring_t;
+  h.gamma = (float)c.gamma; h.clip = (float)c.err_clip;
+  h.grad = ctx->grad; h.dH = ctx->dz_fc[0]; h.dH_bf16 = ctx->dh_bf16;
+  h.fc_partial = ctx->fc_partial; h.fc_splits = gf.splits; h.fc_split_stride = (long long)gf.BN * gf.M;
+  h.fc_bias[0] = ctx->theta_local + F.b_off; h.fc_bias[1] = ctx->theta_hat + F.b_off;
+  h.act_out[0] = ctx->act_fc[0][0]; h.act_out[1] = ctx->act_fc[0][1];
+  h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
+  h.s_dq = ctx->head_dq; h.s_act = ctx->head_act; h.s_loss = ctx->head_loss;
+  PB("head_td", 2);
+  launch_head_f32(h, st);
+  PE();
+  // a7 FC backward: dW[h][d] += sum_j dH[j][h] a2[j][d]  and  dz2[j][d] = [a2 > 0] sum_h dH[j][h] W[h][d]
+  TcGemmArgs gw{};
+  gw.A[0] = ctx->dh_bf16; gw.lda = F.H; gw.a_mn = 1;
+  gw.B[0] = ctx->a2_bf16; gw.ldb = F.D; gw.b_mn = 1;
+  gw.M = F.H; gw.N = F.D; gw.K = b; gw.BN = 144; gw.kper = b; gw.splits = 1;
+  gw.epi = TC_EPI_ACCUM; gw.C[0] = ctx->grad + F.w_off; gw.ldc = F.D;
+  TcGemmArgs gx{};
+  gx.A[0] = ctx->theta_local_bf16 + F.w_off; gx.lda = F.D; gx.a_mn = 1;
+  gx.B[0] = ctx->dh_bf16; gx.ldb = F.H; gx.b_mn = 0;
+  gx.M = F.D; gx.N = b; gx.K = F.H; gx.BN = b; gx.kper = F.H; gx.splits = 1;
+  gx.epi = TC_EPI_MASK_T; gx.out_bf16 = ctx->dz2_bf16; gx.mask = ctx->a2_bf16; gx.ldo = F.D;
+  PB("fc1_bwd", 2);
+  launch_tc_gemm(gw, 1, st);
+  launch_tc_gemm(gx, 1, st);
+  PE();
+  // a8/a9 conv backward
+  BwdConvArgs ba{};
+  ba.ring_s = ctx->ring_s; ba.idx = ctx->idx; ba.a1_save = ctx->a1_save; ba.dz2 = ctx->dz2_bf16;
+  ba.theta = ctx->theta_local_bf16;
+  ba.w1_off = L1.w_off; ba.b1_off = L1.b_off; ba.w2_off = L2.w_off; ba.b2_off = L2.b_off;
+  ba.n = b; ba.partial = ctx->bwd_partial; ba.counter = ctx->tc_counters + 32; ba.grad = ctx->grad;
+  PB("conv_bwd", 1);
+  launch_bwd_conv_bf16(ba, st);
+  PE();
+  if (ctx->keep_grad)
+    CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+  // a11 push + a12 shard update
+  if (push) {
+    const float div = (float)((double)ctx->world * c.n_push);
+    const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
+    if (ctx->world > 1) {
+      PB("push_reduce_scatter", 0);
+      NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
+      CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
+      PE();
+      PB("rmsprop_update", 1);
+      launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
+                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, st);
+      PE();
+    } else {
+      PB("rmsprop_update", 1);
+      launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
+                     (float)c.rms_eps, nullptr, ctx->alias_local ? ctx->theta_local_bf16 : nullptr, ctx->ctr, 1, st);
+      PE();
+    }
+  }
+  CK(cudaGetLastError());
+  return DQN_OK;
+}
+
+static int enqueue_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
+  return ctx->bf16 ? enqueue_step_bf16(ctx, fetch, refresh, push) : enqueue_step_f32(ctx, fetch, refresh, push);
+}
+
 // Replay the graph of one step variant (captured on first use). profile: the
 // variant with event records around each region. *kernels += kernel nodes run.
 static int run_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push, bool profile, long long* kernels) {
-  if (!ctx->use_graphs && !profile) return enqueue_step_f32(ctx, fetch, refresh, push);
+  if (!ctx->use_graphs && !profile) return enqueue_step(ctx, fetch, refresh, push);
   const int v = (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0) | (profile ? 8 : 0);
   if (!ctx->graphs[v]) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     ctx->capture_variant = v;
-    int rc = enqueue_step_f32(ctx, fetch, refresh, push);
+    int rc = enqueue_step(ctx, fetch, refresh, push);
     ctx->capture_variant = -1;
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
     if (rc) return rc;
@@ -765,16 +958,16 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
                            cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
-  if (hc.T != (unsigned long long)ctx->T || hc.n != ctx->n)
+  if (hc.T != (unsigned long long)ctx->T)
     return set_err(ctx, DQN_ECUDA, "device step counters diverged from the host schedule");
-  if (hc.nonfinite_rounds > 0) ctx->diverged = true;
+  if (hc.nonfinite > 0) ctx->diverged = true;
   if (stats) {
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     stats->device_ms = ms;
     stats->generation = ctx->n;
     stats->steps_done = ctx->T;
-    stats->nonfinite_rounds = hc.nonfinite_rounds;
+    stats->nonfinite_elems = hc.nonfinite;
     stats->kernel_launches = kernels;
     double lm = 0.0;
     for (float l : loss) lm += l;
@@ -799,6 +992,28 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
     const int m = (int)std::min<long long>(b, n - i0);
     CK(cudaMemcpyAsync(ctx->q_stage, states + i0 * sb, m * sb, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        st));
+    const float* in = nullptr;
+    if (ctx->bf16) {  // conv1's s2d staging, then the tensor-core forward with theta_local
+      const FcShape& F = net.fc[0];
+      launch_push_s2d(ctx->q_stage_s2d, nullptr, nullptr, nullptr, nullptr, b, 0, 0, m, ctx->q_stage, nullptr,
+                      nullptr, nullptr, nullptr, st);
+      FwdConvArgs fa{};
+      fa.ring[0] = ctx->q_stage_s2d;
+      fa.theta[0] = ctx->theta_local_bf16;
+      fa.theta_f32[0] = ctx->theta_local;
+      fa.w1_off = net.conv[0].w_off; fa.b1_off = net.conv[0].b_off;
+      fa.w2_off = net.conv[1].w_off; fa.b2_off = net.conv[1].b_off;
+      fa.n = m; fa.a2 = ctx->a2_bf16;
+      launch_fwd_conv_bf16(fa, 1, st);
+      TcGemmArgs gf{};
+      gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.lda = F.D;
+      gf.B[0] = ctx->a2_bf16; gf.ldb = F.D;
+      gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = (m + 15) / 16 * 16; gf.kper = F.D / ctx->fc_splits;
+      gf.splits = ctx->fc_splits; gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
+      gf.counters = ctx->tc_counters; gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
+      launch_tc_gemm(gf, 1, st);
+      in = ctx->act_fc[0][0];
+    } else {
     ImgSrc src{};
     src.u8[0] = ctx->q_stage;
     src.stride = sb;
@@ -812,8 +1027,9 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
       }
       launch_conv_fwd_f32(net.conv[i], s2, ctx->theta_local, nullptr, ctx->act_conv[i][0], nullptr, m, 1, st);
     }
-    const float* in = ctx->act_conv[net.n_conv - 1][0];
-    for (int l = 0; l < net.n_fc; ++l) {
+    in = ctx->act_conv[net.n_conv - 1][0];
+    }
+    for (int l = 0; l < net.n_fc && !ctx->bf16; ++l) {
       const FcShape& F = net.fc[l];
       GemmArgs g{};
       g.A[0] = in; g.sam = F.D; g.sak = 1;

@@ -1,0 +1,795 @@
+// kernels_bf16.cu — the tensor-core replica step (precision DQN_BF16) for the
+// Mnih-2013 network of BASELINE.json configs[0..3] (conv16 8x8/4, conv32 4x4/2,
+// fc256, |A| outputs). bf16 operands, fp32 accumulation in TMEM (tcgen05).
+//
+// Both strided convolutions are rewritten by space-to-depth (s2d) as 2x2
+// stride-1 convolutions (conv1: 84x84x4 -> 21x21x64, conv2: 20x20x16 ->
+// 10x10x64), so every filter tap is a ROW SHIFT of one shared-memory image:
+// with the image stored as UMMA no-swizzle K-major chunk planes
+// [channel/8][pixel][8 x bf16], the A operand of tap (dy,dx) is the same planes
+// started dy*W+dx pixels later ("virtual rows" m' = oy*W + ox; the column
+// ox = W-1 is computed and discarded). The replay ring holds conv1's s2d layout
+// directly (pushed once, gathered every step) and conv1's epilogue writes its
+// activation straight into conv2's s2d layout, so the whole forward of one
+// state (sample -> gather -> conv1 -> conv2) is one CTA with no HBM round trip.
+//
+// Formulas: P:61-67 (network), P:121 (target network on s'), P:123 (gradient).
+#include <algorithm>
+#include <cstdio>
+#include "dqn_internal.h"
+#include "philox.cuh"
+#include "sm100.cuh"
+
+namespace dqn {
+using namespace dqn_sm100;
+
+namespace mnih {
+// conv1: 4x84x84 -> s2d(4) 21x21x64 -> 2x2/1 -> 20x20x16
+constexpr int X_W = 21, X_PIX = 441, X_ALLOC = 544, C1 = 16, M1V = 420, M1_TILES = 4;
+// conv2: 16x20x20 -> s2d(2) 10x10x64 -> 2x2/1 -> 9x9x32
+constexpr int A1_W = 10, A1_PIX = 100, A1_ALLOC = 144, C2 = 32, M2V = 90;
+constexpr int K = 256;      // 4 taps x 64 channels for both convolutions
+constexpr int D = 2592;     // 32 x 9 x 9 flattened (C,H,W)
+constexpr int SLOT = 28224; // bytes of one u8 s2d state
+__device__ __forceinline__ int tap_shift1(int t) { return (t >> 1) * X_W + (t & 1); }
+__device__ __forceinline__ int tap_shift2(int t) { return (t >> 1) * A1_W + (t & 1); }
+}  // namespace mnih
+
+static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ------------------------------------------------------------------ push: canonical -> s2d ring slots
+// out[p*64 + c'] with p = py*21 + px, c' = f*16 + iy*4 + ix  <-  in[f][4py+iy][4px+ix]
+// One thread writes one 16-byte vector (pixel p, frame f): four 4-byte rows of the 4x4 block.
+__global__ void push_s2d_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
+                                long long cap, long long count0, long long first, const uint8_t* s,
+                                const int32_t* a, const float* r, const uint8_t* sn, const uint8_t* t) {
+  const long long i = blockIdx.y;
+  const long long slot = (count0 + first + i) % cap;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;  // (pixel, frame)
+  if (v < mnih::X_PIX * 4) {
+    const int p = v >> 2, f = v & 3;
+    const int py = p / 21, px = p % 21;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      if (which == 1 && ring_sn == nullptr) break;  // states only (dqn_q_values staging)
+      const uint8_t* src = (which ? sn : s) + i * mnih::SLOT + f * 7056 + (4 * py) * 84 + 4 * px;
+      uint4 o;
+      o.x = *reinterpret_cast<const uint32_t*>(src);
+      o.y = *reinterpret_cast<const uint32_t*>(src + 84);
+      o.z = *reinterpret_cast<const uint32_t*>(src + 168);
+      o.w = *reinterpret_cast<const uint32_t*>(src + 252);
+      uint8_t* dst = (which ? ring_sn : ring_s) + slot * mnih::SLOT + p * 64 + f * 16;
+      *reinterpret_cast<uint4*>(dst) = o;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ring_a != nullptr) {
+    ring_a[slot] = a[i];
+    ring_r[slot] = r[i];
+    ring_t[slot] = t[i] ? 1 : 0;
+  }
+}
+
+void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t, long long cap,
+                     long long count0, long long first, long long n, const uint8_t* s, const int32_t* a,
+                     const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st) {
+  if (n <= 0) return;
+  dim3 grid(cdiv(mnih::X_PIX * 4, 256), (unsigned)n);
+  push_s2d_kernel<<<grid, 256, 0, st>>>(ring_s, ring_sn, ring_a, ring_r, ring_t, cap, count0, first, s, a, r, sn, t);
+}
+
+// ------------------------------------------------------------------ shared helpers
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// 16 u8 -> 16 exact bf16 (integers < 256 are exact in bf16), as two 16-byte chunks
+__device__ __forceinline__ void u8x16_to_bf16(const uint4 q, uint4& lo, uint4& hi) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  uint32_t o[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float b0 = (float)(w[i] & 0xFF), b1 = (float)((w[i] >> 8) & 0xFF);
+    const float b2 = (float)((w[i] >> 16) & 0xFF), b3 = (float)(w[i] >> 24);
+    o[2 * i] = pack_bf16(b0, b1);
+    o[2 * i + 1] = pack_bf16(b2, b3);
+  }
+  lo = make_uint4(o[0], o[1], o[2], o[3]);
+  hi = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// Expand one u8 s2d state (already in shared memory, 28224 B) into bf16 chunk planes
+// [8][X_ALLOC][16 B] (pixels >= 441 left untouched).
+__device__ __forceinline__ void expand_state(uint8_t* sX, const uint8_t* sU8) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(sU8);
+  for (int v = threadIdx.x; v < mnih::X_PIX * 4; v += blockDim.x) {
+    const int p = v >> 2, q = v & 3;
+    uint4 lo, hi;
+    u8x16_to_bf16(s4[v], lo, hi);
+    *reinterpret_cast<uint4*>(sX + ((2 * q) * mnih::X_ALLOC + p) * 16) = lo;
+    *reinterpret_cast<uint4*>(sX + ((2 * q + 1) * mnih::X_ALLOC + p) * 16) = hi;
+  }
+}
+
+// conv1 B operand [kchunk 32][n 16][8]: k = t*64 + c', t = dy*2+dx, c' = f*16+iy*4+ix -> W1[n][f][4dy+iy][4dx+ix]
+// (fixed trip counts for 128 threads, fully unrolled: every thread's gathers are in flight together)
+__device__ __forceinline__ void stage_w1(uint8_t* sW, const __nv_bfloat16* __restrict__ w) {
+#pragma unroll
+  for (int it = 0; it < 32 * mnih::C1 / 128; ++it) {
+    const int e = threadIdx.x + it * 128;
+    const int kc = e / mnih::C1, n = e % mnih::C1;
+    uint32_t o[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      uint16_t pr[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = kc * 8 + 2 * h + u;
+        const int t = k >> 6, c = k & 63;
+        const int f = c >> 4, iy = (c >> 2) & 3, ix = c & 3;
+        const int ky = 4 * (t >> 1) + iy, kx = 4 * (t & 1) + ix;
+        pr[u] = __bfloat16_as_ushort(w[((n * 4 + f) * 8 + ky) * 8 + kx]);
+      }
+      o[h] = pr[0] | ((uint32_t)pr[1] << 16);
+    }
+    *reinterpret_cast<uint4*>(sW + (kc * mnih::C1 + n) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+// conv2 B operand [kchunk 32][n 32][8]: k = t*64 + c'', c'' = (iy*2+ix)*16 + c -> W2[n][c][2dy+iy][2dx+ix]
+__device__ __forceinline__ void stage_w2(uint8_t* sW, const __nv_bfloat16* __restrict__ w) {
+#pragma unroll
+  for (int it = 0; it < 32 * mnih::C2 / 128; ++it) {
+    const int e = threadIdx.x + it * 128;
+    const int kc = e / mnih::C2, n = e % mnih::C2;
+    uint32_t o[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      uint16_t pr[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = kc * 8 + 2 * h + u;
+        const int t = k >> 6, c2 = k & 63;
+        const int q = c2 >> 4, c = c2 & 15;
+        const int ky = 2 * (t >> 1) + (q >> 1), kx = 2 * (t & 1) + (q & 1);
+        pr[u] = __bfloat16_as_ushort(w[((n * 16 + c) * 4 + ky) * 4 + kx]);
+      }
+      o[h] = pr[0] | ((uint32_t)pr[1] << 16);
+    }
+    *reinterpret_cast<uint4*>(sW + (kc * mnih::C2 + n) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// ------------------------------------------------------------------ a1-a4: sample + gather + conv1 + conv2
+// grid (n_images, groups): group 0 = s_j with theta (local), group 1 = s'_j with theta^.
+// Writes a2[g*n + j][2592] (bf16, canonical (C,H,W) flatten, post-ReLU) and, for group 0,
+// a1_save[j] (conv1 activation as conv2's s2d chunk planes, the backward's operand).
+constexpr int FWD_SX = 0;
+constexpr int FWD_SA1 = FWD_SX + 8 * mnih::X_ALLOC * 16;       // 69632
+constexpr int FWD_SW1 = FWD_SA1 + 8 * mnih::A1_ALLOC * 16;     // +18432
+constexpr int FWD_SW2 = FWD_SW1 + 32 * mnih::C1 * 16;          // +8192
+constexpr int FWD_SU8 = FWD_SW2 + 32 * mnih::C2 * 16;          // +16384
+constexpr int FWD_SMEM = FWD_SU8 + mnih::SLOT;                  // +28224 = 140864
+
+__global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, bar_ld;
+  __shared__ uint32_t tbase;
+  const int j = blockIdx.x, g = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sX = smem + FWD_SX;
+  uint8_t* sA1 = smem + FWD_SA1;
+  uint8_t* sW1 = smem + FWD_SW1;
+  uint8_t* sW2 = smem + FWD_SW2;
+  uint8_t* sU8 = smem + FWD_SU8;
+  if (threadIdx.x == 0) {
+    long long slot = j;
+    if (a.ctr) slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)j, a.ctr->ring_size);  // a1
+    if (g == 0 && a.idx) a.idx[j] = (int)slot;
+    mbar_init(&bar, 1);
+    mbar_init(&bar_ld, 1);
+    fence_mbar_init();
+    // a2 gather: the whole u8 state in one TMA bulk copy (28,224 contiguous bytes of the ring slot)
+    mbar_arrive_expect_tx(&bar_ld, mnih::SLOT);
+    bulk_g2s(sU8, a.ring[g] + slot * mnih::SLOT, mnih::SLOT, &bar_ld);
+  }
+  if (warp == 0) tmem_alloc(&tbase, 128);
+  __syncthreads();  // barriers initialised before anyone waits on them
+  const __nv_bfloat16* th = a.theta[g];
+  stage_w1(sW1, th + a.w1_off);
+  stage_w2(sW2, th + a.w2_off);
+  mbar_wait(&bar_ld, 0);
+  expand_state(sX, sU8);  // u8 -> exact bf16 (1/255 folded into the epilogue)
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  // ---- conv1: 4 M-tiles x 4 taps x 4 K-steps, M = 128, N = 16
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, mnih::C1, 0, 0);
+    const uint32_t xb = smem_u32(sX), wb = smem_u32(sW1);
+    for (int mt = 0; mt < mnih::M1_TILES; ++mt)
+      for (int t = 0; t < 4; ++t)
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ad = make_desc(xb + (2 * kk) * mnih::X_ALLOC * 16 + (mt * 128 + mnih::tap_shift1(t)) * 16,
+                                        mnih::X_ALLOC * 16, 128);
+          const uint64_t bd = make_desc(wb + (t * 8 + 2 * kk) * mnih::C1 * 16, mnih::C1 * 16, 128);
+          mma_bf16(tmem + mt * mnih::C1, ad, bd, idesc, (t | kk) != 0);
+        }
+    mma_commit(&bar);
+  }
+  __syncwarp();
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  // ---- conv1 epilogue: x (1/255) + b1, ReLU, bf16, into conv2's s2d planes
+  {
+    const float* b1 = a.theta_f32[g] + a.b1_off;
+    float bias[mnih::C1];
+#pragma unroll
+    for (int n = 0; n < mnih::C1; ++n) bias[n] = __ldg(b1 + n);
+    for (int mt = 0; mt < mnih::M1_TILES; ++mt) {
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + mt * mnih::C1, v);
+      const int m = mt * 128 + 32 * warp + lane;
+      const int oy = m / mnih::X_W, ox = m % mnih::X_W;
+      if (m < mnih::M1V && ox < 20) {
+        uint32_t o[8];
+#pragma unroll
+        for (int n = 0; n < 16; n += 2) {
+          const float z0 = fmaxf(fmaf(v[n], 1.0f / 255.0f, bias[n]), 0.0f);
+          const float z1 = fmaxf(fmaf(v[n + 1], 1.0f / 255.0f, bias[n + 1]), 0.0f);
+          o[n >> 1] = pack_bf16(z0, z1);
+        }
+        const int p2 = (oy >> 1) * mnih::A1_W + (ox >> 1);
+        const int j0 = (((oy & 1) << 1) | (ox & 1)) * 2;
+        *reinterpret_cast<uint4*>(sA1 + (j0 * mnih::A1_ALLOC + p2) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(sA1 + ((j0 + 1) * mnih::A1_ALLOC + p2) * 16) = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    }
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // ---- conv2: 1 M-tile x 4 taps x 4 K-steps, M = 128, N = 32
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, mnih::C2, 0, 0);
+    const uint32_t ab = smem_u32(sA1), wb = smem_u32(sW2);
+    for (int t = 0; t < 4; ++t)
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t ad = make_desc(ab + (2 * kk) * mnih::A1_ALLOC * 16 + mnih::tap_shift2(t) * 16,
+                                      mnih::A1_ALLOC * 16, 128);
+        const uint64_t bd = make_desc(wb + (t * 8 + 2 * kk) * mnih::C2 * 16, mnih::C2 * 16, 128);
+        mma_bf16(tmem + 64, ad, bd, idesc, (t | kk) != 0);
+      }
+    mma_commit(&bar);
+  }
+  // save conv1's activation (group 0) for the backward while conv2 runs
+  if (g == 0 && a.a1_save) {
+    const uint4* src = reinterpret_cast<const uint4*>(sA1);
+    uint4* dst = reinterpret_cast<uint4*>(a.a1_save + (long long)j * 8 * mnih::A1_ALLOC * 16);
+    for (int v = threadIdx.x; v < 8 * mnih::A1_ALLOC; v += blockDim.x) dst[v] = src[v];
+  }
+  __syncwarp();
+  mbar_wait(&bar, 1);
+  tc_fence_after();
+  // ---- conv2 epilogue: + b2, ReLU, bf16, canonical flatten d = c*81 + oy*9 + ox
+  {
+    const float* b2 = a.theta_f32[g] + a.b2_off;
+    const int m = 32 * warp + lane;
+    const int oy = m / mnih::A1_W, ox = m % mnih::A1_W;
+    const bool ok = m < mnih::M2V && ox < 9;
+    __nv_bfloat16* out = a.a2 + ((long long)g * a.n + j) * mnih::D + oy * 9 + ox;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 64 + 16 * h, v);
+      if (ok) {
+#pragma unroll
+        for (int n = 0; n < 16; ++n) {
+          const int c = 16 * h + n;
+          out[c * 81] = __float2bfloat16_rn(fmaxf(v[n] + __ldg(b2 + c), 0.0f));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 128);
+}
+
+void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st) {
+  dim3 grid(a.n, groups);
+  fwd_conv_bf16_kernel<<<grid, 128, FWD_SMEM, st>>>(a);
+}
+
+// ------------------------------------------------------------------ generic small tcgen05 GEMM
+// D[m][n] = sum_k A(m,k) B(n,k), bf16 operands from global, fp32 accumulate in TMEM.
+// One CTA = one (group, m-tile of 128, n-tile of BN, k-split); the CTA stages its
+// whole K slice at once (these GEMMs are latency-bound: M, N <= 2592, K <= 2592).
+
+__global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (a.N + a.BN - 1) / a.BN;
+  const int m_tiles = (a.M + 127) / 128;
+  const int mt = blockIdx.x % m_tiles, nt = blockIdx.x / m_tiles;
+  const int split = blockIdx.y, g = blockIdx.z;
+  const int m0 = mt * 128, n0 = nt * a.BN;
+  const int k0 = split * a.kper;
+  const int KC = min(a.kper, a.K - k0);  // multiple of 16 by construction
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + 128 * a.kper * 2;
+  (void)n_tiles;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  // ---- stage A (128 rows x KC) and B (BN rows x KC), 16-byte vectors
+  const __nv_bfloat16* Ag = a.A[g];
+  const __nv_bfloat16* Bg = a.B[g];
+  const int kch = KC / 8;
+  // all 16-byte pieces go out as cp.async (LDGSTS) so a thread keeps dozens of loads in flight
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  if (!a.a_mn) {  // K-major: smem [kc][row][8]
+    for (int e = threadIdx.x; e < 128 * kch; e += blockDim.x) {
+      const int r = e / kch, c = e % kch;
+      const int m = m0 + r;
+      uint8_t* d = sA + (c * 128 + r) * 16;
+      if (m < a.M) cp_async16(d, Ag + (long long)m * a.lda + k0 + 8 * c);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  } else {        // MN-major: smem [row/8][k][8]
+    for (int e = threadIdx.x; e < 16 * KC; e += blockDim.x) {
+      const int gi = e % 16, k = e / 16;
+      const int m = m0 + 8 * gi;
+      uint8_t* d = sA + (gi * KC + k) * 16;
+      if (m < a.M) cp_async16(d, Ag + (long long)(k0 + k) * a.lda + m);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  }
+  const int bn = a.BN;
+  if (!a.b_mn) {
+    for (int e = threadIdx.x; e < bn * kch; e += blockDim.x) {
+      const int r = e / kch, c = e % kch;
+      const int n = n0 + r;
+      uint8_t* d = sB + (c * bn + r) * 16;
+      if (n < a.N) cp_async16(d, Bg + (long long)n * a.ldb + k0 + 8 * c);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  } else {
+    const int ng = bn / 8;
+    for (int e = threadIdx.x; e < ng * KC; e += blockDim.x) {
+      const int gi = e % ng, k = e / ng;
+      const int n = n0 + 8 * gi;
+      uint8_t* d = sB + (gi * KC + k) * 16;
+      if (n < a.N) cp_async16(d, Bg + (long long)(k0 + k) * a.ldb + n);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  }
+  cp_async_wait_all();
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, bn, a.a_mn, a.b_mn);
+    const uint32_t ab = smem_u32(sA), bb = smem_u32(sB);
+    for (int kk = 0; kk < KC / 16; ++kk) {
+      const uint64_t ad = a.a_mn ? make_desc(ab + kk * 256, 128, KC * 16) : make_desc(ab + kk * 2 * 128 * 16, 128 * 16, 128);
+      const uint64_t bd = a.b_mn ? make_desc(bb + kk * 256, 128, KC * 16) : make_desc(bb + kk * 2 * bn * 16, bn * 16, 128);
+      mma_bf16(tmem, ad, bd, idesc, kk > 0);
+    }
+    mma_commit(&bar);
+  }
+  __syncwarp();
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  const int m = m0 + 32 * warp + lane;
+  const uint32_t trow = tmem + ((uint32_t)(32 * warp) << 16);
+  if (a.epi == TC_EPI_ACCUM) {
+    // TMEM -> shared tile [128][bn+4] (the MMAs are complete, so the operand staging area is free),
+    // then a coalesced read-modify-write of C by the whole CTA with many 16-byte accesses in flight
+    float* sD = reinterpret_cast<float*>(smem);
+    const int ld = bn + 4;
+    for (int c = 0; c < bn; c += 16) {
+      float v[16];
+      tmem_ld16(trow + c, v);
+      float* row = sD + (32 * warp + lane) * ld + c;
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(row + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    }
+    __syncthreads();
+    const int nv = bn / 4;
+    const bool vec = (a.ldc % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.C[g]) & 15) == 0);
+    constexpr int BATCH = 12;  // loads of a batch are all issued before any store (C may alias nothing else,
+                               // but the compiler cannot know that)
+    for (int e0 = threadIdx.x; e0 < 128 * nv; e0 += 128 * BATCH) {
+      float4 o[BATCH];
+      float* dst[BATCH];
+      bool ok[BATCH];
+#pragma unroll
+      for (int k = 0; k < BATCH; ++k) {
+        const int e = e0 + k * 128;
+        const int r = e / nv, q = e % nv;
+        const int mm = m0 + r, n = n0 + 4 * q;
+        ok[k] = e < 128 * nv && mm < a.M && vec && n + 4 <= a.N;
+        dst[k] = a.C[g] + (long long)mm * a.ldc + n;
+        o[k] = ok[k] ? *reinterpret_cast<const float4*>(dst[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < BATCH; ++k) {
+        const int e = e0 + k * 128;
+        if (e >= 128 * nv) break;
+        const int r = e / nv, q = e % nv;
+        const int mm = m0 + r, n = n0 + 4 * q;
+        const float4 d = *reinterpret_cast<const float4*>(sD + r * ld + 4 * q);
+        if (ok[k]) {
+          o[k].x += d.x; o[k].y += d.y; o[k].z += d.z; o[k].w += d.w;
+          *reinterpret_cast<float4*>(dst[k]) = o[k];
+        } else if (mm < a.M) {
+          const float dv[4] = {d.x, d.y, d.z, d.w};
+          for (int i = 0; i < 4 && n + i < a.N; ++i) dst[k][i] += dv[i];
+        }
+      }
+    }
+  } else if (a.epi == TC_EPI_MASK_T) {
+    for (int c = 0; c < bn; c += 16) {
+      float v[16];
+      tmem_ld16(trow + c, v);
+      if (m < a.M) {
+        unsigned short mk[16];  // all 16 mask loads in flight before the stores
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int n = n0 + c + i;
+          mk[i] = n < a.N ? __ldg(reinterpret_cast<const unsigned short*>(a.mask) + (long long)n * a.ldo + m) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int n = n0 + c + i;
+          if (n < a.N)  // bf16 > 0 <=> sign bit clear and not +0
+            a.out_bf16[(long long)n * a.ldo + m] = __float2bfloat16_rn((mk[i] & 0x8000u) == 0 && mk[i] != 0 ? v[i] : 0.0f);
+        }
+      }
+    }
+  } else {  // TC_EPI_FC_FWD: split partials, transposed to [g][split][n][m] (coalesced over m)
+    float* pbase = a.partial + ((long long)g * a.splits + split) * (long long)a.BN * a.M;
+    for (int c = 0; c < bn; c += 16) {
+      float v[16];
+      tmem_ld16(trow + c, v);
+      if (m < a.M) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pbase[(long long)(n0 + c + i) * a.M + m] = v[i];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+// h[g][n][m] = relu(sum_split partial[g][split][n][m] + bias[g][m]), splits summed in order
+__global__ void fc_reduce_kernel(TcGemmArgs a) {
+  const int g = blockIdx.y;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)a.M * a.N) return;
+  const int n = (int)(e / a.M), m = (int)(e % a.M);
+  const float* p = a.partial + (long long)g * a.splits * a.BN * a.M + (long long)n * a.M + m;
+  float s = 0.0f;
+#pragma unroll 6
+  for (int sp = 0; sp < a.splits; ++sp) s += p[(long long)sp * a.BN * a.M];
+  a.h_out[g][(long long)n * a.M + m] = fmaxf(s + a.bias[g][m], 0.0f);
+}
+
+void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st) {
+  const int m_tiles = cdiv(a.M, 128), n_tiles = cdiv(a.N, a.BN);
+  size_t smem = (size_t)(128 + a.BN) * a.kper * 2;
+  if (a.epi == TC_EPI_ACCUM) smem = std::max(smem, (size_t)128 * (a.BN + 4) * 4);  // epilogue tile
+  dim3 grid(m_tiles * n_tiles, a.splits, groups);
+  tc_gemm_kernel<<<grid, 128, smem, st>>>(a);
+  if (a.epi == TC_EPI_FC_FWD && a.h_out[0] != nullptr) {  // else the TD head reduces the partials itself
+    dim3 rg(cdiv((long long)a.M * a.N, 256), groups);
+    fc_reduce_kernel<<<rg, 256, 0, st>>>(a);
+  }
+}
+
+// ------------------------------------------------------------------ a8/a9: fused conv backward
+// One CTA per image j of the minibatch (group 0: s_j, theta). Per image:
+//   conv2 dW  D2[(t,c'')][n2] += sum_{m'} A1(m'+shift_t)[c''] dZ2[m'][n2]      (2 M-tiles, MN-major A and B)
+//   conv2 dX  dA1[p][c''] = sum_t sum_n2 dZ2(p - shift_t)[n2] W2[n2][c''][t]     (K-major, zero-padded rows)
+//   dZ1 = dA1 * [A1 > 0]  (ReLU'(0) = 0), re-laid out for conv1's virtual rows
+//   conv1 dW  D1[(t,c')][n] += sum_{m'} X(m'+shift_t)[c'] dZ1[m'][n]            (2 M-tiles, MN-major A and B)
+//   db2 += sum dZ2, db1 += sum dZ1 (SIMT)
+// An M = 128 tile spans two taps whose shifts differ by one pixel, so the image
+// planes are stored twice (second copy one pixel ahead) and SBO walks 16 planes.
+// Per-image partials are reduced in image order by the last CTA (deterministic).
+constexpr int BWD_PART_W1 = 256 * 16;            // (t,c') x n
+constexpr int BWD_PART_W2 = 256 * 32;            // (t,c'') x n2
+constexpr int BWD_PART = kBwdPart;
+constexpr int BWD_ROWS1 = 432;                   // conv1 virtual rows 420 padded to K-steps of 16
+constexpr int BWD_ROWS2 = 96;                    // conv2 virtual rows 90 padded
+constexpr int DZ2_OFF = 11;                      // zero rows ahead of dZ2 (largest tap shift)
+constexpr int DZ2_ALLOC = 144;
+constexpr int BWD_SX = 0;                                                  // 16 planes x X_ALLOC x 16
+constexpr int BWD_SA1 = BWD_SX + 16 * mnih::X_ALLOC * 16;                  // 139264
+constexpr int BWD_SDZ2 = BWD_SA1 + 16 * mnih::A1_ALLOC * 16;               // +36864
+constexpr int BWD_SDZ1 = BWD_SDZ2 + 4 * DZ2_ALLOC * 16;                    // +9216
+constexpr int BWD_SW2 = BWD_SDZ1 + 2 * BWD_ROWS1 * 16;                     // +13824
+constexpr int BWD_SMEM = BWD_SW2 + 4 * 4 * 64 * 16;                        // +16384 = 215552
+
+__global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  __shared__ float s_db1[16], s_db2[32];
+  const int j = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sX = smem + BWD_SX;
+  uint8_t* sA1 = smem + BWD_SA1;
+  uint8_t* sDZ2 = smem + BWD_SDZ2;
+  uint8_t* sDZ1 = smem + BWD_SDZ1;
+  uint8_t* sW2 = smem + BWD_SW2;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  // ---- zero the pads the MMAs read (garbage rows are multiplied by zero dZ rows, so must be finite)
+  {
+    uint4 z = make_uint4(0, 0, 0, 0);
+    for (int e = threadIdx.x; e < 16 * (mnih::X_ALLOC - mnih::X_PIX + 1); e += blockDim.x) {
+      const int pl = e / (mnih::X_ALLOC - mnih::X_PIX + 1), p = mnih::X_PIX - 1 + e % (mnih::X_ALLOC - mnih::X_PIX + 1);
+      *reinterpret_cast<uint4*>(sX + (pl * mnih::X_ALLOC + p) * 16) = z;
+    }
+    for (int e = threadIdx.x; e < 16 * (mnih::A1_ALLOC - mnih::A1_PIX + 1); e += blockDim.x) {
+      const int pl = e / (mnih::A1_ALLOC - mnih::A1_PIX + 1), p = mnih::A1_PIX - 1 + e % (mnih::A1_ALLOC - mnih::A1_PIX + 1);
+      *reinterpret_cast<uint4*>(sA1 + (pl * mnih::A1_ALLOC + p) * 16) = z;
+    }
+    for (int e = threadIdx.x; e < 4 * DZ2_ALLOC; e += blockDim.x) reinterpret_cast<uint4*>(sDZ2)[e] = z;
+    for (int e = threadIdx.x; e < 2 * BWD_ROWS1; e += blockDim.x) reinterpret_cast<uint4*>(sDZ1)[e] = z;
+  }
+  // ---- W2 as the B operand of conv2 dX, per tap: [t][n2/8][c'' 64][8]  (B(c'', n2) = W2[n2][c][ky][kx])
+#pragma unroll
+  for (int it = 0; it < 4 * 4 * 64 / 128; ++it) {  // 128 threads, all gathers in flight
+    const int e = threadIdx.x + it * 128;
+    const int c2 = e % 64, kc = (e / 64) % 4, t = e / 256;
+    const int q = c2 >> 4, c = c2 & 15;
+    const int ky = 2 * (t >> 1) + (q >> 1), kx = 2 * (t & 1) + (q & 1);
+    uint32_t o[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int n0 = kc * 8 + 2 * h;
+      const uint16_t lo = __bfloat16_as_ushort(a.theta[a.w2_off + ((n0 * 16 + c) * 4 + ky) * 4 + kx]);
+      const uint16_t hi = __bfloat16_as_ushort(a.theta[a.w2_off + (((n0 + 1) * 16 + c) * 4 + ky) * 4 + kx]);
+      o[h] = lo | ((uint32_t)hi << 16);
+    }
+    *reinterpret_cast<uint4*>(sW2 + ((t * 4 + kc) * 64 + c2) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+  // ---- X (s_j) into planes 0..7 and the one-pixel-ahead copy into planes 8..15
+  {
+    // every thread issues all of its loads before the first conversion (latency, not bandwidth, bound)
+    constexpr int XIT = (mnih::X_PIX * 4 + 127) / 128, AIT = (8 * mnih::A1_PIX + 127) / 128;
+    const uint4* s4 = reinterpret_cast<const uint4*>(a.ring_s + (long long)a.idx[j] * mnih::SLOT);
+    const uint4* a4 = reinterpret_cast<const uint4*>(a.a1_save + (long long)j * 8 * mnih::A1_ALLOC * 16);
+    uint4 xb[XIT], ab[AIT];
+#pragma unroll
+    for (int it = 0; it < XIT; ++it) {
+      const int v = threadIdx.x + it * 128;
+      xb[it] = v < mnih::X_PIX * 4 ? __ldg(s4 + v) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int it = 0; it < AIT; ++it) {
+      const int v = threadIdx.x + it * 128;
+      ab[it] = v < 8 * mnih::A1_PIX ? __ldg(a4 + (v / mnih::A1_PIX) * mnih::A1_ALLOC + v % mnih::A1_PIX)
+                                   : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int it = 0; it < XIT; ++it) {
+      const int v = threadIdx.x + it * 128;
+      if (v >= mnih::X_PIX * 4) break;
+      const int p = v >> 2, q = v & 3;
+      uint4 lo, hi;
+      u8x16_to_bf16(xb[it], lo, hi);
+      *reinterpret_cast<uint4*>(sX + ((2 * q) * mnih::X_ALLOC + p) * 16) = lo;
+      *reinterpret_cast<uint4*>(sX + ((2 * q + 1) * mnih::X_ALLOC + p) * 16) = hi;
+      if (p > 0) {
+        *reinterpret_cast<uint4*>(sX + ((8 + 2 * q) * mnih::X_ALLOC + p - 1) * 16) = lo;
+        *reinterpret_cast<uint4*>(sX + ((9 + 2 * q) * mnih::X_ALLOC + p - 1) * 16) = hi;
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < AIT; ++it) {
+      const int v = threadIdx.x + it * 128;
+      if (v >= 8 * mnih::A1_PIX) break;
+      const int pl = v / mnih::A1_PIX, p = v % mnih::A1_PIX;
+      *reinterpret_cast<uint4*>(sA1 + (pl * mnih::A1_ALLOC + p) * 16) = ab[it];
+      if (p > 0) *reinterpret_cast<uint4*>(sA1 + ((8 + pl) * mnih::A1_ALLOC + p - 1) * 16) = ab[it];
+    }
+  }
+  __syncthreads();  // zero-filled dZ2 planes before the scatter below
+  // ---- dZ2 (canonical [n2][81]) into planes [n2/8][DZ2_OFF + m'][8], m' = oy*10 + ox; + db2
+  {
+    const unsigned short* d = reinterpret_cast<const unsigned short*>(a.dz2 + (long long)j * mnih::D);
+#pragma unroll
+    for (int it = 0; it < (4 * 81 + 127) / 128; ++it) {
+      const int e = threadIdx.x + it * 128;
+      if (e < 4 * 81) {
+        const int kc = e / 81, p = e % 81;
+        const int oy = p / 9, ox = p % 9;
+        uint32_t o[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          o[h] = __ldg(d + (kc * 8 + 2 * h) * 81 + p) | ((uint32_t)__ldg(d + (kc * 8 + 2 * h + 1) * 81 + p) << 16);
+        *reinterpret_cast<uint4*>(sDZ2 + (kc * DZ2_ALLOC + DZ2_OFF + oy * 10 + ox) * 16) =
+            make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (warp == 1) {  // db2 = sum of dZ2 over positions (zero rows contribute nothing)
+    float s = 0.0f;
+    const __nv_bfloat16* col = reinterpret_cast<const __nv_bfloat16*>(sDZ2 + (lane >> 3) * DZ2_ALLOC * 16) + (lane & 7);
+    for (int r = DZ2_OFF; r < DZ2_OFF + mnih::M2V; ++r) s += __bfloat162float(col[r * 8]);
+    s_db2[lane] = s;
+  }
+  // TMEM columns: [0,32) conv1 dW (2 tiles x 16), [32,96) conv2 dW (2 tiles x 32), [128,192) conv2 dX
+  if (threadIdx.x == 0) {
+    const uint32_t xa = smem_u32(sA1), dz2 = smem_u32(sDZ2), w2 = smem_u32(sW2);
+    // conv2 dW: M = (t pair, c'') via 16 planes, K = m' (6 steps), N = 32 (B MN-major: dZ2 planes)
+    const uint32_t id_dw2 = make_idesc_bf16(128, 32, 1, 1);
+    for (int mt = 0; mt < 2; ++mt)
+      for (int kk = 0; kk < BWD_ROWS2 / 16; ++kk) {
+        const int sh = mt * 10;  // taps (0,1) -> shifts 0,1 ; taps (2,3) -> 10,11
+        const uint64_t ad = make_desc(xa + (sh + 16 * kk) * 16, 128, mnih::A1_ALLOC * 16);
+        const uint64_t bd = make_desc(dz2 + (DZ2_OFF + 16 * kk) * 16, 128, DZ2_ALLOC * 16);
+        mma_bf16(tmem + 32 + 32 * mt, ad, bd, id_dw2, kk > 0);
+      }
+    // conv2 dX: M = s2d pixel rows (100 -> 128), K = n2 (2 steps per tap), N = 64 (c'')
+    const uint32_t id_dx = make_idesc_bf16(128, 64, 0, 0);
+    for (int t = 0; t < 4; ++t)
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint64_t ad = make_desc(dz2 + (2 * kk) * DZ2_ALLOC * 16 + (DZ2_OFF - mnih::tap_shift2(t)) * 16,
+                                      DZ2_ALLOC * 16, 128);
+        const uint64_t bd = make_desc(w2 + ((t * 4 + 2 * kk) * 64) * 16, 64 * 16, 128);
+        mma_bf16(tmem + 128, ad, bd, id_dx, (t | kk) != 0);
+      }
+    mma_commit(&bar);
+  }
+  __syncwarp();
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  // ---- dZ1 = dA1 * [A1 > 0], into conv1 virtual rows m1 = y*21 + x, planes [n/8][m1][8]
+  {
+    const int p = 32 * warp + lane;  // s2d(2) pixel row of conv2's input
+    float v[64];
+#pragma unroll
+    for (int c = 0; c < 64; c += 16) tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 128 + c, v + c);
+    if (p < mnih::A1_PIX) {
+      const int py = p / 10, px = p % 10;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // (iy, ix) sub-pixel
+        const uint4 m0 = *reinterpret_cast<const uint4*>(sA1 + ((2 * q) * mnih::A1_ALLOC + p) * 16);
+        const uint4 m1 = *reinterpret_cast<const uint4*>(sA1 + ((2 * q + 1) * mnih::A1_ALLOC + p) * 16);
+        const uint32_t mw[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        uint32_t o[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const float a_lo = __uint_as_float(mw[h] << 16), a_hi = __uint_as_float(mw[h] & 0xFFFF0000u);
+          const float d_lo = a_lo > 0.0f ? v[16 * q + 2 * h] : 0.0f;
+          const float d_hi = a_hi > 0.0f ? v[16 * q + 2 * h + 1] : 0.0f;
+          o[h] = pack_bf16(d_lo, d_hi);
+        }
+        const int y = 2 * py + (q >> 1), x = 2 * px + (q & 1);
+        const int m1r = y * mnih::X_W + x;
+        *reinterpret_cast<uint4*>(sDZ1 + (0 * BWD_ROWS1 + m1r) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(sDZ1 + (1 * BWD_ROWS1 + m1r) * 16) = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    }
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    // conv1 dW: M = (t pair, c') via 16 X planes, K = m1 (27 steps), N = 16 (B MN-major: dZ1 planes)
+    const uint32_t xb = smem_u32(sX), dz1 = smem_u32(sDZ1);
+    const uint32_t id_dw1 = make_idesc_bf16(128, 16, 1, 1);
+    for (int mt = 0; mt < 2; ++mt)
+      for (int kk = 0; kk < BWD_ROWS1 / 16; ++kk) {
+        const int sh = mt * mnih::X_W;  // taps (0,1) -> 0,1 ; (2,3) -> 21,22
+        const uint64_t ad = make_desc(xb + (sh + 16 * kk) * 16, 128, mnih::X_ALLOC * 16);
+        const uint64_t bd = make_desc(dz1 + (16 * kk) * 16, 128, BWD_ROWS1 * 16);
+        mma_bf16(tmem + 16 * mt, ad, bd, id_dw1, kk > 0);
+      }
+    mma_commit(&bar);
+  }
+  // db1 from the dZ1 planes while conv1 dW runs
+  if (threadIdx.x < 16) {
+    const int n = threadIdx.x;
+    float s = 0.0f;
+    for (int r = 0; r < 420; ++r) {
+      const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(sDZ1 + ((n >> 3) * BWD_ROWS1 + r) * 16);
+      s += __bfloat162float(row[n & 7]);
+    }
+    s_db1[n] = s;
+  }
+  __syncwarp();
+  mbar_wait(&bar, 1);
+  tc_fence_after();
+  // ---- per-image partials: row = (t, c) of the tile, columns = output channels
+  float* part = a.partial + (long long)j * BWD_PART;
+  {
+    const int r = 32 * warp + lane;  // M row within a tile
+    for (int mt = 0; mt < 2; ++mt) {
+      float v[32];
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 16 * mt, v);
+      float* d1 = part + (mt * 128 + r) * 16;
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(d1 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 32 + 32 * mt, v);
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 32 + 32 * mt + 16, v + 16);
+      float* d2 = part + BWD_PART_W1 + (mt * 128 + r) * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(d2 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    }
+    if (threadIdx.x < 16) part[BWD_PART_W1 + BWD_PART_W2 + threadIdx.x] = s_db1[threadIdx.x];
+    if (threadIdx.x < 32) part[BWD_PART_W1 + BWD_PART_W2 + 16 + threadIdx.x] = s_db2[threadIdx.x];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+// Sum the per-image partials in image order (deterministic) and scatter into G's canonical layout.
+__global__ void bwd_reduce_kernel(BwdConvArgs a) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= BWD_PART) return;
+  {
+    float s = 0.0f;
+#pragma unroll 8
+    for (int i = 0; i < a.n; ++i) s += a.partial[(long long)i * BWD_PART + e];
+    long long dst;
+    if (e < BWD_PART_W1) {  // (mt*128 + r, n) with r -> tap t = 2*mt + r/64, c' = r%64
+      const int row = e / 16, n = e % 16;
+      const int t = 2 * (row / 128) + ((row % 128) >> 6), c = row & 63;
+      const int f = c >> 4, iy = (c >> 2) & 3, ix = c & 3;
+      const int ky = 4 * (t >> 1) + iy, kx = 4 * (t & 1) + ix;
+      dst = a.w1_off + ((n * 4 + f) * 8 + ky) * 8 + kx;
+    } else if (e < BWD_PART_W1 + BWD_PART_W2) {
+      const int ee = e - BWD_PART_W1;
+      const int row = ee / 32, n = ee % 32;
+      const int t = 2 * (row / 128) + ((row % 128) >> 6), c2 = row & 63;
+      const int q = c2 >> 4, c = c2 & 15;
+      const int ky = 2 * (t >> 1) + (q >> 1), kx = 2 * (t & 1) + (q & 1);
+      dst = a.w2_off + ((n * 16 + c) * 4 + ky) * 4 + kx;
+    } else if (e < BWD_PART_W1 + BWD_PART_W2 + 16) {
+      dst = a.b1_off + (e - BWD_PART_W1 - BWD_PART_W2);
+      s *= 1.0f;
+    } else {
+      dst = a.b2_off + (e - BWD_PART_W1 - BWD_PART_W2 - 16);
+    }
+    if (e < BWD_PART_W1) s *= 1.0f / 255.0f;  // conv1 saw integer-valued x: d/dW of (W.u)/255
+    a.grad[dst] += s;
+  }
+}
+
+void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st) {
+  bwd_conv_bf16_kernel<<<a.n, 128, BWD_SMEM, st>>>(a);
+  bwd_reduce_kernel<<<cdiv(BWD_PART, 128), 128, 0, st>>>(a);
+}
+
+void init_bf16_kernel_attrs() {
+  cudaFuncSetAttribute(fwd_conv_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWD_SMEM);
+  cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(bwd_conv_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM);
+}
+
+}  // namespace dqn

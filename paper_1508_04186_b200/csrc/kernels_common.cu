@@ -81,62 +81,56 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
 // the working-precision copy that the fetch all-gathers (a13), and the reset of
 // the gradient accumulator. r is updated first and theta uses the new r (A5);
 // eps sits inside the root (A4).
+// One 16-byte vector per thread (n is a multiple of 64): every load is issued up
+// front, there is no loop-carried latency and no fence. The round counter n is
+// mirrored by the host (deterministic schedule); non-finite elements are counted
+// (sticky) with one atomic per offending thread.
 __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r, float* __restrict__ g, long long n,
-                               float div, float lr, float rho, float omr, float eps, float* __restrict__ pub_f32,
-                               __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr,
-                               int count_round) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
+                               float inv_div, float lr, float rho, float omr, float eps, float* __restrict__ pub_f32,
+                               __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr, int zero_g) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n / 4) return;
+  const float4 g4 = reinterpret_cast<const float4*>(g)[i];
+  float4 t4 = reinterpret_cast<const float4*>(theta)[i];
+  float4 r4 = reinterpret_cast<const float4*>(r)[i];
+  if (zero_g) reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+  float rv[4] = {r4.x, r4.y, r4.z, r4.w};
+  const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
   unsigned bad = 0;
-  for (; i < n; i += stride) {
-    float gb = g[i] / div;
-    g[i] = 0.0f;
-    float th = theta[i];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float gb = gv[q] * inv_div;  // mean over N * n_push gradients (A7, A8)
     if (isfinite(gb)) {
-      float rr = rho * r[i] + omr * gb * gb;
-      r[i] = rr;
-      th = th - lr * gb / sqrtf(rr + eps);
-      theta[i] = th;
+      const float rr = rho * rv[q] + omr * gb * gb;
+      rv[q] = rr;
+      tv[q] = tv[q] - lr * gb * rsqrtf(rr + eps);
     } else {
       ++bad;
     }
-    if (pub_f32) pub_f32[i] = th;
-    if (pub_bf16) pub_bf16[i] = __float2bfloat16_rn(th);
+  }
+  t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);
+  reinterpret_cast<float4*>(theta)[i] = t4;
+  reinterpret_cast<float4*>(r)[i] = make_float4(rv[0], rv[1], rv[2], rv[3]);
+  if (pub_f32) reinterpret_cast<float4*>(pub_f32)[i] = t4;
+  if (pub_bf16) {
+    uint2 o;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(t4.x, t4.y), hi = __floats2bfloat162_rn(t4.z, t4.w);
+    o.x = *reinterpret_cast<uint32_t*>(&lo);
+    o.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(pub_bf16)[i] = o;
   }
   if (bad) atomicAdd(&ctr->nonfinite, bad);
-  // the last block to finish closes the round: n <- n + 1 (Alg. 2, A22)
-  if (count_round) {
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = (atomicAdd(&ctr->blocks_done, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (last && threadIdx.x == 0) {
-      __threadfence();
-      ctr->blocks_done = 0;
-      ctr->n += 1;
-      unsigned nf = atomicAdd(&ctr->nonfinite, 0u);
-      if (nf != ctr->nonfinite_last) {
-        ctr->nonfinite_rounds += 1;
-        ctr->nonfinite_last = nf;
-      }
-    }
-  }
 }
-
-__global__ void bump_generation_kernel(DevCounters* ctr) { ctr->n += 1; }
 
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
-                    float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int count_round,
+                    float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
                     cudaStream_t st) {
-  int blocks = (int)((n + 255) / 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  if (blocks < 1) blocks = 1;
-  rmsprop_kernel<<<blocks, 256, 0, st>>>(theta, r, g, n, div, lr, rho, omr, eps, pub_f32, pub_bf16, ctr,
-                                         count_round);
+  const int blocks = (int)((n / 4 + 255) / 256);
+  rmsprop_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(theta, r, g, n, 1.0f / div, lr, rho, omr, eps, pub_f32,
+                                                          pub_bf16, ctr, zero_g);
 }
 
-void launch_bump_generation(DevCounters* ctr, cudaStream_t st) { bump_generation_kernel<<<1, 1, 0, st>>>(ctr); }
 
 __global__ void f32_to_bf16_kernel(const float* src, __nv_bfloat16* dst, long long n) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;

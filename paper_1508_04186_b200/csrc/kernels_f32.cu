@@ -382,97 +382,6 @@ void launch_bias_grad(const float* dz, int b, int H, float* dst, cudaStream_t st
   bias_grad_kernel<<<cdiv(H, 256), 256, 0, st>>>(dz, b, H, dst);
 }
 
-// ------------------------------------------------------------------ a6 head (TD target + loss + output layer)
-// Per sample j:
-//   Q'_j = W^_o h'_j + b^_o ; m_j = max_a' Q'_j (warp-shuffle max), g_j = argmax (lowest index)
-//   y_j = term_j ? r_j : r_j + gamma m_j                       (a select, A14)
-//   delta_j = Q(s_j)_{a_j} - y_j ; dQ_j = clamp(delta_j, -c, c) / b at a_j only (A2, A3)
-//   dW_o[a] += sum_{j: a_j = a} dQ_j h_j ; db_o[a] += sum dQ_j
-//   dH_j = dQ_j W_o[a_j] * [h_j > 0]          (d pre-activation of the previous layer)
-// Single CTA; every reduction over j is in ascending j.
-__global__ void __launch_bounds__(256) head_f32_kernel(HeadArgs h) {
-  extern __shared__ float4 sm4[];
-  float* s_dq = reinterpret_cast<float*>(sm4);       // [b]
-  int* s_a = reinterpret_cast<int*>(s_dq + h.b);     // [b]
-  float* s_loss = reinterpret_cast<float*>(s_a + h.b);  // [b]
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  const unsigned long long T = h.ctr->T;
-  const int dslot = (int)(T % kDiagSteps);
-  for (int j = warp; j < h.b; j += nw) {
-    const int slot = h.idx[j];
-    const float* hn = h.act[1] + (long long)j * h.H;
-    float best = 0.0f;
-    int barg = 0;
-    for (int a = 0; a < h.A; ++a) {
-      const float* w = h.theta_hat + h.w_off + (long long)a * h.H;
-      float s = 0.0f;
-      for (int i = lane; i < h.H; i += 32) s = fmaf(w[i], hn[i], s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const float q = s + h.theta_hat[h.b_off + a];
-      if (a == 0 || q > best) { best = q; barg = a; }
-    }
-    const int act = h.ring_a[slot];
-    const float r = h.ring_r[slot];
-    const float y = h.ring_term[slot] ? r : r + h.gamma * best;
-    const float* hs = h.act[0] + (long long)j * h.H;
-    const float* w = h.theta + h.w_off + (long long)act * h.H;
-    float s = 0.0f;
-    for (int i = lane; i < h.H; i += 32) s = fmaf(w[i], hs[i], s);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const float q = s + h.theta[h.b_off + act];
-    const float delta = q - y;
-    float dc = delta;
-    if (h.clip > 0.0f) dc = fminf(fmaxf(dc, -h.clip), h.clip);
-    if (lane == 0) {
-      s_dq[j] = dc / (float)h.b;
-      s_a[j] = act;
-      s_loss[j] = 0.5f * delta * delta;
-      h.diag_idx[(long long)dslot * h.b + j] = slot;
-      h.diag_amax[(long long)dslot * h.b + j] = barg;
-    }
-  }
-  __syncthreads();
-  // output-layer gradient
-  for (int e = threadIdx.x; e < h.A * h.H; e += blockDim.x) {
-    const int a = e / h.H, i = e % h.H;
-    float s = 0.0f;
-    for (int j = 0; j < h.b; ++j)
-      if (s_a[j] == a) s = fmaf(s_dq[j], h.act[0][(long long)j * h.H + i], s);
-    h.grad[h.w_off + e] += s;
-  }
-  for (int a = threadIdx.x; a < h.A; a += blockDim.x) {
-    float s = 0.0f;
-    for (int j = 0; j < h.b; ++j)
-      if (s_a[j] == a) s += s_dq[j];
-    h.grad[h.b_off + a] += s;
-  }
-  // d pre-activation of the previous layer (+ its bias gradient when it is an FC)
-  for (int i = threadIdx.x; i < h.H; i += blockDim.x) {
-    float sb = 0.0f;
-    for (int j = 0; j < h.b; ++j) {
-      const float hv = h.act[0][(long long)j * h.H + i];
-      const float d = hv > 0.0f ? s_dq[j] * h.theta[h.w_off + (long long)s_a[j] * h.H + i] : 0.0f;
-      h.dH[(long long)j * h.H + i] = d;
-      sb += d;
-    }
-    if (h.prev_is_fc) h.grad[h.prev_b_off + i] += sb;
-  }
-  if (threadIdx.x == 0) {
-    float l = 0.0f;
-    for (int j = 0; j < h.b; ++j) l += s_loss[j];
-    h.diag_loss[dslot] = l / (float)h.b;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) h.ctr->T = T + 1;  // the step is complete for the sampler
-}
-
-void launch_head_f32(const HeadArgs& h, cudaStream_t st) {
-  const size_t smem = (size_t)h.b * 3 * sizeof(float) + 16;
-  head_f32_kernel<<<1, 256, smem, st>>>(h);
-}
-
 // ------------------------------------------------------------------ a15 acting head (Q only)
 __global__ void q_head_f32_kernel(const float* __restrict__ act, const float* __restrict__ theta, long long w_off,
                                   long long b_off, int H, int A, int n, float* q, int* argmax) {

@@ -1,0 +1,141 @@
+// kernels_head.cu — a6, the fused TD head of Alg. 1, shared by both
+// precisions. Two launches:
+//
+// head_sample (one CTA per sample j, so the b samples run in parallel):
+//   [bf16 path] h_j, h'_j = ReLU(sum over FC split-K partials + b_fc)   (a5's reduction, fused here)
+//   Q'_j = W^_o h'_j + b^_o ; m_j = max_a' Q'_j, g_j = argmax (lowest index on ties, A20)
+//   y_j = term_j ? r_j : r_j + gamma m_j                              (a select, A14)
+//   delta_j = Q(s_j; theta)_{a_j} - y_j ; dQ_j = clamp(delta_j, -c, c) / b at a_j only (A2, A3)
+//   dH_j = dQ_j W_o[a_j] * [h_j > 0]        (d pre-activation of the previous layer, ReLU'(0) = 0)
+// head_finish (cross-sample sums in ascending j: deterministic):
+//   dW_o[a] += sum_{j: a_j = a} dQ_j h_j ; db_o[a] += sum dQ_j ; db_fc += sum_j dH_j
+//   loss = (1/b) sum 1/2 delta^2 (A27) ; T <- T + 1 (the sampler's step counter)
+#include "dqn_internal.h"
+
+namespace dqn {
+
+constexpr int HS_THREADS = 256;
+constexpr int HS_AMAX = 32;
+
+__global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
+  extern __shared__ float4 sm4[];
+  const int H = h.H, A = h.A, j = blockIdx.x;
+  float* s_h0 = reinterpret_cast<float*>(sm4);  // [H]
+  float* s_h1 = s_h0 + H;                       // [H]
+  __shared__ float s_q[HS_AMAX];
+  __shared__ float s_qa;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = HS_THREADS / 32;
+  // ---- the two hidden activation rows of sample j
+  if (h.fc_partial) {
+    for (int u = threadIdx.x; u < H; u += HS_THREADS) {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const float* p = h.fc_partial + (long long)g * h.fc_splits * h.fc_split_stride + (long long)j * H + u;
+        float s = 0.0f;
+#pragma unroll 6
+        for (int sp = 0; sp < h.fc_splits; ++sp) s += __ldg(p + (long long)sp * h.fc_split_stride);
+        const float v = fmaxf(s + __ldg(h.fc_bias[g] + u), 0.0f);
+        (g ? s_h1 : s_h0)[u] = v;
+        h.act_out[g][(long long)j * H + u] = v;
+      }
+    }
+  } else {
+    for (int u = threadIdx.x; u < H; u += HS_THREADS) {
+      s_h0[u] = __ldg(h.act[0] + (long long)j * H + u);
+      s_h1[u] = __ldg(h.act[1] + (long long)j * H + u);
+    }
+  }
+  const int slot = __ldg(h.idx + j);
+  const int act = __ldg(h.ring_a + slot);
+  __syncthreads();
+  // ---- Q'(s'_j; theta^) for every action (warp per action) and Q(s_j; theta)_{a_j}
+  for (int a = warp; a <= A; a += nw) {
+    const bool target = a < A;
+    const float* w = target ? h.theta_hat + h.w_off + (long long)a * H : h.theta + h.w_off + (long long)act * H;
+    const float* x = target ? s_h1 : s_h0;
+    float s = 0.0f;
+    for (int i = lane; i < H; i += 32) s = fmaf(__ldg(w + i), x[i], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (target) s_q[a] = s + __ldg(h.theta_hat + h.b_off + a);
+      else s_qa = s + __ldg(h.theta + h.b_off + act);
+    }
+  }
+  __syncthreads();
+  __shared__ float s_dq;
+  if (threadIdx.x == 0) {
+    float best = s_q[0];
+    int barg = 0;
+    for (int a = 1; a < A; ++a)
+      if (s_q[a] > best) { best = s_q[a]; barg = a; }
+    const float r = __ldg(h.ring_r + slot);
+    const float y = __ldg(h.ring_term + slot) ? r : r + h.gamma * best;
+    const float delta = s_qa - y;
+    float dc = delta;
+    if (h.clip > 0.0f) dc = fminf(fmaxf(dc, -h.clip), h.clip);
+    const float dq = dc / (float)h.b;
+    s_dq = dq;
+    h.s_dq[j] = dq;
+    h.s_act[j] = act;
+    h.s_loss[j] = 0.5f * delta * delta;
+    const int dslot = (int)(h.ctr->T % kDiagSteps);
+    h.diag_idx[(long long)dslot * h.b + j] = slot;
+    h.diag_amax[(long long)dslot * h.b + j] = barg;
+  }
+  __syncthreads();
+  const float dq = s_dq;
+  const float* wa = h.theta + h.w_off + (long long)act * H;
+  for (int u = threadIdx.x; u < H; u += HS_THREADS) {
+    const float d = s_h0[u] > 0.0f ? dq * __ldg(wa + u) : 0.0f;
+    h.dH[(long long)j * H + u] = d;
+    if (h.dH_bf16) h.dH_bf16[(long long)j * H + u] = __float2bfloat16_rn(d);
+  }
+}
+
+// Cross-sample sums; e in [0, A*H) -> dW_o, [A*H, A*H + A) -> db_o, then H entries of db_fc.
+__global__ void head_finish_kernel(HeadArgs h) {
+  const int H = h.H, A = h.A;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const float* h0 = h.fc_partial ? h.act_out[0] : h.act[0];
+  if (e < A * H) {
+    const int a = e / H, u = e % H;
+    float s = 0.0f;
+    for (int j = 0; j < h.b; ++j)
+      if (h.s_act[j] == a) s = fmaf(h.s_dq[j], h0[(long long)j * H + u], s);
+    h.grad[h.w_off + e] += s;
+  } else if (e < A * H + A) {
+    const int a = e - A * H;
+    float s = 0.0f;
+    for (int j = 0; j < h.b; ++j)
+      if (h.s_act[j] == a) s += h.s_dq[j];
+    h.grad[h.b_off + a] += s;
+  } else if (e < A * H + A + H) {
+    if (h.prev_is_fc) {
+      const int u = e - A * H - A;
+      float s = 0.0f;
+      for (int j = 0; j < h.b; ++j) s += h.dH[(long long)j * H + u];
+      h.grad[h.prev_b_off + u] += s;
+    }
+  } else if (e == A * H + A + H) {
+    const unsigned long long T = h.ctr->T;
+    float l = 0.0f;
+    for (int j = 0; j < h.b; ++j) l += h.s_loss[j];
+    h.diag_loss[T % kDiagSteps] = l / (float)h.b;
+    h.ctr->T = T + 1;  // this step is complete for the sampler
+  }
+}
+
+size_t head_smem_bytes(int A, int H, int b) {
+  (void)A;
+  (void)b;
+  return (size_t)2 * H * sizeof(float);
+}
+
+void launch_head_f32(const HeadArgs& h, cudaStream_t st) {
+  head_sample_kernel<<<h.b, HS_THREADS, head_smem_bytes(h.A, h.H, h.b), st>>>(h);
+  const int n = h.A * h.H + h.A + h.H + 1;
+  head_finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(h);
+}
+
+}  // namespace dqn

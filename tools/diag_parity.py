@@ -27,7 +27,8 @@ def table(x, y, net, title):
     for nm, (off, cnt) in zip(names, O.tensor_table(net)):
         yy, xx = np.asarray(y[off:off + cnt], np.float64), np.asarray(x[off:off + cnt], np.float64)
         den = max(np.max(np.abs(yy)), 1e-30)
-        print(f"  {nm:8s} n={cnt:7d} |y|inf={den:.3e} normwise={np.max(np.abs(xx - yy)) / den:.3e}")
+        l2 = np.linalg.norm(xx - yy) / max(np.linalg.norm(yy), 1e-30)
+        print(f"  {nm:8s} n={cnt:7d} |y|inf={den:.3e} normwise={np.max(np.abs(xx - yy)) / den:.3e} rel_l2={l2:.3e}")
 
 
 def main():

@@ -16,6 +16,14 @@ prec = D.BF16 if "--bf16" in sys.argv else D.FP32
 steps = 6
 dc, on, oc = nets(minibatch=32, replay_capacity=1000, lr=2.5e-4, precision=prec)
 theta0 = he_theta(on, 3)
+if "--smooth" in sys.argv:  # every hidden pre-activation > 0: no ReLU kink near any unit
+    tt = O.tensor_table(on)
+    theta0 = np.abs(theta0)
+    for i, (off, cnt) in enumerate(tt[:-2]):
+        if i % 2 == 1:
+            theta0[off:off + cnt] = 0.1
+    # keep the output layer signed so targets and errors have both signs
+    theta0[tt[-2][0]:] = he_theta(on, 3)[tt[-2][0]:]
 rp, raw = replay(on, 1000, 1234)
 g = D.DQN(dc, init_params=theta0)
 g.push(*raw)
@@ -32,3 +40,8 @@ for k in range(steps):
     th_next, _ = O.rmsprop(th, r_k, gr, oc.lr, oc.rms_decay, oc.rms_eps)
     gpu_next = g.params(D.PARAMS_SERVER)
     table(gpu_next - th, th_next - th, on, f"update at step {k} (oracle rule at the GPU state)")
+# forward parity of the acting path at the final state
+states = rp.s[:64]
+q, am = g.q_values(states)
+qo, amo = O.q_values(on, g.params(D.PARAMS_LOCAL).astype(np.float64), states)
+print("q_values normwise", np.max(np.abs(q - qo)) / np.max(np.abs(qo)), "argmax agree", np.mean(am == amo))
