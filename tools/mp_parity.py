@@ -1,0 +1,67 @@
+"""Worker for the multi-GPU parity test (launched by torch.distributed.run, one rank per GPU).
+
+Each rank is replica k of Alg. 1 and owner of shard k of Alg. 2: it pushes its own
+seeded replay (independent per-worker histories), runs `steps` lock-step
+replica steps through the C ABI (NCCL reduce-scatter push + all-gather fetch), and
+rank 0 writes the gathered server theta, the generation and every rank's sampled
+indices to --out (npz). The test compares that file with the oracle's N-replica run.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--precision", default="fp32")
+    ap.add_argument("--n-push", type=int, default=1)
+    ap.add_argument("--n-fetch", type=int, default=1)
+    ap.add_argument("--target-sync", type=int, default=2)
+    ap.add_argument("--b", type=int, default=16)
+    ap.add_argument("--tiny", action="store_true")
+    ap.add_argument("--smooth", action="store_true")
+    ap.add_argument("--lr", type=float, default=1e-3)
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    import paper_1508_04186_b200 as D
+    from tests.helpers import he_theta, nets, replay
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = [D.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    kw = dict(frames=3, height=17, width=13, convs=((5, 5, 2), (6, 3, 2)), fcs=(19,), n_actions=5) if a.tiny else {}
+    prec = D.FP32 if a.precision == "fp32" else D.BF16
+    dc, on, oc = nets(minibatch=a.b, replay_capacity=200, n_push=a.n_push, n_fetch=a.n_fetch,
+                      target_sync=a.target_sync, lr=a.lr, precision=prec, **kw)
+    theta0 = he_theta(on, 3)
+    if a.smooth:
+        from tests.test_gpu_parity_bf16 import smooth_theta
+        theta0 = smooth_theta(on, 3)
+    g = D.DQN(dc, rank=rank, world=world, nccl_id=obj[0], init_params=theta0)
+    _, raw = replay(on, 250, 100 + rank)
+    g.push(*raw)
+    out = g.train(a.steps, want_idx=True)
+    th = g.params(D.PARAMS_SERVER)        # collective
+    idx = torch.from_numpy(out["idx"]).cuda()
+    gathered = [torch.zeros_like(idx) for _ in range(world)]
+    dist.all_gather(gathered, idx)
+    if rank == 0:
+        np.savez(a.out, theta=th, n=out["generation"], idx=np.stack([x.cpu().numpy() for x in gathered]))
+    g.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
