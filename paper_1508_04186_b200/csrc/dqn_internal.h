@@ -159,6 +159,7 @@ struct TcGemmArgs {
   const __nv_bfloat16* B[2];
   long long ldb;  // B(n,k) = b_mn ? B[k*ldb + n] : B[n*ldb + k]
   int a_mn, b_mn;
+  int pre_b;      // 1: B is not the immediate predecessor's output (staged before the PDL wait)
   int M, N, K;
   int BN;         // n-tile (multiple of 16, <= 256)
   int kper;       // K per split (multiple of 16)

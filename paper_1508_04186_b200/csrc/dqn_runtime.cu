@@ -777,11 +777,13 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   gw.B[0] = ctx->a2_bf16; gw.ldb = F.D; gw.b_mn = 1;
   gw.M = F.H; gw.N = F.D; gw.K = b; gw.BN = 144; gw.kper = b; gw.splits = 1;
   gw.epi = TC_EPI_ACCUM; gw.C[0] = ctx->grad + F.w_off; gw.ldc = F.D;
+  gw.pre_b = 1;  // dH (head_sample) and a2 (conv fwd) are two or more launches back
   TcGemmArgs gx{};
   gx.A[0] = ctx->theta_local_bf16 + F.w_off; gx.lda = F.D; gx.a_mn = 1;
   gx.B[0] = ctx->dh_bf16; gx.ldb = F.H; gx.b_mn = 0;
   gx.M = F.D; gx.N = b; gx.K = F.H; gx.BN = b; gx.kper = F.H; gx.splits = 1;
   gx.epi = TC_EPI_MASK_T; gx.out_bf16 = ctx->dz2_bf16; gx.mask = ctx->a2_bf16; gx.ldo = F.D;
+  gx.pre_b = 1;  // dH: head_sample is three launches back
   PB("fc1_bwd", 2);
   launch_tc_gemm(gw, 1, st);
   launch_tc_gemm(gx, 1, st);

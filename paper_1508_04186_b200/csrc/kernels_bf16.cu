@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdio>
 #include "dqn_internal.h"
+#include "pdl.cuh"
 #include "philox.cuh"
 #include "sm100.cuh"
 
@@ -193,11 +194,13 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   }
   if (warp == 0) tmem_alloc(&tbase, 128);
   __syncthreads();  // barriers initialised before anyone waits on them
+  mbar_wait(&bar_ld, 0);
+  expand_state(sX, sU8);  // u8 -> exact bf16 (1/255 folded into the epilogue)
+  // everything above overlaps the previous kernel (the update that publishes theta); weights after the wait
+  pdl_sync();
   const __nv_bfloat16* th = a.theta[g];
   stage_w1(sW1, th + a.w1_off);
   stage_w2(sW2, th + a.w2_off);
-  mbar_wait(&bar_ld, 0);
-  expand_state(sX, sU8);  // u8 -> exact bf16 (1/255 folded into the epilogue)
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
 
 void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st) {
   dim3 grid(a.n, groups);
-  fwd_conv_bf16_kernel<<<grid, 128, FWD_SMEM, st>>>(a);
+  launch_pdl(fwd_conv_bf16_kernel, grid, dim3(128), FWD_SMEM, st, a);
 }
 
 // ------------------------------------------------------------------ generic small tcgen05 GEMM
@@ -351,6 +354,8 @@ __global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
     }
   }
   const int bn = a.BN;
+  // A is always data of an earlier launch (weights / dH); B waits for the predecessor unless flagged
+  if (!a.pre_b) pdl_sync();
   if (!a.b_mn) {
     for (int e = threadIdx.x; e < bn * kch; e += blockDim.x) {
       const int r = e / kch, c = e % kch;
@@ -370,6 +375,7 @@ __global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
     }
   }
   cp_async_wait_all();
+  if (a.pre_b) pdl_sync();  // the epilogue's outputs may still be read by the predecessor
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -473,6 +479,7 @@ __global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
 
 // h[g][n][m] = relu(sum_split partial[g][split][n][m] + bias[g][m]), splits summed in order
 __global__ void fc_reduce_kernel(TcGemmArgs a) {
+  pdl_sync();
   const int g = blockIdx.y;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= (long long)a.M * a.N) return;
@@ -489,10 +496,10 @@ void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st) {
   size_t smem = (size_t)(128 + a.BN) * a.kper * 2;
   if (a.epi == TC_EPI_ACCUM) smem = std::max(smem, (size_t)128 * (a.BN + 4) * 4);  // epilogue tile
   dim3 grid(m_tiles * n_tiles, a.splits, groups);
-  tc_gemm_kernel<<<grid, 128, smem, st>>>(a);
+  launch_pdl(tc_gemm_kernel, grid, dim3(128), smem, st, a);
   if (a.epi == TC_EPI_FC_FWD && a.h_out[0] != nullptr) {  // else the TD head reduces the partials itself
     dim3 rg(cdiv((long long)a.M * a.N, 256), groups);
-    fc_reduce_kernel<<<rg, 256, 0, st>>>(a);
+    launch_pdl(fc_reduce_kernel, rg, dim3(256), 0, st, a);
   }
 }
 
@@ -611,6 +618,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
     }
   }
   __syncthreads();  // zero-filled dZ2 planes before the scatter below
+  pdl_sync();       // dZ2 is the predecessor's (FC dX) output; everything above overlapped it
   // ---- dZ2 (canonical [n2][81]) into planes [n2/8][DZ2_OFF + m'][8], m' = oy*10 + ox; + db2
   {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(a.dz2 + (long long)j * mnih::D);
@@ -750,6 +758,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
 
 // Sum the per-image partials in image order (deterministic) and scatter into G's canonical layout.
 __global__ void bwd_reduce_kernel(BwdConvArgs a) {
+  pdl_sync();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= BWD_PART) return;
   {
@@ -782,8 +791,8 @@ __global__ void bwd_reduce_kernel(BwdConvArgs a) {
 }
 
 void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st) {
-  bwd_conv_bf16_kernel<<<a.n, 128, BWD_SMEM, st>>>(a);
-  bwd_reduce_kernel<<<cdiv(BWD_PART, 128), 128, 0, st>>>(a);
+  launch_pdl(bwd_conv_bf16_kernel, dim3(a.n), dim3(128), BWD_SMEM, st, a);
+  launch_pdl(bwd_reduce_kernel, dim3(cdiv(BWD_PART, 128)), dim3(128), 0, st, a);
 }
 
 void init_bf16_kernel_attrs() {

@@ -3,6 +3,7 @@
 //   push path (validation + FIFO ring writes, "Store experience" of Alg. 1)
 //   a12 fused RMSProp shard update of Alg. 2
 #include "dqn_internal.h"
+#include "pdl.cuh"
 #include "philox.cuh"
 
 namespace dqn {
@@ -88,6 +89,7 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
 __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r, float* __restrict__ g, long long n,
                                float inv_div, float lr, float rho, float omr, float eps, float* __restrict__ pub_f32,
                                __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr, int zero_g) {
+  pdl_sync();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n / 4) return;
   const float4 g4 = reinterpret_cast<const float4*>(g)[i];
@@ -127,8 +129,8 @@ void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, fl
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
                     cudaStream_t st) {
   const int blocks = (int)((n / 4 + 255) / 256);
-  rmsprop_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(theta, r, g, n, 1.0f / div, lr, rho, omr, eps, pub_f32,
-                                                          pub_bf16, ctr, zero_g);
+  launch_pdl(rmsprop_kernel, dim3(blocks < 1 ? 1 : blocks), dim3(256), 0, st, theta, r, g, n, 1.0f / div, lr, rho, omr,
+             eps, pub_f32, pub_bf16, ctr, zero_g);
 }
 
 

@@ -11,6 +11,7 @@
 //   dW_o[a] += sum_{j: a_j = a} dQ_j h_j ; db_o[a] += sum dQ_j ; db_fc += sum_j dH_j
 //   loss = (1/b) sum 1/2 delta^2 (A27) ; T <- T + 1 (the sampler's step counter)
 #include "dqn_internal.h"
+#include "pdl.cuh"
 
 namespace dqn {
 
@@ -25,6 +26,12 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
   __shared__ float s_q[HS_AMAX];
   __shared__ float s_qa;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = HS_THREADS / 32;
+  // sampled slot and its (a, r, terminal): outputs of launches before the predecessor (PDL-safe)
+  const int slot = __ldg(h.idx + j);
+  const int act = __ldg(h.ring_a + slot);
+  const float r = __ldg(h.ring_r + slot);
+  const uint8_t term = __ldg(h.ring_term + slot);
+  pdl_sync();
   // ---- the two hidden activation rows of sample j
   if (h.fc_partial) {
     for (int u = threadIdx.x; u < H; u += HS_THREADS) {
@@ -45,8 +52,6 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
       s_h1[u] = __ldg(h.act[1] + (long long)j * H + u);
     }
   }
-  const int slot = __ldg(h.idx + j);
-  const int act = __ldg(h.ring_a + slot);
   __syncthreads();
   // ---- Q'(s'_j; theta^) for every action (warp per action) and Q(s_j; theta)_{a_j}
   for (int a = warp; a <= A; a += nw) {
@@ -69,8 +74,7 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
     int barg = 0;
     for (int a = 1; a < A; ++a)
       if (s_q[a] > best) { best = s_q[a]; barg = a; }
-    const float r = __ldg(h.ring_r + slot);
-    const float y = __ldg(h.ring_term + slot) ? r : r + h.gamma * best;
+    const float y = term ? r : r + h.gamma * best;
     const float delta = s_qa - y;
     float dc = delta;
     if (h.clip > 0.0f) dc = fminf(fmaxf(dc, -h.clip), h.clip);
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
 
 // Cross-sample sums; e in [0, A*H) -> dW_o, [A*H, A*H + A) -> db_o, then H entries of db_fc.
 __global__ void head_finish_kernel(HeadArgs h) {
+  pdl_sync();
   const int H = h.H, A = h.A;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const float* h0 = h.fc_partial ? h.act_out[0] : h.act[0];
@@ -133,9 +138,9 @@ size_t head_smem_bytes(int A, int H, int b) {
 }
 
 void launch_head_f32(const HeadArgs& h, cudaStream_t st) {
-  head_sample_kernel<<<h.b, HS_THREADS, head_smem_bytes(h.A, h.H, h.b), st>>>(h);
+  launch_pdl(head_sample_kernel, dim3(h.b), dim3(HS_THREADS), head_smem_bytes(h.A, h.H, h.b), st, h);
   const int n = h.A * h.H + h.A + h.H + 1;
-  head_finish_kernel<<<(n + 255) / 256, 256, 0, st>>>(h);
+  launch_pdl(head_finish_kernel, dim3((n + 255) / 256), dim3(256), 0, st, h);
 }
 
 }  // namespace dqn

@@ -1,0 +1,38 @@
+// pdl.cuh — Programmatic Dependent Launch (sm_90+): a kernel launched with
+// programmaticStreamSerialization may start while its predecessor is still
+// running; it must execute pdl_wait() (griddepcontrol.wait) before touching
+// anything the predecessor writes. Every kernel here triggers its dependent
+// right after its own wait, so code placed BEFORE pdl_wait() may read data
+// produced two or more launches back (transitively complete) — never data of
+// the immediate predecessor. Captured into CUDA graphs as programmatic edges.
+#pragma once
+#include <cuda_runtime.h>
+#include <utility>
+
+namespace dqn {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// the usual pair: wait for the predecessor, then let the successor start its prologue
+__device__ __forceinline__ void pdl_sync() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+}  // namespace dqn
