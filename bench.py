@@ -56,6 +56,7 @@ def region_work(name: str, b: int):
         "conv2_fwd": (2 * 2 * b * macs(c2), 2 * b * c1["N"] * c1["HoWo"] * 4 + 2 * b * c2["N"] * c2["HoWo"] * 4),
         "fc1_fwd": (2 * 2 * b * D * Hfc, 2 * b * D * 4 + 2 * D * Hfc * 4 + 2 * b * Hfc * 4),
         "head_td": (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 * 2),
+        "head_sample": (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 * 2),
         "fc1_bwd": (4 * b * D * Hfc, b * Hfc * 4 + b * D * 4 * 2 + D * Hfc * 4 * 3),
         "conv2_bwd": (2 * 2 * b * macs(c2), b * c2["N"] * c2["HoWo"] * 4 + 3 * b * c1["N"] * c1["HoWo"] * 4),
         "conv1_bwd": (2 * b * macs(c1), b * state + b * c1["N"] * c1["HoWo"] * 4),
@@ -65,6 +66,7 @@ def region_work(name: str, b: int):
     # fused regions of the bf16 tensor-core path
     w["conv_fwd"] = tuple(x + y for x, y in zip(w["conv1_fwd"], w["conv2_fwd"]))
     w["conv_bwd"] = tuple(x + y for x, y in zip(w["conv1_bwd"], w["conv2_bwd"]))
+    w["fc1_bwd_head_finish"] = w["fc1_bwd"]
     return w.get(name, (0, 0))
 
 

@@ -134,7 +134,7 @@ void launch_conv_bwd_dw_f32(const ConvShape& cs, const float* dout, const ImgSrc
 void launch_reduce_rows(const float* partial, int rows, long long E, float* dst, cudaStream_t st);
 void launch_gemm_f32(const GemmArgs& g, cudaStream_t st);
 void launch_bias_grad(const float* dz, int b, int H, float* dst, cudaStream_t st);
-void launch_head_f32(const HeadArgs& h, cudaStream_t st);
+void launch_head_f32(const HeadArgs& h, cudaStream_t st, bool with_finish = true);
 size_t head_smem_bytes(int A, int H, int b);
 void launch_q_head_f32(const float* act, const float* theta, long long w_off, long long b_off, int H, int A, int n,
                        float* q, int* argmax, cudaStream_t st);
@@ -159,7 +159,8 @@ struct TcGemmArgs {
   const __nv_bfloat16* B[2];
   long long ldb;  // B(n,k) = b_mn ? B[k*ldb + n] : B[n*ldb + k]
   int a_mn, b_mn;
-  int pre_b;      // 1: B is not the immediate predecessor's output (staged before the PDL wait)
+  int pre_a;      // 1: A is not the immediate predecessor's output (staged before the PDL wait)
+  int pre_b;      // same for B
   int M, N, K;
   int BN;         // n-tile (multiple of 16, <= 256)
   int kper;       // K per split (multiple of 16)
@@ -197,6 +198,9 @@ void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* 
                      const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st);
 void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st);
 void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st);
+// one launch: the tiles of GEMM p0, the tiles of GEMM p1 (single split, group 0 each), then the
+// cross-sample TD-head finish (head_finish.cuh) — the bf16 path's whole FC backward
+void launch_tc_pair_with_head(const TcGemmArgs& p0, const TcGemmArgs& p1, const HeadArgs& head, cudaStream_t st);
 void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st);
 
 }  // namespace dqn

@@ -748,6 +748,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   gf.B[0] = ctx->a2_bf16; gf.B[1] = ctx->a2_bf16 + (long long)b * F.D; gf.ldb = F.D; gf.b_mn = 0;
   gf.M = F.H; gf.N = b; gf.K = F.D; gf.BN = b; gf.kper = F.D / ctx->fc_splits; gf.splits = ctx->fc_splits;
   gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial; gf.counters = ctx->tc_counters;
+  gf.pre_a = 1; gf.pre_b = 0;  // W from the previous step's update; a2 from the predecessor
   gf.bias[0] = ctx->theta_local + F.b_off; gf.bias[1] = ctx->theta_hat + F.b_off;
   // (h_out left null: the TD head reduces the split-K partials, adds the bias and applies ReLU)
   PB("fc1_fwd", 1);
@@ -768,8 +769,8 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   h.act_out[0] = ctx->act_fc[0][0]; h.act_out[1] = ctx->act_fc[0][1];
   h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
   h.s_dq = ctx->head_dq; h.s_act = ctx->head_act; h.s_loss = ctx->head_loss;
-  PB("head_td", 2);
-  launch_head_f32(h, st);
+  PB("head_sample", 1);
+  launch_head_f32(h, st, /*with_finish=*/false);
   PE();
   // a7 FC backward: dW[h][d] += sum_j dH[j][h] a2[j][d]  and  dz2[j][d] = [a2 > 0] sum_h dH[j][h] W[h][d]
   TcGemmArgs gw{};
@@ -777,16 +778,15 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   gw.B[0] = ctx->a2_bf16; gw.ldb = F.D; gw.b_mn = 1;
   gw.M = F.H; gw.N = F.D; gw.K = b; gw.BN = 144; gw.kper = b; gw.splits = 1;
   gw.epi = TC_EPI_ACCUM; gw.C[0] = ctx->grad + F.w_off; gw.ldc = F.D;
-  gw.pre_b = 1;  // dH (head_sample) and a2 (conv fwd) are two or more launches back
+  gw.pre_a = 0; gw.pre_b = 1;  // dH comes from the predecessor (head_sample), a2 from the conv forward
   TcGemmArgs gx{};
   gx.A[0] = ctx->theta_local_bf16 + F.w_off; gx.lda = F.D; gx.a_mn = 1;
   gx.B[0] = ctx->dh_bf16; gx.ldb = F.H; gx.b_mn = 0;
   gx.M = F.D; gx.N = b; gx.K = F.H; gx.BN = b; gx.kper = F.H; gx.splits = 1;
   gx.epi = TC_EPI_MASK_T; gx.out_bf16 = ctx->dz2_bf16; gx.mask = ctx->a2_bf16; gx.ldo = F.D;
-  gx.pre_b = 1;  // dH: head_sample is three launches back
-  PB("fc1_bwd", 2);
-  launch_tc_gemm(gw, 1, st);
-  launch_tc_gemm(gx, 1, st);
+  gx.pre_a = 1; gx.pre_b = 0;  // W is published by the previous step's update; dH by the predecessor
+  PB("fc1_bwd_head_finish", 1);
+  launch_tc_pair_with_head(gw, gx, h, st);
   PE();
   // a8/a9 conv backward
   BwdConvArgs ba{};
@@ -1012,6 +1012,7 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
       gf.B[0] = ctx->a2_bf16; gf.ldb = F.D;
       gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = (m + 15) / 16 * 16; gf.kper = F.D / ctx->fc_splits;
       gf.splits = ctx->fc_splits; gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
+      gf.pre_a = 1; gf.pre_b = 0;
       gf.counters = ctx->tc_counters; gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
       launch_tc_gemm(gf, 1, st);
       in = ctx->act_fc[0][0];

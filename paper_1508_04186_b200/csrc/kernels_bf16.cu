@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdio>
 #include "dqn_internal.h"
+#include "head_finish.cuh"
 #include "pdl.cuh"
 #include "philox.cuh"
 #include "sm100.cuh"
@@ -310,15 +311,12 @@ void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st) {
 // One CTA = one (group, m-tile of 128, n-tile of BN, k-split); the CTA stages its
 // whole K slice at once (these GEMMs are latency-bound: M, N <= 2592, K <= 2592).
 
-__global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar;
-  __shared__ uint32_t tbase;
+__device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int split, int g, uint8_t* smem,
+                                             uint64_t& bar, uint32_t& tbase) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (a.N + a.BN - 1) / a.BN;
   const int m_tiles = (a.M + 127) / 128;
-  const int mt = blockIdx.x % m_tiles, nt = blockIdx.x / m_tiles;
-  const int split = blockIdx.y, g = blockIdx.z;
+  const int mt = tile % m_tiles, nt = tile / m_tiles;
   const int m0 = mt * 128, n0 = nt * a.BN;
   const int k0 = split * a.kper;
   const int KC = min(a.kper, a.K - k0);  // multiple of 16 by construction
@@ -333,6 +331,7 @@ __global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
   // ---- stage A (128 rows x KC) and B (BN rows x KC), 16-byte vectors
   const __nv_bfloat16* Ag = a.A[g];
   const __nv_bfloat16* Bg = a.B[g];
+  if (!a.pre_a) pdl_sync();
   const int kch = KC / 8;
   // all 16-byte pieces go out as cp.async (LDGSTS) so a thread keeps dozens of loads in flight
   const uint4 z4 = make_uint4(0, 0, 0, 0);
@@ -354,8 +353,8 @@ __global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
     }
   }
   const int bn = a.BN;
-  // A is always data of an earlier launch (weights / dH); B waits for the predecessor unless flagged
-  if (!a.pre_b) pdl_sync();
+  // operands produced by the immediate predecessor are staged after the PDL wait (pre_a / pre_b flags)
+  if (a.pre_a && !a.pre_b) pdl_sync();
   if (!a.b_mn) {
     for (int e = threadIdx.x; e < bn * kch; e += blockDim.x) {
       const int r = e / kch, c = e % kch;
@@ -375,7 +374,7 @@ __global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
     }
   }
   cp_async_wait_all();
-  if (a.pre_b) pdl_sync();  // the epilogue's outputs may still be read by the predecessor
+  if (a.pre_a && a.pre_b) pdl_sync();  // the epilogue's outputs may still be read by the predecessor
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -477,6 +476,49 @@ __global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
+__global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  tc_gemm_tile(a, blockIdx.x, blockIdx.y, blockIdx.z, smem, bar, tbase);
+}
+
+struct TcPairArgs {
+  TcGemmArgs p0, p1;
+  int tiles0, tiles1;
+  HeadArgs head;
+};
+
+__global__ void __launch_bounds__(128) tc_pair_kernel(TcPairArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int bx = blockIdx.x;
+  if (bx < a.tiles0) {
+    tc_gemm_tile(a.p0, bx, 0, 0, smem, bar, tbase);
+  } else if (bx < a.tiles0 + a.tiles1) {
+    tc_gemm_tile(a.p1, bx - a.tiles0, 0, 0, smem, bar, tbase);
+  } else {
+    pdl_sync();  // the TD head's per-sample outputs come from the predecessor
+    const int n = head_finish_elems(a.head);
+    for (int e = (bx - a.tiles0 - a.tiles1) * 128 + threadIdx.x; e < n; e += (gridDim.x - a.tiles0 - a.tiles1) * 128)
+      head_finish_elem(a.head, e);
+  }
+}
+
+static size_t tc_smem(const TcGemmArgs& a) {
+  size_t smem = (size_t)(128 + a.BN) * a.kper * 2;
+  if (a.epi == TC_EPI_ACCUM) smem = std::max(smem, (size_t)128 * (a.BN + 4) * 4);  // epilogue tile
+  return smem;
+}
+
+void launch_tc_pair_with_head(const TcGemmArgs& p0, const TcGemmArgs& p1, const HeadArgs& head, cudaStream_t st) {
+  TcPairArgs a{p0, p1, cdiv(p0.M, 128) * cdiv(p0.N, p0.BN), cdiv(p1.M, 128) * cdiv(p1.N, p1.BN), head};
+  const int head_ctas = cdiv(head.A * head.H + head.A + head.H + 1, 128);
+  launch_pdl(tc_pair_kernel, dim3(a.tiles0 + a.tiles1 + head_ctas), dim3(128), std::max(tc_smem(p0), tc_smem(p1)), st,
+             a);
+}
+
 // h[g][n][m] = relu(sum_split partial[g][split][n][m] + bias[g][m]), splits summed in order
 __global__ void fc_reduce_kernel(TcGemmArgs a) {
   pdl_sync();
@@ -493,8 +535,7 @@ __global__ void fc_reduce_kernel(TcGemmArgs a) {
 
 void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st) {
   const int m_tiles = cdiv(a.M, 128), n_tiles = cdiv(a.N, a.BN);
-  size_t smem = (size_t)(128 + a.BN) * a.kper * 2;
-  if (a.epi == TC_EPI_ACCUM) smem = std::max(smem, (size_t)128 * (a.BN + 4) * 4);  // epilogue tile
+  const size_t smem = tc_smem(a);
   dim3 grid(m_tiles * n_tiles, a.splits, groups);
   launch_pdl(tc_gemm_kernel, grid, dim3(128), smem, st, a);
   if (a.epi == TC_EPI_FC_FWD && a.h_out[0] != nullptr) {  // else the TD head reduces the partials itself
@@ -798,6 +839,7 @@ void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st) {
 void init_bf16_kernel_attrs() {
   cudaFuncSetAttribute(fwd_conv_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWD_SMEM);
   cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(bwd_conv_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM);
 }
 

@@ -11,6 +11,7 @@
 //   dW_o[a] += sum_{j: a_j = a} dQ_j h_j ; db_o[a] += sum dQ_j ; db_fc += sum_j dH_j
 //   loss = (1/b) sum 1/2 delta^2 (A27) ; T <- T + 1 (the sampler's step counter)
 #include "dqn_internal.h"
+#include "head_finish.cuh"
 #include "pdl.cuh"
 
 namespace dqn {
@@ -100,35 +101,8 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
 // Cross-sample sums; e in [0, A*H) -> dW_o, [A*H, A*H + A) -> db_o, then H entries of db_fc.
 __global__ void head_finish_kernel(HeadArgs h) {
   pdl_sync();
-  const int H = h.H, A = h.A;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const float* h0 = h.fc_partial ? h.act_out[0] : h.act[0];
-  if (e < A * H) {
-    const int a = e / H, u = e % H;
-    float s = 0.0f;
-    for (int j = 0; j < h.b; ++j)
-      if (h.s_act[j] == a) s = fmaf(h.s_dq[j], h0[(long long)j * H + u], s);
-    h.grad[h.w_off + e] += s;
-  } else if (e < A * H + A) {
-    const int a = e - A * H;
-    float s = 0.0f;
-    for (int j = 0; j < h.b; ++j)
-      if (h.s_act[j] == a) s += h.s_dq[j];
-    h.grad[h.b_off + a] += s;
-  } else if (e < A * H + A + H) {
-    if (h.prev_is_fc) {
-      const int u = e - A * H - A;
-      float s = 0.0f;
-      for (int j = 0; j < h.b; ++j) s += h.dH[(long long)j * H + u];
-      h.grad[h.prev_b_off + u] += s;
-    }
-  } else if (e == A * H + A + H) {
-    const unsigned long long T = h.ctr->T;
-    float l = 0.0f;
-    for (int j = 0; j < h.b; ++j) l += h.s_loss[j];
-    h.diag_loss[T % kDiagSteps] = l / (float)h.b;
-    h.ctr->T = T + 1;  // this step is complete for the sampler
-  }
+  if (e < head_finish_elems(h)) head_finish_elem(h, e);
 }
 
 size_t head_smem_bytes(int A, int H, int b) {
@@ -137,8 +111,9 @@ size_t head_smem_bytes(int A, int H, int b) {
   return (size_t)2 * H * sizeof(float);
 }
 
-void launch_head_f32(const HeadArgs& h, cudaStream_t st) {
+void launch_head_f32(const HeadArgs& h, cudaStream_t st, bool with_finish) {
   launch_pdl(head_sample_kernel, dim3(h.b), dim3(HS_THREADS), head_smem_bytes(h.A, h.H, h.b), st, h);
+  if (!with_finish) return;  // the bf16 path runs the finish inside its fused FC-backward launch
   const int n = h.A * h.H + h.A + h.H + 1;
   launch_pdl(head_finish_kernel, dim3((n + 255) / 256), dim3(256), 0, st, h);
 }
