@@ -70,6 +70,25 @@ def region_work(name: str, b: int):
     return w.get(name, (0, 0))
 
 
+REGION_KERNELS = {"conv_fwd": ["fwd_conv_bf16_kernel"], "fc1_fwd": ["tc_gemm_kernel"],
+                  "head_sample": ["head_sample_kernel"], "fc1_bwd_head_finish": ["tc_pair_kernel"],
+                  "conv_bwd": ["bwd_conv_bf16_kernel", "bwd_reduce_kernel"], "rmsprop_update": ["rmsprop_kernel"]}
+
+
+def region_traffic(name: str, dtype: str):
+    """DRAM bytes (read + write) per launch of a region's kernels, from the committed `ncu --set full`
+    capture of this round (profiles/r1_traffic.json), or None when not captured."""
+    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if dtype != "bf16" or not os.path.exists(p) or name not in REGION_KERNELS:
+        return None
+    with open(p) as f:
+        t = json.load(f)
+    try:
+        return sum((t[k]["dram_read_MB"] + t[k]["dram_write_MB"]) * 1e6 for k in REGION_KERNELS[name])
+    except KeyError:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
 
@@ -325,7 +344,7 @@ def main():
             roof = {"bound": "hbm", "achieved": byts / (top["avg_us"] * 1e-6) / 1e9, "peak": pk["hbm"],
                     "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = None
+        roof["traffic"] = region_traffic(top["name"], dtype)
         roof["kernel"] = top["name"]
         roof["avg_us"] = top["avg_us"]
         roof["share_of_step"] = top["avg_us"] / step_us if step_us else None
