@@ -387,7 +387,7 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
            const uint8_t* const* s, const int32_t* const* a, const double* const* r,
            const uint8_t* const* s_next, const uint8_t* const* term, const double* theta0, int64_t steps,
            double* theta_out, double* r_out, int64_t* n_out, double* loss, int64_t* idx, int32_t* amax,
-           double* grad0) {
+           double* grad0, int64_t* stale_hist) {
   shape_t sh;
   if (build_shapes(net, &sh)) return -1;
   const int N = cfg->n_replicas, b = cfg->minibatch;
@@ -429,6 +429,12 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
   }
   double* g = (double*)malloc(sizeof(double) * P);
   double* gbar = (double*)malloc(sizeof(double) * P);
+  /* O13: the server's last L+1 published states; a fetch returns theta^(max(n - L, 0)) */
+  const int L = cfg->fetch_lag > 0 ? cfg->fetch_lag : 0;
+  double* hist = (double*)malloc(sizeof(double) * P * (L + 1));
+  memcpy(hist, theta0, sizeof(double) * P);
+  int64_t* pend = (int64_t*)calloc((size_t)N * cfg->n_push, sizeof(int64_t)); /* n_local per step of the round */
+  if (stale_hist) memset(stale_hist, 0, sizeof(int64_t) * 32);
   uint8_t* bs = (uint8_t*)malloc(b * sz);
   uint8_t* bsn = (uint8_t*)malloc(b * sz);
   int32_t* ba = (int32_t*)malloc(sizeof(int32_t) * b);
@@ -442,8 +448,9 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
     for (int k = 0; k < N; ++k) {
       /* O10 "Fetch model theta and iteration number n from server", every n_fetch steps (A9) */
       if (T % cfg->n_fetch == 0) {
-        memcpy(th_local[k], theta, sizeof(double) * P);
-        n_local[k] = n;
+        const int64_t m = n - L > 0 ? n - L : 0; /* L = 0: the current server theta */
+        memcpy(th_local[k], hist + (m % (L + 1)) * P, sizeof(double) * P);
+        n_local[k] = m;
         /* O11 target refresh every C generations (A10) */
         if (n_local[k] - ell[k] >= cfg->target_sync) {
           memcpy(th_hat[k], th_local[k], sizeof(double) * P);
@@ -469,6 +476,7 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
       if (grad0 && T == 0 && k == 0) memcpy(grad0, g, sizeof(double) * P);
       /* O8 accumulate until the push (A8: no local update) */
       for (int64_t i = 0; i < P; ++i) acc[k][i] += g[i];
+      pend[(int64_t)k * cfg->n_push + T % cfg->n_push] = n_local[k]; /* generation this gradient used */
     }
     /* O9 server round when the push is due (A7) */
     if ((T + 1) % cfg->n_push == 0) {
@@ -482,7 +490,14 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
         if (!isfinite(gbar[i])) { rc = -3; continue; }
         or_rmsprop(theta + i, rms + i, gbar + i, 1, cfg->lr, cfg->rms_decay, cfg->rms_eps);
       }
+      /* A25: every replica step of this round contributes n - n_local (its theta's generation) */
+      if (stale_hist)
+        for (int64_t e = 0; e < (int64_t)N * cfg->n_push; ++e) {
+          const int64_t s = n - pend[e];
+          stale_hist[s < 31 ? s : 31] += 1;
+        }
       n += 1; /* A22 */
+      memcpy(hist + (n % (L + 1)) * P, theta, sizeof(double) * P);
       for (int k = 0; k < N; ++k) memset(acc[k], 0, sizeof(double) * P);
     }
   }
@@ -491,6 +506,7 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
   if (n_out) *n_out = n;
 
   free(g); free(gbar); free(bs); free(bsn); free(ba); free(br); free(bt); free(y); free(am);
+  free(hist); free(pend);
   for (int k = 0; k < N; ++k) { free(th_local[k]); free(th_hat[k]); free(acc[k]); }
   free(th_local); free(th_hat); free(acc); free(n_local); free(ell);
   free(theta); free(rms);

@@ -40,6 +40,8 @@ typedef struct {
   double rms_eps;          /* inside the root (A4) */
   double err_clip;         /* 0 = off (A3) */
   uint64_t seed;           /* sampler key (A11) */
+  int32_t fetch_lag;       /* 0: synchronous; L > 0: a fetch returns theta as it was L rounds ago (O13, A32) */
+  int32_t pad;
 } or_train_cfg;
 
 /* ---- shapes (O0) ---- */
@@ -96,7 +98,7 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
            const uint8_t* const* s, const int32_t* const* a, const double* const* r,
            const uint8_t* const* s_next, const uint8_t* const* term, const double* theta0, int64_t steps,
            double* theta_out, double* r_out, int64_t* n_out, double* loss, int64_t* idx, int32_t* amax,
-           double* grad0);
+           double* grad0, int64_t* stale_hist /* [32]: staleness n_apply - n_local per replica step (A25) */);
 
 #ifdef __cplusplus
 }

@@ -46,7 +46,7 @@ class _Cfg(C.Structure):
     _fields_ = [("n_replicas", C.c_int32), ("minibatch", C.c_int32), ("n_push", C.c_int32),
                 ("n_fetch", C.c_int32), ("target_sync", C.c_int64), ("gamma", C.c_double),
                 ("lr", C.c_double), ("rms_decay", C.c_double), ("rms_eps", C.c_double),
-                ("err_clip", C.c_double), ("seed", C.c_uint64)]
+                ("err_clip", C.c_double), ("seed", C.c_uint64), ("fetch_lag", C.c_int32), ("pad", C.c_int32)]
 
 
 @dataclass
@@ -93,6 +93,8 @@ class TrainCfg:
     rms_eps: float = 1e-8
     err_clip: float = 0.0
     seed: int = 0xD15EA5E
+    fetch_lag: int = 0   # O13 / A32: a fetch returns theta as it was `fetch_lag` rounds ago
+    pad: int = 0
 
     def c(self) -> _Cfg:
         c = _Cfg()
@@ -133,7 +135,7 @@ def lib():
         _lib.or_rmsprop.argtypes = [D, D, D, C.c_int64, C.c_double, C.c_double, C.c_double]
         _lib.or_run.restype = C.c_int
         _lib.or_run.argtypes = [C.POINTER(_Net), C.POINTER(_Cfg), C.c_int64, I64, C.POINTER(U8), C.POINTER(I32),
-                                C.POINTER(D), C.POINTER(U8), C.POINTER(U8), D, C.c_int64, D, D, I64, D, I64, I32, D]
+                                C.POINTER(D), C.POINTER(U8), C.POINTER(U8), D, C.c_int64, D, D, I64, D, I64, I32, D, I64]
     return _lib
 
 
@@ -295,8 +297,10 @@ def run(net: Net, cfg: TrainCfg, capacity: int, replays: Sequence[Replay], theta
     idx = np.zeros((N, steps, cfg.minibatch), np.int64)
     amax = np.zeros((N, steps, cfg.minibatch), np.int32)
     g0 = np.zeros(P) if want_grad0 else None
+    stale = np.zeros(32, np.int64)
     rc = lib().or_run(C.byref(net.c()), C.byref(cfg.c()), capacity, _p(n_pushed, C.c_int64), S, A, R, SN, TT,
                       _p(theta0, C.c_double), steps, _p(theta, C.c_double), _p(rr, C.c_double),
                       _p(n_out, C.c_int64), _p(loss, C.c_double), _p(idx, C.c_int64), _p(amax, C.c_int32),
-                      _p(g0, C.c_double) if g0 is not None else None)
-    return dict(rc=rc, theta=theta, r=rr, n=int(n_out[0]), loss=loss, idx=idx, amax=amax, grad0=g0)
+                      _p(g0, C.c_double) if g0 is not None else None, _p(stale, C.c_int64))
+    return dict(rc=rc, theta=theta, r=rr, n=int(n_out[0]), loss=loss, idx=idx, amax=amax, grad0=g0,
+                staleness=stale)

@@ -34,10 +34,12 @@ def ring_view(rp, cap):
     return [slot_of[sl] for sl in range(size)]
 
 
-def serial_reference(cfg, replays, theta0, steps, cap, net=TINY):
-    """Alg. 1 x N + Alg. 2 written out: fetch every n_fetch, refresh when n-l >= C,
-    accumulate, mean over N*n_push, one RMSProp per round."""
+def serial_reference(cfg, replays, theta0, steps, cap, net=TINY, stale=None):
+    """Alg. 1 x N + Alg. 2 written out: fetch every n_fetch (theta as it was fetch_lag rounds
+    ago, O13), refresh when n-l >= C, accumulate, mean over N*n_push, one RMSProp per round."""
     N, b = cfg.n_replicas, cfg.minibatch
+    history = [theta0.copy()]          # server theta after 0, 1, 2, ... rounds
+    used = {}                          # (k, T) -> generation of the theta the gradient used
     theta = theta0.copy()
     r = np.zeros_like(theta)
     n = 0
@@ -50,8 +52,9 @@ def serial_reference(cfg, replays, theta0, steps, cap, net=TINY):
     for T in range(steps):
         for k in range(N):
             if T % cfg.n_fetch == 0:
-                th_local[k] = theta.copy()
-                n_loc[k] = n
+                m = max(n - cfg.fetch_lag, 0)
+                th_local[k] = history[m].copy()
+                n_loc[k] = m
                 if n_loc[k] - ell[k] >= cfg.target_sync:
                     th_hat[k] = th_local[k].copy()
                     ell[k] = n_loc[k]
@@ -60,10 +63,16 @@ def serial_reference(cfg, replays, theta0, steps, cap, net=TINY):
             y, _ = O.targets(net, th_hat[k], rp.s_next[idx], rp.r[idx], rp.term[idx], cfg.gamma)
             _, g = O.loss_grad(net, th_local[k], rp.s[idx], rp.a[idx], y, cfg.err_clip)
             acc[k] += g
+            used[(k, T)] = n_loc[k]
         if (T + 1) % cfg.n_push == 0:
             gbar = sum(acc) / (N * cfg.n_push)
+            if stale is not None:
+                for k in range(N):
+                    for t in range(T + 1 - cfg.n_push, T + 1):
+                        stale[min(n - used[(k, t)], 31)] += 1
             theta, r = O.rmsprop(theta, r, gbar, cfg.lr, cfg.rms_decay, cfg.rms_eps)
             n += 1
+            history.append(theta.copy())
             acc = [np.zeros_like(theta) for _ in range(N)]
     return theta, r, n
 
@@ -153,3 +162,28 @@ def test_nonfinite_reward_is_flagged_and_not_applied():
     moved = out["theta"] != theta0
     # every element whose mean gradient is non-finite keeps its value (A24)
     assert np.all(np.isfinite(out["theta"])) and not np.all(moved)
+
+
+@pytest.mark.parametrize("N,n_push,n_fetch,lag", [(1, 1, 1, 1), (2, 2, 2, 1), (2, 3, 1, 2), (1, 2, 3, 1)])
+def test_async_lag_twin_equals_serial_loop(N, n_push, n_fetch, lag):
+    """O13: the asynchronous mode's deterministic twin — fetches land `lag` rounds late — and its
+    staleness histogram (A25) against the written-out loop."""
+    cfg = O.TrainCfg(n_replicas=N, minibatch=3, n_push=n_push, n_fetch=n_fetch, target_sync=2, lr=1e-2,
+                     gamma=0.9, fetch_lag=lag)
+    replays = make_replays(N, 50, 300)
+    theta0 = he_theta(TINY, 4)
+    steps = 7
+    out = O.run(TINY, cfg, CAP, replays, theta0, steps)
+    stale = np.zeros(32, np.int64)
+    th, r, n = serial_reference(cfg, replays, theta0, steps, CAP, stale=stale)
+    assert out["n"] == n
+    np.testing.assert_allclose(out["theta"], th, rtol=0, atol=1e-13)
+    assert np.array_equal(out["staleness"], stale)
+    assert stale.sum() == N * n_push * (steps // n_push)
+
+
+def test_lag1_one_step_rounds_have_staleness_one():
+    # n_push = n_fetch = 1, lag 1: round 0 uses theta^(0) (staleness 0), every later round theta^(n-1)
+    cfg = O.TrainCfg(n_replicas=1, minibatch=2, fetch_lag=1)
+    out = O.run(TINY, cfg, CAP, make_replays(1, 30, 5), he_theta(TINY, 1), 6)
+    assert out["staleness"][0] == 1 and out["staleness"][1] == 5 and out["staleness"].sum() == 6
