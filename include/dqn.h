@@ -47,8 +47,10 @@ enum {
 enum { DQN_FP32 = 0,   /* fp32 SIMT kernels; parity <= 1e-5 vs the fp64 oracle            */
        DQN_BF16 = 1 }; /* bf16 operands on tcgen05 tensor cores, fp32 accumulate; <= 2e-2 */
 /* push / fetch schedule (DESIGN.md §2 a11-a13) */
-enum { DQN_DETERMINISTIC = 0, /* lock-step, reproducible                         */
-       DQN_ASYNC = 1 };       /* reserved: asynchronous staleness mode (next row) */
+enum { DQN_DETERMINISTIC = 0, /* lock-step: a fetch returns the current server theta                    */
+       DQN_ASYNC = 1 };       /* the server round (push, RMSProp, publish) overlaps the next steps on a
+                                 second stream; a fetch returns the server theta of one round earlier
+                                 (lag 1, the deterministic twin of Downpour's staleness, O13 / A32)   */
 /* which parameter vector dqn_get_params returns */
 enum {
   DQN_PARAMS_SERVER = 0, /* global theta of Alg. 2 (fp32 masters, gathered over ranks: collective) */
@@ -99,6 +101,8 @@ typedef struct {
   float* loss_per_step;      /* [k]                                                                  */
   /* output */
   int64_t kernel_launches;   /* kernels of this library launched by the call (graph kernel nodes)     */
+  int64_t staleness_hist[32];/* DQN_ASYNC: replica steps by staleness n_apply - n_local (A25), since create;
+                                bucket 31 collects >= 31. All zero in the deterministic mode.          */
 } dqn_step_stats;
 
 /* Per-region device time of the replica step (diagnostic; dqn_profile_steps). */

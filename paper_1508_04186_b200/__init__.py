@@ -48,7 +48,8 @@ class _Config(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("loss_mean", C.c_double), ("generation", C.c_int64), ("steps_done", C.c_int64),
                 ("device_ms", C.c_float), ("nonfinite_elems", C.c_int64), ("sampled_idx", C.c_void_p),
-                ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p), ("kernel_launches", C.c_int64)]
+                ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p), ("kernel_launches", C.c_int64),
+                ("staleness_hist", C.c_int64 * 32)]
 
 
 class _RegionTime(C.Structure):
@@ -208,7 +209,7 @@ class DQN:
         rc = lib().dqn_train_steps(self._h, k, C.byref(st))
         out = dict(loss_mean=st.loss_mean, generation=st.generation, steps_done=st.steps_done,
                    device_ms=st.device_ms, nonfinite_elems=st.nonfinite_elems, idx=idx, argmax=am, loss=lp,
-                   kernel_launches=st.kernel_launches, rc=rc)
+                   kernel_launches=st.kernel_launches, staleness=np.array(st.staleness_hist[:], np.int64), rc=rc)
         self._check(rc)
         return out
 

@@ -59,6 +59,16 @@ struct dqn_ctx {
   int* diag_amax = nullptr;
   // bf16 tensor-core path (precision == DQN_BF16)
   bool bf16 = false;
+  // DQN_ASYNC: the push -> RMSProp -> publish round runs on comm_stream while
+  // the replica keeps stepping; a fetch returns the server theta of one round earlier (lag 1)
+  bool async = false;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_grad = nullptr, ev_gen[2] = {};  // ev_gen[m % 2]: theta^(m) published in theta_pub[m % 2]
+  float* g_send = nullptr;                        // [P_pad] gradient handed to the round in flight
+  float* theta_pub[2] = {};                       // [P_pad] published server theta, by generation parity
+  __nv_bfloat16* theta_pub_bf16[2] = {};
+  long long stale_hist[32] = {};                  // A25: n_apply - n_local per replica step
+  std::vector<long long> round_nloc;              // n_local of the steps of the current round
   __nv_bfloat16* theta_local_bf16 = nullptr;  // [P_pad] working copy the tensor cores read
   __nv_bfloat16* theta_hat_bf16 = nullptr;    // [P_pad]
   __nv_bfloat16* a2_bf16 = nullptr;           // [2b][2592] conv2 activations (s: theta, s': theta^)
@@ -194,7 +204,7 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   if (c->replay_capacity < 1) { *why = "replay_capacity must be >= 1"; return DQN_EINVAL; }
   if (c->n_push < 1 || c->n_fetch < 1) { *why = "n_push and n_fetch must be >= 1"; return DQN_EINVAL; }
   if (c->precision != DQN_FP32 && c->precision != DQN_BF16) { *why = "unknown precision"; return DQN_EINVAL; }
-  if (c->sync_mode != DQN_DETERMINISTIC) { *why = "only DQN_DETERMINISTIC is implemented"; return DQN_EINVAL; }
+  if (c->sync_mode != DQN_DETERMINISTIC && c->sync_mode != DQN_ASYNC) { *why = "unknown sync_mode"; return DQN_EINVAL; }
   if (!(c->rms_decay >= 0.0 && c->rms_decay < 1.0) || !(c->rms_eps >= 0.0) || !(c->lr >= 0.0) ||
       !std::isfinite(c->gamma) || !(c->err_clip >= 0.0)) {
     *why = "invalid hyper-parameter"; return DQN_EINVAL;
@@ -286,6 +296,14 @@ static void free_all(dqn_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_grad) cudaEventDestroy(c->ev_grad);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_gen[i]) cudaEventDestroy(c->ev_gen[i]);
+    if (c->theta_pub[i]) cudaFree(c->theta_pub[i]);
+    if (c->theta_pub_bf16[i]) cudaFree(c->theta_pub_bf16[i]);
+  }
+  if (c->g_send) cudaFree(c->g_send);
 }
 
 // split-K factor so a GEMM fills the machine (148 SMs)
@@ -316,7 +334,8 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   ctx->cap = cfg->replay_capacity;
   ctx->use_graphs = !(getenv("DQN_NO_GRAPH") && atoi(getenv("DQN_NO_GRAPH")));
   ctx->keep_grad = getenv("DQN_KEEP_GRAD") && atoi(getenv("DQN_KEEP_GRAD"));
-  ctx->alias_local = (world == 1 && cfg->n_fetch == 1);
+  ctx->async = cfg->sync_mode == DQN_ASYNC;
+  ctx->alias_local = (world == 1 && cfg->n_fetch == 1 && !ctx->async);
   ctx->bf16 = cfg->precision == DQN_BF16;
 
   if (cuda_stream) {
@@ -430,6 +449,20 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     launch_f32_to_bf16(ctx->theta_hat, ctx->theta_local_bf16, ctx->P_pad, ctx->stream);
     launch_f32_to_bf16(ctx->theta_hat, ctx->theta_hat_bf16, ctx->P_pad, ctx->stream);
     CK(cudaGetLastError());
+  }
+  if (ctx->async) {  // theta^(0) published in slot 0; the comm stream and its events
+    CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_grad, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&ctx->ev_gen[i], cudaEventDisableTiming));
+      if ((rc = dalloc(ctx, &ctx->theta_pub[i], ctx->P_pad))) return rc;
+      if (ctx->bf16 && (rc = dalloc(ctx, &ctx->theta_pub_bf16[i], ctx->P_pad))) return rc;
+    }
+    if ((rc = dalloc(ctx, &ctx->g_send, ctx->P_pad))) return rc;
+    CK(cudaMemcpyAsync(ctx->theta_pub[0], ctx->theta_hat, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    if (ctx->bf16) launch_f32_to_bf16(ctx->theta_pub[0], ctx->theta_pub_bf16[0], ctx->P_pad, ctx->stream);
+    CK(cudaEventRecord(ctx->ev_gen[0], ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
 
@@ -566,11 +599,11 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
       CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_master, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
       PE();
     }
-    if (refresh) {
-      PB("target_refresh", 0);
-      CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
-      PE();
-    }
+  }
+  if (refresh) {  // right after a fetch (the async mode's fetch is enqueued ahead of the graph)
+    PB("target_refresh", 0);
+    CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+    PE();
   }
   // a1 sample
   PB("sample", 1);
@@ -723,13 +756,13 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
       launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
       PE();
     }
-    if (refresh) {
-      PB("target_refresh", 0);
-      CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(ctx->theta_hat_bf16, ctx->theta_local_bf16, sizeof(__nv_bfloat16) * ctx->P_pad,
-                         cudaMemcpyDeviceToDevice, st));
-      PE();
-    }
+  }
+  if (refresh) {
+    PB("target_refresh", 0);
+    CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->theta_hat_bf16, ctx->theta_local_bf16, sizeof(__nv_bfloat16) * ctx->P_pad,
+                       cudaMemcpyDeviceToDevice, st));
+    PE();
   }
   // a1-a4: sample + gather + conv1 + conv2 for s (theta) and s' (theta^), tcgen05
   FwdConvArgs fa{};
@@ -860,20 +893,87 @@ static int run_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push, bool prof
   return DQN_OK;
 }
 
-// O10 / O11 / O9 schedule of step T (host mirror; identical on every rank)
+// O10 / O11 / O9 schedule of step T (host mirror; identical on every rank). In the asynchronous
+// mode a fetch returns theta^(max(n - 1, 0)), the server state one round earlier (O13, A32).
 static void schedule(dqn_ctx* ctx, bool* fetch, bool* refresh, bool* push) {
   const dqn_config& c = ctx->cfg;
   const long long T = ctx->T;
   *fetch = (T % c.n_fetch) == 0;
   *refresh = false;
   if (*fetch) {
-    ctx->n_local = ctx->n;
+    ctx->n_local = ctx->async ? std::max(ctx->n - 1, 0LL) : ctx->n;
     if (ctx->n_local - ctx->ell >= c.target_sync) {
       *refresh = true;
       ctx->ell = ctx->n_local;
     }
   }
   *push = ((T + 1) % c.n_push) == 0;
+}
+
+// async fetch, enqueued on the compute stream ahead of the step graph: wait until theta^(m) is
+// published, then copy it into the working buffers the graphs read
+static int async_fetch(dqn_ctx* ctx) {
+  const int s = (int)(ctx->n_local % 2);
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gen[s], 0));
+  CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_pub[s], sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  if (ctx->bf16)
+    CK(cudaMemcpyAsync(ctx->theta_local_bf16, ctx->theta_pub_bf16[s], sizeof(__nv_bfloat16) * ctx->P_pad,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+  return DQN_OK;
+}
+
+// async push: hand the accumulated gradient to the comm stream, which runs the whole server round
+// (reduce-scatter, RMSProp on the owned shard, all-gather into theta_pub[(n+1) % 2]) while the
+// replica keeps stepping. All NCCL traffic of this mode lives on the comm stream, in rank order.
+static int async_push(dqn_ctx* ctx) {
+  const dqn_config& c = ctx->cfg;
+  cudaStream_t cs = ctx->comm_stream;
+  CK(cudaMemcpyAsync(ctx->g_send, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, ctx->stream));
+  CK(cudaEventRecord(ctx->ev_grad, ctx->stream));
+  CK(cudaStreamWaitEvent(cs, ctx->ev_grad, 0));
+  const float div = (float)((double)ctx->world * c.n_push);
+  const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
+  const int s = (int)((ctx->n + 1) % 2);
+  if (ctx->world > 1) {
+    NK(ncclReduceScatter(ctx->g_send, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, cs));
+    launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
+                   (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, cs);
+    NK(ncclAllGather(ctx->theta_master, ctx->theta_pub[s], (size_t)ctx->shard, ncclFloat, ctx->comm, cs));
+  } else {
+    launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_send, ctx->P_pad, div, (float)c.lr, rho, omr,
+                   (float)c.rms_eps, ctx->theta_pub[s], nullptr, ctx->ctr, 0, cs);
+  }
+  if (ctx->bf16) launch_f32_to_bf16(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->P_pad, cs);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_gen[s], cs));
+  return DQN_OK;
+}
+
+// One replica step T: schedule, (async fetch), the step graph, (async push), counters.
+static int do_step(dqn_ctx* ctx, bool profile, long long* kernels, bool* out_fetch, bool* out_refresh,
+                   bool* out_push) {
+  bool fetch, refresh, push;
+  schedule(ctx, &fetch, &refresh, &push);
+  int rc;
+  if (ctx->async && fetch && (rc = async_fetch(ctx))) return rc;
+  const bool g_fetch = fetch && !ctx->async, g_push = push && !ctx->async;
+  if ((rc = run_step(ctx, g_fetch, refresh, g_push, profile, kernels))) return rc;
+  if (ctx->async) {
+    ctx->round_nloc.push_back(ctx->n_local);
+    if (push) {
+      if ((rc = async_push(ctx))) return rc;
+      for (long long nl : ctx->round_nloc) ctx->stale_hist[std::min(ctx->n - nl, 31LL)] += 1;  // A25
+      ctx->round_nloc.clear();
+    }
+  }
+  if (push) ctx->n += 1;
+  ctx->T += 1;
+  if (out_fetch) *out_fetch = g_fetch;
+  if (out_refresh) *out_refresh = refresh;
+  if (out_push) *out_push = g_push;
+  return DQN_OK;
 }
 
 extern "C" int dqn_profile_steps(dqn_ctx* ctx, int64_t k, dqn_region_time* out, int32_t cap, int32_t* n_regions) {
@@ -886,11 +986,8 @@ extern "C" int dqn_profile_steps(dqn_ctx* ctx, int64_t k, dqn_region_time* out, 
   std::vector<int> cnt, kern;
   for (long long s = 0; s < k; ++s) {
     bool fetch, refresh, push;
-    schedule(ctx, &fetch, &refresh, &push);
-    int rc = run_step(ctx, fetch, refresh, push, true, nullptr);
+    int rc = do_step(ctx, true, nullptr, &fetch, &refresh, &push);
     if (rc) return rc;
-    if (push) ctx->n += 1;
-    ctx->T += 1;
     CK(cudaStreamSynchronize(ctx->stream));
     const int v = (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0) | 8;
     for (auto& m : ctx->marks[v]) {
@@ -930,12 +1027,8 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
   long long kernels = 0;
   for (long long s = 0; s < k; ++s) {
     // O10 / O11: fetch at the start of step T when T % n_fetch == 0, then refresh theta^ when n - l >= C
-    bool fetch, refresh, push;
-    schedule(ctx, &fetch, &refresh, &push);
-    int rc = run_step(ctx, fetch, refresh, push, false, &kernels);
+    int rc = do_step(ctx, false, &kernels, nullptr, nullptr, nullptr);
     if (rc) return rc;
-    if (push) ctx->n += 1;
-    ctx->T += 1;
   }
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   DevCounters hc;
@@ -970,6 +1063,7 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
     stats->generation = ctx->n;
     stats->steps_done = ctx->T;
     stats->nonfinite_elems = hc.nonfinite;
+    for (int i = 0; i < 32; ++i) stats->staleness_hist[i] = ctx->stale_hist[i];
     stats->kernel_launches = kernels;
     double lm = 0.0;
     for (float l : loss) lm += l;
@@ -1074,8 +1168,14 @@ extern "C" int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, 
     case DQN_PARAMS_SERVER:
     case DQN_PARAMS_RMS: {
       float* shard = which == DQN_PARAMS_SERVER ? ctx->theta_master : ctx->rms;
+      if (ctx->async) {  // let the round in flight finish; the server state lives on the comm stream
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaStreamSynchronize(ctx->comm_stream));
+      }
       if (ctx->world > 1) {
-        NK(ncclAllGather(shard, ctx->gather_tmp, (size_t)ctx->shard, ncclFloat, ctx->comm, ctx->stream));
+        cudaStream_t cs = ctx->async ? ctx->comm_stream : ctx->stream;
+        NK(ncclAllGather(shard, ctx->gather_tmp, (size_t)ctx->shard, ncclFloat, ctx->comm, cs));
+        CK(cudaStreamSynchronize(cs));
         src = ctx->gather_tmp;
       } else {
         src = shard;
@@ -1108,6 +1208,7 @@ extern "C" const char* dqn_last_error(const dqn_ctx* ctx) { return ctx ? ctx->er
 extern "C" void dqn_destroy(dqn_ctx* ctx) {
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
   free_all(ctx);
   delete ctx;
 }

@@ -63,3 +63,22 @@ def test_two_replicas_bf16_mnih(tmp_path):
     assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
     assert per_tensor_rel(res["theta"], ref["theta"], on) < 2e-2
     assert rel_l2_per_tensor(res["theta"] - th0, ref["theta"] - th0, on) < 0.1
+
+
+def test_two_replicas_async_fp32_match_lag1_twin(tmp_path):
+    """DQN_ASYNC at N = 2: the reduce-scatter / update / all-gather round overlaps the next steps on
+    the comm stream; the result equals the oracle's lag-1 twin (O13)."""
+    if n_gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_ranks(2, tmp_path, "--tiny", "--n-push", "2", "--n-fetch", "2", "--target-sync", "1", "--steps", "8",
+                    "--async-mode")
+    dc, on, oc = nets(minibatch=16, replay_capacity=200, n_push=2, n_fetch=2, target_sync=1, lr=1e-3, **TINY_KW)
+    oc.n_replicas = 2
+    oc.fetch_lag = 1
+    reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
+    ref = O.run(on, oc, 200, reps, he_theta(on, 3).astype(np.float64), 8)
+    assert int(res["n"]) == ref["n"]
+    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
+    assert per_tensor_rel(res["theta"], ref["theta"], on) < 1e-5
+    # rank 0's histogram counts its own replica steps; the oracle's counts both replicas
+    assert np.array_equal(res["staleness"] * 2, ref["staleness"])

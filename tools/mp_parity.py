@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--b", type=int, default=16)
     ap.add_argument("--tiny", action="store_true")
     ap.add_argument("--smooth", action="store_true")
+    ap.add_argument("--async-mode", action="store_true")
     ap.add_argument("--lr", type=float, default=1e-3)
     a = ap.parse_args()
     import torch
@@ -43,7 +44,8 @@ def main():
     kw = dict(frames=3, height=17, width=13, convs=((5, 5, 2), (6, 3, 2)), fcs=(19,), n_actions=5) if a.tiny else {}
     prec = D.FP32 if a.precision == "fp32" else D.BF16
     dc, on, oc = nets(minibatch=a.b, replay_capacity=200, n_push=a.n_push, n_fetch=a.n_fetch,
-                      target_sync=a.target_sync, lr=a.lr, precision=prec, **kw)
+                      target_sync=a.target_sync, lr=a.lr, precision=prec,
+                      sync_mode=D.ASYNC if a.async_mode else D.DETERMINISTIC, **kw)
     theta0 = he_theta(on, 3)
     if a.smooth:
         from tests.test_gpu_parity_bf16 import smooth_theta
@@ -57,7 +59,8 @@ def main():
     gathered = [torch.zeros_like(idx) for _ in range(world)]
     dist.all_gather(gathered, idx)
     if rank == 0:
-        np.savez(a.out, theta=th, n=out["generation"], idx=np.stack([x.cpu().numpy() for x in gathered]))
+        np.savez(a.out, theta=th, n=out["generation"], idx=np.stack([x.cpu().numpy() for x in gathered]),
+                 staleness=out["staleness"])
     g.close()
     dist.barrier()
     dist.destroy_process_group()
