@@ -28,6 +28,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 MNIH = dict(convs=((16, 8, 4), (32, 4, 2)), fcs=(256,), n_actions=6)
+SCALED = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=18)
+# BASELINE.json configs[0..4]; C = target refresh period, async = DQN_ASYNC (lag-1 staleness mode)
+CONFIGS = {
+    "c1": dict(idx=0, net=MNIH, b=32, replay=1000, n_push=1, n_fetch=1, C=2**62, async_=False),
+    "c2": dict(idx=1, net=MNIH, b=32, replay=1_000_000, n_push=1, n_fetch=1, C=1000, async_=False),
+    "c3": dict(idx=2, net=MNIH, b=32, replay=1_000_000, n_push=1, n_fetch=1, C=1000, async_=False),
+    "c4": dict(idx=3, net=MNIH, b=256, replay=1_000_000, n_push=10, n_fetch=10, C=1000, async_=True),
+    "c5": dict(idx=4, net=SCALED, b=512, replay=1_000_000, n_push=1, n_fetch=1, C=1000, async_=False),
+}
+for _c in CONFIGS.values():
+    _c["async"] = _c.pop("async_")
+
+
+def net_name(net):
+    conv = ", ".join(f"conv{f} {k}x{k}/{s}" for f, k, s in net["convs"])
+    return f"{conv}, fc{net['fcs'][0]}, {net['n_actions']} actions"
 METRIC = "DQN transitions/sec trained (device-timed, max over ranks) at 1/2/4/8 B200"
 UNIT = "transitions/s"
 FP32_ALU_PEAK_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # FFMA lanes x SMs x clocks.max.sm
@@ -43,29 +59,32 @@ def peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
-def region_work(name: str, b: int):
-    """Algorithmic FLOPs and bytes of one step region of the Mnih net."""
+def region_work(name: str, b: int, net=MNIH):
+    """Algorithmic FLOPs and bytes of one step region. Convolutions: forward on s (theta)
+    and s' (theta^), backward dW for every layer and dX for every layer but the first; FC likewise."""
     F, H, W = 4, 84, 84
-    c1 = dict(C=4, N=16, k=8, HoWo=400)
-    c2 = dict(C=16, N=32, k=4, HoWo=81)
-    D, Hfc, A = 2592, 256, 6
-    macs = lambda L: L["HoWo"] * L["N"] * L["C"] * L["k"] ** 2  # noqa: E731
     state = F * H * W
-    w = {
-        "conv1_fwd": (2 * 2 * b * macs(c1), 2 * b * state + 2 * b * c1["N"] * c1["HoWo"] * 4),
-        "conv2_fwd": (2 * 2 * b * macs(c2), 2 * b * c1["N"] * c1["HoWo"] * 4 + 2 * b * c2["N"] * c2["HoWo"] * 4),
-        "fc1_fwd": (2 * 2 * b * D * Hfc, 2 * b * D * 4 + 2 * D * Hfc * 4 + 2 * b * Hfc * 4),
-        "head_td": (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 * 2),
-        "head_sample": (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 * 2),
-        "fc1_bwd": (4 * b * D * Hfc, b * Hfc * 4 + b * D * 4 * 2 + D * Hfc * 4 * 3),
-        "conv2_bwd": (2 * 2 * b * macs(c2), b * c2["N"] * c2["HoWo"] * 4 + 3 * b * c1["N"] * c1["HoWo"] * 4),
-        "conv1_bwd": (2 * b * macs(c1), b * state + b * c1["N"] * c1["HoWo"] * 4),
-        "rmsprop_update": (0, 677686 * 4 * 6),
-        "sample": (0, b * 4),
-    }
+    layers, c, h = [], F, H
+    for (n, k, s) in net["convs"]:
+        ho = (h - k) // s + 1
+        layers.append(dict(C=c, N=n, k=k, HoWo=ho * ho))
+        c, h = n, ho
+    D, Hfc, A = c * h * h, net["fcs"][0], net["n_actions"]
+    macs = lambda L: L["HoWo"] * L["N"] * L["C"] * L["k"] ** 2  # noqa: E731
+    P = sum(L["N"] * (L["C"] * L["k"] ** 2 + 1) for L in layers) + Hfc * (D + 1) + A * (Hfc + 1)
+    w = {}
+    for i, L in enumerate(layers):
+        act_in = 4 * b * (state if i == 0 else layers[i - 1]["N"] * layers[i - 1]["HoWo"])
+        w[f"conv{i + 1}_fwd"] = (2 * 2 * b * macs(L), 2 * act_in + 2 * 4 * b * L["N"] * L["HoWo"])
+        w[f"conv{i + 1}_bwd"] = ((2 if i else 1) * 2 * b * macs(L), act_in + 4 * b * L["N"] * L["HoWo"])
+    w["fc1_fwd"] = (2 * 2 * b * D * Hfc, 2 * b * D * 4 + 2 * D * Hfc * 4 + 2 * b * Hfc * 4)
+    w["head_td"] = w["head_sample"] = (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 * 2)
+    w["fc1_bwd"] = (4 * b * D * Hfc, b * Hfc * 4 + b * D * 4 * 2 + D * Hfc * 4 * 3)
+    w["rmsprop_update"] = (0, P * 4 * 6)
+    w["sample"] = (0, b * 4)
     # fused regions of the bf16 tensor-core path
-    w["conv_fwd"] = tuple(x + y for x, y in zip(w["conv1_fwd"], w["conv2_fwd"]))
-    w["conv_bwd"] = tuple(x + y for x, y in zip(w["conv1_bwd"], w["conv2_bwd"]))
+    w["conv_fwd"] = tuple(sum(w[f"conv{i + 1}_fwd"][q] for i in range(len(layers))) for q in range(2))
+    w["conv_bwd"] = tuple(sum(w[f"conv{i + 1}_bwd"][q] for i in range(len(layers))) for q in range(2))
     w["fc1_bwd_head_finish"] = w["fc1_bwd"]
     return w.get(name, (0, 0))
 
@@ -216,7 +235,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "bf16"])
-    ap.add_argument("--replay", type=int, default=1_000_000)
+    ap.add_argument("--replay", type=int, default=None, help="replay capacity per replica (default: the config's)")
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default: c2 at N = 1, c3 at N > 1)")
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--profile-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -249,12 +270,18 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    ck = args.config or ("c2" if world == 1 else "c3")
+    C = CONFIGS[ck]
+    if args.replay is None:
+        args.replay = C["replay"]
     prec = {"fp32": D.FP32, "bf16": D.BF16}.get(args.precision)
-    b = 32
+    b = C["b"]
+    net = C["net"]
     cfg = None
     for p in ([prec] if prec is not None else [D.BF16, D.FP32]):
-        cfg = D.Config(**MNIH, minibatch=b, replay_capacity=args.replay, target_sync=1000, precision=p,
-                       lr=2.5e-4, gamma=0.99, n_push=1, n_fetch=1)
+        cfg = D.Config(**net, minibatch=b, replay_capacity=args.replay, target_sync=C["C"], precision=p,
+                       lr=2.5e-4, gamma=0.99, n_push=C["n_push"], n_fetch=C["n_fetch"],
+                       sync_mode=D.ASYNC if C["async"] else D.DETERMINISTIC)
         try:
             dqn = D.DQN(cfg, rank=rank, world=world, nccl_id=nccl_id, stream=stream.cuda_stream)
             break
@@ -269,7 +296,7 @@ def main():
     done = 0
     while done < args.replay:
         n = min(chunk, args.replay - done)
-        s, a, r, sn, t = synth.g_pong_torch(n, 4, 84, 84, 6, 0x5EED + 1000 * rank + done, "cuda")
+        s, a, r, sn, t = synth.g_pong_torch(n, 4, 84, 84, net["n_actions"], 0x5EED + 1000 * rank + done, "cuda")
         dqn.push(s, a, r, sn, t)
         done += n
     del s, a, r, sn, t
@@ -333,7 +360,7 @@ def main():
     if regions:
         step_us = sum(r["avg_us"] for r in regions if r["steps"] >= args.profile_steps // 2)
         top = max(regions, key=lambda r: r["avg_us"])
-        flops, byts = region_work(top["name"], b)
+        flops, byts = region_work(top["name"], b, net)
         if dtype == "bf16" and flops:
             roof = {"bound": "tensor", "achieved": flops / (top["avg_us"] * 1e-6) / 1e12, "peak": pk["bf16_sus"],
                     "unit": "TFLOP/s"}
@@ -361,14 +388,16 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-        "config": {"workload": "BASELINE.json configs[1]" if world == 1 else "BASELINE.json configs[2]",
-                   "net": "Mnih-2013 (conv16 8x8/4, conv32 4x4/2, fc256, 6 actions)", "minibatch_per_replica": b,
-                   "replay_per_replica": args.replay, "target_sync_C": 1000, "n_push": 1, "n_fetch": 1,
+        "config": {"workload": f"BASELINE.json configs[{C['idx']}]", "net": net_name(net), "minibatch_per_replica": b,
+                   "replay_per_replica": args.replay, "target_sync_C": C["C"] if C["C"] < 2**40 else None,
+                   "n_push": C["n_push"], "n_fetch": C["n_fetch"],
+                   "sync_mode": "async (lag-1 fetch)" if C["async"] else "deterministic",
                    "parallelism": f"dp{world} + sharded parameter server", "gamma": 0.99,
                    "l2": "inputs larger than L2: each step gathers 32 random slots of a "
                          f"{args.replay * 56454 / 1e9:.1f} GB replay",
                    "prefill_s": round(prefill_s, 1)},
         "gpu_launches": launches,
+        "staleness_hist": [int(x) for x in out["staleness"][:8]] if C["async"] else None,
         "clocks": clk.summary(),
         "e2e": e2e,
         "roofline": roof,
