@@ -139,6 +139,38 @@ size_t head_smem_bytes(int A, int H, int b);
 void launch_q_head_f32(const float* act, const float* theta, long long w_off, long long b_off, int H, int A, int n,
                        float* q, int* argmax, cudaStream_t st);
 
+// NEXT-1: push + RMSProp + fetch in one kernel over NVLink peer memory (kernels_comm.cu)
+constexpr int kMaxWorld = 8;
+struct ServerRoundArgs {
+  int world, rank, n_push;
+  long long shard;                              // elements owned per rank (multiple of 64)
+  long long grad_elems;                         // P_pad
+  float* grad[kMaxWorld];                       // every rank's G (peer pointers; [rank] is local)
+  float* theta_local[kMaxWorld];                // every rank's working theta (fp32)
+  __nv_bfloat16* theta_local_bf16[kMaxWorld];   // and its bf16 copy (nullptr on the fp32 path)
+  unsigned long long* flags[kMaxWorld];         // every rank's barrier-A array [world]
+  unsigned long long* done[kMaxWorld];          // every rank's barrier-B counter
+  unsigned long long* my_flags;
+  unsigned long long* my_done;
+  float* theta_master;                          // owned shard
+  float* rms;
+  float inv_div, lr, rho, omr, eps;
+  DevCounters* ctr;
+  unsigned long long* trace;                    // optional [64][4] globaltimer stamps (DQN_TRACE_COMM=1)
+};
+void launch_server_round(const ServerRoundArgs& a, cudaStream_t st);
+// the acquire half of the round's second barrier, run at the start of the next step
+struct FusedAcquire {
+  const unsigned long long* done;               // nullptr: no fused round in this context
+  unsigned long long per_round;                 // world * server-round blocks
+  int n_push;
+  float* grad;                                  // this rank's G, cleared once every peer has read it
+  long long grad_elems;
+  DevCounters* ctr;
+};
+void launch_fused_round_acquire(const FusedAcquire& f, cudaStream_t st);
+int server_round_blocks(long long shard);
+
 // bf16 tensor-core path, Mnih-2013 net (kernels_bf16.cu)
 struct FwdConvArgs {
   const uint8_t* ring[2];          // s / s' rings (s2d) or a staging buffer (ctr == nullptr: image j = slot j)
@@ -152,6 +184,7 @@ struct FwdConvArgs {
   int n;
   __nv_bfloat16* a2;               // [groups*n][2592]
   uint8_t* a1_save;                // [n][8][144][16] or nullptr
+  FusedAcquire acq;                // NEXT-1: the previous round's deliveries (acq.done == nullptr: none)
 };
 struct TcGemmArgs {
   const __nv_bfloat16* A[2];

@@ -69,6 +69,13 @@ struct dqn_ctx {
   __nv_bfloat16* theta_pub_bf16[2] = {};
   long long stale_hist[32] = {};                  // A25: n_apply - n_local per replica step
   std::vector<long long> round_nloc;              // n_local of the steps of the current round
+  // NEXT-1 fused server round over NVLink peer memory (world > 1, deterministic, n_fetch == 1)
+  bool fused_comm = false;
+  ServerRoundArgs sra{};                          // peer pointers etc., filled at create
+  FusedAcquire acq{};                             // the next step's acquire half (acq.done == nullptr: off)
+  unsigned long long* flags = nullptr;            // [kMaxWorld] barrier A (written by peers)
+  unsigned long long* done = nullptr;             // barrier B counter (incremented by peers)
+  std::vector<void*> ipc_opened;                  // peer mappings to close at destroy
   __nv_bfloat16* theta_local_bf16 = nullptr;  // [P_pad] working copy the tensor cores read
   __nv_bfloat16* theta_hat_bf16 = nullptr;    // [P_pad]
   __nv_bfloat16* a2_bf16 = nullptr;           // [2b][2592] conv2 activations (s: theta, s': theta^)
@@ -297,6 +304,10 @@ static void free_all(dqn_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (c->sra.trace) cudaFree(c->sra.trace);
+  if (c->flags) cudaFree(c->flags);
+  if (c->done) cudaFree(c->done);
   if (c->ev_grad) cudaEventDestroy(c->ev_grad);
   for (int i = 0; i < 2; ++i) {
     if (c->ev_gen[i]) cudaEventDestroy(c->ev_gen[i]);
@@ -315,6 +326,71 @@ static int pick_splits(int M, int N, int K, int groups) {
 }
 
 static thread_local std::string g_create_err;
+
+// NEXT-1 setup: export G, theta_local (+bf16), the barrier arrays with CUDA IPC, exchange the
+// handles over the NCCL communicator (one all-gather), map every peer's buffers.
+static int setup_fused_comm(dqn_ctx* ctx) {
+  const int N = ctx->world, me = ctx->rank;
+  int rc;
+  if ((rc = dalloc(ctx, &ctx->flags, kMaxWorld))) return rc;
+  if ((rc = dalloc(ctx, &ctx->done, 1))) return rc;
+  CK(cudaMemset(ctx->flags, 0, sizeof(unsigned long long) * kMaxWorld));
+  CK(cudaMemset(ctx->done, 0, sizeof(unsigned long long)));
+  void* mine[5] = {ctx->grad, ctx->theta_local, ctx->theta_local_bf16, ctx->flags, ctx->done};
+  constexpr int H = (int)sizeof(cudaIpcMemHandle_t);
+  std::vector<char> hbuf(5 * H, 0), all((size_t)N * 5 * H, 0);
+  for (int i = 0; i < 5; ++i)
+    if (mine[i]) CK(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(hbuf.data() + i * H), mine[i]));
+  char* d_all = nullptr;
+  CK(cudaMalloc(&d_all, all.size()));
+  CK(cudaMemcpy(d_all + (size_t)me * 5 * H, hbuf.data(), 5 * H, cudaMemcpyHostToDevice));
+  ncclResult_t nr = ncclAllGather(d_all + (size_t)me * 5 * H, d_all, 5 * H, ncclChar, ctx->comm, ctx->stream);
+  cudaError_t ce = cudaStreamSynchronize(ctx->stream);
+  if (nr == ncclSuccess && ce == cudaSuccess) ce = cudaMemcpy(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost);
+  cudaFree(d_all);
+  if (nr != ncclSuccess) return set_err(ctx, DQN_ENCCL, std::string("handle exchange: ") + ncclGetErrorString(nr));
+  CK(ce);
+  ServerRoundArgs& a = ctx->sra;
+  for (int p = 0; p < N; ++p) {
+    void* ptr[5] = {};
+    for (int i = 0; i < 5; ++i) {
+      if (!mine[i]) continue;
+      if (p == me) {
+        ptr[i] = mine[i];
+      } else {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, all.data() + ((size_t)p * 5 + i) * H, H);
+        CK(cudaIpcOpenMemHandle(&ptr[i], h, cudaIpcMemLazyEnablePeerAccess));
+        ctx->ipc_opened.push_back(ptr[i]);
+      }
+    }
+    a.grad[p] = static_cast<float*>(ptr[0]);
+    a.theta_local[p] = static_cast<float*>(ptr[1]);
+    a.theta_local_bf16[p] = static_cast<__nv_bfloat16*>(ptr[2]);
+    a.flags[p] = static_cast<unsigned long long*>(ptr[3]);
+    a.done[p] = static_cast<unsigned long long*>(ptr[4]);
+  }
+  const dqn_config& c = ctx->cfg;
+  a.world = N; a.rank = me; a.n_push = c.n_push;
+  a.shard = ctx->shard; a.grad_elems = ctx->P_pad;
+  a.my_flags = ctx->flags; a.my_done = ctx->done;
+  a.theta_master = ctx->theta_master; a.rms = ctx->rms;
+  a.inv_div = (float)(1.0 / ((double)N * c.n_push));
+  a.lr = (float)c.lr; a.rho = (float)c.rms_decay; a.omr = (float)(1.0 - c.rms_decay); a.eps = (float)c.rms_eps;
+  a.ctr = ctx->ctr;
+  ctx->acq.done = ctx->done;
+  ctx->acq.per_round = (unsigned long long)N * server_round_blocks(ctx->shard);
+  ctx->acq.n_push = c.n_push;
+  ctx->acq.grad = ctx->grad;
+  ctx->acq.grad_elems = ctx->P_pad;
+  ctx->acq.ctr = ctx->ctr;
+  const char* tr = getenv("DQN_TRACE_COMM");
+  if (tr && atoi(tr)) {
+    if ((rc = dalloc(ctx, &a.trace, 64 * 4))) return rc;
+    CK(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 256));
+  }
+  return DQN_OK;
+}
 
 static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world, const void* nccl_unique_id,
                        void* cuda_stream) {
@@ -470,6 +546,9 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof(id));
     NK(ncclCommInitRank(&ctx->comm, world, id, rank));
+    const char* fe = getenv("DQN_FUSED_COMM");
+    ctx->fused_comm = !ctx->async && cfg->n_fetch == 1 && world <= kMaxWorld && !(fe && atoi(fe) == 0);
+    if (ctx->fused_comm && (rc = setup_fused_comm(ctx))) return rc;
   }
   return DQN_OK;
 }
@@ -590,7 +669,9 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   cudaStream_t st = ctx->stream;
   // a13 fetch + a14 target refresh
   if (fetch) {
-    if (ctx->world > 1) {
+    if (ctx->fused_comm) {
+      // delivered into theta_local by the previous round's fused server-round kernel (NEXT-1)
+    } else if (ctx->world > 1) {
       PB("fetch_all_gather", 0);
       NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
       PE();
@@ -603,6 +684,11 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   if (refresh) {  // right after a fetch (the async mode's fetch is enqueued ahead of the graph)
     PB("target_refresh", 0);
     CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+    PE();
+  }
+  if (ctx->fused_comm) {  // the previous round's deliveries into theta_local, then clear G
+    PB("server_round_acquire", 1);
+    launch_fused_round_acquire(ctx->acq, st);
     PE();
   }
   // a1 sample
@@ -711,7 +797,11 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   if (push) {
     const float div = (float)((double)ctx->world * c.n_push);
     const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
-    if (ctx->world > 1) {
+    if (ctx->fused_comm) {
+      PB("server_round_fused", 1);
+      launch_server_round(ctx->sra, st);
+      PE();
+    } else if (ctx->world > 1) {
       PB("push_reduce_scatter", 0);
       NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
       CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
@@ -745,7 +835,9 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   const ConvShape& L2 = net.conv[1];
   cudaStream_t st = ctx->stream;
   if (fetch) {  // a13 + a14
-    if (ctx->world > 1) {
+    if (ctx->fused_comm) {
+      // delivered into theta_local by the previous round's fused server-round kernel (NEXT-1)
+    } else if (ctx->world > 1) {
       PB("fetch_all_gather", 1);
       NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
       launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
@@ -772,6 +864,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   fa.w1_off = L1.w_off; fa.b1_off = L1.b_off; fa.w2_off = L2.w_off; fa.b2_off = L2.b_off;
   fa.idx = ctx->idx; fa.ctr = ctx->ctr; fa.seed = c.seed; fa.rank = (unsigned)ctx->rank; fa.n = b;
   fa.a2 = ctx->a2_bf16; fa.a1_save = ctx->a1_save;
+  fa.acq = ctx->acq;
   PB("conv_fwd", 1);
   launch_fwd_conv_bf16(fa, 2, st);
   PE();
@@ -836,7 +929,11 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   if (push) {
     const float div = (float)((double)ctx->world * c.n_push);
     const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
-    if (ctx->world > 1) {
+    if (ctx->fused_comm) {
+      PB("server_round_fused", 1);
+      launch_server_round(ctx->sra, st);
+      PE();
+    } else if (ctx->world > 1) {
       PB("push_reduce_scatter", 0);
       NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
       CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
@@ -1053,6 +1150,24 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
                            cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->sra.trace) {  // DQN_TRACE_COMM=1: phases of the fused server round (block 0), last 64 rounds
+    unsigned long long t[256];
+    if (cudaMemcpy(t, ctx->sra.trace, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      double s[3] = {0, 0, 0};
+      int n = 0;
+      for (int r = 0; r < 64; ++r)
+        if (t[r * 4] && t[r * 4 + 3] > t[r * 4]) {
+          for (int q = 0; q < 3; ++q) s[q] += (double)(t[r * 4 + q + 1] - t[r * 4 + q]);
+          ++n;
+        }
+      if (n)
+        fprintf(stderr, "[dqn rank %d] fused round: barrier A %.2f us, reduce+update+deliver %.2f us, barrier B %.2f us\n",
+                ctx->rank, s[0] / n / 1e3, s[1] / n / 1e3, s[2] / n / 1e3);
+      fflush(stderr);
+    }
+  }
+  if (hc.bad_input & 0x80000000u)
+    return set_err(ctx, DQN_ECUDA, "fused server round: peer barrier timed out (ranks out of step?)");
   if (hc.T != (unsigned long long)ctx->T)
     return set_err(ctx, DQN_ECUDA, "device step counters diverged from the host schedule");
   if (hc.nonfinite > 0) ctx->diverged = true;

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdio>
 #include "dqn_internal.h"
+#include "fused_acquire.cuh"
 #include "head_finish.cuh"
 #include "pdl.cuh"
 #include "philox.cuh"
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   expand_state(sX, sU8);  // u8 -> exact bf16 (1/255 folded into the epilogue)
   // everything above overlaps the previous kernel (the update that publishes theta); weights after the wait
   pdl_sync();
+  fused_round_acquire(a.acq);  // N > 1 fused server round: peers' deliveries into theta_local complete
   const __nv_bfloat16* th = a.theta[g];
   stage_w1(sW1, th + a.w1_off);
   stage_w2(sW2, th + a.w2_off);
