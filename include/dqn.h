@@ -162,7 +162,9 @@ int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, float* q, int32
 
 /* Copy a parameter vector (DQN_PARAMS_*) in canonical order into out[cap]
  * (cap >= P, host or device). n_params / generation may be NULL.
- * SERVER and RMS are collective when world > 1. */
+ * SERVER and RMS are collective when world > 1; so is LOCAL on a bf16 context with
+ * world > 1 and the fused server round (DQN_DETERMINISTIC, n_fetch = 1), where the
+ * working copy equals the gathered SERVER vector and is returned as such. */
 int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, int64_t* n_params, uint64_t* generation);
 
 /* Replay occupancy: total pushes so far and min(count, capacity). */

@@ -148,25 +148,27 @@ struct ServerRoundArgs {
   float* grad[kMaxWorld];                       // every rank's G (peer pointers; [rank] is local)
   float* theta_local[kMaxWorld];                // every rank's working theta (fp32)
   __nv_bfloat16* theta_local_bf16[kMaxWorld];   // and its bf16 copy (nullptr on the fp32 path)
+  long long f32_peer_lo, f32_peer_hi;           // theta range read only as bf16: no fp32 copy to peers
   unsigned long long* flags[kMaxWorld];         // every rank's barrier-A array [world]
   unsigned long long* done[kMaxWorld];          // every rank's barrier-B counter
   unsigned long long* my_flags;
   unsigned long long* my_done;
+  unsigned long long* my_join;                  // local gpu-scope join counter of barrier B
   float* theta_master;                          // owned shard
   float* rms;
   float inv_div, lr, rho, omr, eps;
   DevCounters* ctr;
-  unsigned long long* trace;                    // optional [64][4] globaltimer stamps (DQN_TRACE_COMM=1)
+  unsigned long long* trace;                    // optional [64][8] globaltimer stamps (DQN_TRACE_COMM=1)
 };
 void launch_server_round(const ServerRoundArgs& a, cudaStream_t st);
 // the acquire half of the round's second barrier, run at the start of the next step
 struct FusedAcquire {
-  const unsigned long long* done;               // nullptr: no fused round in this context
-  unsigned long long per_round;                 // world * server-round blocks
-  int n_push;
+  const unsigned long long* done;               // this rank's barrier-B counter (rounds * world)
+  int world, n_push;
   float* grad;                                  // this rank's G, cleared once every peer has read it
   long long grad_elems;
-  DevCounters* ctr;
+  DevCounters* ctr;                             // nullptr: no fused round in this context
+  unsigned long long* trace;                    // the server round's trace (slots 6, 7) or nullptr
 };
 void launch_fused_round_acquire(const FusedAcquire& f, cudaStream_t st);
 int server_round_blocks(long long shard);

@@ -72,7 +72,7 @@ struct dqn_ctx {
   // NEXT-1 fused server round over NVLink peer memory (world > 1, deterministic, n_fetch == 1)
   bool fused_comm = false;
   ServerRoundArgs sra{};                          // peer pointers etc., filled at create
-  FusedAcquire acq{};                             // the next step's acquire half (acq.done == nullptr: off)
+  FusedAcquire acq{};                             // the next step's acquire half (acq.ctr == nullptr: off)
   unsigned long long* flags = nullptr;            // [kMaxWorld] barrier A (written by peers)
   unsigned long long* done = nullptr;             // barrier B counter (incremented by peers)
   std::vector<void*> ipc_opened;                  // peer mappings to close at destroy
@@ -101,6 +101,12 @@ struct dqn_ctx {
   // graphs per (fetch, refresh, push) variant; [8..15]: the same with profiling event records
   cudaGraphExec_t graphs[16] = {};
   long long graph_kernels[16] = {};
+  // multi-step graphs: kChunkLog lengths 2^0..2^(kChunkLog-1) of consecutive same-variant steps,
+  // so the programmatic (PDL) edges also span step boundaries (a graph boundary serialises)
+  static constexpr int kChunkLog = 5;
+  cudaGraphExec_t chunk_graphs[8][kChunkLog] = {};
+  long long chunk_kernels[8][kChunkLog] = {};
+  bool chunks_ready = false;
   // profiling (dqn_profile_steps): event pairs around each step region, per graph variant
   struct ProfMark {
     std::string name;
@@ -275,6 +281,9 @@ static int dalloc(dqn_ctx* ctx, T** p, long long n) {
 static void free_all(dqn_ctx* c) {
   for (auto& g : c->graphs)
     if (g) cudaGraphExecDestroy(g);
+  for (auto& row : c->chunk_graphs)
+    for (auto& g : row)
+      if (g) cudaGraphExecDestroy(g);
   for (auto& v : c->marks)
     for (auto& m : v) {
       cudaEventDestroy(m.a);
@@ -333,9 +342,11 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   const int N = ctx->world, me = ctx->rank;
   int rc;
   if ((rc = dalloc(ctx, &ctx->flags, kMaxWorld))) return rc;
-  if ((rc = dalloc(ctx, &ctx->done, 1))) return rc;
+  // done[0]: barrier-B counter (peers add to it), done[1]: the local blocks' join counter
+  const long long n_done = 2;
+  if ((rc = dalloc(ctx, &ctx->done, n_done))) return rc;
   CK(cudaMemset(ctx->flags, 0, sizeof(unsigned long long) * kMaxWorld));
-  CK(cudaMemset(ctx->done, 0, sizeof(unsigned long long)));
+  CK(cudaMemset(ctx->done, 0, sizeof(unsigned long long) * n_done));
   void* mine[5] = {ctx->grad, ctx->theta_local, ctx->theta_local_bf16, ctx->flags, ctx->done};
   constexpr int H = (int)sizeof(cudaIpcMemHandle_t);
   std::vector<char> hbuf(5 * H, 0), all((size_t)N * 5 * H, 0);
@@ -373,21 +384,29 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   const dqn_config& c = ctx->cfg;
   a.world = N; a.rank = me; a.n_push = c.n_push;
   a.shard = ctx->shard; a.grad_elems = ctx->P_pad;
-  a.my_flags = ctx->flags; a.my_done = ctx->done;
+  a.my_flags = ctx->flags; a.my_done = ctx->done; a.my_join = ctx->done + 1;
   a.theta_master = ctx->theta_master; a.rms = ctx->rms;
   a.inv_div = (float)(1.0 / ((double)N * c.n_push));
   a.lr = (float)c.lr; a.rho = (float)c.rms_decay; a.omr = (float)(1.0 - c.rms_decay); a.eps = (float)c.rms_eps;
   a.ctr = ctx->ctr;
+  if (ctx->bf16) {  // the FC weight is read only through theta_local_bf16
+    const FcShape& F = ctx->net.fc[0];
+    a.f32_peer_lo = F.w_off;
+    a.f32_peer_hi = F.w_off + (long long)F.H * F.D;
+  }
   ctx->acq.done = ctx->done;
-  ctx->acq.per_round = (unsigned long long)N * server_round_blocks(ctx->shard);
+  ctx->acq.world = N;
   ctx->acq.n_push = c.n_push;
   ctx->acq.grad = ctx->grad;
   ctx->acq.grad_elems = ctx->P_pad;
   ctx->acq.ctr = ctx->ctr;
   const char* tr = getenv("DQN_TRACE_COMM");
   if (tr && atoi(tr)) {
-    if ((rc = dalloc(ctx, &a.trace, 64 * 4))) return rc;
-    CK(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 256));
+    if ((rc = dalloc(ctx, &a.trace, 64 * 16))) return rc;
+    std::vector<unsigned long long> init(64 * 16, 0);
+    for (int r = 0; r < 64; ++r) init[r * 16 + 4] = ~0ull;  // atomicMin slot
+    CK(cudaMemcpy(a.trace, init.data(), sizeof(unsigned long long) * 64 * 16, cudaMemcpyHostToDevice));
+    ctx->acq.trace = a.trace;
   }
   return DQN_OK;
 }
@@ -851,7 +870,10 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   }
   if (refresh) {
     PB("target_refresh", 0);
-    CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+    if (ctx->fused_comm)  // theta_local's fp32 FC weight holds only this rank's slice (kernels_comm.cu)
+      NK(ncclAllGather(ctx->theta_master, ctx->theta_hat, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
+    else
+      CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(ctx->theta_hat_bf16, ctx->theta_local_bf16, sizeof(__nv_bfloat16) * ctx->P_pad,
                        cudaMemcpyDeviceToDevice, st));
     PE();
@@ -957,34 +979,42 @@ static int enqueue_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   return ctx->bf16 ? enqueue_step_bf16(ctx, fetch, refresh, push) : enqueue_step_f32(ctx, fetch, refresh, push);
 }
 
+// Capture `len` consecutive steps of variant v (bits: 1 fetch, 2 refresh, 4 push, 8 profiling
+// event records) into one graph; *kernels = its kernel nodes.
+static int capture_steps(dqn_ctx* ctx, int v, int len, cudaGraphExec_t* exec, long long* kernels) {
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  ctx->capture_variant = v;
+  int rc = DQN_OK;
+  for (int i = 0; i < len && rc == DQN_OK; ++i) rc = enqueue_step(ctx, v & 1, v & 2, v & 4);
+  ctx->capture_variant = -1;
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (rc) return rc;
+  if (e != cudaSuccess) return set_err(ctx, DQN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  size_t n = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CK(cudaGraphGetNodes(g, nodes.data(), &n));
+  long long nk = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    CK(cudaGraphNodeGetType(nd, &t));
+    if (t == cudaGraphNodeTypeKernel) ++nk;
+  }
+  *kernels = nk;
+  e = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  return DQN_OK;
+}
+
 // Replay the graph of one step variant (captured on first use). profile: the
 // variant with event records around each region. *kernels += kernel nodes run.
 static int run_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push, bool profile, long long* kernels) {
   if (!ctx->use_graphs && !profile) return enqueue_step(ctx, fetch, refresh, push);
   const int v = (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0) | (profile ? 8 : 0);
-  if (!ctx->graphs[v]) {
-    cudaGraph_t g;
-    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    ctx->capture_variant = v;
-    int rc = enqueue_step(ctx, fetch, refresh, push);
-    ctx->capture_variant = -1;
-    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
-    if (rc) return rc;
-    if (e != cudaSuccess) return set_err(ctx, DQN_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    size_t n = 0;
-    CK(cudaGraphGetNodes(g, nullptr, &n));
-    std::vector<cudaGraphNode_t> nodes(n);
-    CK(cudaGraphGetNodes(g, nodes.data(), &n));
-    long long nk = 0;
-    for (auto nd : nodes) {
-      cudaGraphNodeType t;
-      CK(cudaGraphNodeGetType(nd, &t));
-      if (t == cudaGraphNodeTypeKernel) ++nk;
-    }
-    ctx->graph_kernels[v] = nk;
-    CK(cudaGraphInstantiate(&ctx->graphs[v], g, 0));
-    cudaGraphDestroy(g);
-  }
+  int rc;
+  if (!ctx->graphs[v] && (rc = capture_steps(ctx, v, 1, &ctx->graphs[v], &ctx->graph_kernels[v]))) return rc;
   CK(cudaGraphLaunch(ctx->graphs[v], ctx->stream));
   if (kernels) *kernels += ctx->graph_kernels[v];
   return DQN_OK;
@@ -1073,6 +1103,66 @@ static int do_step(dqn_ctx* ctx, bool profile, long long* kernels, bool* out_fet
   return DQN_OK;
 }
 
+// Host schedule of one step of the synchronous modes (do_step without the launch): variant bits.
+static int plan_step(dqn_ctx* ctx) {
+  bool fetch, refresh, push;
+  schedule(ctx, &fetch, &refresh, &push);
+  if (push) ctx->n += 1;
+  ctx->T += 1;
+  return (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0);
+}
+
+static int launch_chunk(dqn_ctx* ctx, int v, int l, long long* kernels) {
+  int rc;
+  cudaGraphExec_t& g = ctx->chunk_graphs[v][l];
+  if (!g && (rc = capture_steps(ctx, v, 1 << l, &g, &ctx->chunk_kernels[v][l]))) return rc;
+  CK(cudaGraphLaunch(g, ctx->stream));
+  *kernels += ctx->chunk_kernels[v][l];
+  return DQN_OK;
+}
+
+// Capture, once, the multi-step graphs the schedule can ask for, so that no capture falls into
+// a caller's timed region (a missing one is still captured on first use).
+static int prepare_chunks(dqn_ctx* ctx) {
+  const dqn_config& c = ctx->cfg;
+  ctx->chunks_ready = true;
+  for (int v = 0; v < 8; ++v) {
+    const bool fetch = v & 1, refresh = v & 2, push = v & 4;
+    if ((refresh && !fetch) || (c.n_fetch == 1 && !fetch) || (c.n_push == 1 && !push)) continue;
+    const int nl = (refresh && c.target_sync > 1) ? 1 : dqn_ctx::kChunkLog;  // refreshes are >= C rounds apart
+    for (int l = 0; l < nl; ++l) {
+      if (ctx->chunk_graphs[v][l]) continue;
+      int rc = capture_steps(ctx, v, 1 << l, &ctx->chunk_graphs[v][l], &ctx->chunk_kernels[v][l]);
+      if (rc) return rc;
+    }
+  }
+  return DQN_OK;
+}
+
+// k steps of a synchronous mode as runs of same-variant steps, each run replayed as
+// power-of-two multi-step graphs (the kernels of consecutive steps then overlap via PDL).
+static int run_steps_chunked(dqn_ctx* ctx, long long k, long long* kernels) {
+  int rc;
+  if (!ctx->chunks_ready && (rc = prepare_chunks(ctx))) return rc;
+  const int max_len = 1 << (dqn_ctx::kChunkLog - 1);
+  for (long long s = 0; s < k;) {
+    const int v = plan_step(ctx);
+    int len = 1;
+    while (len < max_len && s + len < k) {
+      const long long saved[4] = {ctx->T, ctx->n, ctx->n_local, ctx->ell};
+      if (plan_step(ctx) != v) {
+        ctx->T = saved[0]; ctx->n = saved[1]; ctx->n_local = saved[2]; ctx->ell = saved[3];
+        break;
+      }
+      ++len;
+    }
+    for (int l = dqn_ctx::kChunkLog - 1; l >= 0; --l)
+      if ((len >> l) & 1 && (rc = launch_chunk(ctx, v, l, kernels))) return rc;
+    s += len;
+  }
+  return DQN_OK;
+}
+
 extern "C" int dqn_profile_steps(dqn_ctx* ctx, int64_t k, dqn_region_time* out, int32_t cap, int32_t* n_regions) {
   if (!ctx) return DQN_EINVAL;
   if (ctx->poisoned) return DQN_ESTATE;
@@ -1122,10 +1212,15 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
   const long long T0 = ctx->T;
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   long long kernels = 0;
-  for (long long s = 0; s < k; ++s) {
-    // O10 / O11: fetch at the start of step T when T % n_fetch == 0, then refresh theta^ when n - l >= C
-    int rc = do_step(ctx, false, &kernels, nullptr, nullptr, nullptr);
+  if (ctx->use_graphs && !ctx->async) {
+    int rc = run_steps_chunked(ctx, k, &kernels);
     if (rc) return rc;
+  } else {
+    for (long long s = 0; s < k; ++s) {
+      // O10 / O11: fetch at the start of step T when T % n_fetch == 0, then refresh theta^ when n - l >= C
+      int rc = do_step(ctx, false, &kernels, nullptr, nullptr, nullptr);
+      if (rc) return rc;
+    }
   }
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   DevCounters hc;
@@ -1151,18 +1246,38 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
   }
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->sra.trace) {  // DQN_TRACE_COMM=1: phases of the fused server round (block 0), last 64 rounds
-    unsigned long long t[256];
+    unsigned long long t[1024];
     if (cudaMemcpy(t, ctx->sra.trace, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
-      double s[3] = {0, 0, 0};
+      // intervals: barrier A, work, release (block 0); first block start -> last release;
+      // block 0 release -> next step past pdl_sync; acquire spin
+      double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
       int n = 0;
-      for (int r = 0; r < 64; ++r)
-        if (t[r * 4] && t[r * 4 + 3] > t[r * 4]) {
-          for (int q = 0; q < 3; ++q) s[q] += (double)(t[r * 4 + q + 1] - t[r * 4 + q]);
-          ++n;
+      for (int r = 0; r < 63; ++r) {  // skip the newest slot (its next-step stamps are not there yet)
+        const unsigned long long* q = t + r * 16;
+        if (!q[0] || q[3] <= q[0] || !q[7] || q[6] < q[3] || q[4] == ~0ull) continue;
+        s[0] += (double)(q[1] - q[0]); s[1] += (double)(q[2] - q[1]); s[2] += (double)(q[3] - q[2]);
+        s[3] += (double)(q[5] - q[4]); s[4] += (double)(q[6] - q[3]); s[5] += (double)(q[7] - q[6]);
+        if (q[8] && q[10]) {  // the next step's first kernel (bf16): entry, gather landed, past pdl_sync
+          s[6] += (double)q[8] - (double)q[5]; s[7] += (double)(q[9] - q[8]); s[8] += (double)(q[10] - q[9]);
+        }
+        ++n;
+      }
+      if (getenv("DQN_TRACE_RAW"))
+        for (int r = 0; r < 64; ++r) {
+          const unsigned long long* q = t + r * 16;
+          fprintf(stderr, "[dqn rank %d] slot %d:", ctx->rank, r);
+          for (int k = 0; k < 8; ++k) fprintf(stderr, " %lld", (long long)(q[k] - q[0]));
+          fprintf(stderr, "\n");
         }
       if (n)
-        fprintf(stderr, "[dqn rank %d] fused round: barrier A %.2f us, reduce+update+deliver %.2f us, barrier B %.2f us\n",
-                ctx->rank, s[0] / n / 1e3, s[1] / n / 1e3, s[2] / n / 1e3);
+        fprintf(stderr,
+                "[dqn rank %d] fused round (%d rounds): barrier A %.2f us, reduce+update+deliver %.2f us, release %.2f us;"
+                " all blocks %.2f us; release -> next kernel %.2f us; acquire %.2f us\n",
+                ctx->rank, n, s[0] / n / 1e3, s[1] / n / 1e3, s[2] / n / 1e3, s[3] / n / 1e3, s[4] / n / 1e3,
+                s[5] / n / 1e3);
+      if (n && ctx->bf16)
+        fprintf(stderr, "[dqn rank %d] next fwd: entry - last round block %.2f us, gather %.2f us, expand+pdl_sync %.2f us\n",
+                ctx->rank, s[6] / n / 1e3, s[7] / n / 1e3, s[8] / n / 1e3);
       fflush(stderr);
     }
   }
@@ -1280,9 +1395,17 @@ extern "C" int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, 
   const cudaMemcpyKind kind = is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   const float* src = nullptr;
   switch (which) {
+    case DQN_PARAMS_LOCAL:
+      if (!(ctx->fused_comm && ctx->bf16)) {
+        src = ctx->theta_local;
+        break;
+      }
+      // fused bf16 round: theta_local's fp32 FC weight holds only this rank's slice, and with
+      // n_fetch = 1 the working copy equals the gathered server parameters
+      [[fallthrough]];
     case DQN_PARAMS_SERVER:
     case DQN_PARAMS_RMS: {
-      float* shard = which == DQN_PARAMS_SERVER ? ctx->theta_master : ctx->rms;
+      float* shard = which == DQN_PARAMS_RMS ? ctx->rms : ctx->theta_master;
       if (ctx->async) {  // let the round in flight finish; the server state lives on the comm stream
         CK(cudaStreamSynchronize(ctx->stream));
         CK(cudaStreamSynchronize(ctx->comm_stream));
@@ -1297,7 +1420,6 @@ extern "C" int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, 
       }
       break;
     }
-    case DQN_PARAMS_LOCAL: src = ctx->theta_local; break;
     case DQN_PARAMS_TARGET: src = ctx->theta_hat; break;
     case DQN_PARAMS_GRAD:
       if (!ctx->grad_snap) return set_err(ctx, DQN_EINVAL, "gradient snapshots need DQN_KEEP_GRAD=1 at create");

@@ -8,36 +8,45 @@ namespace dqn {
 
 constexpr long long kSpinLimit = 1LL << 26;  // ~ seconds with the nanosleep back-off
 
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// poll until *p >= want (acquire, system scope); bounded: a timeout sets the error bit and returns
+__device__ __forceinline__ void spin_acquire_sys(const unsigned long long* p, unsigned long long want,
+                                                 DevCounters* ctr) {
+  long long spin = 0;
+  while (ld_acquire_sys(p) < want) {
+    __nanosleep(32);
+    if (++spin > kSpinLimit) {
+      atomicOr(&ctr->bad_input, 0x80000000u);  // peer barrier timeout (reported as ECUDA by the host)
+      return;
+    }
+  }
 }
 
-// If the previous step ran a server round: wait until every block of every rank has
-// released its deliveries into this rank's theta_local (done >= rounds * N * blocks), then
-// clear this rank's G (every peer read its slice before releasing). Call after pdl_wait()
-// and before touching theta_local or G. Bounded spin; a timeout is reported, not hung on.
+// If the previous step ran a server round: wait until every rank's last block has released
+// its deliveries into this rank's theta_local (done >= rounds * N), then clear this rank's G
+// (every peer read its slice before releasing). Call after pdl_wait() and before touching
+// theta_local or G (and before pdl_trigger(): the successor reads theta before its own wait).
 __device__ __forceinline__ void fused_round_acquire(const FusedAcquire& f) {
-  if (f.done == nullptr) return;
+  if (f.ctr == nullptr) return;  // no fused round in this context
   const unsigned long long T = f.ctr->T;
   if (T == 0 || T % (unsigned long long)f.n_push != 0) return;  // the previous step did not push
-  const unsigned long long expect = (T / (unsigned long long)f.n_push) * f.per_round;
+  const unsigned long long rounds = T / (unsigned long long)f.n_push;
+  unsigned long long* tr = nullptr;
+  if (f.trace && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+    tr = f.trace + (rounds % 64) * 16;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[6]));
+  }
   if (threadIdx.x == 0) {
-    long long spin = 0;
-    while (ld_acquire_sys(f.done) < expect) {
-      __nanosleep(32);
-      if (++spin > kSpinLimit) {
-        atomicOr(&f.ctr->bad_input, 0x80000000u);
-        break;
-      }
-    }
+    spin_acquire_sys(f.done, rounds * (unsigned long long)f.world, f.ctr);
+    if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[7]));
   }
   __syncthreads();
   const long long g4 = f.grad_elems / 4;

@@ -30,8 +30,7 @@ namespace mnih {
 // conv1: 4x84x84 -> s2d(4) 21x21x64 -> 2x2/1 -> 20x20x16
 constexpr int X_W = 21, X_PIX = 441, X_ALLOC = 544, C1 = 16, M1V = 420, M1_TILES = 4;
 // conv2: 16x20x20 -> s2d(2) 10x10x64 -> 2x2/1 -> 9x9x32
-constexpr int A1_W = 10, A1_PIX = 100, A1_ALLOC = 144, C2 = 32, M2V = 90;
-constexpr int K = 256;      // 4 taps x 64 channels for both convolutions
+constexpr int A1_W = 10, A1_PIX = 100, A1_ALLOC = 144, C2 = 32, M2V = 90;  // K = 4 taps x 64 ch = 256 for both
 constexpr int D = 2592;     // 32 x 9 x 9 flattened (C,H,W)
 constexpr int SLOT = 28224; // bytes of one u8 s2d state
 __device__ __forceinline__ int tap_shift1(int t) { return (t >> 1) * X_W + (t & 1); }
@@ -183,6 +182,11 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   uint8_t* sW1 = smem + FWD_SW1;
   uint8_t* sW2 = smem + FWD_SW2;
   uint8_t* sU8 = smem + FWD_SU8;
+  unsigned long long* tr = nullptr;  // DQN_TRACE_COMM stamps (slots 8-10 of the previous round)
+  if (a.acq.trace && j == 0 && g == 0 && threadIdx.x == 0 && a.acq.ctr->T % a.acq.n_push == 0) {
+    tr = a.acq.trace + ((a.acq.ctr->T / a.acq.n_push) % 64) * 16;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[8]));
+  }
   if (threadIdx.x == 0) {
     long long slot = j;
     if (a.ctr) slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)j, a.ctr->ring_size);  // a1
@@ -197,10 +201,13 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   if (warp == 0) tmem_alloc(&tbase, 128);
   __syncthreads();  // barriers initialised before anyone waits on them
   mbar_wait(&bar_ld, 0);
+  if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[9]));
   expand_state(sX, sU8);  // u8 -> exact bf16 (1/255 folded into the epilogue)
   // everything above overlaps the previous kernel (the update that publishes theta); weights after the wait
-  pdl_sync();
+  pdl_wait();
+  if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[10]));
   fused_round_acquire(a.acq);  // N > 1 fused server round: peers' deliveries into theta_local complete
+  pdl_trigger();               // only now: the FC forward reads the delivered weights before its wait
   const __nv_bfloat16* th = a.theta[g];
   stage_w1(sW1, th + a.w1_off);
   stage_w2(sW2, th + a.w2_off);

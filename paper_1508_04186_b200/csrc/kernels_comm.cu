@@ -6,16 +6,23 @@
 //            in rank order p = 0..N-1 (deterministic; the oracle sums in rank order too)
 //   update : mean over N*n_push, RMSProp on the owned shard (A4/A5/A7/A24)
 //   fetch  : the updated shard is stored straight into every replica's working copy
-//            theta_local (fp32 and, on the bf16 path, bf16) on every peer
+//            theta_local (fp32 and, on the bf16 path, bf16) on every peer; on the bf16 path
+//            the FC weight (98% of P) is read only as bf16, so its fp32 copy stays local
+//            (theta_hat's fp32 copy and dqn_get_params gather it from the masters instead)
 //
 // replacing ncclReduceScatter + update kernel + ncclAllGather (+ the bf16 conversion).
-// Two cross-GPU barriers with monotone counters (no reset, graph-replayable):
-//   A (gradients complete): each rank stores `round` into flags[rank] on every peer
-//     (release, system scope) and waits until all N entries of its own flags reach it;
-//   B (shards delivered): every block adds 1 to done[] on every peer after its remote
-//     stores (release). The acquire half (done >= rounds * N * blocks, then clear G — all
-//     peers have read it by then) runs in the next step's first kernel
-//     (fused_acquire.cuh), so stragglers overlap the next forward's replay gather.
+// Two cross-GPU barriers with monotone counters (no reset, graph-replayable), built so that
+// each rank issues ONE system-scope release per barrier (a system-scope fence costs
+// microseconds and serialises when hundreds of CTAs issue it; measured in DESIGN.md):
+//   A (gradients complete): block 0 fences (acq_rel, system scope) — G was completed by
+//     the preceding kernels — and stores `T` into flags[rank] on every peer (relaxed);
+//     every block polls its own flags with ld.acquire.sys until all N entries reach T;
+//   B (shards delivered): the blocks join on a local counter at gpu scope (acq_rel RMW);
+//     the last block to join fences at system scope and adds 1 to done[] on every peer:
+//     by cumulativity every block's peer stores happen-before that add. The acquire half
+//     (ld.acquire.sys polling until done >= rounds * N, then clear G — all peers have read
+//     it by then) runs in the next step's first kernel (fused_acquire.cuh), so it overlaps
+//     the next forward's replay gather.
 // Every spin is bounded; on timeout the kernel records an error and falls through, so
 // a desynchronised group cannot hang the GPU.
 #include <algorithm>
@@ -30,8 +37,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// trace slots per round: 0-3 block 0 after pdl_wait / barrier A / work / release, 4 earliest
+// block start, 5 latest block release, 6-7 next step's first kernel after pdl_wait / acquire,
+// 8-10 next forward's entry / replay gather landed / past pdl_wait
 #define TRACE(k) \
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[(round_idx % 64) * 4 + (k)] = gtimer()
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[(round_idx % 64) * 16 + (k)] = gtimer()
 
 __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   pdl_wait();     // G of this rank is complete (the backward kernels precede in stream order)
@@ -41,22 +51,15 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   const unsigned long long T = a.ctr->T;
   const unsigned long long round_idx = T / (unsigned long long)a.n_push;
   TRACE(0);
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[((round_idx + 1) % 64) * 16 + 4] = ~0ull;
+  if (a.trace && threadIdx.x == 0) atomicMin(a.trace + (round_idx % 64) * 16 + 4, gtimer());
   // ---- barrier A
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
-      __threadfence_system();
-      for (int p = 0; p < a.world; ++p) st_release_sys(a.flags[p] + a.rank, T);
+      fence_acq_rel_sys();
+      for (int p = 0; p < a.world; ++p) st_relaxed_sys(a.flags[p] + a.rank, T);
     }
-    for (int p = 0; p < a.world; ++p) {
-      long long spin = 0;
-      while (ld_acquire_sys(a.my_flags + p) < T) {
-        __nanosleep(32);
-        if (++spin > kSpinLimit) {
-          atomicOr(&a.ctr->bad_input, 0x80000000u);  // peer barrier timeout (reported as ECUDA by the host)
-          break;
-        }
-      }
-    }
+    for (int p = 0; p < a.world; ++p) spin_acquire_sys(a.my_flags + p, T, a.ctr);
   }
   __syncthreads();
   TRACE(1);
@@ -98,25 +101,36 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
       h.x = *reinterpret_cast<uint32_t*>(&lo);
       h.y = *reinterpret_cast<uint32_t*>(&hi);
     }
+    const long long e = base + 4 * i;
+    const bool f32_all = e < a.f32_peer_lo || e + 4 > a.f32_peer_hi;
     for (int p = 0; p < a.world; ++p) {
-      reinterpret_cast<float4*>(a.theta_local[p] + base)[i] = t4;
+      if (p == a.rank || f32_all) reinterpret_cast<float4*>(a.theta_local[p] + base)[i] = t4;
       if (a.theta_local_bf16[p]) reinterpret_cast<uint2*>(a.theta_local_bf16[p] + base)[i] = h;
     }
   }
   if (bad) atomicAdd(&a.ctr->nonfinite, bad);
-  // ---- barrier B, release half: the CTA barrier orders every thread's remote stores before
-  // thread 0's system-scope release, which is cumulative (no per-thread system fence needed)
+  // ---- barrier B, release half: the CTA barrier orders every thread's stores before thread 0's
+  // gpu-scope release into the join counter; the last block releases once at system scope
   __syncthreads();
   TRACE(2);
-  if (threadIdx.x == 0)
-    for (int p = 0; p < a.world; ++p) red_release_sys_add(a.done[p], 1ull);
+  if (threadIdx.x == 0) {
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(a.my_join), "l"(1ull) : "memory");
+    if (old == round_idx * (unsigned long long)gridDim.x - 1) {
+      fence_acq_rel_sys();
+      for (int p = 0; p < a.world; ++p)
+        asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(a.done[p]), "l"(1ull) : "memory");
+    }
+  }
   TRACE(3);
+  if (a.trace && threadIdx.x == 0) atomicMax(a.trace + (round_idx % 64) * 16 + 5, gtimer());
 }
 
 // fp32 path: the acquire half as its own (tiny) kernel at the start of a step
 __global__ void fused_round_acquire_kernel(FusedAcquire f) {
-  pdl_sync();
+  pdl_wait();
   fused_round_acquire(f);
+  pdl_trigger();
 }
 
 void launch_fused_round_acquire(const FusedAcquire& f, cudaStream_t st) {
