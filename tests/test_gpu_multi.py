@@ -82,3 +82,36 @@ def test_two_replicas_async_fp32_match_lag1_twin(tmp_path):
     assert per_tensor_rel(res["theta"], ref["theta"], on) < 1e-5
     # rank 0's histogram counts its own replica steps; the oracle's counts both replicas
     assert np.array_equal(res["staleness"] * 2, ref["staleness"])
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_many_replicas_fp32_match_oracle(tmp_path, world):
+    """N = 4 / 8 (skipped on smaller boxes): the fused server round (NEXT-1) with every rank owning
+    1/N of theta, against the oracle's N-replica lock-step run."""
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    res = run_ranks(world, tmp_path, "--tiny", "--n-push", "1", "--n-fetch", "1", "--target-sync", "2", "--steps", "5")
+    dc, on, oc = nets(minibatch=16, replay_capacity=200, target_sync=2, lr=1e-3, **TINY_KW)
+    oc.n_replicas = world
+    reps = [replay(on, 250, 100 + k)[0] for k in range(world)]
+    ref = O.run(on, oc, 200, reps, he_theta(on, 3).astype(np.float64), 5)
+    assert int(res["n"]) == ref["n"]
+    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
+    assert per_tensor_rel(res["theta"], ref["theta"], on) < 1e-5
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_many_replicas_bf16_mnih(tmp_path, world):
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from tests.test_gpu_parity_bf16 import rel_l2_per_tensor, smooth_theta
+    res = run_ranks(world, tmp_path, "--precision", "bf16", "--b", "32", "--steps", "3", "--smooth", "--lr", "1e-4")
+    dc, on, oc = nets(minibatch=32, replay_capacity=200, lr=1e-4, target_sync=2)
+    oc.n_replicas = world
+    reps = [replay(on, 250, 100 + k)[0] for k in range(world)]
+    th0 = smooth_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 3)
+    assert int(res["n"]) == ref["n"]
+    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
+    assert per_tensor_rel(res["theta"], ref["theta"], on) < 2e-2
+    assert rel_l2_per_tensor(res["theta"] - th0, ref["theta"] - th0, on) < 0.1
