@@ -334,6 +334,9 @@ def main():
     ha = torch.zeros(ne, dtype=torch.int32).pin_memory()
     hr = torch.zeros(ne, dtype=torch.float32).pin_memory()
     ht = torch.zeros(ne, dtype=torch.uint8).pin_memory()
+    for i in range(min(3, ne)):  # untimed warm-up of the host-push path
+        dqn.push(hs[i:i + 1], ha[i:i + 1], hr[i:i + 1], hsn[i:i + 1], ht[i:i + 1])
+        dqn.train(1, want_loss=True)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -136,7 +136,12 @@ int dqn_create(const dqn_config* cfg, int rank, int world, const void* nccl_uniq
  * n transitions, oldest first: s and s_next [n][F][H][W] u8 (frames oldest
  * first), a [n] in [0, n_actions), r [n] finite, terminal [n] (0/1).
  * Push i goes to slot (count + i) mod capacity (FIFO last-N).
- * DQN_EINVAL (nothing stored) on an out-of-range action or non-finite reward. */
+ * DQN_EINVAL (nothing stored) on an out-of-range action or non-finite reward.
+ * Host buffers are validated on the host and packed into library-owned pinned
+ * staging before the call returns (the caller may reuse them at once); the copy
+ * to the device and the ring write are then ordered on the context's stream
+ * without a host sync. Device buffers are validated on the device and the call
+ * synchronises the stream before returning. */
 int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a, const float* r,
                          const uint8_t* s_next, const uint8_t* terminal);
 

@@ -117,7 +117,8 @@ void launch_validate_push(const int32_t* a, const float* r, long long n, int A, 
 void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
                            long long cap, long long count0, long long n_total, long long first, long long n,
                            long long state_bytes, const uint8_t* s, const int32_t* a, const float* r,
-                           const uint8_t* sn, const uint8_t* t, cudaStream_t st);
+                           const uint8_t* sn, const uint8_t* t, cudaStream_t st, long long* ring_size_out = nullptr,
+                           long long ring_size = 0);
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
                     cudaStream_t st);
@@ -230,7 +231,8 @@ constexpr int kBwdPart = 256 * 16 + 256 * 32 + 16 + 32;
 void init_bf16_kernel_attrs();
 void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t, long long cap,
                      long long count0, long long first, long long n, const uint8_t* s, const int32_t* a,
-                     const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st);
+                     const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st,
+                     long long* ring_size_out = nullptr, long long ring_size = 0);
 void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st);
 void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st);
 // one launch: the tiles of GEMM p0, the tiles of GEMM p1 (single split, group 0 each), then the

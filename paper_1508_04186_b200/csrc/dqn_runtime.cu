@@ -92,10 +92,18 @@ struct dqn_ctx {
   float* q_out = nullptr;
   int* q_amax = nullptr;
   // push staging (host inputs)
-  uint8_t *push_s = nullptr, *push_sn = nullptr, *push_t = nullptr;
-  int32_t* push_a = nullptr;
-  float* push_r = nullptr;
+  // host-buffer pushes: inputs packed into one of two pinned staging buffers, one H2D copy per
+  // chunk into d_stage, the ring kernel; no host sync (the inputs are consumed by the pack)
+  uint8_t* d_stage = nullptr;  // push_chunk transitions (~4 MB), allocated at create
+  uint8_t* h_stage[2] = {};
+  cudaEvent_t ev_stage[2] = {};
+  int stage_flip = 0;
   long long push_chunk = 0;
+  // pinned landing zone of dqn_train_steps' per-call outputs
+  struct HostOut {
+    DevCounters ctr;
+    float loss[kDiagSteps];
+  }* h_out = nullptr;
   // host mirrors of the deterministic schedule (identical on every rank)
   long long T = 0, n = 0, n_local = 0, ell = 0;
   // graphs per (fetch, refresh, push) variant; [8..15]: the same with profiling event records
@@ -291,11 +299,16 @@ static void free_all(dqn_ctx* c) {
     }
   void* ptrs[] = {c->ring_s, c->ring_sn, c->ring_t, c->ring_a, c->ring_r, c->rms, c->grad, c->g_shard,
                   c->theta_hat, c->grad_snap, c->gather_tmp, c->partial, c->idx, c->ctr, c->diag_loss,
-                  c->diag_idx, c->diag_amax, c->head_dq, c->head_act, c->head_loss, c->q_stage, c->q_out, c->q_amax, c->push_s, c->push_sn, c->push_t,
-                  c->push_a, c->push_r, c->theta_local_bf16, c->theta_hat_bf16, c->a2_bf16, c->a1_save,
+                  c->diag_idx, c->diag_amax, c->head_dq, c->head_act, c->head_loss, c->q_stage, c->q_out, c->q_amax, c->d_stage,
+                  c->theta_local_bf16, c->theta_hat_bf16, c->a2_bf16, c->a1_save,
                   c->dh_bf16, c->dz2_bf16, c->fc_partial, c->tc_counters, c->bwd_partial, c->q_stage_s2d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (int i = 0; i < 2; ++i) {
+    if (c->h_stage[i]) cudaFreeHost(c->h_stage[i]);
+    if (c->ev_stage[i]) cudaEventDestroy(c->ev_stage[i]);
+  }
+  if (c->h_out) cudaFreeHost(c->h_out);
   if (c->theta_local && !c->alias_local) cudaFree(c->theta_local);
   if (c->theta_master) cudaFree(c->theta_master);
   for (int i = 0; i < kMaxConv; ++i) {
@@ -411,6 +424,8 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   return DQN_OK;
 }
 
+static long long align16(long long x) { return (x + 15) & ~15LL; }
+
 static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world, const void* nccl_unique_id,
                        void* cuda_stream) {
   ctx->cfg = *cfg;
@@ -438,6 +453,17 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   } else {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault));  // blocking: ordered after legacy-stream producers
     ctx->own_stream = true;
+  }
+  {  // host-push staging (pinned, double-buffered) and the pinned landing zone of train outputs
+    const long long sb = ctx->net.state_bytes;
+    ctx->push_chunk = std::min<long long>(ctx->cap, std::max<long long>(1, (4LL << 20) / (2 * sb + 12)));
+    const long long bytes = align16(2 * ctx->push_chunk * sb) + 3 * align16(4 * ctx->push_chunk);
+    if ((rc = dalloc(ctx, &ctx->d_stage, bytes))) return rc;
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage[i]), bytes, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&ctx->ev_stage[i], cudaEventDisableTiming));
+    }
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_out), sizeof(dqn_ctx::HostOut), cudaHostAllocDefault));
   }
   CK(cudaEventCreate(&ctx->ev0));
   CK(cudaEventCreate(&ctx->ev1));
@@ -597,15 +623,21 @@ extern "C" int dqn_create(const dqn_config* cfg, int rank, int world, const void
 // ------------------------------------------------------------------ push (Alg. 1 "Store")
 // Items [i0, i0+m) of the call (device pointers to their first element) go to slots
 // (count + i0 + i) mod cap; the bf16 path stores conv1's space-to-depth layout.
+// items [i0, i0 + m) of this call into their ring slots; the kernel also publishes the replay
+// size after them (min(count, cap), read by the sampler)
 static void push_ring(dqn_ctx* ctx, long long i0, long long m, const uint8_t* s, const int32_t* a, const float* r,
                       const uint8_t* sn, const uint8_t* t) {
+  const long long size = std::min(ctx->count + i0 + m, ctx->cap);
+  long long* size_out = &ctx->ctr->ring_size;
   if (ctx->bf16)
     launch_push_s2d(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, i0, m, s,
-                    a, r, sn, t, ctx->stream);
+                    a, r, sn, t, ctx->stream, size_out, size);
   else
     launch_push_canonical(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, 0,
-                          i0, m, ctx->net.state_bytes, s, a, r, sn, t, ctx->stream);
+                          i0, m, ctx->net.state_bytes, s, a, r, sn, t, ctx->stream, size_out, size);
 }
+
+
 extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a, const float* r,
                                     const uint8_t* s_next, const uint8_t* terminal) {
   if (!ctx) return DQN_EINVAL;
@@ -623,26 +655,28 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
     for (long long i = 0; i < n; ++i)
       if (a[i] < 0 || a[i] >= ctx->net.A || !std::isfinite(r[i]))
         return set_err(ctx, DQN_EINVAL, "action out of range or non-finite reward at item " + std::to_string(i));
-    if (!ctx->push_s) {
-      ctx->push_chunk = std::min<long long>(ctx->cap, std::max<long long>(1, (256LL << 20) / (2 * sb)));
-      int rc;
-      if ((rc = dalloc(ctx, &ctx->push_s, ctx->push_chunk * sb))) return rc;
-      if ((rc = dalloc(ctx, &ctx->push_sn, ctx->push_chunk * sb))) return rc;
-      if ((rc = dalloc(ctx, &ctx->push_t, ctx->push_chunk))) return rc;
-      if ((rc = dalloc(ctx, &ctx->push_a, ctx->push_chunk))) return rc;
-      if ((rc = dalloc(ctx, &ctx->push_r, ctx->push_chunk))) return rc;
-    }
+    // chunk layout (host pinned and device): s [m][sb] | s' [m][sb] | a [m] i32 | r [m] f32 | term [m] u8
     for (long long i0 = first; i0 < n; i0 += ctx->push_chunk) {
       const long long m = std::min(ctx->push_chunk, n - i0);
-      CK(cudaMemcpyAsync(ctx->push_s, s + i0 * sb, m * sb, cudaMemcpyHostToDevice, ctx->stream));
-      CK(cudaMemcpyAsync(ctx->push_sn, s_next + i0 * sb, m * sb, cudaMemcpyHostToDevice, ctx->stream));
-      CK(cudaMemcpyAsync(ctx->push_a, a + i0, m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
-      CK(cudaMemcpyAsync(ctx->push_r, r + i0, m * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
-      CK(cudaMemcpyAsync(ctx->push_t, terminal + i0, m, cudaMemcpyHostToDevice, ctx->stream));
-      push_ring(ctx, i0, m, ctx->push_s, ctx->push_a, ctx->push_r, ctx->push_sn, ctx->push_t);
+      const long long o_sn = m * sb, o_a = align16(2 * m * sb), o_r = o_a + align16(4 * m), o_t = o_r + align16(4 * m);
+      const int buf = ctx->stage_flip;
+      ctx->stage_flip ^= 1;
+      CK(cudaEventSynchronize(ctx->ev_stage[buf]));  // its previous H2D copy has drained
+      uint8_t* h = ctx->h_stage[buf];
+      std::memcpy(h, s + i0 * sb, m * sb);
+      std::memcpy(h + o_sn, s_next + i0 * sb, m * sb);
+      std::memcpy(h + o_a, a + i0, m * sizeof(int32_t));
+      std::memcpy(h + o_r, r + i0, m * sizeof(float));
+      std::memcpy(h + o_t, terminal + i0, m);
+      CK(cudaMemcpyAsync(ctx->d_stage, h, o_t + m, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaEventRecord(ctx->ev_stage[buf], ctx->stream));
+      uint8_t* d = ctx->d_stage;
+      push_ring(ctx, i0, m, d, reinterpret_cast<const int32_t*>(d + o_a), reinterpret_cast<const float*>(d + o_r),
+                d + o_sn, d + o_t);
       CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(ctx->stream));  // staging is reused by the next chunk
     }
+    ctx->count += n;  // enqueued: the sampler of any later step reads the published size in stream order
+    return DQN_OK;
   } else {
     CK(cudaMemsetAsync(&ctx->ctr->bad_input, 0, sizeof(unsigned), ctx->stream));
     launch_validate_push(a, r, n, ctx->net.A, ctx->ctr, ctx->stream);
@@ -657,9 +691,7 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
     }
   }
   ctx->count += n;
-  const long long size = std::min(ctx->count, ctx->cap);
-  CK(cudaMemcpyAsync(&ctx->ctr->ring_size, &size, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // device inputs: read by the ring kernel before returning
   return DQN_OK;
 }
 
@@ -1223,16 +1255,15 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
     }
   }
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
-  DevCounters hc;
-  CK(cudaMemcpyAsync(&hc, ctx->ctr, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+  dqn_ctx::HostOut* ho = ctx->h_out;
+  CK(cudaMemcpyAsync(&ho->ctr, ctx->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, ctx->stream));
   std::vector<float> loss;
   const bool diag_ok = k > 0 && k <= kDiagSteps;
-  if (diag_ok) {
-    loss.resize(k);
-    for (long long s = 0; s < k; ++s) {
-      const long long slot = (T0 + s) % kDiagSteps;
-      CK(cudaMemcpyAsync(&loss[s], ctx->diag_loss + slot, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-    }
+  if (diag_ok) {  // the k loss slots of the ring: at most two contiguous pieces
+    const long long s0 = T0 % kDiagSteps, n0 = std::min<long long>(k, kDiagSteps - s0);
+    CK(cudaMemcpyAsync(ho->loss, ctx->diag_loss + s0, sizeof(float) * n0, cudaMemcpyDeviceToHost, ctx->stream));
+    if (k > n0)
+      CK(cudaMemcpyAsync(ho->loss + n0, ctx->diag_loss, sizeof(float) * (k - n0), cudaMemcpyDeviceToHost, ctx->stream));
     if (stats && stats->sampled_idx)
       for (long long s = 0; s < k; ++s)
         CK(cudaMemcpyAsync(stats->sampled_idx + s * c.minibatch,
@@ -1245,6 +1276,8 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
                            cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
+  const DevCounters hc = ho->ctr;
+  if (diag_ok) loss.assign(ho->loss, ho->loss + k);
   if (ctx->sra.trace) {  // DQN_TRACE_COMM=1: phases of the fused server round (block 0), last 64 rounds
     unsigned long long t[1024];
     if (cudaMemcpy(t, ctx->sra.trace, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {

@@ -44,8 +44,10 @@ static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b)
 // One thread writes one 16-byte vector (pixel p, frame f): four 4-byte rows of the 4x4 block.
 __global__ void push_s2d_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
                                 long long cap, long long count0, long long first, const uint8_t* s,
-                                const int32_t* a, const float* r, const uint8_t* sn, const uint8_t* t) {
+                                const int32_t* a, const float* r, const uint8_t* sn, const uint8_t* t,
+                                long long* ring_size_out, long long ring_size) {
   const long long i = blockIdx.y;
+  if (ring_size_out && i == 0 && blockIdx.x == 0 && threadIdx.x == 0) *ring_size_out = ring_size;
   const long long slot = (count0 + first + i) % cap;
   const int v = blockIdx.x * blockDim.x + threadIdx.x;  // (pixel, frame)
   if (v < mnih::X_PIX * 4) {
@@ -73,10 +75,12 @@ __global__ void push_s2d_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring
 
 void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t, long long cap,
                      long long count0, long long first, long long n, const uint8_t* s, const int32_t* a,
-                     const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st) {
+                     const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st, long long* ring_size_out,
+                     long long ring_size) {
   if (n <= 0) return;
   dim3 grid(cdiv(mnih::X_PIX * 4, 256), (unsigned)n);
-  push_s2d_kernel<<<grid, 256, 0, st>>>(ring_s, ring_sn, ring_a, ring_r, ring_t, cap, count0, first, s, a, r, sn, t);
+  push_s2d_kernel<<<grid, 256, 0, st>>>(ring_s, ring_sn, ring_a, ring_r, ring_t, cap, count0, first, s, a, r, sn, t,
+                                        ring_size_out, ring_size);
 }
 
 // ------------------------------------------------------------------ shared helpers

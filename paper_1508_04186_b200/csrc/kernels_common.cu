@@ -39,8 +39,9 @@ void launch_validate_push(const int32_t* a, const float* r, long long n, int A, 
 __global__ void push_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
                             long long cap, long long count0, long long first, long long state_bytes,
                             const uint8_t* s, const int32_t* a, const float* r, const uint8_t* sn,
-                            const uint8_t* t) {
+                            const uint8_t* t, long long* ring_size_out, long long ring_size) {
   long long i = blockIdx.x;
+  if (ring_size_out && i == 0 && threadIdx.x == 0) *ring_size_out = ring_size;
   long long slot = (count0 + first + i) % cap;
   const uint8_t* src0 = s + i * state_bytes;
   const uint8_t* src1 = sn + i * state_bytes;
@@ -69,11 +70,12 @@ __global__ void push_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, 
 void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
                            long long cap, long long count0, long long n_total, long long first, long long n,
                            long long state_bytes, const uint8_t* s, const int32_t* a, const float* r,
-                           const uint8_t* sn, const uint8_t* t, cudaStream_t st) {
+                           const uint8_t* sn, const uint8_t* t, cudaStream_t st, long long* ring_size_out,
+                           long long ring_size) {
   (void)n_total;
   if (n <= 0) return;
   push_kernel<<<(unsigned)n, 256, 0, st>>>(ring_s, ring_sn, ring_a, ring_r, ring_t, cap, count0, first, state_bytes,
-                                           s, a, r, sn, t);
+                                           s, a, r, sn, t, ring_size_out, ring_size);
 }
 
 // ---------------------------------------------------------------- a12 update
