@@ -396,8 +396,9 @@ def main():
                    "n_push": C["n_push"], "n_fetch": C["n_fetch"],
                    "sync_mode": "async (lag-1 fetch)" if C["async"] else "deterministic",
                    "parallelism": f"dp{world} + sharded parameter server", "gamma": 0.99,
-                   "l2": "inputs larger than L2: each step gathers 32 random slots of a "
-                         f"{args.replay * 56454 / 1e9:.1f} GB replay",
+                   "l2": f"inputs larger than L2: each step gathers {b} random s and s' slots of a "
+                         f"{args.replay * 56454 / 1e9:.1f} GB replay from HBM (bf16 path: the step's forward "
+                         "bulk-prefetches the next step's slots into L2; the counter-based sampler knows them)",
                    "prefill_s": round(prefill_s, 1)},
         "gpu_launches": launches,
         "staleness_hist": [int(x) for x in out["staleness"][:8]] if C["async"] else None,

@@ -201,6 +201,13 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     // a2 gather: the whole u8 state in one TMA bulk copy (28,224 contiguous bytes of the ring slot)
     mbar_arrive_expect_tx(&bar_ld, mnih::SLOT);
     bulk_g2s(sU8, a.ring[g] + slot * mnih::SLOT, mnih::SLOT, &bar_ld);
+    // the sampler is counter-based: step T+1's slot is known now. Prefetch it into L2 so that the
+    // next step's gather is an L2 hit with a warm TLB (a random 28 KB slot of a 56 GB ring
+    // otherwise costs a page walk); harmless if a push changes the ring size before T+1.
+    if (a.ctr) {
+      const long long nxt = sample_slot(a.seed, a.rank, a.ctr->T + 1, (unsigned)j, a.ctr->ring_size);
+      bulk_prefetch_l2(a.ring[g] + nxt * mnih::SLOT, mnih::SLOT);
+    }
   }
   if (warp == 0) tmem_alloc(&tbase, 128);
   __syncthreads();  // barriers initialised before anyone waits on them
