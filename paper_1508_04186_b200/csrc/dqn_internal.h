@@ -78,6 +78,7 @@ struct GemmArgs {
 };
 
 struct HeadArgs {
+  int st_id;                  // DQN_TRACE_STEP slot (step_trace.cuh), 0 = none
   const float* act[2];        // [b][H]: input of the output layer for s (theta) / s' (theta^)
   // bf16 path: act[] is produced here from the FC split-K partials [g][split][b_row][H]
   const float* fc_partial;    // nullptr: act[] given
@@ -121,8 +122,10 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
                            long long ring_size = 0);
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
-                    cudaStream_t st);
-void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st);
+                    cudaStream_t st, long long img_off = -1,
+                    long long w1_off = 0, long long w2_off = 0);
+void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st, long long img_off = -1,
+                        long long w1_off = 0, long long w2_off = 0);
 
 // fp32 SIMT path (kernels_f32.cu)
 void init_f32_kernel_attrs();
@@ -150,6 +153,7 @@ struct ServerRoundArgs {
   float* theta_local[kMaxWorld];                // every rank's working theta (fp32)
   __nv_bfloat16* theta_local_bf16[kMaxWorld];   // and its bf16 copy (nullptr on the fp32 path)
   long long f32_peer_lo, f32_peer_hi;           // theta range read only as bf16: no fp32 copy to peers
+  long long img_off, w1_off, w2_off;            // bf16 path: conv weight image (wimg.cuh), img_off < 0: none
   unsigned long long* flags[kMaxWorld];         // every rank's barrier-A array [world]
   unsigned long long* done[kMaxWorld];          // every rank's barrier-B counter
   unsigned long long* my_flags;
@@ -188,6 +192,7 @@ struct FwdConvArgs {
   __nv_bfloat16* a2;               // [groups*n][2592]
   uint8_t* a1_save;                // [n][8][144][16] or nullptr
   FusedAcquire acq;                // NEXT-1: the previous round's deliveries (acq.done == nullptr: none)
+  long long img_off;               // conv weight image (wimg.cuh) inside theta[g]
 };
 struct TcGemmArgs {
   const __nv_bfloat16* A[2];
@@ -211,6 +216,7 @@ struct TcGemmArgs {
   __nv_bfloat16* out_bf16;  // TC_EPI_MASK_T: out[n*ldo + m] = mask[n*ldo + m] > 0 ? D : 0
   const __nv_bfloat16* mask;
   long long ldo;
+  int st_id;                // DQN_TRACE_STEP slot (step_trace.cuh), 0 = none
 };
 enum { TC_EPI_ACCUM = 0, TC_EPI_FC_FWD = 1, TC_EPI_MASK_T = 2 };
 struct BwdConvArgs {
@@ -229,6 +235,11 @@ constexpr int kMnihSlot = 28224;
 constexpr int kA1Bytes = 8 * 144 * 16;
 constexpr int kBwdPart = 256 * 16 + 256 * 32 + 16 + 32;
 void init_bf16_kernel_attrs();
+// DQN_TRACE_STEP accessors, one per translation unit (step_trace.cuh)
+void step_trace_bf16(int on, unsigned long long* out);
+void step_trace_head(int on, unsigned long long* out);
+void step_trace_common(int on, unsigned long long* out);
+void step_trace_comm(int on, unsigned long long* out);
 void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t, long long cap,
                      long long count0, long long first, long long n, const uint8_t* s, const int32_t* a,
                      const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st,

@@ -17,6 +17,8 @@
 
 #include "../../include/dqn.h"
 #include "dqn_internal.h"
+#include "step_trace.cuh"
+#include "wimg.cuh"
 
 using namespace dqn;
 
@@ -76,8 +78,11 @@ struct dqn_ctx {
   unsigned long long* flags = nullptr;            // [kMaxWorld] barrier A (written by peers)
   unsigned long long* done = nullptr;             // barrier B counter (incremented by peers)
   std::vector<void*> ipc_opened;                  // peer mappings to close at destroy
-  __nv_bfloat16* theta_local_bf16 = nullptr;  // [P_pad] working copy the tensor cores read
-  __nv_bfloat16* theta_hat_bf16 = nullptr;    // [P_pad]
+  __nv_bfloat16* theta_local_bf16 = nullptr;  // [P_bf16] working copy the tensor cores read
+  __nv_bfloat16* theta_hat_bf16 = nullptr;    // [P_bf16]
+  // every bf16 theta buffer holds P_pad canonical entries followed by the conv weights' forward
+  // image (wimg.cuh) at img_off = P_pad
+  long long P_bf16 = 0, img_off = -1, w1_off = 0, w2_off = 0;
   __nv_bfloat16* a2_bf16 = nullptr;           // [2b][2592] conv2 activations (s: theta, s': theta^)
   uint8_t* a1_save = nullptr;                 // [b][8][144][16] conv1 activations (s2d planes)
   __nv_bfloat16* dh_bf16 = nullptr;           // [b][H]
@@ -124,6 +129,7 @@ struct dqn_ctx {
   std::vector<ProfMark> marks[16];
   int capture_variant = -1;  // >= 8 while capturing a profiling graph
   bool use_graphs = true;
+  bool step_trace = false;  // DQN_TRACE_STEP=1
   bool keep_grad = false;
   bool alias_local = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -402,6 +408,7 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   a.inv_div = (float)(1.0 / ((double)N * c.n_push));
   a.lr = (float)c.lr; a.rho = (float)c.rms_decay; a.omr = (float)(1.0 - c.rms_decay); a.eps = (float)c.rms_eps;
   a.ctr = ctx->ctr;
+  a.img_off = ctx->img_off; a.w1_off = ctx->w1_off; a.w2_off = ctx->w2_off;
   if (ctx->bf16) {  // the FC weight is read only through theta_local_bf16
     const FcShape& F = ctx->net.fc[0];
     a.f32_peer_lo = F.w_off;
@@ -464,6 +471,15 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
       CK(cudaEventCreateWithFlags(&ctx->ev_stage[i], cudaEventDisableTiming));
     }
     CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_out), sizeof(dqn_ctx::HostOut), cudaHostAllocDefault));
+  }
+  if (const char* v = getenv("DQN_TRACE_STEP")) {
+    if (atoi(v)) {
+      ctx->step_trace = true;
+      step_trace_bf16(1, nullptr);
+      step_trace_head(1, nullptr);
+      step_trace_common(1, nullptr);
+      step_trace_comm(1, nullptr);
+    }
   }
   CK(cudaEventCreate(&ctx->ev0));
   CK(cudaEventCreate(&ctx->ev1));
@@ -532,8 +548,12 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     init_bf16_kernel_attrs();
     const int H = net.fc[0].H;
     ctx->fc_splits = 18;  // K = 2592 = 18 x 144
-    if ((rc = dalloc(ctx, &ctx->theta_local_bf16, ctx->P_pad))) return rc;
-    if ((rc = dalloc(ctx, &ctx->theta_hat_bf16, ctx->P_pad))) return rc;
+    ctx->img_off = ctx->P_pad;
+    ctx->P_bf16 = ctx->P_pad + kWimgElems;
+    ctx->w1_off = net.conv[0].w_off;
+    ctx->w2_off = net.conv[1].w_off;
+    if ((rc = dalloc(ctx, &ctx->theta_local_bf16, ctx->P_bf16))) return rc;
+    if ((rc = dalloc(ctx, &ctx->theta_hat_bf16, ctx->P_bf16))) return rc;
     if ((rc = dalloc(ctx, &ctx->a2_bf16, 2LL * b * 2592))) return rc;
     if ((rc = dalloc(ctx, &ctx->a1_save, (long long)b * kA1Bytes))) return rc;
     if ((rc = dalloc(ctx, &ctx->dh_bf16, (long long)b * H))) return rc;
@@ -567,8 +587,10 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   }
   CK(cudaMemcpyAsync(ctx->theta_hat, th.data(), sizeof(float) * ctx->P_pad, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->bf16) {
-    launch_f32_to_bf16(ctx->theta_hat, ctx->theta_local_bf16, ctx->P_pad, ctx->stream);
-    launch_f32_to_bf16(ctx->theta_hat, ctx->theta_hat_bf16, ctx->P_pad, ctx->stream);
+    launch_f32_to_bf16(ctx->theta_hat, ctx->theta_local_bf16, ctx->P_pad, ctx->stream, ctx->img_off, ctx->w1_off,
+                       ctx->w2_off);
+    launch_f32_to_bf16(ctx->theta_hat, ctx->theta_hat_bf16, ctx->P_pad, ctx->stream, ctx->img_off, ctx->w1_off,
+                       ctx->w2_off);
     CK(cudaGetLastError());
   }
   if (ctx->async) {  // theta^(0) published in slot 0; the comm stream and its events
@@ -577,12 +599,14 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     for (int i = 0; i < 2; ++i) {
       CK(cudaEventCreateWithFlags(&ctx->ev_gen[i], cudaEventDisableTiming));
       if ((rc = dalloc(ctx, &ctx->theta_pub[i], ctx->P_pad))) return rc;
-      if (ctx->bf16 && (rc = dalloc(ctx, &ctx->theta_pub_bf16[i], ctx->P_pad))) return rc;
+      if (ctx->bf16 && (rc = dalloc(ctx, &ctx->theta_pub_bf16[i], ctx->P_bf16))) return rc;
     }
     if ((rc = dalloc(ctx, &ctx->g_send, ctx->P_pad))) return rc;
     CK(cudaMemcpyAsync(ctx->theta_pub[0], ctx->theta_hat, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice,
                        ctx->stream));
-    if (ctx->bf16) launch_f32_to_bf16(ctx->theta_pub[0], ctx->theta_pub_bf16[0], ctx->P_pad, ctx->stream);
+    if (ctx->bf16)
+      launch_f32_to_bf16(ctx->theta_pub[0], ctx->theta_pub_bf16[0], ctx->P_pad, ctx->stream, ctx->img_off, ctx->w1_off,
+                         ctx->w2_off);
     CK(cudaEventRecord(ctx->ev_gen[0], ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -891,12 +915,14 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
     } else if (ctx->world > 1) {
       PB("fetch_all_gather", 1);
       NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
-      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
+      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st, ctx->img_off, ctx->w1_off,
+                         ctx->w2_off);
       PE();
     } else if (!ctx->alias_local) {
       PB("fetch_copy", 1);
       CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_master, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
-      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
+      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st, ctx->img_off, ctx->w1_off,
+                         ctx->w2_off);
       PE();
     }
   }
@@ -906,7 +932,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
       NK(ncclAllGather(ctx->theta_master, ctx->theta_hat, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
     else
       CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(ctx->theta_hat_bf16, ctx->theta_local_bf16, sizeof(__nv_bfloat16) * ctx->P_pad,
+    CK(cudaMemcpyAsync(ctx->theta_hat_bf16, ctx->theta_local_bf16, sizeof(__nv_bfloat16) * ctx->P_bf16,
                        cudaMemcpyDeviceToDevice, st));
     PE();
   }
@@ -919,6 +945,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   fa.idx = ctx->idx; fa.ctr = ctx->ctr; fa.seed = c.seed; fa.rank = (unsigned)ctx->rank; fa.n = b;
   fa.a2 = ctx->a2_bf16; fa.a1_save = ctx->a1_save;
   fa.acq = ctx->acq;
+  fa.img_off = ctx->img_off;
   PB("conv_fwd", 1);
   launch_fwd_conv_bf16(fa, 2, st);
   PE();
@@ -927,6 +954,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.A[1] = ctx->theta_hat_bf16 + F.w_off; gf.lda = F.D; gf.a_mn = 0;
   gf.B[0] = ctx->a2_bf16; gf.B[1] = ctx->a2_bf16 + (long long)b * F.D; gf.ldb = F.D; gf.b_mn = 0;
   gf.M = F.H; gf.N = b; gf.K = F.D; gf.BN = b; gf.kper = F.D / ctx->fc_splits; gf.splits = ctx->fc_splits;
+  gf.st_id = ST_FC_FWD;
   gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial; gf.counters = ctx->tc_counters;
   gf.pre_a = 1; gf.pre_b = 0;  // W from the previous step's update; a2 from the predecessor
   gf.bias[0] = ctx->theta_local + F.b_off; gf.bias[1] = ctx->theta_hat + F.b_off;
@@ -947,6 +975,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   h.fc_partial = ctx->fc_partial; h.fc_splits = gf.splits; h.fc_split_stride = (long long)gf.BN * gf.M;
   h.fc_bias[0] = ctx->theta_local + F.b_off; h.fc_bias[1] = ctx->theta_hat + F.b_off;
   h.act_out[0] = ctx->act_fc[0][0]; h.act_out[1] = ctx->act_fc[0][1];
+  h.st_id = ST_HEAD;
   h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
   h.s_dq = ctx->head_dq; h.s_act = ctx->head_act; h.s_loss = ctx->head_loss;
   PB("head_sample", 1);
@@ -966,6 +995,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   gx.epi = TC_EPI_MASK_T; gx.out_bf16 = ctx->dz2_bf16; gx.mask = ctx->a2_bf16; gx.ldo = F.D;
   gx.pre_a = 1; gx.pre_b = 0;  // W is published by the previous step's update; dH by the predecessor
   PB("fc1_bwd_head_finish", 1);
+  gw.st_id = gx.st_id = ST_FC_BWD;
   launch_tc_pair_with_head(gw, gx, h, st);
   PE();
   // a8/a9 conv backward
@@ -999,7 +1029,8 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
     } else {
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
-                     (float)c.rms_eps, nullptr, ctx->alias_local ? ctx->theta_local_bf16 : nullptr, ctx->ctr, 1, st);
+                     (float)c.rms_eps, nullptr, ctx->alias_local ? ctx->theta_local_bf16 : nullptr, ctx->ctr, 1, st,
+                   ctx->alias_local ? ctx->img_off : -1, ctx->w1_off, ctx->w2_off);
       PE();
     }
   }
@@ -1077,7 +1108,7 @@ static int async_fetch(dqn_ctx* ctx) {
   CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_pub[s], sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice,
                      ctx->stream));
   if (ctx->bf16)
-    CK(cudaMemcpyAsync(ctx->theta_local_bf16, ctx->theta_pub_bf16[s], sizeof(__nv_bfloat16) * ctx->P_pad,
+    CK(cudaMemcpyAsync(ctx->theta_local_bf16, ctx->theta_pub_bf16[s], sizeof(__nv_bfloat16) * ctx->P_bf16,
                        cudaMemcpyDeviceToDevice, ctx->stream));
   return DQN_OK;
 }
@@ -1104,7 +1135,8 @@ static int async_push(dqn_ctx* ctx) {
     launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_send, ctx->P_pad, div, (float)c.lr, rho, omr,
                    (float)c.rms_eps, ctx->theta_pub[s], nullptr, ctx->ctr, 0, cs);
   }
-  if (ctx->bf16) launch_f32_to_bf16(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->P_pad, cs);
+  if (ctx->bf16)
+    launch_f32_to_bf16(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->P_pad, cs, ctx->img_off, ctx->w1_off, ctx->w2_off);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_gen[s], cs));
   return DQN_OK;
@@ -1277,6 +1309,26 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
   }
   CK(cudaStreamSynchronize(ctx->stream));
   const DevCounters hc = ho->ctr;
+  if (ctx->step_trace) {  // DQN_TRACE_STEP=1: the last step's kernel timeline (CTA 0 stamps)
+    unsigned long long t[4][ST_N][3] = {}, m[ST_N][3] = {};
+    step_trace_bf16(0, &t[0][0][0]);
+    step_trace_head(0, &t[1][0][0]);
+    step_trace_common(0, &t[2][0][0]);
+    step_trace_comm(0, &t[3][0][0]);
+    for (int u = 0; u < 4; ++u)
+      for (int q = 0; q < ST_N; ++q)
+        for (int w = 0; w < 3; ++w)
+          if (t[u][q][w]) m[q][w] = t[u][q][w];
+    static const char* nm[ST_N] = {"", "conv_fwd", "fc_fwd", "head", "fc_bwd+finish", "conv_bwd", "bwd_reduce",
+                                   "update", "server_round", "fwd:staged/conv1 mma/conv1 epi", "fwd:conv2 mma"};
+    const unsigned long long t0 = m[ST_FWD][0];
+    fprintf(stderr, "[dqn rank %d] step timeline (us from conv_fwd entry: entry / past wait / exit):", ctx->rank);
+    for (int q = 1; q < ST_N; ++q)
+      if (m[q][0] && t0)
+        fprintf(stderr, " %s %.2f/%.2f/%.2f;", nm[q], ((double)m[q][0] - (double)t0) / 1e3,
+                ((double)m[q][1] - (double)t0) / 1e3, ((double)m[q][2] - (double)t0) / 1e3);
+    fprintf(stderr, "\n");
+  }
   if (diag_ok) loss.assign(ho->loss, ho->loss + k);
   if (ctx->sra.trace) {  // DQN_TRACE_COMM=1: phases of the fused server round (block 0), last 64 rounds
     unsigned long long t[1024];
@@ -1358,6 +1410,7 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
                       nullptr, nullptr, nullptr, st);
       FwdConvArgs fa{};
       fa.ring[0] = ctx->q_stage_s2d;
+      fa.img_off = ctx->img_off;
       fa.theta[0] = ctx->theta_local_bf16;
       fa.theta_f32[0] = ctx->theta_local;
       fa.w1_off = net.conv[0].w_off; fa.b1_off = net.conv[0].b_off;

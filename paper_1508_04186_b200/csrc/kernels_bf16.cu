@@ -20,6 +20,8 @@
 #include "fused_acquire.cuh"
 #include "head_finish.cuh"
 #include "pdl.cuh"
+#include "step_trace.cuh"
+#include "wimg.cuh"
 #include "philox.cuh"
 #include "sm100.cuh"
 
@@ -116,54 +118,6 @@ __device__ __forceinline__ void expand_state(uint8_t* sX, const uint8_t* sU8) {
   }
 }
 
-// conv1 B operand [kchunk 32][n 16][8]: k = t*64 + c', t = dy*2+dx, c' = f*16+iy*4+ix -> W1[n][f][4dy+iy][4dx+ix]
-// (fixed trip counts for 128 threads, fully unrolled: every thread's gathers are in flight together)
-__device__ __forceinline__ void stage_w1(uint8_t* sW, const __nv_bfloat16* __restrict__ w) {
-#pragma unroll
-  for (int it = 0; it < 32 * mnih::C1 / 128; ++it) {
-    const int e = threadIdx.x + it * 128;
-    const int kc = e / mnih::C1, n = e % mnih::C1;
-    uint32_t o[4];
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      uint16_t pr[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int k = kc * 8 + 2 * h + u;
-        const int t = k >> 6, c = k & 63;
-        const int f = c >> 4, iy = (c >> 2) & 3, ix = c & 3;
-        const int ky = 4 * (t >> 1) + iy, kx = 4 * (t & 1) + ix;
-        pr[u] = __bfloat16_as_ushort(w[((n * 4 + f) * 8 + ky) * 8 + kx]);
-      }
-      o[h] = pr[0] | ((uint32_t)pr[1] << 16);
-    }
-    *reinterpret_cast<uint4*>(sW + (kc * mnih::C1 + n) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
-  }
-}
-// conv2 B operand [kchunk 32][n 32][8]: k = t*64 + c'', c'' = (iy*2+ix)*16 + c -> W2[n][c][2dy+iy][2dx+ix]
-__device__ __forceinline__ void stage_w2(uint8_t* sW, const __nv_bfloat16* __restrict__ w) {
-#pragma unroll
-  for (int it = 0; it < 32 * mnih::C2 / 128; ++it) {
-    const int e = threadIdx.x + it * 128;
-    const int kc = e / mnih::C2, n = e % mnih::C2;
-    uint32_t o[4];
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      uint16_t pr[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int k = kc * 8 + 2 * h + u;
-        const int t = k >> 6, c2 = k & 63;
-        const int q = c2 >> 4, c = c2 & 15;
-        const int ky = 2 * (t >> 1) + (q >> 1), kx = 2 * (t & 1) + (q & 1);
-        pr[u] = __bfloat16_as_ushort(w[((n * 16 + c) * 4 + ky) * 4 + kx]);
-      }
-      o[h] = pr[0] | ((uint32_t)pr[1] << 16);
-    }
-    *reinterpret_cast<uint4*>(sW + (kc * mnih::C2 + n) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
-  }
-}
-
 // ------------------------------------------------------------------ a1-a4: sample + gather + conv1 + conv2
 // grid (n_images, groups): group 0 = s_j with theta (local), group 1 = s'_j with theta^.
 // Writes a2[g*n + j][2592] (bf16, canonical (C,H,W) flatten, post-ReLU) and, for group 0,
@@ -181,6 +135,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   __shared__ uint32_t tbase;
   const int j = blockIdx.x, g = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  st_stamp(ST_FWD, 0);
   uint8_t* sX = smem + FWD_SX;
   uint8_t* sA1 = smem + FWD_SA1;
   uint8_t* sW1 = smem + FWD_SW1;
@@ -216,16 +171,24 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   expand_state(sX, sU8);  // u8 -> exact bf16 (1/255 folded into the epilogue)
   // everything above overlaps the previous kernel (the update that publishes theta); weights after the wait
   pdl_wait();
+  st_stamp(ST_FWD, 1);
   if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[10]));
   fused_round_acquire(a.acq);  // N > 1 fused server round: peers' deliveries into theta_local complete
   pdl_trigger();               // only now: the FC forward reads the delivered weights before its wait
-  const __nv_bfloat16* th = a.theta[g];
-  stage_w1(sW1, th + a.w1_off);
-  stage_w2(sW2, th + a.w2_off);
+  // conv1 + conv2 B operands: the weight image the update wrote after the canonical entries
+  // (wimg.cuh), contiguous with sW1 | sW2 in shared memory: 1,536 16-byte async copies
+  static_assert(FWD_SW2 == FWD_SW1 + kW1Elems * 2 && kWimgElems * 2 == 1536 * 16, "weight image layout");
+  {
+    const uint4* img = reinterpret_cast<const uint4*>(a.theta[g] + a.img_off);
+#pragma unroll
+    for (int it = 0; it < 1536 / 128; ++it) cp_async16(sW1 + (threadIdx.x + it * 128) * 16, img + threadIdx.x + it * 128);
+    cp_async_wait_all();
+  }
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  st_stamp(ST_P1, 0);
   const uint32_t tmem = tbase;
   // ---- conv1: 4 M-tiles x 4 taps x 4 K-steps, M = 128, N = 16
   if (threadIdx.x == 0) {
@@ -244,6 +207,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   __syncwarp();
   mbar_wait(&bar, 0);
   tc_fence_after();
+  st_stamp(ST_P1, 1);
   // ---- conv1 epilogue: x (1/255) + b1, ReLU, bf16, into conv2's s2d planes
   {
     const float* b1 = a.theta_f32[g] + a.b1_off;
@@ -274,6 +238,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  st_stamp(ST_P1, 2);
   // ---- conv2: 1 M-tile x 4 taps x 4 K-steps, M = 128, N = 32
   if (threadIdx.x == 0) {
     const uint32_t idesc = make_idesc_bf16(128, mnih::C2, 0, 0);
@@ -295,6 +260,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   }
   __syncwarp();
   mbar_wait(&bar, 1);
+  st_stamp(ST_P2, 0);
   tc_fence_after();
   // ---- conv2 epilogue: + b2, ReLU, bf16, canonical flatten d = c*81 + oy*9 + ox
   {
@@ -319,6 +285,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 128);
+  st_stamp(ST_FWD, 2);
 }
 
 void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st) {
@@ -351,7 +318,7 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
   // ---- stage A (128 rows x KC) and B (BN rows x KC), 16-byte vectors
   const __nv_bfloat16* Ag = a.A[g];
   const __nv_bfloat16* Bg = a.B[g];
-  if (!a.pre_a) pdl_sync();
+  if (!a.pre_a) { pdl_sync(); st_stamp(a.st_id, 1); }
   const int kch = KC / 8;
   // all 16-byte pieces go out as cp.async (LDGSTS) so a thread keeps dozens of loads in flight
   const uint4 z4 = make_uint4(0, 0, 0, 0);
@@ -374,7 +341,7 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
   }
   const int bn = a.BN;
   // operands produced by the immediate predecessor are staged after the PDL wait (pre_a / pre_b flags)
-  if (a.pre_a && !a.pre_b) pdl_sync();
+  if (a.pre_a && !a.pre_b) { pdl_sync(); st_stamp(a.st_id, 1); }
   if (!a.b_mn) {
     for (int e = threadIdx.x; e < bn * kch; e += blockDim.x) {
       const int r = e / kch, c = e % kch;
@@ -394,7 +361,7 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
     }
   }
   cp_async_wait_all();
-  if (a.pre_a && a.pre_b) pdl_sync();  // the epilogue's outputs may still be read by the predecessor
+  if (a.pre_a && a.pre_b) { pdl_sync(); st_stamp(a.st_id, 1); }  // the epilogue's outputs may still be read by the predecessor
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -500,7 +467,9 @@ __global__ void __launch_bounds__(128) tc_gemm_kernel(TcGemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
+  st_stamp(a.st_id, 0);
   tc_gemm_tile(a, blockIdx.x, blockIdx.y, blockIdx.z, smem, bar, tbase);
+  st_stamp(a.st_id, 2);
 }
 
 struct TcPairArgs {
@@ -514,6 +483,7 @@ __global__ void __launch_bounds__(128) tc_pair_kernel(TcPairArgs a) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   const int bx = blockIdx.x;
+  st_stamp(ST_FC_BWD, 0);
   if (bx < a.tiles0) {
     tc_gemm_tile(a.p0, bx, 0, 0, smem, bar, tbase);
   } else if (bx < a.tiles0 + a.tiles1) {
@@ -524,6 +494,7 @@ __global__ void __launch_bounds__(128) tc_pair_kernel(TcPairArgs a) {
     for (int e = (bx - a.tiles0 - a.tiles1) * 128 + threadIdx.x; e < n; e += (gridDim.x - a.tiles0 - a.tiles1) * 128)
       head_finish_elem(a.head, e);
   }
+  st_stamp(ST_FC_BWD, 2);
 }
 
 static size_t tc_smem(const TcGemmArgs& a) {
@@ -595,6 +566,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
   __shared__ float s_db1[16], s_db2[32];
   const int j = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  st_stamp(ST_CONV_BWD, 0);
   uint8_t* sX = smem + BWD_SX;
   uint8_t* sA1 = smem + BWD_SA1;
   uint8_t* sDZ2 = smem + BWD_SDZ2;
@@ -680,6 +652,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
   }
   __syncthreads();  // zero-filled dZ2 planes before the scatter below
   pdl_sync();       // dZ2 is the predecessor's (FC dX) output; everything above overlapped it
+  st_stamp(ST_CONV_BWD, 1);
   // ---- dZ2 (canonical [n2][81]) into planes [n2/8][DZ2_OFF + m'][8], m' = oy*10 + ox; + db2
   {
     const unsigned short* d = reinterpret_cast<const unsigned short*>(a.dz2 + (long long)j * mnih::D);
@@ -815,11 +788,14 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 256);
+  st_stamp(ST_CONV_BWD, 2);
 }
 
 // Sum the per-image partials in image order (deterministic) and scatter into G's canonical layout.
 __global__ void bwd_reduce_kernel(BwdConvArgs a) {
+  st_stamp(ST_BWD_REDUCE, 0);
   pdl_sync();
+  st_stamp(ST_BWD_REDUCE, 1);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= BWD_PART) return;
   {
@@ -849,6 +825,7 @@ __global__ void bwd_reduce_kernel(BwdConvArgs a) {
     if (e < BWD_PART_W1) s *= 1.0f / 255.0f;  // conv1 saw integer-valued x: d/dW of (W.u)/255
     a.grad[dst] += s;
   }
+  st_stamp(ST_BWD_REDUCE, 2);
 }
 
 void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st) {
@@ -862,5 +839,7 @@ void init_bf16_kernel_attrs() {
   cudaFuncSetAttribute(tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(bwd_conv_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM);
 }
+
+DQN_STEP_TRACE_HOST(bf16)
 
 }  // namespace dqn

@@ -29,6 +29,8 @@
 #include "dqn_internal.h"
 #include "fused_acquire.cuh"
 #include "pdl.cuh"
+#include "step_trace.cuh"
+#include "wimg.cuh"
 
 namespace dqn {
 
@@ -44,7 +46,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[(round_idx % 64) * 16 + (k)] = gtimer()
 
 __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
+  st_stamp(ST_ROUND, 0);
   pdl_wait();     // G of this rank is complete (the backward kernels precede in stream order)
+  st_stamp(ST_ROUND, 1);
   pdl_trigger();  // the next step's gather does not depend on this round
   // round id and round index from the step counter (identical on every rank): the head has
   // already advanced T to (step + 1), and push rounds end exactly at (step + 1) % n_push == 0
@@ -107,6 +111,15 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
       if (p == a.rank || f32_all) reinterpret_cast<float4*>(a.theta_local[p] + base)[i] = t4;
       if (a.theta_local_bf16[p]) reinterpret_cast<uint2*>(a.theta_local_bf16[p] + base)[i] = h;
     }
+    if (a.img_off >= 0 && e + 3 >= min(a.w1_off, a.w2_off) && e < max(a.w1_off, a.w2_off) + kW2Elems) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int sl = wimg_slot(e + q, a.w1_off, a.w2_off);
+        if (sl < 0) continue;
+        const __nv_bfloat16 v = __float2bfloat16_rn(tv[q]);
+        for (int p = 0; p < a.world; ++p) a.theta_local_bf16[p][a.img_off + sl] = v;
+      }
+    }
   }
   if (bad) atomicAdd(&a.ctr->nonfinite, bad);
   // ---- barrier B, release half: the CTA barrier orders every thread's stores before thread 0's
@@ -124,6 +137,7 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   }
   TRACE(3);
   if (a.trace && threadIdx.x == 0) atomicMax(a.trace + (round_idx % 64) * 16 + 5, gtimer());
+  st_stamp(ST_ROUND, 2);
 }
 
 // fp32 path: the acquire half as its own (tiny) kernel at the start of a step
@@ -146,5 +160,7 @@ int server_round_blocks(long long shard) {
 void launch_server_round(const ServerRoundArgs& a, cudaStream_t st) {
   launch_pdl(server_round_kernel, dim3(server_round_blocks(a.shard)), dim3(256), 0, st, a);
 }
+
+DQN_STEP_TRACE_HOST(comm)
 
 }  // namespace dqn

@@ -5,6 +5,8 @@
 #include "dqn_internal.h"
 #include "pdl.cuh"
 #include "philox.cuh"
+#include "step_trace.cuh"
+#include "wimg.cuh"
 
 namespace dqn {
 
@@ -90,8 +92,11 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
 // (sticky) with one atomic per offending thread.
 __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r, float* __restrict__ g, long long n,
                                float inv_div, float lr, float rho, float omr, float eps, float* __restrict__ pub_f32,
-                               __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr, int zero_g) {
+                               __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr, int zero_g, long long img_off,
+                               long long w1_off, long long w2_off) {
+  st_stamp(ST_UPDATE, 0);
   pdl_sync();
+  st_stamp(ST_UPDATE, 1);
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n / 4) return;
   const float4 g4 = reinterpret_cast<const float4*>(g)[i];
@@ -123,30 +128,50 @@ __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r,
     o.x = *reinterpret_cast<uint32_t*>(&lo);
     o.y = *reinterpret_cast<uint32_t*>(&hi);
     reinterpret_cast<uint2*>(pub_bf16)[i] = o;
+    if (img_off >= 0 && 4 * i + 3 >= min(w1_off, w2_off) && 4 * i < max(w1_off, w2_off) + kW2Elems) {
+      const float tq[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int sl = wimg_slot(4 * i + q, w1_off, w2_off);
+        if (sl >= 0) pub_bf16[img_off + sl] = __float2bfloat16_rn(tq[q]);
+      }
+    }
   }
   if (bad) atomicAdd(&ctr->nonfinite, bad);
+  st_stamp(ST_UPDATE, 2);
 }
 
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
-                    cudaStream_t st) {
+                    cudaStream_t st, long long img_off, long long w1_off, long long w2_off) {
   const int blocks = (int)((n / 4 + 255) / 256);
   launch_pdl(rmsprop_kernel, dim3(blocks < 1 ? 1 : blocks), dim3(256), 0, st, theta, r, g, n, 1.0f / div, lr, rho, omr,
-             eps, pub_f32, pub_bf16, ctr, zero_g);
+             eps, pub_f32, pub_bf16, ctr, zero_g, img_off, w1_off, w2_off);
 }
 
 
-__global__ void f32_to_bf16_kernel(const float* src, __nv_bfloat16* dst, long long n) {
+__global__ void f32_to_bf16_kernel(const float* src, __nv_bfloat16* dst, long long n, long long img_off,
+                                   long long w1_off, long long w2_off) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   long long stride = (long long)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) dst[i] = __float2bfloat16_rn(src[i]);
+  for (; i < n; i += stride) {
+    const __nv_bfloat16 v = __float2bfloat16_rn(src[i]);
+    dst[i] = v;
+    if (img_off >= 0) {  // the conv weights' forward image (wimg.cuh)
+      const int sl = wimg_slot(i, w1_off, w2_off);
+      if (sl >= 0) dst[img_off + sl] = v;
+    }
+  }
 }
 
-void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st) {
+void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st, long long img_off,
+                        long long w1_off, long long w2_off) {
   if (n <= 0) return;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  f32_to_bf16_kernel<<<blocks, 256, 0, st>>>(src, dst, n);
+  f32_to_bf16_kernel<<<blocks, 256, 0, st>>>(src, dst, n, img_off, w1_off, w2_off);
 }
+
+DQN_STEP_TRACE_HOST(common)
 
 }  // namespace dqn

@@ -13,6 +13,7 @@
 #include "dqn_internal.h"
 #include "head_finish.cuh"
 #include "pdl.cuh"
+#include "step_trace.cuh"
 
 namespace dqn {
 
@@ -28,11 +29,13 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
   __shared__ float s_qa;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = HS_THREADS / 32;
   // sampled slot and its (a, r, terminal): outputs of launches before the predecessor (PDL-safe)
+  st_stamp(h.st_id, 0);
   const int slot = __ldg(h.idx + j);
   const int act = __ldg(h.ring_a + slot);
   const float r = __ldg(h.ring_r + slot);
   const uint8_t term = __ldg(h.ring_term + slot);
   pdl_sync();
+  st_stamp(h.st_id, 1);
   // ---- the two hidden activation rows of sample j
   if (h.fc_partial) {
     for (int u = threadIdx.x; u < H; u += HS_THREADS) {
@@ -96,6 +99,7 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
     h.dH[(long long)j * H + u] = d;
     if (h.dH_bf16) h.dH_bf16[(long long)j * H + u] = __float2bfloat16_rn(d);
   }
+  st_stamp(h.st_id, 2);
 }
 
 // Cross-sample sums; e in [0, A*H) -> dW_o, [A*H, A*H + A) -> db_o, then H entries of db_fc.
@@ -117,5 +121,7 @@ void launch_head_f32(const HeadArgs& h, cudaStream_t st, bool with_finish) {
   const int n = h.A * h.H + h.A + h.H + 1;
   launch_pdl(head_finish_kernel, dim3((n + 255) / 256), dim3(256), 0, st, h);
 }
+
+DQN_STEP_TRACE_HOST(head)
 
 }  // namespace dqn
