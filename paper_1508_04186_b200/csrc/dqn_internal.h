@@ -235,6 +235,7 @@ constexpr int kMnihSlot = 28224;
 constexpr int kA1Bytes = 8 * 144 * 16;
 constexpr int kBwdPart = 256 * 16 + 256 * 32 + 16 + 32;
 void init_bf16_kernel_attrs();
+void init_head_kernel_attrs();
 // DQN_TRACE_STEP accessors, one per translation unit (step_trace.cuh)
 void step_trace_bf16(int on, unsigned long long* out);
 void step_trace_head(int on, unsigned long long* out);

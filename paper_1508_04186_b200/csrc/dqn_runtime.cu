@@ -238,7 +238,7 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   }
   {  // the TD head keeps the output layers and 32 samples' activations in shared memory
     const FcShape& O = net->fc[net->n_fc];
-    if (O.H > 32 || head_smem_bytes(O.H, O.D, c->minibatch) > 227 * 1024) {
+    if (O.H > 32 || head_smem_bytes(O.H, O.D, c->minibatch) > 226 * 1024) {
       *why = "output layer too large for the TD-head kernel (|A| <= 32)"; return DQN_EINVAL;
     }
   }
@@ -544,6 +544,7 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   if ((rc = dalloc(ctx, &ctx->q_stage, qn * sb))) return rc;
   if ((rc = dalloc(ctx, &ctx->q_out, qn * net.A))) return rc;
   if ((rc = dalloc(ctx, &ctx->q_amax, qn))) return rc;
+  init_head_kernel_attrs();
   if (ctx->bf16) {
     init_bf16_kernel_attrs();
     const int H = net.fc[0].H;

@@ -19,32 +19,48 @@ namespace dqn {
 
 constexpr int HS_THREADS = 256;
 constexpr int HS_AMAX = 32;
+constexpr int HS_MAX_SPLITS = 24;
 
+// dynamic smem: h [H] | h' [H] | W^_o [A][H] | W_o[a_j] [H]
 __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
   extern __shared__ float4 sm4[];
   const int H = h.H, A = h.A, j = blockIdx.x;
   float* s_h0 = reinterpret_cast<float*>(sm4);  // [H]
   float* s_h1 = s_h0 + H;                       // [H]
-  __shared__ float s_q[HS_AMAX];
-  __shared__ float s_qa;
+  float* s_wt = s_h1 + H;                       // [A][H]: theta^'s output layer
+  float* s_wa = s_wt + A * H;                   // [H]: theta's output-layer row of the taken action
+  __shared__ float s_q[HS_AMAX], s_bt[HS_AMAX];
+  __shared__ float s_qa_b, s_qa;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = HS_THREADS / 32;
-  // sampled slot and its (a, r, terminal): outputs of launches before the predecessor (PDL-safe)
   st_stamp(h.st_id, 0);
+  // everything here is at least two launches old (PDL-safe): the sampled slot and its (a, r,
+  // terminal), and the output layers of theta (updated by the previous step) and theta^
   const int slot = __ldg(h.idx + j);
   const int act = __ldg(h.ring_a + slot);
   const float r = __ldg(h.ring_r + slot);
   const uint8_t term = __ldg(h.ring_term + slot);
+  for (int e = threadIdx.x; e < A * H; e += HS_THREADS) s_wt[e] = __ldg(h.theta_hat + h.w_off + e);
+  for (int u = threadIdx.x; u < H; u += HS_THREADS) s_wa[u] = __ldg(h.theta + h.w_off + (long long)act * H + u);
+  if (threadIdx.x < A) s_bt[threadIdx.x] = __ldg(h.theta_hat + h.b_off + threadIdx.x);
+  if (threadIdx.x == 0) s_qa_b = __ldg(h.theta + h.b_off + act);
   pdl_sync();
   st_stamp(h.st_id, 1);
   // ---- the two hidden activation rows of sample j
   if (h.fc_partial) {
+    const int ns = h.fc_splits;
     for (int u = threadIdx.x; u < H; u += HS_THREADS) {
+      float pv[2][HS_MAX_SPLITS];  // every split of both groups in flight at once
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
-        const float* p = h.fc_partial + (long long)g * h.fc_splits * h.fc_split_stride + (long long)j * H + u;
+        const float* p = h.fc_partial + (long long)g * ns * h.fc_split_stride + (long long)j * H + u;
+#pragma unroll
+        for (int sp = 0; sp < HS_MAX_SPLITS; ++sp) pv[g][sp] = sp < ns ? __ldcg(p + (long long)sp * h.fc_split_stride) : 0.0f;
+      }
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
         float s = 0.0f;
-#pragma unroll 6
-        for (int sp = 0; sp < h.fc_splits; ++sp) s += __ldg(p + (long long)sp * h.fc_split_stride);
+#pragma unroll
+        for (int sp = 0; sp < HS_MAX_SPLITS; ++sp) s += pv[g][sp];  // split order (zeros past ns are exact)
         const float v = fmaxf(s + __ldg(h.fc_bias[g] + u), 0.0f);
         (g ? s_h1 : s_h0)[u] = v;
         h.act_out[g][(long long)j * H + u] = v;
@@ -60,15 +76,15 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
   // ---- Q'(s'_j; theta^) for every action (warp per action) and Q(s_j; theta)_{a_j}
   for (int a = warp; a <= A; a += nw) {
     const bool target = a < A;
-    const float* w = target ? h.theta_hat + h.w_off + (long long)a * H : h.theta + h.w_off + (long long)act * H;
+    const float* w = target ? s_wt + a * H : s_wa;
     const float* x = target ? s_h1 : s_h0;
     float s = 0.0f;
-    for (int i = lane; i < H; i += 32) s = fmaf(__ldg(w + i), x[i], s);
+    for (int i = lane; i < H; i += 32) s = fmaf(w[i], x[i], s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
-      if (target) s_q[a] = s + __ldg(h.theta_hat + h.b_off + a);
-      else s_qa = s + __ldg(h.theta + h.b_off + act);
+      if (target) s_q[a] = s + s_bt[a];
+      else s_qa = s + s_qa_b;
     }
   }
   __syncthreads();
@@ -93,9 +109,8 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
   }
   __syncthreads();
   const float dq = s_dq;
-  const float* wa = h.theta + h.w_off + (long long)act * H;
   for (int u = threadIdx.x; u < H; u += HS_THREADS) {
-    const float d = s_h0[u] > 0.0f ? dq * __ldg(wa + u) : 0.0f;
+    const float d = s_h0[u] > 0.0f ? dq * s_wa[u] : 0.0f;
     h.dH[(long long)j * H + u] = d;
     if (h.dH_bf16) h.dH_bf16[(long long)j * H + u] = __float2bfloat16_rn(d);
   }
@@ -110,9 +125,14 @@ __global__ void head_finish_kernel(HeadArgs h) {
 }
 
 size_t head_smem_bytes(int A, int H, int b) {
-  (void)A;
   (void)b;
-  return (size_t)2 * H * sizeof(float);
+  return (size_t)(3 + A) * H * sizeof(float);
+}
+
+void init_head_kernel_attrs() {
+  // the 227 KB opt-in limit includes the kernel's static shared memory
+  cudaFuncSetAttribute(head_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+  cudaGetLastError();  // an attribute refusal only limits the largest head; validate_cfg bounds it
 }
 
 void launch_head_f32(const HeadArgs& h, cudaStream_t st, bool with_finish) {
