@@ -217,6 +217,8 @@ struct TcGemmArgs {
   const __nv_bfloat16* mask;
   long long ldo;
   int st_id;                // DQN_TRACE_STEP slot (step_trace.cuh), 0 = none
+  int st_ph;                // DQN_TRACE_STEP phase slot of tile 0 (staged / MMA done), 0 = none
+  int store;                // TC_EPI_ACCUM: 1 = C = D (C known to be zero / overwritten), 0 = C += D
 };
 enum { TC_EPI_ACCUM = 0, TC_EPI_FC_FWD = 1, TC_EPI_MASK_T = 2 };
 struct BwdConvArgs {

@@ -989,6 +989,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   gw.M = F.H; gw.N = F.D; gw.K = b; gw.BN = 144; gw.kper = b; gw.splits = 1;
   gw.epi = TC_EPI_ACCUM; gw.C[0] = ctx->grad + F.w_off; gw.ldc = F.D;
   gw.pre_a = 0; gw.pre_b = 1;  // dH comes from the predecessor (head_sample), a2 from the conv forward
+  gw.store = c.n_push == 1;     // n_push = 1: this step's gradient is the whole accumulator (A8)
   TcGemmArgs gx{};
   gx.A[0] = ctx->theta_local_bf16 + F.w_off; gx.lda = F.D; gx.a_mn = 1;
   gx.B[0] = ctx->dh_bf16; gx.ldb = F.H; gx.b_mn = 0;
@@ -997,6 +998,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   gx.pre_a = 1; gx.pre_b = 0;  // W is published by the previous step's update; dH by the predecessor
   PB("fc1_bwd_head_finish", 1);
   gw.st_id = gx.st_id = ST_FC_BWD;
+  gw.st_ph = ST_P3; gx.st_ph = ST_P4;
   launch_tc_pair_with_head(gw, gx, h, st);
   PE();
   // a8/a9 conv backward
@@ -1321,7 +1323,9 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
         for (int w = 0; w < 3; ++w)
           if (t[u][q][w]) m[q][w] = t[u][q][w];
     static const char* nm[ST_N] = {"", "conv_fwd", "fc_fwd", "head", "fc_bwd+finish", "conv_bwd", "bwd_reduce",
-                                   "update", "server_round", "fwd:staged/conv1 mma/conv1 epi", "fwd:conv2 mma"};
+                                   "update", "server_round", "fwd:staged/conv1 mma/conv1 epi", "fwd:conv2 mma",
+                                   "fc dW tile: staged/mma/exit", "fc dX tile: staged/mma/exit",
+                                   "head finish: wait/-/exit", "dX epi chunks"};
     const unsigned long long t0 = m[ST_FWD][0];
     fprintf(stderr, "[dqn rank %d] step timeline (us from conv_fwd entry: entry / past wait / exit):", ctx->rank);
     for (int q = 1; q < ST_N; ++q)

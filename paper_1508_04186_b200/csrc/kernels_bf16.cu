@@ -298,6 +298,36 @@ void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st) {
 // One CTA = one (group, m-tile of 128, n-tile of BN, k-split); the CTA stages its
 // whole K slice at once (these GEMMs are latency-bound: M, N <= 2592, K <= 2592).
 
+// the TC_EPI_MASK_T mask tile [BN][128] bf16 is staged in shared memory when it fits the 200 KB budget
+__host__ __device__ __forceinline__ bool tc_mask_fits(const TcGemmArgs& a) {
+  return (long long)(128 + a.BN) * a.kper * 2 + (long long)a.BN * 256 <= 200 * 1024;
+}
+
+// B (BN rows x KC) into [kc][n][8] (K-major) or [n/8][k][8] (MN-major), 16-byte async copies
+__device__ __forceinline__ void stage_b_operand(const TcGemmArgs& a, const __nv_bfloat16* Bg, uint8_t* sB, int n0,
+                                                int k0, int KC, int kch) {
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  const int bn = a.BN;
+  if (!a.b_mn) {
+    for (int e = threadIdx.x; e < bn * kch; e += blockDim.x) {
+      const int r = e / kch, c = e % kch;
+      const int n = n0 + r;
+      uint8_t* d = sB + (c * bn + r) * 16;
+      if (n < a.N) cp_async16(d, Bg + (long long)n * a.ldb + k0 + 8 * c);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  } else {
+    const int ng = bn / 8;
+    for (int e = threadIdx.x; e < ng * KC; e += blockDim.x) {
+      const int gi = e % ng, k = e / ng;
+      const int n = n0 + 8 * gi;
+      uint8_t* d = sB + (gi * KC + k) * 16;
+      if (n < a.N) cp_async16(d, Bg + (long long)(k0 + k) * a.ldb + n);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  }
+}
+
 __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int split, int g, uint8_t* smem,
                                              uint64_t& bar, uint32_t& tbase) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -318,10 +348,26 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
   // ---- stage A (128 rows x KC) and B (BN rows x KC), 16-byte vectors
   const __nv_bfloat16* Ag = a.A[g];
   const __nv_bfloat16* Bg = a.B[g];
-  if (!a.pre_a) { pdl_sync(); st_stamp(a.st_id, 1); }
   const int kch = KC / 8;
-  // all 16-byte pieces go out as cp.async (LDGSTS) so a thread keeps dozens of loads in flight
+  // all 16-byte pieces go out as cp.async (LDGSTS) so a thread keeps dozens of loads in flight;
+  // operands older than the immediate predecessor (pre_a / pre_b) are staged before the PDL wait
   const uint4 z4 = make_uint4(0, 0, 0, 0);
+  const bool b_first = a.pre_b && !a.pre_a;
+  if (b_first) stage_b_operand(a, Bg, sB, n0, k0, KC, kch);
+  // TC_EPI_MASK_T: the ReLU mask tile [BN][128] (two or more launches old) lands in shared memory
+  // before the wait, so the epilogue has no global loads on its critical path
+  unsigned short* sMask = reinterpret_cast<unsigned short*>(smem + (128 + a.BN) * a.kper * 2);
+  const bool mask_smem = a.epi == TC_EPI_MASK_T && tc_mask_fits(a);
+  if (mask_smem) {
+    for (int e = threadIdx.x; e < a.BN * 16; e += blockDim.x) {
+      const int nl = e / 16, ch = e % 16;
+      const int n = n0 + nl, mm = m0 + 8 * ch;
+      uint8_t* d = reinterpret_cast<uint8_t*>(sMask + nl * 128 + 8 * ch);
+      if (n < a.N && mm + 8 <= a.M) cp_async16(d, a.mask + (long long)n * a.ldo + mm);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  }
+  if (!a.pre_a) { pdl_sync(); st_stamp(a.st_id, 1); }
   if (!a.a_mn) {  // K-major: smem [kc][row][8]
     for (int e = threadIdx.x; e < 128 * kch; e += blockDim.x) {
       const int r = e / kch, c = e % kch;
@@ -342,30 +388,15 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
   const int bn = a.BN;
   // operands produced by the immediate predecessor are staged after the PDL wait (pre_a / pre_b flags)
   if (a.pre_a && !a.pre_b) { pdl_sync(); st_stamp(a.st_id, 1); }
-  if (!a.b_mn) {
-    for (int e = threadIdx.x; e < bn * kch; e += blockDim.x) {
-      const int r = e / kch, c = e % kch;
-      const int n = n0 + r;
-      uint8_t* d = sB + (c * bn + r) * 16;
-      if (n < a.N) cp_async16(d, Bg + (long long)n * a.ldb + k0 + 8 * c);
-      else *reinterpret_cast<uint4*>(d) = z4;
-    }
-  } else {
-    const int ng = bn / 8;
-    for (int e = threadIdx.x; e < ng * KC; e += blockDim.x) {
-      const int gi = e % ng, k = e / ng;
-      const int n = n0 + 8 * gi;
-      uint8_t* d = sB + (gi * KC + k) * 16;
-      if (n < a.N) cp_async16(d, Bg + (long long)(k0 + k) * a.ldb + n);
-      else *reinterpret_cast<uint4*>(d) = z4;
-    }
-  }
+  if (!b_first) stage_b_operand(a, Bg, sB, n0, k0, KC, kch);
   cp_async_wait_all();
   if (a.pre_a && a.pre_b) { pdl_sync(); st_stamp(a.st_id, 1); }  // the epilogue's outputs may still be read by the predecessor
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  const bool ph = a.st_ph && tile == 0 && split == 0 && g == 0;  // DQN_TRACE_STEP phase stamps
+  if (ph) st_stamp_here(a.st_ph, 0);
   const uint32_t tmem = tbase;
   if (threadIdx.x == 0) {
     const uint32_t idesc = make_idesc_bf16(128, bn, a.a_mn, a.b_mn);
@@ -380,9 +411,26 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
   __syncwarp();
   mbar_wait(&bar, 0);
   tc_fence_after();
+  if (ph) st_stamp_here(a.st_ph, 1);
   const int m = m0 + 32 * warp + lane;
   const uint32_t trow = tmem + ((uint32_t)(32 * warp) << 16);
-  if (a.epi == TC_EPI_ACCUM) {
+  if (a.epi == TC_EPI_ACCUM && a.store) {
+    // plain store: each thread writes its row's bn contiguous floats straight from TMEM (16-byte
+    // stores; a warp's 32 rows complete whole 128-byte lines over consecutive chunks)
+    float* crow = a.C[g] + (long long)m * a.ldc + n0;
+    const bool vec = ((a.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.C[g]) & 15) == 0) && (n0 & 3) == 0;
+    for (int c = 0; c < bn; c += 16) {
+      float v[16];
+      tmem_ld16(trow + c, v);
+      if (m >= a.M) continue;
+      if (vec && n0 + c + 16 <= a.N) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(crow + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      } else {
+        for (int i = 0; i < 16 && n0 + c + i < a.N; ++i) crow[c + i] = v[i];
+      }
+    }
+  } else if (a.epi == TC_EPI_ACCUM) {
     // TMEM -> shared tile [128][bn+4] (the MMAs are complete, so the operand staging area is free),
     // then a coalesced read-modify-write of C by the whole CTA with many 16-byte accesses in flight
     float* sD = reinterpret_cast<float*>(smem);
@@ -410,7 +458,7 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
         const int mm = m0 + r, n = n0 + 4 * q;
         ok[k] = e < 128 * nv && mm < a.M && vec && n + 4 <= a.N;
         dst[k] = a.C[g] + (long long)mm * a.ldc + n;
-        o[k] = ok[k] ? *reinterpret_cast<const float4*>(dst[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        o[k] = ok[k] && !a.store ? *reinterpret_cast<const float4*>(dst[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int k = 0; k < BATCH; ++k) {
@@ -424,7 +472,7 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
           *reinterpret_cast<float4*>(dst[k]) = o[k];
         } else if (mm < a.M) {
           const float dv[4] = {d.x, d.y, d.z, d.w};
-          for (int i = 0; i < 4 && n + i < a.N; ++i) dst[k][i] += dv[i];
+          for (int i = 0; i < 4 && n + i < a.N; ++i) dst[k][i] = a.store ? dv[i] : dst[k][i] + dv[i];
         }
       }
     }
@@ -433,11 +481,12 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
       float v[16];
       tmem_ld16(trow + c, v);
       if (m < a.M) {
-        unsigned short mk[16];  // all 16 mask loads in flight before the stores
+        unsigned short mk[16];  // from the staged tile, or all 16 global loads in flight
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + c + i;
-          mk[i] = n < a.N ? __ldg(reinterpret_cast<const unsigned short*>(a.mask) + (long long)n * a.ldo + m) : 0;
+          mk[i] = mask_smem ? sMask[(c + i) * 128 + (m - m0)]
+                            : (n < a.N ? __ldg(reinterpret_cast<const unsigned short*>(a.mask) + (long long)n * a.ldo + m) : 0);
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -446,6 +495,7 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
             a.out_bf16[(long long)n * a.ldo + m] = __float2bfloat16_rn((mk[i] & 0x8000u) == 0 && mk[i] != 0 ? v[i] : 0.0f);
         }
       }
+      if (ph && c < 48) st_stamp_here(ST_P6, c / 16);
     }
   } else {  // TC_EPI_FC_FWD: split partials, transposed to [g][split][n][m] (coalesced over m)
     float* pbase = a.partial + ((long long)g * a.splits + split) * (long long)a.BN * a.M;
@@ -486,19 +536,24 @@ __global__ void __launch_bounds__(128) tc_pair_kernel(TcPairArgs a) {
   st_stamp(ST_FC_BWD, 0);
   if (bx < a.tiles0) {
     tc_gemm_tile(a.p0, bx, 0, 0, smem, bar, tbase);
+    if (bx == 0) st_stamp_here(ST_P3, 2);
   } else if (bx < a.tiles0 + a.tiles1) {
     tc_gemm_tile(a.p1, bx - a.tiles0, 0, 0, smem, bar, tbase);
+    if (bx == a.tiles0) st_stamp_here(ST_P4, 2);
   } else {
     pdl_sync();  // the TD head's per-sample outputs come from the predecessor
+    if (bx == a.tiles0 + a.tiles1) st_stamp_here(ST_P5, 0);
     const int n = head_finish_elems(a.head);
     for (int e = (bx - a.tiles0 - a.tiles1) * 128 + threadIdx.x; e < n; e += (gridDim.x - a.tiles0 - a.tiles1) * 128)
       head_finish_elem(a.head, e);
+    if (bx == a.tiles0 + a.tiles1) st_stamp_here(ST_P5, 2);
   }
   st_stamp(ST_FC_BWD, 2);
 }
 
 static size_t tc_smem(const TcGemmArgs& a) {
   size_t smem = (size_t)(128 + a.BN) * a.kper * 2;
+  if (a.epi == TC_EPI_MASK_T && tc_mask_fits(a)) smem += (size_t)a.BN * 128 * 2;  // the mask tile
   if (a.epi == TC_EPI_ACCUM) smem = std::max(smem, (size_t)128 * (a.BN + 4) * 4);  // epilogue tile
   return smem;
 }
