@@ -986,7 +986,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   TcGemmArgs gw{};
   gw.A[0] = ctx->dh_bf16; gw.lda = F.H; gw.a_mn = 1;
   gw.B[0] = ctx->a2_bf16; gw.ldb = F.D; gw.b_mn = 1;
-  gw.M = F.H; gw.N = F.D; gw.K = b; gw.BN = 144; gw.kper = b; gw.splits = 1;
+  gw.M = F.H; gw.N = F.D; gw.K = b; gw.BN = 96; gw.kper = b; gw.splits = 1;  // 54 CTAs: short store epilogues
   gw.epi = TC_EPI_ACCUM; gw.C[0] = ctx->grad + F.w_off; gw.ldc = F.D;
   gw.pre_a = 0; gw.pre_b = 1;  // dH comes from the predecessor (head_sample), a2 from the conv forward
   gw.store = c.n_push == 1;     // n_push = 1: this step's gradient is the whole accumulator (A8)
@@ -1325,7 +1325,7 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
     static const char* nm[ST_N] = {"", "conv_fwd", "fc_fwd", "head", "fc_bwd+finish", "conv_bwd", "bwd_reduce",
                                    "update", "server_round", "fwd:staged/conv1 mma/conv1 epi", "fwd:conv2 mma",
                                    "fc dW tile: staged/mma/exit", "fc dX tile: staged/mma/exit",
-                                   "head finish: wait/-/exit", "dX epi chunks"};
+                                   "head finish: wait/-/exit", "dX epi chunks", "dX chunk0: tmem ld/mask"};
     const unsigned long long t0 = m[ST_FWD][0];
     fprintf(stderr, "[dqn rank %d] step timeline (us from conv_fwd entry: entry / past wait / exit):", ctx->rank);
     for (int q = 1; q < ST_N; ++q)

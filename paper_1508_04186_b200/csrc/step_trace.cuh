@@ -7,7 +7,7 @@
 
 namespace dqn {
 
-enum { ST_NONE = 0, ST_FWD, ST_FC_FWD, ST_HEAD, ST_FC_BWD, ST_CONV_BWD, ST_BWD_REDUCE, ST_UPDATE, ST_ROUND, ST_P1, ST_P2, ST_P3, ST_P4, ST_P5, ST_P6, ST_N };
+enum { ST_NONE = 0, ST_FWD, ST_FC_FWD, ST_HEAD, ST_FC_BWD, ST_CONV_BWD, ST_BWD_REDUCE, ST_UPDATE, ST_ROUND, ST_P1, ST_P2, ST_P3, ST_P4, ST_P5, ST_P6, ST_P7, ST_N };
 static __device__ unsigned long long g_st[ST_N][3];
 static __device__ int g_st_on;
 
