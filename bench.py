@@ -81,6 +81,8 @@ def region_work(name: str, b: int, net=MNIH):
     w["head_td"] = w["head_sample"] = (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 * 2)
     w["fc1_bwd"] = (4 * b * D * Hfc, b * Hfc * 4 + b * D * 4 * 2 + D * Hfc * 4 * 3)
     w["rmsprop_update"] = (0, P * 4 * 6)
+    conv_params = sum(L["N"] * (L["C"] * L["k"] ** 2 + 1) for L in layers)
+    w["reduce_update"] = (0, P * 4 * 6 + b * conv_params * 4)  # + the per-image conv partials
     w["sample"] = (0, b * 4)
     # fused regions of the bf16 tensor-core path
     w["conv_fwd"] = tuple(sum(w[f"conv{i + 1}_fwd"][q] for i in range(len(layers))) for q in range(2))
@@ -91,7 +93,8 @@ def region_work(name: str, b: int, net=MNIH):
 
 REGION_KERNELS = {"conv_fwd": ["fwd_conv_bf16_kernel"], "fc1_fwd": ["tc_gemm_kernel"],
                   "head_sample": ["head_sample_kernel"], "fc1_bwd_head_finish": ["tc_pair_kernel"],
-                  "conv_bwd": ["bwd_conv_bf16_kernel", "bwd_reduce_kernel"], "rmsprop_update": ["rmsprop_kernel"]}
+                  "conv_bwd": ["bwd_conv_bf16_kernel", "bwd_reduce_kernel"], "rmsprop_update": ["rmsprop_kernel"],
+                  "reduce_update": ["reduce_update_kernel"]}
 
 
 def region_traffic(name: str, dtype: str):

@@ -233,6 +233,18 @@ struct BwdConvArgs {
   unsigned* counter;
   float* grad;
 };
+struct ReduceUpdateArgs {
+  BwdConvArgs b;                   // the conv partials and offsets
+  float* theta;                    // fp32 theta (= theta_local at N = 1)
+  float* r;
+  float* g;                        // G (non-conv part; cleared after reading)
+  long long n;                     // P_pad
+  float inv_div, lr, rho, omr, eps;
+  __nv_bfloat16* pub_bf16;         // theta_local_bf16 (+ the conv weight image at img_off)
+  long long img_off;
+  DevCounters* ctr;
+};
+void launch_reduce_update(const ReduceUpdateArgs& u, cudaStream_t st);
 constexpr int kMnihSlot = 28224;
 constexpr int kA1Bytes = 8 * 144 * 16;
 constexpr int kBwdPart = 256 * 16 + 256 * 32 + 16 + 32;
@@ -252,6 +264,6 @@ void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st);
 // one launch: the tiles of GEMM p0, the tiles of GEMM p1 (single split, group 0 each), then the
 // cross-sample TD-head finish (head_finish.cuh) — the bf16 path's whole FC backward
 void launch_tc_pair_with_head(const TcGemmArgs& p0, const TcGemmArgs& p1, const HeadArgs& head, cudaStream_t st);
-void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st);
+void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st, bool with_reduce = true);
 
 }  // namespace dqn

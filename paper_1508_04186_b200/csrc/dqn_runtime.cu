@@ -1007,8 +1007,11 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   ba.theta = ctx->theta_local_bf16;
   ba.w1_off = L1.w_off; ba.b1_off = L1.b_off; ba.w2_off = L2.w_off; ba.b2_off = L2.b_off;
   ba.n = b; ba.partial = ctx->bwd_partial; ba.counter = ctx->tc_counters + 32; ba.grad = ctx->grad;
-  PB("conv_bwd", 1);
-  launch_bwd_conv_bf16(ba, st);
+  // N = 1, n_push = 1: the conv partials' reduction runs inside the update (reduce_update_kernel)
+  const bool fuse_reduce = push && ctx->world == 1 && c.n_push == 1 && !ctx->keep_grad && ctx->alias_local &&
+                           L1.w_off == 0 && L2.b_off + L2.N == kBwdPart;
+  PB("conv_bwd", fuse_reduce ? 1 : 2);
+  launch_bwd_conv_bf16(ba, st, !fuse_reduce);
   PE();
   if (ctx->keep_grad)
     CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
@@ -1028,6 +1031,15 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
                      (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, st);
+      PE();
+    } else if (fuse_reduce) {
+      PB("reduce_update", 1);
+      ReduceUpdateArgs u{};
+      u.b = ba;
+      u.theta = ctx->theta_master; u.r = ctx->rms; u.g = ctx->grad; u.n = ctx->P_pad;
+      u.inv_div = 1.0f / div; u.lr = (float)c.lr; u.rho = rho; u.omr = omr; u.eps = (float)c.rms_eps;
+      u.pub_bf16 = ctx->theta_local_bf16; u.img_off = ctx->img_off; u.ctr = ctx->ctr;
+      launch_reduce_update(u, st);
       PE();
     } else {
       PB("rmsprop_update", 1);

@@ -846,6 +846,36 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
   st_stamp(ST_CONV_BWD, 2);
 }
 
+// canonical theta index of per-image partial entry e (tap-permuted conv dW rows, then the biases)
+__device__ __forceinline__ long long bwd_part_dst(int e, const BwdConvArgs& a) {
+  if (e < BWD_PART_W1) {  // (mt*128 + r, n) with r -> tap t = 2*mt + r/64, c' = r%64
+    const int row = e / 16, n = e % 16;
+    const int t = 2 * (row / 128) + ((row % 128) >> 6), c = row & 63;
+    const int f = c >> 4, iy = (c >> 2) & 3, ix = c & 3;
+    const int ky = 4 * (t >> 1) + iy, kx = 4 * (t & 1) + ix;
+    return a.w1_off + ((n * 4 + f) * 8 + ky) * 8 + kx;
+  }
+  if (e < BWD_PART_W1 + BWD_PART_W2) {
+    const int ee = e - BWD_PART_W1;
+    const int row = ee / 32, n = ee % 32;
+    const int t = 2 * (row / 128) + ((row % 128) >> 6), c2 = row & 63;
+    const int q = c2 >> 4, c = c2 & 15;
+    const int ky = 2 * (t >> 1) + (q >> 1), kx = 2 * (t & 1) + (q & 1);
+    return a.w2_off + ((n * 16 + c) * 4 + ky) * 4 + kx;
+  }
+  if (e < BWD_PART_W1 + BWD_PART_W2 + 16) return a.b1_off + (e - BWD_PART_W1 - BWD_PART_W2);
+  return a.b2_off + (e - BWD_PART_W1 - BWD_PART_W2 - 16);
+}
+
+// the sum over images of partial entry e, in image order (deterministic); conv1's dW carries the
+// 1/255 of the integer-valued input (d/dW of (W.u)/255)
+__device__ __forceinline__ float bwd_part_sum(int e, const BwdConvArgs& a) {
+  float s = 0.0f;
+#pragma unroll 8
+  for (int i = 0; i < a.n; ++i) s += a.partial[(long long)i * BWD_PART + e];
+  return e < BWD_PART_W1 ? s * (1.0f / 255.0f) : s;
+}
+
 // Sum the per-image partials in image order (deterministic) and scatter into G's canonical layout.
 __global__ void bwd_reduce_kernel(BwdConvArgs a) {
   st_stamp(ST_BWD_REDUCE, 0);
@@ -853,39 +883,77 @@ __global__ void bwd_reduce_kernel(BwdConvArgs a) {
   st_stamp(ST_BWD_REDUCE, 1);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= BWD_PART) return;
-  {
-    float s = 0.0f;
-#pragma unroll 8
-    for (int i = 0; i < a.n; ++i) s += a.partial[(long long)i * BWD_PART + e];
-    long long dst;
-    if (e < BWD_PART_W1) {  // (mt*128 + r, n) with r -> tap t = 2*mt + r/64, c' = r%64
-      const int row = e / 16, n = e % 16;
-      const int t = 2 * (row / 128) + ((row % 128) >> 6), c = row & 63;
-      const int f = c >> 4, iy = (c >> 2) & 3, ix = c & 3;
-      const int ky = 4 * (t >> 1) + iy, kx = 4 * (t & 1) + ix;
-      dst = a.w1_off + ((n * 4 + f) * 8 + ky) * 8 + kx;
-    } else if (e < BWD_PART_W1 + BWD_PART_W2) {
-      const int ee = e - BWD_PART_W1;
-      const int row = ee / 32, n = ee % 32;
-      const int t = 2 * (row / 128) + ((row % 128) >> 6), c2 = row & 63;
-      const int q = c2 >> 4, c = c2 & 15;
-      const int ky = 2 * (t >> 1) + (q >> 1), kx = 2 * (t & 1) + (q & 1);
-      dst = a.w2_off + ((n * 16 + c) * 4 + ky) * 4 + kx;
-    } else if (e < BWD_PART_W1 + BWD_PART_W2 + 16) {
-      dst = a.b1_off + (e - BWD_PART_W1 - BWD_PART_W2);
-      s *= 1.0f;
-    } else {
-      dst = a.b2_off + (e - BWD_PART_W1 - BWD_PART_W2 - 16);
-    }
-    if (e < BWD_PART_W1) s *= 1.0f / 255.0f;  // conv1 saw integer-valued x: d/dW of (W.u)/255
-    a.grad[dst] += s;
-  }
+  a.grad[bwd_part_dst(e, a)] += bwd_part_sum(e, a);
   st_stamp(ST_BWD_REDUCE, 2);
 }
 
-void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st) {
+void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st, bool with_reduce) {
   launch_pdl(bwd_conv_bf16_kernel, dim3(a.n), dim3(128), BWD_SMEM, st, a);
-  launch_pdl(bwd_reduce_kernel, dim3(cdiv(BWD_PART, 128)), dim3(128), 0, st, a);
+  if (with_reduce) launch_pdl(bwd_reduce_kernel, dim3(cdiv(BWD_PART, 128)), dim3(128), 0, st, a);
+}
+
+// N = 1, n_push = 1: the image-order reduction of the conv partials fused into the RMSProp update
+// (one launch and one G round trip fewer). Threads [0, BWD_PART) own one conv parameter each (the
+// conv parameters are the canonical prefix [0, BWD_PART) of theta); the rest own a float4 of the
+// remaining parameters and read G as rmsprop_kernel does. Same arithmetic per element as
+// rmsprop_kernel (A4, A5, A24).
+__device__ __forceinline__ bool rms_elem(float& th, float& r, float g, const ReduceUpdateArgs& u) {
+  const float gb = g * u.inv_div;
+  if (!isfinite(gb)) return false;
+  const float rr = u.rho * r + u.omr * gb * gb;
+  r = rr;
+  th = th - u.lr * gb * rsqrtf(rr + u.eps);
+  return true;
+}
+
+__global__ void __launch_bounds__(256) reduce_update_kernel(ReduceUpdateArgs u) {
+  st_stamp(ST_UPDATE, 0);
+  pdl_sync();
+  st_stamp(ST_UPDATE, 1);
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  unsigned bad = 0;
+  if (t < BWD_PART) {
+    const int e = (int)t;
+    const float g = bwd_part_sum(e, u.b);
+    const long long d = bwd_part_dst(e, u.b);
+    float th = u.theta[d], r = u.r[d];
+    if (rms_elem(th, r, g, u)) {
+      u.theta[d] = th;
+      u.r[d] = r;
+    } else {
+      ++bad;
+    }
+    const __nv_bfloat16 hb = __float2bfloat16_rn(th);
+    u.pub_bf16[d] = hb;
+    const int sl = wimg_slot(d, u.b.w1_off, u.b.w2_off);
+    if (sl >= 0) u.pub_bf16[u.img_off + sl] = hb;
+  } else {
+    const long long i = BWD_PART / 4 + (t - BWD_PART);
+    if (i >= u.n / 4) return;
+    const float4 g4 = reinterpret_cast<const float4*>(u.g)[i];
+    float4 t4 = reinterpret_cast<const float4*>(u.theta)[i];
+    float4 r4 = reinterpret_cast<const float4*>(u.r)[i];
+    reinterpret_cast<float4*>(u.g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float tv[4] = {t4.x, t4.y, t4.z, t4.w}, rv[4] = {r4.x, r4.y, r4.z, r4.w};
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (!rms_elem(tv[q], rv[q], gv[q], u)) ++bad;
+    t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);
+    reinterpret_cast<float4*>(u.theta)[i] = t4;
+    reinterpret_cast<float4*>(u.r)[i] = make_float4(rv[0], rv[1], rv[2], rv[3]);
+    uint2 o;
+    o.x = pack_bf16(t4.x, t4.y);
+    o.y = pack_bf16(t4.z, t4.w);
+    reinterpret_cast<uint2*>(u.pub_bf16)[i] = o;
+  }
+  if (bad) atomicAdd(&u.ctr->nonfinite, bad);
+  st_stamp(ST_UPDATE, 2);
+}
+
+void launch_reduce_update(const ReduceUpdateArgs& u, cudaStream_t st) {
+  const long long threads = BWD_PART + (u.n / 4 - BWD_PART / 4);
+  launch_pdl(reduce_update_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, u);
 }
 
 void init_bf16_kernel_attrs() {

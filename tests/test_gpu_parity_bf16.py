@@ -132,3 +132,30 @@ def test_bf16_run_to_run_bit_identical():
         res.append(g.params(D.PARAMS_SERVER))
         g.close()
     assert np.array_equal(res[0], res[1])
+
+
+def test_fused_reduce_update_path():
+    """N = 1 without DQN_KEEP_GRAD: the conv partials' reduction runs inside the update kernel
+    (reduce_update_kernel). Its theta after 5 steps must follow the oracle like the two-kernel path
+    (smooth regime, 2e-2) and agree with that path to fp32 rounding."""
+    dc, on, oc = nets(minibatch=32, replay_capacity=1000, precision=D.BF16, lr=1e-5)
+    theta0 = smooth_theta(on, 7)
+    res = {}
+    for keep in ("1", None):
+        if keep is None:
+            os.environ.pop("DQN_KEEP_GRAD", None)
+        try:
+            g, rp, _ = make(dc, on, theta0, 1000, 77)
+            g.train(5)
+            res[keep] = (g.params(D.PARAMS_SERVER).astype(np.float64), g.params(D.PARAMS_LOCAL).astype(np.float64))
+            g.close()
+        finally:
+            os.environ["DQN_KEEP_GRAD"] = "1"
+    ref = O.run(on, oc, 1000, [rp], theta0.astype(np.float64), 5)
+    th0 = theta0.astype(np.float64)
+    for keep in ("1", None):
+        th, loc = res[keep]
+        assert np.array_equal(th, loc)  # N = 1: the working copy is the server theta
+        assert per_tensor_rel(th, ref["theta"], on) < TOL
+        assert rel_l2_per_tensor(th - th0, ref["theta"] - th0, on) < 0.1
+    assert per_tensor_rel(res[None][0], res["1"][0], on) < 1e-5
