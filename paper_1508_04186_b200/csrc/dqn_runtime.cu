@@ -1337,7 +1337,7 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
     static const char* nm[ST_N] = {"", "conv_fwd", "fc_fwd", "head", "fc_bwd+finish", "conv_bwd", "bwd_reduce",
                                    "update", "server_round", "fwd:staged/conv1 mma/conv1 epi", "fwd:conv2 mma",
                                    "fc dW tile: staged/mma/exit", "fc dX tile: staged/mma/exit",
-                                   "head finish: wait/-/exit", "dX epi chunks", "dX chunk0: tmem ld/mask"};
+                                   "head finish: wait/-/exit", "bwd: dZ2 staged/conv2 mma/dZ1 epi", "bwd: db1 done/conv1 dW mma"};
     const unsigned long long t0 = m[ST_FWD][0];
     fprintf(stderr, "[dqn rank %d] step timeline (us from conv_fwd entry: entry / past wait / exit):", ctx->rank);
     for (int q = 1; q < ST_N; ++q)

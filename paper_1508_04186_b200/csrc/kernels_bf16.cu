@@ -730,6 +730,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  st_stamp(ST_P6, 0);
   const uint32_t tmem = tbase;
   if (warp == 1) {  // db2 = sum of dZ2 over positions (zero rows contribute nothing)
     float s = 0.0f;
@@ -763,6 +764,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
   __syncwarp();
   mbar_wait(&bar, 0);
   tc_fence_after();
+  st_stamp(ST_P6, 1);
   // ---- dZ1 = dA1 * [A1 > 0], into conv1 virtual rows m1 = y*21 + x, planes [n/8][m1][8]
   {
     const int p = 32 * warp + lane;  // s2d(2) pixel row of conv2's input
@@ -795,6 +797,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  st_stamp(ST_P6, 2);
   if (threadIdx.x == 0) {
     // conv1 dW: M = (t pair, c') via 16 X planes, K = m1 (27 steps), N = 16 (B MN-major: dZ1 planes)
     const uint32_t xb = smem_u32(sX), dz1 = smem_u32(sDZ1);
@@ -808,19 +811,28 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
       }
     mma_commit(&bar);
   }
-  // db1 from the dZ1 planes while conv1 dW runs
-  if (threadIdx.x < 16) {
-    const int n = threadIdx.x;
+  // db1 from the dZ1 planes while conv1 dW runs: all 128 threads, channel n = tid % 16 over the
+  // row slice tid / 16 (8 slices of rows), then the 8 slice sums in slice order (deterministic)
+  __shared__ float s_db1_part[8][16];
+  {
+    const int n = threadIdx.x & 15, sl = threadIdx.x >> 4;
+    const __nv_bfloat16* colp = reinterpret_cast<const __nv_bfloat16*>(sDZ1 + (n >> 3) * BWD_ROWS1 * 16) + (n & 7);
     float s = 0.0f;
-    for (int r = 0; r < 420; ++r) {
-      const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(sDZ1 + ((n >> 3) * BWD_ROWS1 + r) * 16);
-      s += __bfloat162float(row[n & 7]);
-    }
-    s_db1[n] = s;
+    for (int r = sl * 53; r < min(420, sl * 53 + 53); ++r) s += __bfloat162float(colp[r * 8]);
+    s_db1_part[sl][n] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    float s = 0.0f;
+#pragma unroll
+    for (int sl = 0; sl < 8; ++sl) s += s_db1_part[sl][threadIdx.x];
+    s_db1[threadIdx.x] = s;
   }
   __syncwarp();
+  st_stamp(ST_P7, 0);
   mbar_wait(&bar, 1);
   tc_fence_after();
+  st_stamp(ST_P7, 1);
   // ---- per-image partials: row = (t, c) of the tile, columns = output channels
   float* part = a.partial + (long long)j * BWD_PART;
   {
