@@ -219,6 +219,7 @@ struct TcGemmArgs {
   int st_id;                // DQN_TRACE_STEP slot (step_trace.cuh), 0 = none
   int st_ph;                // DQN_TRACE_STEP phase slot of tile 0 (staged / MMA done), 0 = none
   int store;                // TC_EPI_ACCUM: 1 = C = D (C known to be zero / overwritten), 0 = C += D
+  int hwc_HW, hwc_C;        // TC_EPI_MASK_T: write feature m = c*HW + p to p*C + c (NHWC dZ), 0: off
 };
 enum { TC_EPI_ACCUM = 0, TC_EPI_FC_FWD = 1, TC_EPI_MASK_T = 2 };
 struct BwdConvArgs {
@@ -233,6 +234,49 @@ struct BwdConvArgs {
   unsigned* counter;
   float* grad;
 };
+// ---- generic bf16 conv path (kernels_conv.cu): every conv as a stride-1 conv over a s2d grid
+struct GConvFwdArgs {
+  const __nv_bfloat16* x[2];       // input grid [b][Hs][Ws][Cs] per group (layers >= 2)
+  const uint8_t* ring[2];          // layer 1: replay rings (s2d u8 slots) or a staging buffer
+  int* idx;                        // layer 1, group 0: sampled slots out (nullptr: not recorded)
+  const DevCounters* ctr;          // layer 1: sampler state (nullptr: image j = slot j)
+  unsigned long long seed;
+  unsigned rank;
+  int first;                       // 1: layer 1 (u8 input, 1/255 folded into the epilogue)
+  int b, Hs, Ws, Cs, Th, Tw, Ho, Wo, N;
+  int s_next;                      // stride of the next conv (its s2d factor), 0: canonical flatten out
+  const __nv_bfloat16* wpk[2];     // packed forward weights [N][Th*Tw*Cs] per group
+  const float* bias[2];            // fp32 canonical biases per group
+  __nv_bfloat16* out[2];
+};
+void launch_gconv_fwd(const GConvFwdArgs& a, int groups, cudaStream_t st);
+struct GConvDgradArgs {
+  const __nv_bfloat16* dz;         // layer output gradient [b][Ho][Wo][N]
+  const __nv_bfloat16* wpkT;       // packed data-gradient weights [Cs][Th*Tw*N]
+  const __nv_bfloat16* xmask;      // the layer input activation [b][Hs][Ws][Cs] (post-ReLU)
+  __nv_bfloat16* dzprev;           // previous layer's output gradient [b][Hs*s][Ws*s][Cs/s^2]
+  int b, Hs, Ws, Cs, Th, Tw, Ho, Wo, N, s;
+};
+void launch_gconv_dgrad(const GConvDgradArgs& a, cudaStream_t st);
+struct GConvWgradArgs {
+  const __nv_bfloat16* x;          // layer input grid (group 0), layers >= 2
+  const uint8_t* ring;             // layer 1: the s ring and the sampled slots
+  const int* idx;
+  int first;
+  const __nv_bfloat16* dz;         // [b][Ho][Wo][N]
+  int b, Hs, Ws, Cs, Th, Tw, Ho, Wo, N, ipc;  // ipc: images per CTA (K range)
+  float* partial;                  // [ranges][Th*Tw*Cs][N]
+  float* partial_db;               // [ranges][N]
+  const int* w_canon;              // per dW row (tap, c'): canonical offset at n = 0 (-1: none)
+  long long w_off, w_nstride, b_off;
+  float* grad;
+  int store;                       // 1: G = sum (n_push = 1), 0: G += sum
+};
+void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st);
+void launch_gpack(const float* theta, __nv_bfloat16* dst, long long img_off, const int2* map, long long n,
+                  cudaStream_t st);
+void init_conv_kernel_attrs();
+
 struct ReduceUpdateArgs {
   BwdConvArgs b;                   // the conv partials and offsets
   float* theta;                    // fp32 theta (= theta_local at N = 1)

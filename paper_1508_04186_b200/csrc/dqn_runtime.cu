@@ -61,6 +61,20 @@ struct dqn_ctx {
   int* diag_amax = nullptr;
   // bf16 tensor-core path (precision == DQN_BF16)
   bool bf16 = false;
+  // generic bf16 conv path (bf16 && not the Mnih stack): per-layer geometry, buffers, pack maps
+  bool gpath = false;
+  struct GLayer {
+    int Hs, Ws, Cs, Th, Tw, Ho, Wo, N, s;   // s: this layer's stride (its input grid is s2d by s)
+    long long fwd_pack, dg_pack;            // offsets of the packed weights after P_pad (-1: none)
+    int ipc;                                // images per wgrad CTA
+    int* w_canon = nullptr;                 // [Th*Tw*Cs]
+    __nv_bfloat16* x[2] = {};               // input grid per group (layers >= 2)
+    __nv_bfloat16* dz = nullptr;            // output gradient [b][Ho][Wo][N]
+  } gl[kMaxConv];
+  int2* pack_map = nullptr;                 // [pack_n]: packed slots of each canonical conv parameter
+  long long pack_n = 0, gpack_off = -1;
+  float* gw_partial = nullptr;
+  float* gw_partial_db = nullptr;
   // DQN_ASYNC: the push -> RMSProp -> publish round runs on comm_stream while
   // the replica keeps stepping; a fetch returns the server theta of one round earlier (lag 1)
   bool async = false;
@@ -224,6 +238,34 @@ static void gaussian_init(std::vector<float>& th, double std_, uint64_t seed) {
   }
 }
 
+// the Mnih-2013 conv stack of BASELINE.json configs[0..3] (the specialised bf16 kernels)
+static bool is_mnih_stack(const dqn_config* c) {
+  return c->frames == 4 && c->height == 84 && c->width == 84 && c->n_conv == 2 && c->conv_filters[0] == 16 &&
+         c->conv_kernel[0] == 8 && c->conv_stride[0] == 4 && c->conv_filters[1] == 32 && c->conv_kernel[1] == 4 &&
+         c->conv_stride[1] == 2 && c->n_fc == 1;
+}
+
+// The generic bf16 conv path's shape contract (kernels_conv.cu); nullptr when supported.
+static const char* gpath_unsupported(const NetShape& net, const dqn_config* c) {
+  if (!(net.F == 4 && net.Hin == 84 && net.Win == 84)) return "DQN_BF16 needs 84x84x4 frame stacks";
+  if (net.n_fc != 1) return "DQN_BF16 needs exactly one hidden FC layer";
+  const ConvShape& L0 = net.conv[0];
+  if (L0.k != 8 || L0.s != 4) return "DQN_BF16: the first conv must be 8x8 / 4 (the replay ring's s2d layout)";
+  for (int i = 0; i < net.n_conv; ++i) {
+    const ConvShape& L = net.conv[i];
+    if (L.N % 16 != 0 || L.N > 256) return "DQN_BF16: conv filters must be a multiple of 16 and <= 256";
+    if (i == 0) continue;
+    if (L.s != 1 && L.s != 2) return "DQN_BF16: conv strides after the first must be 1 or 2";
+    if (L.k % L.s != 0 || L.H % L.s != 0 || L.W % L.s != 0) return "DQN_BF16: k and the input size must be multiples of the stride";
+    if ((L.C * L.s * L.s) % 64 != 0 || L.C * L.s * L.s > 256) return "DQN_BF16: C*s*s must be a multiple of 64 and <= 256";
+    if (L.N % 64 != 0) return "DQN_BF16: filters of convs after the first must be a multiple of 64";
+  }
+  const FcShape& F = net.fc[0];
+  if (F.D % 16 != 0 || F.H % 16 != 0 || F.H > 512) return "DQN_BF16: FC sizes must be multiples of 16 (units <= 512)";
+  if (c->minibatch % 16 != 0 || c->minibatch > 512) return "DQN_BF16 needs minibatch % 16 == 0 and <= 512";
+  return nullptr;
+}
+
 static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   if (!build_net(c, net)) { *why = "invalid layer chain (valid convolutions need integer output sizes)"; return DQN_EINVAL; }
   if (c->n_conv < 1) { *why = "at least one convolution layer is required"; return DQN_EINVAL; }
@@ -244,12 +286,15 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   }
   if (c->precision == DQN_BF16) {
     // the tensor-core kernels are specialised to the Mnih-2013 convolution stack (BASELINE.json configs[0..3])
-    const bool mnih = c->frames == 4 && c->height == 84 && c->width == 84 && c->n_conv == 2 &&
-                      c->conv_filters[0] == 16 && c->conv_kernel[0] == 8 && c->conv_stride[0] == 4 &&
-                      c->conv_filters[1] == 32 && c->conv_kernel[1] == 4 && c->conv_stride[1] == 2 && c->n_fc == 1;
-    if (!mnih) { *why = "DQN_BF16 supports the Mnih-2013 conv stack (conv16 8x8/4, conv32 4x4/2, one FC)"; return DQN_EINVAL; }
-    if (c->minibatch % 16 != 0 || c->minibatch > 256) { *why = "DQN_BF16 needs minibatch % 16 == 0 and <= 256"; return DQN_EINVAL; }
-    if (c->fc_units[0] % 16 != 0 || c->fc_units[0] > 1024) { *why = "DQN_BF16 needs fc units % 16 == 0"; return DQN_EINVAL; }
+    const bool mnih = is_mnih_stack(c);
+    if (mnih) {
+      if (c->minibatch % 16 != 0 || c->minibatch > 256) { *why = "DQN_BF16 needs minibatch % 16 == 0 and <= 256"; return DQN_EINVAL; }
+      if (c->fc_units[0] % 16 != 0 || c->fc_units[0] > 1024) { *why = "DQN_BF16 needs fc units % 16 == 0"; return DQN_EINVAL; }
+      return DQN_OK;
+    }
+    // generic tensor-core conv path (kernels_conv.cu): every conv a stride-1 conv over a s2d grid
+    const char* g = gpath_unsupported(*net, c);
+    if (g) { *why = g; return DQN_EINVAL; }
     return DQN_OK;
   }
   // fp32 kernels stage one input image (+ one filter chunk) in shared memory
@@ -310,6 +355,15 @@ static void free_all(dqn_ctx* c) {
                   c->dh_bf16, c->dz2_bf16, c->fc_partial, c->tc_counters, c->bwd_partial, c->q_stage_s2d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& G : c->gl) {
+    if (G.w_canon) cudaFree(G.w_canon);
+    for (auto* x : G.x)
+      if (x) cudaFree(x);
+    if (G.dz) cudaFree(G.dz);
+  }
+  if (c->pack_map) cudaFree(c->pack_map);
+  if (c->gw_partial) cudaFree(c->gw_partial);
+  if (c->gw_partial_db) cudaFree(c->gw_partial_db);
   for (int i = 0; i < 2; ++i) {
     if (c->h_stage[i]) cudaFreeHost(c->h_stage[i]);
     if (c->ev_stage[i]) cudaEventDestroy(c->ev_stage[i]);
@@ -431,6 +485,93 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   return DQN_OK;
 }
 
+// Generic bf16 conv path (kernels_conv.cu): layer geometry, packed-weight maps, buffers.
+static int setup_gpath(dqn_ctx* ctx) {
+  const NetShape& net = ctx->net;
+  const int b = ctx->cfg.minibatch;
+  int rc;
+  init_bf16_kernel_attrs();
+  init_conv_kernel_attrs();
+  const FcShape& F = net.fc[0];
+  // FC forward split-K: K per split a multiple of 16 dividing D, operands within the 200 KB budget
+  const int BN = std::min(b, 256);
+  ctx->fc_splits = 0;
+  for (int sp = 1; sp <= F.D / 16; ++sp)
+    if (F.D % sp == 0 && (F.D / sp) % 16 == 0 && (long long)(128 + BN) * (F.D / sp) * 2 <= 200 * 1024) {
+      ctx->fc_splits = sp;
+      break;
+    }
+  if (!ctx->fc_splits) return set_err(ctx, DQN_EINVAL, "FC input too large for the tensor-core split-K");
+  long long pk = 0, max_part = 0, max_db = 0;
+  std::vector<int2> map((size_t)(net.conv[net.n_conv - 1].b_off + net.conv[net.n_conv - 1].N), make_int2(-1, -1));
+  for (int i = 0; i < net.n_conv; ++i) {
+    const ConvShape& L = net.conv[i];
+    dqn_ctx::GLayer& G = ctx->gl[i];
+    const int s = i == 0 ? 4 : L.s;
+    G.s = s;
+    G.Hs = i == 0 ? 21 : L.H / s;
+    G.Ws = i == 0 ? 21 : L.W / s;
+    G.Cs = L.C * s * s;
+    G.Th = G.Tw = L.k / s;
+    G.Ho = L.Ho; G.Wo = L.Wo; G.N = L.N;
+    const int T = G.Th * G.Tw, K = T * G.Cs;
+    G.fwd_pack = pk;
+    pk += (long long)L.N * K;
+    G.dg_pack = -1;
+    if (i > 0) {
+      G.dg_pack = pk;
+      pk += (long long)G.Cs * T * L.N;
+    }
+    const int mt = (K + 127) / 128;
+    const int ranges = std::max(1, std::min(b, 296 / mt));
+    G.ipc = (b + ranges - 1) / ranges;
+    const long long nr = (b + G.ipc - 1) / G.ipc;
+    max_part = std::max(max_part, nr * K * L.N);
+    max_db = std::max(max_db, nr * L.N);
+    std::vector<int> canon((size_t)K, -1);
+    for (int t = 0; t < T; ++t)
+      for (int cs = 0; cs < G.Cs; ++cs) {
+        int c, iy, ix;
+        if (i == 0) {  // the ring's s2d order c' = f*16 + iy*4 + ix
+          c = cs / 16; iy = (cs / 4) % 4; ix = cs % 4;
+        } else {       // c' = (iy*s + ix)*C + c
+          c = cs % L.C; iy = (cs / L.C) / s; ix = (cs / L.C) % s;
+        }
+        const int ky = (t / G.Tw) * s + iy, kx = (t % G.Tw) * s + ix;
+        const int off = (c * L.k + ky) * L.k + kx;
+        canon[(size_t)t * G.Cs + cs] = off;
+        for (int n = 0; n < L.N; ++n) {
+          int2& d = map[(size_t)(L.w_off + (long long)n * L.C * L.k * L.k + off)];
+          d.x = (int)(G.fwd_pack + (long long)n * K + (long long)t * G.Cs + cs);
+          if (i > 0) d.y = (int)(G.dg_pack + (long long)cs * T * L.N + (long long)t * L.N + n);
+        }
+      }
+    if ((rc = dalloc(ctx, &G.w_canon, K))) return rc;
+    CK(cudaMemcpy(G.w_canon, canon.data(), sizeof(int) * K, cudaMemcpyHostToDevice));
+    if (i > 0)
+      for (int g = 0; g < 2; ++g)
+        if ((rc = dalloc(ctx, &G.x[g], (long long)b * G.Hs * G.Ws * G.Cs))) return rc;
+    if ((rc = dalloc(ctx, &G.dz, (long long)b * L.Ho * L.Wo * L.N))) return rc;
+  }
+  ctx->pack_n = (long long)map.size();
+  if ((rc = dalloc(ctx, &ctx->pack_map, ctx->pack_n))) return rc;
+  CK(cudaMemcpy(ctx->pack_map, map.data(), sizeof(int2) * map.size(), cudaMemcpyHostToDevice));
+  ctx->img_off = -1;  // no Mnih weight image
+  ctx->gpack_off = ctx->P_pad;
+  ctx->P_bf16 = ctx->P_pad + pk;
+  if ((rc = dalloc(ctx, &ctx->theta_local_bf16, ctx->P_bf16))) return rc;
+  if ((rc = dalloc(ctx, &ctx->theta_hat_bf16, ctx->P_bf16))) return rc;
+  if ((rc = dalloc(ctx, &ctx->a2_bf16, 2LL * b * F.D))) return rc;
+  if ((rc = dalloc(ctx, &ctx->dh_bf16, (long long)b * F.H))) return rc;
+  if ((rc = dalloc(ctx, &ctx->fc_partial, 2LL * ctx->fc_splits * F.H * b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->tc_counters, 64))) return rc;
+  CK(cudaMemsetAsync(ctx->tc_counters, 0, 64 * sizeof(unsigned), ctx->stream));
+  if ((rc = dalloc(ctx, &ctx->q_stage_s2d, (long long)b * kMnihSlot))) return rc;
+  if ((rc = dalloc(ctx, &ctx->gw_partial, max_part))) return rc;
+  if ((rc = dalloc(ctx, &ctx->gw_partial_db, max_db))) return rc;
+  return DQN_OK;
+}
+
 static long long align16(long long x) { return (x + 15) & ~15LL; }
 
 static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world, const void* nccl_unique_id,
@@ -454,6 +595,7 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   ctx->async = cfg->sync_mode == DQN_ASYNC;
   ctx->alias_local = (world == 1 && cfg->n_fetch == 1 && !ctx->async);
   ctx->bf16 = cfg->precision == DQN_BF16;
+  ctx->gpath = ctx->bf16 && !is_mnih_stack(cfg);
 
   if (cuda_stream) {
     ctx->stream = (cudaStream_t)cuda_stream;
@@ -545,7 +687,8 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   if ((rc = dalloc(ctx, &ctx->q_out, qn * net.A))) return rc;
   if ((rc = dalloc(ctx, &ctx->q_amax, qn))) return rc;
   init_head_kernel_attrs();
-  if (ctx->bf16) {
+  if (ctx->gpath && (rc = setup_gpath(ctx))) return rc;
+  if (ctx->bf16 && !ctx->gpath) {
     init_bf16_kernel_attrs();
     const int H = net.fc[0].H;
     ctx->fc_splits = 18;  // K = 2592 = 18 x 144
@@ -592,6 +735,10 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
                        ctx->w2_off);
     launch_f32_to_bf16(ctx->theta_hat, ctx->theta_hat_bf16, ctx->P_pad, ctx->stream, ctx->img_off, ctx->w1_off,
                        ctx->w2_off);
+    if (ctx->gpath) {
+      launch_gpack(ctx->theta_hat, ctx->theta_local_bf16, ctx->gpack_off, ctx->pack_map, ctx->pack_n, ctx->stream);
+      launch_gpack(ctx->theta_hat, ctx->theta_hat_bf16, ctx->gpack_off, ctx->pack_map, ctx->pack_n, ctx->stream);
+    }
     CK(cudaGetLastError());
   }
   if (ctx->async) {  // theta^(0) published in slot 0; the comm stream and its events
@@ -608,6 +755,8 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     if (ctx->bf16)
       launch_f32_to_bf16(ctx->theta_pub[0], ctx->theta_pub_bf16[0], ctx->P_pad, ctx->stream, ctx->img_off, ctx->w1_off,
                          ctx->w2_off);
+    if (ctx->gpath)
+      launch_gpack(ctx->theta_pub[0], ctx->theta_pub_bf16[0], ctx->gpack_off, ctx->pack_map, ctx->pack_n, ctx->stream);
     CK(cudaEventRecord(ctx->ev_gen[0], ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -973,7 +1122,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   h.idx = ctx->idx; h.ring_a = ctx->ring_a; h.ring_r = ctx->ring_r; h.ring_term = ctx->ring_t;
   h.gamma = (float)c.gamma; h.clip = (float)c.err_clip;
   h.grad = ctx->grad; h.dH = ctx->dz_fc[0]; h.dH_bf16 = ctx->dh_bf16;
-  h.fc_partial = ctx->fc_partial; h.fc_splits = gf.splits; h.fc_split_stride = (long long)gf.BN * gf.M;
+  h.fc_partial = ctx->fc_partial; h.fc_splits = gf.splits; h.fc_split_stride = (long long)gf.N * gf.M;
   h.fc_bias[0] = ctx->theta_local + F.b_off; h.fc_bias[1] = ctx->theta_hat + F.b_off;
   h.act_out[0] = ctx->act_fc[0][0]; h.act_out[1] = ctx->act_fc[0][1];
   h.st_id = ST_HEAD;
@@ -1053,7 +1202,177 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   return DQN_OK;
 }
 
+// ------------------------------------------------------------------ one replica step (generic bf16 conv path)
+// gpack (conv weights of theta -> packed images), conv forward per layer (both groups), FC forward
+// (split-K), TD head, FC dW + dX (+ReLU mask, NHWC) + head finish, per layer wgrad (+ range
+// reduction into G) and dgrad, the update. Kernels: kernels_conv.cu, kernels_bf16.cu (tc_gemm).
+static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
+  const NetShape& net = ctx->net;
+  const dqn_config& c = ctx->cfg;
+  const int b = c.minibatch, nl = net.n_conv;
+  const FcShape& F = net.fc[0];
+  const FcShape& O = net.fc[1];
+  cudaStream_t st = ctx->stream;
+  if (ctx->fused_comm) {  // the previous round's deliveries into theta_local, then clear G
+    PB("server_round_acquire", 1);
+    launch_fused_round_acquire(ctx->acq, st);
+    PE();
+  }
+  if (fetch) {  // a13
+    if (ctx->fused_comm) {
+    } else if (ctx->world > 1) {
+      PB("fetch_all_gather", 1);
+      NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
+      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
+      PE();
+    } else if (!ctx->alias_local) {
+      PB("fetch_copy", 1);
+      CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_master, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
+      PE();
+    }
+  }
+  // packed conv weights of the working theta (changed by every update)
+  PB("gpack", 1);
+  launch_gpack(ctx->theta_local, ctx->theta_local_bf16, ctx->gpack_off, ctx->pack_map, ctx->pack_n, st);
+  PE();
+  if (refresh) {  // a14: theta^ <- theta, packed images included
+    PB("target_refresh", 0);
+    if (ctx->fused_comm)
+      NK(ncclAllGather(ctx->theta_master, ctx->theta_hat, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
+    else
+      CK(cudaMemcpyAsync(ctx->theta_hat, ctx->theta_local, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ctx->theta_hat_bf16, ctx->theta_local_bf16, sizeof(__nv_bfloat16) * ctx->P_bf16,
+                       cudaMemcpyDeviceToDevice, st));
+    PE();
+  }
+  // a1-a4s: sample + gather (layer 1) and every conv forward, s with theta and s' with theta^
+  PB("conv_fwd", nl);
+  for (int i = 0; i < nl; ++i) {
+    const ConvShape& L = net.conv[i];
+    const dqn_ctx::GLayer& G = ctx->gl[i];
+    GConvFwdArgs a{};
+    a.first = i == 0;
+    if (i == 0) {
+      a.ring[0] = ctx->ring_s; a.ring[1] = ctx->ring_sn;
+      a.idx = ctx->idx; a.ctr = ctx->ctr; a.seed = c.seed; a.rank = (unsigned)ctx->rank;
+    } else {
+      a.x[0] = G.x[0]; a.x[1] = G.x[1];
+    }
+    a.b = b; a.Hs = G.Hs; a.Ws = G.Ws; a.Cs = G.Cs; a.Th = G.Th; a.Tw = G.Tw; a.Ho = G.Ho; a.Wo = G.Wo; a.N = L.N;
+    a.s_next = i + 1 < nl ? ctx->gl[i + 1].s : 0;
+    a.wpk[0] = ctx->theta_local_bf16 + ctx->gpack_off + G.fwd_pack;
+    a.wpk[1] = ctx->theta_hat_bf16 + ctx->gpack_off + G.fwd_pack;
+    a.bias[0] = ctx->theta_local + L.b_off; a.bias[1] = ctx->theta_hat + L.b_off;
+    for (int g = 0; g < 2; ++g) a.out[g] = i + 1 < nl ? ctx->gl[i + 1].x[g] : ctx->a2_bf16 + (long long)g * b * F.D;
+    launch_gconv_fwd(a, 2, st);
+  }
+  PE();
+  // a5: FC forward, split-K partials (the head reduces them)
+  TcGemmArgs gf{};
+  gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.A[1] = ctx->theta_hat_bf16 + F.w_off; gf.lda = F.D;
+  gf.B[0] = ctx->a2_bf16; gf.B[1] = ctx->a2_bf16 + (long long)b * F.D; gf.ldb = F.D;
+  gf.M = F.H; gf.N = b; gf.K = F.D; gf.BN = std::min(b, 256); gf.kper = F.D / ctx->fc_splits; gf.splits = ctx->fc_splits;
+  gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial; gf.counters = ctx->tc_counters;
+  gf.pre_a = 1; gf.pre_b = 0;
+  gf.bias[0] = ctx->theta_local + F.b_off; gf.bias[1] = ctx->theta_hat + F.b_off;
+  PB("fc1_fwd", 1);
+  launch_tc_gemm(gf, 2, st);
+  PE();
+  // a6 head
+  HeadArgs h{};
+  h.st_id = ST_HEAD;
+  h.act[0] = ctx->act_fc[0][0]; h.act[1] = ctx->act_fc[0][1];
+  h.theta = ctx->theta_local; h.theta_hat = ctx->theta_hat;
+  h.w_off = O.w_off; h.b_off = O.b_off;
+  h.prev_is_fc = 1; h.prev_b_off = F.b_off;
+  h.H = O.D; h.A = O.H; h.b = b;
+  h.idx = ctx->idx; h.ring_a = ctx->ring_a; h.ring_r = ctx->ring_r; h.ring_term = ctx->ring_t;
+  h.gamma = (float)c.gamma; h.clip = (float)c.err_clip;
+  h.grad = ctx->grad; h.dH = ctx->dz_fc[0]; h.dH_bf16 = ctx->dh_bf16;
+  h.fc_partial = ctx->fc_partial; h.fc_splits = gf.splits; h.fc_split_stride = (long long)gf.N * gf.M;
+  h.fc_bias[0] = ctx->theta_local + F.b_off; h.fc_bias[1] = ctx->theta_hat + F.b_off;
+  h.act_out[0] = ctx->act_fc[0][0]; h.act_out[1] = ctx->act_fc[0][1];
+  h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
+  h.s_dq = ctx->head_dq; h.s_act = ctx->head_act; h.s_loss = ctx->head_loss;
+  PB("head_sample", 1);
+  launch_head_f32(h, st, false);
+  PE();
+  // a7: FC dW (plain store at n_push = 1) + FC dX (x ReLU mask, into the last conv's NHWC dZ) + head finish
+  const dqn_ctx::GLayer& GL = ctx->gl[nl - 1];
+  TcGemmArgs gw{};
+  gw.A[0] = ctx->dh_bf16; gw.lda = F.H; gw.a_mn = 1;
+  gw.B[0] = ctx->a2_bf16; gw.ldb = F.D; gw.b_mn = 1;
+  gw.M = F.H; gw.N = F.D; gw.K = b; gw.BN = 64; gw.kper = b; gw.splits = 1;
+  gw.epi = TC_EPI_ACCUM; gw.C[0] = ctx->grad + F.w_off; gw.ldc = F.D; gw.store = c.n_push == 1;
+  gw.pre_a = 0; gw.pre_b = 1;
+  TcGemmArgs gx{};
+  gx.A[0] = ctx->theta_local_bf16 + F.w_off; gx.lda = F.D; gx.a_mn = 1;
+  gx.B[0] = ctx->dh_bf16; gx.ldb = F.H; gx.b_mn = 0;
+  gx.M = F.D; gx.N = b; gx.K = F.H; gx.BN = 64; gx.kper = F.H; gx.splits = 1;
+  gx.epi = TC_EPI_MASK_T; gx.out_bf16 = GL.dz; gx.mask = ctx->a2_bf16; gx.ldo = F.D;
+  gx.hwc_HW = GL.Ho * GL.Wo; gx.hwc_C = GL.N;
+  gx.pre_a = 1; gx.pre_b = 0;
+  PB("fc1_bwd_head_finish", 1);
+  gw.st_id = gx.st_id = ST_FC_BWD;
+  launch_tc_pair_with_head(gw, gx, h, st);
+  PE();
+  // a8/a9: per layer, top down: wgrad (+ range reduction into G), then dgrad into the layer below
+  PB("conv_bwd", 3 * nl - 1);
+  for (int i = nl - 1; i >= 0; --i) {
+    const ConvShape& L = net.conv[i];
+    const dqn_ctx::GLayer& G = ctx->gl[i];
+    GConvWgradArgs w{};
+    w.first = i == 0;
+    if (i == 0) { w.ring = ctx->ring_s; w.idx = ctx->idx; } else { w.x = G.x[0]; }
+    w.dz = G.dz;
+    w.b = b; w.Hs = G.Hs; w.Ws = G.Ws; w.Cs = G.Cs; w.Th = G.Th; w.Tw = G.Tw; w.Ho = G.Ho; w.Wo = G.Wo; w.N = L.N;
+    w.ipc = G.ipc; w.partial = ctx->gw_partial; w.partial_db = ctx->gw_partial_db;
+    w.w_canon = G.w_canon; w.w_off = L.w_off; w.w_nstride = (long long)L.C * L.k * L.k; w.b_off = L.b_off;
+    w.grad = ctx->grad; w.store = c.n_push == 1;
+    launch_gconv_wgrad(w, st);
+    if (i > 0) {
+      GConvDgradArgs d{};
+      d.dz = G.dz; d.wpkT = ctx->theta_local_bf16 + ctx->gpack_off + G.dg_pack; d.xmask = G.x[0];
+      d.dzprev = ctx->gl[i - 1].dz;
+      d.b = b; d.Hs = G.Hs; d.Ws = G.Ws; d.Cs = G.Cs; d.Th = G.Th; d.Tw = G.Tw; d.Ho = G.Ho; d.Wo = G.Wo; d.N = L.N;
+      d.s = G.s;
+      launch_gconv_dgrad(d, st);
+    }
+  }
+  PE();
+  if (ctx->keep_grad)
+    CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
+  // a11 push + a12 shard update (+ a13 fetch in the fused round)
+  if (push) {
+    const float div = (float)((double)ctx->world * c.n_push);
+    const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
+    if (ctx->fused_comm) {
+      PB("server_round_fused", 1);
+      launch_server_round(ctx->sra, st);
+      PE();
+    } else if (ctx->world > 1) {
+      PB("push_reduce_scatter", 0);
+      NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
+      CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
+      PE();
+      PB("rmsprop_update", 1);
+      launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
+                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, st);
+      PE();
+    } else {
+      PB("rmsprop_update", 1);
+      launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
+                     (float)c.rms_eps, nullptr, ctx->alias_local ? ctx->theta_local_bf16 : nullptr, ctx->ctr, 1, st);
+      PE();
+    }
+  }
+  CK(cudaGetLastError());
+  return DQN_OK;
+}
+
 static int enqueue_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
+  if (ctx->gpath) return enqueue_step_gpath(ctx, fetch, refresh, push);
   return ctx->bf16 ? enqueue_step_bf16(ctx, fetch, refresh, push) : enqueue_step_f32(ctx, fetch, refresh, push);
 }
 
@@ -1152,6 +1471,7 @@ static int async_push(dqn_ctx* ctx) {
   }
   if (ctx->bf16)
     launch_f32_to_bf16(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->P_pad, cs, ctx->img_off, ctx->w1_off, ctx->w2_off);
+  if (ctx->gpath) launch_gpack(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->gpack_off, ctx->pack_map, ctx->pack_n, cs);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_gen[s], cs));
   return DQN_OK;
@@ -1421,7 +1741,34 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
     CK(cudaMemcpyAsync(ctx->q_stage, states + i0 * sb, m * sb, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        st));
     const float* in = nullptr;
-    if (ctx->bf16) {  // conv1's s2d staging, then the tensor-core forward with theta_local
+    if (ctx->gpath) {  // s2d staging, the generic tensor-core conv forward, FC split-K + reduction
+      const FcShape& F = net.fc[0];
+      launch_push_s2d(ctx->q_stage_s2d, nullptr, nullptr, nullptr, nullptr, b, 0, 0, m, ctx->q_stage, nullptr,
+                      nullptr, nullptr, nullptr, st);
+      for (int i = 0; i < net.n_conv; ++i) {
+        const ConvShape& L = net.conv[i];
+        const dqn_ctx::GLayer& G = ctx->gl[i];
+        GConvFwdArgs a{};
+        a.first = i == 0;
+        if (i == 0) a.ring[0] = ctx->q_stage_s2d;  // ctr == nullptr: image j = slot j
+        else a.x[0] = G.x[0];
+        a.b = m; a.Hs = G.Hs; a.Ws = G.Ws; a.Cs = G.Cs; a.Th = G.Th; a.Tw = G.Tw; a.Ho = G.Ho; a.Wo = G.Wo; a.N = L.N;
+        a.s_next = i + 1 < net.n_conv ? ctx->gl[i + 1].s : 0;
+        a.wpk[0] = ctx->theta_local_bf16 + ctx->gpack_off + G.fwd_pack;
+        a.bias[0] = ctx->theta_local + L.b_off;
+        a.out[0] = i + 1 < net.n_conv ? ctx->gl[i + 1].x[0] : ctx->a2_bf16;
+        launch_gconv_fwd(a, 1, st);
+      }
+      TcGemmArgs gf{};
+      gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.lda = F.D;
+      gf.B[0] = ctx->a2_bf16; gf.ldb = F.D;
+      gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = std::min(256, (m + 15) / 16 * 16); gf.kper = F.D / ctx->fc_splits;
+      gf.splits = ctx->fc_splits; gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
+      gf.pre_a = 1; gf.pre_b = 0;
+      gf.counters = ctx->tc_counters; gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
+      launch_tc_gemm(gf, 1, st);
+      in = ctx->act_fc[0][0];
+    } else if (ctx->bf16) {  // conv1's s2d staging, then the tensor-core forward with theta_local
       const FcShape& F = net.fc[0];
       launch_push_s2d(ctx->q_stage_s2d, nullptr, nullptr, nullptr, nullptr, b, 0, 0, m, ctx->q_stage, nullptr,
                       nullptr, nullptr, nullptr, st);

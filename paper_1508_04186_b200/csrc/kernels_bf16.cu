@@ -491,20 +491,22 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + c + i;
+          const long long om = a.hwc_HW ? (long long)(m % a.hwc_HW) * a.hwc_C + m / a.hwc_HW : (long long)m;
           if (n < a.N)  // bf16 > 0 <=> sign bit clear and not +0
-            a.out_bf16[(long long)n * a.ldo + m] = __float2bfloat16_rn((mk[i] & 0x8000u) == 0 && mk[i] != 0 ? v[i] : 0.0f);
+            a.out_bf16[(long long)n * a.ldo + om] = __float2bfloat16_rn((mk[i] & 0x8000u) == 0 && mk[i] != 0 ? v[i] : 0.0f);
         }
       }
       if (ph && c < 48) st_stamp_here(ST_P6, c / 16);
     }
   } else {  // TC_EPI_FC_FWD: split partials, transposed to [g][split][n][m] (coalesced over m)
-    float* pbase = a.partial + ((long long)g * a.splits + split) * (long long)a.BN * a.M;
+    float* pbase = a.partial + ((long long)g * a.splits + split) * (long long)a.N * a.M;
     for (int c = 0; c < bn; c += 16) {
       float v[16];
       tmem_ld16(trow + c, v);
       if (m < a.M) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pbase[(long long)(n0 + c + i) * a.M + m] = v[i];
+        for (int i = 0; i < 16; ++i)
+          if (n0 + c + i < a.N) pbase[(long long)(n0 + c + i) * a.M + m] = v[i];  // split stride is N*M
       }
     }
   }
@@ -572,10 +574,10 @@ __global__ void fc_reduce_kernel(TcGemmArgs a) {
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= (long long)a.M * a.N) return;
   const int n = (int)(e / a.M), m = (int)(e % a.M);
-  const float* p = a.partial + (long long)g * a.splits * a.BN * a.M + (long long)n * a.M + m;
+  const float* p = a.partial + (long long)g * a.splits * a.N * a.M + (long long)n * a.M + m;
   float s = 0.0f;
 #pragma unroll 6
-  for (int sp = 0; sp < a.splits; ++sp) s += p[(long long)sp * a.BN * a.M];
+  for (int sp = 0; sp < a.splits; ++sp) s += p[(long long)sp * a.N * a.M];
   a.h_out[g][(long long)n * a.M + m] = fmaxf(s + a.bias[g][m], 0.0f);
 }
 

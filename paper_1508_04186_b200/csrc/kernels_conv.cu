@@ -1,0 +1,552 @@
+// kernels_conv.cu — the generic bf16 tensor-core conv path (a3/a4/a4s forward, a8/a9 backward)
+// for conv stacks other than the Mnih-2013 one, e.g. the scaled net of BASELINE.json configs[4]
+// (conv32 8x8/4, conv64 4x4/2, conv64 3x3/1).
+//
+// Every k x k / s convolution is a stride-1 convolution with kt = k/s taps per axis over a
+// space-to-depth grid (Hs, Ws, Cs = C*s*s), so one implicit-GEMM kernel shape covers all layers.
+// Activations live in HBM as [image][y][x][channel] bf16 (channels contiguous: one 16-byte chunk
+// = 8 channels of one pixel). Channel order of a s2d grid: layer 1 reads the replay ring's order
+// c' = f*16 + iy*4 + ix (push_s2d); later layers use c' = (iy*s + ix)*C + c, written directly by
+// the previous layer's epilogue. Weights are read from "packed images" inside the bf16 theta
+// buffer (the update writes them; pack maps computed at create): forward [N][K], K = tap*Cs + c'
+// and data-gradient [Cs][T*N].
+//
+// Three tcgen05 kernels, M = 128 rows per CTA, 128 threads, K staged in chunks of 64 with a
+// two-stage cp.async pipeline, fp32 accumulators in TMEM:
+//   gconv_fwd   rows = output pixels of 128 (image, y, x); K = (tap, c'); N = Cout
+//               epilogue: (x 1/255 on layer 1) + bias, ReLU, bf16 into the next layer's grid or
+//               the canonical (C,H,W) flatten of the FC input
+//   gconv_dgrad rows = input-grid pixels; K = (tap, n) over dZ shifted back by the tap; N = Cs
+//               epilogue: x [input activation > 0] (ReLU'), scattered back to the previous
+//               layer's output grid (inverse space-to-depth) as its dZ
+//   gconv_wgrad rows = (tap, c') of dW; K = (image, output pixel) over a range of images;
+//               N = Cout; both operands MN-major; per-range partials (+ db), reduced in range
+//               order by gconv_wreduce into G (deterministic)
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <unistd.h>
+#include "dqn_internal.h"
+#include "pdl.cuh"
+#include "philox.cuh"
+#include "sm100.cuh"
+#include "step_trace.cuh"
+
+namespace dqn {
+using namespace dqn_sm100;
+
+namespace {
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// 8 u8 (two words) -> 8 exact bf16 as one 16-byte chunk
+__device__ __forceinline__ uint4 u8x8_to_bf16(uint32_t w0, uint32_t w1) {
+  return make_uint4(pack2((float)(w0 & 0xFF), (float)((w0 >> 8) & 0xFF)),
+                    pack2((float)((w0 >> 16) & 0xFF), (float)(w0 >> 24)),
+                    pack2((float)(w1 & 0xFF), (float)((w1 >> 8) & 0xFF)),
+                    pack2((float)((w1 >> 16) & 0xFF), (float)(w1 >> 24)));
+}
+// bounded mbarrier wait: a lost MMA completion is recorded (g_gconv_err) and the wait abandoned,
+// so a bug cannot hang the GPU; the host reports it (gconv_debug / dqn_train_steps)
+__device__ unsigned long long g_gconv_err;
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity, int where) {
+  uint32_t done;
+  long long n = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (!done && ++n > (1LL << 24)) {
+      atomicExch(&g_gconv_err, ((unsigned long long)where << 48) | ((unsigned long long)blockIdx.y << 32) |
+                                   ((unsigned long long)blockIdx.x << 8) | parity);
+      return;
+    }
+  } while (!done);
+}
+// bf16 bits > 0 (sign clear, not +0)
+__device__ __forceinline__ bool bf16_pos(uint32_t h) { return (h & 0x8000u) == 0 && (h & 0x7FFFu) != 0; }
+
+constexpr int KCH = 64;                     // K per pipeline chunk
+constexpr int A_BYTES = 128 * KCH * 2;      // 16 KB
+constexpr int B_MAX_BYTES = 256 * KCH * 2;  // 32 KB (N <= 256)
+constexpr int STAGE_BYTES = A_BYTES + B_MAX_BYTES;
+constexpr int GCONV_SMEM = 2 * STAGE_BYTES;  // 96 KB
+
+// One MMA K-chunk (64 = 4 x K16) from the stage buffers; A and B K-major [kc][rows][8] or
+// MN-major [rows/8][k][8] as flagged.
+__device__ __forceinline__ void issue_chunk(uint32_t tmem, uint32_t sa, uint32_t sb, int nB, bool a_mn, bool b_mn,
+                                            bool first_chunk) {
+  const uint32_t idesc = make_idesc_bf16(128, nB, a_mn, b_mn);
+#pragma unroll
+  for (int kk = 0; kk < KCH / 16; ++kk) {
+    const uint64_t ad = a_mn ? make_desc(sa + kk * 256, 128, KCH * 16) : make_desc(sa + (2 * kk) * 128 * 16, 128 * 16, 128);
+    const uint64_t bd = b_mn ? make_desc(sb + kk * 256, 128, KCH * 16) : make_desc(sb + (2 * kk) * nB * 16, nB * 16, 128);
+    mma_bf16(tmem, ad, bd, idesc, (!first_chunk || kk > 0) ? 1u : 0u);
+  }
+}
+
+}  // namespace
+
+// DQN_GCONV_DEBUG=1: per-CTA progress codes in mapped host memory, readable while a kernel runs
+__device__ unsigned* g_prog;
+__device__ __forceinline__ void prog(unsigned code) {
+  if (g_prog && threadIdx.x == 0) {
+    *(volatile unsigned*)(g_prog + blockIdx.y * 4096 + blockIdx.x) = code;
+    __threadfence_system();
+  }
+}
+static unsigned* h_prog = nullptr;
+
+// DQN_GCONV_DEBUG=1: wait for every generic-path launch (bounded) and name a kernel that hangs
+static void gconv_debug(const char* what, cudaStream_t st) {
+  static int on = -1;
+  if (on < 0) on = getenv("DQN_GCONV_DEBUG") ? atoi(getenv("DQN_GCONV_DEBUG")) : 0;
+  if (!on) return;
+  if (!h_prog) {
+    cudaHostAlloc(reinterpret_cast<void**>(&h_prog), 8192 * sizeof(unsigned), cudaHostAllocMapped);
+    unsigned* d = nullptr;
+    cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h_prog, 0);
+    cudaMemcpyToSymbol(g_prog, &d, sizeof(d));
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "gconv debug: launch of %s: %s\n", what, cudaGetErrorString(e));
+  for (int i = 0; i < 5000; ++i) {
+    e = cudaStreamQuery(st);
+    if (e != cudaErrorNotReady) {
+      unsigned long long err = 0;
+      cudaMemcpyFromSymbol(&err, g_gconv_err, sizeof(err));
+      fprintf(stderr, "gconv debug: %s done (%s) err %llx\n", what, cudaGetErrorString(e), err);
+      return;
+    }
+    usleep(1000);
+  }
+  fprintf(stderr, "gconv debug: %s still running after 5 s; progress codes:", what);
+  for (int i = 0; i < 64; ++i) fprintf(stderr, " %u", h_prog[i]);
+  fprintf(stderr, "\n");
+  fflush(stderr);
+  _exit(3);
+}
+
+// ------------------------------------------------------------------ forward
+__global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tbase;
+  const int g = blockIdx.y, tid = threadIdx.x, warp = tid >> 5;
+  const int HoWo = a.Ho * a.Wo, T = a.Th * a.Tw, cbn = a.Cs / KCH, nch = T * cbn, K = T * a.Cs;
+  const long long M = (long long)a.b * HoWo;
+  const long long m0 = (long long)blockIdx.x * 128;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  prog(1);
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  prog(2);
+  // this thread's A row
+  const long long m = m0 + tid;
+  const bool row_ok = m < M;
+  int img = 0, oy = 0, ox = 0;
+  if (row_ok) {
+    img = (int)(m / HoWo);
+    const int p = (int)(m % HoWo);
+    oy = p / a.Wo;
+    ox = p % a.Wo;
+  }
+  pdl_sync();  // the input grid / replay slots and the packed weights come from earlier launches
+  prog(3);
+  const uint8_t* xrow8 = nullptr;
+  const __nv_bfloat16* xrow = nullptr;
+  if (row_ok) {
+    if (a.first) {
+      long long slot;
+      if (a.ctr) {
+        slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)img, a.ctr->ring_size);  // a1
+        if (g == 0 && oy == 0 && ox == 0 && a.idx) a.idx[img] = (int)slot;
+      } else {
+        slot = img;  // staging buffer: image j = slot j
+      }
+      xrow8 = a.ring[g] + slot * (long long)a.Hs * a.Ws * a.Cs;
+    } else {
+      xrow = a.x[g] + (long long)img * a.Hs * a.Ws * a.Cs;
+    }
+  }
+  const __nv_bfloat16* W = a.wpk[g];
+  __syncthreads();
+  auto stage = [&](int c, int buf) {
+    uint8_t* sA = smem + buf * STAGE_BYTES;
+    uint8_t* sB = sA + A_BYTES;
+    const int t = c / cbn, cb = c % cbn;
+    const int ty = t / a.Tw, tx = t % a.Tw;
+    // A: this thread's row, 64 channels of tap t = 8 chunks -> [kc][128][8]
+    if (row_ok) {
+      const long long pix = (long long)(oy + ty) * a.Ws + (ox + tx);
+      if (a.first) {
+        const uint4* src = reinterpret_cast<const uint4*>(xrow8 + pix * a.Cs + cb * KCH);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 v = __ldg(src + q);
+          *reinterpret_cast<uint4*>(sA + ((2 * q) * 128 + tid) * 16) = u8x8_to_bf16(v.x, v.y);
+          *reinterpret_cast<uint4*>(sA + ((2 * q + 1) * 128 + tid) * 16) = u8x8_to_bf16(v.z, v.w);
+        }
+      } else {
+        const __nv_bfloat16* src = xrow + pix * a.Cs + cb * KCH;
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc) cp_async16(sA + (kc * 128 + tid) * 16, src + 8 * kc);
+      }
+    } else {
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) *reinterpret_cast<uint4*>(sA + (kc * 128 + tid) * 16) = make_uint4(0, 0, 0, 0);
+    }
+    // B: N rows x 8 chunks of the packed [N][K] weights
+    for (int e = tid; e < a.N * 8; e += 128) {
+      const int n = e >> 3, kc = e & 7;
+      cp_async16(sB + (kc * a.N + n) * 16, W + (long long)n * K + c * KCH + 8 * kc);
+    }
+    cp_async_commit();
+  };
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      if (c >= 1) mbar_wait_bounded(&bar[buf ^ 1], ((c - 1) >> 1) & 1, 1);  // chunk c-1's MMAs released that buffer
+      stage(c + 1, buf ^ 1);
+      cp_async_wait_n<1>();
+    } else {
+      cp_async_wait_n<0>();
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + buf * STAGE_BYTES);
+      issue_chunk(tbase, sa, sa + A_BYTES, a.N, false, false, c == 0);
+      mma_commit(&bar[buf]);
+    }
+    prog(10 + c);
+  }
+  mbar_wait_bounded(&bar[(nch - 1) & 1], ((nch - 1) >> 1) & 1, 3);
+  tc_fence_after();
+  prog(100);
+  // ---- epilogue: row m, N columns (tcgen05.ld is warp-collective: every lane loads, valid rows store)
+  {
+    const float* bias = a.bias[g];
+    const float scale = a.first ? 1.0f / 255.0f : 1.0f;
+    const uint32_t trow = tbase + ((uint32_t)(32 * warp) << 16);
+    __nv_bfloat16* out = a.out[g];
+    for (int c0 = 0; c0 < a.N; c0 += 16) {
+      float v[16];
+      tmem_ld16(trow + c0, v);
+      if (!row_ok) continue;
+      uint32_t o[8];
+#pragma unroll
+      for (int i = 0; i < 16; i += 2)
+        o[i >> 1] = pack2(fmaxf(fmaf(v[i], scale, __ldg(bias + c0 + i)), 0.0f),
+                          fmaxf(fmaf(v[i + 1], scale, __ldg(bias + c0 + i + 1)), 0.0f));
+      if (a.s_next == 0) {  // canonical (C,H,W) flatten: out[img][n*HoWo + p]
+        __nv_bfloat16* dst = out + (long long)img * a.N * HoWo + (long long)oy * a.Wo + ox;
+        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(o);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dst[(long long)(c0 + i) * HoWo] = hv[i];
+      } else {  // next grid (s2d by s_next): pixel (oy/s, ox/s), channel (iy*s + ix)*N + n
+        const int s = a.s_next, Wn = a.Wo / s, Cn = a.N * s * s;
+        const int py = oy / s, px = ox / s, q = (oy % s) * s + (ox % s);
+        if (oy < (a.Ho / s) * s && ox < Wn * s) {  // rows beyond the next grid are never read
+          uint4* dst = reinterpret_cast<uint4*>(out + (((long long)img * (a.Ho / s) + py) * Wn + px) * Cn + q * a.N + c0);
+          dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+          dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+
+void launch_gconv_fwd(const GConvFwdArgs& a, int groups, cudaStream_t st) {
+  const long long M = (long long)a.b * a.Ho * a.Wo;
+  launch_pdl(gconv_fwd_kernel, dim3((unsigned)((M + 127) / 128), groups), dim3(128), GCONV_SMEM, st, a);
+  gconv_debug("gconv_fwd", st);
+}
+
+// ------------------------------------------------------------------ data gradient
+__global__ void __launch_bounds__(128) gconv_dgrad_kernel(GConvDgradArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int T = a.Th * a.Tw, nbn = a.N / KCH, nch = T * nbn, KT = T * a.N;
+  const int HsWs = a.Hs * a.Ws;
+  const long long M = (long long)a.b * HsWs;
+  const long long m = (long long)blockIdx.x * 128 + tid;
+  const bool row_ok = m < M;
+  int img = 0, py = 0, px = 0;
+  if (row_ok) {
+    img = (int)(m / HsWs);
+    const int p = (int)(m % HsWs);
+    py = p / a.Ws;
+    px = p % a.Ws;
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  pdl_sync();
+  __syncthreads();
+  auto stage = [&](int c, int buf) {
+    uint8_t* sA = smem + buf * STAGE_BYTES;
+    uint8_t* sB = sA + A_BYTES;
+    const int t = c / nbn, nb = c % nbn;
+    const int ty = t / a.Tw, tx = t % a.Tw;
+    const int oy = py - ty, ox = px - tx;  // dX[i] = sum_t W_t^T dZ[i - t]
+    if (row_ok && oy >= 0 && oy < a.Ho && ox >= 0 && ox < a.Wo) {
+      const __nv_bfloat16* src = a.dz + (((long long)img * a.Ho + oy) * a.Wo + ox) * a.N + nb * KCH;
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) cp_async16(sA + (kc * 128 + tid) * 16, src + 8 * kc);
+    } else {
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) *reinterpret_cast<uint4*>(sA + (kc * 128 + tid) * 16) = make_uint4(0, 0, 0, 0);
+    }
+    for (int e = tid; e < a.Cs * 8; e += 128) {
+      const int n = e >> 3, kc = e & 7;
+      cp_async16(sB + (kc * a.Cs + n) * 16, a.wpkT + (long long)n * KT + c * KCH + 8 * kc);
+    }
+    cp_async_commit();
+  };
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      if (c >= 1) mbar_wait_bounded(&bar[buf ^ 1], ((c - 1) >> 1) & 1, 2);
+      stage(c + 1, buf ^ 1);
+      cp_async_wait_n<1>();
+    } else {
+      cp_async_wait_n<0>();
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + buf * STAGE_BYTES);
+      issue_chunk(tbase, sa, sa + A_BYTES, a.Cs, false, false, c == 0);
+      mma_commit(&bar[buf]);
+    }
+  }
+  mbar_wait_bounded(&bar[(nch - 1) & 1], ((nch - 1) >> 1) & 1, 3);
+  tc_fence_after();
+  {  // tcgen05.ld is warp-collective: every lane loads, valid rows store
+    const uint32_t trow = tbase + ((uint32_t)(32 * warp) << 16);
+    const __nv_bfloat16* xm = a.xmask + (long long)m * a.Cs;  // the layer input, same grid
+    const int s = a.s, Cp = a.Cs / (s * s), Wp = a.Ws * s, Hp = a.Hs * s;
+    for (int c0 = 0; c0 < a.Cs; c0 += 16) {
+      float v[16];
+      tmem_ld16(trow + c0, v);
+      if (!row_ok) continue;
+      const uint4 mk0 = *reinterpret_cast<const uint4*>(xm + c0), mk1 = *reinterpret_cast<const uint4*>(xm + c0 + 8);
+      const uint32_t mw[8] = {mk0.x, mk0.y, mk0.z, mk0.w, mk1.x, mk1.y, mk1.z, mk1.w};
+      uint32_t o[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        o[h] = pack2(bf16_pos(mw[h] & 0xFFFFu) ? v[2 * h] : 0.0f, bf16_pos(mw[h] >> 16) ? v[2 * h + 1] : 0.0f);
+      // c' = (iy*s + ix)*Cp + c  ->  previous layer's output pixel (py*s + iy, px*s + ix), channel c
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int cc = c0 + 8 * half, q = cc / Cp, ch = cc % Cp;
+        const int y = py * s + q / s, x = px * s + q % s;
+        uint4* dst = reinterpret_cast<uint4*>(a.dzprev + (((long long)img * Hp + y) * Wp + x) * Cp + ch);
+        *dst = make_uint4(o[4 * half], o[4 * half + 1], o[4 * half + 2], o[4 * half + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+
+void launch_gconv_dgrad(const GConvDgradArgs& a, cudaStream_t st) {
+  const long long M = (long long)a.b * a.Hs * a.Ws;
+  launch_pdl(gconv_dgrad_kernel, dim3((unsigned)((M + 127) / 128)), dim3(128), GCONV_SMEM, st, a);
+  gconv_debug("gconv_dgrad", st);
+}
+
+// ------------------------------------------------------------------ weight gradient
+__global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int T = a.Th * a.Tw, HoWo = a.Ho * a.Wo, MK = T * a.Cs;
+  const int m0 = blockIdx.x * 128, range = blockIdx.y;
+  const int img0 = range * a.ipc, nimg = min(a.ipc, a.b - img0);
+  const int npos = nimg * HoWo, nch = (npos + KCH - 1) / KCH;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  pdl_sync();
+  __syncthreads();
+  const int ng = a.N / 8;
+  float db = 0.0f;  // m-tile 0 CTAs: column sums of dZ over this range (thread n < N)
+  auto stage = [&](int c, int buf) {
+    uint8_t* sA = smem + buf * STAGE_BYTES;
+    uint8_t* sB = sA + A_BYTES;
+    // A MN-major [16 row groups][64 k][8]: rows (tap, c'), k = position of this chunk
+    for (int e = tid; e < 16 * KCH; e += 128) {
+      const int gi = e % 16, k = e / 16;
+      const int q = c * KCH + k, r = m0 + 8 * gi;
+      uint8_t* d = sA + (gi * KCH + k) * 16;
+      if (q < npos && r < MK) {
+        const int im = img0 + q / HoWo, p = q % HoWo;
+        const int t = r / a.Cs, cc = r % a.Cs;
+        const int y = p / a.Wo + t / a.Tw, x = p % a.Wo + t % a.Tw;
+        const long long pix = ((long long)y * a.Ws + x) * a.Cs + cc;
+        if (a.first) {
+          const long long slot = a.idx[im];
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.ring + slot * (long long)a.Hs * a.Ws * a.Cs + pix));
+          *reinterpret_cast<uint4*>(d) = u8x8_to_bf16(v.x, v.y);
+        } else {
+          cp_async16(d, a.x + (long long)im * a.Hs * a.Ws * a.Cs + pix);
+        }
+      } else {
+        *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    // B MN-major [N/8][64 k][8]: dZ[image][p][n..n+7]
+    for (int e = tid; e < ng * KCH; e += 128) {
+      const int gi = e % ng, k = e / ng;
+      const int q = c * KCH + k;
+      uint8_t* d = sB + (gi * KCH + k) * 16;
+      if (q < npos) {
+        const int im = img0 + q / HoWo, p = q % HoWo;
+        cp_async16(d, a.dz + ((long long)im * HoWo + p) * a.N + 8 * gi);
+      } else {
+        *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    cp_async_commit();
+  };
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      if (c >= 1) mbar_wait_bounded(&bar[buf ^ 1], ((c - 1) >> 1) & 1, 2);
+      stage(c + 1, buf ^ 1);
+      cp_async_wait_n<1>();
+    } else {
+      cp_async_wait_n<0>();
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (blockIdx.x == 0 && tid < a.N) {  // db: this chunk's 64 positions of column n, in k order
+      const __nv_bfloat16* col =
+          reinterpret_cast<const __nv_bfloat16*>(smem + buf * STAGE_BYTES + A_BYTES + (tid / 8) * KCH * 16) + (tid % 8);
+      for (int k = 0; k < KCH; ++k) db += __bfloat162float(col[k * 8]);
+    }
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + buf * STAGE_BYTES);
+      issue_chunk(tbase, sa, sa + A_BYTES, a.N, true, true, c == 0);
+      mma_commit(&bar[buf]);
+    }
+  }
+  if (nch > 0) {
+    mbar_wait_bounded(&bar[(nch - 1) & 1], ((nch - 1) >> 1) & 1, 3);
+    tc_fence_after();
+  }
+  // ---- partial[range][row][n]
+  const int r = m0 + 32 * warp + (tid & 31);
+  float* prow = a.partial + ((long long)range * MK + r) * a.N;
+  const uint32_t trow = tbase + ((uint32_t)(32 * warp) << 16);
+  for (int c0 = 0; c0 < a.N; c0 += 16) {
+    float v[16];
+    if (nch > 0) tmem_ld16(trow + c0, v);
+    else
+      for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+    if (r < MK) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(prow + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    }
+  }
+  if (blockIdx.x == 0 && tid < a.N) a.partial_db[(long long)range * a.N + tid] = db;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+
+// G[canonical] (+)= sum over ranges (in range order) of the partials; (x 1/255 on layer 1's W)
+__global__ void gconv_wreduce_kernel(GConvWgradArgs a) {
+  pdl_sync();
+  const int T = a.Th * a.Tw, MK = T * a.Cs;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nw = (long long)MK * a.N;
+  if (e >= nw + a.N) return;
+  const int nr = (a.b + a.ipc - 1) / a.ipc;
+  float s = 0.0f;
+  long long dst;
+  if (e < nw) {
+    const int row = (int)(e / a.N), n = (int)(e % a.N);
+    for (int q = 0; q < nr; ++q) s += a.partial[((long long)q * MK + row) * a.N + n];
+    if (a.first) s *= 1.0f / 255.0f;
+    dst = a.w_canon[row] >= 0 ? a.w_off + (long long)n * a.w_nstride + a.w_canon[row] : -1;
+  } else {
+    const int n = (int)(e - nw);
+    for (int q = 0; q < nr; ++q) s += a.partial_db[(long long)q * a.N + n];
+    dst = a.b_off + n;
+  }
+  if (dst < 0) return;
+  if (a.store) a.grad[dst] = s;
+  else a.grad[dst] += s;
+}
+
+void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
+  const int T = a.Th * a.Tw, MK = T * a.Cs;
+  const int ranges = (a.b + a.ipc - 1) / a.ipc;
+  launch_pdl(gconv_wgrad_kernel, dim3((MK + 127) / 128, ranges), dim3(128), GCONV_SMEM, st, a);
+  gconv_debug("gconv_wgrad", st);
+  const long long n = (long long)MK * a.N + a.N;
+  launch_pdl(gconv_wreduce_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, a);
+  gconv_debug("gconv_wreduce", st);
+}
+
+void init_conv_kernel_attrs() {
+  cudaFuncSetAttribute(gconv_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GCONV_SMEM);
+  cudaFuncSetAttribute(gconv_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GCONV_SMEM);
+  cudaFuncSetAttribute(gconv_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GCONV_SMEM);
+}
+
+// ------------------------------------------------------------------ packed weight images
+// dst[img_off + map[i].x] (and .y) = bf16(theta[i]) for the conv parameters i < n (map < 0: none)
+__global__ void gpack_kernel(const float* theta, __nv_bfloat16* dst, long long img_off, const int2* map, long long n) {
+  pdl_sync();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int2 d = map[i];
+  if (d.x < 0 && d.y < 0) return;
+  const __nv_bfloat16 v = __float2bfloat16_rn(theta[i]);
+  if (d.x >= 0) dst[img_off + d.x] = v;
+  if (d.y >= 0) dst[img_off + d.y] = v;
+}
+
+void launch_gpack(const float* theta, __nv_bfloat16* dst, long long img_off, const int2* map, long long n,
+                  cudaStream_t st) {
+  if (n <= 0) return;
+  launch_pdl(gpack_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, theta, dst, img_off, map, n);
+  gconv_debug("gpack", st);
+}
+
+}  // namespace dqn
