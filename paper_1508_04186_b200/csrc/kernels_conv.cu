@@ -42,6 +42,9 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait_n() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
+}
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&h);
@@ -76,10 +79,21 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
 __device__ __forceinline__ bool bf16_pos(uint32_t h) { return (h & 0x8000u) == 0 && (h & 0x7FFFu) != 0; }
 
 constexpr int KCH = 64;                     // K per pipeline chunk
+constexpr int NS = 3;                       // pipeline stages (chunks in flight)
 constexpr int A_BYTES = 128 * KCH * 2;      // 16 KB
-constexpr int B_MAX_BYTES = 256 * KCH * 2;  // 32 KB (N <= 256)
-constexpr int STAGE_BYTES = A_BYTES + B_MAX_BYTES;
-constexpr int GCONV_SMEM = 2 * STAGE_BYTES;  // 96 KB
+constexpr int U8_BYTES = 128 * KCH;         // layer 1: raw u8 A chunk, converted after its copy lands
+// one stage: A [16 KB] | B [nB x 64 bf16] | (layer 1) u8 A [8 KB]
+__host__ __device__ constexpr int stage_bytes(int nB, int first) {
+  return ((A_BYTES + nB * KCH * 2 + (first ? U8_BYTES : 0)) + 1023) / 1024 * 1024;
+}
+constexpr int GCONV_SMEM_MAX = NS * stage_bytes(256, 1);
+// TMEM columns of an accumulator of n fp32 columns (power of two >= 32): small N leaves room for
+// more co-resident CTAs (these kernels are latency-bound per CTA)
+__device__ __forceinline__ uint32_t tmem_cols(int n) {
+  uint32_t c = 32;
+  while (c < (uint32_t)n) c <<= 1;
+  return c;
+}
 
 // One MMA K-chunk (64 = 4 x K16) from the stage buffers; A and B K-major [kc][rows][8] or
 // MN-major [rows/8][k][8] as flagged.
@@ -139,19 +153,18 @@ static void gconv_debug(const char* what, cudaStream_t st) {
 // ------------------------------------------------------------------ forward
 __global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[NS];
   __shared__ uint32_t tbase;
   const int g = blockIdx.y, tid = threadIdx.x, warp = tid >> 5;
   const int HoWo = a.Ho * a.Wo, T = a.Th * a.Tw, cbn = a.Cs / KCH, nch = T * cbn, K = T * a.Cs;
   const long long M = (long long)a.b * HoWo;
   const long long m0 = (long long)blockIdx.x * 128;
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
   prog(1);
-  if (warp == 0) tmem_alloc(&tbase, 256);
+  if (warp == 0) tmem_alloc(&tbase, tmem_cols(a.N));
   prog(2);
   // this thread's A row
   const long long m = m0 + tid;
@@ -182,23 +195,21 @@ __global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
     }
   }
   const __nv_bfloat16* W = a.wpk[g];
+  const int SB = stage_bytes(a.N, a.first);
   __syncthreads();
   auto stage = [&](int c, int buf) {
-    uint8_t* sA = smem + buf * STAGE_BYTES;
+    uint8_t* sA = smem + buf * SB;
     uint8_t* sB = sA + A_BYTES;
     const int t = c / cbn, cb = c % cbn;
     const int ty = t / a.Tw, tx = t % a.Tw;
     // A: this thread's row, 64 channels of tap t = 8 chunks -> [kc][128][8]
     if (row_ok) {
       const long long pix = (long long)(oy + ty) * a.Ws + (ox + tx);
-      if (a.first) {
-        const uint4* src = reinterpret_cast<const uint4*>(xrow8 + pix * a.Cs + cb * KCH);
+      if (a.first) {  // 64 raw bytes of this row into the u8 area; converted once they land
+        const uint8_t* src = xrow8 + pix * a.Cs + cb * KCH;
+        uint8_t* su = sA + A_BYTES + a.N * KCH * 2 + tid * KCH;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint4 v = __ldg(src + q);
-          *reinterpret_cast<uint4*>(sA + ((2 * q) * 128 + tid) * 16) = u8x8_to_bf16(v.x, v.y);
-          *reinterpret_cast<uint4*>(sA + ((2 * q + 1) * 128 + tid) * 16) = u8x8_to_bf16(v.z, v.w);
-        }
+        for (int q = 0; q < 4; ++q) cp_async16(su + 16 * q, src + 16 * q);
       } else {
         const __nv_bfloat16* src = xrow + pix * a.Cs + cb * KCH;
 #pragma unroll
@@ -215,27 +226,40 @@ __global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
     }
     cp_async_commit();
   };
-  stage(0, 0);
+  for (int c = 0; c < NS - 1; ++c) {  // prologue: chunks 0 .. NS-2 in flight
+    if (c < nch) stage(c, c);
+    else cp_async_commit();
+  }
   for (int c = 0; c < nch; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nch) {
-      if (c >= 1) mbar_wait_bounded(&bar[buf ^ 1], ((c - 1) >> 1) & 1, 1);  // chunk c-1's MMAs released that buffer
-      stage(c + 1, buf ^ 1);
-      cp_async_wait_n<1>();
+    const int buf = c % NS, cn = c + NS - 1;
+    if (cn < nch) {
+      if (c >= 1) mbar_wait_bounded(&bar[(c - 1) % NS], ((c - 1) / NS) & 1, 1);  // chunk c-1 released buffer cn % NS
+      stage(cn, cn % NS);
     } else {
-      cp_async_wait_n<0>();
+      cp_async_commit();  // keeps one group per iteration
+    }
+    cp_async_wait_n<NS - 1>();  // this thread's copies of chunk c have landed
+    if (a.first && row_ok) {  // this thread's own row
+      uint8_t* sA = smem + buf * SB;
+      const uint4* su = reinterpret_cast<const uint4*>(sA + A_BYTES + a.N * KCH * 2 + tid * KCH);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = su[q];
+        *reinterpret_cast<uint4*>(sA + ((2 * q) * 128 + tid) * 16) = u8x8_to_bf16(v.x, v.y);
+        *reinterpret_cast<uint4*>(sA + ((2 * q + 1) * 128 + tid) * 16) = u8x8_to_bf16(v.z, v.w);
+      }
     }
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + buf * STAGE_BYTES);
+      const uint32_t sa = smem_u32(smem + buf * SB);
       issue_chunk(tbase, sa, sa + A_BYTES, a.N, false, false, c == 0);
       mma_commit(&bar[buf]);
     }
     prog(10 + c);
   }
-  mbar_wait_bounded(&bar[(nch - 1) & 1], ((nch - 1) >> 1) & 1, 3);
+  mbar_wait_bounded(&bar[(nch - 1) % NS], ((nch - 1) / NS) & 1, 3);
   tc_fence_after();
   prog(100);
   // ---- epilogue: row m, N columns (tcgen05.ld is warp-collective: every lane loads, valid rows store)
@@ -271,19 +295,20 @@ __global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, 256);
+  if (warp == 0) tmem_dealloc(tbase, tmem_cols(a.N));
 }
 
 void launch_gconv_fwd(const GConvFwdArgs& a, int groups, cudaStream_t st) {
   const long long M = (long long)a.b * a.Ho * a.Wo;
-  launch_pdl(gconv_fwd_kernel, dim3((unsigned)((M + 127) / 128), groups), dim3(128), GCONV_SMEM, st, a);
+  launch_pdl(gconv_fwd_kernel, dim3((unsigned)((M + 127) / 128), groups), dim3(128), NS * stage_bytes(a.N, a.first),
+             st, a);
   gconv_debug("gconv_fwd", st);
 }
 
 // ------------------------------------------------------------------ data gradient
 __global__ void __launch_bounds__(128) gconv_dgrad_kernel(GConvDgradArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[NS];
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int T = a.Th * a.Tw, nbn = a.N / KCH, nch = T * nbn, KT = T * a.N;
@@ -299,15 +324,15 @@ __global__ void __launch_bounds__(128) gconv_dgrad_kernel(GConvDgradArgs a) {
     px = p % a.Ws;
   }
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(&tbase, 256);
+  if (warp == 0) tmem_alloc(&tbase, tmem_cols(a.Cs));
   pdl_sync();
+  const int SB = stage_bytes(a.Cs, 0);
   __syncthreads();
   auto stage = [&](int c, int buf) {
-    uint8_t* sA = smem + buf * STAGE_BYTES;
+    uint8_t* sA = smem + buf * SB;
     uint8_t* sB = sA + A_BYTES;
     const int t = c / nbn, nb = c % nbn;
     const int ty = t / a.Tw, tx = t % a.Tw;
@@ -326,26 +351,29 @@ __global__ void __launch_bounds__(128) gconv_dgrad_kernel(GConvDgradArgs a) {
     }
     cp_async_commit();
   };
-  stage(0, 0);
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nch) stage(c, c);
+    else cp_async_commit();
+  }
   for (int c = 0; c < nch; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nch) {
-      if (c >= 1) mbar_wait_bounded(&bar[buf ^ 1], ((c - 1) >> 1) & 1, 2);
-      stage(c + 1, buf ^ 1);
-      cp_async_wait_n<1>();
+    const int buf = c % NS, cn = c + NS - 1;
+    if (cn < nch) {
+      if (c >= 1) mbar_wait_bounded(&bar[(c - 1) % NS], ((c - 1) / NS) & 1, 2);
+      stage(cn, cn % NS);
     } else {
-      cp_async_wait_n<0>();
+      cp_async_commit();
     }
+    cp_async_wait_n<NS - 1>();
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + buf * STAGE_BYTES);
+      const uint32_t sa = smem_u32(smem + buf * SB);
       issue_chunk(tbase, sa, sa + A_BYTES, a.Cs, false, false, c == 0);
       mma_commit(&bar[buf]);
     }
   }
-  mbar_wait_bounded(&bar[(nch - 1) & 1], ((nch - 1) >> 1) & 1, 3);
+  mbar_wait_bounded(&bar[(nch - 1) % NS], ((nch - 1) / NS) & 1, 3);
   tc_fence_after();
   {  // tcgen05.ld is warp-collective: every lane loads, valid rows store
     const uint32_t trow = tbase + ((uint32_t)(32 * warp) << 16);
@@ -373,19 +401,19 @@ __global__ void __launch_bounds__(128) gconv_dgrad_kernel(GConvDgradArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, 256);
+  if (warp == 0) tmem_dealloc(tbase, tmem_cols(a.Cs));
 }
 
 void launch_gconv_dgrad(const GConvDgradArgs& a, cudaStream_t st) {
   const long long M = (long long)a.b * a.Hs * a.Ws;
-  launch_pdl(gconv_dgrad_kernel, dim3((unsigned)((M + 127) / 128)), dim3(128), GCONV_SMEM, st, a);
+  launch_pdl(gconv_dgrad_kernel, dim3((unsigned)((M + 127) / 128)), dim3(128), NS * stage_bytes(a.Cs, 0), st, a);
   gconv_debug("gconv_dgrad", st);
 }
 
 // ------------------------------------------------------------------ weight gradient
 __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[NS];
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int T = a.Th * a.Tw, HoWo = a.Ho * a.Wo, MK = T * a.Cs;
@@ -393,17 +421,20 @@ __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
   const int img0 = range * a.ipc, nimg = min(a.ipc, a.b - img0);
   const int npos = nimg * HoWo, nch = (npos + KCH - 1) / KCH;
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(&tbase, 256);
+  if (warp == 0) tmem_alloc(&tbase, tmem_cols(a.N));
   pdl_sync();
+  const int SB = stage_bytes(a.N, a.first);
+  const int U8OFF = A_BYTES + a.N * KCH * 2;  // layer 1's raw pieces inside a stage
   __syncthreads();
   const int ng = a.N / 8;
-  float db = 0.0f;  // m-tile 0 CTAs: column sums of dZ over this range (thread n < N)
+  // db (m-tile 0 CTAs): column sums of dZ over this range. Thread tid always sees column group
+  // tid % ng of the staged B chunks (128 % ng == 0) and keeps 8 running sums; combined at the end
+  float dbacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   auto stage = [&](int c, int buf) {
-    uint8_t* sA = smem + buf * STAGE_BYTES;
+    uint8_t* sA = smem + buf * SB;
     uint8_t* sB = sA + A_BYTES;
     // A MN-major [16 row groups][64 k][8]: rows (tap, c'), k = position of this chunk
     for (int e = tid; e < 16 * KCH; e += 128) {
@@ -415,10 +446,9 @@ __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
         const int t = r / a.Cs, cc = r % a.Cs;
         const int y = p / a.Wo + t / a.Tw, x = p % a.Wo + t % a.Tw;
         const long long pix = ((long long)y * a.Ws + x) * a.Cs + cc;
-        if (a.first) {
+        if (a.first) {  // 8 raw bytes into the u8 area (piece e), converted after the wait
           const long long slot = a.idx[im];
-          const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.ring + slot * (long long)a.Hs * a.Ws * a.Cs + pix));
-          *reinterpret_cast<uint4*>(d) = u8x8_to_bf16(v.x, v.y);
+          cp_async8(sA + U8OFF + e * 8, a.ring + slot * (long long)a.Hs * a.Ws * a.Cs + pix);
         } else {
           cp_async16(d, a.x + (long long)im * a.Hs * a.Ws * a.Cs + pix);
         }
@@ -440,32 +470,54 @@ __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
     }
     cp_async_commit();
   };
-  stage(0, 0);
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nch) stage(c, c);
+    else cp_async_commit();
+  }
   for (int c = 0; c < nch; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nch) {
-      if (c >= 1) mbar_wait_bounded(&bar[buf ^ 1], ((c - 1) >> 1) & 1, 2);
-      stage(c + 1, buf ^ 1);
-      cp_async_wait_n<1>();
+    const int buf = c % NS, cn = c + NS - 1;
+    if (cn < nch) {
+      if (c >= 1) mbar_wait_bounded(&bar[(c - 1) % NS], ((c - 1) / NS) & 1, 2);
+      stage(cn, cn % NS);
     } else {
-      cp_async_wait_n<0>();
+      cp_async_commit();
+    }
+    cp_async_wait_n<NS - 1>();
+    if (a.first) {  // convert the pieces this thread copied (same e sequence as the stage)
+      uint8_t* sA = smem + buf * SB;
+      for (int e = tid; e < 16 * KCH; e += 128) {
+        const int gi = e % 16, k = e / 16;
+        const int q = c * KCH + k, r = m0 + 8 * gi;
+        if (q < npos && r < MK) {
+          const uint2 v = *reinterpret_cast<const uint2*>(sA + U8OFF + e * 8);
+          *reinterpret_cast<uint4*>(sA + (gi * KCH + k) * 16) = u8x8_to_bf16(v.x, v.y);
+        }
+      }
     }
     fence_async_smem();
     __syncthreads();
-    if (blockIdx.x == 0 && tid < a.N) {  // db: this chunk's 64 positions of column n, in k order
-      const __nv_bfloat16* col =
-          reinterpret_cast<const __nv_bfloat16*>(smem + buf * STAGE_BYTES + A_BYTES + (tid / 8) * KCH * 16) + (tid % 8);
-      for (int k = 0; k < KCH; ++k) db += __bfloat162float(col[k * 8]);
+    if (blockIdx.x == 0) {  // db: 16-byte rows of the B chunk, 8 columns at a time
+      const uint8_t* sB = smem + buf * SB + A_BYTES;
+      for (int e = tid; e < ng * KCH; e += 128) {
+        const int gi = e % ng, k = e / ng;
+        const uint4 v = *reinterpret_cast<const uint4*>(sB + (gi * KCH + k) * 16);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          dbacc[2 * h] += __uint_as_float(w[h] << 16);
+          dbacc[2 * h + 1] += __uint_as_float(w[h] & 0xFFFF0000u);
+        }
+      }
     }
     if (tid == 0) {
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + buf * STAGE_BYTES);
+      const uint32_t sa = smem_u32(smem + buf * SB);
       issue_chunk(tbase, sa, sa + A_BYTES, a.N, true, true, c == 0);
       mma_commit(&bar[buf]);
     }
   }
   if (nch > 0) {
-    mbar_wait_bounded(&bar[(nch - 1) & 1], ((nch - 1) >> 1) & 1, 3);
+    mbar_wait_bounded(&bar[(nch - 1) % NS], ((nch - 1) / NS) & 1, 3);
     tc_fence_after();
   }
   // ---- partial[range][row][n]
@@ -482,10 +534,22 @@ __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
       for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(prow + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     }
   }
-  if (blockIdx.x == 0 && tid < a.N) a.partial_db[(long long)range * a.N + tid] = db;
+  if (blockIdx.x == 0) {  // combine the per-thread sums of each column group in thread order
+    float* s_db = reinterpret_cast<float*>(smem);  // the stage buffers are free (all MMAs done)
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s_db[tid * 8 + i] = dbacc[i];
+    __syncthreads();
+    if (tid < a.N) {
+      const int gi = tid / 8, i = tid % 8;
+      float t = 0.0f;
+      for (int u = gi; u < 128; u += ng) t += s_db[u * 8 + i];
+      a.partial_db[(long long)range * a.N + tid] = t;
+    }
+  }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, 256);
+  if (warp == 0) tmem_dealloc(tbase, tmem_cols(a.N));
 }
 
 // G[canonical] (+)= sum over ranges (in range order) of the partials; (x 1/255 on layer 1's W)
@@ -516,7 +580,7 @@ __global__ void gconv_wreduce_kernel(GConvWgradArgs a) {
 void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
   const int T = a.Th * a.Tw, MK = T * a.Cs;
   const int ranges = (a.b + a.ipc - 1) / a.ipc;
-  launch_pdl(gconv_wgrad_kernel, dim3((MK + 127) / 128, ranges), dim3(128), GCONV_SMEM, st, a);
+  launch_pdl(gconv_wgrad_kernel, dim3((MK + 127) / 128, ranges), dim3(128), NS * stage_bytes(a.N, a.first), st, a);
   gconv_debug("gconv_wgrad", st);
   const long long n = (long long)MK * a.N + a.N;
   launch_pdl(gconv_wreduce_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, a);
@@ -524,9 +588,16 @@ void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
 }
 
 void init_conv_kernel_attrs() {
-  cudaFuncSetAttribute(gconv_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GCONV_SMEM);
-  cudaFuncSetAttribute(gconv_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GCONV_SMEM);
-  cudaFuncSetAttribute(gconv_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GCONV_SMEM);
+  // the 227 KB opt-in limit includes each kernel's static shared memory
+  auto set = [](const void* f) {
+    cudaFuncAttributes at{};
+    cudaFuncGetAttributes(&at, f);
+    const int mx = std::min<int>(GCONV_SMEM_MAX, 227 * 1024 - (int)at.sharedSizeBytes - 1024);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  };
+  set((const void*)gconv_fwd_kernel);
+  set((const void*)gconv_dgrad_kernel);
+  set((const void*)gconv_wgrad_kernel);
 }
 
 // ------------------------------------------------------------------ packed weight images
