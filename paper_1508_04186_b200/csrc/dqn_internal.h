@@ -276,6 +276,7 @@ void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st);
 void launch_gpack(const float* theta, __nv_bfloat16* dst, long long img_off, const int2* map, long long n,
                   cudaStream_t st);
 void init_conv_kernel_attrs();
+unsigned long long gconv_error();
 
 struct ReduceUpdateArgs {
   BwdConvArgs b;                   // the conv partials and offsets

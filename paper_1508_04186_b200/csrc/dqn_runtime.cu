@@ -1705,6 +1705,8 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
   }
   if (hc.bad_input & 0x80000000u)
     return set_err(ctx, DQN_ECUDA, "fused server round: peer barrier timed out (ranks out of step?)");
+  if (ctx->gpath && gconv_error())
+    return set_err(ctx, DQN_ECUDA, "generic conv kernel: an MMA completion was never signalled (bounded wait expired)");
   if (hc.T != (unsigned long long)ctx->T)
     return set_err(ctx, DQN_ECUDA, "device step counters diverged from the host schedule");
   if (hc.nonfinite > 0) ctx->diverged = true;

@@ -587,6 +587,13 @@ void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
   gconv_debug("gconv_wreduce", st);
 }
 
+// the recorded lost-MMA-completion word (0: none), read after a synchronisation
+unsigned long long gconv_error() {
+  unsigned long long e = 0;
+  cudaMemcpyFromSymbol(&e, g_gconv_err, sizeof(e));
+  return e;
+}
+
 void init_conv_kernel_attrs() {
   // the 227 KB opt-in limit includes each kernel's static shared memory
   auto set = [](const void* f) {
