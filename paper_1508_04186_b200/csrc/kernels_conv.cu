@@ -49,12 +49,20 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+// 4 u8 -> 4 exact bf16 (two words) without I2F: 0x4B0000bb is the float 2^23 + b, minus 2^23 is
+// exactly b (< 256), whose low 16 bits are zero, so its upper half is the bf16 of b
+__device__ __forceinline__ uint2 u8x4_to_bf16(uint32_t w) {
+  const float f0 = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440)) - 8388608.0f;
+  const float f1 = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7441)) - 8388608.0f;
+  const float f2 = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7442)) - 8388608.0f;
+  const float f3 = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7443)) - 8388608.0f;
+  return make_uint2(__byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632),
+                    __byte_perm(__float_as_uint(f2), __float_as_uint(f3), 0x7632));
+}
 // 8 u8 (two words) -> 8 exact bf16 as one 16-byte chunk
 __device__ __forceinline__ uint4 u8x8_to_bf16(uint32_t w0, uint32_t w1) {
-  return make_uint4(pack2((float)(w0 & 0xFF), (float)((w0 >> 8) & 0xFF)),
-                    pack2((float)((w0 >> 16) & 0xFF), (float)(w0 >> 24)),
-                    pack2((float)(w1 & 0xFF), (float)((w1 >> 8) & 0xFF)),
-                    pack2((float)((w1 >> 16) & 0xFF), (float)(w1 >> 24)));
+  const uint2 a = u8x4_to_bf16(w0), b = u8x4_to_bf16(w1);
+  return make_uint4(a.x, a.y, b.x, b.y);
 }
 // bounded mbarrier wait: a lost MMA completion is recorded (g_gconv_err) and the wait abandoned,
 // so a bug cannot hang the GPU; the host reports it (gconv_debug / dqn_train_steps)
@@ -430,43 +438,51 @@ __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
   const int U8OFF = A_BYTES + a.N * KCH * 2;  // layer 1's raw pieces inside a stage
   __syncthreads();
   const int ng = a.N / 8;
+  // source offset of every position q of this image range (tap 0, c' = 0), computed once: the
+  // staging loops below then need no integer division
+  long long* s_pos = reinterpret_cast<long long*>(smem + NS * SB);
+  {
+    const long long grid = (long long)a.Hs * a.Ws * a.Cs;
+    for (int q = tid; q < npos; q += 128) {
+      const int im = img0 + q / HoWo, p = q % HoWo;
+      const long long base = a.first ? (long long)a.idx[im] * grid : (long long)im * grid;
+      s_pos[q] = base + ((long long)(p / a.Wo) * a.Ws + (p % a.Wo)) * a.Cs;
+    }
+  }
+  // this thread's fixed A row group (tid % 16) and tap, fixed B column group (tid % ng)
+  const int gi_a = tid % 16, k0_a = tid / 16, r_a = m0 + 8 * gi_a;
+  const bool r_ok = r_a < MK;
+  const int t_a = r_ok ? r_a / a.Cs : 0, cc_a = r_ok ? r_a % a.Cs : 0;
+  const long long tapoff = ((long long)(t_a / a.Tw) * a.Ws + (t_a % a.Tw)) * a.Cs + cc_a;
+  const int gi_b = tid % ng, k0_b = tid / ng, kstep_b = 128 / ng;
+  const __nv_bfloat16* dzr = a.dz + (long long)img0 * HoWo * a.N + 8 * gi_b;
+  __syncthreads();
   // db (m-tile 0 CTAs): column sums of dZ over this range. Thread tid always sees column group
   // tid % ng of the staged B chunks (128 % ng == 0) and keeps 8 running sums; combined at the end
   float dbacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   auto stage = [&](int c, int buf) {
     uint8_t* sA = smem + buf * SB;
     uint8_t* sB = sA + A_BYTES;
-    // A MN-major [16 row groups][64 k][8]: rows (tap, c'), k = position of this chunk
-    for (int e = tid; e < 16 * KCH; e += 128) {
-      const int gi = e % 16, k = e / 16;
-      const int q = c * KCH + k, r = m0 + 8 * gi;
-      uint8_t* d = sA + (gi * KCH + k) * 16;
-      if (q < npos && r < MK) {
-        const int im = img0 + q / HoWo, p = q % HoWo;
-        const int t = r / a.Cs, cc = r % a.Cs;
-        const int y = p / a.Wo + t / a.Tw, x = p % a.Wo + t % a.Tw;
-        const long long pix = ((long long)y * a.Ws + x) * a.Cs + cc;
-        if (a.first) {  // 8 raw bytes into the u8 area (piece e), converted after the wait
-          const long long slot = a.idx[im];
-          cp_async8(sA + U8OFF + e * 8, a.ring + slot * (long long)a.Hs * a.Ws * a.Cs + pix);
-        } else {
-          cp_async16(d, a.x + (long long)im * a.Hs * a.Ws * a.Cs + pix);
-        }
+    // A MN-major [16 row groups][64 k][8]: rows (tap, c'), k = position of this chunk; piece
+    // e = tid + 128 j is (row group tid % 16, k = tid / 16 + 8 j)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = k0_a + 8 * j, q = c * KCH + k;
+      uint8_t* d = sA + (gi_a * KCH + k) * 16;
+      if (q < npos && r_ok) {
+        const long long off = s_pos[q] + tapoff;
+        if (a.first) cp_async8(sA + U8OFF + (tid + 128 * j) * 8, a.ring + off);  // converted after the wait
+        else cp_async16(d, a.x + off);
       } else {
         *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
       }
     }
-    // B MN-major [N/8][64 k][8]: dZ[image][p][n..n+7]
-    for (int e = tid; e < ng * KCH; e += 128) {
-      const int gi = e % ng, k = e / ng;
+    // B MN-major [N/8][64 k][8]: dZ rows of the range are contiguous (position-major NHWC)
+    for (int k = k0_b; k < KCH; k += kstep_b) {
       const int q = c * KCH + k;
-      uint8_t* d = sB + (gi * KCH + k) * 16;
-      if (q < npos) {
-        const int im = img0 + q / HoWo, p = q % HoWo;
-        cp_async16(d, a.dz + ((long long)im * HoWo + p) * a.N + 8 * gi);
-      } else {
-        *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
-      }
+      uint8_t* d = sB + (gi_b * KCH + k) * 16;
+      if (q < npos) cp_async16(d, dzr + (long long)q * a.N);
+      else *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
     }
     cp_async_commit();
   };
@@ -483,14 +499,14 @@ __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
       cp_async_commit();
     }
     cp_async_wait_n<NS - 1>();
-    if (a.first) {  // convert the pieces this thread copied (same e sequence as the stage)
+    if (a.first && r_ok) {  // convert the pieces this thread copied (same sequence as the stage)
       uint8_t* sA = smem + buf * SB;
-      for (int e = tid; e < 16 * KCH; e += 128) {
-        const int gi = e % 16, k = e / 16;
-        const int q = c * KCH + k, r = m0 + 8 * gi;
-        if (q < npos && r < MK) {
-          const uint2 v = *reinterpret_cast<const uint2*>(sA + U8OFF + e * 8);
-          *reinterpret_cast<uint4*>(sA + (gi * KCH + k) * 16) = u8x8_to_bf16(v.x, v.y);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0_a + 8 * j;
+        if (c * KCH + k < npos) {
+          const uint2 v = *reinterpret_cast<const uint2*>(sA + U8OFF + (tid + 128 * j) * 8);
+          *reinterpret_cast<uint4*>(sA + (gi_a * KCH + k) * 16) = u8x8_to_bf16(v.x, v.y);
         }
       }
     }
@@ -580,7 +596,9 @@ __global__ void gconv_wreduce_kernel(GConvWgradArgs a) {
 void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
   const int T = a.Th * a.Tw, MK = T * a.Cs;
   const int ranges = (a.b + a.ipc - 1) / a.ipc;
-  launch_pdl(gconv_wgrad_kernel, dim3((MK + 127) / 128, ranges), dim3(128), NS * stage_bytes(a.N, a.first), st, a);
+  const int pos_bytes = (a.ipc * a.Ho * a.Wo * 8 + 1023) / 1024 * 1024;  // the position table
+  launch_pdl(gconv_wgrad_kernel, dim3((MK + 127) / 128, ranges), dim3(128),
+             NS * stage_bytes(a.N, a.first) + pos_bytes, st, a);
   gconv_debug("gconv_wgrad", st);
   const long long n = (long long)MK * a.N + a.N;
   launch_pdl(gconv_wreduce_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, a);
