@@ -568,29 +568,42 @@ __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
   if (warp == 0) tmem_dealloc(tbase, tmem_cols(a.N));
 }
 
-// G[canonical] (+)= sum over ranges (in range order) of the partials; (x 1/255 on layer 1's W)
-__global__ void gconv_wreduce_kernel(GConvWgradArgs a) {
+// G[canonical] (+)= sum over the ranges of the partials (x 1/255 on layer 1's W). Block = 32
+// consecutive entries x 8 range groups: each group sums its ranges in order, then the 8 group sums
+// are added in group order (a fixed order: deterministic).
+__global__ void __launch_bounds__(256) gconv_wreduce_kernel(GConvWgradArgs a) {
   pdl_sync();
   const int T = a.Th * a.Tw, MK = T * a.Cs;
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long nw = (long long)MK * a.N;
-  if (e >= nw + a.N) return;
-  const int nr = (a.b + a.ipc - 1) / a.ipc;
+  const long long nw = (long long)MK * a.N, total = nw + a.N;
+  const int el = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const long long e = blockIdx.x * 32LL + el;
+  const int nr = (a.b + a.ipc - 1) / a.ipc, per = (nr + 7) / 8;
+  const int q0 = grp * per, q1 = min(nr, q0 + per);
   float s = 0.0f;
+  if (e < total) {
+    if (e < nw)
+      for (int q = q0; q < q1; ++q) s += a.partial[(long long)q * nw + e];
+    else
+      for (int q = q0; q < q1; ++q) s += a.partial_db[(long long)q * a.N + (e - nw)];
+  }
+  __shared__ float red[8][32];
+  red[grp][el] = s;
+  __syncthreads();
+  if (grp != 0 || e >= total) return;
+  float t = 0.0f;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) t += red[g][el];
   long long dst;
   if (e < nw) {
     const int row = (int)(e / a.N), n = (int)(e % a.N);
-    for (int q = 0; q < nr; ++q) s += a.partial[((long long)q * MK + row) * a.N + n];
-    if (a.first) s *= 1.0f / 255.0f;
-    dst = a.w_canon[row] >= 0 ? a.w_off + (long long)n * a.w_nstride + a.w_canon[row] : -1;
+    if (a.first) t *= 1.0f / 255.0f;
+    if (a.w_canon[row] < 0) return;
+    dst = a.w_off + (long long)n * a.w_nstride + a.w_canon[row];
   } else {
-    const int n = (int)(e - nw);
-    for (int q = 0; q < nr; ++q) s += a.partial_db[(long long)q * a.N + n];
-    dst = a.b_off + n;
+    dst = a.b_off + (e - nw);
   }
-  if (dst < 0) return;
-  if (a.store) a.grad[dst] = s;
-  else a.grad[dst] += s;
+  if (a.store) a.grad[dst] = t;
+  else a.grad[dst] += t;
 }
 
 void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
@@ -601,7 +614,7 @@ void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
              NS * stage_bytes(a.N, a.first) + pos_bytes, st, a);
   gconv_debug("gconv_wgrad", st);
   const long long n = (long long)MK * a.N + a.N;
-  launch_pdl(gconv_wreduce_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, a);
+  launch_pdl(gconv_wreduce_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, st, a);
   gconv_debug("gconv_wreduce", st);
 }
 
