@@ -87,7 +87,7 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
 __device__ __forceinline__ bool bf16_pos(uint32_t h) { return (h & 0x8000u) == 0 && (h & 0x7FFFu) != 0; }
 
 constexpr int KCH = 64;                     // K per pipeline chunk
-constexpr int NS = 3;                       // pipeline stages (chunks in flight)
+constexpr int NS = 2;                       // pipeline stages (chunks in flight)
 constexpr int A_BYTES = 128 * KCH * 2;      // 16 KB
 constexpr int U8_BYTES = 128 * KCH;         // layer 1: raw u8 A chunk, converted after its copy lands
 // one stage: A [16 KB] | B [nB x 64 bf16] | (layer 1) u8 A [8 KB]
