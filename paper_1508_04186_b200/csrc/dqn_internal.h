@@ -277,6 +277,10 @@ void launch_gpack(const float* theta, __nv_bfloat16* dst, long long img_off, con
                   cudaStream_t st);
 void init_conv_kernel_attrs();
 unsigned long long gconv_error();
+// pipelined tcgen05 GEMM (generic path FC layers): K split into chunks of 64 (kper % 64 == 0)
+void launch_gemm_pipe(const TcGemmArgs& a, int groups, cudaStream_t st);
+void launch_fc_reduce(const TcGemmArgs& a, int groups, cudaStream_t st);
+void launch_head_finish_warp(const HeadArgs& h, cudaStream_t st);
 
 struct ReduceUpdateArgs {
   BwdConvArgs b;                   // the conv partials and offsets

@@ -493,11 +493,10 @@ static int setup_gpath(dqn_ctx* ctx) {
   init_bf16_kernel_attrs();
   init_conv_kernel_attrs();
   const FcShape& F = net.fc[0];
-  // FC forward split-K: K per split a multiple of 16 dividing D, operands within the 200 KB budget
-  const int BN = std::min(b, 256);
+  // FC forward split-K (gemm_pipe): K per split a multiple of 16 dividing D, at most 8 chunks of 64
   ctx->fc_splits = 0;
   for (int sp = 1; sp <= F.D / 16; ++sp)
-    if (F.D % sp == 0 && (F.D / sp) % 16 == 0 && (long long)(128 + BN) * (F.D / sp) * 2 <= 200 * 1024) {
+    if (F.D % sp == 0 && (F.D / sp) % 16 == 0 && F.D / sp <= 512) {
       ctx->fc_splits = sp;
       break;
     }
@@ -1272,12 +1271,10 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   TcGemmArgs gf{};
   gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.A[1] = ctx->theta_hat_bf16 + F.w_off; gf.lda = F.D;
   gf.B[0] = ctx->a2_bf16; gf.B[1] = ctx->a2_bf16 + (long long)b * F.D; gf.ldb = F.D;
-  gf.M = F.H; gf.N = b; gf.K = F.D; gf.BN = std::min(b, 256); gf.kper = F.D / ctx->fc_splits; gf.splits = ctx->fc_splits;
-  gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial; gf.counters = ctx->tc_counters;
-  gf.pre_a = 1; gf.pre_b = 0;
-  gf.bias[0] = ctx->theta_local + F.b_off; gf.bias[1] = ctx->theta_hat + F.b_off;
+  gf.M = F.H; gf.N = b; gf.K = F.D; gf.BN = std::min(b, 128); gf.kper = F.D / ctx->fc_splits; gf.splits = ctx->fc_splits;
+  gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
   PB("fc1_fwd", 1);
-  launch_tc_gemm(gf, 2, st);
+  launch_gemm_pipe(gf, 2, st);
   PE();
   // a6 head
   HeadArgs h{};
@@ -1298,7 +1295,7 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   PB("head_sample", 1);
   launch_head_f32(h, st, false);
   PE();
-  // a7: FC dW (plain store at n_push = 1) + FC dX (x ReLU mask, into the last conv's NHWC dZ) + head finish
+  // a7: FC dW (plain store at n_push = 1) + FC dX (x ReLU mask, into the last conv's NHWC dZ)
   const dqn_ctx::GLayer& GL = ctx->gl[nl - 1];
   TcGemmArgs gw{};
   gw.A[0] = ctx->dh_bf16; gw.lda = F.H; gw.a_mn = 1;
@@ -1312,9 +1309,10 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   gx.M = F.D; gx.N = b; gx.K = F.H; gx.BN = 64; gx.kper = F.H; gx.splits = 1;
   gx.epi = TC_EPI_MASK_T; gx.out_bf16 = GL.dz; gx.mask = ctx->a2_bf16; gx.ldo = F.D;
   gx.hwc_HW = GL.Ho * GL.Wo; gx.hwc_C = GL.N;
-  gx.pre_a = 1; gx.pre_b = 0;
+  // one launch: the FC dW and dX tiles plus the head finish CTAs run side by side (tc_pair); the
+  // whole K (= b and H <= 512) is staged at once, which the 200 KB budget allows at BN = 64
+  gx.pre_a = 1; gx.pre_b = 0; gw.pre_a = 0; gw.pre_b = 1;
   PB("fc1_bwd_head_finish", 1);
-  gw.st_id = gx.st_id = ST_FC_BWD;
   launch_tc_pair_with_head(gw, gx, h, st);
   PE();
   // a8/a9: per layer, top down: wgrad (+ range reduction into G), then dgrad into the layer below
@@ -1764,11 +1762,11 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
       TcGemmArgs gf{};
       gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.lda = F.D;
       gf.B[0] = ctx->a2_bf16; gf.ldb = F.D;
-      gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = std::min(256, (m + 15) / 16 * 16); gf.kper = F.D / ctx->fc_splits;
+      gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = std::min(128, (m + 15) / 16 * 16); gf.kper = F.D / ctx->fc_splits;
       gf.splits = ctx->fc_splits; gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
-      gf.pre_a = 1; gf.pre_b = 0;
-      gf.counters = ctx->tc_counters; gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
-      launch_tc_gemm(gf, 1, st);
+      gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
+      launch_gemm_pipe(gf, 1, st);
+      launch_fc_reduce(gf, 1, st);
       in = ctx->act_fc[0][0];
     } else if (ctx->bf16) {  // conv1's s2d staging, then the tensor-core forward with theta_local
       const FcShape& F = net.fc[0];

@@ -592,6 +592,12 @@ void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st) {
   }
 }
 
+// the FC forward's split-K reduction + bias + ReLU alone (after launch_gemm_pipe)
+void launch_fc_reduce(const TcGemmArgs& a, int groups, cudaStream_t st) {
+  dim3 rg(cdiv((long long)a.M * a.N, 256), groups);
+  launch_pdl(fc_reduce_kernel, rg, dim3(256), 0, st, a);
+}
+
 // ------------------------------------------------------------------ a8/a9: fused conv backward
 // One CTA per image j of the minibatch (group 0: s_j, theta). Per image:
 //   conv2 dW  D2[(t,c'')][n2] += sum_{m'} A1(m'+shift_t)[c''] dZ2[m'][n2]      (2 M-tiles, MN-major A and B)

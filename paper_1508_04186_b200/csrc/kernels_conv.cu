@@ -106,10 +106,9 @@ __device__ __forceinline__ uint32_t tmem_cols(int n) {
 // One MMA K-chunk (64 = 4 x K16) from the stage buffers; A and B K-major [kc][rows][8] or
 // MN-major [rows/8][k][8] as flagged.
 __device__ __forceinline__ void issue_chunk(uint32_t tmem, uint32_t sa, uint32_t sb, int nB, bool a_mn, bool b_mn,
-                                            bool first_chunk) {
+                                            bool first_chunk, int ksteps = KCH / 16) {
   const uint32_t idesc = make_idesc_bf16(128, nB, a_mn, b_mn);
-#pragma unroll
-  for (int kk = 0; kk < KCH / 16; ++kk) {
+  for (int kk = 0; kk < ksteps; ++kk) {
     const uint64_t ad = a_mn ? make_desc(sa + kk * 256, 128, KCH * 16) : make_desc(sa + (2 * kk) * 128 * 16, 128 * 16, 128);
     const uint64_t bd = b_mn ? make_desc(sb + kk * 256, 128, KCH * 16) : make_desc(sb + (2 * kk) * nB * 16, nB * 16, 128);
     mma_bf16(tmem, ad, bd, idesc, (!first_chunk || kk > 0) ? 1u : 0u);
@@ -618,6 +617,8 @@ void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
   gconv_debug("gconv_wreduce", st);
 }
 
+__global__ void __launch_bounds__(128) gemm_pipe_kernel(TcGemmArgs a);
+
 // the recorded lost-MMA-completion word (0: none), read after a synchronisation
 unsigned long long gconv_error() {
   unsigned long long e = 0;
@@ -636,6 +637,182 @@ void init_conv_kernel_attrs() {
   set((const void*)gconv_fwd_kernel);
   set((const void*)gconv_dgrad_kernel);
   set((const void*)gconv_wgrad_kernel);
+  set((const void*)gemm_pipe_kernel);
+}
+
+// ------------------------------------------------------------------ pipelined GEMM (generic path FC layers)
+// D[m][n] = sum_k A(m,k) B(n,k) over this CTA's K split, in chunks of 64 through the stage ring
+// (K-major or MN-major operands as flagged), with the epilogues the FC layers need:
+//   TC_EPI_ACCUM + store : C[m*ldc + n] = D           (FC dW, n_push = 1)
+//   TC_EPI_ACCUM         : C[m*ldc + n] += D
+//   TC_EPI_MASK_T        : out[n*ldo + m'] = mask[n*ldo + m] > 0 ? D : 0, m' = NHWC remap (FC dX)
+//   TC_EPI_FC_FWD        : partial[g][split][n][m] = D    (FC forward, reduced by the TD head)
+__global__ void __launch_bounds__(128) gemm_pipe_kernel(TcGemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar[NS];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = blockIdx.z, split = blockIdx.y;
+  const int m_tiles = (a.M + 127) / 128;
+  const int mt = blockIdx.x % m_tiles, nt = blockIdx.x / m_tiles;
+  const int m0 = mt * 128, n0 = nt * a.BN, bn = a.BN;
+  const int k0 = split * a.kper, KC = min(a.kper, a.K - k0), nch = (KC + KCH - 1) / KCH;  // KC % 16 == 0
+  const int SB = ((A_BYTES + bn * KCH * 2) + 1023) / 1024 * 1024;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, tmem_cols(bn));
+  pdl_sync();
+  __syncthreads();
+  const __nv_bfloat16* Ag = a.A[g];
+  const __nv_bfloat16* Bg = a.B[g];
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  auto stage = [&](int c, int buf) {
+    uint8_t* sA = smem + buf * SB;
+    uint8_t* sB = sA + A_BYTES;
+    const int kb = k0 + c * KCH, klen = min(KCH, KC - c * KCH);  // the last chunk may be short
+    if (!a.a_mn) {  // [kc][128][8]
+      for (int e = tid; e < 128 * 8; e += 128) {
+        const int r = e >> 3, kc = e & 7, m = m0 + r;
+        uint8_t* d = sA + (kc * 128 + r) * 16;
+        if (m < a.M && 8 * kc < klen) cp_async16(d, Ag + (long long)m * a.lda + kb + 8 * kc);
+        else *reinterpret_cast<uint4*>(d) = z4;
+      }
+    } else {        // [16][64 k][8]
+      for (int e = tid; e < 16 * KCH; e += 128) {
+        const int gi = e & 15, k = e >> 4, m = m0 + 8 * gi;
+        uint8_t* d = sA + (gi * KCH + k) * 16;
+        if (m < a.M && k < klen) cp_async16(d, Ag + (long long)(kb + k) * a.lda + m);
+        else *reinterpret_cast<uint4*>(d) = z4;
+      }
+    }
+    if (!a.b_mn) {  // [kc][bn][8]
+      for (int e = tid; e < bn * 8; e += 128) {
+        const int r = e >> 3, kc = e & 7, n = n0 + r;
+        uint8_t* d = sB + (kc * bn + r) * 16;
+        if (n < a.N && 8 * kc < klen) cp_async16(d, Bg + (long long)n * a.ldb + kb + 8 * kc);
+        else *reinterpret_cast<uint4*>(d) = z4;
+      }
+    } else {        // [bn/8][64 k][8]
+      const int ng = bn / 8;
+      for (int e = tid; e < ng * KCH; e += 128) {
+        const int gi = e % ng, k = e / ng, n = n0 + 8 * gi;
+        uint8_t* d = sB + (gi * KCH + k) * 16;
+        if (n < a.N && k < klen) cp_async16(d, Bg + (long long)(kb + k) * a.ldb + n);
+        else *reinterpret_cast<uint4*>(d) = z4;
+      }
+    }
+    cp_async_commit();
+  };
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nch) stage(c, c);
+    else cp_async_commit();
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c % NS, cn = c + NS - 1;
+    if (cn < nch) {
+      if (c >= 1) mbar_wait_bounded(&bar[(c - 1) % NS], ((c - 1) / NS) & 1, 4);
+      stage(cn, cn % NS);
+    } else {
+      cp_async_commit();
+    }
+    cp_async_wait_n<NS - 1>();
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + buf * SB);
+      issue_chunk(tbase, sa, sa + A_BYTES, bn, a.a_mn, a.b_mn, c == 0, (min(KCH, KC - c * KCH) + 15) / 16);
+      mma_commit(&bar[buf]);
+    }
+  }
+  mbar_wait_bounded(&bar[(nch - 1) % NS], ((nch - 1) / NS) & 1, 5);
+  tc_fence_after();
+  const int m = m0 + 32 * warp + lane;
+  const uint32_t trow = tbase + ((uint32_t)(32 * warp) << 16);
+  for (int c = 0; c < bn; c += 16) {
+    float v[16];
+    tmem_ld16(trow + c, v);  // warp-collective: every lane loads
+    if (m >= a.M) continue;
+    if (a.epi == TC_EPI_ACCUM) {
+      float* crow = a.C[g] + (long long)m * a.ldc + n0 + c;
+      for (int i = 0; i < 16 && n0 + c + i < a.N; ++i) crow[i] = a.store ? v[i] : crow[i] + v[i];
+    } else if (a.epi == TC_EPI_MASK_T) {
+      const long long om = a.hwc_HW ? (long long)(m % a.hwc_HW) * a.hwc_C + m / a.hwc_HW : (long long)m;
+      unsigned short mk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int n = n0 + c + i;
+        mk[i] = n < a.N ? __ldg(reinterpret_cast<const unsigned short*>(a.mask) + (long long)n * a.ldo + m) : 0;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int n = n0 + c + i;
+        if (n < a.N) a.out_bf16[(long long)n * a.ldo + om] = __float2bfloat16_rn(bf16_pos(mk[i]) ? v[i] : 0.0f);
+      }
+    } else {  // TC_EPI_FC_FWD
+      float* pbase = a.partial + ((long long)g * a.splits + split) * (long long)a.N * a.M;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (n0 + c + i < a.N) pbase[(long long)(n0 + c + i) * a.M + m] = v[i];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, tmem_cols(bn));
+}
+
+void launch_gemm_pipe(const TcGemmArgs& a, int groups, cudaStream_t st) {
+  const int m_tiles = (a.M + 127) / 128, n_tiles = (a.N + a.BN - 1) / a.BN;
+  const int SB = ((A_BYTES + a.BN * KCH * 2) + 1023) / 1024 * 1024;
+  launch_pdl(gemm_pipe_kernel, dim3(m_tiles * n_tiles, a.splits, groups), dim3(128), NS * SB, st, a);
+  gconv_debug("gemm_pipe", st);
+}
+
+// ------------------------------------------------------------------ TD head finish, one warp per element
+// The cross-sample sums of head_finish.cuh for large b: lane l sums samples j = l, l+32, ... in
+// ascending order, then the 32 lane sums combine in a fixed shuffle tree (deterministic).
+__global__ void __launch_bounds__(256) head_finish_warp_kernel(HeadArgs h) {
+  pdl_sync();
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int H = h.H, A = h.A;
+  if (e >= A * H + A + H + 1) return;
+  const float* h0 = h.fc_partial ? h.act_out[0] : h.act[0];
+  float s = 0.0f;
+  if (e < A * H) {
+    const int a = e / H, u = e % H;
+    for (int j = lane; j < h.b; j += 32)
+      if (h.s_act[j] == a) s = fmaf(h.s_dq[j], h0[(long long)j * H + u], s);
+  } else if (e < A * H + A) {
+    const int a = e - A * H;
+    for (int j = lane; j < h.b; j += 32)
+      if (h.s_act[j] == a) s += h.s_dq[j];
+  } else if (e < A * H + A + H) {
+    if (!h.prev_is_fc) return;
+    const int u = e - A * H - A;
+    for (int j = lane; j < h.b; j += 32) s += h.dH[(long long)j * H + u];
+  } else {
+    for (int j = lane; j < h.b; j += 32) s += h.s_loss[j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane != 0) return;
+  if (e < A * H) h.grad[h.w_off + e] += s;
+  else if (e < A * H + A) h.grad[h.b_off + (e - A * H)] += s;
+  else if (e < A * H + A + H) h.grad[h.prev_b_off + (e - A * H - A)] += s;
+  else {
+    const unsigned long long T = h.ctr->T;
+    h.diag_loss[T % kDiagSteps] = s / (float)h.b;
+    h.ctr->T = T + 1;  // this step is complete for the sampler
+  }
+}
+
+void launch_head_finish_warp(const HeadArgs& h, cudaStream_t st) {
+  const int n = h.A * h.H + h.A + h.H + 1;
+  launch_pdl(head_finish_warp_kernel, dim3((n + 7) / 8), dim3(256), 0, st, h);
+  gconv_debug("head_finish_warp", st);
 }
 
 // ------------------------------------------------------------------ packed weight images
