@@ -115,3 +115,23 @@ def test_many_replicas_bf16_mnih(tmp_path, world):
     assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
     assert per_tensor_rel(res["theta"], ref["theta"], on) < 2e-2
     assert rel_l2_per_tensor(res["theta"] - th0, ref["theta"] - th0, on) < 0.1
+
+
+def test_two_replicas_bf16_scaled_generic_path(tmp_path):
+    """The generic bf16 conv path (scaled net, BASELINE.json configs[4]) at N = 2 with the fused server
+    round, smooth regime: theta after 3 rounds follows the oracle's 2-replica run."""
+    if n_gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    from tests.test_gpu_parity_bf16 import rel_l2_per_tensor, smooth_theta
+    kw = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=18)
+    res = run_ranks(2, tmp_path, "--precision", "bf16", "--scaled", "--b", "32", "--steps", "3", "--smooth", "--lr",
+                    "1e-5")
+    dc, on, oc = nets(minibatch=32, replay_capacity=200, lr=1e-5, target_sync=2, **kw)
+    oc.n_replicas = 2
+    reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
+    th0 = smooth_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 3)
+    assert int(res["n"]) == ref["n"]
+    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
+    assert per_tensor_rel(res["theta"], ref["theta"], on) < 2e-2
+    assert rel_l2_per_tensor(res["theta"] - th0, ref["theta"] - th0, on) < 0.1

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--target-sync", type=int, default=2)
     ap.add_argument("--b", type=int, default=16)
     ap.add_argument("--tiny", action="store_true")
+    ap.add_argument("--scaled", action="store_true", help="BASELINE configs[4] net (generic bf16 conv path)")
     ap.add_argument("--smooth", action="store_true")
     ap.add_argument("--async-mode", action="store_true")
     ap.add_argument("--lr", type=float, default=1e-3)
@@ -42,6 +43,8 @@ def main():
     obj = [D.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     kw = dict(frames=3, height=17, width=13, convs=((5, 5, 2), (6, 3, 2)), fcs=(19,), n_actions=5) if a.tiny else {}
+    if a.scaled:
+        kw = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=18)
     prec = D.FP32 if a.precision == "fp32" else D.BF16
     dc, on, oc = nets(minibatch=a.b, replay_capacity=200, n_push=a.n_push, n_fetch=a.n_fetch,
                       target_sync=a.target_sync, lr=a.lr, precision=prec,
