@@ -51,6 +51,13 @@ enum { DQN_DETERMINISTIC = 0, /* lock-step: a fetch returns the current server t
        DQN_ASYNC = 1 };       /* the server round (push, RMSProp, publish) overlaps the next steps on a
                                  second stream; a fetch returns the server theta of one round earlier
                                  (lag 1, the deterministic twin of Downpour's staleness, O13 / A32)   */
+/* how a push round combines the N workers' gradients (Alg. 2)
+ *   MEAN         : one RMSProp application of the mean of the N*n_push gradients, n += 1 (A7)
+ *   PER_GRADIENT : Alg. 2 literally - each worker's gradient (mean of its n_push) applied in turn
+ *                  in rank order, one RMSProp application and n += 1 each (A33). N > 1 needs the
+ *                  fused server round (DQN_DETERMINISTIC, n_fetch = 1); DQN_ASYNC is rejected. */
+enum { DQN_SERVER_MEAN = 0, DQN_SERVER_PER_GRADIENT = 1 };
+
 /* which parameter vector dqn_get_params returns */
 enum {
   DQN_PARAMS_SERVER = 0, /* global theta of Alg. 2 (fp32 masters, gathered over ranks: collective) */
@@ -86,6 +93,8 @@ typedef struct {
   double init_std;                     /* xi of theta_i ~ N(0, xi) (A19)           */
   uint64_t init_seed;
   const float* init_params;            /* optional: P floats in canonical order (host or device); copied */
+  int32_t server_rule;                 /* DQN_SERVER_MEAN (A7, default) | DQN_SERVER_PER_GRADIENT (A33) */
+  int32_t reserved;                    /* 0                                                */
 } dqn_config;
 
 typedef struct {

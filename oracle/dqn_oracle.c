@@ -479,7 +479,25 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
       pend[(int64_t)k * cfg->n_push + T % cfg->n_push] = n_local[k]; /* generation this gradient used */
     }
     /* O9 server round when the push is due (A7) */
-    if ((T + 1) % cfg->n_push == 0) {
+    if ((T + 1) % cfg->n_push == 0 && cfg->server_rule == 1) {
+      /* A33: "for all workers k ... RMSPropUpdate(Delta theta_k); n <- n + 1" in rank order, each
+         gradient the mean of that worker's n_push accumulated gradients (A8) */
+      if (stale_hist)
+        for (int64_t e = 0; e < (int64_t)N * cfg->n_push; ++e) {
+          const int64_t s = n - pend[e];
+          stale_hist[s < 31 ? s : 31] += 1;
+        }
+      for (int k = 0; k < N; ++k) {
+        for (int64_t i = 0; i < P; ++i) {
+          gbar[i] = acc[k][i] / (double)cfg->n_push;
+          if (!isfinite(gbar[i])) { rc = -3; continue; }
+          or_rmsprop(theta + i, rms + i, gbar + i, 1, cfg->lr, cfg->rms_decay, cfg->rms_eps);
+        }
+        n += 1;
+        memcpy(hist + (n % (L + 1)) * P, theta, sizeof(double) * P);
+      }
+      for (int k = 0; k < N; ++k) memset(acc[k], 0, sizeof(double) * P);
+    } else if ((T + 1) % cfg->n_push == 0) {
       for (int64_t i = 0; i < P; ++i) {
         double sum = 0.0;
         for (int k = 0; k < N; ++k) sum += acc[k][i]; /* rank order */

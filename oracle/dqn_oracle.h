@@ -41,7 +41,9 @@ typedef struct {
   double err_clip;         /* 0 = off (A3) */
   uint64_t seed;           /* sampler key (A11) */
   int32_t fetch_lag;       /* 0: synchronous; L > 0: a fetch returns theta as it was L rounds ago (O13, A32) */
-  int32_t pad;
+  int32_t server_rule;     /* 0: mean of the round's N gradients, one RMSProp, n += 1 (A7);
+                              1: Alg. 2 literally - each worker's gradient applied in turn (rank order),
+                              one RMSProp and n += 1 per gradient (A33) */
 } or_train_cfg;
 
 /* ---- shapes (O0) ---- */

@@ -46,7 +46,7 @@ class _Cfg(C.Structure):
     _fields_ = [("n_replicas", C.c_int32), ("minibatch", C.c_int32), ("n_push", C.c_int32),
                 ("n_fetch", C.c_int32), ("target_sync", C.c_int64), ("gamma", C.c_double),
                 ("lr", C.c_double), ("rms_decay", C.c_double), ("rms_eps", C.c_double),
-                ("err_clip", C.c_double), ("seed", C.c_uint64), ("fetch_lag", C.c_int32), ("pad", C.c_int32)]
+                ("err_clip", C.c_double), ("seed", C.c_uint64), ("fetch_lag", C.c_int32), ("server_rule", C.c_int32)]
 
 
 @dataclass
@@ -94,7 +94,7 @@ class TrainCfg:
     err_clip: float = 0.0
     seed: int = 0xD15EA5E
     fetch_lag: int = 0   # O13 / A32: a fetch returns theta as it was `fetch_lag` rounds ago
-    pad: int = 0
+    server_rule: int = 0  # 0: mean per round (A7); 1: Alg. 2 literally, one update per gradient (A33)
 
     def c(self) -> _Cfg:
         c = _Cfg()

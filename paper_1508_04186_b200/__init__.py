@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(_PKG, "libdqn.so")
 OK, EINVAL, EEMPTY, ENONFINITE, ENOMEM, ECUDA, ENCCL, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
 FP32, BF16 = 0, 1
 DETERMINISTIC, ASYNC = 0, 1
+SERVER_MEAN, SERVER_PER_GRADIENT = 0, 1
 PARAMS_SERVER, PARAMS_LOCAL, PARAMS_TARGET, PARAMS_GRAD, PARAMS_RMS = 0, 1, 2, 3, 4
 _NAMES = {0: "OK", -1: "EINVAL", -2: "EEMPTY", -3: "ENONFINITE", -4: "ENOMEM", -5: "ECUDA", -6: "ENCCL",
           -7: "ESTATE"}
@@ -42,7 +43,8 @@ class _Config(C.Structure):
                 ("rms_eps", C.c_double), ("err_clip", C.c_double), ("replay_capacity", C.c_int64),
                 ("n_push", C.c_int32), ("n_fetch", C.c_int32), ("target_sync", C.c_int64),
                 ("precision", C.c_int32), ("sync_mode", C.c_int32), ("seed", C.c_uint64),
-                ("init_std", C.c_double), ("init_seed", C.c_uint64), ("init_params", C.c_void_p)]
+                ("init_std", C.c_double), ("init_seed", C.c_uint64), ("init_params", C.c_void_p),
+                ("server_rule", C.c_int32), ("reserved", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -80,6 +82,7 @@ class Config:
     seed: int = 0xD15EA5E
     init_std: float = 0.01
     init_seed: int = 7
+    server_rule: int = 0   # SERVER_MEAN (A7) | SERVER_PER_GRADIENT (A33)
 
     def to_c(self, init_ptr: Optional[int] = None) -> _Config:
         c = _Config()
@@ -91,7 +94,8 @@ class Config:
         for i, u in enumerate(self.fcs):
             c.fc_units[i] = u
         for name in ("n_actions", "minibatch", "gamma", "lr", "rms_decay", "rms_eps", "err_clip", "replay_capacity",
-                     "n_push", "n_fetch", "target_sync", "precision", "sync_mode", "seed", "init_std", "init_seed"):
+                     "n_push", "n_fetch", "target_sync", "precision", "sync_mode", "seed", "init_std", "init_seed",
+                     "server_rule"):
             setattr(c, name, getattr(self, name))
         c.init_params = init_ptr
         return c

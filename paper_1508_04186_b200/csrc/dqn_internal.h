@@ -162,6 +162,8 @@ struct ServerRoundArgs {
   float* theta_master;                          // owned shard
   float* rms;
   float inv_div, lr, rho, omr, eps;
+  int per_gradient;                             // A33: apply each worker's gradient in rank order
+  float inv_np;                                 // 1 / n_push (per-gradient rule)
   DevCounters* ctr;
   unsigned long long* trace;                    // optional [64][8] globaltimer stamps (DQN_TRACE_COMM=1)
 };

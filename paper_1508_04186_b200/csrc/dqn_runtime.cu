@@ -87,6 +87,7 @@ struct dqn_ctx {
   std::vector<long long> round_nloc;              // n_local of the steps of the current round
   // NEXT-1 fused server round over NVLink peer memory (world > 1, deterministic, n_fetch == 1)
   bool fused_comm = false;
+  long long n_per_round = 1;  // server generations per push round: 1 (mean rule) or N (per-gradient rule)
   ServerRoundArgs sra{};                          // peer pointers etc., filled at create
   FusedAcquire acq{};                             // the next step's acquire half (acq.ctr == nullptr: off)
   unsigned long long* flags = nullptr;            // [kMaxWorld] barrier A (written by peers)
@@ -274,6 +275,10 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   if (c->n_push < 1 || c->n_fetch < 1) { *why = "n_push and n_fetch must be >= 1"; return DQN_EINVAL; }
   if (c->precision != DQN_FP32 && c->precision != DQN_BF16) { *why = "unknown precision"; return DQN_EINVAL; }
   if (c->sync_mode != DQN_DETERMINISTIC && c->sync_mode != DQN_ASYNC) { *why = "unknown sync_mode"; return DQN_EINVAL; }
+  if (c->server_rule != DQN_SERVER_MEAN && c->server_rule != DQN_SERVER_PER_GRADIENT) { *why = "unknown server_rule"; return DQN_EINVAL; }
+  if (c->server_rule == DQN_SERVER_PER_GRADIENT && c->sync_mode == DQN_ASYNC) {
+    *why = "DQN_SERVER_PER_GRADIENT needs DQN_DETERMINISTIC"; return DQN_EINVAL;
+  }
   if (!(c->rms_decay >= 0.0 && c->rms_decay < 1.0) || !(c->rms_eps >= 0.0) || !(c->lr >= 0.0) ||
       !std::isfinite(c->gamma) || !(c->err_clip >= 0.0)) {
     *why = "invalid hyper-parameter"; return DQN_EINVAL;
@@ -460,6 +465,8 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   a.my_flags = ctx->flags; a.my_done = ctx->done; a.my_join = ctx->done + 1;
   a.theta_master = ctx->theta_master; a.rms = ctx->rms;
   a.inv_div = (float)(1.0 / ((double)N * c.n_push));
+  a.per_gradient = c.server_rule == DQN_SERVER_PER_GRADIENT;
+  a.inv_np = (float)(1.0 / (double)c.n_push);
   a.lr = (float)c.lr; a.rho = (float)c.rms_decay; a.omr = (float)(1.0 - c.rms_decay); a.eps = (float)c.rms_eps;
   a.ctr = ctx->ctr;
   a.img_off = ctx->img_off; a.w1_off = ctx->w1_off; a.w2_off = ctx->w2_off;
@@ -766,8 +773,11 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     NK(ncclCommInitRank(&ctx->comm, world, id, rank));
     const char* fe = getenv("DQN_FUSED_COMM");
     ctx->fused_comm = !ctx->async && cfg->n_fetch == 1 && world <= kMaxWorld && !(fe && atoi(fe) == 0);
+    if (cfg->server_rule == DQN_SERVER_PER_GRADIENT && !ctx->fused_comm)
+      return set_err(ctx, DQN_EINVAL, "DQN_SERVER_PER_GRADIENT with N > 1 needs the fused server round (n_fetch = 1)");
     if (ctx->fused_comm && (rc = setup_fused_comm(ctx))) return rc;
   }
+  ctx->n_per_round = cfg->server_rule == DQN_SERVER_PER_GRADIENT ? world : 1;  // n += 1 per applied gradient (A22)
   return DQN_OK;
 }
 
@@ -1492,7 +1502,7 @@ static int do_step(dqn_ctx* ctx, bool profile, long long* kernels, bool* out_fet
       ctx->round_nloc.clear();
     }
   }
-  if (push) ctx->n += 1;
+  if (push) ctx->n += ctx->n_per_round;
   ctx->T += 1;
   if (out_fetch) *out_fetch = g_fetch;
   if (out_refresh) *out_refresh = refresh;
@@ -1504,7 +1514,7 @@ static int do_step(dqn_ctx* ctx, bool profile, long long* kernels, bool* out_fet
 static int plan_step(dqn_ctx* ctx) {
   bool fetch, refresh, push;
   schedule(ctx, &fetch, &refresh, &push);
-  if (push) ctx->n += 1;
+  if (push) ctx->n += ctx->n_per_round;
   ctx->T += 1;
   return (fetch ? 1 : 0) | (refresh ? 2 : 0) | (push ? 4 : 0);
 }

@@ -84,16 +84,35 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
     float4 t4 = reinterpret_cast<const float4*>(a.theta_master)[i];
     float4 r4 = reinterpret_cast<const float4*>(a.rms)[i];
     float tv[4] = {t4.x, t4.y, t4.z, t4.w}, rv[4] = {r4.x, r4.y, r4.z, r4.w};
-    const float gv[4] = {acc.x, acc.y, acc.z, acc.w};
+    if (a.per_gradient) {  // A33: Alg. 2 literally, worker p's gradient then p+1's (rank order)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float gb = gv[q] * a.inv_div;
-      if (isfinite(gb)) {
-        const float rr = a.rho * rv[q] + a.omr * gb * gb;
-        rv[q] = rr;
-        tv[q] = tv[q] - a.lr * gb * rsqrtf(rr + a.eps);
-      } else {
-        ++bad;
+      for (int p = 0; p < kMaxWorld; ++p) {
+        if (p >= a.world) break;
+        const float gp[4] = {v[p].x, v[p].y, v[p].z, v[p].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float gb = gp[q] * a.inv_np;
+          if (isfinite(gb)) {
+            const float rr = a.rho * rv[q] + a.omr * gb * gb;
+            rv[q] = rr;
+            tv[q] = tv[q] - a.lr * gb * rsqrtf(rr + a.eps);
+          } else {
+            ++bad;
+          }
+        }
+      }
+    } else {
+      const float gv[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float gb = gv[q] * a.inv_div;
+        if (isfinite(gb)) {
+          const float rr = a.rho * rv[q] + a.omr * gb * gb;
+          rv[q] = rr;
+          tv[q] = tv[q] - a.lr * gb * rsqrtf(rr + a.eps);
+        } else {
+          ++bad;
+        }
       }
     }
     t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);

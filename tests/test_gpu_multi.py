@@ -135,3 +135,21 @@ def test_two_replicas_bf16_scaled_generic_path(tmp_path):
     assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
     assert per_tensor_rel(res["theta"], ref["theta"], on) < 2e-2
     assert rel_l2_per_tensor(res["theta"] - th0, ref["theta"] - th0, on) < 0.1
+
+
+@pytest.mark.parametrize("n_push", [1, 2])
+def test_two_replicas_per_gradient_rule(tmp_path, n_push):
+    """DQN_SERVER_PER_GRADIENT (A33, Alg. 2 literally): the fused server round applies worker 0's then
+    worker 1's gradient, one RMSProp and n += 1 each; against the oracle's server_rule = 1 run."""
+    if n_gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_ranks(2, tmp_path, "--tiny", "--n-push", str(n_push), "--n-fetch", "1", "--target-sync", "3",
+                    "--steps", "6", "--server-rule", "1")
+    dc, on, oc = nets(minibatch=16, replay_capacity=200, n_push=n_push, target_sync=3, lr=1e-3, **TINY_KW)
+    oc.n_replicas = 2
+    oc.server_rule = 1
+    reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
+    ref = O.run(on, oc, 200, reps, he_theta(on, 3).astype(np.float64), 6)
+    assert int(res["n"]) == ref["n"] == 2 * (6 // n_push)
+    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
+    assert per_tensor_rel(res["theta"], ref["theta"], on) < 1e-5

@@ -64,7 +64,18 @@ def serial_reference(cfg, replays, theta0, steps, cap, net=TINY, stale=None):
             _, g = O.loss_grad(net, th_local[k], rp.s[idx], rp.a[idx], y, cfg.err_clip)
             acc[k] += g
             used[(k, T)] = n_loc[k]
-        if (T + 1) % cfg.n_push == 0:
+        if (T + 1) % cfg.n_push == 0 and cfg.server_rule == 1:
+            # Alg. 2 literally (A33): each worker's gradient (mean of its n_push) applied in rank order
+            if stale is not None:
+                for k in range(N):
+                    for t in range(T + 1 - cfg.n_push, T + 1):
+                        stale[min(n - used[(k, t)], 31)] += 1
+            for k in range(N):
+                theta, r = O.rmsprop(theta, r, acc[k] / cfg.n_push, cfg.lr, cfg.rms_decay, cfg.rms_eps)
+                n += 1
+                history.append(theta.copy())
+            acc = [np.zeros_like(theta) for _ in range(N)]
+        elif (T + 1) % cfg.n_push == 0:
             gbar = sum(acc) / (N * cfg.n_push)
             if stale is not None:
                 for k in range(N):
@@ -187,3 +198,41 @@ def test_lag1_one_step_rounds_have_staleness_one():
     cfg = O.TrainCfg(n_replicas=1, minibatch=2, fetch_lag=1)
     out = O.run(TINY, cfg, CAP, make_replays(1, 30, 5), he_theta(TINY, 1), 6)
     assert out["staleness"][0] == 1 and out["staleness"][1] == 5 and out["staleness"].sum() == 6
+
+
+@pytest.mark.parametrize("N,n_push,n_fetch,C,lag", [(2, 1, 1, 2, 0), (3, 2, 3, 1, 0), (2, 1, 1, 1, 1)])
+def test_per_gradient_rule_equals_serial_loop(N, n_push, n_fetch, C, lag):
+    """A33: server_rule = 1 applies every worker's gradient in turn (one RMSProp and n += 1 each)."""
+    cfg = O.TrainCfg(n_replicas=N, minibatch=4, n_push=n_push, n_fetch=n_fetch, target_sync=C, lr=1e-2,
+                     fetch_lag=lag, server_rule=1)
+    reps = make_replays(N, 30, 71)
+    th0 = he_theta(TINY, 5)
+    ref = O.run(TINY, cfg, CAP, reps, th0, 6)
+    th, r, n = serial_reference(cfg, reps, th0, 6, CAP)
+    assert ref["n"] == n == N * (6 // n_push)
+    assert np.allclose(ref["theta"], th, rtol=0, atol=1e-13)
+    assert np.allclose(ref["r"], r, rtol=0, atol=1e-13)
+
+
+def test_per_gradient_rule_with_one_worker_is_the_mean_rule():
+    for n_push in (1, 2):
+        base = O.TrainCfg(n_replicas=1, minibatch=4, n_push=n_push, target_sync=3, lr=1e-2)
+        per = O.TrainCfg(n_replicas=1, minibatch=4, n_push=n_push, target_sync=3, lr=1e-2, server_rule=1)
+        reps = make_replays(1, 30, 72)
+        th0 = he_theta(TINY, 6)
+        a, b = O.run(TINY, base, CAP, reps, th0, 6), O.run(TINY, per, CAP, reps, th0, 6)
+        assert np.array_equal(a["theta"], b["theta"]) and a["n"] == b["n"]
+
+
+def test_per_gradient_rule_two_equal_gradients_closed_form():
+    """Two applications of the same gradient (Alg. 2 P:142-146 twice): r1 = .9 r + .1 g^2,
+    th1 = th - a g / sqrt(r1 + eps), then r2, th2 from (th1, r1)."""
+    g, th, r, a, eps = 0.3, 0.5, 0.2, 0.01, 1e-8
+    r1 = 0.9 * r + 0.1 * g * g
+    th1 = th - a * g / np.sqrt(r1 + eps)
+    r2 = 0.9 * r1 + 0.1 * g * g
+    th2 = th1 - a * g / np.sqrt(r2 + eps)
+    t, rr = np.array([th]), np.array([r])
+    for _ in range(2):
+        t, rr = O.rmsprop(t, rr, np.array([g]), a, 0.9, eps)
+    assert abs(t[0] - th2) < 1e-15 and abs(rr[0] - r2) < 1e-15

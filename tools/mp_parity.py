@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--smooth", action="store_true")
     ap.add_argument("--async-mode", action="store_true")
     ap.add_argument("--lr", type=float, default=1e-3)
+    ap.add_argument("--server-rule", type=int, default=0, help="0 mean (A7), 1 per gradient (A33)")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -48,7 +49,7 @@ def main():
     prec = D.FP32 if a.precision == "fp32" else D.BF16
     dc, on, oc = nets(minibatch=a.b, replay_capacity=200, n_push=a.n_push, n_fetch=a.n_fetch,
                       target_sync=a.target_sync, lr=a.lr, precision=prec,
-                      sync_mode=D.ASYNC if a.async_mode else D.DETERMINISTIC, **kw)
+                      sync_mode=D.ASYNC if a.async_mode else D.DETERMINISTIC, server_rule=a.server_rule, **kw)
     theta0 = he_theta(on, 3)
     if a.smooth:
         from tests.test_gpu_parity_bf16 import smooth_theta
