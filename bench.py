@@ -244,6 +244,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--profile-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dedup", action="store_true",
+                    help="frame-deduplicated replay (F+1 frames per slot; G-pong stacks slide by one frame)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
@@ -284,7 +286,7 @@ def main():
     for p in ([prec] if prec is not None else [D.BF16, D.FP32]):
         cfg = D.Config(**net, minibatch=b, replay_capacity=args.replay, target_sync=C["C"], precision=p,
                        lr=2.5e-4, gamma=0.99, n_push=C["n_push"], n_fetch=C["n_fetch"],
-                       sync_mode=D.ASYNC if C["async"] else D.DETERMINISTIC)
+                       sync_mode=D.ASYNC if C["async"] else D.DETERMINISTIC, replay_dedup=int(args.dedup))
         try:
             dqn = D.DQN(cfg, rank=rank, world=world, nccl_id=nccl_id, stream=stream.cuda_stream)
             break
@@ -332,8 +334,9 @@ def main():
     # ---- e2e: through the public API with host buffers; per step push the step's new experience
     # (Alg. 1: one Store per iteration) from pinned host memory, run the step, read the loss back
     ne = args.e2e_steps
-    hs = torch.from_numpy(synth.g_pong(ne, 4, 84, 84, 6, 99 + rank)[0]).pin_memory()
-    hsn = torch.from_numpy(synth.g_pong(ne, 4, 84, 84, 6, 98 + rank)[0]).pin_memory()
+    gp = synth.g_pong(ne + 3, 4, 84, 84, 6, 99 + rank)  # s' = s shifted by one frame + a new frame
+    hs = torch.from_numpy(gp[0]).pin_memory()
+    hsn = torch.from_numpy(gp[3]).pin_memory()
     ha = torch.zeros(ne, dtype=torch.int32).pin_memory()
     hr = torch.zeros(ne, dtype=torch.float32).pin_memory()
     ht = torch.zeros(ne, dtype=torch.uint8).pin_memory()
@@ -395,7 +398,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
         "config": {"workload": f"BASELINE.json configs[{C['idx']}]", "net": net_name(net), "minibatch_per_replica": b,
-                   "replay_per_replica": args.replay, "target_sync_C": C["C"] if C["C"] < 2**40 else None,
+                   "replay_per_replica": args.replay, "replay_dedup": bool(args.dedup),
+                   "target_sync_C": C["C"] if C["C"] < 2**40 else None,
                    "n_push": C["n_push"], "n_fetch": C["n_fetch"],
                    "sync_mode": "async (lag-1 fetch)" if C["async"] else "deterministic",
                    "parallelism": f"dp{world} + sharded parameter server", "gamma": 0.99,

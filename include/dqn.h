@@ -94,7 +94,9 @@ typedef struct {
   uint64_t init_seed;
   const float* init_params;            /* optional: P floats in canonical order (host or device); copied */
   int32_t server_rule;                 /* DQN_SERVER_MEAN (A7, default) | DQN_SERVER_PER_GRADIENT (A33) */
-  int32_t reserved;                    /* 0                                                */
+  int32_t replay_dedup;                /* 1: frame-deduplicated replay (NEXT-4): every pushed s' must be
+                                          s shifted by one frame plus a new frame (Atari-style stacks);
+                                          a slot stores F+1 frames instead of 2F (DQN_EINVAL otherwise) */
 } dqn_config;
 
 typedef struct {

@@ -44,7 +44,7 @@ class _Config(C.Structure):
                 ("n_push", C.c_int32), ("n_fetch", C.c_int32), ("target_sync", C.c_int64),
                 ("precision", C.c_int32), ("sync_mode", C.c_int32), ("seed", C.c_uint64),
                 ("init_std", C.c_double), ("init_seed", C.c_uint64), ("init_params", C.c_void_p),
-                ("server_rule", C.c_int32), ("reserved", C.c_int32)]
+                ("server_rule", C.c_int32), ("replay_dedup", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -83,6 +83,7 @@ class Config:
     init_std: float = 0.01
     init_seed: int = 7
     server_rule: int = 0   # SERVER_MEAN (A7) | SERVER_PER_GRADIENT (A33)
+    replay_dedup: int = 0  # 1: F+1 frames per slot (s' = s shifted by one frame + a new frame)
 
     def to_c(self, init_ptr: Optional[int] = None) -> _Config:
         c = _Config()
@@ -95,7 +96,7 @@ class Config:
             c.fc_units[i] = u
         for name in ("n_actions", "minibatch", "gamma", "lr", "rms_decay", "rms_eps", "err_clip", "replay_capacity",
                      "n_push", "n_fetch", "target_sync", "precision", "sync_mode", "seed", "init_std", "init_seed",
-                     "server_rule"):
+                     "server_rule", "replay_dedup"):
             setattr(c, name, getattr(self, name))
         c.init_params = init_ptr
         return c

@@ -115,11 +115,13 @@ struct HeadArgs {
 void launch_sample(int* idx, int b, unsigned long long seed, unsigned rank, const DevCounters* ctr,
                    cudaStream_t st);
 void launch_validate_push(const int32_t* a, const float* r, long long n, int A, DevCounters* ctr, cudaStream_t st);
+void launch_validate_dedup(const uint8_t* s, const uint8_t* sn, long long n, long long sb, long long fb,
+                           DevCounters* ctr, cudaStream_t st);
 void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
                            long long cap, long long count0, long long n_total, long long first, long long n,
                            long long state_bytes, const uint8_t* s, const int32_t* a, const float* r,
                            const uint8_t* sn, const uint8_t* t, cudaStream_t st, long long* ring_size_out = nullptr,
-                           long long ring_size = 0);
+                           long long ring_size = 0, long long stride = 0, int dedup = 0);
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
                     cudaStream_t st, long long img_off = -1,
@@ -195,6 +197,7 @@ struct FwdConvArgs {
   uint8_t* a1_save;                // [n][8][144][16] or nullptr
   FusedAcquire acq;                // NEXT-1: the previous round's deliveries (acq.done == nullptr: none)
   long long img_off;               // conv weight image (wimg.cuh) inside theta[g]
+  long long slot_stride;           // bytes between replay slots (28,224, or 35,280 with frame dedup)
 };
 struct TcGemmArgs {
   const __nv_bfloat16* A[2];
@@ -226,6 +229,7 @@ struct TcGemmArgs {
 enum { TC_EPI_ACCUM = 0, TC_EPI_FC_FWD = 1, TC_EPI_MASK_T = 2 };
 struct BwdConvArgs {
   const uint8_t* ring_s;
+  long long slot_stride;
   const int* idx;
   const uint8_t* a1_save;
   const __nv_bfloat16* dz2;        // [n][2592]
@@ -245,6 +249,7 @@ struct GConvFwdArgs {
   unsigned long long seed;
   unsigned rank;
   int first;                       // 1: layer 1 (u8 input, 1/255 folded into the epilogue)
+  long long slot_stride;           // layer 1: bytes between replay slots (frame-major s2d)
   int b, Hs, Ws, Cs, Th, Tw, Ho, Wo, N;
   int s_next;                      // stride of the next conv (its s2d factor), 0: canonical flatten out
   const __nv_bfloat16* wpk[2];     // packed forward weights [N][Th*Tw*Cs] per group
@@ -265,6 +270,7 @@ struct GConvWgradArgs {
   const uint8_t* ring;             // layer 1: the s ring and the sampled slots
   const int* idx;
   int first;
+  long long slot_stride;
   const __nv_bfloat16* dz;         // [b][Ho][Wo][N]
   int b, Hs, Ws, Cs, Th, Tw, Ho, Wo, N, ipc;  // ipc: images per CTA (K range)
   float* partial;                  // [ranges][Th*Tw*Cs][N]
@@ -309,7 +315,8 @@ void step_trace_comm(int on, unsigned long long* out);
 void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t, long long cap,
                      long long count0, long long first, long long n, const uint8_t* s, const int32_t* a,
                      const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st,
-                     long long* ring_size_out = nullptr, long long ring_size = 0);
+                     long long* ring_size_out = nullptr, long long ring_size = 0, long long stride = 28224,
+                     int dedup = 0);
 void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st);
 void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st);
 // one launch: the tiles of GEMM p0, the tiles of GEMM p1 (single split, group 0 each), then the

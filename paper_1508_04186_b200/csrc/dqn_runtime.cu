@@ -31,6 +31,10 @@ struct dqn_ctx {
   ncclComm_t comm = nullptr;
   // replay memory D_k: FIFO ring of the last `cap` experiences
   uint8_t *ring_s = nullptr, *ring_sn = nullptr, *ring_t = nullptr;
+  // replay slots: `slot_stride` bytes apart; with frame dedup one buffer of F+1 frames per slot,
+  // s = frames 0..F-1 (ring_s), s' = frames 1..F (ring_sn = ring_s + one frame, not owned)
+  long long slot_stride = 0;
+  bool dedup = false;
   int32_t* ring_a = nullptr;
   float* ring_r = nullptr;
   long long cap = 0, count = 0;
@@ -276,6 +280,7 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   if (c->precision != DQN_FP32 && c->precision != DQN_BF16) { *why = "unknown precision"; return DQN_EINVAL; }
   if (c->sync_mode != DQN_DETERMINISTIC && c->sync_mode != DQN_ASYNC) { *why = "unknown sync_mode"; return DQN_EINVAL; }
   if (c->server_rule != DQN_SERVER_MEAN && c->server_rule != DQN_SERVER_PER_GRADIENT) { *why = "unknown server_rule"; return DQN_EINVAL; }
+  if (c->replay_dedup != 0 && (c->replay_dedup != 1 || c->frames < 2)) { *why = "replay_dedup needs 0, or 1 with frames >= 2"; return DQN_EINVAL; }
   if (c->server_rule == DQN_SERVER_PER_GRADIENT && c->sync_mode == DQN_ASYNC) {
     *why = "DQN_SERVER_PER_GRADIENT needs DQN_DETERMINISTIC"; return DQN_EINVAL;
   }
@@ -353,7 +358,7 @@ static void free_all(dqn_ctx* c) {
       cudaEventDestroy(m.a);
       cudaEventDestroy(m.b);
     }
-  void* ptrs[] = {c->ring_s, c->ring_sn, c->ring_t, c->ring_a, c->ring_r, c->rms, c->grad, c->g_shard,
+  void* ptrs[] = {c->ring_s, c->dedup ? nullptr : c->ring_sn, c->ring_t, c->ring_a, c->ring_r, c->rms, c->grad, c->g_shard,
                   c->theta_hat, c->grad_snap, c->gather_tmp, c->partial, c->idx, c->ctr, c->diag_loss,
                   c->diag_idx, c->diag_amax, c->head_dq, c->head_act, c->head_loss, c->q_stage, c->q_out, c->q_amax, c->d_stage,
                   c->theta_local_bf16, c->theta_hat_bf16, c->a2_bf16, c->a1_save,
@@ -634,9 +639,12 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   init_f32_kernel_attrs();
 
   // replay memory: both stacks of every experience, action, reward, terminal flag
-  const long long sb = net.state_bytes;
-  if ((rc = dalloc(ctx, &ctx->ring_s, ctx->cap * sb))) return rc;
-  if ((rc = dalloc(ctx, &ctx->ring_sn, ctx->cap * sb))) return rc;
+  const long long sb = net.state_bytes, fb = sb / net.F;
+  ctx->dedup = cfg->replay_dedup != 0;
+  ctx->slot_stride = ctx->dedup ? sb + fb : sb;
+  if ((rc = dalloc(ctx, &ctx->ring_s, ctx->cap * ctx->slot_stride))) return rc;
+  if (ctx->dedup) ctx->ring_sn = ctx->ring_s + fb;
+  else if ((rc = dalloc(ctx, &ctx->ring_sn, ctx->cap * sb))) return rc;
   if ((rc = dalloc(ctx, &ctx->ring_t, ctx->cap))) return rc;
   if ((rc = dalloc(ctx, &ctx->ring_a, ctx->cap))) return rc;
   if ((rc = dalloc(ctx, &ctx->ring_r, ctx->cap))) return rc;
@@ -814,10 +822,11 @@ static void push_ring(dqn_ctx* ctx, long long i0, long long m, const uint8_t* s,
   long long* size_out = &ctx->ctr->ring_size;
   if (ctx->bf16)
     launch_push_s2d(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, i0, m, s,
-                    a, r, sn, t, ctx->stream, size_out, size);
+                    a, r, sn, t, ctx->stream, size_out, size, ctx->slot_stride, ctx->dedup);
   else
     launch_push_canonical(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, 0,
-                          i0, m, ctx->net.state_bytes, s, a, r, sn, t, ctx->stream, size_out, size);
+                          i0, m, ctx->net.state_bytes, s, a, r, sn, t, ctx->stream, size_out, size, ctx->slot_stride,
+                          ctx->dedup);
 }
 
 
@@ -838,6 +847,12 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
     for (long long i = 0; i < n; ++i)
       if (a[i] < 0 || a[i] >= ctx->net.A || !std::isfinite(r[i]))
         return set_err(ctx, DQN_EINVAL, "action out of range or non-finite reward at item " + std::to_string(i));
+    if (ctx->dedup) {  // s'[0..F-2] must be s[1..F-1] (frames shared; only s'[F-1] is stored)
+      const long long fb = sb / ctx->net.F;
+      for (long long i = first; i < n; ++i)
+        if (std::memcmp(s_next + i * sb, s + i * sb + fb, (size_t)(sb - fb)) != 0)
+          return set_err(ctx, DQN_EINVAL, "replay_dedup: s' is not s shifted by one frame at item " + std::to_string(i));
+    }
     // chunk layout (host pinned and device): s [m][sb] | s' [m][sb] | a [m] i32 | r [m] f32 | term [m] u8
     for (long long i0 = first; i0 < n; i0 += ctx->push_chunk) {
       const long long m = std::min(ctx->push_chunk, n - i0);
@@ -863,10 +878,12 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
   } else {
     CK(cudaMemsetAsync(&ctx->ctr->bad_input, 0, sizeof(unsigned), ctx->stream));
     launch_validate_push(a, r, n, ctx->net.A, ctx->ctr, ctx->stream);
+    if (ctx->dedup) launch_validate_dedup(s, s_next, n, sb, sb / ctx->net.F, ctx->ctr, ctx->stream);
     unsigned bad = 0;
     CK(cudaMemcpyAsync(&bad, &ctx->ctr->bad_input, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (bad) return set_err(ctx, DQN_EINVAL, "action out of range or non-finite reward in device push");
+    if (bad) return set_err(ctx, DQN_EINVAL, "action out of range, non-finite reward or (replay_dedup) s' not s "
+                                               "shifted by one frame in device push");
     for (long long i0 = first; i0 < n; i0 += 65535) {
       const long long m = std::min<long long>(65535, n - i0);
       push_ring(ctx, i0, m, s + i0 * sb, a + i0, r + i0, s_next + i0 * sb, terminal + i0);
@@ -934,7 +951,7 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   src0.u8[0] = ctx->ring_s;
   src0.u8[1] = ctx->ring_sn;
   src0.idx = ctx->idx;
-  src0.stride = net.state_bytes;
+  src0.stride = ctx->slot_stride;
   for (int i = 0; i < net.n_conv; ++i) {
     ImgSrc src = src0;
     if (i > 0) {
@@ -1013,7 +1030,7 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
     const ConvShape& L = net.conv[i];
     ImgSrc src{};
     if (i == 0) {
-      src.u8[0] = ctx->ring_s; src.idx = ctx->idx; src.stride = net.state_bytes;
+      src.u8[0] = ctx->ring_s; src.idx = ctx->idx; src.stride = ctx->slot_stride;
     } else {
       src.f32[0] = ctx->act_conv[i - 1][0];
       src.stride = (long long)L.C * L.H * L.W;
@@ -1105,6 +1122,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   fa.a2 = ctx->a2_bf16; fa.a1_save = ctx->a1_save;
   fa.acq = ctx->acq;
   fa.img_off = ctx->img_off;
+  fa.slot_stride = ctx->slot_stride;
   PB("conv_fwd", 1);
   launch_fwd_conv_bf16(fa, 2, st);
   PE();
@@ -1161,7 +1179,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   PE();
   // a8/a9 conv backward
   BwdConvArgs ba{};
-  ba.ring_s = ctx->ring_s; ba.idx = ctx->idx; ba.a1_save = ctx->a1_save; ba.dz2 = ctx->dz2_bf16;
+  ba.ring_s = ctx->ring_s; ba.slot_stride = ctx->slot_stride; ba.idx = ctx->idx; ba.a1_save = ctx->a1_save; ba.dz2 = ctx->dz2_bf16;
   ba.theta = ctx->theta_local_bf16;
   ba.w1_off = L1.w_off; ba.b1_off = L1.b_off; ba.w2_off = L2.w_off; ba.b2_off = L2.b_off;
   ba.n = b; ba.partial = ctx->bwd_partial; ba.counter = ctx->tc_counters + 32; ba.grad = ctx->grad;
@@ -1263,7 +1281,7 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     GConvFwdArgs a{};
     a.first = i == 0;
     if (i == 0) {
-      a.ring[0] = ctx->ring_s; a.ring[1] = ctx->ring_sn;
+      a.ring[0] = ctx->ring_s; a.ring[1] = ctx->ring_sn; a.slot_stride = ctx->slot_stride;
       a.idx = ctx->idx; a.ctr = ctx->ctr; a.seed = c.seed; a.rank = (unsigned)ctx->rank;
     } else {
       a.x[0] = G.x[0]; a.x[1] = G.x[1];
@@ -1332,7 +1350,7 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     const dqn_ctx::GLayer& G = ctx->gl[i];
     GConvWgradArgs w{};
     w.first = i == 0;
-    if (i == 0) { w.ring = ctx->ring_s; w.idx = ctx->idx; } else { w.x = G.x[0]; }
+    if (i == 0) { w.ring = ctx->ring_s; w.idx = ctx->idx; w.slot_stride = ctx->slot_stride; } else { w.x = G.x[0]; }
     w.dz = G.dz;
     w.b = b; w.Hs = G.Hs; w.Ws = G.Ws; w.Cs = G.Cs; w.Th = G.Th; w.Tw = G.Tw; w.Ho = G.Ho; w.Wo = G.Wo; w.N = L.N;
     w.ipc = G.ipc; w.partial = ctx->gw_partial; w.partial_db = ctx->gw_partial_db;
@@ -1760,7 +1778,7 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
         const dqn_ctx::GLayer& G = ctx->gl[i];
         GConvFwdArgs a{};
         a.first = i == 0;
-        if (i == 0) a.ring[0] = ctx->q_stage_s2d;  // ctr == nullptr: image j = slot j
+        if (i == 0) { a.ring[0] = ctx->q_stage_s2d; a.slot_stride = kMnihSlot; }  // ctr == nullptr: image j = slot j
         else a.x[0] = G.x[0];
         a.b = m; a.Hs = G.Hs; a.Ws = G.Ws; a.Cs = G.Cs; a.Th = G.Th; a.Tw = G.Tw; a.Ho = G.Ho; a.Wo = G.Wo; a.N = L.N;
         a.s_next = i + 1 < net.n_conv ? ctx->gl[i + 1].s : 0;
@@ -1785,6 +1803,7 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
       FwdConvArgs fa{};
       fa.ring[0] = ctx->q_stage_s2d;
       fa.img_off = ctx->img_off;
+      fa.slot_stride = kMnihSlot;
       fa.theta[0] = ctx->theta_local_bf16;
       fa.theta_f32[0] = ctx->theta_local;
       fa.w1_off = net.conv[0].w_off; fa.b1_off = net.conv[0].b_off;

@@ -42,29 +42,31 @@ __device__ __forceinline__ int tap_shift2(int t) { return (t >> 1) * A1_W + (t &
 static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // ------------------------------------------------------------------ push: canonical -> s2d ring slots
-// out[p*64 + c'] with p = py*21 + px, c' = f*16 + iy*4 + ix  <-  in[f][4py+iy][4px+ix]
-// One thread writes one 16-byte vector (pixel p, frame f): four 4-byte rows of the 4x4 block.
+// Frame-major s2d slots: out[f][p][16] with p = py*21 + px, byte iy*4 + ix  <-  in[f][4py+iy][4px+ix]
+// (channel c' = f*16 + iy*4 + ix of conv1's s2d grid), slot stride `stride` bytes. With `dedup` the
+// s' ring aliases the s ring one frame later (5 frames per slot: s = frames 0-3, s' = 1-4) and only
+// the new frame of s' is written. One thread writes one 16-byte vector (frame f, pixel p).
 __global__ void push_s2d_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
                                 long long cap, long long count0, long long first, const uint8_t* s,
                                 const int32_t* a, const float* r, const uint8_t* sn, const uint8_t* t,
-                                long long* ring_size_out, long long ring_size) {
+                                long long* ring_size_out, long long ring_size, long long stride, int dedup) {
   const long long i = blockIdx.y;
   if (ring_size_out && i == 0 && blockIdx.x == 0 && threadIdx.x == 0) *ring_size_out = ring_size;
   const long long slot = (count0 + first + i) % cap;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;  // (pixel, frame)
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;  // (frame, pixel)
   if (v < mnih::X_PIX * 4) {
-    const int p = v >> 2, f = v & 3;
+    const int f = v / mnih::X_PIX, p = v % mnih::X_PIX;
     const int py = p / 21, px = p % 21;
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
-      if (which == 1 && ring_sn == nullptr) break;  // states only (dqn_q_values staging)
+      if (which == 1 && (ring_sn == nullptr || (dedup && f != 3))) break;  // q staging: states only
       const uint8_t* src = (which ? sn : s) + i * mnih::SLOT + f * 7056 + (4 * py) * 84 + 4 * px;
       uint4 o;
       o.x = *reinterpret_cast<const uint32_t*>(src);
       o.y = *reinterpret_cast<const uint32_t*>(src + 84);
       o.z = *reinterpret_cast<const uint32_t*>(src + 168);
       o.w = *reinterpret_cast<const uint32_t*>(src + 252);
-      uint8_t* dst = (which ? ring_sn : ring_s) + slot * mnih::SLOT + p * 64 + f * 16;
+      uint8_t* dst = (which ? ring_sn : ring_s) + slot * stride + f * 7056 + p * 16;
       *reinterpret_cast<uint4*>(dst) = o;
     }
   }
@@ -78,11 +80,11 @@ __global__ void push_s2d_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring
 void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t, long long cap,
                      long long count0, long long first, long long n, const uint8_t* s, const int32_t* a,
                      const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st, long long* ring_size_out,
-                     long long ring_size) {
+                     long long ring_size, long long stride, int dedup) {
   if (n <= 0) return;
   dim3 grid(cdiv(mnih::X_PIX * 4, 256), (unsigned)n);
   push_s2d_kernel<<<grid, 256, 0, st>>>(ring_s, ring_sn, ring_a, ring_r, ring_t, cap, count0, first, s, a, r, sn, t,
-                                        ring_size_out, ring_size);
+                                        ring_size_out, ring_size, stride, dedup);
 }
 
 // ------------------------------------------------------------------ shared helpers
@@ -110,7 +112,7 @@ __device__ __forceinline__ void u8x16_to_bf16(const uint4 q, uint4& lo, uint4& h
 __device__ __forceinline__ void expand_state(uint8_t* sX, const uint8_t* sU8) {
   const uint4* s4 = reinterpret_cast<const uint4*>(sU8);
   for (int v = threadIdx.x; v < mnih::X_PIX * 4; v += blockDim.x) {
-    const int p = v >> 2, q = v & 3;
+    const int q = v / mnih::X_PIX, p = v % mnih::X_PIX;  // frame-major slot: frame q, pixel p
     uint4 lo, hi;
     u8x16_to_bf16(s4[v], lo, hi);
     *reinterpret_cast<uint4*>(sX + ((2 * q) * mnih::X_ALLOC + p) * 16) = lo;
@@ -155,13 +157,13 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     fence_mbar_init();
     // a2 gather: the whole u8 state in one TMA bulk copy (28,224 contiguous bytes of the ring slot)
     mbar_arrive_expect_tx(&bar_ld, mnih::SLOT);
-    bulk_g2s(sU8, a.ring[g] + slot * mnih::SLOT, mnih::SLOT, &bar_ld);
+    bulk_g2s(sU8, a.ring[g] + slot * a.slot_stride, mnih::SLOT, &bar_ld);
     // the sampler is counter-based: step T+1's slot is known now. Prefetch it into L2 so that the
     // next step's gather is an L2 hit with a warm TLB (a random 28 KB slot of a 56 GB ring
     // otherwise costs a page walk); harmless if a push changes the ring size before T+1.
     if (a.ctr) {
       const long long nxt = sample_slot(a.seed, a.rank, a.ctr->T + 1, (unsigned)j, a.ctr->ring_size);
-      bulk_prefetch_l2(a.ring[g] + nxt * mnih::SLOT, mnih::SLOT);
+      bulk_prefetch_l2(a.ring[g] + nxt * a.slot_stride, mnih::SLOT);
     }
   }
   if (warp == 0) tmem_alloc(&tbase, 128);
@@ -676,7 +678,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
   {
     // every thread issues all of its loads before the first conversion (latency, not bandwidth, bound)
     constexpr int XIT = (mnih::X_PIX * 4 + 127) / 128, AIT = (8 * mnih::A1_PIX + 127) / 128;
-    const uint4* s4 = reinterpret_cast<const uint4*>(a.ring_s + (long long)a.idx[j] * mnih::SLOT);
+    const uint4* s4 = reinterpret_cast<const uint4*>(a.ring_s + (long long)a.idx[j] * a.slot_stride);
     const uint4* a4 = reinterpret_cast<const uint4*>(a.a1_save + (long long)j * 8 * mnih::A1_ALLOC * 16);
     uint4 xb[XIT], ab[AIT];
 #pragma unroll
@@ -694,7 +696,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
     for (int it = 0; it < XIT; ++it) {
       const int v = threadIdx.x + it * 128;
       if (v >= mnih::X_PIX * 4) break;
-      const int p = v >> 2, q = v & 3;
+      const int q = v / mnih::X_PIX, p = v % mnih::X_PIX;  // frame-major slot: frame q, pixel p
       uint4 lo, hi;
       u8x16_to_bf16(xb[it], lo, hi);
       *reinterpret_cast<uint4*>(sX + ((2 * q) * mnih::X_ALLOC + p) * 16) = lo;

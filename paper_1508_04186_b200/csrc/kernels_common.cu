@@ -31,6 +31,30 @@ __global__ void validate_push_kernel(const int32_t* a, const float* r, long long
   if (a[i] < 0 || a[i] >= A || !isfinite(r[i])) atomicAdd(&ctr->bad_input, 1u);
 }
 
+// replay_dedup: flag any item whose s'[0..F-2] differs from s[1..F-1] (16-byte words when aligned)
+__global__ void validate_dedup_kernel(const uint8_t* s, const uint8_t* sn, long long sb, long long fb,
+                                      DevCounters* ctr) {
+  const long long i = blockIdx.x;
+  const uint8_t* a = s + i * sb + fb;
+  const uint8_t* b = sn + i * sb;
+  const long long n = sb - fb;
+  bool diff = false;
+  if (((((uintptr_t)a) | ((uintptr_t)b) | n) & 15) == 0) {
+    for (long long v = threadIdx.x; v < n / 16; v += blockDim.x) {
+      const uint4 x = reinterpret_cast<const uint4*>(a)[v], y = reinterpret_cast<const uint4*>(b)[v];
+      diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+    }
+  } else {
+    for (long long v = threadIdx.x; v < n; v += blockDim.x) diff |= a[v] != b[v];
+  }
+  if (diff) atomicOr(&ctr->bad_input, 2u);
+}
+
+void launch_validate_dedup(const uint8_t* s, const uint8_t* sn, long long n, long long sb, long long fb,
+                           DevCounters* ctr, cudaStream_t st) {
+  if (n > 0) validate_dedup_kernel<<<(unsigned)n, 256, 0, st>>>(s, sn, sb, fb, ctr);
+}
+
 void launch_validate_push(const int32_t* a, const float* r, long long n, int A, DevCounters* ctr, cudaStream_t st) {
   if (n <= 0) return;
   validate_push_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, r, n, A, ctr);
@@ -38,29 +62,33 @@ void launch_validate_push(const int32_t* a, const float* r, long long n, int A, 
 
 // Item i of this chunk (global push index n_total_before + first + i) goes to
 // slot (count0 + first + i) mod cap. One CTA per transition, 16-byte copies.
+// canonical [F][H][W] slots, slot stride `stride` bytes (state_bytes, or (F+1) frames with frame
+// dedup: the s' ring then aliases the s ring one frame later and only the new frame of s' is written)
 __global__ void push_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t,
                             long long cap, long long count0, long long first, long long state_bytes,
                             const uint8_t* s, const int32_t* a, const float* r, const uint8_t* sn,
-                            const uint8_t* t, long long* ring_size_out, long long ring_size) {
+                            const uint8_t* t, long long* ring_size_out, long long ring_size, long long stride,
+                            long long frame_bytes) {
   long long i = blockIdx.x;
   if (ring_size_out && i == 0 && threadIdx.x == 0) *ring_size_out = ring_size;
   long long slot = (count0 + first + i) % cap;
+  // s: the whole stack; s': the whole stack, or (dedup) only its last frame
+  const long long off1 = frame_bytes ? state_bytes - frame_bytes : 0;
   const uint8_t* src0 = s + i * state_bytes;
-  const uint8_t* src1 = sn + i * state_bytes;
-  uint8_t* dst0 = ring_s + slot * state_bytes;
-  uint8_t* dst1 = ring_sn + slot * state_bytes;
-  bool vec = ((state_bytes & 15) == 0) && ((((uintptr_t)src0) | ((uintptr_t)src1)) & 15) == 0;
+  const uint8_t* src1 = sn + i * state_bytes + off1;
+  uint8_t* dst0 = ring_s + slot * stride;
+  uint8_t* dst1 = ring_sn + slot * stride + off1;
+  const long long n1 = state_bytes - off1;
+  bool vec = ((state_bytes & 15) == 0) && ((n1 & 15) == 0) && ((stride & 15) == 0) &&
+             ((((uintptr_t)src0) | ((uintptr_t)src1) | ((uintptr_t)dst0) | ((uintptr_t)dst1)) & 15) == 0;
   if (vec) {
-    long long nv = state_bytes / 16;
-    for (long long v = threadIdx.x; v < nv; v += blockDim.x) {
+    for (long long v = threadIdx.x; v < state_bytes / 16; v += blockDim.x)
       reinterpret_cast<uint4*>(dst0)[v] = reinterpret_cast<const uint4*>(src0)[v];
+    for (long long v = threadIdx.x; v < n1 / 16; v += blockDim.x)
       reinterpret_cast<uint4*>(dst1)[v] = reinterpret_cast<const uint4*>(src1)[v];
-    }
   } else {
-    for (long long v = threadIdx.x; v < state_bytes; v += blockDim.x) {
-      dst0[v] = src0[v];
-      dst1[v] = src1[v];
-    }
+    for (long long v = threadIdx.x; v < state_bytes; v += blockDim.x) dst0[v] = src0[v];
+    for (long long v = threadIdx.x; v < n1; v += blockDim.x) dst1[v] = src1[v];
   }
   if (threadIdx.x == 0) {
     ring_a[slot] = a[i];
@@ -73,11 +101,13 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
                            long long cap, long long count0, long long n_total, long long first, long long n,
                            long long state_bytes, const uint8_t* s, const int32_t* a, const float* r,
                            const uint8_t* sn, const uint8_t* t, cudaStream_t st, long long* ring_size_out,
-                           long long ring_size) {
+                           long long ring_size, long long stride, int dedup) {
   (void)n_total;
   if (n <= 0) return;
+  if (stride <= 0) stride = state_bytes;
   push_kernel<<<(unsigned)n, 256, 0, st>>>(ring_s, ring_sn, ring_a, ring_r, ring_t, cap, count0, first, state_bytes,
-                                           s, a, r, sn, t, ring_size_out, ring_size);
+                                           s, a, r, sn, t, ring_size_out, ring_size, stride,
+                                           dedup ? stride - state_bytes : 0);
 }
 
 // ---------------------------------------------------------------- a12 update

@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
       } else {
         slot = img;  // staging buffer: image j = slot j
       }
-      xrow8 = a.ring[g] + slot * (long long)a.Hs * a.Ws * a.Cs;
+      xrow8 = a.ring[g] + slot * a.slot_stride;  // frame-major s2d slot [frame][pixel][16]
     } else {
       xrow = a.x[g] + (long long)img * a.Hs * a.Ws * a.Cs;
     }
@@ -213,10 +213,10 @@ __global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
     if (row_ok) {
       const long long pix = (long long)(oy + ty) * a.Ws + (ox + tx);
       if (a.first) {  // 64 raw bytes of this row into the u8 area; converted once they land
-        const uint8_t* src = xrow8 + pix * a.Cs + cb * KCH;
+        const uint8_t* src = xrow8 + pix * 16;  // 4 frames x 16 bytes = the 64 s2d channels
         uint8_t* su = sA + A_BYTES + a.N * KCH * 2 + tid * KCH;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) cp_async16(su + 16 * q, src + 16 * q);
+        for (int q = 0; q < 4; ++q) cp_async16(su + 16 * q, src + (long long)q * a.Hs * a.Ws * 16);
       } else {
         const __nv_bfloat16* src = xrow + pix * a.Cs + cb * KCH;
 #pragma unroll
@@ -441,18 +441,22 @@ __global__ void __launch_bounds__(128) gconv_wgrad_kernel(GConvWgradArgs a) {
   // staging loops below then need no integer division
   long long* s_pos = reinterpret_cast<long long*>(smem + NS * SB);
   {
+    // layer 1: frame-major s2d replay slot [frame][pixel][16]; later layers: [pixel][Cs]
     const long long grid = (long long)a.Hs * a.Ws * a.Cs;
+    const int pstride = a.first ? 16 : a.Cs;
     for (int q = tid; q < npos; q += 128) {
       const int im = img0 + q / HoWo, p = q % HoWo;
-      const long long base = a.first ? (long long)a.idx[im] * grid : (long long)im * grid;
-      s_pos[q] = base + ((long long)(p / a.Wo) * a.Ws + (p % a.Wo)) * a.Cs;
+      const long long base = a.first ? (long long)a.idx[im] * a.slot_stride : (long long)im * grid;
+      s_pos[q] = base + ((long long)(p / a.Wo) * a.Ws + (p % a.Wo)) * pstride;
     }
   }
   // this thread's fixed A row group (tid % 16) and tap, fixed B column group (tid % ng)
   const int gi_a = tid % 16, k0_a = tid / 16, r_a = m0 + 8 * gi_a;
   const bool r_ok = r_a < MK;
   const int t_a = r_ok ? r_a / a.Cs : 0, cc_a = r_ok ? r_a % a.Cs : 0;
-  const long long tapoff = ((long long)(t_a / a.Tw) * a.Ws + (t_a % a.Tw)) * a.Cs + cc_a;
+  const long long tapoff =
+      a.first ? ((long long)(t_a / a.Tw) * a.Ws + (t_a % a.Tw)) * 16 + (long long)(cc_a / 16) * a.Hs * a.Ws * 16 + cc_a % 16
+              : ((long long)(t_a / a.Tw) * a.Ws + (t_a % a.Tw)) * a.Cs + cc_a;
   const int gi_b = tid % ng, k0_b = tid / ng, kstep_b = 128 / ng;
   const __nv_bfloat16* dzr = a.dz + (long long)img0 * HoWo * a.N + 8 * gi_b;
   __syncthreads();
