@@ -535,3 +535,117 @@ out_rings:
   free(rings);
   return rc;
 }
+
+
+/* ======================================================================= NEXT-3 acting (Snake) */
+static void snake_draw(uint64_t seed, uint32_t env, uint64_t t, uint32_t purpose, uint32_t out[4]) {
+  const uint32_t ctr[4] = {env, (uint32_t)t, (uint32_t)(t >> 32), purpose};
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  or_philox4x32_10(ctr, key, out);
+}
+
+/* the k-th free cell (row-major) with k = floor(x * free / 2^32); -1 if the grid is full */
+static int snake_place_apple(const or_snake* g, int n, uint32_t x) {
+  char occ[1024];
+  memset(occ, 0, sizeof(occ));
+  for (int i = 0; i < g->len; ++i) occ[g->body[i]] = 1;
+  const int free_cells = n * n - g->len;
+  if (free_cells <= 0) return -1;
+  int k = (int)(((uint64_t)x * (uint64_t)free_cells) >> 32);
+  for (int c = 0; c < n * n; ++c)
+    if (!occ[c] && k-- == 0) return c;
+  return -1;
+}
+
+void or_snake_reset(or_snake* g, int n, uint64_t seed, uint32_t env, uint64_t t) {
+  const int c = n / 2;
+  g->len = 2;               /* "starts with body length of two", horizontal, heading right */
+  g->dir = 1;
+  g->since = 0;
+  g->body[0] = (int16_t)(c * n + c);
+  g->body[1] = (int16_t)(c * n + c - 1);
+  uint32_t x[4];
+  snake_draw(seed, env, t, 2, x);
+  g->apple = snake_place_apple(g, n, x[0]);
+}
+
+double or_snake_step(or_snake* g, int n, int action, uint64_t seed, uint32_t env, uint64_t t, int* term) {
+  *term = 0;
+  if ((action + 2) % 4 != g->dir) g->dir = action; /* a reversing action keeps the direction */
+  const int hy = g->body[0] / n, hx = g->body[0] % n;
+  const int ny = hy + (g->dir == 2) - (g->dir == 0), nx = hx + (g->dir == 1) - (g->dir == 3);
+  if (ny < 0 || ny >= n || nx < 0 || nx >= n) { *term = 1; return -1.0; } /* wall: death (SPEC closure) */
+  const int nh = ny * n + nx;
+  if (nh == g->apple) { /* eat: grow by one, +1, new apple */
+    for (int i = g->len; i > 0; --i) g->body[i] = g->body[i - 1];
+    g->body[0] = (int16_t)nh;
+    g->len += 1;
+    g->since = 0;
+    uint32_t x[4];
+    snake_draw(seed, env, t, 1, x);
+    g->apple = snake_place_apple(g, n, x[0]);
+    if (g->apple < 0) *term = 1; /* grid full */
+    return 1.0;
+  }
+  for (int i = 0; i < g->len - 1; ++i) /* the tail cell moves away this step */
+    if (g->body[i] == nh) { *term = 1; return -1.0; }
+  for (int i = g->len - 1; i > 0; --i) g->body[i] = g->body[i - 1];
+  g->body[0] = (int16_t)nh;
+  g->since += 1;
+  if (g->since >= 200 * n) *term = 1; /* step cap without an apple, reward 0 (SPEC) */
+  return 0.0;
+}
+
+void or_snake_render(const or_snake* g, int n, int px, uint8_t* frame) {
+  uint8_t cell[1024];
+  memset(cell, 0, sizeof(cell));
+  for (int i = 1; i < g->len; ++i) cell[g->body[i]] = 128;
+  cell[g->body[0]] = 191;
+  if (g->apple >= 0) cell[g->apple] = 255;
+  const int d = n * px;
+  for (int y = 0; y < d; ++y)
+    for (int x = 0; x < d; ++x) frame[y * d + x] = cell[(y / px) * n + (x / px)];
+}
+
+int or_eps_greedy(uint64_t seed, uint32_t env, uint64_t t, uint64_t eps_thr, int greedy) {
+  uint32_t x[4];
+  snake_draw(seed, env, t, 0, x);
+  if ((uint64_t)x[0] < eps_thr) return (int)(x[1] >> 30);
+  return greedy;
+}
+
+void or_collect(int n, int F, int H, int E, int64_t steps, uint64_t seed, uint64_t eps_thr, const int32_t* greedy,
+                int init, or_snake* games, uint8_t* stacks, uint64_t t0, int32_t* a_log, double* r_log,
+                uint8_t* t_log, int64_t* episodes) {
+  const int px = H / n;
+  const int64_t fb = (int64_t)H * H;
+  uint8_t* frame = (uint8_t*)malloc(fb);
+  if (init)
+    for (int e = 0; e < E; ++e) { /* episode start: the first frame replicated F times (SPEC) */
+      or_snake_reset(&games[e], n, seed, (uint32_t)e, ~0ULL);
+      or_snake_render(&games[e], n, px, frame);
+      for (int f = 0; f < F; ++f) memcpy(stacks + ((int64_t)e * F + f) * fb, frame, fb);
+    }
+  for (int64_t s = 0; s < steps; ++s) {
+    const uint64_t t = t0 + (uint64_t)s;
+    for (int e = 0; e < E; ++e) {
+      const int a = or_eps_greedy(seed, (uint32_t)e, t, eps_thr, greedy ? greedy[s * E + e] : 0);
+      int term;
+      const double r = or_snake_step(&games[e], n, a, seed, (uint32_t)e, t, &term);
+      if (a_log) a_log[s * E + e] = a;
+      if (r_log) r_log[s * E + e] = r;
+      if (t_log) t_log[s * E + e] = (uint8_t)term;
+      /* phi_{t+1}: drop the oldest frame, append the new one (Alg. 1 "preprocess", S:push_frame) */
+      uint8_t* st = stacks + (int64_t)e * F * fb;
+      memmove(st, st + fb, (size_t)((F - 1) * fb));
+      or_snake_render(&games[e], n, px, st + (F - 1) * fb);
+      if (term) {
+        if (episodes) episodes[e] += 1;
+        or_snake_reset(&games[e], n, seed, (uint32_t)e, t);
+        or_snake_render(&games[e], n, px, frame);
+        for (int f = 0; f < F; ++f) memcpy(st + f * fb, frame, fb);
+      }
+    }
+  }
+  free(frame);
+}

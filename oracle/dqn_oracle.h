@@ -102,6 +102,32 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
            double* theta_out, double* r_out, int64_t* n_out, double* loss, int64_t* idx, int32_t* amax,
            double* grad0, int64_t* stale_hist /* [32]: staleness n_apply - n_local per replica step (A25) */);
 
+/* ---- NEXT-3: the acting side of Alg. 1 on the paper's Snake game (rules
+ * closed in SPEC S:216-262, readings A34-A36 in DESIGN.md). Actions 0 up, 1 right, 2 down, 3 left;
+ * a reversing action keeps the direction. Cells: empty 0, body 128, head 191, apple 255 (u8 of the
+ * SPEC's 0 / 0.5 / 0.75 / 1 render, rounded). Frames are the grid scaled by an integer factor
+ * (area averaging of whole cells = replication). Random draws: Philox4x32-10 with key = seed,
+ * counter (env, t_lo, t_hi, purpose): purpose 0 the eps-greedy draws (x0 explore, x1 action), 1 the
+ * apple after eating, 2 the apple of a reset (the initial reset uses t = 2^64 - 1). */
+typedef struct {
+  int32_t len, dir, apple, since;   /* body length, direction, apple cell, steps since the last apple */
+  int16_t body[1024];               /* cells y*n + x, head first (n*n <= 1024) */
+} or_snake;
+void or_snake_reset(or_snake* g, int n, uint64_t seed, uint32_t env, uint64_t t);
+/* one step; returns the reward, sets *term (wall / self collision -1, grid full or 200*n steps
+ * without an apple 0); a terminal step leaves the state unchanged */
+double or_snake_step(or_snake* g, int n, int action, uint64_t seed, uint32_t env, uint64_t t, int* term);
+void or_snake_render(const or_snake* g, int n, int px, uint8_t* frame /* [n*px][n*px] */);
+/* eps-greedy: explore iff x0 < eps_thr (eps_thr = floor(eps * 2^32) in [0, 2^32]); the
+ * random action is x1 >> 30 (4 actions); else the given greedy action */
+int or_eps_greedy(uint64_t seed, uint32_t env, uint64_t t, uint64_t eps_thr, int greedy);
+/* E envs, `steps` acting steps of the collector with the greedy actions given per step
+ * (greedy[steps][E], may be NULL when eps_thr = 2^32): stacks [E][F][H][W] in/out (F frames,
+ * oldest first; created by the initial reset when init != 0), per-step logs (may be NULL). */
+void or_collect(int n, int F, int H, int E, int64_t steps, uint64_t seed, uint64_t eps_thr, const int32_t* greedy,
+                int init, or_snake* games, uint8_t* stacks, uint64_t t0, int32_t* a_log, double* r_log,
+                uint8_t* t_log, int64_t* episodes);
+
 #ifdef __cplusplus
 }
 #endif

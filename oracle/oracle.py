@@ -11,6 +11,7 @@ are DESIGN.md §3 (A1..A29).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from dataclasses import dataclass, field
@@ -133,10 +134,69 @@ def lib():
         _lib.or_min_abs_preact.restype = C.c_double
         _lib.or_min_abs_preact.argtypes = [C.POINTER(_Net), D, C.c_int64, U8]
         _lib.or_rmsprop.argtypes = [D, D, D, C.c_int64, C.c_double, C.c_double, C.c_double]
+        _lib.or_snake_reset.argtypes = [C.POINTER(Snake), C.c_int, C.c_uint64, C.c_uint32, C.c_uint64]
+        _lib.or_snake_step.restype = C.c_double
+        _lib.or_snake_step.argtypes = [C.POINTER(Snake), C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_uint64,
+                                       C.POINTER(C.c_int)]
+        _lib.or_snake_render.argtypes = [C.POINTER(Snake), C.c_int, C.c_int, U8]
+        _lib.or_eps_greedy.restype = C.c_int
+        _lib.or_eps_greedy.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int]
+        _lib.or_collect.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_uint64, C.c_uint64, I32,
+                                    C.c_int, C.POINTER(Snake), U8, C.c_uint64, I32, D, U8, I64]
         _lib.or_run.restype = C.c_int
         _lib.or_run.argtypes = [C.POINTER(_Net), C.POINTER(_Cfg), C.c_int64, I64, C.POINTER(U8), C.POINTER(I32),
                                 C.POINTER(D), C.POINTER(U8), C.POINTER(U8), D, C.c_int64, D, D, I64, D, I64, I32, D, I64]
     return _lib
+
+
+class Snake(C.Structure):
+    """or_snake: body length, direction, apple cell, steps since the last apple, body cells head first."""
+    _fields_ = [("len", C.c_int32), ("dir", C.c_int32), ("apple", C.c_int32), ("since", C.c_int32),
+                ("body", C.c_int16 * 1024)]
+
+
+def eps_threshold(eps: float) -> int:
+    """floor(eps * 2^32) in [0, 2^32]: explore iff the 32-bit draw is below it."""
+    return min(1 << 32, int(math.floor(eps * 4294967296.0)))
+
+
+def snake_reset(n: int, seed: int, env: int, t: int) -> Snake:
+    g = Snake()
+    lib().or_snake_reset(C.byref(g), n, seed, env, t)
+    return g
+
+
+def snake_step(g: Snake, n: int, action: int, seed: int, env: int, t: int):
+    term = C.c_int(0)
+    r = lib().or_snake_step(C.byref(g), n, action, seed, env, t, C.byref(term))
+    return r, bool(term.value)
+
+
+def snake_render(g: Snake, n: int, px: int) -> np.ndarray:
+    f = np.zeros((n * px, n * px), np.uint8)
+    lib().or_snake_render(C.byref(g), n, px, _p(f, C.c_uint8))
+    return f
+
+
+def eps_greedy(seed: int, env: int, t: int, eps: float, greedy: int) -> int:
+    return int(lib().or_eps_greedy(seed, env, t, eps_threshold(eps), greedy))
+
+
+def collect(n: int, F: int, H: int, E: int, steps: int, seed: int, eps: float, greedy=None, state=None, t0: int = 0):
+    """E Snake games x `steps` eps-greedy acting steps (or_collect). state = (games, stacks) to continue a
+    previous call (else the initial resets). Returns dict(stacks, games, a, r, term, episodes)."""
+    init = state is None
+    games = (Snake * E)() if init else state[0]
+    stacks = np.zeros((E, F, H, H), np.uint8) if init else state[1]
+    a = np.zeros((steps, E), np.int32)
+    r = np.zeros((steps, E), np.float64)
+    t = np.zeros((steps, E), np.uint8)
+    ep = np.zeros(E, np.int64)
+    gr = None if greedy is None else np.ascontiguousarray(greedy, dtype=np.int32)
+    lib().or_collect(n, F, H, E, steps, seed, eps_threshold(eps), _p(gr, C.c_int32) if gr is not None else None,
+                     int(init), games, _p(stacks, C.c_uint8), t0, _p(a, C.c_int32), _p(r, C.c_double),
+                     _p(t, C.c_uint8), _p(ep, C.c_int64))
+    return dict(stacks=stacks, games=games, a=a, r=r, term=t, episodes=ep)
 
 
 def _p(a: np.ndarray, ct):
