@@ -183,6 +183,33 @@ int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, float* q, int32
  * working copy equals the gathered SERVER vector and is returned as such. */
 int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, int64_t* n_params, uint64_t* generation);
 
+/* NEXT-3 — the acting side of Alg. 1 on the GPU: n_envs parallel games of the paper's
+ * Snake (an n x n grid, `grid` = n, rendered at height/n pixels per cell; rules closed as in
+ * walls and self-collision end the game with -1, an apple gives +1 and one body
+ * length, 200*n steps without an apple end it with 0; A34-A36), played for `steps` steps with
+ * the eps-greedy behaviour policy on Q(phi; theta_local) from the network's forward; every
+ * step's transition (phi_t, a_t, r_t, phi_{t+1}, terminal) is stored into the replay on the device.
+ * Needs n_actions == 4 (up, right, down, left), height == width, height % grid == 0, 4 <= grid <= 32,
+ * height*width % 16 == 0 and n_envs <= minibatch. The games persist in the context: the first call
+ * creates them from (n_envs, grid, env_seed); later calls must pass the same values and continue.
+ * Random draws are Philox4x32-10 keyed by env_seed (counter: env, step, purpose), so runs are
+ * reproducible and equal the oracle's or_collect whenever the greedy actions agree (always at eps=1).
+ * stats (may be NULL): env_steps, episodes finished, reward sum, device ms, optional per-step
+ * logs [steps][n_envs] of actions / rewards / terminals (host or device, NULL to skip). */
+typedef struct {
+  int64_t env_steps;
+  int64_t episodes;
+  double reward_sum;
+  float device_ms;
+  int32_t* actions;
+  float* rewards;
+  uint8_t* terminals;
+} dqn_collect_stats;
+int dqn_collect(dqn_ctx* ctx, int32_t n_envs, int32_t grid, int64_t steps, double epsilon, uint64_t env_seed,
+                dqn_collect_stats* stats);
+/* The current frame stacks of the collector's games, [n_envs][F][H][W] u8 (host or device). */
+int dqn_env_stacks(dqn_ctx* ctx, uint8_t* out, int64_t cap_bytes);
+
 /* Replay occupancy: total pushes so far and min(count, capacity). */
 int dqn_replay_size(const dqn_ctx* ctx, int64_t* count, int64_t* size);
 

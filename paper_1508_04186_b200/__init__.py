@@ -54,6 +54,11 @@ class _Stats(C.Structure):
                 ("staleness_hist", C.c_int64 * 32)]
 
 
+class _CollectStats(C.Structure):
+    _fields_ = [("env_steps", C.c_int64), ("episodes", C.c_int64), ("reward_sum", C.c_double), ("device_ms", C.c_float),
+                ("actions", C.c_void_p), ("rewards", C.c_void_p), ("terminals", C.c_void_p)]
+
+
 class _RegionTime(C.Structure):
     _fields_ = [("name", C.c_char * 48), ("avg_us", C.c_double), ("kernels", C.c_int32), ("steps", C.c_int32)]
 
@@ -132,12 +137,15 @@ def lib() -> C.CDLL:
         L.dqn_last_error.restype = C.c_char_p
         L.dqn_last_error.argtypes = [P]
         L.dqn_destroy.argtypes = [P]
+        L.dqn_collect.argtypes = [P, C.c_int32, C.c_int32, C.c_int64, C.c_double, C.c_uint64, C.POINTER(_CollectStats)]
+        L.dqn_env_stacks.argtypes = [P, P, C.c_int64]
         _lib = L
     return _lib
 
 
 EXPORTED = ("dqn_param_count", "dqn_nccl_id_bytes", "dqn_nccl_unique_id", "dqn_create", "dqn_push_transitions",
-            "dqn_train_steps", "dqn_profile_steps", "dqn_q_values", "dqn_get_params", "dqn_replay_size", "dqn_last_error", "dqn_destroy")
+            "dqn_train_steps", "dqn_profile_steps", "dqn_q_values", "dqn_get_params", "dqn_replay_size", "dqn_last_error",
+            "dqn_destroy", "dqn_collect", "dqn_env_stacks")
 
 
 def param_count(cfg: Config) -> int:
@@ -216,6 +224,26 @@ class DQN:
                    device_ms=st.device_ms, nonfinite_elems=st.nonfinite_elems, idx=idx, argmax=am, loss=lp,
                    kernel_launches=st.kernel_launches, staleness=np.array(st.staleness_hist[:], np.int64), rc=rc)
         self._check(rc)
+        return out
+
+    def collect(self, n_envs: int, grid: int, steps: int, epsilon: float, seed: int, want_log: bool = False) -> dict:
+        """NEXT-3: `steps` acting steps of n_envs on-GPU Snake games with the eps-greedy policy on theta_local;
+        every transition is stored into the replay. Returns stats (+ per-step logs [steps][n_envs])."""
+        st = _CollectStats()
+        logs = {}
+        if want_log:
+            logs = dict(a=np.zeros((steps, n_envs), np.int32), r=np.zeros((steps, n_envs), np.float32),
+                        term=np.zeros((steps, n_envs), np.uint8))
+            st.actions, st.rewards, st.terminals = (logs["a"].ctypes.data, logs["r"].ctypes.data,
+                                                    logs["term"].ctypes.data)
+        self._check(lib().dqn_collect(self._h, n_envs, grid, steps, epsilon, seed, C.byref(st)))
+        return dict(env_steps=st.env_steps, episodes=st.episodes, reward_sum=st.reward_sum, device_ms=st.device_ms,
+                    **logs)
+
+    def env_stacks(self, n_envs: int) -> np.ndarray:
+        c = self.cfg
+        out = np.zeros((n_envs, c.frames, c.height, c.width), np.uint8)
+        self._check(lib().dqn_env_stacks(self._h, out.ctypes.data, out.nbytes))
         return out
 
     def profile(self, k: int) -> list:

@@ -290,6 +290,31 @@ void launch_gemm_pipe(const TcGemmArgs& a, int groups, cudaStream_t st);
 void launch_fc_reduce(const TcGemmArgs& a, int groups, cudaStream_t st);
 void launch_head_finish_warp(const HeadArgs& h, cudaStream_t st);
 
+// ---- NEXT-3 on-GPU acting (kernels_env.cu): Snake games, eps-greedy, Store
+struct EnvGame {
+  int32_t len, dir, apple, since;  // body length, direction (0 up 1 right 2 down 3 left), apple cell, steps since apple
+  int16_t body[1024];              // cells y*n + x, head first
+};
+struct EnvArgs {
+  EnvGame* games;
+  uint8_t* stacks;                 // [E][F][H][H] current phi of every game
+  uint8_t *s_stage, *sn_stage;     // [E][F][H][H] the step's transition (push input)
+  int32_t* a_stage;
+  float* r_stage;
+  uint8_t* t_stage;
+  const int* greedy;               // [E] argmax Q of the current stacks
+  int n, F, H, E;
+  unsigned long long seed, t, eps_thr;
+  int32_t* a_log;                  // optional [steps][E] logs (row log_row)
+  float* r_log;
+  uint8_t* t_log;
+  long long log_row;
+  long long* episodes;             // [E] finished episodes
+  double* reward_sum;              // [E] accumulated reward
+};
+void launch_env_init(const EnvArgs& a, cudaStream_t st);
+void launch_env_act(const EnvArgs& a, cudaStream_t st);
+
 struct ReduceUpdateArgs {
   BwdConvArgs b;                   // the conv partials and offsets
   float* theta;                    // fp32 theta (= theta_local at N = 1)

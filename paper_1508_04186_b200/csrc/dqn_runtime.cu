@@ -91,6 +91,17 @@ struct dqn_ctx {
   std::vector<long long> round_nloc;              // n_local of the steps of the current round
   // NEXT-1 fused server round over NVLink peer memory (world > 1, deterministic, n_fetch == 1)
   bool fused_comm = false;
+  // NEXT-3 collector (dqn_collect): the games persist between calls
+  struct Collector {
+    int E = 0, n = 0;
+    unsigned long long seed = 0, t = 0;
+    EnvGame* games = nullptr;
+    uint8_t *stacks = nullptr, *s_stage = nullptr, *sn_stage = nullptr, *t_stage = nullptr;
+    int32_t* a_stage = nullptr;
+    float* r_stage = nullptr;
+    long long* episodes = nullptr;
+    double* reward_sum = nullptr;
+  } env;
   long long n_per_round = 1;  // server generations per push round: 1 (mean rule) or N (per-gradient rule)
   ServerRoundArgs sra{};                          // peer pointers etc., filled at create
   FusedAcquire acq{};                             // the next step's acquire half (acq.ctr == nullptr: off)
@@ -372,6 +383,12 @@ static void free_all(dqn_ctx* c) {
     if (G.dz) cudaFree(G.dz);
   }
   if (c->pack_map) cudaFree(c->pack_map);
+  {
+    void* ep[] = {c->env.games, c->env.stacks, c->env.s_stage, c->env.sn_stage, c->env.t_stage, c->env.a_stage,
+                  c->env.r_stage, c->env.episodes, c->env.reward_sum};
+    for (void* p : ep)
+      if (p) cudaFree(p);
+  }
   if (c->gw_partial) cudaFree(c->gw_partial);
   if (c->gw_partial_db) cudaFree(c->gw_partial_db);
   for (int i = 0; i < 2; ++i) {
@@ -1755,6 +1772,217 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
 }
 
 // ------------------------------------------------------------------ acting boundary (a15)
+// The forward of m <= b states already in ctx->q_stage (canonical u8) with theta_local, Q into
+// ctx->q_out [m][A] and the greedy actions into ctx->q_amax [m] (lowest index on ties); enqueued on
+// the context stream without a host synchronisation (a15; reused by the on-GPU collector).
+static int q_enqueue(dqn_ctx* ctx, int m) {
+  const NetShape& net = ctx->net;
+  const int b = ctx->cfg.minibatch;
+  const long long sb = net.state_bytes;
+  (void)sb;
+  cudaStream_t st = ctx->stream;
+  const float* in = nullptr;
+  if (ctx->gpath) {  // s2d staging, the generic tensor-core conv forward, FC split-K + reduction
+    const FcShape& F = net.fc[0];
+    launch_push_s2d(ctx->q_stage_s2d, nullptr, nullptr, nullptr, nullptr, b, 0, 0, m, ctx->q_stage, nullptr,
+                    nullptr, nullptr, nullptr, st);
+    for (int i = 0; i < net.n_conv; ++i) {
+      const ConvShape& L = net.conv[i];
+      const dqn_ctx::GLayer& G = ctx->gl[i];
+      GConvFwdArgs a{};
+      a.first = i == 0;
+      if (i == 0) { a.ring[0] = ctx->q_stage_s2d; a.slot_stride = kMnihSlot; }  // ctr == nullptr: image j = slot j
+      else a.x[0] = G.x[0];
+      a.b = m; a.Hs = G.Hs; a.Ws = G.Ws; a.Cs = G.Cs; a.Th = G.Th; a.Tw = G.Tw; a.Ho = G.Ho; a.Wo = G.Wo; a.N = L.N;
+      a.s_next = i + 1 < net.n_conv ? ctx->gl[i + 1].s : 0;
+      a.wpk[0] = ctx->theta_local_bf16 + ctx->gpack_off + G.fwd_pack;
+      a.bias[0] = ctx->theta_local + L.b_off;
+      a.out[0] = i + 1 < net.n_conv ? ctx->gl[i + 1].x[0] : ctx->a2_bf16;
+      launch_gconv_fwd(a, 1, st);
+    }
+    TcGemmArgs gf{};
+    gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.lda = F.D;
+    gf.B[0] = ctx->a2_bf16; gf.ldb = F.D;
+    gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = std::min(128, (m + 15) / 16 * 16); gf.kper = F.D / ctx->fc_splits;
+    gf.splits = ctx->fc_splits; gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
+    gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
+    launch_gemm_pipe(gf, 1, st);
+    launch_fc_reduce(gf, 1, st);
+    in = ctx->act_fc[0][0];
+  } else if (ctx->bf16) {  // conv1's s2d staging, then the tensor-core forward with theta_local
+    const FcShape& F = net.fc[0];
+    launch_push_s2d(ctx->q_stage_s2d, nullptr, nullptr, nullptr, nullptr, b, 0, 0, m, ctx->q_stage, nullptr,
+                    nullptr, nullptr, nullptr, st);
+    FwdConvArgs fa{};
+    fa.ring[0] = ctx->q_stage_s2d;
+    fa.img_off = ctx->img_off;
+    fa.slot_stride = kMnihSlot;
+    fa.theta[0] = ctx->theta_local_bf16;
+    fa.theta_f32[0] = ctx->theta_local;
+    fa.w1_off = net.conv[0].w_off; fa.b1_off = net.conv[0].b_off;
+    fa.w2_off = net.conv[1].w_off; fa.b2_off = net.conv[1].b_off;
+    fa.n = m; fa.a2 = ctx->a2_bf16;
+    launch_fwd_conv_bf16(fa, 1, st);
+    TcGemmArgs gf{};
+    gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.lda = F.D;
+    gf.B[0] = ctx->a2_bf16; gf.ldb = F.D;
+    gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = (m + 15) / 16 * 16; gf.kper = F.D / ctx->fc_splits;
+    gf.splits = ctx->fc_splits; gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
+    gf.pre_a = 1; gf.pre_b = 0;
+    gf.counters = ctx->tc_counters; gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
+    launch_tc_gemm(gf, 1, st);
+    in = ctx->act_fc[0][0];
+  } else {
+  ImgSrc src{};
+  src.u8[0] = ctx->q_stage;
+  src.stride = sb;
+  for (int i = 0; i < net.n_conv; ++i) {
+    ImgSrc s2 = src;
+    if (i > 0) {
+      s2 = ImgSrc{};
+      s2.f32[0] = ctx->act_conv[i - 1][0];
+      const ConvShape& P = net.conv[i - 1];
+      s2.stride = (long long)P.N * P.Ho * P.Wo;
+    }
+    launch_conv_fwd_f32(net.conv[i], s2, ctx->theta_local, nullptr, ctx->act_conv[i][0], nullptr, m, 1, st);
+  }
+  in = ctx->act_conv[net.n_conv - 1][0];
+  }
+  for (int l = 0; l < net.n_fc && !ctx->bf16; ++l) {
+    const FcShape& F = net.fc[l];
+    GemmArgs g{};
+    g.A[0] = in; g.sam = F.D; g.sak = 1;
+    g.B[0] = ctx->theta_local + F.w_off; g.sbk = 1; g.sbn = F.D;
+    g.C[0] = ctx->act_fc[l][0]; g.scm = F.H; g.scn = 1;
+    g.bias[0] = ctx->theta_local + F.b_off;
+    g.M = m; g.N = F.H; g.K = F.D; g.groups = 1; g.splits = pick_splits(b, F.H, F.D, 1);
+    g.epi = EPI_BIAS_RELU; g.partial = ctx->partial;
+    launch_gemm_f32(g, st);
+    in = ctx->act_fc[l][0];
+  }
+  const FcShape& O = net.fc[net.n_fc];
+  launch_q_head_f32(in, ctx->theta_local, O.w_off, O.b_off, O.D, O.H, m, ctx->q_out, ctx->q_amax, st);
+  CK(cudaGetLastError());
+  return DQN_OK;
+}
+
+// ------------------------------------------------------------------ NEXT-3: on-GPU acting
+extern "C" int dqn_collect(dqn_ctx* ctx, int32_t n_envs, int32_t grid, int64_t steps, double epsilon, uint64_t env_seed,
+                           dqn_collect_stats* stats) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  const NetShape& net = ctx->net;
+  const int F = net.F, H = net.Hin;
+  if (net.A != 4) return set_err(ctx, DQN_EINVAL, "dqn_collect: the Snake game needs n_actions == 4");
+  if (net.Hin != net.Win || grid < 4 || grid > 32 || H % grid != 0 || ((long long)H * H) % 16 != 0)
+    return set_err(ctx, DQN_EINVAL, "dqn_collect: needs square frames, 4 <= grid <= 32, height % grid == 0, H*H % 16 == 0");
+  if (n_envs < 1 || n_envs > ctx->cfg.minibatch || n_envs > ctx->cap || steps < 0 || !(epsilon >= 0.0 && epsilon <= 1.0))
+    return set_err(ctx, DQN_EINVAL, "dqn_collect: 1 <= n_envs <= min(minibatch, capacity), steps >= 0, eps in [0, 1]");
+  dqn_ctx::Collector& C = ctx->env;
+  cudaStream_t st = ctx->stream;
+  const long long sb = net.state_bytes;
+  int rc;
+  if (!C.games) {
+    C.E = n_envs; C.n = grid; C.seed = env_seed; C.t = 0;
+    if ((rc = dalloc(ctx, &C.games, n_envs))) return rc;
+    if ((rc = dalloc(ctx, &C.stacks, n_envs * sb))) return rc;
+    if ((rc = dalloc(ctx, &C.s_stage, n_envs * sb))) return rc;
+    if ((rc = dalloc(ctx, &C.sn_stage, n_envs * sb))) return rc;
+    if ((rc = dalloc(ctx, &C.t_stage, n_envs))) return rc;
+    if ((rc = dalloc(ctx, &C.a_stage, n_envs))) return rc;
+    if ((rc = dalloc(ctx, &C.r_stage, n_envs))) return rc;
+    if ((rc = dalloc(ctx, &C.episodes, n_envs))) return rc;
+    if ((rc = dalloc(ctx, &C.reward_sum, n_envs))) return rc;
+    CK(cudaMemsetAsync(C.episodes, 0, sizeof(long long) * n_envs, st));
+    CK(cudaMemsetAsync(C.reward_sum, 0, sizeof(double) * n_envs, st));
+    EnvArgs a{};
+    a.games = C.games; a.stacks = C.stacks; a.n = grid; a.F = F; a.H = H; a.E = n_envs; a.seed = env_seed;
+    launch_env_init(a, st);
+    CK(cudaGetLastError());
+  } else if (C.E != n_envs || C.n != grid || C.seed != env_seed) {
+    return set_err(ctx, DQN_EINVAL, "dqn_collect: n_envs, grid and env_seed must match the first call");
+  }
+  // per-call logs (device scratch when the caller passes host buffers)
+  int32_t* a_log = nullptr;
+  float* r_log = nullptr;
+  uint8_t* t_log = nullptr;
+  const bool want = stats && (stats->actions || stats->rewards || stats->terminals) && steps > 0;
+  if (want) {
+    if ((rc = dalloc(ctx, &a_log, steps * n_envs))) return rc;
+    if ((rc = dalloc(ctx, &r_log, steps * n_envs))) return rc;
+    if ((rc = dalloc(ctx, &t_log, steps * n_envs))) return rc;
+  }
+  std::vector<long long> ep0(n_envs), ep1(n_envs);
+  std::vector<double> rs0(n_envs), rs1(n_envs);
+  CK(cudaMemcpyAsync(ep0.data(), C.episodes, sizeof(long long) * n_envs, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rs0.data(), C.reward_sum, sizeof(double) * n_envs, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(ctx->ev0, st));
+  const unsigned long long thr =
+      epsilon >= 1.0 ? (1ULL << 32) : (unsigned long long)std::floor(epsilon * 4294967296.0);
+  for (long long s = 0; s < steps; ++s) {
+    // Q(phi; theta_local) of every game's stack, greedy actions into ctx->q_amax
+    CK(cudaMemcpyAsync(ctx->q_stage, C.stacks, n_envs * sb, cudaMemcpyDeviceToDevice, st));
+    if ((rc = q_enqueue(ctx, n_envs))) return rc;
+    EnvArgs a{};
+    a.games = C.games; a.stacks = C.stacks; a.s_stage = C.s_stage; a.sn_stage = C.sn_stage;
+    a.a_stage = C.a_stage; a.r_stage = C.r_stage; a.t_stage = C.t_stage; a.greedy = ctx->q_amax;
+    a.n = grid; a.F = F; a.H = H; a.E = n_envs; a.seed = env_seed; a.t = C.t; a.eps_thr = thr;
+    a.a_log = a_log; a.r_log = r_log; a.t_log = t_log; a.log_row = s;
+    a.episodes = C.episodes; a.reward_sum = C.reward_sum;
+    launch_env_act(a, st);
+    // Store (Alg. 1): the step's transitions into the replay, on the device
+    push_ring(ctx, 0, n_envs, C.s_stage, C.a_stage, C.r_stage, C.sn_stage, C.t_stage);
+    CK(cudaGetLastError());
+    ctx->count += n_envs;
+    C.t += 1;
+  }
+  CK(cudaEventRecord(ctx->ev1, st));
+  CK(cudaMemcpyAsync(ep1.data(), C.episodes, sizeof(long long) * n_envs, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rs1.data(), C.reward_sum, sizeof(double) * n_envs, cudaMemcpyDeviceToHost, st));
+  if (want) {
+    auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost; };
+    if (stats->actions)
+      CK(cudaMemcpyAsync(stats->actions, a_log, sizeof(int32_t) * steps * n_envs, kind(stats->actions), st));
+    if (stats->rewards)
+      CK(cudaMemcpyAsync(stats->rewards, r_log, sizeof(float) * steps * n_envs, kind(stats->rewards), st));
+    if (stats->terminals)
+      CK(cudaMemcpyAsync(stats->terminals, t_log, steps * n_envs, kind(stats->terminals), st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (want) {
+    cudaFree(a_log);
+    cudaFree(r_log);
+    cudaFree(t_log);
+  }
+  if (stats) {
+    stats->env_steps = steps * n_envs;
+    long long de = 0;
+    double dr = 0.0;
+    for (int e = 0; e < n_envs; ++e) {
+      de += ep1[e] - ep0[e];
+      dr += rs1[e] - rs0[e];
+    }
+    stats->episodes = de;
+    stats->reward_sum = dr;
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    stats->device_ms = ms;
+  }
+  return DQN_OK;
+}
+
+extern "C" int dqn_env_stacks(dqn_ctx* ctx, uint8_t* out, int64_t cap_bytes) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  if (!ctx->env.games) return set_err(ctx, DQN_ESTATE, "dqn_env_stacks: no games yet (call dqn_collect first)");
+  const long long bytes = (long long)ctx->env.E * ctx->net.state_bytes;
+  if (!out || cap_bytes < bytes) return set_err(ctx, DQN_EINVAL, "dqn_env_stacks: output smaller than n_envs * F*H*W");
+  CK(cudaMemcpyAsync(out, ctx->env.stacks, bytes, is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DQN_OK;
+}
+
 extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, float* q, int32_t* argmax) {
   if (!ctx) return DQN_EINVAL;
   if (ctx->poisoned) return DQN_ESTATE;
@@ -1768,88 +1996,8 @@ extern "C" int dqn_q_values(dqn_ctx* ctx, int64_t n, const uint8_t* states, floa
     const int m = (int)std::min<long long>(b, n - i0);
     CK(cudaMemcpyAsync(ctx->q_stage, states + i0 * sb, m * sb, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        st));
-    const float* in = nullptr;
-    if (ctx->gpath) {  // s2d staging, the generic tensor-core conv forward, FC split-K + reduction
-      const FcShape& F = net.fc[0];
-      launch_push_s2d(ctx->q_stage_s2d, nullptr, nullptr, nullptr, nullptr, b, 0, 0, m, ctx->q_stage, nullptr,
-                      nullptr, nullptr, nullptr, st);
-      for (int i = 0; i < net.n_conv; ++i) {
-        const ConvShape& L = net.conv[i];
-        const dqn_ctx::GLayer& G = ctx->gl[i];
-        GConvFwdArgs a{};
-        a.first = i == 0;
-        if (i == 0) { a.ring[0] = ctx->q_stage_s2d; a.slot_stride = kMnihSlot; }  // ctr == nullptr: image j = slot j
-        else a.x[0] = G.x[0];
-        a.b = m; a.Hs = G.Hs; a.Ws = G.Ws; a.Cs = G.Cs; a.Th = G.Th; a.Tw = G.Tw; a.Ho = G.Ho; a.Wo = G.Wo; a.N = L.N;
-        a.s_next = i + 1 < net.n_conv ? ctx->gl[i + 1].s : 0;
-        a.wpk[0] = ctx->theta_local_bf16 + ctx->gpack_off + G.fwd_pack;
-        a.bias[0] = ctx->theta_local + L.b_off;
-        a.out[0] = i + 1 < net.n_conv ? ctx->gl[i + 1].x[0] : ctx->a2_bf16;
-        launch_gconv_fwd(a, 1, st);
-      }
-      TcGemmArgs gf{};
-      gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.lda = F.D;
-      gf.B[0] = ctx->a2_bf16; gf.ldb = F.D;
-      gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = std::min(128, (m + 15) / 16 * 16); gf.kper = F.D / ctx->fc_splits;
-      gf.splits = ctx->fc_splits; gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
-      gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
-      launch_gemm_pipe(gf, 1, st);
-      launch_fc_reduce(gf, 1, st);
-      in = ctx->act_fc[0][0];
-    } else if (ctx->bf16) {  // conv1's s2d staging, then the tensor-core forward with theta_local
-      const FcShape& F = net.fc[0];
-      launch_push_s2d(ctx->q_stage_s2d, nullptr, nullptr, nullptr, nullptr, b, 0, 0, m, ctx->q_stage, nullptr,
-                      nullptr, nullptr, nullptr, st);
-      FwdConvArgs fa{};
-      fa.ring[0] = ctx->q_stage_s2d;
-      fa.img_off = ctx->img_off;
-      fa.slot_stride = kMnihSlot;
-      fa.theta[0] = ctx->theta_local_bf16;
-      fa.theta_f32[0] = ctx->theta_local;
-      fa.w1_off = net.conv[0].w_off; fa.b1_off = net.conv[0].b_off;
-      fa.w2_off = net.conv[1].w_off; fa.b2_off = net.conv[1].b_off;
-      fa.n = m; fa.a2 = ctx->a2_bf16;
-      launch_fwd_conv_bf16(fa, 1, st);
-      TcGemmArgs gf{};
-      gf.A[0] = ctx->theta_local_bf16 + F.w_off; gf.lda = F.D;
-      gf.B[0] = ctx->a2_bf16; gf.ldb = F.D;
-      gf.M = F.H; gf.N = m; gf.K = F.D; gf.BN = (m + 15) / 16 * 16; gf.kper = F.D / ctx->fc_splits;
-      gf.splits = ctx->fc_splits; gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
-      gf.pre_a = 1; gf.pre_b = 0;
-      gf.counters = ctx->tc_counters; gf.bias[0] = ctx->theta_local + F.b_off; gf.h_out[0] = ctx->act_fc[0][0];
-      launch_tc_gemm(gf, 1, st);
-      in = ctx->act_fc[0][0];
-    } else {
-    ImgSrc src{};
-    src.u8[0] = ctx->q_stage;
-    src.stride = sb;
-    for (int i = 0; i < net.n_conv; ++i) {
-      ImgSrc s2 = src;
-      if (i > 0) {
-        s2 = ImgSrc{};
-        s2.f32[0] = ctx->act_conv[i - 1][0];
-        const ConvShape& P = net.conv[i - 1];
-        s2.stride = (long long)P.N * P.Ho * P.Wo;
-      }
-      launch_conv_fwd_f32(net.conv[i], s2, ctx->theta_local, nullptr, ctx->act_conv[i][0], nullptr, m, 1, st);
-    }
-    in = ctx->act_conv[net.n_conv - 1][0];
-    }
-    for (int l = 0; l < net.n_fc && !ctx->bf16; ++l) {
-      const FcShape& F = net.fc[l];
-      GemmArgs g{};
-      g.A[0] = in; g.sam = F.D; g.sak = 1;
-      g.B[0] = ctx->theta_local + F.w_off; g.sbk = 1; g.sbn = F.D;
-      g.C[0] = ctx->act_fc[l][0]; g.scm = F.H; g.scn = 1;
-      g.bias[0] = ctx->theta_local + F.b_off;
-      g.M = m; g.N = F.H; g.K = F.D; g.groups = 1; g.splits = pick_splits(b, F.H, F.D, 1);
-      g.epi = EPI_BIAS_RELU; g.partial = ctx->partial;
-      launch_gemm_f32(g, st);
-      in = ctx->act_fc[l][0];
-    }
-    const FcShape& O = net.fc[net.n_fc];
-    launch_q_head_f32(in, ctx->theta_local, O.w_off, O.b_off, O.D, O.H, m, ctx->q_out, ctx->q_amax, st);
-    CK(cudaGetLastError());
+    int rc = q_enqueue(ctx, m);
+    if (rc) return rc;
     CK(cudaMemcpyAsync(q + i0 * net.A, ctx->q_out, sizeof(float) * m * net.A,
                        dev_q ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
     if (argmax)
