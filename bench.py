@@ -244,6 +244,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--profile-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-acting", dest="acting", action="store_false",
+                    help="skip the on-GPU acting measurement (NEXT-3)")
     ap.add_argument("--dedup", action="store_true",
                     help="frame-deduplicated replay (F+1 frames per slot; G-pong stacks slide by one frame)")
     args = ap.parse_args()
@@ -362,6 +364,18 @@ def main():
            "what": "per step: dqn_push_transitions of 1 new experience from pinned host memory + "
                    "dqn_train_steps(1) + loss/counters D2H"}
 
+    # ---- NEXT-3 acting: on-GPU Snake games, eps-greedy on Q from the forward, Store into the replay
+    acting = None
+    if args.acting and world == 1:
+        acfg = D.Config(**dict(MNIH, n_actions=4), minibatch=256, replay_capacity=100_000, precision=cfg.precision)
+        ag = D.DQN(acfg, stream=stream.cuda_stream)
+        ag.collect(256, 12, 3, 0.1, 0xACE)  # creates the games; warm-up
+        ares = ag.collect(256, 12, 100, 0.1, 0xACE)
+        acting = {"env_steps_per_s": ares["env_steps"] / (ares["device_ms"] / 1e3), "n_envs": 256, "steps": 100,
+                  "epsilon": 0.1, "game": "Snake 12x12 rendered 84x84 (P:216, SPEC closures)",
+                  "what": "per step: Q forward of 256 stacks, eps-greedy, game step + render, Store into the replay"}
+        ag.close()
+
     # ---- per-region device times (CUDA events inside the replayed step graph)
     regions = dqn.profile(args.profile_steps) if args.profile_steps > 0 else []
     pk = peaks()
@@ -411,6 +425,7 @@ def main():
         "staleness_hist": [int(x) for x in out["staleness"][:8]] if C["async"] else None,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "acting": acting,
         "roofline": roof,
         "regions_us": {r["name"]: round(r["avg_us"], 2) for r in regions},
     }
