@@ -325,8 +325,14 @@ struct ReduceUpdateArgs {
   __nv_bfloat16* pub_bf16;         // theta_local_bf16 (+ the conv weight image at img_off)
   long long img_off;
   DevCounters* ctr;
+  int early;                       // 1: the non-conv part [kBwdPart, n) is updated by the conv backward's
+                                   //    extra CTAs (launch_bwd_conv_update); this launch does the conv part only
 };
 void launch_reduce_update(const ReduceUpdateArgs& u, cudaStream_t st);
+// N = 1, n_push = 1: the conv backward launch plus `upd_ctas` CTAs that apply the RMSProp update to the
+// non-conv parameters [kBwdPart, u.n) (FC, output layer: their gradients are complete when the conv
+// backward passes its PDL wait), off the step's critical path; u.early must be 1.
+void launch_bwd_conv_update(const BwdConvArgs& a, const ReduceUpdateArgs& u, int upd_ctas, cudaStream_t st);
 constexpr int kMnihSlot = 28224;
 constexpr int kA1Bytes = 8 * 144 * 16;
 constexpr int kBwdPart = 256 * 16 + 256 * 32 + 16 + 32;

@@ -160,6 +160,8 @@ struct dqn_ctx {
   int capture_variant = -1;  // >= 8 while capturing a profiling graph
   bool use_graphs = true;
   bool step_trace = false;  // DQN_TRACE_STEP=1
+  int num_sms = 148;
+  bool early_update = true; // N = 1 bf16: FC / output-layer RMSProp inside the conv backward launch (DQN_EARLY_UPDATE=0: off)
   bool keep_grad = false;
   bool alias_local = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -641,6 +643,12 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
       CK(cudaEventCreateWithFlags(&ctx->ev_stage[i], cudaEventDisableTiming));
     }
     CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_out), sizeof(dqn_ctx::HostOut), cudaHostAllocDefault));
+  }
+  if (const char* v = getenv("DQN_EARLY_UPDATE")) ctx->early_update = atoi(v) != 0;
+  {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+      ctx->num_sms = sms;
   }
   if (const char* v = getenv("DQN_TRACE_STEP")) {
     if (atoi(v)) {
@@ -1203,8 +1211,21 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   // N = 1, n_push = 1: the conv partials' reduction runs inside the update (reduce_update_kernel)
   const bool fuse_reduce = push && ctx->world == 1 && c.n_push == 1 && !ctx->keep_grad && ctx->alias_local &&
                            L1.w_off == 0 && L2.b_off + L2.N == kBwdPart;
+  ReduceUpdateArgs u{};
+  if (fuse_reduce) {
+    const float div = (float)((double)ctx->world * c.n_push);
+    u.b = ba;
+    u.theta = ctx->theta_master; u.r = ctx->rms; u.g = ctx->grad; u.n = ctx->P_pad;
+    u.inv_div = 1.0f / div; u.lr = (float)c.lr; u.rho = (float)c.rms_decay; u.omr = (float)(1.0 - c.rms_decay);
+    u.eps = (float)c.rms_eps;
+    u.pub_bf16 = ctx->theta_local_bf16; u.img_off = ctx->img_off; u.ctr = ctx->ctr;
+    u.early = ctx->early_update && b + 32 <= ctx->num_sms ? 1 : 0;  // needs SMs the conv CTAs leave free
+  }
   PB("conv_bwd", fuse_reduce ? 1 : 2);
-  launch_bwd_conv_bf16(ba, st, !fuse_reduce);
+  if (u.early)  // the non-conv update rides on the SMs the per-image conv CTAs leave free
+    launch_bwd_conv_update(ba, u, ctx->num_sms - b, st);
+  else
+    launch_bwd_conv_bf16(ba, st, !fuse_reduce);
   PE();
   if (ctx->keep_grad)
     CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
@@ -1227,11 +1248,6 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
       PE();
     } else if (fuse_reduce) {
       PB("reduce_update", 1);
-      ReduceUpdateArgs u{};
-      u.b = ba;
-      u.theta = ctx->theta_master; u.r = ctx->rms; u.g = ctx->grad; u.n = ctx->P_pad;
-      u.inv_div = 1.0f / div; u.lr = (float)c.lr; u.rho = rho; u.omr = omr; u.eps = (float)c.rms_eps;
-      u.pub_bf16 = ctx->theta_local_bf16; u.img_off = ctx->img_off; u.ctr = ctx->ctr;
       launch_reduce_update(u, st);
       PE();
     } else {

@@ -479,6 +479,9 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
       }
     }
   } else if (a.epi == TC_EPI_MASK_T) {
+    // output feature m of sample n goes to n*ldo + om (NHWC re-layout for the generic conv path)
+    const long long om = a.hwc_HW ? (long long)(m % a.hwc_HW) * a.hwc_C + m / a.hwc_HW : (long long)m;
+    __nv_bfloat16* const orow = a.out_bf16 + om;
     for (int c = 0; c < bn; c += 16) {
       float v[16];
       tmem_ld16(trow + c, v);
@@ -493,9 +496,8 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + c + i;
-          const long long om = a.hwc_HW ? (long long)(m % a.hwc_HW) * a.hwc_C + m / a.hwc_HW : (long long)m;
           if (n < a.N)  // bf16 > 0 <=> sign bit clear and not +0
-            a.out_bf16[(long long)n * a.ldo + om] = __float2bfloat16_rn((mk[i] & 0x8000u) == 0 && mk[i] != 0 ? v[i] : 0.0f);
+            orow[(long long)n * a.ldo] = __float2bfloat16_rn((mk[i] & 0x8000u) == 0 && mk[i] != 0 ? v[i] : 0.0f);
         }
       }
       if (ph && c < 48) st_stamp_here(ST_P6, c / 16);
@@ -506,9 +508,13 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
       float v[16];
       tmem_ld16(trow + c, v);
       if (m < a.M) {
+        float* prow = pbase + (long long)(n0 + c) * a.M + m;  // split stride is N*M
+        if (n0 + c + 16 <= a.N) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (n0 + c + i < a.N) pbase[(long long)(n0 + c + i) * a.M + m] = v[i];  // split stride is N*M
+          for (int i = 0; i < 16; ++i) prow[(long long)i * a.M] = v[i];
+        } else {
+          for (int i = 0; i < 16 && n0 + c + i < a.N; ++i) prow[(long long)i * a.M] = v[i];
+        }
       }
     }
   }
@@ -624,12 +630,18 @@ constexpr int BWD_SDZ1 = BWD_SDZ2 + 4 * DZ2_ALLOC * 16;                    // +9
 constexpr int BWD_SW2 = BWD_SDZ1 + 2 * BWD_ROWS1 * 16;                     // +13824
 constexpr int BWD_SMEM = BWD_SW2 + 4 * 4 * 64 * 16;                        // +16384 = 215552
 
-__global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a) {
+__device__ void rms_tail(const ReduceUpdateArgs& u, int cta, int ctas);
+
+__global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, ReduceUpdateArgs u) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   __shared__ float s_db1[16], s_db2[32];
   const int j = blockIdx.x;
+  if (j >= a.n) {  // early-update CTAs (u.early): RMSProp of the non-conv parameters, off the critical path
+    rms_tail(u, j - a.n, gridDim.x - a.n);
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   st_stamp(ST_CONV_BWD, 0);
   uint8_t* sX = smem + BWD_SX;
@@ -910,7 +922,7 @@ __global__ void bwd_reduce_kernel(BwdConvArgs a) {
 }
 
 void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st, bool with_reduce) {
-  launch_pdl(bwd_conv_bf16_kernel, dim3(a.n), dim3(128), BWD_SMEM, st, a);
+  launch_pdl(bwd_conv_bf16_kernel, dim3(a.n), dim3(128), BWD_SMEM, st, a, ReduceUpdateArgs{});
   if (with_reduce) launch_pdl(bwd_reduce_kernel, dim3(cdiv(BWD_PART, 128)), dim3(128), 0, st, a);
 }
 
@@ -919,13 +931,58 @@ void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st, bool with_reduc
 // conv parameters are the canonical prefix [0, BWD_PART) of theta); the rest own a float4 of the
 // remaining parameters and read G as rmsprop_kernel does. Same arithmetic per element as
 // rmsprop_kernel (A4, A5, A24).
+// Rounding pinned with explicit intrinsics (no context-dependent FMA contraction), so the update is
+// bit-identical whichever launch applies it (reduce_update_kernel or the conv backward's extra CTAs).
 __device__ __forceinline__ bool rms_elem(float& th, float& r, float g, const ReduceUpdateArgs& u) {
-  const float gb = g * u.inv_div;
+  const float gb = __fmul_rn(g, u.inv_div);
   if (!isfinite(gb)) return false;
-  const float rr = u.rho * r + u.omr * gb * gb;
+  const float rr = __fmaf_rn(u.rho, r, __fmul_rn(__fmul_rn(u.omr, gb), gb));
   r = rr;
-  th = th - u.lr * gb * rsqrtf(rr + u.eps);
+  th = __fmaf_rn(-__fmul_rn(u.lr, gb), rsqrtf(__fadd_rn(rr, u.eps)), th);
   return true;
+}
+
+// RMSProp of the float4 i of theta (non-conv part): G read then cleared, theta / r / bf16 published.
+// Split into the loads and the rest so that callers can keep several float4s' loads in flight.
+struct Rms4 { float4 g, t, r; };
+__device__ __forceinline__ Rms4 rms_load4(const ReduceUpdateArgs& u, long long i) {
+  return Rms4{reinterpret_cast<const float4*>(u.g)[i], reinterpret_cast<const float4*>(u.theta)[i],
+              reinterpret_cast<const float4*>(u.r)[i]};
+}
+__device__ __forceinline__ unsigned rms_apply4(const ReduceUpdateArgs& u, long long i, const Rms4& x) {
+  unsigned bad = 0;
+  reinterpret_cast<float4*>(u.g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float tv[4] = {x.t.x, x.t.y, x.t.z, x.t.w}, rv[4] = {x.r.x, x.r.y, x.r.z, x.r.w};
+  const float gv[4] = {x.g.x, x.g.y, x.g.z, x.g.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (!rms_elem(tv[q], rv[q], gv[q], u)) ++bad;
+  reinterpret_cast<float4*>(u.theta)[i] = make_float4(tv[0], tv[1], tv[2], tv[3]);
+  reinterpret_cast<float4*>(u.r)[i] = make_float4(rv[0], rv[1], rv[2], rv[3]);
+  uint2 o;
+  o.x = pack_bf16(tv[0], tv[1]);
+  o.y = pack_bf16(tv[2], tv[3]);
+  reinterpret_cast<uint2*>(u.pub_bf16)[i] = o;
+  return bad;
+}
+
+// non-conv float4 range of the update, grid-strided over the conv backward's extra CTAs (u.early);
+// RMS_BATCH float4s per thread with all their loads issued first
+constexpr int RMS_BATCH = 6;
+__device__ void rms_tail(const ReduceUpdateArgs& u, int cta, int ctas) {
+  pdl_sync();  // the FC / output-layer gradients come from the predecessor (FC backward + head finish)
+  unsigned bad = 0;
+  const long long n4 = u.n / 4, stride = (long long)ctas * 128;
+  for (long long i0 = BWD_PART / 4 + (long long)cta * 128 + threadIdx.x; i0 < n4; i0 += stride * RMS_BATCH) {
+    Rms4 x[RMS_BATCH];
+#pragma unroll
+    for (int k = 0; k < RMS_BATCH; ++k)
+      if (i0 + k * stride < n4) x[k] = rms_load4(u, i0 + k * stride);
+#pragma unroll
+    for (int k = 0; k < RMS_BATCH; ++k)
+      if (i0 + k * stride < n4) bad += rms_apply4(u, i0 + k * stride, x[k]);
+  }
+  if (bad) atomicAdd(&u.ctr->nonfinite, bad);
 }
 
 __global__ void __launch_bounds__(256) reduce_update_kernel(ReduceUpdateArgs u) {
@@ -951,31 +1008,20 @@ __global__ void __launch_bounds__(256) reduce_update_kernel(ReduceUpdateArgs u) 
     if (sl >= 0) u.pub_bf16[u.img_off + sl] = hb;
   } else {
     const long long i = BWD_PART / 4 + (t - BWD_PART);
-    if (i >= u.n / 4) return;
-    const float4 g4 = reinterpret_cast<const float4*>(u.g)[i];
-    float4 t4 = reinterpret_cast<const float4*>(u.theta)[i];
-    float4 r4 = reinterpret_cast<const float4*>(u.r)[i];
-    reinterpret_cast<float4*>(u.g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    float tv[4] = {t4.x, t4.y, t4.z, t4.w}, rv[4] = {r4.x, r4.y, r4.z, r4.w};
-    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (!rms_elem(tv[q], rv[q], gv[q], u)) ++bad;
-    t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);
-    reinterpret_cast<float4*>(u.theta)[i] = t4;
-    reinterpret_cast<float4*>(u.r)[i] = make_float4(rv[0], rv[1], rv[2], rv[3]);
-    uint2 o;
-    o.x = pack_bf16(t4.x, t4.y);
-    o.y = pack_bf16(t4.z, t4.w);
-    reinterpret_cast<uint2*>(u.pub_bf16)[i] = o;
+    if (u.early || i >= u.n / 4) return;  // early: the conv backward's extra CTAs own this part
+    bad += rms_apply4(u, i, rms_load4(u, i));
   }
   if (bad) atomicAdd(&u.ctr->nonfinite, bad);
   st_stamp(ST_UPDATE, 2);
 }
 
 void launch_reduce_update(const ReduceUpdateArgs& u, cudaStream_t st) {
-  const long long threads = BWD_PART + (u.n / 4 - BWD_PART / 4);
+  const long long threads = BWD_PART + (u.early ? 0 : u.n / 4 - BWD_PART / 4);
   launch_pdl(reduce_update_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, u);
+}
+
+void launch_bwd_conv_update(const BwdConvArgs& a, const ReduceUpdateArgs& u, int upd_ctas, cudaStream_t st) {
+  launch_pdl(bwd_conv_bf16_kernel, dim3(a.n + upd_ctas), dim3(128), BWD_SMEM, st, a, u);
 }
 
 void init_bf16_kernel_attrs() {

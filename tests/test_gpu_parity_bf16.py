@@ -137,13 +137,17 @@ def test_bf16_run_to_run_bit_identical():
 def test_fused_reduce_update_path():
     """N = 1 without DQN_KEEP_GRAD: the conv partials' reduction runs inside the update kernel
     (reduce_update_kernel). Its theta after 5 steps must follow the oracle like the two-kernel path
-    (smooth regime, 2e-2) and agree with that path to fp32 rounding."""
+    (smooth regime, 2e-2) and agree with that path to fp32 rounding. By default the FC / output-layer
+    part of that update runs in extra CTAs of the conv backward launch (DQN_EARLY_UPDATE); with it off
+    the same per-element arithmetic runs in reduce_update_kernel, so the two runs are bit-identical."""
     dc, on, oc = nets(minibatch=32, replay_capacity=1000, precision=D.BF16, lr=1e-5)
     theta0 = smooth_theta(on, 7)
     res = {}
-    for keep in ("1", None):
-        if keep is None:
+    for keep in ("1", None, "late"):
+        if keep != "1":
             os.environ.pop("DQN_KEEP_GRAD", None)
+        if keep == "late":
+            os.environ["DQN_EARLY_UPDATE"] = "0"
         try:
             g, rp, _ = make(dc, on, theta0, 1000, 77)
             g.train(5)
@@ -151,6 +155,8 @@ def test_fused_reduce_update_path():
             g.close()
         finally:
             os.environ["DQN_KEEP_GRAD"] = "1"
+            os.environ.pop("DQN_EARLY_UPDATE", None)
+    assert np.array_equal(res[None][0], res["late"][0]) and np.array_equal(res[None][1], res["late"][1])
     ref = O.run(on, oc, 1000, [rp], theta0.astype(np.float64), 5)
     th0 = theta0.astype(np.float64)
     for keep in ("1", None):
