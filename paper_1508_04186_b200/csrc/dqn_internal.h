@@ -168,6 +168,11 @@ struct ServerRoundArgs {
   float inv_np;                                 // 1 / n_push (per-gradient rule)
   DevCounters* ctr;
   unsigned long long* trace;                    // optional [64][8] globaltimer stamps (DQN_TRACE_COMM=1)
+  // conv-first delivery (bf16 Mnih path): the blocks holding the conv parameters (the canonical prefix,
+  // conv4 float4s of this rank's shard; 0: none) release them early through a second counter
+  long long conv4;
+  unsigned long long* done_c[kMaxWorld];        // every rank's conv-release counter
+  unsigned long long* my_join_c;                // local join counter of the conv blocks
 };
 void launch_server_round(const ServerRoundArgs& a, cudaStream_t st);
 // the acquire half of the round's second barrier, run at the start of the next step
@@ -178,6 +183,12 @@ struct FusedAcquire {
   long long grad_elems;
   DevCounters* ctr;                             // nullptr: no fused round in this context
   unsigned long long* trace;                    // the server round's trace (slots 6, 7) or nullptr
+  // conv-first delivery: the next step's conv forward waits only for the conv parameters (done_c >=
+  // rounds * n_c, n_c = ranks owning conv parameters) instead of the round's grid completion, and the
+  // FC forward acquires the whole round (done) and clears G
+  const unsigned long long* done_c;
+  int n_c;
+  int conv_first;
 };
 void launch_fused_round_acquire(const FusedAcquire& f, cudaStream_t st);
 int server_round_blocks(long long shard);
@@ -225,6 +236,7 @@ struct TcGemmArgs {
   int st_ph;                // DQN_TRACE_STEP phase slot of tile 0 (staged / MMA done), 0 = none
   int store;                // TC_EPI_ACCUM: 1 = C = D (C known to be zero / overwritten), 0 = C += D
   int hwc_HW, hwc_C;        // TC_EPI_MASK_T: write feature m = c*HW + p to p*C + c (NHWC dZ), 0: off
+  FusedAcquire acq;         // conv-first delivery (acq.conv_first): the FC forward acquires the round
 };
 enum { TC_EPI_ACCUM = 0, TC_EPI_FC_FWD = 1, TC_EPI_MASK_T = 2 };
 struct BwdConvArgs {

@@ -444,8 +444,9 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   const int N = ctx->world, me = ctx->rank;
   int rc;
   if ((rc = dalloc(ctx, &ctx->flags, kMaxWorld))) return rc;
-  // done[0]: barrier-B counter (peers add to it), done[1]: the local blocks' join counter
-  const long long n_done = 2;
+  // done[0]: barrier-B counter (peers add to it), done[1]: the local blocks' join counter,
+  // done[2]: conv-release counter (peers add to it), done[3]: the local conv blocks' join counter
+  const long long n_done = 4;
   if ((rc = dalloc(ctx, &ctx->done, n_done))) return rc;
   CK(cudaMemset(ctx->flags, 0, sizeof(unsigned long long) * kMaxWorld));
   CK(cudaMemset(ctx->done, 0, sizeof(unsigned long long) * n_done));
@@ -505,6 +506,18 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   ctx->acq.grad = ctx->grad;
   ctx->acq.grad_elems = ctx->P_pad;
   ctx->acq.ctr = ctx->ctr;
+  // conv-first delivery (bf16 Mnih path, conv parameters = the canonical prefix [0, kBwdPart))
+  const char* cf = getenv("DQN_CONV_FIRST");
+  const bool mnih_bf16 = ctx->bf16 && !ctx->gpath && ctx->img_off >= 0 && ctx->w1_off == 0 &&
+                         ctx->net.conv[1].b_off + ctx->net.conv[1].N == kBwdPart;
+  if (mnih_bf16 && !(cf && atoi(cf) == 0)) {
+    for (int p = 0; p < N; ++p) a.done_c[p] = a.done[p] + 2;
+    a.my_join_c = ctx->done + 3;
+    a.conv4 = std::min(ctx->shard / 4, std::max(0LL, ((long long)kBwdPart - (long long)me * ctx->shard) / 4));
+    ctx->acq.done_c = ctx->done + 2;
+    ctx->acq.n_c = (int)std::min<long long>(N, (kBwdPart + ctx->shard - 1) / ctx->shard);
+    ctx->acq.conv_first = 1;
+  }
   const char* tr = getenv("DQN_TRACE_COMM");
   if (tr && atoi(tr)) {
     if ((rc = dalloc(ctx, &a.trace, 64 * 16))) return rc;
@@ -1160,6 +1173,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial; gf.counters = ctx->tc_counters;
   gf.pre_a = 1; gf.pre_b = 0;  // W from the previous step's update; a2 from the predecessor
   gf.bias[0] = ctx->theta_local + F.b_off; gf.bias[1] = ctx->theta_hat + F.b_off;
+  if (ctx->acq.conv_first) gf.acq = ctx->acq;  // the previous round's FC deliveries, G cleared
   // (h_out left null: the TD head reduces the split-K partials, adds the bias and applies ReLU)
   PB("fc1_fwd", 1);
   launch_tc_gemm(gf, 2, st);

@@ -50,9 +50,23 @@ __device__ __forceinline__ void fused_round_acquire(const FusedAcquire& f) {
   }
   __syncthreads();
   const long long g4 = f.grad_elems / 4;
-  const long long blk = blockIdx.y * (long long)gridDim.x + blockIdx.x, nblk = (long long)gridDim.x * gridDim.y;
+  const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  const long long nblk = (long long)gridDim.x * gridDim.y * gridDim.z;
   for (long long i = blk * blockDim.x + threadIdx.x; i < g4; i += nblk * blockDim.x)
     reinterpret_cast<float4*>(f.grad)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// conv-first delivery: true if the previous step ran a server round (then the caller must not rely
+// on griddepcontrol.wait for it); waits until every owner of conv parameters released them
+// (done_c >= rounds * n_c). Thread 0 polls; the block synchronises.
+__device__ __forceinline__ bool fused_round_acquire_conv(const FusedAcquire& f) {
+  if (f.ctr == nullptr || !f.conv_first) return false;
+  const unsigned long long T = f.ctr->T;
+  if (T == 0 || T % (unsigned long long)f.n_push != 0) return false;
+  const unsigned long long rounds = T / (unsigned long long)f.n_push;
+  if (threadIdx.x == 0) spin_acquire_sys(f.done_c, rounds * (unsigned long long)f.n_c, f.ctr);
+  __syncthreads();
+  return true;
 }
 
 }  // namespace dqn

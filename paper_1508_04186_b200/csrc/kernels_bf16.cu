@@ -172,10 +172,17 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[9]));
   expand_state(sX, sU8);  // u8 -> exact bf16 (1/255 folded into the epilogue)
   // everything above overlaps the previous kernel (the update that publishes theta); weights after the wait
-  pdl_wait();
-  st_stamp(ST_FWD, 1);
-  if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[10]));
-  fused_round_acquire(a.acq);  // N > 1 fused server round: peers' deliveries into theta_local complete
+  if (fused_round_acquire_conv(a.acq)) {
+    // conv-first delivery: the previous step's server round released the conv parameters early; no
+    // griddepcontrol.wait on the round's grid (its FC deliveries are acquired by the FC forward)
+    st_stamp(ST_FWD, 1);
+    if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[10]));
+  } else {
+    pdl_wait();
+    st_stamp(ST_FWD, 1);
+    if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[10]));
+    fused_round_acquire(a.acq);  // N > 1 fused server round: peers' deliveries into theta_local complete
+  }
   pdl_trigger();               // only now: the FC forward reads the delivered weights before its wait
   // conv1 + conv2 B operands: the weight image the update wrote after the canonical entries
   // (wimg.cuh), contiguous with sW1 | sW2 in shared memory: 1,536 16-byte async copies
@@ -347,6 +354,9 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(&tbase, 256);
+  // conv-first delivery (FC forward after a server round): the round's FC deliveries complete and every
+  // peer done reading this rank's G, which is cleared here (before the W staging below)
+  if (a.acq.ctr && a.acq.conv_first) fused_round_acquire(a.acq);
   // ---- stage A (128 rows x KC) and B (BN rows x KC), 16-byte vectors
   const __nv_bfloat16* Ag = a.A[g];
   const __nv_bfloat16* Bg = a.B[g];

@@ -145,6 +145,19 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   // gpu-scope release into the join counter; the last block releases once at system scope
   __syncthreads();
   TRACE(2);
+  // conv-first delivery: the blocks holding conv parameters (the first nb_c blocks of the owner(s) of
+  // the canonical prefix) first join their own counter; the last of them releases the conv weights to
+  // every peer (done_c), so the next step's conv forward can start before this round ends
+  const unsigned long long nb_c = (unsigned long long)((a.conv4 + blockDim.x - 1) / blockDim.x);
+  if (threadIdx.x == 0 && blockIdx.x < nb_c) {
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(a.my_join_c), "l"(1ull) : "memory");
+    if (old == round_idx * nb_c - 1) {
+      fence_acq_rel_sys();
+      for (int p = 0; p < a.world; ++p)
+        asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(a.done_c[p]), "l"(1ull) : "memory");
+    }
+  }
   if (threadIdx.x == 0) {
     unsigned long long old;
     asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(a.my_join), "l"(1ull) : "memory");

@@ -21,12 +21,13 @@ def n_gpus():
     return torch.cuda.device_count()
 
 
-def run_ranks(world, tmp_path, *extra):
-    out = str(tmp_path / "mp.npz")
+def run_ranks(world, tmp_path, *extra, env=None, tag="mp"):
+    out = str(tmp_path / f"{tag}.npz")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tools", "mp_parity.py"),
            "--out", out, *extra]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
 
