@@ -242,6 +242,7 @@ def main():
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="BASELINE.json config (default: c2 at N = 1, c3 at N > 1)")
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--e2e-chunk", type=int, default=50, help="Alg. 1 iterations per dqn_store_and_train call (e2e)")
     ap.add_argument("--profile-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-acting", dest="acting", action="store_false",
@@ -342,27 +343,54 @@ def main():
     ha = torch.zeros(ne, dtype=torch.int32).pin_memory()
     hr = torch.zeros(ne, dtype=torch.float32).pin_memory()
     ht = torch.zeros(ne, dtype=torch.uint8).pin_memory()
-    for i in range(min(3, ne)):  # untimed warm-up of the host-push path
+    for i in range(min(3, ne)):  # untimed warm-up of both host-push paths
         dqn.push(hs[i:i + 1], ha[i:i + 1], hr[i:i + 1], hsn[i:i + 1], ht[i:i + 1])
         dqn.train(1, want_loss=True)
-    barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(ne):
-        dqn.push(hs[i:i + 1], ha[i:i + 1], hr[i:i + 1], hsn[i:i + 1], ht[i:i + 1])
-        dqn.train(1, want_loss=True)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ems = e0.elapsed_time(e1)
-    if dist is not None:
-        tt = torch.tensor([ems], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ems = float(tt.item())
-    e2e = {"value": world * b * ne / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * 4 * 84 * 84 + 4 + 4 + 1,
-           "d2h_bytes_per_step": 4 + 48, "steps": ne,
-           "what": "per step: dqn_push_transitions of 1 new experience from pinned host memory + "
-                   "dqn_train_steps(1) + loss/counters D2H"}
+        if not C["async"]:
+            dqn.train(1, want_loss=True, store=(hs[i:i + 1], ha[i:i + 1], hr[i:i + 1], hsn[i:i + 1], ht[i:i + 1]))
+
+    def timed(fn):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        if dist is not None:
+            tt = torch.tensor([t], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    # (1) Alg. 1's loop through dqn_store_and_train, `chunk` iterations per call: every iteration stores
+    # its new experience (H2D from pinned host memory) and runs one step; every step's loss comes back
+    ch = max(1, args.e2e_chunk)
+
+    def loop_store_and_train():
+        for i0 in range(0, ne, ch):
+            m = min(ch, ne - i0)
+            sl = slice(i0, i0 + m)
+            dqn.train(m, want_loss=True, store=(hs[sl], ha[sl], hr[sl], hsn[sl], ht[sl]))
+
+    # (2) one push call and one train call (with its host sync) per step
+    def loop_sync_per_step():
+        for i in range(ne):
+            dqn.push(hs[i:i + 1], ha[i:i + 1], hr[i:i + 1], hsn[i:i + 1], ht[i:i + 1])
+            dqn.train(1, want_loss=True)
+
+    ems1 = timed(loop_sync_per_step)
+    ems = ems1 if C["async"] else timed(loop_store_and_train)  # store_and_train is the deterministic schedule's
+    h2d = 2 * 4 * 84 * 84 + 4 + 4 + 1
+    e2e = {"value": world * b * ne / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": 4 + 48 / ch, "steps": ne,
+           "what": (f"Alg. 1 loop through dqn_store_and_train, {ch} iterations per call: per step the new experience "
+                    "H2D from pinned host memory, its Store, one replica step, its loss D2H; one host sync per call")
+           if not C["async"] else "DQN_ASYNC: as sync_per_step (dqn_store_and_train needs the deterministic schedule)",
+           "sync_per_step": {"value": world * b * ne / (ems1 / 1e3), "d2h_bytes_per_step": 4 + 48,
+                             "what": "per step: dqn_push_transitions(1, pinned host) + dqn_train_steps(1) "
+                                     "(host sync) + loss/counters D2H"}}
 
     # ---- NEXT-3 acting: on-GPU Snake games, eps-greedy on Q from the forward, Store into the replay
     acting = None

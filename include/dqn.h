@@ -166,6 +166,18 @@ int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_
  * DQN_ENONFINITE if any round so far produced a non-finite mean gradient. */
 int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats);
 
+/* Alg. 1's loop for k iterations, in one call (collective: every rank
+ * passes the same k): iteration i stores transition i ("Store experience ... in D",
+ * P:117; arguments and layout as dqn_push_transitions, k items) and then runs one
+ * replica step exactly as dqn_train_steps(1) (sample from D including that item,
+ * gradient, the server round it triggers). Equivalent to k alternating calls
+ * dqn_push_transitions(1 item) + dqn_train_steps(1), with one host synchronisation
+ * at the end instead of one per iteration. stats as dqn_train_steps (loss_per_step
+ * receives the k losses). Errors: as dqn_push_transitions (validated before anything
+ * runs) and dqn_train_steps; DQN_EINVAL in DQN_ASYNC mode. */
+int dqn_store_and_train(dqn_ctx* ctx, int64_t k, const uint8_t* s, const int32_t* a, const float* r,
+                        const uint8_t* s_next, const uint8_t* terminal, dqn_step_stats* stats);
+
 /* Diagnostic twin of dqn_train_steps (collective, same semantics: it advances the
  * run by k real steps): the step graphs are captured with CUDA event records
  * around every region, each step is replayed and synchronised, and the mean

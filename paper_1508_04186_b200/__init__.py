@@ -130,6 +130,7 @@ def lib() -> C.CDLL:
         L.dqn_create.argtypes = [C.POINTER(_Config), C.c_int, C.c_int, P, P, C.POINTER(P)]
         L.dqn_push_transitions.argtypes = [P, C.c_int64, P, P, P, P, P]
         L.dqn_train_steps.argtypes = [P, C.c_int64, C.POINTER(_Stats)]
+        L.dqn_store_and_train.argtypes = [P, C.c_int64, P, P, P, P, P, C.POINTER(_Stats)]
         L.dqn_q_values.argtypes = [P, C.c_int64, P, P, P]
         L.dqn_profile_steps.argtypes = [P, C.c_int64, C.POINTER(_RegionTime), C.c_int32, C.POINTER(C.c_int32)]
         L.dqn_get_params.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
@@ -145,7 +146,7 @@ def lib() -> C.CDLL:
 
 EXPORTED = ("dqn_param_count", "dqn_nccl_id_bytes", "dqn_nccl_unique_id", "dqn_create", "dqn_push_transitions",
             "dqn_train_steps", "dqn_profile_steps", "dqn_q_values", "dqn_get_params", "dqn_replay_size", "dqn_last_error",
-            "dqn_destroy", "dqn_collect", "dqn_env_stacks")
+            "dqn_destroy", "dqn_collect", "dqn_env_stacks", "dqn_store_and_train")
 
 
 def param_count(cfg: Config) -> int:
@@ -210,7 +211,10 @@ class DQN:
         pt, k5 = _ptr(term, np.uint8)
         self._check(lib().dqn_push_transitions(self._h, n, ps, pa, pr, pn, pt))
 
-    def train(self, k: int, want_idx: bool = False, want_argmax: bool = False, want_loss: bool = False) -> dict:
+    def train(self, k: int, want_idx: bool = False, want_argmax: bool = False, want_loss: bool = False,
+              store=None) -> dict:
+        """k replica steps (dqn_train_steps); with store = (s, a, r, s_next, term) of k transitions, Alg. 1's
+        loop instead: transition i is stored, then step i runs (dqn_store_and_train)."""
         st = _Stats()
         b = self.cfg.minibatch
         idx = np.zeros((k, b), np.int32) if want_idx else None
@@ -219,7 +223,18 @@ class DQN:
         st.sampled_idx = idx.ctypes.data if idx is not None else None
         st.target_argmax = am.ctypes.data if am is not None else None
         st.loss_per_step = lp.ctypes.data if lp is not None else None
-        rc = lib().dqn_train_steps(self._h, k, C.byref(st))
+        if store is None:
+            rc = lib().dqn_train_steps(self._h, k, C.byref(st))
+        else:
+            s_, a_, r_, sn_, t_ = store
+            if len(a_) != k:
+                raise ValueError("store needs exactly k transitions")
+            ps, k1 = _ptr(s_, np.uint8)
+            pa, k2 = _ptr(a_, np.int32)
+            pr, k3 = _ptr(r_, np.float32)
+            pn, k4 = _ptr(sn_, np.uint8)
+            pt, k5 = _ptr(t_, np.uint8)
+            rc = lib().dqn_store_and_train(self._h, k, ps, pa, pr, pn, pt, C.byref(st))
         out = dict(loss_mean=st.loss_mean, generation=st.generation, steps_done=st.steps_done,
                    device_ms=st.device_ms, nonfinite_elems=st.nonfinite_elems, idx=idx, argmax=am, loss=lp,
                    kernel_launches=st.kernel_launches, staleness=np.array(st.staleness_hist[:], np.int64), rc=rc)

@@ -868,8 +868,13 @@ static void push_ring(dqn_ctx* ctx, long long i0, long long m, const uint8_t* s,
 }
 
 
-extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a, const float* r,
-                                    const uint8_t* s_next, const uint8_t* terminal) {
+static int run_steps_chunked(dqn_ctx* ctx, long long k, long long* kernels);
+
+// Alg. 1 "Store" of n items (host or device buffers). With `steps` != nullptr (dqn_store_and_train) every
+// item is stored and then one replica step runs (Alg. 1's loop): push_ring(item i) followed by
+// the one-step graph, no host synchronisation; *steps counts the kernels launched.
+static int push_impl(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a, const float* r,
+                     const uint8_t* s_next, const uint8_t* terminal, long long* steps) {
   if (!ctx) return DQN_EINVAL;
   if (ctx->poisoned) return DQN_ESTATE;
   if (n < 0 || (n > 0 && (!s || !a || !r || !s_next || !terminal))) return set_err(ctx, DQN_EINVAL, "bad push args");
@@ -879,8 +884,28 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
   if (dev != is_device_ptr(a) || dev != is_device_ptr(r) || dev != is_device_ptr(s_next) ||
       dev != is_device_ptr(terminal))
     return set_err(ctx, DQN_EINVAL, "push buffers must all be host or all be device memory");
-  // only the last min(n, cap) items survive; item i goes to slot (count + i) mod cap
-  const long long first = n > ctx->cap ? n - ctx->cap : 0;
+  // only the last min(n, cap) items survive; item i goes to slot (count + i) mod cap (interleaved with
+  // steps, every item is sampled from before it is overwritten, so all are stored)
+  const long long first = n > ctx->cap && !steps ? n - ctx->cap : 0;
+  // push items [i0, i0 + m) (device pointers to item i0), then, interleaved, one step after each item
+  auto store = [&](long long i0, long long m, const uint8_t* ds, const int32_t* da, const float* dr, const uint8_t* dsn,
+                   const uint8_t* dt) -> int {
+    if (!steps) {
+      push_ring(ctx, i0, m, ds, da, dr, dsn, dt);
+      CK(cudaGetLastError());
+      return DQN_OK;
+    }
+    for (long long j = 0; j < m; ++j) {
+      push_ring(ctx, i0 + j, 1, ds + j * sb, da + j, dr + j, dsn + j * sb, dt + j);
+      CK(cudaGetLastError());
+      const long long c0 = ctx->count;
+      ctx->count = c0 + i0 + j + 1;  // the step sees the item (EEMPTY checks, graph planning)
+      const int rc = run_steps_chunked(ctx, 1, steps);
+      ctx->count = c0;
+      if (rc) return rc;
+    }
+    return DQN_OK;
+  };
   if (!dev) {
     for (long long i = 0; i < n; ++i)
       if (a[i] < 0 || a[i] >= ctx->net.A || !std::isfinite(r[i]))
@@ -907,9 +932,9 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
       CK(cudaMemcpyAsync(ctx->d_stage, h, o_t + m, cudaMemcpyHostToDevice, ctx->stream));
       CK(cudaEventRecord(ctx->ev_stage[buf], ctx->stream));
       uint8_t* d = ctx->d_stage;
-      push_ring(ctx, i0, m, d, reinterpret_cast<const int32_t*>(d + o_a), reinterpret_cast<const float*>(d + o_r),
-                d + o_sn, d + o_t);
-      CK(cudaGetLastError());
+      int rc = store(i0, m, d, reinterpret_cast<const int32_t*>(d + o_a), reinterpret_cast<const float*>(d + o_r),
+                     d + o_sn, d + o_t);
+      if (rc) return rc;
     }
     ctx->count += n;  // enqueued: the sampler of any later step reads the published size in stream order
     return DQN_OK;
@@ -924,14 +949,20 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
                                                "shifted by one frame in device push");
     for (long long i0 = first; i0 < n; i0 += 65535) {
       const long long m = std::min<long long>(65535, n - i0);
-      push_ring(ctx, i0, m, s + i0 * sb, a + i0, r + i0, s_next + i0 * sb, terminal + i0);
-      CK(cudaGetLastError());
+      int rc = store(i0, m, s + i0 * sb, a + i0, r + i0, s_next + i0 * sb, terminal + i0);
+      if (rc) return rc;
     }
   }
   ctx->count += n;
-  CK(cudaStreamSynchronize(ctx->stream));  // device inputs: read by the ring kernel before returning
+  if (!steps) CK(cudaStreamSynchronize(ctx->stream));  // device inputs: read by the ring kernel before returning
   return DQN_OK;
 }
+
+extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a, const float* r,
+                                    const uint8_t* s_next, const uint8_t* terminal) {
+  return push_impl(ctx, n, s, a, r, s_next, terminal, nullptr);
+}
+
 
 // ------------------------------------------------------------------ profiling marks
 static void prof_begin(dqn_ctx* ctx, const std::string& name, int kernels) {
@@ -1675,12 +1706,13 @@ extern "C" int dqn_profile_steps(dqn_ctx* ctx, int64_t k, dqn_region_time* out, 
   return DQN_OK;
 }
 
+static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kernels, dqn_step_stats* stats);
+
 extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
   if (!ctx) return DQN_EINVAL;
   if (ctx->poisoned) return DQN_ESTATE;
   if (k < 0) return set_err(ctx, DQN_EINVAL, "k must be >= 0");
   if (ctx->count == 0) return set_err(ctx, DQN_EEMPTY, "replay memory is empty (A13)");
-  const dqn_config& c = ctx->cfg;
   const long long T0 = ctx->T;
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   long long kernels = 0;
@@ -1694,6 +1726,29 @@ extern "C" int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats) {
       if (rc) return rc;
     }
   }
+  return finish_steps(ctx, T0, k, kernels, stats);
+}
+
+extern "C" int dqn_store_and_train(dqn_ctx* ctx, int64_t k, const uint8_t* s, const int32_t* a, const float* r,
+                                   const uint8_t* s_next, const uint8_t* terminal, dqn_step_stats* stats) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  if (k < 0) return set_err(ctx, DQN_EINVAL, "k must be >= 0");
+  if (!ctx->use_graphs || ctx->async)
+    return set_err(ctx, DQN_EINVAL, "dqn_store_and_train needs the deterministic graph-replayed schedule");
+  if (k == 0) return DQN_OK;
+  const long long T0 = ctx->T;
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  long long kernels = 0;
+  int rc = push_impl(ctx, k, s, a, r, s_next, terminal, &kernels);
+  if (rc) return rc;
+  return finish_steps(ctx, T0, k, kernels, stats);
+}
+
+// the end of a train call: counters, losses and diagnostics to pinned memory, ONE stream
+// synchronisation, device-side error checks, stats
+static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kernels, dqn_step_stats* stats) {
+  const dqn_config& c = ctx->cfg;
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   dqn_ctx::HostOut* ho = ctx->h_out;
   CK(cudaMemcpyAsync(&ho->ctr, ctx->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, ctx->stream));

@@ -913,10 +913,17 @@ __device__ __forceinline__ long long bwd_part_dst(int e, const BwdConvArgs& a) {
 
 // the sum over images of partial entry e, in image order (deterministic); conv1's dW carries the
 // 1/255 of the integer-valued input (d/dW of (W.u)/255)
+// (the loads of 32 images are issued together, then summed in image order: latency, not bandwidth, bound)
 __device__ __forceinline__ float bwd_part_sum(int e, const BwdConvArgs& a) {
   float s = 0.0f;
-#pragma unroll 8
-  for (int i = 0; i < a.n; ++i) s += a.partial[(long long)i * BWD_PART + e];
+  for (int i0 = 0; i0 < a.n; i0 += 32) {
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = i0 + k < a.n ? __ldcg(a.partial + (long long)(i0 + k) * BWD_PART + e) : 0.0f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (i0 + k < a.n) s += v[k];
+  }
   return e < BWD_PART_W1 ? s * (1.0f / 255.0f) : s;
 }
 
