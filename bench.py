@@ -97,6 +97,14 @@ REGION_KERNELS = {"conv_fwd": ["fwd_conv_bf16_kernel"], "fc1_fwd": ["tc_gemm_ker
                   "reduce_update": ["reduce_update_kernel"]}
 
 
+def conv_param_count(net=MNIH) -> int:
+    c, n_params = 4, 0
+    for (n, k, s) in net["convs"]:
+        n_params += n * (c * k * k + 1)
+        c = n
+    return n_params
+
+
 def region_traffic(name: str, dtype: str):
     """DRAM bytes (read + write) per launch of a region's kernels, from the committed `ncu --set full`
     capture of this round (profiles/r1_traffic.json), or None when not captured."""
@@ -105,10 +113,8 @@ def region_traffic(name: str, dtype: str):
         return None
     with open(p) as f:
         t = json.load(f)
-    try:
-        return sum((t[k]["dram_read_MB"] + t[k]["dram_write_MB"]) * 1e6 for k in REGION_KERNELS[name])
-    except KeyError:
-        return None
+    ks = [k for k in REGION_KERNELS[name] if k in t]  # the kernels of the region that ran in the capture
+    return sum((t[k]["dram_read_MB"] + t[k]["dram_write_MB"]) * 1e6 for k in ks) if ks else None
 
 
 class ClockSampler:
@@ -247,6 +253,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-acting", dest="acting", action="store_false",
                     help="skip the on-GPU acting measurement (NEXT-3)")
+    ap.add_argument("--fc", type=int, default=None,
+                    help="override the hidden FC width of the config's net (model-size sweep, SURVEY §8(d) BJ.c5)")
     ap.add_argument("--dedup", action="store_true",
                     help="frame-deduplicated replay (F+1 frames per slot; G-pong stacks slide by one frame)")
     args = ap.parse_args()
@@ -284,7 +292,7 @@ def main():
         args.replay = C["replay"]
     prec = {"fp32": D.FP32, "bf16": D.BF16}.get(args.precision)
     b = C["b"]
-    net = C["net"]
+    net = C["net"] if args.fc is None else dict(C["net"], fcs=(args.fc,))
     cfg = None
     for p in ([prec] if prec is not None else [D.BF16, D.FP32]):
         cfg = D.Config(**net, minibatch=b, replay_capacity=args.replay, target_sync=C["C"], precision=p,
@@ -412,7 +420,19 @@ def main():
         step_us = sum(r["avg_us"] for r in regions if r["steps"] >= args.profile_steps // 2)
         top = max(regions, key=lambda r: r["avg_us"])
         flops, byts = region_work(top["name"], b, net)
-        if dtype == "bf16" and flops:
+        names = {r["name"] for r in regions}
+        # N = 1 bf16 Mnih path: the conv backward launch also runs the early RMSProp update of the non-conv
+        # parameters (26 B/param — read theta, r, G; write theta, r, G = 0, bf16 theta)
+        early = (top["name"] == "conv_bwd" and dtype == "bf16" and world == 1 and "reduce_update" in names
+                 and b + 32 <= 148 and os.environ.get("DQN_EARLY_UPDATE", "1") != "0")
+        if early:
+            byts += (region_work("rmsprop_update", b, net)[1] // 24 - conv_param_count(net)) * 26
+        if early and byts / (pk["hbm"] * 1e9) > flops / (pk["bf16_sus"] * 1e12):  # the binding roofline
+            roof = {"bound": "hbm", "achieved": byts / (top["avg_us"] * 1e-6) / 1e9, "peak": pk["hbm"],
+                    "unit": "GB/s", "algorithmic_bytes": byts, "algorithmic_flops": flops,
+                    "note": "conv backward + early update in one launch: its HBM time (bytes / peak) exceeds its "
+                            "tensor time (flops / peak), so HBM is the binding roofline"}
+        elif dtype == "bf16" and flops:
             roof = {"bound": "tensor", "achieved": flops / (top["avg_us"] * 1e-6) / 1e12, "peak": pk["bf16_sus"],
                     "unit": "TFLOP/s"}
         elif flops:
@@ -439,7 +459,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-        "config": {"workload": f"BASELINE.json configs[{C['idx']}]", "net": net_name(net), "minibatch_per_replica": b,
+        "config": {"workload": f"BASELINE.json configs[{C['idx']}]" + (f", FC width {args.fc} (model-size sweep)"
+                                                                      if args.fc is not None else ""),
+                   "net": net_name(net), "minibatch_per_replica": b,
                    "replay_per_replica": args.replay, "replay_dedup": bool(args.dedup),
                    "target_sync_C": C["C"] if C["C"] < 2**40 else None,
                    "n_push": C["n_push"], "n_fetch": C["n_fetch"],

@@ -313,6 +313,11 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
     if (mnih) {
       if (c->minibatch % 16 != 0 || c->minibatch > 256) { *why = "DQN_BF16 needs minibatch % 16 == 0 and <= 256"; return DQN_EINVAL; }
       if (c->fc_units[0] % 16 != 0 || c->fc_units[0] > 1024) { *why = "DQN_BF16 needs fc units % 16 == 0"; return DQN_EINVAL; }
+      // the FC dX GEMM (tc_pair) stages its whole K = fc units of W and dH in shared memory (200 KB budget)
+      if ((128LL + c->minibatch) * c->fc_units[0] * 2 > 200 * 1024) {
+        *why = "DQN_BF16 (Mnih stack): (128 + minibatch) * fc_units * 2 bytes must fit 200 KB (FC dX staging)";
+        return DQN_EINVAL;
+      }
       return DQN_OK;
     }
     // generic tensor-core conv path (kernels_conv.cu): every conv a stride-1 conv over a s2d grid

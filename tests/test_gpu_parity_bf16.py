@@ -59,9 +59,10 @@ def make(dc, on, theta0, n_items, seed):
     return g, rp, raw
 
 
-@pytest.mark.parametrize("b", [32, 256])
-def test_smooth_regime_gradient_and_q(b):
-    dc, on, oc = nets(minibatch=b, replay_capacity=1000, precision=D.BF16)
+@pytest.mark.parametrize("b,fc", [(32, 256), (256, 256), (32, 128), (32, 512)])
+def test_smooth_regime_gradient_and_q(b, fc):
+    """fc 128 / 512: the model-size sweep points (tools/model_sweep.sh) on the same kernels."""
+    dc, on, oc = nets(minibatch=b, replay_capacity=1000, precision=D.BF16, fcs=(fc,))
     theta0 = smooth_theta(on, 3)
     g, rp, raw = make(dc, on, theta0, 1000, 21)
     th = theta0.astype(np.float64)
@@ -165,3 +166,12 @@ def test_fused_reduce_update_path():
         assert per_tensor_rel(th, ref["theta"], on) < TOL
         assert rel_l2_per_tensor(th - th0, ref["theta"] - th0, on) < 0.1
     assert per_tensor_rel(res[None][0], res["1"][0], on) < 1e-5
+
+
+def test_fc_too_wide_for_the_dx_staging_is_rejected():
+    """(128 + b) * fc * 2 bytes must fit the FC dX GEMM's 200 KB shared-memory staging: DQN_EINVAL at create
+    (nothing is launched), not a failed launch inside the step graph."""
+    dc, _, _ = nets(minibatch=32, replay_capacity=100, precision=D.BF16, fcs=(1024,))
+    with pytest.raises(D.DqnError) as e:
+        D.DQN(dc)
+    assert e.value.code == D.EINVAL
