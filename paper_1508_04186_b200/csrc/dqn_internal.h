@@ -209,7 +209,35 @@ struct FwdConvArgs {
   FusedAcquire acq;                // NEXT-1: the previous round's deliveries (acq.done == nullptr: none)
   long long img_off;               // conv weight image (wimg.cuh) inside theta[g]
   long long slot_stride;           // bytes between replay slots (28,224, or 35,280 with frame dedup)
+  int late;                        // 1: sample + gather after the PDL wait (the predecessor wrote the ring)
 };
+// dqn_store_and_train on the bf16 Mnih path: Alg. 1's Store as the first kernel of every step of the
+// replayed step graph. The graph is fixed, so the chunk of transitions and its position come from here
+// (written by store_ctl_kernel before the chunk's graphs): step T stores item T - base of the chunk into
+// slot (count0 + T - base) mod capacity and publishes the replay size.
+struct StoreCtl {
+  const uint8_t* s;                // [m][F][H][W] canonical u8 (device staging or caller device memory)
+  const uint8_t* sn;
+  const int32_t* a;
+  const float* r;
+  const uint8_t* t;
+  long long base;                  // T of the chunk's first step
+  long long count0;                // pushes before the chunk's first item
+};
+struct StoreArgs {
+  uint8_t* ring_s;
+  uint8_t* ring_sn;
+  int32_t* ring_a;
+  float* ring_r;
+  uint8_t* ring_t;
+  long long cap, stride;
+  int dedup;
+  const StoreCtl* ctl;
+  DevCounters* ctr;
+};
+void launch_store_step(const StoreArgs& a, cudaStream_t st);
+void launch_store_ctl(StoreCtl* ctl, const uint8_t* s, const uint8_t* sn, const int32_t* a, const float* r,
+                      const uint8_t* t, long long base, long long count0, cudaStream_t st);
 struct TcGemmArgs {
   const __nv_bfloat16* A[2];
   long long lda;  // A(m,k) = a_mn ? A[k*lda + m] : A[m*lda + k]

@@ -144,11 +144,15 @@ struct dqn_ctx {
   // graphs per (fetch, refresh, push) variant; [8..15]: the same with profiling event records
   cudaGraphExec_t graphs[16] = {};
   long long graph_kernels[16] = {};
+  // dqn_store_and_train on the bf16 Mnih path: the Store runs inside the step graphs (variant bit 16)
+  StoreCtl* store_ctl = nullptr;
+  bool graph_store = false;
+  bool store_chunks_ready = false;
   // multi-step graphs: kChunkLog lengths 2^0..2^(kChunkLog-1) of consecutive same-variant steps,
   // so the programmatic (PDL) edges also span step boundaries (a graph boundary serialises)
   static constexpr int kChunkLog = 5;
-  cudaGraphExec_t chunk_graphs[8][kChunkLog] = {};
-  long long chunk_kernels[8][kChunkLog] = {};
+  cudaGraphExec_t chunk_graphs[32][kChunkLog] = {};
+  long long chunk_kernels[32][kChunkLog] = {};
   bool chunks_ready = false;
   // profiling (dqn_profile_steps): event pairs around each step region, per graph variant
   struct ProfMark {
@@ -380,7 +384,8 @@ static void free_all(dqn_ctx* c) {
                   c->theta_hat, c->grad_snap, c->gather_tmp, c->partial, c->idx, c->ctr, c->diag_loss,
                   c->diag_idx, c->diag_amax, c->head_dq, c->head_act, c->head_loss, c->q_stage, c->q_out, c->q_amax, c->d_stage,
                   c->theta_local_bf16, c->theta_hat_bf16, c->a2_bf16, c->a1_save,
-                  c->dh_bf16, c->dz2_bf16, c->fc_partial, c->tc_counters, c->bwd_partial, c->q_stage_s2d};
+                  c->dh_bf16, c->dz2_bf16, c->fc_partial, c->tc_counters, c->bwd_partial, c->q_stage_s2d,
+                  c->store_ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& G : c->gl) {
@@ -873,7 +878,7 @@ static void push_ring(dqn_ctx* ctx, long long i0, long long m, const uint8_t* s,
 }
 
 
-static int run_steps_chunked(dqn_ctx* ctx, long long k, long long* kernels);
+static int run_steps_chunked(dqn_ctx* ctx, long long k, long long* kernels, bool store = false);
 
 // Alg. 1 "Store" of n items (host or device buffers). With `steps` != nullptr (dqn_store_and_train) every
 // item is stored and then one replica step runs (Alg. 1's loop): push_ring(item i) followed by
@@ -900,6 +905,16 @@ static int push_impl(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a
       CK(cudaGetLastError());
       return DQN_OK;
     }
+    if (ctx->graph_store) {  // the Store runs as the first kernel of each step of the replayed graphs
+      launch_store_ctl(ctx->store_ctl, ds, dsn, da, dr, dt, ctx->T, ctx->count + i0, ctx->stream);
+      CK(cudaGetLastError());
+      *steps += 1;
+      const long long c0 = ctx->count;
+      ctx->count = c0 + i0 + m;
+      const int rc = run_steps_chunked(ctx, m, steps, true);
+      ctx->count = c0;
+      return rc;
+    }
     for (long long j = 0; j < m; ++j) {
       push_ring(ctx, i0 + j, 1, ds + j * sb, da + j, dr + j, dsn + j * sb, dt + j);
       CK(cudaGetLastError());
@@ -925,18 +940,28 @@ static int push_impl(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a
     for (long long i0 = first; i0 < n; i0 += ctx->push_chunk) {
       const long long m = std::min(ctx->push_chunk, n - i0);
       const long long o_sn = m * sb, o_a = align16(2 * m * sb), o_r = o_a + align16(4 * m), o_t = o_r + align16(4 * m);
-      const int buf = ctx->stage_flip;
-      ctx->stage_flip ^= 1;
-      CK(cudaEventSynchronize(ctx->ev_stage[buf]));  // its previous H2D copy has drained
-      uint8_t* h = ctx->h_stage[buf];
-      std::memcpy(h, s + i0 * sb, m * sb);
-      std::memcpy(h + o_sn, s_next + i0 * sb, m * sb);
-      std::memcpy(h + o_a, a + i0, m * sizeof(int32_t));
-      std::memcpy(h + o_r, r + i0, m * sizeof(float));
-      std::memcpy(h + o_t, terminal + i0, m);
-      CK(cudaMemcpyAsync(ctx->d_stage, h, o_t + m, cudaMemcpyHostToDevice, ctx->stream));
-      CK(cudaEventRecord(ctx->ev_stage[buf], ctx->stream));
       uint8_t* d = ctx->d_stage;
+      if (steps) {
+        // dqn_store_and_train synchronises before returning, so the copies may read the caller's buffers
+        // directly (DMA when they are pinned); no host-side packing
+        CK(cudaMemcpyAsync(d, s + i0 * sb, m * sb, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d + o_sn, s_next + i0 * sb, m * sb, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d + o_a, a + i0, m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d + o_r, r + i0, m * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d + o_t, terminal + i0, m, cudaMemcpyHostToDevice, ctx->stream));
+      } else {
+        const int buf = ctx->stage_flip;
+        ctx->stage_flip ^= 1;
+        CK(cudaEventSynchronize(ctx->ev_stage[buf]));  // its previous H2D copy has drained
+        uint8_t* h = ctx->h_stage[buf];
+        std::memcpy(h, s + i0 * sb, m * sb);
+        std::memcpy(h + o_sn, s_next + i0 * sb, m * sb);
+        std::memcpy(h + o_a, a + i0, m * sizeof(int32_t));
+        std::memcpy(h + o_r, r + i0, m * sizeof(float));
+        std::memcpy(h + o_t, terminal + i0, m);
+        CK(cudaMemcpyAsync(d, h, o_t + m, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaEventRecord(ctx->ev_stage[buf], ctx->stream));
+      }
       int rc = store(i0, m, d, reinterpret_cast<const int32_t*>(d + o_a), reinterpret_cast<const float*>(d + o_r),
                      d + o_sn, d + o_t);
       if (rc) return rc;
@@ -970,17 +995,19 @@ extern "C" int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, c
 
 
 // ------------------------------------------------------------------ profiling marks
+// (only while capturing a profiling variant: bit 8; the in-graph Store variants carry bit 16)
+static bool prof_on(const dqn_ctx* ctx) { return ctx->capture_variant >= 0 && (ctx->capture_variant & 8); }
 static void prof_begin(dqn_ctx* ctx, const std::string& name, int kernels) {
-  if (ctx->capture_variant < 8) return;
+  if (!prof_on(ctx)) return;
   dqn_ctx::ProfMark m{name, nullptr, nullptr, kernels};
   cudaEventCreate(&m.a);
   cudaEventCreate(&m.b);
   cudaEventRecordWithFlags(m.a, ctx->stream, cudaEventRecordExternal);  // a real event node in the graph
-  ctx->marks[ctx->capture_variant].push_back(m);
+  ctx->marks[ctx->capture_variant & 15].push_back(m);
 }
 static void prof_end(dqn_ctx* ctx) {
-  if (ctx->capture_variant < 8) return;
-  cudaEventRecordWithFlags(ctx->marks[ctx->capture_variant].back().b, ctx->stream, cudaEventRecordExternal);
+  if (!prof_on(ctx)) return;
+  cudaEventRecordWithFlags(ctx->marks[ctx->capture_variant & 15].back().b, ctx->stream, cudaEventRecordExternal);
 }
 #define PB(name, k) prof_begin(ctx, name, k)
 #define PE() prof_end(ctx)
@@ -1150,7 +1177,7 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
 // 7 kernels: conv fwd (sample+gather+conv1+conv2, s and s'), FC fwd (split-K, last CTA
 // reduces + bias + ReLU), TD head, FC dW, FC dX (+ReLU mask), conv bwd (conv2 dW/dX,
 // conv1 dW, biases), RMSProp update (+ bf16 publication).
-static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
+static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, bool store) {
   const NetShape& net = ctx->net;
   const dqn_config& c = ctx->cfg;
   const int b = c.minibatch;
@@ -1159,6 +1186,13 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   const ConvShape& L1 = net.conv[0];
   const ConvShape& L2 = net.conv[1];
   cudaStream_t st = ctx->stream;
+  if (store) {  // Alg. 1 "Store" of this iteration's transition (dqn_store_and_train), then the step
+    StoreArgs sa{ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->slot_stride,
+                 ctx->dedup ? 1 : 0, ctx->store_ctl, ctx->ctr};
+    PB("store", 1);
+    launch_store_step(sa, st);
+    PE();
+  }
   if (fetch) {  // a13 + a14
     if (ctx->fused_comm) {
       // delivered into theta_local by the previous round's fused server-round kernel (NEXT-1)
@@ -1197,6 +1231,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push) 
   fa.acq = ctx->acq;
   fa.img_off = ctx->img_off;
   fa.slot_stride = ctx->slot_stride;
+  fa.late = store ? 1 : 0;
   PB("conv_fwd", 1);
   launch_fwd_conv_bf16(fa, 2, st);
   PE();
@@ -1480,19 +1515,19 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   return DQN_OK;
 }
 
-static int enqueue_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
+static int enqueue_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push, bool store = false) {
   if (ctx->gpath) return enqueue_step_gpath(ctx, fetch, refresh, push);
-  return ctx->bf16 ? enqueue_step_bf16(ctx, fetch, refresh, push) : enqueue_step_f32(ctx, fetch, refresh, push);
+  return ctx->bf16 ? enqueue_step_bf16(ctx, fetch, refresh, push, store) : enqueue_step_f32(ctx, fetch, refresh, push);
 }
 
 // Capture `len` consecutive steps of variant v (bits: 1 fetch, 2 refresh, 4 push, 8 profiling
-// event records) into one graph; *kernels = its kernel nodes.
+// event records, 16 in-graph Store) into one graph; *kernels = its kernel nodes.
 static int capture_steps(dqn_ctx* ctx, int v, int len, cudaGraphExec_t* exec, long long* kernels) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   ctx->capture_variant = v;
   int rc = DQN_OK;
-  for (int i = 0; i < len && rc == DQN_OK; ++i) rc = enqueue_step(ctx, v & 1, v & 2, v & 4);
+  for (int i = 0; i < len && rc == DQN_OK; ++i) rc = enqueue_step(ctx, v & 1, v & 2, v & 4, v & 16);
   ctx->capture_variant = -1;
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
   if (rc) return rc;
@@ -1631,12 +1666,14 @@ static int launch_chunk(dqn_ctx* ctx, int v, int l, long long* kernels) {
 
 // Capture, once, the multi-step graphs the schedule can ask for, so that no capture falls into
 // a caller's timed region (a missing one is still captured on first use).
-static int prepare_chunks(dqn_ctx* ctx) {
+static int prepare_chunks(dqn_ctx* ctx, int extra = 0) {
   const dqn_config& c = ctx->cfg;
-  ctx->chunks_ready = true;
-  for (int v = 0; v < 8; ++v) {
-    const bool fetch = v & 1, refresh = v & 2, push = v & 4;
+  if (extra & 16) ctx->store_chunks_ready = true;
+  else ctx->chunks_ready = true;
+  for (int v0 = 0; v0 < 8; ++v0) {
+    const bool fetch = v0 & 1, refresh = v0 & 2, push = v0 & 4;
     if ((refresh && !fetch) || (c.n_fetch == 1 && !fetch) || (c.n_push == 1 && !push)) continue;
+    const int v = v0 | extra;
     const int nl = (refresh && c.target_sync > 1) ? 1 : dqn_ctx::kChunkLog;  // refreshes are >= C rounds apart
     for (int l = 0; l < nl; ++l) {
       if (ctx->chunk_graphs[v][l]) continue;
@@ -1649,16 +1686,17 @@ static int prepare_chunks(dqn_ctx* ctx) {
 
 // k steps of a synchronous mode as runs of same-variant steps, each run replayed as
 // power-of-two multi-step graphs (the kernels of consecutive steps then overlap via PDL).
-static int run_steps_chunked(dqn_ctx* ctx, long long k, long long* kernels) {
+static int run_steps_chunked(dqn_ctx* ctx, long long k, long long* kernels, bool store) {
   int rc;
   if (!ctx->chunks_ready && (rc = prepare_chunks(ctx))) return rc;
+  if (store && !ctx->store_chunks_ready && (rc = prepare_chunks(ctx, 16))) return rc;
   const int max_len = 1 << (dqn_ctx::kChunkLog - 1);
   for (long long s = 0; s < k;) {
-    const int v = plan_step(ctx);
+    const int v = plan_step(ctx) | (store ? 16 : 0);
     int len = 1;
     while (len < max_len && s + len < k) {
       const long long saved[4] = {ctx->T, ctx->n, ctx->n_local, ctx->ell};
-      if (plan_step(ctx) != v) {
+      if ((plan_step(ctx) | (store ? 16 : 0)) != v) {
         ctx->T = saved[0]; ctx->n = saved[1]; ctx->n_local = saved[2]; ctx->ell = saved[3];
         break;
       }
@@ -1742,6 +1780,15 @@ extern "C" int dqn_store_and_train(dqn_ctx* ctx, int64_t k, const uint8_t* s, co
   if (!ctx->use_graphs || ctx->async)
     return set_err(ctx, DQN_EINVAL, "dqn_store_and_train needs the deterministic graph-replayed schedule");
   if (k == 0) return DQN_OK;
+  // bf16 Mnih path: the Store becomes the first kernel of every step inside the replayed multi-step
+  // graphs (store_step_kernel), so the steps keep their PDL overlap; otherwise one ring kernel plus a
+  // one-step graph per iteration (DQN_GRAPH_STORE=0 forces the latter)
+  const char* gs = getenv("DQN_GRAPH_STORE");
+  if (!ctx->store_ctl && ctx->bf16 && !ctx->gpath && !(gs && atoi(gs) == 0)) {
+    int rc0 = dalloc(ctx, &ctx->store_ctl, 1);
+    if (rc0) return rc0;
+    ctx->graph_store = true;
+  }
   const long long T0 = ctx->T;
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   long long kernels = 0;

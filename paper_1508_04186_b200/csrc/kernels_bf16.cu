@@ -77,6 +77,50 @@ __global__ void push_s2d_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring
   }
 }
 
+// Alg. 1 "Store" inside the step graph (dqn_store_and_train): step T writes item T - base of the chunk
+// (StoreCtl) into its ring slot exactly as push_s2d_kernel does, after the previous step's kernels (which
+// read the ring) completed; the conv forward that follows samples and gathers after its own PDL wait.
+__global__ void store_step_kernel(StoreArgs a) {
+  pdl_wait();
+  const StoreCtl c = *a.ctl;
+  const long long i = (long long)a.ctr->T - c.base;
+  const long long slot = (c.count0 + i) % a.cap;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;  // (frame, pixel)
+  if (v < mnih::X_PIX * 4) {
+    const int f = v / mnih::X_PIX, p = v % mnih::X_PIX;
+    const int py = p / 21, px = p % 21;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      if (which == 1 && a.dedup && f != 3) break;  // frame dedup: only the new frame of s'
+      const uint8_t* src = (which ? c.sn : c.s) + i * mnih::SLOT + f * 7056 + (4 * py) * 84 + 4 * px;
+      uint4 o;
+      o.x = *reinterpret_cast<const uint32_t*>(src);
+      o.y = *reinterpret_cast<const uint32_t*>(src + 84);
+      o.z = *reinterpret_cast<const uint32_t*>(src + 168);
+      o.w = *reinterpret_cast<const uint32_t*>(src + 252);
+      *reinterpret_cast<uint4*>((which ? a.ring_sn : a.ring_s) + slot * a.stride + f * 7056 + p * 16) = o;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.ring_a[slot] = c.a[i];
+    a.ring_r[slot] = c.r[i];
+    a.ring_t[slot] = c.t[i] ? 1 : 0;
+    a.ctr->ring_size = c.count0 + i + 1 < a.cap ? c.count0 + i + 1 : a.cap;
+  }
+  pdl_trigger();
+}
+
+void launch_store_step(const StoreArgs& a, cudaStream_t st) {
+  launch_pdl(store_step_kernel, dim3(cdiv(mnih::X_PIX * 4, 256)), dim3(256), 0, st, a);
+}
+
+__global__ void store_ctl_kernel(StoreCtl* ctl, StoreCtl v) { *ctl = v; }
+
+void launch_store_ctl(StoreCtl* ctl, const uint8_t* s, const uint8_t* sn, const int32_t* a, const float* r,
+                      const uint8_t* t, long long base, long long count0, cudaStream_t st) {
+  store_ctl_kernel<<<1, 1, 0, st>>>(ctl, StoreCtl{s, sn, a, r, t, base, count0});
+}
+
 void launch_push_s2d(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, float* ring_r, uint8_t* ring_t, long long cap,
                      long long count0, long long first, long long n, const uint8_t* s, const int32_t* a,
                      const float* r, const uint8_t* sn, const uint8_t* t, cudaStream_t st, long long* ring_size_out,
@@ -143,6 +187,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   uint8_t* sW1 = smem + FWD_SW1;
   uint8_t* sW2 = smem + FWD_SW2;
   uint8_t* sU8 = smem + FWD_SU8;
+  if (a.late) pdl_wait();  // the immediate predecessor (the in-graph Store) wrote the ring and its size
   unsigned long long* tr = nullptr;  // DQN_TRACE_COMM stamps (slots 8-10 of the previous round)
   if (a.acq.trace && j == 0 && g == 0 && threadIdx.x == 0 && a.acq.ctr->T % a.acq.n_push == 0) {
     tr = a.acq.trace + ((a.acq.ctr->T / a.acq.n_push) % 64) * 16;
