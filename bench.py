@@ -59,9 +59,11 @@ def peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
-def region_work(name: str, b: int, net=MNIH):
+def region_work(name: str, b: int, net=MNIH, world: int = 1):
     """Algorithmic FLOPs and bytes of one step region. Convolutions: forward on s (theta)
-    and s' (theta^), backward dW for every layer and dX for every layer but the first; FC likewise."""
+    and s' (theta^), backward dW for every layer and dX for every layer but the first; FC likewise.
+    The fused server round (N = world > 1) moves, per rank and owned parameter: N fp32 gradient reads
+    (N - 1 of them over NVLink), theta and r read and written, bf16 theta stored to N replicas (6N + 16 B)."""
     F, H, W = 4, 84, 84
     state = F * H * W
     layers, c, h = [], F, H
@@ -84,6 +86,8 @@ def region_work(name: str, b: int, net=MNIH):
     conv_params = sum(L["N"] * (L["C"] * L["k"] ** 2 + 1) for L in layers)
     w["reduce_update"] = (0, P * 4 * 6 + b * conv_params * 4)  # + the per-image conv partials
     w["sample"] = (0, b * 4)
+    shard = -(-P // (64 * world)) * 64
+    w["server_round_fused"] = (0, shard * (6 * world + 16))
     # fused regions of the bf16 tensor-core path
     w["conv_fwd"] = tuple(sum(w[f"conv{i + 1}_fwd"][q] for i in range(len(layers))) for q in range(2))
     w["conv_bwd"] = tuple(sum(w[f"conv{i + 1}_bwd"][q] for i in range(len(layers))) for q in range(2))
@@ -419,7 +423,7 @@ def main():
     if regions:
         step_us = sum(r["avg_us"] for r in regions if r["steps"] >= args.profile_steps // 2)
         top = max(regions, key=lambda r: r["avg_us"])
-        flops, byts = region_work(top["name"], b, net)
+        flops, byts = region_work(top["name"], b, net, world)
         names = {r["name"] for r in regions}
         # N = 1 bf16 Mnih path: the conv backward launch also runs the early RMSProp update of the non-conv
         # parameters (26 B/param — read theta, r, G; write theta, r, G = 0, bf16 theta)
@@ -441,6 +445,9 @@ def main():
         else:
             roof = {"bound": "hbm", "achieved": byts / (top["avg_us"] * 1e-6) / 1e9, "peak": pk["hbm"],
                     "unit": "GB/s"}
+        if top["name"] == "server_round_fused":
+            roof["note"] = ("the fused server round (N > 1) is bound by cross-GPU flag latency (two barriers, "
+                            "DESIGN.md §6a), not by its bytes; achieved = its algorithmic bytes / its region time")
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = region_traffic(top["name"], dtype)
         roof["kernel"] = top["name"]
