@@ -109,11 +109,11 @@ def conv_param_count(net=MNIH) -> int:
     return n_params
 
 
-def region_traffic(name: str, dtype: str):
+def region_traffic(name: str, dtype: str, net=MNIH):
     """DRAM bytes (read + write) per launch of a region's kernels, from the committed `ncu --set full`
     capture of this round (profiles/r1_traffic.json), or None when not captured."""
     p = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if dtype != "bf16" or not os.path.exists(p) or name not in REGION_KERNELS:
+    if dtype != "bf16" or net != MNIH or not os.path.exists(p) or name not in REGION_KERNELS:  # Mnih kernels only
         return None
     with open(p) as f:
         t = json.load(f)
@@ -449,7 +449,7 @@ def main():
             roof["note"] = ("the fused server round (N > 1) is bound by cross-GPU flag latency (two barriers, "
                             "DESIGN.md §6a), not by its bytes; achieved = its algorithmic bytes / its region time")
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = region_traffic(top["name"], dtype)
+        roof["traffic"] = region_traffic(top["name"], dtype, dict(net, fcs=tuple(net["fcs"])))
         roof["kernel"] = top["name"]
         roof["avg_us"] = top["avg_us"]
         roof["share_of_step"] = top["avg_us"] / step_us if step_us else None

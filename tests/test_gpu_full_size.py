@@ -23,7 +23,8 @@ from tests.helpers import near_tie_mask, per_tensor_rel
 pytestmark = pytest.mark.gpu
 
 MNIH = dict(convs=((16, 8, 4), (32, 4, 2)), fcs=(256,), n_actions=6)
-CAP, B, CHUNK, SEED0 = 1_000_000, 32, 8192, 0x5EED  # bench.py's prefill: chunks of 8192, seed 0x5EED + offset
+SCALED = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=18)
+CAP, CHUNK, SEED0 = 1_000_000, 8192, 0x5EED  # bench.py's prefill: chunks of 8192, seed 0x5EED + offset
 
 
 def rel_l2_per_tensor(x, y, net):
@@ -34,19 +35,21 @@ def rel_l2_per_tensor(x, y, net):
     return worst
 
 
-def test_config1_full_size_sampled_outputs():
+@pytest.mark.parametrize("net,B,T", [(MNIH, 32, 1500), (SCALED, 512, 1100)], ids=["configs1-mnih", "configs4-scaled"])
+def test_full_size_sampled_outputs(net, B, T):
+    """configs[1] (Mnih, b = 32: the kernels specialised to the Mnih stack) and configs[4] at N = 1
+    (scaled net, b = 512: the generic tensor-core conv path)."""
     import torch
     assert torch.cuda.is_available(), "gpu tests need a CUDA device"
     if torch.cuda.mem_get_info()[0] < 64e9:
         pytest.skip("needs ~60 GB of free device memory (1M-slot replay)")
-    cfg = D.Config(**MNIH, minibatch=B, replay_capacity=CAP, target_sync=1000, precision=D.BF16, lr=2.5e-4,
+    cfg = D.Config(**net, minibatch=B, replay_capacity=CAP, target_sync=1000, precision=D.BF16, lr=2.5e-4,
                    gamma=0.99, n_push=1, n_fetch=1, sync_mode=D.DETERMINISTIC)
     g = D.DQN(cfg)
     for done in range(0, CAP, CHUNK):
         n = min(CHUNK, CAP - done)
-        g.push(*synth.g_pong_torch(n, 4, 84, 84, 6, SEED0 + done, "cuda"))
+        g.push(*synth.g_pong_torch(n, 4, 84, 84, net["n_actions"], SEED0 + done, "cuda"))
     torch.cuda.synchronize()
-    T = 1500
     g.train(T)
     th = g.params(D.PARAMS_LOCAL).astype(np.float64)
     r = g.params(D.PARAMS_RMS).astype(np.float64)
@@ -58,15 +61,15 @@ def test_config1_full_size_sampled_outputs():
     idx = out["idx"][0]
     assert list(idx) == [O.sample_index(cfg.seed, 0, T, j, CAP) for j in range(B)]
     # the sampled transitions: push j went to slot j (no wrap), regenerated from its prefill chunk
-    s, a, rw, sn, t = [], [], [], [], []
-    for slot in idx:
-        c0 = (int(slot) // CHUNK) * CHUNK
-        item = synth.g_pong_torch(min(CHUNK, CAP - c0), 4, 84, 84, 6, SEED0 + c0, "cuda")
-        k = int(slot) - c0
-        for lst, x in zip((s, a, rw, sn, t), item):
-            lst.append(x[k].cpu().numpy())
-    s, a, rw, sn, t = (np.stack(x) for x in (s, a, rw, sn, t))
-    on = O.Net(**MNIH)
+    items = {}
+    for c0 in sorted({(int(v) // CHUNK) * CHUNK for v in idx}):
+        chunk = synth.g_pong_torch(min(CHUNK, CAP - c0), 4, 84, 84, net["n_actions"], SEED0 + c0, "cuda")
+        for v in idx:
+            if (int(v) // CHUNK) * CHUNK == c0:
+                items[int(v)] = [x[int(v) - c0].cpu().numpy() for x in chunk]
+        del chunk
+    s, a, rw, sn, t = (np.stack([items[int(v)][q] for v in idx]) for q in range(5))
+    on = O.Net(**net)
     y, am = O.targets(on, th_hat, sn, rw.astype(np.float64), t, 0.99)
     qn, _ = O.q_values(on, th_hat, sn)
     ok = near_tie_mask(qn, 2e-2)
