@@ -165,7 +165,6 @@ struct dqn_ctx {
   bool use_graphs = true;
   bool step_trace = false;  // DQN_TRACE_STEP=1
   int num_sms = 148;
-  bool gpath_fc_pipe = false; // generic path: FC backward on the pipelined GEMM (DQN_GPATH_FC_PIPE=1)
   bool early_update = true; // N = 1 bf16: FC / output-layer RMSProp inside the conv backward launch (DQN_EARLY_UPDATE=0: off)
   bool keep_grad = false;
   bool alias_local = false;
@@ -669,7 +668,6 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_out), sizeof(dqn_ctx::HostOut), cudaHostAllocDefault));
   }
   if (const char* v = getenv("DQN_EARLY_UPDATE")) ctx->early_update = atoi(v) != 0;
-  if (const char* v = getenv("DQN_GPATH_FC_PIPE")) ctx->gpath_fc_pipe = atoi(v) != 0;
   {
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
@@ -1460,18 +1458,9 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   // one launch: the FC dW and dX tiles plus the head finish CTAs run side by side (tc_pair); the
   // whole K (= b and H <= 512) is staged at once, which the 200 KB budget allows at BN = 64
   gx.pre_a = 1; gx.pre_b = 0; gw.pre_a = 0; gw.pre_b = 1;
-  if (ctx->gpath_fc_pipe) {  // large b: the K-pipelined GEMM for both, then the head finish
-    gw.BN = gx.BN = 128;
-    PB("fc1_bwd_head_finish", 3);
-    launch_gemm_pipe(gw, 1, st);
-    launch_gemm_pipe(gx, 1, st);
-    launch_head_finish_warp(h, st);
-    PE();
-  } else {
-    PB("fc1_bwd_head_finish", 1);
-    launch_tc_pair_with_head(gw, gx, h, st);
-    PE();
-  }
+  PB("fc1_bwd_head_finish", 1);
+  launch_tc_pair_with_head(gw, gx, h, st);
+  PE();
   // a8/a9: per layer, top down: wgrad (+ range reduction into G), then dgrad into the layer below
   PB("conv_bwd", 3 * nl - 1);
   for (int i = nl - 1; i >= 0; --i) {
