@@ -1279,7 +1279,9 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   TcGemmArgs gx{};
   gx.A[0] = ctx->theta_local_bf16 + F.w_off; gx.lda = F.D; gx.a_mn = 1;
   gx.B[0] = ctx->dh_bf16; gx.ldb = F.H; gx.b_mn = 0;
-  gx.M = F.D; gx.N = b; gx.K = F.H; gx.BN = b; gx.kper = F.H; gx.splits = 1;
+  // n-tiles of 16 samples (b <= 32) or 64: more CTAs, each with a shorter ReLU-mask epilogue (measured:
+  // 35.95 -> 35.35 us/step at b = 32; BJ.c4, b = 256: 2.16 M -> 2.40 M tr/s with 64 instead of 256)
+  gx.M = F.D; gx.N = b; gx.K = F.H; gx.BN = b <= 32 ? 16 : 64; gx.kper = F.H; gx.splits = 1;
   gx.epi = TC_EPI_MASK_T; gx.out_bf16 = ctx->dz2_bf16; gx.mask = ctx->a2_bf16; gx.ldo = F.D;
   gx.pre_a = 1; gx.pre_b = 0;  // W is published by the previous step's update; dH by the predecessor
   PB("fc1_bwd_head_finish", 1);
