@@ -172,8 +172,10 @@ constexpr int FWD_SX = 0;
 constexpr int FWD_SA1 = FWD_SX + 8 * mnih::X_ALLOC * 16;       // 69632
 constexpr int FWD_SW1 = FWD_SA1 + 8 * mnih::A1_ALLOC * 16;     // +18432
 constexpr int FWD_SW2 = FWD_SW1 + 32 * mnih::C1 * 16;          // +8192
-constexpr int FWD_SU8 = FWD_SW2 + 32 * mnih::C2 * 16;          // +16384
-constexpr int FWD_SMEM = FWD_SU8 + mnih::SLOT;                  // +28224 = 140864
+constexpr int FWD_SMEM = FWD_SW2 + 32 * mnih::C2 * 16;         // +16384 = 112640: two CTAs per SM
+// the gathered u8 slot lands over sA1 | sW1 | sW2, which are written only after it was expanded into sX
+constexpr int FWD_SU8 = FWD_SA1;
+static_assert(FWD_SU8 + mnih::SLOT <= FWD_SMEM, "u8 staging inside the kernel's shared memory");
 
 __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   mbar_wait(&bar_ld, 0);
   if (tr) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[9]));
   expand_state(sX, sU8);  // u8 -> exact bf16 (1/255 folded into the epilogue)
+  __syncthreads();        // every thread has read the u8 slot before the weights land over it
   // everything above overlaps the previous kernel (the update that publishes theta); weights after the wait
   if (fused_round_acquire_conv(a.acq)) {
     // conv-first delivery: the previous step's server round released the conv parameters early; no
