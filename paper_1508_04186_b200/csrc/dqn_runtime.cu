@@ -576,7 +576,10 @@ static int setup_gpath(dqn_ctx* ctx) {
       pk += (long long)G.Cs * T * L.N;
     }
     const int mt = (K + 127) / 128;
-    const int ranges = std::max(1, std::min(b, 296 / mt));
+    // weight-gradient CTAs per layer ≈ wg_ctas (image ranges × M tiles): 4 × 148 measured best on BJ.configs[4]
+    // (296: 875 K, 444: 922 K, 592: 924 K, 888: 899 K tr/s); DQN_GCONV_WG_CTAS overrides
+    static const int wg_ctas = getenv("DQN_GCONV_WG_CTAS") ? std::max(1, atoi(getenv("DQN_GCONV_WG_CTAS"))) : 592;
+    const int ranges = std::max(1, std::min(b, wg_ctas / mt));
     G.ipc = (b + ranges - 1) / ranges;
     const long long nr = (b + G.ipc - 1) / G.ipc;
     max_part = std::max(max_part, nr * K * L.N);
