@@ -11,6 +11,7 @@ namespace dqn {
 constexpr int kMaxConv = 4;
 constexpr int kMaxFc = 4;
 constexpr int kDiagSteps = 4096;  // ring of per-step diagnostics (idx, argmax, loss)
+constexpr int kHeadMaxSplits = 24;  // FC forward split-K partials the TD head sums (head_sample_kernel)
 
 // One valid convolution layer (A16): in C x H x W, out N x Ho x Wo.
 struct ConvShape {

@@ -554,7 +554,8 @@ static int setup_gpath(dqn_ctx* ctx) {
       ctx->fc_splits = sp;
       break;
     }
-  if (!ctx->fc_splits) return set_err(ctx, DQN_EINVAL, "FC input too large for the tensor-core split-K");
+  if (!ctx->fc_splits || ctx->fc_splits > kHeadMaxSplits)  // the head sums at most kHeadMaxSplits partials
+    return set_err(ctx, DQN_EINVAL, "FC input too large for the tensor-core split-K");
   long long pk = 0, max_part = 0, max_db = 0;
   std::vector<int2> map((size_t)(net.conv[net.n_conv - 1].b_off + net.conv[net.n_conv - 1].N), make_int2(-1, -1));
   for (int i = 0; i < net.n_conv; ++i) {

@@ -19,7 +19,7 @@ namespace dqn {
 
 constexpr int HS_THREADS = 256;
 constexpr int HS_AMAX = 32;
-constexpr int HS_MAX_SPLITS = 24;
+constexpr int HS_MAX_SPLITS = kHeadMaxSplits;
 
 // dynamic smem: h [H] | h' [H] | W^_o [A][H] | W_o[a_j] [H]
 __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
