@@ -63,7 +63,9 @@ enum {
   DQN_PARAMS_SERVER = 0, /* global theta of Alg. 2 (fp32 masters, gathered over ranks: collective) */
   DQN_PARAMS_LOCAL = 1,  /* this replica's fetched theta (Alg. 1 "Fetch model theta")       */
   DQN_PARAMS_TARGET = 2, /* this replica's target theta^                             */
-  DQN_PARAMS_GRAD = 3,   /* this replica's last-step gradient Delta theta; diagnostic      */
+  DQN_PARAMS_GRAD = 3,   /* the gradient this replica pushed in its last push round: sum over its
+                            n_push steps of Delta theta (A8), before the mean; needs
+                            cfg.keep_grad = 1 (DQN_EINVAL otherwise); diagnostic                   */
   DQN_PARAMS_RMS = 4     /* RMSProp accumulator r of Alg. 2 (gathered: collective)                 */
 };
 
@@ -97,6 +99,11 @@ typedef struct {
   int32_t replay_dedup;                /* 1: frame-deduplicated replay (NEXT-4): every pushed s' must be
                                           s shifted by one frame plus a new frame (Atari-style stacks);
                                           a slot stores F+1 frames instead of 2F (DQN_EINVAL otherwise) */
+  int32_t keep_grad;                   /* 1: the kernels that consume this replica's pushed gradient (the
+                                          update / server round, or the acquire that clears it) also store
+                                          it into a snapshot that dqn_get_params(DQN_PARAMS_GRAD) returns.
+                                          Diagnostic; the step's kernels, launch configuration and
+                                          arithmetic are otherwise unchanged (it adds one store per element) */
 } dqn_config;
 
 typedef struct {

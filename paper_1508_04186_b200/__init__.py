@@ -44,7 +44,7 @@ class _Config(C.Structure):
                 ("n_push", C.c_int32), ("n_fetch", C.c_int32), ("target_sync", C.c_int64),
                 ("precision", C.c_int32), ("sync_mode", C.c_int32), ("seed", C.c_uint64),
                 ("init_std", C.c_double), ("init_seed", C.c_uint64), ("init_params", C.c_void_p),
-                ("server_rule", C.c_int32), ("replay_dedup", C.c_int32)]
+                ("server_rule", C.c_int32), ("replay_dedup", C.c_int32), ("keep_grad", C.c_int32)]
 
 
 class _Stats(C.Structure):
@@ -89,6 +89,7 @@ class Config:
     init_seed: int = 7
     server_rule: int = 0   # SERVER_MEAN (A7) | SERVER_PER_GRADIENT (A33)
     replay_dedup: int = 0  # 1: F+1 frames per slot (s' = s shifted by one frame + a new frame)
+    keep_grad: int = 0     # 1: the update kernels also store the pushed gradient (DQN_PARAMS_GRAD)
 
     def to_c(self, init_ptr: Optional[int] = None) -> _Config:
         c = _Config()
@@ -101,7 +102,7 @@ class Config:
             c.fc_units[i] = u
         for name in ("n_actions", "minibatch", "gamma", "lr", "rms_decay", "rms_eps", "err_clip", "replay_capacity",
                      "n_push", "n_fetch", "target_sync", "precision", "sync_mode", "seed", "init_std", "init_seed",
-                     "server_rule", "replay_dedup"):
+                     "server_rule", "replay_dedup", "keep_grad"):
             setattr(c, name, getattr(self, name))
         c.init_params = init_ptr
         return c
@@ -178,6 +179,23 @@ def _ptr(x, dtype) -> Tuple[int, object]:
         pass
     a = np.ascontiguousarray(x, dtype=dtype)
     return a.ctypes.data, a
+
+
+def _out_ptr(x, dtype, name: str) -> Tuple[int, object]:
+    """Address of an output buffer the library writes in place: it must already be contiguous with the
+    right dtype (a converted copy would be written instead of the caller's buffer)."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            want = {np.int32: torch.int32, np.float32: torch.float32}[dtype]
+            if x.dtype != want or not x.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous {want} tensor")
+            return x.data_ptr(), x
+    except ImportError:
+        pass
+    if not isinstance(x, np.ndarray) or x.dtype != dtype or not x.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{name} must be a C-contiguous numpy array of {np.dtype(dtype).name}")
+    return x.ctypes.data, x
 
 
 class DQN:
@@ -270,19 +288,22 @@ class DQN:
                 for i in range(min(n.value, 64))]
 
     def q_values(self, states, q_out=None, argmax_out=None):
+        """Q(s, .; theta_local) and the greedy actions (dqn_q_values). Caller-given outputs must be contiguous
+        float32 / int32 (numpy or torch, host or CUDA): they are written in place."""
         n = len(states)
         A = self.cfg.n_actions
         ps, k1 = _ptr(states, np.uint8)
         q = q_out if q_out is not None else np.zeros((n, A), np.float32)
         am = argmax_out if argmax_out is not None else np.zeros(n, np.int32)
-        pq, _ = _ptr(q, np.float32)
-        pa, _ = _ptr(am, np.int32)
+        pq, kq = _out_ptr(q, np.float32, "q_out")
+        pa, ka = _out_ptr(am, np.int32, "argmax_out")
         self._check(lib().dqn_q_values(self._h, n, ps, pq, pa))
+        del k1, kq, ka
         return q, am
 
     def params(self, which: int = PARAMS_SERVER, out=None):
         o = out if out is not None else np.zeros(self.P, np.float32)
-        po, _ = _ptr(o, np.float32)
+        po, ko = _out_ptr(o, np.float32, "out")
         n = C.c_int64()
         g = C.c_uint64()
         self._check(lib().dqn_get_params(self._h, which, po, self.P, C.byref(n), C.byref(g)))

@@ -126,7 +126,7 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
                     cudaStream_t st, long long img_off = -1,
-                    long long w1_off = 0, long long w2_off = 0);
+                    long long w1_off = 0, long long w2_off = 0, float* g_snap = nullptr);
 void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st, long long img_off = -1,
                         long long w1_off = 0, long long w2_off = 0);
 
@@ -190,6 +190,7 @@ struct FusedAcquire {
   const unsigned long long* done_c;
   int n_c;
   int conv_first;
+  float* g_snap;                                // cfg.keep_grad: G copied here before it is cleared (or nullptr)
 };
 void launch_fused_round_acquire(const FusedAcquire& f, cudaStream_t st);
 int server_round_blocks(long long shard);
@@ -322,6 +323,7 @@ struct GConvWgradArgs {
   int store;                       // 1: G = sum (n_push = 1), 0: G += sum
 };
 void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st);
+bool gconv_wgrad_fits(int N, int first, int ipc, int HoWo);  // shared memory of a wgrad CTA within the attribute
 void launch_gpack(const float* theta, __nv_bfloat16* dst, long long img_off, const int2* map, long long n,
                   cudaStream_t st);
 void init_conv_kernel_attrs();
@@ -368,6 +370,7 @@ struct ReduceUpdateArgs {
   DevCounters* ctr;
   int early;                       // 1: the non-conv part [kBwdPart, n) is updated by the conv backward's
                                    //    extra CTAs (launch_bwd_conv_update); this launch does the conv part only
+  float* g_snap;                   // cfg.keep_grad: every consumed gradient element also stored here (or nullptr)
 };
 void launch_reduce_update(const ReduceUpdateArgs& u, cudaStream_t st);
 // N = 1, n_push = 1: the conv backward launch plus `upd_ctas` CTAs that apply the RMSProp update to the

@@ -516,6 +516,7 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   ctx->acq.grad = ctx->grad;
   ctx->acq.grad_elems = ctx->P_pad;
   ctx->acq.ctr = ctx->ctr;
+  ctx->acq.g_snap = ctx->grad_snap;
   // conv-first delivery (bf16 Mnih path, conv parameters = the canonical prefix [0, kBwdPart))
   const char* cf = getenv("DQN_CONV_FIRST");
   const bool mnih_bf16 = ctx->bf16 && !ctx->gpath && ctx->img_off >= 0 && ctx->w1_off == 0 &&
@@ -555,7 +556,10 @@ static int setup_gpath(dqn_ctx* ctx) {
       break;
     }
   if (!ctx->fc_splits || ctx->fc_splits > kHeadMaxSplits)  // the head sums at most kHeadMaxSplits partials
-    return set_err(ctx, DQN_EINVAL, "FC input too large for the tensor-core split-K");
+    return set_err(ctx, DQN_EINVAL, "DQN_BF16: the FC input D = " + std::to_string(F.D) + " needs " +
+                                        (ctx->fc_splits ? std::to_string(ctx->fc_splits) : std::string("no valid")) +
+                                        " split-K partials of <= 512 (a multiple of 16 dividing D); the TD head sums at most " +
+                                        std::to_string(kHeadMaxSplits));
   long long pk = 0, max_part = 0, max_db = 0;
   std::vector<int2> map((size_t)(net.conv[net.n_conv - 1].b_off + net.conv[net.n_conv - 1].N), make_int2(-1, -1));
   for (int i = 0; i < net.n_conv; ++i) {
@@ -582,6 +586,10 @@ static int setup_gpath(dqn_ctx* ctx) {
     static const int wg_ctas = getenv("DQN_GCONV_WG_CTAS") ? std::max(1, atoi(getenv("DQN_GCONV_WG_CTAS"))) : 592;
     const int ranges = std::max(1, std::min(b, wg_ctas / mt));
     G.ipc = (b + ranges - 1) / ranges;
+    while (G.ipc > 1 && !gconv_wgrad_fits(L.N, i == 0, G.ipc, G.Ho * G.Wo)) --G.ipc;  // position table + ring
+    if (!gconv_wgrad_fits(L.N, i == 0, G.ipc, G.Ho * G.Wo))
+      return set_err(ctx, DQN_EINVAL, "DQN_BF16: conv layer " + std::to_string(i + 1) +
+                                          " too large for the weight-gradient kernel's shared memory");
     const long long nr = (b + G.ipc - 1) / G.ipc;
     max_part = std::max(max_part, nr * K * L.N);
     max_db = std::max(max_db, nr * L.N);
@@ -648,7 +656,7 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   ctx->shard = ctx->P_pad / world;
   ctx->cap = cfg->replay_capacity;
   ctx->use_graphs = !(getenv("DQN_NO_GRAPH") && atoi(getenv("DQN_NO_GRAPH")));
-  ctx->keep_grad = getenv("DQN_KEEP_GRAD") && atoi(getenv("DQN_KEEP_GRAD"));
+  ctx->keep_grad = cfg->keep_grad != 0;
   ctx->async = cfg->sync_mode == DQN_ASYNC;
   ctx->alias_local = (world == 1 && cfg->n_fetch == 1 && !ctx->async);
   ctx->bf16 = cfg->precision == DQN_BF16;
@@ -1147,8 +1155,6 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
                                       ctx->dz_conv[i - 1], b, st);
     PE();
   }
-  if (ctx->keep_grad)
-    CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
   // a11 push + a12 shard update (Alg. 2 RMSPropUpdate; n <- n + 1)
   if (push) {
     const float div = (float)((double)ctx->world * c.n_push);
@@ -1159,6 +1165,8 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
       PE();
     } else if (ctx->world > 1) {
       PB("push_reduce_scatter", 0);
+      if (ctx->grad_snap)
+        CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
       NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
       CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
       PE();
@@ -1169,7 +1177,7 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
     } else {
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
-                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 1, st);
+                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 1, st, -1, 0, 0, ctx->grad_snap);
       PE();
     }
   }
@@ -1302,7 +1310,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   ba.w1_off = L1.w_off; ba.b1_off = L1.b_off; ba.w2_off = L2.w_off; ba.b2_off = L2.b_off;
   ba.n = b; ba.partial = ctx->bwd_partial; ba.counter = ctx->tc_counters + 32; ba.grad = ctx->grad;
   // N = 1, n_push = 1: the conv partials' reduction runs inside the update (reduce_update_kernel)
-  const bool fuse_reduce = push && ctx->world == 1 && c.n_push == 1 && !ctx->keep_grad && ctx->alias_local &&
+  const bool fuse_reduce = push && ctx->world == 1 && c.n_push == 1 && ctx->alias_local &&
                            L1.w_off == 0 && L2.b_off + L2.N == kBwdPart;
   ReduceUpdateArgs u{};
   if (fuse_reduce) {
@@ -1312,6 +1320,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
     u.inv_div = 1.0f / div; u.lr = (float)c.lr; u.rho = (float)c.rms_decay; u.omr = (float)(1.0 - c.rms_decay);
     u.eps = (float)c.rms_eps;
     u.pub_bf16 = ctx->theta_local_bf16; u.img_off = ctx->img_off; u.ctr = ctx->ctr;
+    u.g_snap = ctx->grad_snap;
     u.early = ctx->early_update && b + 32 <= ctx->num_sms ? 1 : 0;  // needs SMs the conv CTAs leave free
   }
   PB("conv_bwd", fuse_reduce ? 1 : 2);
@@ -1320,8 +1329,6 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   else
     launch_bwd_conv_bf16(ba, st, !fuse_reduce);
   PE();
-  if (ctx->keep_grad)
-    CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
   // a11 push + a12 shard update
   if (push) {
     const float div = (float)((double)ctx->world * c.n_push);
@@ -1332,6 +1339,8 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
       PE();
     } else if (ctx->world > 1) {
       PB("push_reduce_scatter", 0);
+      if (ctx->grad_snap)
+        CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
       NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
       CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
       PE();
@@ -1347,7 +1356,7 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
                      (float)c.rms_eps, nullptr, ctx->alias_local ? ctx->theta_local_bf16 : nullptr, ctx->ctr, 1, st,
-                   ctx->alias_local ? ctx->img_off : -1, ctx->w1_off, ctx->w2_off);
+                   ctx->alias_local ? ctx->img_off : -1, ctx->w1_off, ctx->w2_off, ctx->grad_snap);
       PE();
     }
   }
@@ -1493,8 +1502,6 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     }
   }
   PE();
-  if (ctx->keep_grad)
-    CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
   // a11 push + a12 shard update (+ a13 fetch in the fused round)
   if (push) {
     const float div = (float)((double)ctx->world * c.n_push);
@@ -1505,6 +1512,8 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
       PE();
     } else if (ctx->world > 1) {
       PB("push_reduce_scatter", 0);
+      if (ctx->grad_snap)
+        CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, st));
       NK(ncclReduceScatter(ctx->grad, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, st));
       CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, st));
       PE();
@@ -1515,7 +1524,8 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     } else {
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
-                     (float)c.rms_eps, nullptr, ctx->alias_local ? ctx->theta_local_bf16 : nullptr, ctx->ctr, 1, st);
+                     (float)c.rms_eps, nullptr, ctx->alias_local ? ctx->theta_local_bf16 : nullptr, ctx->ctr, 1, st, -1, 0,
+                     0, ctx->grad_snap);
       PE();
     }
   }
@@ -1554,6 +1564,8 @@ static int capture_steps(dqn_ctx* ctx, int v, int len, cudaGraphExec_t* exec, lo
   e = cudaGraphInstantiate(exec, g, 0);
   cudaGraphDestroy(g);
   CK(e);
+  // upload now, so that the first launch (possibly inside a caller's timed region) does not pay for it
+  CK(cudaGraphUpload(*exec, ctx->stream));
   return DQN_OK;
 }
 
@@ -1605,7 +1617,11 @@ static int async_fetch(dqn_ctx* ctx) {
 static int async_push(dqn_ctx* ctx) {
   const dqn_config& c = ctx->cfg;
   cudaStream_t cs = ctx->comm_stream;
+  // g_send is still read by the previous round (generation n) until it publishes ev_gen[n % 2]
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gen[ctx->n % 2], 0));
   CK(cudaMemcpyAsync(ctx->g_send, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (ctx->grad_snap)
+    CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, ctx->stream));
   CK(cudaEventRecord(ctx->ev_grad, ctx->stream));
   CK(cudaStreamWaitEvent(cs, ctx->ev_grad, 0));
@@ -1927,6 +1943,13 @@ static int q_enqueue(dqn_ctx* ctx, int m) {
   (void)sb;
   cudaStream_t st = ctx->stream;
   const float* in = nullptr;
+  if (ctx->fused_comm && ctx->T > 0 && ctx->T % ctx->cfg.n_push == 0) {
+    // the last step pushed: acquire the peers' deliveries of that round into theta_local before reading
+    // it (the next step's first kernel would do it; G is cleared here and harmlessly again there)
+    FusedAcquire f = ctx->acq;
+    f.g_snap = nullptr;  // keep the round's gradient snapshot
+    launch_fused_round_acquire(f, st);
+  }
   if (ctx->gpath) {  // s2d staging, the generic tensor-core conv forward, FC split-K + reduction
     const FcShape& F = net.fc[0];
     launch_push_s2d(ctx->q_stage_s2d, nullptr, nullptr, nullptr, nullptr, b, 0, 0, m, ctx->q_stage, nullptr,
@@ -2194,7 +2217,7 @@ extern "C" int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, 
     }
     case DQN_PARAMS_TARGET: src = ctx->theta_hat; break;
     case DQN_PARAMS_GRAD:
-      if (!ctx->grad_snap) return set_err(ctx, DQN_EINVAL, "gradient snapshots need DQN_KEEP_GRAD=1 at create");
+      if (!ctx->grad_snap) return set_err(ctx, DQN_EINVAL, "gradient snapshots need cfg.keep_grad = 1 at create");
       src = ctx->grad_snap;
       break;
     default: return set_err(ctx, DQN_EINVAL, "unknown parameter vector");

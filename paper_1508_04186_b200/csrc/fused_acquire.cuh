@@ -52,8 +52,10 @@ __device__ __forceinline__ void fused_round_acquire(const FusedAcquire& f) {
   const long long g4 = f.grad_elems / 4;
   const long long blk = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   const long long nblk = (long long)gridDim.x * gridDim.y * gridDim.z;
-  for (long long i = blk * blockDim.x + threadIdx.x; i < g4; i += nblk * blockDim.x)
+  for (long long i = blk * blockDim.x + threadIdx.x; i < g4; i += nblk * blockDim.x) {
+    if (f.g_snap) reinterpret_cast<float4*>(f.g_snap)[i] = reinterpret_cast<const float4*>(f.grad)[i];  // keep_grad
     reinterpret_cast<float4*>(f.grad)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 }
 
 // conv-first delivery: true if the previous step ran a server round (then the caller must not rely

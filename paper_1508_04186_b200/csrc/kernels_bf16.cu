@@ -1017,6 +1017,7 @@ __device__ __forceinline__ Rms4 rms_load4(const ReduceUpdateArgs& u, long long i
 __device__ __forceinline__ unsigned rms_apply4(const ReduceUpdateArgs& u, long long i, const Rms4& x) {
   unsigned bad = 0;
   reinterpret_cast<float4*>(u.g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (u.g_snap) reinterpret_cast<float4*>(u.g_snap)[i] = x.g;  // cfg.keep_grad (diagnostic)
   float tv[4] = {x.t.x, x.t.y, x.t.z, x.t.w}, rv[4] = {x.r.x, x.r.y, x.r.z, x.r.w};
   const float gv[4] = {x.g.x, x.g.y, x.g.z, x.g.w};
 #pragma unroll
@@ -1060,6 +1061,7 @@ __global__ void __launch_bounds__(256) reduce_update_kernel(ReduceUpdateArgs u) 
     const int e = (int)t;
     const float g = bwd_part_sum(e, u.b);
     const long long d = bwd_part_dst(e, u.b);
+    if (u.g_snap) u.g_snap[d] = g;  // cfg.keep_grad (diagnostic)
     float th = u.theta[d], r = u.r[d];
     if (rms_elem(th, r, g, u)) {
       u.theta[d] = th;

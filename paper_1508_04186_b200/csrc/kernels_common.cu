@@ -123,7 +123,7 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
 __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r, float* __restrict__ g, long long n,
                                float inv_div, float lr, float rho, float omr, float eps, float* __restrict__ pub_f32,
                                __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr, int zero_g, long long img_off,
-                               long long w1_off, long long w2_off) {
+                               long long w1_off, long long w2_off, float* __restrict__ g_snap) {
   st_stamp(ST_UPDATE, 0);
   pdl_sync();
   st_stamp(ST_UPDATE, 1);
@@ -133,6 +133,7 @@ __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r,
   float4 t4 = reinterpret_cast<const float4*>(theta)[i];
   float4 r4 = reinterpret_cast<const float4*>(r)[i];
   if (zero_g) reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (g_snap) reinterpret_cast<float4*>(g_snap)[i] = g4;  // cfg.keep_grad (diagnostic)
   float tv[4] = {t4.x, t4.y, t4.z, t4.w};
   float rv[4] = {r4.x, r4.y, r4.z, r4.w};
   const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
@@ -173,10 +174,10 @@ __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r,
 
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
-                    cudaStream_t st, long long img_off, long long w1_off, long long w2_off) {
+                    cudaStream_t st, long long img_off, long long w1_off, long long w2_off, float* g_snap) {
   const int blocks = (int)((n / 4 + 255) / 256);
   launch_pdl(rmsprop_kernel, dim3(blocks < 1 ? 1 : blocks), dim3(256), 0, st, theta, r, g, n, 1.0f / div, lr, rho, omr,
-             eps, pub_f32, pub_bf16, ctr, zero_g, img_off, w1_off, w2_off);
+             eps, pub_f32, pub_bf16, ctr, zero_g, img_off, w1_off, w2_off, g_snap);
 }
 
 

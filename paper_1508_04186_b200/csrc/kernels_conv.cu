@@ -609,12 +609,20 @@ __global__ void __launch_bounds__(256) gconv_wreduce_kernel(GConvWgradArgs a) {
   else a.grad[dst] += t;
 }
 
+// dynamic shared memory of a weight-gradient CTA: the stage ring plus the position table of its images
+static int gconv_wgrad_smem(int N, int first, int ipc, int HoWo) {
+  return NS * stage_bytes(N, first) + (ipc * HoWo * 8 + 1023) / 1024 * 1024;
+}
+static int g_wgrad_smem_cap = 0;  // the kernel's dynamic shared-memory attribute (init_conv_kernel_attrs)
+bool gconv_wgrad_fits(int N, int first, int ipc, int HoWo) {
+  return gconv_wgrad_smem(N, first, ipc, HoWo) <= g_wgrad_smem_cap;
+}
+
 void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
   const int T = a.Th * a.Tw, MK = T * a.Cs;
   const int ranges = (a.b + a.ipc - 1) / a.ipc;
-  const int pos_bytes = (a.ipc * a.Ho * a.Wo * 8 + 1023) / 1024 * 1024;  // the position table
   launch_pdl(gconv_wgrad_kernel, dim3((MK + 127) / 128, ranges), dim3(128),
-             NS * stage_bytes(a.N, a.first) + pos_bytes, st, a);
+             gconv_wgrad_smem(a.N, a.first, a.ipc, a.Ho * a.Wo), st, a);
   gconv_debug("gconv_wgrad", st);
   const long long n = (long long)MK * a.N + a.N;
   launch_pdl(gconv_wreduce_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, st, a);
@@ -632,16 +640,18 @@ unsigned long long gconv_error() {
 
 void init_conv_kernel_attrs() {
   // the 227 KB opt-in limit includes each kernel's static shared memory
-  auto set = [](const void* f) {
+  auto set = [](const void* f, bool full) {
     cudaFuncAttributes at{};
     cudaFuncGetAttributes(&at, f);
-    const int mx = std::min<int>(GCONV_SMEM_MAX, 227 * 1024 - (int)at.sharedSizeBytes - 1024);
+    const int cap = 227 * 1024 - (int)at.sharedSizeBytes - 1024;
+    const int mx = full ? cap : std::min<int>(GCONV_SMEM_MAX, cap);
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    return mx;
   };
-  set((const void*)gconv_fwd_kernel);
-  set((const void*)gconv_dgrad_kernel);
-  set((const void*)gconv_wgrad_kernel);
-  set((const void*)gemm_pipe_kernel);
+  set((const void*)gconv_fwd_kernel, false);
+  set((const void*)gconv_dgrad_kernel, false);
+  g_wgrad_smem_cap = set((const void*)gconv_wgrad_kernel, true);  // the ring + the position table
+  set((const void*)gemm_pipe_kernel, false);
 }
 
 // ------------------------------------------------------------------ pipelined GEMM (generic path FC layers)

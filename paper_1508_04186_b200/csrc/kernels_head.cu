@@ -3,7 +3,7 @@
 //
 // head_sample (one CTA per sample j, so the b samples run in parallel):
 //   [bf16 path] h_j, h'_j = ReLU(sum over FC split-K partials + b_fc)   (a5's reduction, fused here)
-//   Q'_j = W^_o h'_j + b^_o ; m_j = max_a' Q'_j, g_j = argmax (lowest index on ties, A20)
+//   Q'_j = W^_o h'_j + b^_o ; m_j = max_a' Q'_j, g_j = argmax (warp-shuffle reduction; lowest index on ties, A20)
 //   y_j = term_j ? r_j : r_j + gamma m_j                              (a select, A14)
 //   delta_j = Q(s_j; theta)_{a_j} - y_j ; dQ_j = clamp(delta_j, -c, c) / b at a_j only (A2, A3)
 //   dH_j = dQ_j W_o[a_j] * [h_j > 0]        (d pre-activation of the previous layer, ReLU'(0) = 0)
@@ -89,23 +89,31 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
   }
   __syncthreads();
   __shared__ float s_dq;
-  if (threadIdx.x == 0) {
-    float best = s_q[0];
-    int barg = 0;
-    for (int a = 1; a < A; ++a)
-      if (s_q[a] > best) { best = s_q[a]; barg = a; }
-    const float y = term ? r : r + h.gamma * best;
-    const float delta = s_qa - y;
-    float dc = delta;
-    if (h.clip > 0.0f) dc = fminf(fmaxf(dc, -h.clip), h.clip);
-    const float dq = dc / (float)h.b;
-    s_dq = dq;
-    h.s_dq[j] = dq;
-    h.s_act[j] = act;
-    h.s_loss[j] = 0.5f * delta * delta;
-    const int dslot = (int)(h.ctr->T % kDiagSteps);
-    h.diag_idx[(long long)dslot * h.b + j] = slot;
-    h.diag_amax[(long long)dslot * h.b + j] = barg;
+  if (warp == 0) {
+    // m_j = max_a' Q'_j and its argmax by a warp-shuffle reduction over the actions (lane a holds Q'_a,
+    // A <= 32); ties keep the lowest index (A20)
+    float best = lane < A ? s_q[lane] : -INFINITY;
+    int barg = lane < A ? lane : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, barg, o);
+      if (ob > best || (ob == best && oa < barg)) { best = ob; barg = oa; }
+    }
+    if (lane == 0) {
+      const float y = term ? r : r + h.gamma * best;  // a select, never (1 - term) * m (A14)
+      const float delta = s_qa - y;
+      float dc = delta;
+      if (h.clip > 0.0f) dc = fminf(fmaxf(dc, -h.clip), h.clip);  // error clip (A3)
+      const float dq = dc / (float)h.b;
+      s_dq = dq;
+      h.s_dq[j] = dq;
+      h.s_act[j] = act;
+      h.s_loss[j] = 0.5f * delta * delta;
+      const int dslot = (int)(h.ctr->T % kDiagSteps);
+      h.diag_idx[(long long)dslot * h.b + j] = slot;
+      h.diag_amax[(long long)dslot * h.b + j] = barg;
+    }
   }
   __syncthreads();
   const float dq = s_dq;

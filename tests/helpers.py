@@ -10,6 +10,7 @@ from oracle import oracle as O
 
 
 def nets(convs=((16, 8, 4), (32, 4, 2)), fcs=(256,), n_actions=6, frames=4, height=84, width=84, **kw):
+    kw.setdefault("keep_grad", 1)  # the update kernels also store the pushed gradient (same kernels, DQN_PARAMS_GRAD)
     dc = D.Config(frames=frames, height=height, width=width, convs=convs, fcs=fcs, n_actions=n_actions, **kw)
     on = O.Net(frames=frames, height=height, width=width, convs=convs, fcs=fcs, n_actions=n_actions)
     oc = O.TrainCfg(n_replicas=1, minibatch=dc.minibatch, n_push=dc.n_push, n_fetch=dc.n_fetch,

@@ -26,7 +26,6 @@ TOL = 2e-2
 def _cuda():
     import torch
     assert torch.cuda.is_available(), "gpu tests need a CUDA device"
-    os.environ["DQN_KEEP_GRAD"] = "1"
     yield
 
 
@@ -155,8 +154,7 @@ def test_fused_reduce_update_path():
             res[keep] = (g.params(D.PARAMS_SERVER).astype(np.float64), g.params(D.PARAMS_LOCAL).astype(np.float64))
             g.close()
         finally:
-            os.environ["DQN_KEEP_GRAD"] = "1"
-            os.environ.pop("DQN_EARLY_UPDATE", None)
+                    os.environ.pop("DQN_EARLY_UPDATE", None)
     assert np.array_equal(res[None][0], res["late"][0]) and np.array_equal(res[None][1], res["late"][1])
     ref = O.run(on, oc, 1000, [rp], theta0.astype(np.float64), 5)
     th0 = theta0.astype(np.float64)

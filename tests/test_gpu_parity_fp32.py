@@ -21,7 +21,6 @@ TINY_KW = dict(frames=3, height=17, width=13, convs=((5, 5, 2), (6, 3, 2)), fcs=
 def _cuda():
     import torch
     assert torch.cuda.is_available(), "gpu tests need a CUDA device"
-    os.environ["DQN_KEEP_GRAD"] = "1"
     yield
 
 

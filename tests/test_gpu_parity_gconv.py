@@ -20,7 +20,6 @@ SCALED = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=
 def _cuda():
     import torch
     assert torch.cuda.is_available(), "gpu tests need a CUDA device"
-    os.environ["DQN_KEEP_GRAD"] = "1"
     yield
 
 

@@ -17,7 +17,6 @@ pytestmark = pytest.mark.gpu
 def _cuda():
     import torch
     assert torch.cuda.is_available(), "gpu tests need a CUDA device"
-    os.environ.pop("DQN_KEEP_GRAD", None)
     yield
 
 
