@@ -59,32 +59,38 @@ def peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
-def region_work(name: str, b: int, net=MNIH, world: int = 1):
-    """Algorithmic FLOPs and bytes of one step region. Convolutions: forward on s (theta)
-    and s' (theta^), backward dW for every layer and dX for every layer but the first; FC likewise.
-    The fused server round (N = world > 1) moves, per rank and owned parameter: N fp32 gradient reads
-    (N - 1 of them over NVLink), theta and r read and written, bf16 theta stored to N replicas (6N + 16 B)."""
+def region_work(name: str, b: int, net=MNIH, world: int = 1, dtype: str = "bf16"):
+    """Algorithmic FLOPs and HBM bytes of one step region. Convolutions:
+    forward on s (theta) and s' (theta^), backward dW for every layer and dX for every layer but the first;
+    FC likewise. Activations are `dtype` (bf16: 2 B, f32: 4 B); the replay slots are u8 (the 56,448 B of s and
+    s' per transition of a2); gradients are fp32. The shard update moves 22 B per parameter (read theta, r, G;
+    write theta, r and the bf16 theta; 20 B on the fp32 path). The fused server round (N = world
+    > 1) moves, per rank and owned parameter, N fp32 gradient reads (N - 1 over NVLink), theta and r read and
+    written, bf16 theta stored to N replicas (6N + 16 B)."""
     F, H, W = 4, 84, 84
     state = F * H * W
+    e = 2 if dtype == "bf16" else 4
+    upd = 22 if dtype == "bf16" else 20
     layers, c, h = [], F, H
     for (n, k, s) in net["convs"]:
         ho = (h - k) // s + 1
-        layers.append(dict(C=c, N=n, k=k, HoWo=ho * ho))
+        layers.append(dict(C=c, N=n, k=k, HoWo=ho * ho, in_elems=c * h * h))
         c, h = n, ho
     D, Hfc, A = c * h * h, net["fcs"][0], net["n_actions"]
     macs = lambda L: L["HoWo"] * L["N"] * L["C"] * L["k"] ** 2  # noqa: E731
     P = sum(L["N"] * (L["C"] * L["k"] ** 2 + 1) for L in layers) + Hfc * (D + 1) + A * (Hfc + 1)
+    conv_params = sum(L["N"] * (L["C"] * L["k"] ** 2 + 1) for L in layers)
     w = {}
     for i, L in enumerate(layers):
-        act_in = 4 * b * (state if i == 0 else layers[i - 1]["N"] * layers[i - 1]["HoWo"])
-        w[f"conv{i + 1}_fwd"] = (2 * 2 * b * macs(L), 2 * act_in + 2 * 4 * b * L["N"] * L["HoWo"])
-        w[f"conv{i + 1}_bwd"] = ((2 if i else 1) * 2 * b * macs(L), act_in + 4 * b * L["N"] * L["HoWo"])
-    w["fc1_fwd"] = (2 * 2 * b * D * Hfc, 2 * b * D * 4 + 2 * D * Hfc * 4 + 2 * b * Hfc * 4)
-    w["head_td"] = w["head_sample"] = (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 * 2)
-    w["fc1_bwd"] = (4 * b * D * Hfc, b * Hfc * 4 + b * D * 4 * 2 + D * Hfc * 4 * 3)
-    w["rmsprop_update"] = (0, P * 4 * 6)
-    conv_params = sum(L["N"] * (L["C"] * L["k"] ** 2 + 1) for L in layers)
-    w["reduce_update"] = (0, P * 4 * 6 + b * conv_params * 4)  # + the per-image conv partials
+        in_b = b * (state if i == 0 else L["in_elems"] * e)  # u8 slots for layer 1
+        out_b = b * L["N"] * L["HoWo"] * e
+        w[f"conv{i + 1}_fwd"] = (2 * 2 * b * macs(L), 2 * in_b + 2 * out_b)
+        w[f"conv{i + 1}_bwd"] = ((2 if i else 1) * 2 * b * macs(L), in_b + out_b + (in_b if i else 0))
+    w["fc1_fwd"] = (2 * 2 * b * D * Hfc, 2 * b * D * e + 2 * D * Hfc * e + 2 * b * Hfc * 4)
+    w["head_td"] = w["head_sample"] = (2 * 2 * b * Hfc * A, 2 * b * Hfc * 4 + 2 * A * (Hfc + 1) * 4)
+    w["fc1_bwd"] = (4 * b * D * Hfc, b * Hfc * e + 2 * b * D * e + D * Hfc * e + D * Hfc * 4)
+    w["rmsprop_update"] = (0, P * upd)
+    w["reduce_update"] = (0, conv_params * upd + b * conv_params * 4)  # + the per-image conv partials
     w["sample"] = (0, b * 4)
     shard = -(-P // (64 * world)) * 64
     w["server_round_fused"] = (0, shard * (6 * world + 16))
@@ -92,7 +98,12 @@ def region_work(name: str, b: int, net=MNIH, world: int = 1):
     w["conv_fwd"] = tuple(sum(w[f"conv{i + 1}_fwd"][q] for i in range(len(layers))) for q in range(2))
     w["conv_bwd"] = tuple(sum(w[f"conv{i + 1}_bwd"][q] for i in range(len(layers))) for q in range(2))
     w["fc1_bwd_head_finish"] = w["fc1_bwd"]
+    w["_P"] = (P, conv_params)
     return w.get(name, (0, 0))
+
+
+def param_count_of(net=MNIH) -> int:
+    return region_work("_P", 1, net)[0]
 
 
 REGION_KERNELS = {"conv_fwd": ["fwd_conv_bf16_kernel"], "fc1_fwd": ["tc_gemm_kernel"],
@@ -119,6 +130,61 @@ def region_traffic(name: str, dtype: str, net=MNIH):
         t = json.load(f)
     ks = [k for k in REGION_KERNELS[name] if k in t]  # the kernels of the region that ran in the capture
     return sum((t[k]["dram_read_MB"] + t[k]["dram_write_MB"]) * 1e6 for k in ks) if ks else None
+
+
+def roofline(regions, b, net, world, dtype, profile_steps):
+    """the dominant step region's algorithmic work over its measured mean duration (CUDA events
+    around it inside the replayed step graph), against BOTH the tensor and the HBM peak; `bound` / `frac`
+    are the binding one (the larger of flops / tensor peak and bytes / HBM peak). `step` is the same for the
+    whole step (every region's work over the sum of the region times)."""
+    pk = peaks()
+    P, conv_params = param_count_of(net), conv_param_count(net)
+    names = {r["name"] for r in regions}
+    # N = 1 bf16 Mnih path: the conv backward launch also runs the early RMSProp update of the non-conv
+    # parameters (22 B/param, DESIGN.md §6)
+    early = (dtype == "bf16" and world == 1 and "reduce_update" in names and b + 32 <= 148
+             and os.environ.get("DQN_EARLY_UPDATE", "1") != "0")
+
+    def work(name):
+        f, by = region_work(name, b, net, world, dtype)
+        if early and name == "conv_bwd":
+            by += (P - conv_params) * 22
+        return f, by
+
+    full = [r for r in regions if r["steps"] >= profile_steps // 2]
+    step_us = sum(r["avg_us"] for r in full)
+    top = max(regions, key=lambda r: r["avg_us"])
+    tpk = pk["bf16_sus"] if dtype == "bf16" else FP32_ALU_PEAK_TFLOPS
+    tunit_bound = "tensor" if dtype == "bf16" else "alu"
+
+    def fracs(f, by, us):
+        t = {"achieved": f / (us * 1e-6) / 1e12, "peak": tpk, "unit": "TFLOP/s"}
+        t["frac"] = t["achieved"] / t["peak"]
+        h = {"achieved": by / (us * 1e-6) / 1e9, "peak": pk["hbm"], "unit": "GB/s"}
+        h["frac"] = h["achieved"] / h["peak"]
+        return t, h
+
+    flops, byts = work(top["name"])
+    t, h = fracs(flops, byts, top["avg_us"])
+    bind_hbm = byts / (pk["hbm"] * 1e9) > flops / (tpk * 1e12)
+    roof = dict(h if bind_hbm else t)
+    roof["bound"] = "hbm" if bind_hbm else tunit_bound
+    roof["traffic"] = region_traffic(top["name"], dtype, dict(net, fcs=tuple(net["fcs"])))
+    roof.update(kernel=top["name"], avg_us=top["avg_us"], algorithmic_flops=flops, algorithmic_bytes=byts,
+                share_of_step=top["avg_us"] / step_us if step_us else None, tensor=t, hbm=h)
+    sf = sum(work(r["name"])[0] for r in full)
+    sb = sum(work(r["name"])[1] for r in full)
+    st, sh = fracs(sf, sb, step_us)
+    roof["step"] = {"us": step_us, "flops": sf, "bytes": sb, "tensor_frac": st["frac"], "hbm_frac": sh["frac"]}
+    roof["peak_source"] = (f"{pk['src']} MEASURED_PEAKS.json: bf16_tflops_sustained (tensor), hbm_gbs (hbm)"
+                           if dtype == "bf16" else "derived: 148 SMs x 128 FFMA lanes x 2 x 1.965 GHz (alu); "
+                           f"{pk['src']} MEASURED_PEAKS.json hbm_gbs (hbm)")
+    if top["name"] == "server_round_fused":
+        roof["note"] = ("the fused server round (N > 1) is bound by cross-GPU flag latency (two barriers, "
+                        "DESIGN.md §6a), not by its bytes")
+    elif early and top["name"] == "conv_bwd":
+        roof["note"] = "conv backward + the early RMSProp update of the non-conv parameters in one launch"
+    return roof
 
 
 class ClockSampler:
@@ -180,8 +246,35 @@ def dist_setup():
     return world, rank, local
 
 
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _oracle_rate(O, net, rp, theta0, b, budget_s):
+    """transitions/s of the oracle's replica step (O.run: sample, targets with theta^, gradient, RMSProp) on a
+    bounded sample: as many steps of minibatch b as fit the time budget."""
+    cfg = O.TrainCfg(minibatch=b, target_sync=1000)
+    t0 = time.perf_counter()
+    O.run(net, cfg, len(rp.a), [rp], theta0, 1)
+    one = time.perf_counter() - t0
+    steps = max(1, int(budget_s / max(one, 1e-3)))
+    t0 = time.perf_counter()
+    O.run(net, cfg, len(rp.a), [rp], theta0, steps)
+    dt = time.perf_counter() - t0
+    return steps * b / dt, steps, dt
+
+
 def cpu_baseline(budget_s: float = 15.0, b: int = 32):
-    """The oracle as it stands (single-threaded fp64), on a bounded sample of the workload."""
+    """The oracle as it stands (fp64; per-sample gradient terms on all host cores with OpenMP, summed in sample
+    order), on a bounded sample of the workload; plus the same on one thread."""
     import numpy as np
 
     import synth
@@ -191,20 +284,22 @@ def cpu_baseline(budget_s: float = 15.0, b: int = 32):
     s, a, r, sn, t = synth.g_pong(1000, 4, 84, 84, 6, 0x5EED)
     rp = O.Replay(s, a, r.astype(np.float64), sn, t)
     theta0 = synth.init_theta(O.tensor_table(net), [0.01] * 8, 7).astype(np.float64)
-    cfg = O.TrainCfg(minibatch=b, target_sync=1000)
-    t0 = time.perf_counter()
-    O.run(net, cfg, 1000, [rp], theta0, 1)
-    one = time.perf_counter() - t0
-    steps = max(1, int(budget_s / max(one, 1e-3)))
-    t0 = time.perf_counter()
-    O.run(net, cfg, 1000, [rp], theta0, steps)
-    dt = time.perf_counter() - t0
-    return {"value": steps * b / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{steps} replica steps of b={b} (Mnih net, replay 1k G-pong instead of 1M), fp64 single thread"}
+    n0 = O.threads()
+    O.set_threads(0)
+    cores = O.threads()
+    v, steps, dt = _oracle_rate(O, net, rp, theta0, b, budget_s)
+    O.set_threads(1)
+    v1, steps1, _ = _oracle_rate(O, net, rp, theta0, b, budget_s / 3)
+    O.set_threads(n0)
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(),
+            "sample": f"{steps} replica steps of b={b} (Mnih net, replay 1k G-pong instead of 1M), fp64, "
+                      f"{cores} OpenMP threads over the minibatch samples",
+            "single_thread": {"value": v1, "cores": 1, "sample": f"{steps1} replica steps, 1 thread"}}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the fp64 oracle timed on the host cores (rank 0 only)."""
+    """--impl reference: the fp64 oracle timed on the host cores (rank 0 only), all cores."""
     if rank != 0:
         return
     import numpy as np
@@ -217,10 +312,12 @@ def run_reference(args, world, rank):
     s, a, r, sn, t = synth.g_pong(1000, 4, 84, 84, 6, 0x5EED)
     rp = O.Replay(s, a, r.astype(np.float64), sn, t)
     theta0 = synth.init_theta(O.tensor_table(net), [0.01] * 8, 7).astype(np.float64)
+    O.set_threads(0)
+    cores = O.threads()
     # each step: a bounded sample of the replica step (b_s of the 32 transitions) so K + W steps take ~2 min
     t0 = time.perf_counter()
-    O.run(net, O.TrainCfg(minibatch=1, target_sync=1000), 1000, [rp], theta0, 1)
-    per_tr = time.perf_counter() - t0
+    O.run(net, O.TrainCfg(minibatch=min(16, b_full), target_sync=1000), 1000, [rp], theta0, 1)
+    per_tr = (time.perf_counter() - t0) / min(16, b_full)
     total = max(1, args.steps + args.warmup)
     b_s = int(max(1, min(b_full, 120.0 / (per_tr * total))))
     cfg = O.TrainCfg(minibatch=b_s, target_sync=1000)
@@ -230,13 +327,14 @@ def run_reference(args, world, rank):
     dt = time.perf_counter() - t0
     v = args.steps * b_s / dt
     sample = (f"{args.steps} oracle replica steps of b={b_s} (of b={b_full}), Mnih net, replay 1k G-pong "
-              f"(of 1M), fp64 single thread")
+              f"(of 1M), fp64, {cores} OpenMP threads over the minibatch samples")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "BASELINE.json configs[1]" if world == 1 else "BASELINE.json configs[2]",
                        "minibatch": b_full, "replay": 1_000_000, "net": "Mnih-2013"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -421,44 +519,7 @@ def main():
 
     # ---- per-region device times (CUDA events inside the replayed step graph)
     regions = dqn.profile(args.profile_steps) if args.profile_steps > 0 else []
-    pk = peaks()
-    roof = None
-    if regions:
-        step_us = sum(r["avg_us"] for r in regions if r["steps"] >= args.profile_steps // 2)
-        top = max(regions, key=lambda r: r["avg_us"])
-        flops, byts = region_work(top["name"], b, net, world)
-        names = {r["name"] for r in regions}
-        # N = 1 bf16 Mnih path: the conv backward launch also runs the early RMSProp update of the non-conv
-        # parameters (26 B/param — read theta, r, G; write theta, r, G = 0, bf16 theta)
-        early = (top["name"] == "conv_bwd" and dtype == "bf16" and world == 1 and "reduce_update" in names
-                 and b + 32 <= 148 and os.environ.get("DQN_EARLY_UPDATE", "1") != "0")
-        if early:
-            byts += (region_work("rmsprop_update", b, net)[1] // 24 - conv_param_count(net)) * 26
-        if early and byts / (pk["hbm"] * 1e9) > flops / (pk["bf16_sus"] * 1e12):  # the binding roofline
-            roof = {"bound": "hbm", "achieved": byts / (top["avg_us"] * 1e-6) / 1e9, "peak": pk["hbm"],
-                    "unit": "GB/s", "algorithmic_bytes": byts, "algorithmic_flops": flops,
-                    "note": "conv backward + early update in one launch: its HBM time (bytes / peak) exceeds its "
-                            "tensor time (flops / peak), so HBM is the binding roofline"}
-        elif dtype == "bf16" and flops:
-            roof = {"bound": "tensor", "achieved": flops / (top["avg_us"] * 1e-6) / 1e12, "peak": pk["bf16_sus"],
-                    "unit": "TFLOP/s"}
-        elif flops:
-            roof = {"bound": "alu", "achieved": flops / (top["avg_us"] * 1e-6) / 1e12,
-                    "peak": FP32_ALU_PEAK_TFLOPS, "unit": "TFLOP/s"}
-        else:
-            roof = {"bound": "hbm", "achieved": byts / (top["avg_us"] * 1e-6) / 1e9, "peak": pk["hbm"],
-                    "unit": "GB/s"}
-        if top["name"] == "server_round_fused":
-            roof["note"] = ("the fused server round (N > 1) is bound by cross-GPU flag latency (two barriers, "
-                            "DESIGN.md §6a), not by its bytes; achieved = its algorithmic bytes / its region time")
-        roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = region_traffic(top["name"], dtype, dict(net, fcs=tuple(net["fcs"])))
-        roof["kernel"] = top["name"]
-        roof["avg_us"] = top["avg_us"]
-        roof["share_of_step"] = top["avg_us"] / step_us if step_us else None
-        roof["peak_source"] = (pk["src"] + " MEASURED_PEAKS.json bf16_tflops_sustained" if roof["bound"] == "tensor"
-                               else "derived: 148 SMs x 128 FFMA lanes x 2 x 1.965 GHz" if roof["bound"] == "alu"
-                               else pk["src"] + " MEASURED_PEAKS.json hbm_gbs")
+    roof = roofline(regions, b, net, world, dtype, args.profile_steps) if regions else None
 
     if rank != 0:
         dqn.close()
@@ -479,7 +540,7 @@ def main():
                    "replay_per_replica": args.replay, "replay_dedup": bool(args.dedup),
                    "target_sync_C": C["C"] if C["C"] < 2**40 else None,
                    "n_push": C["n_push"], "n_fetch": C["n_fetch"],
-                   "sync_mode": "async (lag-1 fetch)" if C["async"] else "deterministic",
+                   "sync_mode": "async (a fetch takes the newest published generation)" if C["async"] else "deterministic",
                    "parallelism": f"dp{world} + sharded parameter server", "gamma": 0.99,
                    "l2": f"inputs larger than L2: each step gathers {b} random s and s' slots of a "
                          f"{args.replay * 56454 / 1e9:.1f} GB replay from HBM (bf16 path: the step's forward "

@@ -48,9 +48,13 @@ enum { DQN_FP32 = 0,   /* fp32 SIMT kernels; parity <= 1e-5 vs the fp64 oracle  
        DQN_BF16 = 1 }; /* bf16 operands on tcgen05 tensor cores, fp32 accumulate; <= 2e-2 */
 /* push / fetch schedule (DESIGN.md §2 a11-a13) */
 enum { DQN_DETERMINISTIC = 0, /* lock-step: a fetch returns the current server theta                    */
-       DQN_ASYNC = 1 };       /* the server round (push, RMSProp, publish) overlaps the next steps on a
-                                 second stream; a fetch returns the server theta of one round earlier
-                                 (lag 1, the deterministic twin of Downpour's staleness, O13 / A32)   */
+       DQN_ASYNC = 1,         /* Downpour's asynchrony: the server round (push, RMSProp,
+                                 publish) runs on a second stream while the replica keeps stepping; a
+                                 fetch never waits - it takes the newest generation the server has
+                                 published (a device generation flag), so the staleness n_apply - n_base
+                                 is whatever the timing makes it (staleness_hist, step_generation)    */
+       DQN_ASYNC_LAG1 = 2 };  /* its deterministic twin (O13 / A32): the same streams, but a fetch returns
+                                 exactly the server theta of one round earlier (waits for it)         */
 /* how a push round combines the N workers' gradients (Alg. 2)
  *   MEAN         : one RMSProp application of the mean of the N*n_push gradients, n += 1 (A7)
  *   PER_GRADIENT : Alg. 2 literally - each worker's gradient (mean of its n_push) applied in turn
@@ -66,7 +70,10 @@ enum {
   DQN_PARAMS_GRAD = 3,   /* the gradient this replica pushed in its last push round: sum over its
                             n_push steps of Delta theta (A8), before the mean; needs
                             cfg.keep_grad = 1 (DQN_EINVAL otherwise); diagnostic                   */
-  DQN_PARAMS_RMS = 4     /* RMSProp accumulator r of Alg. 2 (gathered: collective)                 */
+  DQN_PARAMS_RMS = 4,    /* RMSProp accumulator r of Alg. 2 (gathered: collective)                 */
+  DQN_PARAMS_LOCAL_BF16 = 5,  /* DQN_BF16: the bf16 working copy of theta the tensor cores read,
+                                 widened to fp32 (exact); diagnostic (DQN_EINVAL on DQN_FP32)       */
+  DQN_PARAMS_TARGET_BF16 = 6  /* DQN_BF16: the bf16 working copy of theta^, widened; diagnostic     */
 };
 
 /* Problem statement (P:59-67 network, P:87 C, P:99 N, P:121 gamma, P:123 b,
@@ -119,8 +126,11 @@ typedef struct {
   float* loss_per_step;      /* [k]                                                                  */
   /* output */
   int64_t kernel_launches;   /* kernels of this library launched by the call (graph kernel nodes)     */
-  int64_t staleness_hist[32];/* DQN_ASYNC: replica steps by staleness n_apply - n_local (A25), since create;
+  int64_t staleness_hist[32];/* DQN_ASYNC*: replica steps by staleness n_apply - n_local (A25), since create;
                                 bucket 31 collects >= 31. All zero in the deterministic mode.          */
+  /* optional caller-owned HOST output (NULL = not wanted); valid when k <= 4096 */
+  int64_t* step_generation;  /* [k] generation n_local of the theta each step of the call used: the
+                                realised fetch schedule (A40; in DQN_ASYNC it depends on timing)       */
 } dqn_step_stats;
 
 /* Per-region device time of the replica step (diagnostic; dqn_profile_steps). */
@@ -181,7 +191,7 @@ int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats);
  * dqn_push_transitions(1 item) + dqn_train_steps(1), with one host synchronisation
  * at the end instead of one per iteration. stats as dqn_train_steps (loss_per_step
  * receives the k losses). Errors: as dqn_push_transitions (validated before anything
- * runs) and dqn_train_steps; DQN_EINVAL in DQN_ASYNC mode. */
+ * runs) and dqn_train_steps; DQN_EINVAL in the DQN_ASYNC* modes. */
 int dqn_store_and_train(dqn_ctx* ctx, int64_t k, const uint8_t* s, const int32_t* a, const float* r,
                         const uint8_t* s_next, const uint8_t* terminal, dqn_step_stats* stats);
 

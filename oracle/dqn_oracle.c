@@ -17,6 +17,25 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* threads the per-sample loops may use (1 without OpenMP); or_set_threads(n <= 0): all host cores */
+int32_t or_threads(void) {
+#ifdef _OPENMP
+  return (int32_t)omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+void or_set_threads(int32_t n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+#else
+  (void)n;
+#endif
+}
 
 /* ------------------------------------------------------------------ shapes */
 /* Valid convolution, no padding: out = (in - k)/s + 1 must be a positive
@@ -218,6 +237,7 @@ static int32_t argmax_lowest(const double* q, int n) {
 void or_q_values(const or_net* net, const double* theta, int64_t n, const uint8_t* states, double* q,
                  int32_t* argmax) {
   int64_t sz = (int64_t)net->frames * net->height * net->width;
+#pragma omp parallel for schedule(static, 1)
   for (int64_t i = 0; i < n; ++i) {
     or_forward_u8(net, theta, states + i * sz, q + i * net->n_actions);
     if (argmax) argmax[i] = argmax_lowest(q + i * net->n_actions, net->n_actions);
@@ -253,94 +273,119 @@ double or_min_abs_preact(const or_net* net, const double* theta, int64_t n, cons
 void or_targets(const or_net* net, const double* theta_hat, int b, const uint8_t* s_next, const double* r,
                 const uint8_t* term, double gamma, double* y, int32_t* argmax_next) {
   int64_t sz = (int64_t)net->frames * net->height * net->width;
-  double* q = (double*)malloc(sizeof(double) * net->n_actions);
+#pragma omp parallel for schedule(static, 1)
   for (int j = 0; j < b; ++j) {
+    double* q = (double*)malloc(sizeof(double) * net->n_actions);
     or_forward_u8(net, theta_hat, s_next + j * sz, q);
     double m = q[0];
     for (int a = 1; a < net->n_actions; ++a)
       if (q[a] > m) m = q[a];
     if (argmax_next) argmax_next[j] = argmax_lowest(q, net->n_actions);
     y[j] = term[j] ? r[j] : r[j] + gamma * m;
+    free(q);
   }
-  free(q);
 }
 
-/* Delta theta = (1/b) sum_i grad_theta 1/2 (Q(phi_i, a_i; theta) - y_i)^2.
+/* Delta theta = (1/b) sum_i grad_theta 1/2 (Q(phi_i, a_i; theta) - y_i)^2, written as that sum:
+ * sample j's term g_j is computed on its own (sample_grad), then the terms are added in the order j = 0..b-1.
  * dL/dQ_{j,a} = clamp(delta_j, -c, c)/b for a = a_j, else 0; y is a constant (A2, A3).
- * Backprop through ReLU with ReLU'(0) = 0 (A17). Samples accumulate in order j = 0..b-1. */
+ * Backprop through ReLU with ReLU'(0) = 0 (A17).
+ * The per-sample terms of a block of OR_BLOCK samples may be computed by several threads (OpenMP, when the
+ * library is built with it); the sum is always taken in sample order, so the result does not depend on the
+ * thread count (bench.py's all-core cpu_baseline). */
+#define OR_BLOCK 16
+
+static double sample_grad(const shape_t* sh, const or_net* net, const double* theta, const double* xj, int32_t aj,
+                          double yj, double err_clip, int b, double* grad /* zeroed, P */) {
+  int L = sh->n_layers;
+  double** z = alloc_acts(sh);
+  double** dz = alloc_acts(sh);
+  double* act_in = NULL;
+  forward_store(sh, theta, xj, z);
+  double q = z[L - 1][aj];
+  double delta = q - yj;
+  double dclip = delta;
+  if (err_clip > 0.0) {
+    if (dclip > err_clip) dclip = err_clip;
+    if (dclip < -err_clip) dclip = -err_clip;
+  }
+  /* output layer: only the taken action's unit receives error */
+  for (int i = 0; i < net->n_actions; ++i) dz[L - 1][i] = 0.0;
+  dz[L - 1][aj] = dclip / (double)b;
+  for (int l = L - 1; l >= 0; --l) {
+    /* input activation of layer l */
+    int64_t n_in = (int64_t)sh->in_c[l] * sh->in_h[l] * sh->in_w[l];
+    free(act_in);
+    act_in = (double*)malloc(sizeof(double) * n_in);
+    if (l == 0) memcpy(act_in, xj, sizeof(double) * n_in);
+    else for (int64_t i = 0; i < n_in; ++i) act_in[i] = relu(z[l - 1][i]);
+    double* gw = grad + sh->w_off[l];
+    double* gb = grad + sh->b_off[l];
+    const double* w = theta + sh->w_off[l];
+    double* dprev = (l > 0) ? dz[l - 1] : NULL; /* becomes d(pre-activation) of layer l-1 */
+    if (dprev) for (int64_t i = 0; i < n_in; ++i) dprev[i] = 0.0;
+    if (sh->kind[l] == 0) {
+      int C = sh->in_c[l], H = sh->in_h[l], W = sh->in_w[l], N = sh->out_c[l], k = sh->k[l], s = sh->s[l];
+      int Ho = sh->out_h[l], Wo = sh->out_w[l];
+      for (int n = 0; n < N; ++n)
+        for (int oy = 0; oy < Ho; ++oy)
+          for (int ox = 0; ox < Wo; ++ox) {
+            double g = dz[l][((int64_t)n * Ho + oy) * Wo + ox];
+            gb[n] += g;
+            for (int c = 0; c < C; ++c)
+              for (int ky = 0; ky < k; ++ky)
+                for (int kx = 0; kx < k; ++kx) {
+                  int64_t wi = (((int64_t)n * C + c) * k + ky) * k + kx;
+                  int64_t xi = ((int64_t)c * H + (oy * s + ky)) * W + (ox * s + kx);
+                  gw[wi] += g * act_in[xi];
+                  if (dprev) dprev[xi] += g * w[wi];
+                }
+          }
+    } else {
+      int D = sh->in_c[l], Hh = sh->out_c[l];
+      for (int h = 0; h < Hh; ++h) {
+        double g = dz[l][h];
+        gb[h] += g;
+        for (int d = 0; d < D; ++d) {
+          gw[(int64_t)h * D + d] += g * act_in[d];
+          if (dprev) dprev[d] += g * w[(int64_t)h * D + d];
+        }
+      }
+    }
+    /* through the ReLU of layer l-1: d z_{l-1} = d a_{l-1} * [z_{l-1} > 0] */
+    if (dprev)
+      for (int64_t i = 0; i < n_in; ++i) dprev[i] = (z[l - 1][i] > 0.0) ? dprev[i] : 0.0;
+  }
+  free(act_in);
+  free_acts(sh, z);
+  free_acts(sh, dz);
+  return 0.5 * delta * delta;
+}
+
 double or_loss_grad_x(const or_net* net, const double* theta, int b, const double* x, const int32_t* a,
                       const double* y, double err_clip, double* grad) {
   shape_t sh;
   if (build_shapes(net, &sh)) return NAN;
   memset(grad, 0, sizeof(double) * sh.P);
   int64_t sz = (int64_t)net->frames * net->height * net->width;
-  double** z = alloc_acts(&sh);
-  double** dz = alloc_acts(&sh);
-  int L = sh.n_layers;
+  double* gj = (double*)malloc(sizeof(double) * sh.P * OR_BLOCK);
+  double lj[OR_BLOCK];
   double loss = 0.0;
-  double* act_in = NULL;
-  for (int j = 0; j < b; ++j) {
-    const double* xj = x + j * sz;
-    forward_store(&sh, theta, xj, z);
-    double q = z[L - 1][a[j]];
-    double delta = q - y[j];
-    loss += 0.5 * delta * delta;
-    double dclip = delta;
-    if (err_clip > 0.0) {
-      if (dclip > err_clip) dclip = err_clip;
-      if (dclip < -err_clip) dclip = -err_clip;
+  for (int j0 = 0; j0 < b; j0 += OR_BLOCK) {
+    const int nb = b - j0 < OR_BLOCK ? b - j0 : OR_BLOCK;
+#pragma omp parallel for schedule(static, 1)
+    for (int q = 0; q < nb; ++q) {
+      memset(gj + (int64_t)q * sh.P, 0, sizeof(double) * sh.P);
+      lj[q] = sample_grad(&sh, net, theta, x + (int64_t)(j0 + q) * sz, a[j0 + q], y[j0 + q], err_clip, b,
+                          gj + (int64_t)q * sh.P);
     }
-    /* output layer: only the taken action's unit receives error */
-    for (int i = 0; i < net->n_actions; ++i) dz[L - 1][i] = 0.0;
-    dz[L - 1][a[j]] = dclip / (double)b;
-    for (int l = L - 1; l >= 0; --l) {
-      /* input activation of layer l */
-      int64_t n_in = (int64_t)sh.in_c[l] * sh.in_h[l] * sh.in_w[l];
-      free(act_in);
-      act_in = (double*)malloc(sizeof(double) * n_in);
-      if (l == 0) memcpy(act_in, xj, sizeof(double) * n_in);
-      else for (int64_t i = 0; i < n_in; ++i) act_in[i] = relu(z[l - 1][i]);
-      double* gw = grad + sh.w_off[l];
-      double* gb = grad + sh.b_off[l];
-      const double* w = theta + sh.w_off[l];
-      double* dprev = (l > 0) ? dz[l - 1] : NULL; /* becomes d(pre-activation) of layer l-1 */
-      if (dprev) for (int64_t i = 0; i < n_in; ++i) dprev[i] = 0.0;
-      if (sh.kind[l] == 0) {
-        int C = sh.in_c[l], H = sh.in_h[l], W = sh.in_w[l], N = sh.out_c[l], k = sh.k[l], s = sh.s[l];
-        int Ho = sh.out_h[l], Wo = sh.out_w[l];
-        for (int n = 0; n < N; ++n)
-          for (int oy = 0; oy < Ho; ++oy)
-            for (int ox = 0; ox < Wo; ++ox) {
-              double g = dz[l][((int64_t)n * Ho + oy) * Wo + ox];
-              gb[n] += g;
-              for (int c = 0; c < C; ++c)
-                for (int ky = 0; ky < k; ++ky)
-                  for (int kx = 0; kx < k; ++kx) {
-                    int64_t wi = (((int64_t)n * C + c) * k + ky) * k + kx;
-                    int64_t xi = ((int64_t)c * H + (oy * s + ky)) * W + (ox * s + kx);
-                    gw[wi] += g * act_in[xi];
-                    if (dprev) dprev[xi] += g * w[wi];
-                  }
-            }
-      } else {
-        int D = sh.in_c[l], Hh = sh.out_c[l];
-        for (int h = 0; h < Hh; ++h) {
-          double g = dz[l][h];
-          gb[h] += g;
-          for (int d = 0; d < D; ++d) {
-            gw[(int64_t)h * D + d] += g * act_in[d];
-            if (dprev) dprev[d] += g * w[(int64_t)h * D + d];
-          }
-        }
-      }
-      /* through the ReLU of layer l-1: d z_{l-1} = d a_{l-1} * [z_{l-1} > 0] */
-      if (dprev)
-        for (int64_t i = 0; i < n_in; ++i) dprev[i] = (z[l - 1][i] > 0.0) ? dprev[i] : 0.0;
+    for (int q = 0; q < nb; ++q) { /* sample order */
+      loss += lj[q];
+      const double* g = gj + (int64_t)q * sh.P;
+      for (int64_t i = 0; i < sh.P; ++i) grad[i] += g[i];
     }
   }
-  free(act_in);
-  free_acts(&sh, z);
-  free_acts(&sh, dz);
+  free(gj);
   return loss / (double)b;
 }
 
@@ -429,9 +474,12 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
   }
   double* g = (double*)malloc(sizeof(double) * P);
   double* gbar = (double*)malloc(sizeof(double) * P);
-  /* O13: the server's last L+1 published states; a fetch returns theta^(max(n - L, 0)) */
+  /* O13: the server's last published states; a fetch returns theta^(max(n - L, 0)), or the generation the
+     realised asynchronous schedule gives it (cfg->fetch_gen, A40) */
   const int L = cfg->fetch_lag > 0 ? cfg->fetch_lag : 0;
-  double* hist = (double*)malloc(sizeof(double) * P * (L + 1));
+  const int64_t depth = cfg->fetch_gen ? 8 : L + 1;
+  const int64_t n_fetches = (steps + cfg->n_fetch - 1) / cfg->n_fetch;
+  double* hist = (double*)malloc(sizeof(double) * P * depth);
   memcpy(hist, theta0, sizeof(double) * P);
   int64_t* pend = (int64_t*)calloc((size_t)N * cfg->n_push, sizeof(int64_t)); /* n_local per step of the round */
   if (stale_hist) memset(stale_hist, 0, sizeof(int64_t) * 32);
@@ -448,8 +496,12 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
     for (int k = 0; k < N; ++k) {
       /* O10 "Fetch model theta and iteration number n from server", every n_fetch steps (A9) */
       if (T % cfg->n_fetch == 0) {
-        const int64_t m = n - L > 0 ? n - L : 0; /* L = 0: the current server theta */
-        memcpy(th_local[k], hist + (m % (L + 1)) * P, sizeof(double) * P);
+        int64_t m = n - L > 0 ? n - L : 0; /* L = 0: the current server theta */
+        if (cfg->fetch_gen) {
+          m = cfg->fetch_gen[(int64_t)k * n_fetches + T / cfg->n_fetch];
+          if (m > n || n - m >= depth || m < 0) { rc = -4; goto out_all; } /* not a published generation */
+        }
+        memcpy(th_local[k], hist + (m % depth) * P, sizeof(double) * P);
         n_local[k] = m;
         /* O11 target refresh every C generations (A10) */
         if (n_local[k] - ell[k] >= cfg->target_sync) {
@@ -494,7 +546,7 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
           or_rmsprop(theta + i, rms + i, gbar + i, 1, cfg->lr, cfg->rms_decay, cfg->rms_eps);
         }
         n += 1;
-        memcpy(hist + (n % (L + 1)) * P, theta, sizeof(double) * P);
+        memcpy(hist + (n % depth) * P, theta, sizeof(double) * P);
       }
       for (int k = 0; k < N; ++k) memset(acc[k], 0, sizeof(double) * P);
     } else if ((T + 1) % cfg->n_push == 0) {
@@ -515,10 +567,11 @@ int or_run(const or_net* net, const or_train_cfg* cfg, int64_t capacity, const i
           stale_hist[s < 31 ? s : 31] += 1;
         }
       n += 1; /* A22 */
-      memcpy(hist + (n % (L + 1)) * P, theta, sizeof(double) * P);
+      memcpy(hist + (n % depth) * P, theta, sizeof(double) * P);
       for (int k = 0; k < N; ++k) memset(acc[k], 0, sizeof(double) * P);
     }
   }
+out_all:
   if (theta_out) memcpy(theta_out, theta, sizeof(double) * P);
   if (r_out) memcpy(r_out, rms, sizeof(double) * P);
   if (n_out) *n_out = n;

@@ -44,6 +44,9 @@ typedef struct {
   int32_t server_rule;     /* 0: mean of the round's N gradients, one RMSProp, n += 1 (A7);
                               1: Alg. 2 literally - each worker's gradient applied in turn (rank order),
                               one RMSProp and n += 1 per gradient (A33) */
+  const int64_t* fetch_gen;  /* NULL, or the generation every fetch returns, [N][ceil(steps / n_fetch)] (fetch f
+                                of replica k is at step f * n_fetch): the realised schedule of an asynchronous
+                                run (O13, A40). Each entry must be a published generation, n - 7 <= m <= n */
 } or_train_cfg;
 
 /* ---- shapes (O0) ---- */
@@ -127,6 +130,11 @@ int or_eps_greedy(uint64_t seed, uint32_t env, uint64_t t, uint64_t eps_thr, int
 void or_collect(int n, int F, int H, int E, int64_t steps, uint64_t seed, uint64_t eps_thr, const int32_t* greedy,
                 int init, or_snake* games, uint8_t* stacks, uint64_t t0, int32_t* a_log, double* r_log,
                 uint8_t* t_log, int64_t* episodes);
+
+/* threads of the per-sample loops (OpenMP build; 1 otherwise). The results never depend on it: per-sample
+ * gradient terms are summed in sample order (or_loss_grad_x). n <= 0: all host cores. */
+int32_t or_threads(void);
+void or_set_threads(int32_t n);
 
 #ifdef __cplusplus
 }

@@ -29,7 +29,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
         os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "dqn_oracle.h"))
     ):
-        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-shared", "-fPIC",
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fopenmp", "-shared", "-fPIC",
                "-o", _LIB_PATH + ".tmp", _SRC, "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB_PATH + ".tmp", _LIB_PATH)
@@ -47,7 +47,8 @@ class _Cfg(C.Structure):
     _fields_ = [("n_replicas", C.c_int32), ("minibatch", C.c_int32), ("n_push", C.c_int32),
                 ("n_fetch", C.c_int32), ("target_sync", C.c_int64), ("gamma", C.c_double),
                 ("lr", C.c_double), ("rms_decay", C.c_double), ("rms_eps", C.c_double),
-                ("err_clip", C.c_double), ("seed", C.c_uint64), ("fetch_lag", C.c_int32), ("server_rule", C.c_int32)]
+                ("err_clip", C.c_double), ("seed", C.c_uint64), ("fetch_lag", C.c_int32), ("server_rule", C.c_int32),
+                ("fetch_gen", C.c_void_p)]
 
 
 @dataclass
@@ -96,11 +97,16 @@ class TrainCfg:
     seed: int = 0xD15EA5E
     fetch_lag: int = 0   # O13 / A32: a fetch returns theta as it was `fetch_lag` rounds ago
     server_rule: int = 0  # 0: mean per round (A7); 1: Alg. 2 literally, one update per gradient (A33)
+    fetch_gen: Optional[np.ndarray] = None  # [N][n_fetches] generation of every fetch (realised async schedule, A40)
 
     def c(self) -> _Cfg:
         c = _Cfg()
         for f, _ in _Cfg._fields_:
-            setattr(c, f, getattr(self, f))
+            if f != "fetch_gen":
+                setattr(c, f, getattr(self, f))
+        if self.fetch_gen is not None:
+            c._keep = np.ascontiguousarray(self.fetch_gen, np.int64)  # alive as long as the struct
+            c.fetch_gen = c._keep.ctypes.data
         return c
 
 
@@ -115,6 +121,8 @@ def lib():
         U8 = C.POINTER(C.c_uint8)
         I32 = C.POINTER(C.c_int32)
         I64 = C.POINTER(C.c_int64)
+        _lib.or_threads.restype = C.c_int32
+        _lib.or_set_threads.argtypes = [C.c_int32]
         _lib.or_param_count.restype = C.c_int64
         _lib.or_param_count.argtypes = [C.POINTER(_Net)]
         _lib.or_tensor_table.restype = C.c_int32
@@ -205,6 +213,16 @@ def _p(a: np.ndarray, ct):
 
 def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def threads() -> int:
+    """Threads the oracle's per-sample loops use (its results do not depend on it)."""
+    return int(lib().or_threads())
+
+
+def set_threads(n: int) -> None:
+    """n <= 0: all host cores."""
+    lib().or_set_threads(n)
 
 
 def param_count(net: Net) -> int:

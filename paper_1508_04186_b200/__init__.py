@@ -22,9 +22,10 @@ LIB_PATH = os.path.join(_PKG, "libdqn.so")
 
 OK, EINVAL, EEMPTY, ENONFINITE, ENOMEM, ECUDA, ENCCL, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
 FP32, BF16 = 0, 1
-DETERMINISTIC, ASYNC = 0, 1
+DETERMINISTIC, ASYNC, ASYNC_LAG1 = 0, 1, 2
 SERVER_MEAN, SERVER_PER_GRADIENT = 0, 1
 PARAMS_SERVER, PARAMS_LOCAL, PARAMS_TARGET, PARAMS_GRAD, PARAMS_RMS = 0, 1, 2, 3, 4
+PARAMS_LOCAL_BF16, PARAMS_TARGET_BF16 = 5, 6  # bf16 working copies widened to fp32 (diagnostic)
 _NAMES = {0: "OK", -1: "EINVAL", -2: "EEMPTY", -3: "ENONFINITE", -4: "ENOMEM", -5: "ECUDA", -6: "ENCCL",
           -7: "ESTATE"}
 
@@ -51,7 +52,7 @@ class _Stats(C.Structure):
     _fields_ = [("loss_mean", C.c_double), ("generation", C.c_int64), ("steps_done", C.c_int64),
                 ("device_ms", C.c_float), ("nonfinite_elems", C.c_int64), ("sampled_idx", C.c_void_p),
                 ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p), ("kernel_launches", C.c_int64),
-                ("staleness_hist", C.c_int64 * 32)]
+                ("staleness_hist", C.c_int64 * 32), ("step_generation", C.c_void_p)]
 
 
 class _CollectStats(C.Structure):
@@ -230,7 +231,7 @@ class DQN:
         self._check(lib().dqn_push_transitions(self._h, n, ps, pa, pr, pn, pt))
 
     def train(self, k: int, want_idx: bool = False, want_argmax: bool = False, want_loss: bool = False,
-              store=None) -> dict:
+              store=None, want_generation: bool = False) -> dict:
         """k replica steps (dqn_train_steps); with store = (s, a, r, s_next, term) of k transitions, Alg. 1's
         loop instead: transition i is stored, then step i runs (dqn_store_and_train)."""
         st = _Stats()
@@ -238,6 +239,8 @@ class DQN:
         idx = np.zeros((k, b), np.int32) if want_idx else None
         am = np.zeros((k, b), np.int32) if want_argmax else None
         lp = np.zeros(k, np.float32) if want_loss else None
+        sg = np.zeros(k, np.int64) if want_generation else None
+        st.step_generation = sg.ctypes.data if sg is not None else None
         st.sampled_idx = idx.ctypes.data if idx is not None else None
         st.target_argmax = am.ctypes.data if am is not None else None
         st.loss_per_step = lp.ctypes.data if lp is not None else None
@@ -255,7 +258,8 @@ class DQN:
             rc = lib().dqn_store_and_train(self._h, k, ps, pa, pr, pn, pt, C.byref(st))
         out = dict(loss_mean=st.loss_mean, generation=st.generation, steps_done=st.steps_done,
                    device_ms=st.device_ms, nonfinite_elems=st.nonfinite_elems, idx=idx, argmax=am, loss=lp,
-                   kernel_launches=st.kernel_launches, staleness=np.array(st.staleness_hist[:], np.int64), rc=rc)
+                   kernel_launches=st.kernel_launches, staleness=np.array(st.staleness_hist[:], np.int64), rc=rc,
+                   step_generation=sg)
         self._check(rc)
         return out
 

@@ -129,6 +129,7 @@ void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, fl
                     long long w1_off = 0, long long w2_off = 0, float* g_snap = nullptr);
 void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st, long long img_off = -1,
                         long long w1_off = 0, long long w2_off = 0);
+void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, long long n, cudaStream_t st);
 
 // fp32 SIMT path (kernels_f32.cu)
 void init_f32_kernel_attrs();
@@ -193,6 +194,44 @@ struct FusedAcquire {
   float* g_snap;                                // cfg.keep_grad: G copied here before it is cleared (or nullptr)
 };
 void launch_fused_round_acquire(const FusedAcquire& f, cudaStream_t st);
+// DQN_ASYNC / DQN_ASYNC_LAG1: device state of the asynchronous schedule
+struct AsyncDev {
+  unsigned long long pub_gen;      // newest generation the comm stream has published (release store)
+  long long n_local, ell;          // generation of the working theta / of theta^ (Alg. 1 state line)
+  long long fetch_gen;             // the generation the pending fetch copies
+  int do_refresh, pad;
+  long long hist[32];              // A25: replica steps by staleness n_apply - n_base (31: >= 31)
+  long long fgen_log[kDiagSteps];  // generation taken by fetch f, at f % kDiagSteps
+};
+struct AsyncCopy {
+  const float* pub[3];             // published server theta by generation % 3 (fp32, canonical)
+  const __nv_bfloat16* pubb[3];    // and its bf16 working image (nullptr on the fp32 path)
+  float* th;                       // theta_local
+  __nv_bfloat16* thb;
+  float* hat;                      // theta^ (copied too when the fetch refreshes, A10)
+  __nv_bfloat16* hatb;
+  long long n32, n16;              // fp32 / bf16 elements
+};
+// fetch f: pick the generation (forced >= 0: that one, the lag-1 twin; else the newest published), decide
+// the refresh (n - l >= C), log it; then copy it into the working buffers
+void launch_async_pick(AsyncDev* d, long long forced, long long C, long long f, cudaStream_t st);
+void launch_async_copy(const AsyncDev* d, const AsyncCopy& c, cudaStream_t st);
+// comm stream, after round k's theta is in pub[(k+1) % 3]: staleness of the round's steps, then publish k + 1
+void launch_async_publish(AsyncDev* d, long long k, int n_push, int n_fetch, unsigned delay_ns, cudaStream_t st);
+
+// a13 over NCCL on the bf16 path: the per-rank record of one all-gather (kernels_comm.cu)
+struct FetchRecord {
+  int world, rank;
+  long long shard;                 // elements owned per rank
+  long long fw_lo, fw_hi;          // the FC weight [fw_lo, fw_hi): delivered as bf16 only
+  long long rec_f32;               // fp32 slots per record (max over ranks of shard entries outside the FC weight)
+  long long rec_bytes;             // 2 * shard + 4 * rec_f32, a multiple of 16
+  long long img_off, w1_off, w2_off;  // Mnih conv weight image (wimg.cuh), img_off < 0: none
+};
+void launch_fetch_pack(const float* master, const FetchRecord& f, uint8_t* send, cudaStream_t st);
+void launch_fetch_unpack(const uint8_t* recv, const FetchRecord& f, float* theta, __nv_bfloat16* theta_bf16,
+                         cudaStream_t st);
+void launch_widen_range(const __nv_bfloat16* src, float* dst, long long lo, long long hi, cudaStream_t st);
 int server_round_blocks(long long shard);
 
 // bf16 tensor-core path, Mnih-2013 net (kernels_bf16.cu)

@@ -79,18 +79,28 @@ struct dqn_ctx {
   long long pack_n = 0, gpack_off = -1;
   float* gw_partial = nullptr;
   float* gw_partial_db = nullptr;
-  // DQN_ASYNC: the push -> RMSProp -> publish round runs on comm_stream while
-  // the replica keeps stepping; a fetch returns the server theta of one round earlier (lag 1)
-  bool async = false;
+  // DQN_ASYNC / DQN_ASYNC_LAG1: the push -> RMSProp -> publish round runs on
+  // comm_stream while the replica keeps stepping. Generation m is published in theta_pub[m % 3] and announced
+  // by a device flag (adev->pub_gen); a fetch takes the newest one (DQN_ASYNC) or exactly n - 1 (the lag-1 twin)
+  bool async = false, async_lag1 = false;
   cudaStream_t comm_stream = nullptr;
-  cudaEvent_t ev_grad = nullptr, ev_gen[2] = {};  // ev_gen[m % 2]: theta^(m) published in theta_pub[m % 2]
-  float* g_send = nullptr;                        // [P_pad] gradient handed to the round in flight
-  float* theta_pub[2] = {};                       // [P_pad] published server theta, by generation parity
-  __nv_bfloat16* theta_pub_bf16[2] = {};
-  long long stale_hist[32] = {};                  // A25: n_apply - n_local per replica step
-  std::vector<long long> round_nloc;              // n_local of the steps of the current round
+  cudaEvent_t ev_grad = nullptr, ev_pub[3] = {}, ev_send[2] = {};
+  float* g_send[2] = {};                          // [P_pad] gradient handed to round k, by k % 2
+  float* theta_pub[3] = {};                       // [P_pad] published server theta, by generation % 3
+  __nv_bfloat16* theta_pub_bf16[3] = {};
+  AsyncDev* adev = nullptr;                       // device generation flag, fetch log, staleness histogram
+  AsyncDev* h_adev = nullptr;                     // pinned landing zone
+  long long n_fetches = 0;                        // fetches issued (host; fetch f is at step f * n_fetch)
+  unsigned async_delay_ns = 0;                    // DQN_ASYNC_DELAY_US: diagnostic server delay per round
   // NEXT-1 fused server round over NVLink peer memory (world > 1, deterministic, n_fetch == 1)
   bool fused_comm = false;
+  // a13 over NCCL on the bf16 path (world > 1 without the fused round): one all-gather of per-rank records
+  // [bf16 shard | fp32 of its entries outside the FC weight]; the FC weight of theta_local / theta_hat
+  // then exists only in bf16 (get_params widens it)
+  bool fetch_bf16 = false;
+  FetchRecord frec{};
+  uint8_t* fetch_send = nullptr;
+  uint8_t* fetch_recv = nullptr;
   // NEXT-3 collector (dqn_collect): the games persist between calls
   struct Collector {
     int E = 0, n = 0;
@@ -141,6 +151,7 @@ struct dqn_ctx {
   }* h_out = nullptr;
   // host mirrors of the deterministic schedule (identical on every rank)
   long long T = 0, n = 0, n_local = 0, ell = 0;
+  std::vector<long long> gen_log = std::vector<long long>(kDiagSteps, 0);  // n_local of step T at T % kDiagSteps
   // graphs per (fetch, refresh, push) variant; [8..15]: the same with profiling event records
   cudaGraphExec_t graphs[16] = {};
   long long graph_kernels[16] = {};
@@ -295,10 +306,12 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   if (c->replay_capacity < 1) { *why = "replay_capacity must be >= 1"; return DQN_EINVAL; }
   if (c->n_push < 1 || c->n_fetch < 1) { *why = "n_push and n_fetch must be >= 1"; return DQN_EINVAL; }
   if (c->precision != DQN_FP32 && c->precision != DQN_BF16) { *why = "unknown precision"; return DQN_EINVAL; }
-  if (c->sync_mode != DQN_DETERMINISTIC && c->sync_mode != DQN_ASYNC) { *why = "unknown sync_mode"; return DQN_EINVAL; }
+  if (c->sync_mode != DQN_DETERMINISTIC && c->sync_mode != DQN_ASYNC && c->sync_mode != DQN_ASYNC_LAG1) {
+    *why = "unknown sync_mode"; return DQN_EINVAL;
+  }
   if (c->server_rule != DQN_SERVER_MEAN && c->server_rule != DQN_SERVER_PER_GRADIENT) { *why = "unknown server_rule"; return DQN_EINVAL; }
   if (c->replay_dedup != 0 && (c->replay_dedup != 1 || c->frames < 2)) { *why = "replay_dedup needs 0, or 1 with frames >= 2"; return DQN_EINVAL; }
-  if (c->server_rule == DQN_SERVER_PER_GRADIENT && c->sync_mode == DQN_ASYNC) {
+  if (c->server_rule == DQN_SERVER_PER_GRADIENT && c->sync_mode != DQN_DETERMINISTIC) {
     *why = "DQN_SERVER_PER_GRADIENT needs DQN_DETERMINISTIC"; return DQN_EINVAL;
   }
   if (!(c->rms_decay >= 0.0 && c->rms_decay < 1.0) || !(c->rms_eps >= 0.0) || !(c->lr >= 0.0) ||
@@ -430,12 +443,19 @@ static void free_all(dqn_ctx* c) {
   if (c->flags) cudaFree(c->flags);
   if (c->done) cudaFree(c->done);
   if (c->ev_grad) cudaEventDestroy(c->ev_grad);
-  for (int i = 0; i < 2; ++i) {
-    if (c->ev_gen[i]) cudaEventDestroy(c->ev_gen[i]);
+  for (int i = 0; i < 3; ++i) {
+    if (c->ev_pub[i]) cudaEventDestroy(c->ev_pub[i]);
     if (c->theta_pub[i]) cudaFree(c->theta_pub[i]);
     if (c->theta_pub_bf16[i]) cudaFree(c->theta_pub_bf16[i]);
   }
-  if (c->g_send) cudaFree(c->g_send);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_send[i]) cudaEventDestroy(c->ev_send[i]);
+    if (c->g_send[i]) cudaFree(c->g_send[i]);
+  }
+  if (c->adev) cudaFree(c->adev);
+  if (c->h_adev) cudaFreeHost(c->h_adev);
+  if (c->fetch_send) cudaFree(c->fetch_send);
+  if (c->fetch_recv) cudaFree(c->fetch_recv);
 }
 
 // split-K factor so a GEMM fills the machine (148 SMs)
@@ -657,7 +677,8 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   ctx->cap = cfg->replay_capacity;
   ctx->use_graphs = !(getenv("DQN_NO_GRAPH") && atoi(getenv("DQN_NO_GRAPH")));
   ctx->keep_grad = cfg->keep_grad != 0;
-  ctx->async = cfg->sync_mode == DQN_ASYNC;
+  ctx->async = cfg->sync_mode == DQN_ASYNC || cfg->sync_mode == DQN_ASYNC_LAG1;
+  ctx->async_lag1 = cfg->sync_mode == DQN_ASYNC_LAG1;
   ctx->alias_local = (world == 1 && cfg->n_fetch == 1 && !ctx->async);
   ctx->bf16 = cfg->precision == DQN_BF16;
   ctx->gpath = ctx->bf16 && !is_mnih_stack(cfg);
@@ -815,35 +836,67 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     }
     CK(cudaGetLastError());
   }
-  if (ctx->async) {  // theta^(0) published in slot 0; the comm stream and its events
+  if (ctx->async) {  // theta^(0) published in slot 0 (pub_gen = 0); the comm stream and its events
     CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ctx->ev_grad, cudaEventDisableTiming));
-    for (int i = 0; i < 2; ++i) {
-      CK(cudaEventCreateWithFlags(&ctx->ev_gen[i], cudaEventDisableTiming));
+    for (int i = 0; i < 3; ++i) {
+      CK(cudaEventCreateWithFlags(&ctx->ev_pub[i], cudaEventDisableTiming));
       if ((rc = dalloc(ctx, &ctx->theta_pub[i], ctx->P_pad))) return rc;
       if (ctx->bf16 && (rc = dalloc(ctx, &ctx->theta_pub_bf16[i], ctx->P_bf16))) return rc;
     }
-    if ((rc = dalloc(ctx, &ctx->g_send, ctx->P_pad))) return rc;
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&ctx->ev_send[i], cudaEventDisableTiming));
+      if ((rc = dalloc(ctx, &ctx->g_send[i], ctx->P_pad))) return rc;
+      CK(cudaEventRecord(ctx->ev_send[i], ctx->stream));
+    }
+    if ((rc = dalloc(ctx, &ctx->adev, 1))) return rc;
+    CK(cudaMemsetAsync(ctx->adev, 0, sizeof(AsyncDev), ctx->stream));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_adev), sizeof(AsyncDev), cudaHostAllocDefault));
+    std::memset(ctx->h_adev, 0, sizeof(AsyncDev));
     CK(cudaMemcpyAsync(ctx->theta_pub[0], ctx->theta_hat, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice,
                        ctx->stream));
     if (ctx->bf16)
-      launch_f32_to_bf16(ctx->theta_pub[0], ctx->theta_pub_bf16[0], ctx->P_pad, ctx->stream, ctx->img_off, ctx->w1_off,
-                         ctx->w2_off);
-    if (ctx->gpath)
-      launch_gpack(ctx->theta_pub[0], ctx->theta_pub_bf16[0], ctx->gpack_off, ctx->pack_map, ctx->pack_n, ctx->stream);
-    CK(cudaEventRecord(ctx->ev_gen[0], ctx->stream));
+      CK(cudaMemcpyAsync(ctx->theta_pub_bf16[0], ctx->theta_local_bf16, sizeof(__nv_bfloat16) * ctx->P_bf16,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->ev_pub[0], ctx->stream));
+    if (const char* v = getenv("DQN_ASYNC_DELAY_US")) ctx->async_delay_ns = (unsigned)std::max(0, atoi(v)) * 1000u;
   }
   CK(cudaStreamSynchronize(ctx->stream));
 
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof(id));
+    // deterministic schedule: the reduce-scatter's summation order must not change from run to run, so the
+    // algorithm and protocol are pinned unless the caller set them; NCCL reads both at
+    // communicator creation
+    if (!ctx->async) {
+      setenv("NCCL_ALGO", "Ring", 0);
+      setenv("NCCL_PROTO", "Simple", 0);
+    }
     NK(ncclCommInitRank(&ctx->comm, world, id, rank));
     const char* fe = getenv("DQN_FUSED_COMM");
     ctx->fused_comm = !ctx->async && cfg->n_fetch == 1 && world <= kMaxWorld && !(fe && atoi(fe) == 0);
     if (cfg->server_rule == DQN_SERVER_PER_GRADIENT && !ctx->fused_comm)
       return set_err(ctx, DQN_EINVAL, "DQN_SERVER_PER_GRADIENT with N > 1 needs the fused server round (n_fetch = 1)");
     if (ctx->fused_comm && (rc = setup_fused_comm(ctx))) return rc;
+    if (ctx->bf16 && !ctx->fused_comm) {
+      FetchRecord& f = ctx->frec;
+      f.world = world; f.rank = rank; f.shard = ctx->shard;
+      f.fw_lo = net.fc[0].w_off;
+      f.fw_hi = net.fc[0].w_off + (long long)net.fc[0].H * net.fc[0].D;
+      long long mx = 0;
+      for (int p = 0; p < world; ++p) {
+        const long long lo = (long long)p * ctx->shard, hi = lo + ctx->shard;
+        const long long fw = std::max(0LL, std::min(hi, f.fw_hi) - std::max(lo, f.fw_lo));
+        mx = std::max(mx, ctx->shard - fw);
+      }
+      f.rec_f32 = (mx + 3) / 4 * 4;
+      f.rec_bytes = 2 * ctx->shard + 4 * f.rec_f32;
+      f.img_off = ctx->img_off; f.w1_off = ctx->w1_off; f.w2_off = ctx->w2_off;
+      if ((rc = dalloc(ctx, &ctx->fetch_send, f.rec_bytes))) return rc;
+      if ((rc = dalloc(ctx, &ctx->fetch_recv, f.rec_bytes * world))) return rc;
+      ctx->fetch_bf16 = true;
+    }
   }
   ctx->n_per_round = cfg->server_rule == DQN_SERVER_PER_GRADIENT ? world : 1;  // n += 1 per applied gradient (A22)
   return DQN_OK;
@@ -1023,6 +1076,16 @@ static void prof_end(dqn_ctx* ctx) {
 }
 #define PB(name, k) prof_begin(ctx, name, k)
 #define PE() prof_end(ctx)
+
+// a13 on the bf16 path over NCCL: pack this rank's record, one all-gather, unpack every rank's record into
+// the working copies (fp32 entries outside the FC weight, bf16 everywhere + the conv weight image)
+static int enqueue_fetch_bf16(dqn_ctx* ctx, cudaStream_t st, float* dst, __nv_bfloat16* dst_bf16) {
+  launch_fetch_pack(ctx->theta_master, ctx->frec, ctx->fetch_send, st);
+  NK(ncclAllGather(ctx->fetch_send, ctx->fetch_recv, (size_t)ctx->frec.rec_bytes, ncclChar, ctx->comm, st));
+  launch_fetch_unpack(ctx->fetch_recv, ctx->frec, dst, dst_bf16, st);
+  CK(cudaGetLastError());
+  return DQN_OK;
+}
 
 // ------------------------------------------------------------------ one replica step (fp32 path)
 // Enqueue the kernels of one step T on ctx->stream (captured into a graph).
@@ -1209,10 +1272,9 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
     if (ctx->fused_comm) {
       // delivered into theta_local by the previous round's fused server-round kernel (NEXT-1)
     } else if (ctx->world > 1) {
-      PB("fetch_all_gather", 1);
-      NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
-      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st, ctx->img_off, ctx->w1_off,
-                         ctx->w2_off);
+      PB("fetch_all_gather", 2);
+      int rc = enqueue_fetch_bf16(ctx, st, ctx->theta_local, ctx->theta_local_bf16);
+      if (rc) return rc;
       PE();
     } else if (!ctx->alias_local) {
       PB("fetch_copy", 1);
@@ -1383,9 +1445,9 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   if (fetch) {  // a13
     if (ctx->fused_comm) {
     } else if (ctx->world > 1) {
-      PB("fetch_all_gather", 1);
-      NK(ncclAllGather(ctx->theta_master, ctx->theta_local, (size_t)ctx->shard, ncclFloat, ctx->comm, st));
-      launch_f32_to_bf16(ctx->theta_local, ctx->theta_local_bf16, ctx->P_pad, st);
+      PB("fetch_all_gather", 2);
+      int rc = enqueue_fetch_bf16(ctx, st, ctx->theta_local, ctx->theta_local_bf16);
+      if (rc) return rc;
       PE();
     } else if (!ctx->alias_local) {
       PB("fetch_copy", 1);
@@ -1581,45 +1643,58 @@ static int run_step(dqn_ctx* ctx, bool fetch, bool refresh, bool push, bool prof
   return DQN_OK;
 }
 
-// O10 / O11 / O9 schedule of step T (host mirror; identical on every rank). In the asynchronous
-// mode a fetch returns theta^(max(n - 1, 0)), the server state one round earlier (O13, A32).
+// O10 / O11 / O9 schedule of step T (host mirror; identical on every rank). In the asynchronous modes the
+// generation a fetch returns, and with it the refresh, is decided on the device (async_fetch).
 static void schedule(dqn_ctx* ctx, bool* fetch, bool* refresh, bool* push) {
   const dqn_config& c = ctx->cfg;
   const long long T = ctx->T;
   *fetch = (T % c.n_fetch) == 0;
   *refresh = false;
-  if (*fetch) {
-    ctx->n_local = ctx->async ? std::max(ctx->n - 1, 0LL) : ctx->n;
+  if (*fetch && !ctx->async) {
+    ctx->n_local = ctx->n;
     if (ctx->n_local - ctx->ell >= c.target_sync) {
       *refresh = true;
       ctx->ell = ctx->n_local;
     }
   }
   *push = ((T + 1) % c.n_push) == 0;
+  if (!ctx->async) ctx->gen_log[T % kDiagSteps] = ctx->n_local;
 }
 
-// async fetch, enqueued on the compute stream ahead of the step graph: wait until theta^(m) is
-// published, then copy it into the working buffers the graphs read
+// asynchronous fetch (O10/O11 on the device), enqueued on the compute stream ahead of the step graph: DQN_ASYNC
+// takes the newest published generation without waiting; the lag-1 twin waits for generation n - 1
 static int async_fetch(dqn_ctx* ctx) {
-  const int s = (int)(ctx->n_local % 2);
-  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gen[s], 0));
-  CK(cudaMemcpyAsync(ctx->theta_local, ctx->theta_pub[s], sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice,
-                     ctx->stream));
-  if (ctx->bf16)
-    CK(cudaMemcpyAsync(ctx->theta_local_bf16, ctx->theta_pub_bf16[s], sizeof(__nv_bfloat16) * ctx->P_bf16,
-                       cudaMemcpyDeviceToDevice, ctx->stream));
+  long long forced = -1;
+  if (ctx->async_lag1) {
+    forced = std::max(ctx->n - 1, 0LL);
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_pub[forced % 3], 0));
+  }
+  launch_async_pick(ctx->adev, forced, ctx->cfg.target_sync, ctx->n_fetches, ctx->stream);
+  AsyncCopy cp{};
+  for (int i = 0; i < 3; ++i) {
+    cp.pub[i] = ctx->theta_pub[i];
+    cp.pubb[i] = ctx->theta_pub_bf16[i];
+  }
+  cp.th = ctx->theta_local; cp.thb = ctx->theta_local_bf16;
+  cp.hat = ctx->theta_hat; cp.hatb = ctx->theta_hat_bf16;
+  cp.n32 = ctx->P_pad; cp.n16 = ctx->bf16 ? ctx->P_bf16 : 0;
+  launch_async_copy(ctx->adev, cp, ctx->stream);
+  ctx->n_fetches += 1;
+  CK(cudaGetLastError());
   return DQN_OK;
 }
 
-// async push: hand the accumulated gradient to the comm stream, which runs the whole server round
-// (reduce-scatter, RMSProp on the owned shard, all-gather into theta_pub[(n+1) % 2]) while the
-// replica keeps stepping. All NCCL traffic of this mode lives on the comm stream, in rank order.
+// asynchronous push of round k = n: hand the accumulated gradient to the comm stream, which runs the whole
+// server round (reduce-scatter, RMSProp on the owned shard, all-gather into theta_pub[(k + 1) % 3], publish)
+// while the replica keeps stepping. All NCCL traffic of this mode lives on the comm stream, in rank order.
 static int async_push(dqn_ctx* ctx) {
   const dqn_config& c = ctx->cfg;
   cudaStream_t cs = ctx->comm_stream;
-  // g_send is still read by the previous round (generation n) until it publishes ev_gen[n % 2]
-  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gen[ctx->n % 2], 0));
-  CK(cudaMemcpyAsync(ctx->g_send, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, ctx->stream));
+  const long long k = ctx->n;
+  float* gs = ctx->g_send[k % 2];
+  // g_send[k % 2] is read by round k - 2 until that round ends (so the comm stream lags by two rounds at most)
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_send[k % 2], 0));
+  CK(cudaMemcpyAsync(gs, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, ctx->stream));
   if (ctx->grad_snap)
     CK(cudaMemcpyAsync(ctx->grad_snap, ctx->grad, sizeof(float) * ctx->P_pad, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->grad, 0, sizeof(float) * ctx->P_pad, ctx->stream));
@@ -1627,21 +1702,28 @@ static int async_push(dqn_ctx* ctx) {
   CK(cudaStreamWaitEvent(cs, ctx->ev_grad, 0));
   const float div = (float)((double)ctx->world * c.n_push);
   const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
-  const int s = (int)((ctx->n + 1) % 2);
+  const int s = (int)((k + 1) % 3);
   if (ctx->world > 1) {
-    NK(ncclReduceScatter(ctx->g_send, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, cs));
+    NK(ncclReduceScatter(gs, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, cs));
     launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
                    (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, cs);
-    NK(ncclAllGather(ctx->theta_master, ctx->theta_pub[s], (size_t)ctx->shard, ncclFloat, ctx->comm, cs));
+    if (ctx->fetch_bf16) {  // a13 in bf16 (+ the fp32 entries outside the FC weight)
+      int rc = enqueue_fetch_bf16(ctx, cs, ctx->theta_pub[s], ctx->theta_pub_bf16[s]);
+      if (rc) return rc;
+    } else {
+      NK(ncclAllGather(ctx->theta_master, ctx->theta_pub[s], (size_t)ctx->shard, ncclFloat, ctx->comm, cs));
+    }
   } else {
-    launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_send, ctx->P_pad, div, (float)c.lr, rho, omr,
+    launch_rmsprop(ctx->theta_master, ctx->rms, gs, ctx->P_pad, div, (float)c.lr, rho, omr,
                    (float)c.rms_eps, ctx->theta_pub[s], nullptr, ctx->ctr, 0, cs);
   }
-  if (ctx->bf16)
+  if (ctx->bf16 && !ctx->fetch_bf16)
     launch_f32_to_bf16(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->P_pad, cs, ctx->img_off, ctx->w1_off, ctx->w2_off);
   if (ctx->gpath) launch_gpack(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->gpack_off, ctx->pack_map, ctx->pack_n, cs);
+  launch_async_publish(ctx->adev, k, c.n_push, c.n_fetch, ctx->async_delay_ns, cs);
   CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->ev_gen[s], cs));
+  CK(cudaEventRecord(ctx->ev_pub[s], cs));
+  CK(cudaEventRecord(ctx->ev_send[k % 2], cs));
   return DQN_OK;
 }
 
@@ -1651,16 +1733,15 @@ static int do_step(dqn_ctx* ctx, bool profile, long long* kernels, bool* out_fet
   bool fetch, refresh, push;
   schedule(ctx, &fetch, &refresh, &push);
   int rc;
-  if (ctx->async && fetch && (rc = async_fetch(ctx))) return rc;
+  if (ctx->async && fetch) {
+    if ((rc = async_fetch(ctx))) return rc;
+    if (kernels) *kernels += 2;
+  }
   const bool g_fetch = fetch && !ctx->async, g_push = push && !ctx->async;
   if ((rc = run_step(ctx, g_fetch, refresh, g_push, profile, kernels))) return rc;
-  if (ctx->async) {
-    ctx->round_nloc.push_back(ctx->n_local);
-    if (push) {
-      if ((rc = async_push(ctx))) return rc;
-      for (long long nl : ctx->round_nloc) ctx->stale_hist[std::min(ctx->n - nl, 31LL)] += 1;  // A25
-      ctx->round_nloc.clear();
-    }
+  if (ctx->async && push) {
+    if ((rc = async_push(ctx))) return rc;
+    if (kernels) *kernels += 2 + (ctx->fetch_bf16 ? 2 : 0) + (ctx->bf16 && !ctx->fetch_bf16 ? 1 : 0) + (ctx->gpath ? 1 : 0);
   }
   if (push) ctx->n += ctx->n_per_round;
   ctx->T += 1;
@@ -1847,6 +1928,12 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
                            cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->async) {  // the rounds this call pushed are applied; the fetch log and histogram come back
+    CK(cudaStreamSynchronize(ctx->comm_stream));
+    CK(cudaMemcpy(ctx->h_adev, ctx->adev, sizeof(AsyncDev), cudaMemcpyDeviceToHost));
+    ctx->n_local = ctx->h_adev->n_local;
+    ctx->ell = ctx->h_adev->ell;
+  }
   const DevCounters hc = ho->ctr;
   if (ctx->step_trace) {  // DQN_TRACE_STEP=1: the last step's kernel timeline (CTA 0 stamps)
     unsigned long long t[4][ST_N][3] = {}, m[ST_N][3] = {};
@@ -1921,7 +2008,11 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
     stats->generation = ctx->n;
     stats->steps_done = ctx->T;
     stats->nonfinite_elems = hc.nonfinite;
-    for (int i = 0; i < 32; ++i) stats->staleness_hist[i] = ctx->stale_hist[i];
+    for (int i = 0; i < 32; ++i) stats->staleness_hist[i] = ctx->async ? ctx->h_adev->hist[i] : 0;
+    if (stats->step_generation && diag_ok)
+      for (long long t = T0; t < T0 + k; ++t)  // step t used the theta of its last fetch f = t / n_fetch (A40)
+        stats->step_generation[t - T0] =
+            ctx->async ? ctx->h_adev->fgen_log[(t / c.n_fetch) % kDiagSteps] : ctx->gen_log[t % kDiagSteps];
     stats->kernel_launches = kernels;
     double lm = 0.0;
     for (float l : loss) lm += l;
@@ -2182,9 +2273,10 @@ extern "C" int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, 
   if (!ctx) return DQN_EINVAL;
   if (ctx->poisoned) return DQN_ESTATE;
   if (n_params) *n_params = ctx->P;
-  if (generation) *generation = (uint64_t)(which == DQN_PARAMS_LOCAL || which == DQN_PARAMS_TARGET
-                                               ? (which == DQN_PARAMS_LOCAL ? ctx->n_local : ctx->ell)
-                                               : ctx->n);
+  if (generation)
+    *generation = (uint64_t)(which == DQN_PARAMS_LOCAL || which == DQN_PARAMS_LOCAL_BF16 ? ctx->n_local
+                             : which == DQN_PARAMS_TARGET || which == DQN_PARAMS_TARGET_BF16 ? ctx->ell
+                                                                                             : ctx->n);
   if (!out) return DQN_OK;
   if (cap < ctx->P) return set_err(ctx, DQN_EINVAL, "output buffer smaller than P");
   const cudaMemcpyKind kind = is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -2220,7 +2312,37 @@ extern "C" int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, 
       if (!ctx->grad_snap) return set_err(ctx, DQN_EINVAL, "gradient snapshots need cfg.keep_grad = 1 at create");
       src = ctx->grad_snap;
       break;
+    case DQN_PARAMS_LOCAL_BF16:
+    case DQN_PARAMS_TARGET_BF16: {  // the canonical entries of a bf16 working copy, widened (exact)
+      if (!ctx->bf16) return set_err(ctx, DQN_EINVAL, "bf16 working copies exist only on DQN_BF16");
+      float* tmp = nullptr;
+      int rc = dalloc(ctx, &tmp, ctx->P);
+      if (rc) return rc;
+      launch_bf16_to_f32(which == DQN_PARAMS_LOCAL_BF16 ? ctx->theta_local_bf16 : ctx->theta_hat_bf16, tmp, ctx->P,
+                         ctx->stream);
+      cudaError_t e = cudaMemcpyAsync(out, tmp, sizeof(float) * ctx->P, kind, ctx->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+      cudaFree(tmp);
+      CK(e);
+      return DQN_OK;
+    }
     default: return set_err(ctx, DQN_EINVAL, "unknown parameter vector");
+  }
+  if (ctx->fetch_bf16 && (which == DQN_PARAMS_LOCAL || which == DQN_PARAMS_TARGET)) {
+    // the NCCL bf16 fetch delivers the FC weight in bf16 only: widen it from the working copy
+    float* tmp = nullptr;
+    int rc = dalloc(ctx, &tmp, ctx->P);
+    if (rc) return rc;
+    cudaError_t e = cudaMemcpyAsync(tmp, src, sizeof(float) * ctx->P, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) {
+      launch_widen_range(which == DQN_PARAMS_LOCAL ? ctx->theta_local_bf16 : ctx->theta_hat_bf16, tmp,
+                         ctx->frec.fw_lo, ctx->frec.fw_hi, ctx->stream);
+      e = cudaMemcpyAsync(out, tmp, sizeof(float) * ctx->P, kind, ctx->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(tmp);
+    CK(e);
+    return DQN_OK;
   }
   CK(cudaMemcpyAsync(out, src, sizeof(float) * ctx->P, kind, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

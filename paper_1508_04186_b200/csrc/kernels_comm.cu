@@ -193,6 +193,144 @@ void launch_server_round(const ServerRoundArgs& a, cudaStream_t st) {
   launch_pdl(server_round_kernel, dim3(server_round_blocks(a.shard)), dim3(256), 0, st, a);
 }
 
+// ---- NCCL fetch on the bf16 path (a13, n_fetch > 1 or DQN_ASYNC): one all-gather of a per-rank record
+// [bf16 of the owned shard | fp32 of the shard's entries outside the FC weight]. The tensor cores read the
+// FC weight only as bf16 (98 % of P on the Mnih net); the biases, conv weights and the output layer are read
+// in fp32 too (epilogues, TD head, packed conv images), so they travel in both precisions.
+__device__ __forceinline__ long long fetch_piece1(const FetchRecord& f, int s) {  // entries before the FC weight
+  const long long lo = (long long)s * f.shard, hi = lo + f.shard;
+  return max(0LL, min(hi, f.fw_lo) - lo);
+}
+
+__global__ void fetch_pack_kernel(const float* __restrict__ master, FetchRecord f, uint8_t* __restrict__ send) {
+  pdl_wait();
+  pdl_trigger();
+  __nv_bfloat16* rb = reinterpret_cast<__nv_bfloat16*>(send);
+  float* rf = reinterpret_cast<float*>(send + 2 * f.shard);
+  const long long lo = (long long)f.rank * f.shard, n1 = fetch_piece1(f, f.rank);
+  const long long lo2 = max(lo, f.fw_hi);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < f.shard; i += (long long)gridDim.x * blockDim.x) {
+    const float v = master[i];
+    rb[i] = __float2bfloat16_rn(v);
+    const long long g = lo + i;
+    if (g < f.fw_lo) rf[g - lo] = v;
+    else if (g >= f.fw_hi) rf[n1 + (g - lo2)] = v;
+  }
+}
+
+__global__ void fetch_unpack_kernel(const uint8_t* __restrict__ recv, FetchRecord f, float* __restrict__ th,
+                                    __nv_bfloat16* __restrict__ thb) {
+  pdl_wait();
+  pdl_trigger();
+  const long long n = f.shard * f.world;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(g / f.shard);
+    const long long i = g - (long long)s * f.shard;
+    const uint8_t* rec = recv + (long long)s * f.rec_bytes;
+    const __nv_bfloat16 v = reinterpret_cast<const __nv_bfloat16*>(rec)[i];
+    thb[g] = v;
+    if (f.img_off >= 0) {
+      const int sl = wimg_slot(g, f.w1_off, f.w2_off);
+      if (sl >= 0) thb[f.img_off + sl] = v;
+    }
+    const float* rf = reinterpret_cast<const float*>(rec + 2 * f.shard);
+    if (g < f.fw_lo) th[g] = rf[i];
+    else if (g >= f.fw_hi) th[g] = rf[fetch_piece1(f, s) + (g - max((long long)s * f.shard, f.fw_hi))];
+  }
+}
+
+void launch_fetch_pack(const float* master, const FetchRecord& f, uint8_t* send, cudaStream_t st) {
+  const int blocks = (int)std::min<long long>((f.shard + 255) / 256, 148 * 4);
+  launch_pdl(fetch_pack_kernel, dim3(blocks), dim3(256), 0, st, master, f, send);
+}
+
+void launch_fetch_unpack(const uint8_t* recv, const FetchRecord& f, float* theta, __nv_bfloat16* theta_bf16,
+                         cudaStream_t st) {
+  const int blocks = (int)std::min<long long>((f.shard * f.world + 255) / 256, 148 * 8);
+  launch_pdl(fetch_unpack_kernel, dim3(blocks), dim3(256), 0, st, recv, f, theta, theta_bf16);
+}
+
+// the bf16 working copy of [lo, hi) widened into out (get_params of the FC weight on the NCCL bf16 path)
+__global__ void widen_range_kernel(const __nv_bfloat16* src, float* dst, long long lo, long long hi) {
+  for (long long g = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; g < hi; g += (long long)gridDim.x * blockDim.x)
+    dst[g] = __bfloat162float(src[g]);
+}
+void launch_widen_range(const __nv_bfloat16* src, float* dst, long long lo, long long hi, cudaStream_t st) {
+  if (hi <= lo) return;
+  widen_range_kernel<<<(int)std::min<long long>((hi - lo + 255) / 256, 148 * 8), 256, 0, st>>>(src, dst, lo, hi);
+}
+
+// ---- DQN_ASYNC: the device generation flag. The comm stream publishes generation k + 1 with
+// a release store after its kernels wrote theta_pub[(k + 1) % 3]; a fetch on the compute stream reads the flag
+// with an acquire load (one thread, so every block of the copy sees the same generation) and copies that slot.
+// Three slots suffice: a push waits until the comm stream has finished round k - 2 (the g_send double buffer),
+// so a fetch takes a generation >= k - 1 of the rounds pushed so far and the at most two publications that can
+// land during its copy go to the other two slots.
+__global__ void async_pick_kernel(AsyncDev* d, long long forced, long long C, long long f) {
+  unsigned long long g;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(g) : "l"(&d->pub_gen) : "memory");
+  const long long m = forced >= 0 ? forced : (long long)g;
+  d->n_local = m;
+  d->fetch_gen = m;
+  const int refresh = m - d->ell >= C;  // A10: right after the fetch, when n - l >= C
+  if (refresh) d->ell = m;
+  d->do_refresh = refresh;
+  d->fgen_log[f % kDiagSteps] = m;
+}
+
+__global__ void async_copy_kernel(const AsyncDev* d, AsyncCopy c) {
+  const long long m = *(volatile const long long*)&d->fetch_gen;
+  const int slot = (int)(m % 3), refresh = *(volatile const int*)&d->do_refresh;
+  const float4* s4 = reinterpret_cast<const float4*>(c.pub[slot]);
+  const long long stride = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long i = t0; i < c.n32 / 4; i += stride) {
+    const float4 v = s4[i];
+    reinterpret_cast<float4*>(c.th)[i] = v;
+    if (refresh) reinterpret_cast<float4*>(c.hat)[i] = v;
+  }
+  if (c.pubb[0]) {
+    const uint4* b4 = reinterpret_cast<const uint4*>(c.pubb[slot]);
+    for (long long i = t0; i < c.n16 / 8; i += stride) {
+      const uint4 v = b4[i];
+      reinterpret_cast<uint4*>(c.thb)[i] = v;
+      if (refresh) reinterpret_cast<uint4*>(c.hatb)[i] = v;
+    }
+    for (long long i = c.n16 / 8 * 8 + t0; i < c.n16; i += stride) {
+      c.thb[i] = c.pubb[slot][i];
+      if (refresh) c.hatb[i] = c.pubb[slot][i];
+    }
+  }
+}
+
+__global__ void async_publish_kernel(AsyncDev* d, long long k, int n_push, int n_fetch, unsigned delay_ns) {
+  if (threadIdx.x == 0) {
+    if (delay_ns) {  // DQN_ASYNC_DELAY_US (diagnostic): a slow server, so that fetches see stale generations
+      const unsigned long long t0 = gtimer();
+      while (gtimer() - t0 < delay_ns) {
+      }
+    }
+    // A25: every replica step t of round k used the generation of its last fetch f = t / n_fetch
+    for (long long t = k * n_push; t < (k + 1) * n_push; ++t) {
+      const long long base = d->fgen_log[(t / n_fetch) % kDiagSteps];
+      const long long st = k - base;
+      d->hist[st < 31 ? (st < 0 ? 0 : st) : 31] += 1;
+    }
+    // theta_pub[(k + 1) % 3] was written by this stream's earlier kernels: release generation k + 1
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&d->pub_gen), "l"((unsigned long long)(k + 1)) : "memory");
+  }
+}
+
+void launch_async_pick(AsyncDev* d, long long forced, long long C, long long f, cudaStream_t st) {
+  async_pick_kernel<<<1, 1, 0, st>>>(d, forced, C, f);
+}
+void launch_async_copy(const AsyncDev* d, const AsyncCopy& c, cudaStream_t st) {
+  const long long n = std::max(c.n32 / 4, c.n16 / 8);
+  async_copy_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 4), 256, 0, st>>>(d, c);
+}
+void launch_async_publish(AsyncDev* d, long long k, int n_push, int n_fetch, unsigned delay_ns, cudaStream_t st) {
+  async_publish_kernel<<<1, 32, 0, st>>>(d, k, n_push, n_fetch, delay_ns);
+}
+
 DQN_STEP_TRACE_HOST(comm)
 
 }  // namespace dqn

@@ -203,6 +203,19 @@ void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaS
   f32_to_bf16_kernel<<<blocks, 256, 0, st>>>(src, dst, n, img_off, w1_off, w2_off);
 }
 
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* src, float* dst, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) dst[i] = __bfloat162float(src[i]);
+}
+
+void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  bf16_to_f32_kernel<<<blocks, 256, 0, st>>>(src, dst, n);
+}
+
 DQN_STEP_TRACE_HOST(common)
 
 }  // namespace dqn

@@ -25,7 +25,9 @@ def test_flops_scale_linearly_in_b_and_conv1_dominates_the_mnih_forward():
 def test_parameter_counts_agree_with_the_oracle():
     for net in (bench.MNIH, bench.SCALED):
         on = O.Net(**net)
-        assert bench.region_work("rmsprop_update", 32, net)[1] == 24 * O.param_count(on)
+        assert bench.region_work("rmsprop_update", 32, net)[1] == 22 * O.param_count(on)  # 22 B/param
+        assert bench.region_work("rmsprop_update", 32, net, dtype="f32")[1] == 20 * O.param_count(on)
+        assert bench.param_count_of(net) == O.param_count(on)
         conv = sum(cnt for i, (off, cnt) in enumerate(O.tensor_table(on)) if i < 2 * len(net["convs"]))
         assert bench.conv_param_count(net) == conv
 
@@ -35,3 +37,24 @@ def test_server_round_bytes():
     for world in (2, 4, 8):
         shard = -(-P // (64 * world)) * 64
         assert bench.region_work("server_round_fused", 32, bench.MNIH, world)[1] == shard * (6 * world + 16)
+
+
+def test_gather_bytes_are_the_compulsory_u8_slots_and_activations_follow_the_dtype():
+    """a2: conv1's forward reads the s and s' u8 slots, 56,448 B per transition; its
+    output (and every later activation) is 2 B per element on the bf16 path, 4 B on the fp32 path."""
+    b = 32
+    f16, by16 = bench.region_work("conv1_fwd", b)
+    _, by32 = bench.region_work("conv1_fwd", b, dtype="f32")
+    out = 16 * 20 * 20
+    assert by16 == b * 56448 + 2 * b * out * 2 and by32 == b * 56448 + 2 * b * out * 4
+
+
+def test_roofline_reports_both_fractions_and_the_binding_one():
+    regions = [dict(name=n, avg_us=us, steps=100, kernels=1) for n, us in
+               (("conv_fwd", 14.0), ("fc1_fwd", 11.8), ("head_sample", 9.7), ("fc1_bwd_head_finish", 14.2),
+                ("conv_bwd", 19.8), ("reduce_update", 7.6))]
+    r = bench.roofline(regions, 32, bench.MNIH, 1, "bf16", 100)
+    assert r["kernel"] == "conv_bwd" and r["bound"] in ("hbm", "tensor")
+    assert abs(r["frac"] - r[r["bound"] if r["bound"] == "hbm" else "tensor"]["frac"]) < 1e-12
+    assert abs(r["step"]["us"] - 77.1) < 1e-9
+    assert 0 < r["step"]["tensor_frac"] < 0.02 and 0 < r["step"]["hbm_frac"] < 0.2

@@ -2,15 +2,17 @@
 
 The run is configs[1]: a 1M-transition replay on the GPU (56.5 GB of G-pong stacks, generated as bench.py
 generates them), b = 32, C = 1000 (θ̂ refreshed at step 1000), bf16 path with multi-step graphs, PDL and
-the early update.
+the early update; and configs[4] at N = 1 (scaled net, b = 512, the generic tensor-core conv path). θ0 is
+the gated regime's (A38) so that the bar is north_star's 2e-2 on every tensor; alpha = 1e-7 and rms_eps = 1e-2
+keep the gate through T steps (the gated weights are ~1e-4). The hyper-parameters are kernel arguments and
+keep_grad only adds a store, so the kernels and launch configuration are bench.py's.
 
-After 1500 steps, the oracle recomputes the sampled outputs of the next step one by one, from that step's
-inputs (θ, r, θ̂ read back through dqn_get_params and the 32 sampled transitions regenerated on the host):
-* the 32 sampled indices, bit-exact (O3 with size = 1M, T = 1500);
+After T steps, the oracle recomputes the sampled outputs of the next step one by one, from that step's
+inputs (θ, r, θ̂ read back through dqn_get_params and the sampled transitions regenerated on the host):
+* the sampled indices, bit-exact (O3 with size = 1M);
 * the target network's greedy actions, bit-exact outside near-ties (A21);
 * the loss, within 2e-2 (A29);
-* θ after that step — gradient (O7) and then RMSProp (O9) — within north_star's 2e-2 per tensor, and the
-  update Δθ itself per tensor: cosine >= 0.99 and relative L2 < 0.15 (A37).
+* the step's gradient (O7) and update Δθ (then RMSProp O9), per tensor within 2e-2, and the new r (4e-2).
 """
 import numpy as np
 import pytest
@@ -18,21 +20,14 @@ import pytest
 import paper_1508_04186_b200 as D
 import synth
 from oracle import oracle as O
-from tests.helpers import near_tie_mask, per_tensor_rel
+from tests.helpers import delta_rel, gated_theta_separated, near_tie_mask, per_tensor_rel
 
 pytestmark = pytest.mark.gpu
 
 MNIH = dict(convs=((16, 8, 4), (32, 4, 2)), fcs=(256,), n_actions=6)
 SCALED = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=18)
 CAP, CHUNK, SEED0 = 1_000_000, 8192, 0x5EED  # bench.py's prefill: chunks of 8192, seed 0x5EED + offset
-
-
-def rel_l2_per_tensor(x, y, net):
-    worst = 0.0
-    for off, cnt in O.tensor_table(net):
-        xx, yy = np.asarray(x[off:off + cnt], np.float64), np.asarray(y[off:off + cnt], np.float64)
-        worst = max(worst, float(np.linalg.norm(xx - yy) / max(np.linalg.norm(yy), 1e-30)))
-    return worst
+LR = 1e-7
 
 
 @pytest.mark.parametrize("net,B,T", [(MNIH, 32, 1500), (SCALED, 512, 1100)], ids=["configs1-mnih", "configs4-scaled"])
@@ -43,9 +38,10 @@ def test_full_size_sampled_outputs(net, B, T):
     assert torch.cuda.is_available(), "gpu tests need a CUDA device"
     if torch.cuda.mem_get_info()[0] < 64e9:
         pytest.skip("needs ~60 GB of free device memory (1M-slot replay)")
-    cfg = D.Config(**net, minibatch=B, replay_capacity=CAP, target_sync=1000, precision=D.BF16, lr=2.5e-4,
-                   gamma=0.99, n_push=1, n_fetch=1, sync_mode=D.DETERMINISTIC)
-    g = D.DQN(cfg)
+    on = O.Net(**net)
+    cfg = D.Config(**net, minibatch=B, replay_capacity=CAP, target_sync=1000, precision=D.BF16, lr=LR,
+                   rms_eps=1e-2, gamma=0.99, n_push=1, n_fetch=1, sync_mode=D.DETERMINISTIC, keep_grad=1)
+    g = D.DQN(cfg, init_params=gated_theta_separated(on, 17))
     for done in range(0, CAP, CHUNK):
         n = min(CHUNK, CAP - done)
         g.push(*synth.g_pong_torch(n, 4, 84, 84, net["n_actions"], SEED0 + done, "cuda"))
@@ -56,6 +52,8 @@ def test_full_size_sampled_outputs(net, B, T):
     th_hat = g.params(D.PARAMS_TARGET).astype(np.float64)
     out = g.train(1, want_idx=True, want_argmax=True, want_loss=True)
     th2 = g.params(D.PARAMS_LOCAL).astype(np.float64)
+    r2 = g.params(D.PARAMS_RMS).astype(np.float64)
+    g2 = g.params(D.PARAMS_GRAD).astype(np.float64)
     g.close()
 
     idx = out["idx"][0]
@@ -69,7 +67,8 @@ def test_full_size_sampled_outputs(net, B, T):
                 items[int(v)] = [x[int(v) - c0].cpu().numpy() for x in chunk]
         del chunk
     s, a, rw, sn, t = (np.stack([items[int(v)][q] for v in idx]) for q in range(5))
-    on = O.Net(**net)
+    assert O.min_abs_preact(on, th, np.concatenate([s, sn])) > 0.04  # still gated after T steps (A38)
+    assert O.min_abs_preact(on, th_hat, sn) > 0.04
     y, am = O.targets(on, th_hat, sn, rw.astype(np.float64), t, 0.99)
     qn, _ = O.q_values(on, th_hat, sn)
     ok = near_tie_mask(qn, 2e-2)
@@ -77,16 +76,9 @@ def test_full_size_sampled_outputs(net, B, T):
     assert np.array_equal(out["argmax"][0][ok], am[ok])
     loss, grad = O.loss_grad(on, th, s, a, y)
     assert abs(out["loss"][0] - loss) <= 2e-2 * abs(loss)
-    th_ref, _ = O.rmsprop(th, r, grad, 2.5e-4)
     P = O.param_count(on)
-    # north_star's bar: parameters after the step within 2e-2 (max relative error per tensor, A29)
-    assert per_tensor_rel(th2[:P], th_ref[:P], on) < 2e-2
-    # and the step itself: per tensor, the update points where the oracle's does (cosine >= 0.99) and is
-    # within 0.15 in relative L2. After 1500 steps the conv bias gradients are sums over 400 / 81 positions
-    # with heavy cancellation, and units near their ReLU kink take either branch in bf16 (A30/A31), so
-    # the one-step bar at init (0.1, test_gpu_parity_bf16) is measured at 0.10-0.11 here (A37)
-    d_gpu, d_ref = th2[:P] - th[:P], th_ref[:P] - th[:P]
-    for o, c in O.tensor_table(on):
-        x, yv = d_gpu[o:o + c], d_ref[o:o + c]
-        assert np.dot(x, yv) >= 0.99 * np.linalg.norm(x) * np.linalg.norm(yv)
-        assert np.linalg.norm(x - yv) < 0.15 * np.linalg.norm(yv)
+    assert per_tensor_rel(g2[:P], grad, on) < 2e-2
+    th_ref, r_ref = O.rmsprop(th, r, grad, LR, 0.9, 1e-2)
+    # north_star's bar on the step's update of every tensor (A29 on Delta theta, one fp32 ulp of storage, A39)
+    assert delta_rel(th2[:P], th[:P], th_ref[:P], th[:P], on, ulps=1) < 2e-2
+    assert per_tensor_rel(r2[:P], r_ref[:P], on) < 4e-2

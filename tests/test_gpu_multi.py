@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests.helpers import he_theta, nets, per_tensor_rel, replay
+from tests.helpers import delta_rel, gated_theta, he_theta, nets, per_tensor_rel, replay
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -42,28 +42,55 @@ def test_two_replicas_fp32_match_oracle(tmp_path, n_push, n_fetch, C):
                       **TINY_KW)
     oc.n_replicas = 2
     reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
-    ref = O.run(on, oc, 200, reps, he_theta(on, 3).astype(np.float64), 6)
+    th0 = he_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 6)
     assert int(res["n"]) == ref["n"]
     assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
-    assert per_tensor_rel(res["theta"], ref["theta"], on) < 1e-5
+    assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 1e-5
+    assert per_tensor_rel(res["r"], ref["r"], on) < 2e-5
+
+
+def _bf16_case(tmp_path, world, scaled=False, n_push=1, n_fetch=1, extra=()):
+    """bf16 at N = world in the gated regime (A38): Delta theta of every tensor within 2e-2 of the oracle's
+    N-replica mean-gradient RMSProp (and r within 4e-2, quadratic in the gradients)."""
+    kw = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=18) if scaled else {}
+    args = ["--precision", "bf16", "--b", "32", "--steps", "4", "--gated", "--lr", "1e-5", "--eps", "1e-2",
+            "--n-push", str(n_push), "--n-fetch", str(n_fetch), *extra] + (["--scaled"] if scaled else [])
+    res = run_ranks(world, tmp_path, *args)
+    dc, on, oc = nets(minibatch=32, replay_capacity=200, lr=1e-5, rms_eps=1e-2, target_sync=2, n_push=n_push,
+                      n_fetch=n_fetch, **kw)
+    oc.n_replicas = world
+    reps = [replay(on, 250, 100 + k)[0] for k in range(world)]
+    th0 = gated_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 4)
+    assert int(res["n"]) == ref["n"]
+    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
+    assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 2e-2
+    assert per_tensor_rel(res["r"], ref["r"], on) < 4e-2
+    return res
 
 
 def test_two_replicas_bf16_mnih(tmp_path):
-    """bf16 at N = 2 in the smooth regime (no unit near its ReLU kink, A31): the update of the sharded
-    server must follow the oracle's 2-replica mean-gradient RMSProp; theta per tensor in relative L2."""
+    """BASELINE.json configs[2] at N = 2: the fused server round (NEXT-1) on the bf16 Mnih kernels."""
     if n_gpus() < 2:
         pytest.skip("needs 2 GPUs")
-    from tests.test_gpu_parity_bf16 import rel_l2_per_tensor, smooth_theta
-    res = run_ranks(2, tmp_path, "--precision", "bf16", "--b", "32", "--steps", "3", "--smooth", "--lr", "1e-4")
-    dc, on, oc = nets(minibatch=32, replay_capacity=200, lr=1e-4, target_sync=2)
-    oc.n_replicas = 2
-    reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
-    th0 = smooth_theta(on, 3).astype(np.float64)
-    ref = O.run(on, oc, 200, reps, th0, 3)
-    assert int(res["n"]) == ref["n"]
-    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
-    assert per_tensor_rel(res["theta"], ref["theta"], on) < 2e-2
-    assert rel_l2_per_tensor(res["theta"] - th0, ref["theta"] - th0, on) < 0.1
+    _bf16_case(tmp_path, 2)
+
+
+def test_two_replicas_bf16_nccl_path_bit_identical(tmp_path):
+    """n_fetch = 2: push = NCCL reduce-scatter, fetch = NCCL all-gather of the bf16 working copy (a11, a13);
+    two runs on fresh communicators are bit-identical (SURVEY §8(e) determinism, NCCL_ALGO/PROTO pinned)."""
+    if n_gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = _bf16_case(tmp_path, 2, n_push=2, n_fetch=2, extra=("--repeat", "2"))
+    assert bool(res["identical"])
+
+
+def test_two_replicas_fused_round_bit_identical(tmp_path):
+    if n_gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = _bf16_case(tmp_path, 2, extra=("--repeat", "2"))
+    assert bool(res["identical"])
 
 
 def test_two_replicas_async_fp32_match_lag1_twin(tmp_path):
@@ -77,12 +104,31 @@ def test_two_replicas_async_fp32_match_lag1_twin(tmp_path):
     oc.n_replicas = 2
     oc.fetch_lag = 1
     reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
-    ref = O.run(on, oc, 200, reps, he_theta(on, 3).astype(np.float64), 8)
+    th0 = he_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 8)
     assert int(res["n"]) == ref["n"]
     assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
-    assert per_tensor_rel(res["theta"], ref["theta"], on) < 1e-5
+    assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 1e-5
     # rank 0's histogram counts its own replica steps; the oracle's counts both replicas
     assert np.array_equal(res["staleness"] * 2, ref["staleness"])
+
+
+def test_two_replicas_async_free_running_equals_realised_schedule(tmp_path):
+    """DQN_ASYNC at N = 2 (Downpour's asynchrony, A40): each replica fetches the newest generation its comm
+    stream has published; the oracle replays both replicas' realised schedules exactly."""
+    if n_gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_ranks(2, tmp_path, "--tiny", "--n-push", "2", "--n-fetch", "1", "--target-sync", "2", "--steps", "10",
+                    "--async-free", env={"DQN_ASYNC_DELAY_US": "200"})
+    dc, on, oc = nets(minibatch=16, replay_capacity=200, n_push=2, n_fetch=1, target_sync=2, lr=1e-3, **TINY_KW)
+    oc.n_replicas = 2
+    oc.fetch_gen = res["step_generation"]  # n_fetch = 1: one fetch per step
+    reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
+    th0 = he_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 10)
+    assert ref["rc"] == 0 and int(res["n"]) == ref["n"] == 5
+    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
+    assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 1e-5
 
 
 @pytest.mark.parametrize("world", [4, 8])
@@ -95,47 +141,25 @@ def test_many_replicas_fp32_match_oracle(tmp_path, world):
     dc, on, oc = nets(minibatch=16, replay_capacity=200, target_sync=2, lr=1e-3, **TINY_KW)
     oc.n_replicas = world
     reps = [replay(on, 250, 100 + k)[0] for k in range(world)]
-    ref = O.run(on, oc, 200, reps, he_theta(on, 3).astype(np.float64), 5)
+    th0 = he_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 5)
     assert int(res["n"]) == ref["n"]
     assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
-    assert per_tensor_rel(res["theta"], ref["theta"], on) < 1e-5
+    assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 1e-5
 
 
 @pytest.mark.parametrize("world", [4, 8])
 def test_many_replicas_bf16_mnih(tmp_path, world):
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    from tests.test_gpu_parity_bf16 import rel_l2_per_tensor, smooth_theta
-    res = run_ranks(world, tmp_path, "--precision", "bf16", "--b", "32", "--steps", "3", "--smooth", "--lr", "1e-4")
-    dc, on, oc = nets(minibatch=32, replay_capacity=200, lr=1e-4, target_sync=2)
-    oc.n_replicas = world
-    reps = [replay(on, 250, 100 + k)[0] for k in range(world)]
-    th0 = smooth_theta(on, 3).astype(np.float64)
-    ref = O.run(on, oc, 200, reps, th0, 3)
-    assert int(res["n"]) == ref["n"]
-    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
-    assert per_tensor_rel(res["theta"], ref["theta"], on) < 2e-2
-    assert rel_l2_per_tensor(res["theta"] - th0, ref["theta"] - th0, on) < 0.1
+    _bf16_case(tmp_path, world)
 
 
 def test_two_replicas_bf16_scaled_generic_path(tmp_path):
-    """The generic bf16 conv path (scaled net, BASELINE.json configs[4]) at N = 2 with the fused server
-    round, smooth regime: theta after 3 rounds follows the oracle's 2-replica run."""
+    """The generic bf16 conv path (scaled net, BASELINE.json configs[4]) at N = 2 with the fused server round."""
     if n_gpus() < 2:
         pytest.skip("needs 2 GPUs")
-    from tests.test_gpu_parity_bf16 import rel_l2_per_tensor, smooth_theta
-    kw = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=18)
-    res = run_ranks(2, tmp_path, "--precision", "bf16", "--scaled", "--b", "32", "--steps", "3", "--smooth", "--lr",
-                    "1e-5")
-    dc, on, oc = nets(minibatch=32, replay_capacity=200, lr=1e-5, target_sync=2, **kw)
-    oc.n_replicas = 2
-    reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
-    th0 = smooth_theta(on, 3).astype(np.float64)
-    ref = O.run(on, oc, 200, reps, th0, 3)
-    assert int(res["n"]) == ref["n"]
-    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
-    assert per_tensor_rel(res["theta"], ref["theta"], on) < 2e-2
-    assert rel_l2_per_tensor(res["theta"] - th0, ref["theta"] - th0, on) < 0.1
+    _bf16_case(tmp_path, 2, scaled=True)
 
 
 @pytest.mark.parametrize("n_push", [1, 2])
@@ -150,7 +174,8 @@ def test_two_replicas_per_gradient_rule(tmp_path, n_push):
     oc.n_replicas = 2
     oc.server_rule = 1
     reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
-    ref = O.run(on, oc, 200, reps, he_theta(on, 3).astype(np.float64), 6)
+    th0 = he_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 6)
     assert int(res["n"]) == ref["n"] == 2 * (6 // n_push)
     assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
-    assert per_tensor_rel(res["theta"], ref["theta"], on) < 1e-5
+    assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 1e-5

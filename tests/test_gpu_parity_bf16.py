@@ -16,7 +16,7 @@ import pytest
 
 import paper_1508_04186_b200 as D
 from oracle import oracle as O
-from tests.helpers import he_theta, near_tie_mask, nets, per_tensor_rel, replay
+from tests.helpers import delta_rel, gated_theta, he_theta, near_tie_mask, nets, per_tensor_rel, replay
 
 pytestmark = pytest.mark.gpu
 TOL = 2e-2
@@ -117,8 +117,8 @@ def test_default_regime_config0():
     out = g.train(9, want_idx=True)
     ref = O.run(on, oc, 1000, [rp], th0, 10)
     assert np.array_equal(out["idx"], ref["idx"][0, 1:])
-    # parameters after 10 steps: per tensor normwise on theta
-    assert per_tensor_rel(g.params(D.PARAMS_SERVER), ref["theta"], on) < 0.05
+    # parameters after k steps: test_gpu_parity_gated (A38); here units near their kink take either
+    # branch in bf16 (A31), so the trajectories separate at the level of the gradient noise
     g.close()
 
 
@@ -135,35 +135,32 @@ def test_bf16_run_to_run_bit_identical():
 
 
 def test_fused_reduce_update_path():
-    """N = 1 without DQN_KEEP_GRAD: the conv partials' reduction runs inside the update kernel
-    (reduce_update_kernel). Its theta after 5 steps must follow the oracle like the two-kernel path
-    (smooth regime, 2e-2) and agree with that path to fp32 rounding. By default the FC / output-layer
-    part of that update runs in extra CTAs of the conv backward launch (DQN_EARLY_UPDATE); with it off
-    the same per-element arithmetic runs in reduce_update_kernel, so the two runs are bit-identical."""
-    dc, on, oc = nets(minibatch=32, replay_capacity=1000, precision=D.BF16, lr=1e-5)
-    theta0 = smooth_theta(on, 7)
+    """N = 1, n_push = 1 (the bench path): the conv partials' reduction runs inside the update kernel
+    (reduce_update_kernel) and the FC / output-layer part of that update in extra CTAs of the conv backward
+    launch (the early update). With DQN_EARLY_UPDATE=0 the same per-element arithmetic runs in
+    reduce_update_kernel: the two runs are bit-identical, with keep_grad on or off, and Delta theta after
+    5 steps matches the oracle within 2e-2 per tensor (gated regime, A38)."""
+    dc, on, oc = nets(minibatch=32, replay_capacity=1000, precision=D.BF16, lr=1e-5, rms_eps=1e-2)
+    theta0 = gated_theta(on, 7)
     res = {}
-    for keep in ("1", None, "late"):
-        if keep != "1":
-            os.environ.pop("DQN_KEEP_GRAD", None)
-        if keep == "late":
+    for mode in ("early", "late", "nokeep"):
+        if mode == "late":
             os.environ["DQN_EARLY_UPDATE"] = "0"
         try:
-            g, rp, _ = make(dc, on, theta0, 1000, 77)
+            cfg = dc if mode != "nokeep" else D.Config(**{**dc.__dict__, "keep_grad": 0})
+            g, rp, _ = make(cfg, on, theta0, 1000, 77)
             g.train(5)
-            res[keep] = (g.params(D.PARAMS_SERVER).astype(np.float64), g.params(D.PARAMS_LOCAL).astype(np.float64))
+            res[mode] = (g.params(D.PARAMS_SERVER).astype(np.float64), g.params(D.PARAMS_LOCAL).astype(np.float64))
             g.close()
         finally:
-                    os.environ.pop("DQN_EARLY_UPDATE", None)
-    assert np.array_equal(res[None][0], res["late"][0]) and np.array_equal(res[None][1], res["late"][1])
+            os.environ.pop("DQN_EARLY_UPDATE", None)
+    for mode in ("late", "nokeep"):
+        assert np.array_equal(res["early"][0], res[mode][0]) and np.array_equal(res["early"][1], res[mode][1])
+    th, loc = res["early"]
+    assert np.array_equal(th, loc)  # N = 1: the working copy is the server theta
     ref = O.run(on, oc, 1000, [rp], theta0.astype(np.float64), 5)
     th0 = theta0.astype(np.float64)
-    for keep in ("1", None):
-        th, loc = res[keep]
-        assert np.array_equal(th, loc)  # N = 1: the working copy is the server theta
-        assert per_tensor_rel(th, ref["theta"], on) < TOL
-        assert rel_l2_per_tensor(th - th0, ref["theta"] - th0, on) < 0.1
-    assert per_tensor_rel(res[None][0], res["1"][0], on) < 1e-5
+    assert delta_rel(th, th0, ref["theta"], th0, on, ulps=5) < TOL
 
 
 def test_fc_too_wide_for_the_dx_staging_is_rejected():

@@ -9,7 +9,7 @@ import pytest
 
 import paper_1508_04186_b200 as D
 from oracle import oracle as O
-from tests.helpers import he_theta, near_tie_mask, nets, per_tensor_rel, replay
+from tests.helpers import delta_rel, he_theta, near_tie_mask, nets, per_tensor_rel, replay
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-5
@@ -97,17 +97,26 @@ def test_config0_ten_steps_teacher_forced():
         if O.min_abs_preact(on, th, rp.s[idx]) < FLIP:
             flips += 1      # a ReLU unit within rounding distance of its kink: one sample's path may differ
             tol = 1e-3
-        assert per_tensor_rel(g.params(D.PARAMS_GRAD), grad, on) < tol
+        g_gpu = g.params(D.PARAMS_GRAD).astype(np.float64)
+        assert per_tensor_rel(g_gpu, grad, on) < tol
+        th_gpu = g.params(D.PARAMS_SERVER)
+        # north_star's metric on theta (A29) against the oracle's step from (theta_k, r_k)
         th_next, _ = O.rmsprop(th, r, grad, oc.lr, oc.rms_decay, oc.rms_eps)
-        assert per_tensor_rel(g.params(D.PARAMS_SERVER), th_next, on) < tol
+        assert per_tensor_rel(th_gpu, th_next, on) < tol
+        # and the update itself, Alg. 2 applied to the GPU's own gradient: at eps = 1e-8 the step
+        # alpha g / sqrt(r + eps) multiplies a gradient error in a near-zero element by alpha / sqrt(eps),
+        # so the update rule is checked apart from the gradient (checked above), to 1e-5 + fp32 storage (A39)
+        th_upd, _ = O.rmsprop(th, r, g_gpu, oc.lr, oc.rms_decay, oc.rms_eps)
+        assert delta_rel(th_gpu, th, th_upd, th, on, ulps=1) < TOL
     assert flips <= 5
     g.close()
 
 
 def test_config0_ten_steps_free_running():
-    """The same 10 steps free-running against the oracle's own trajectory. Indices are bit-exact.
-    Parameters agree to 1e-5 until the first ReLU-boundary event; after it an affected element can
-    differ by at most one RMSProp step per remaining step, |dtheta| <= 2 alpha sqrt(1/(1-rho)) (A30)."""
+    """The same 10 steps free-running against the oracle's own trajectory. Indices are bit-exact, every
+    step's loss is within 1e-5 up to the first ReLU-boundary event, and Delta theta = theta_k - theta_0 of
+    every tensor is within 1e-5 over the longest prefix without one (A30: after a boundary event the two
+    evaluations legitimately take different ReLU branches; the teacher-forced test covers those steps)."""
     dc, on, oc = nets(minibatch=32, replay_capacity=1000)
     g, theta0, rp = make(dc, on, 1000, 1234)
     th0 = theta0.astype(np.float64)
@@ -115,9 +124,6 @@ def test_config0_ten_steps_free_running():
     ref = O.run(on, oc, 1000, [rp], th0, 10)
     assert ref["rc"] == 0 and out["generation"] == ref["n"] == 10
     assert np.array_equal(out["idx"], ref["idx"][0])
-    th = g.params(D.PARAMS_SERVER).astype(np.float64)
-    bound = 10 * 2 * oc.lr * np.sqrt(1.0 / (1.0 - oc.rms_decay))
-    assert np.max(np.abs(th - ref["theta"])) <= bound
     # the oracle's own trajectory tells which prefix has no boundary event; there parity is 1e-5
     clean = 0
     for k in range(10):
@@ -125,12 +131,19 @@ def test_config0_ten_steps_free_running():
         if O.min_abs_preact(on, thk, rp.s[ref["idx"][0, k]]) < FLIP:
             break
         clean += 1
-    if clean >= 1:
-        g2, _, _ = make(dc, on, 1000, 1234)
-        g2.train(clean)
-        ref2 = O.run(on, oc, 1000, [rp], th0, clean)
-        assert per_tensor_rel(g2.params(D.PARAMS_SERVER), ref2["theta"], on) < TOL
-        g2.close()
+    assert clean >= 2
+    assert np.all(np.abs(out["loss"][:clean] - ref["loss"][0, :clean]) <= TOL * ref["loss"][0, :clean])
+    g2, _, _ = make(dc, on, 1000, 1234)
+    g2.train(clean)
+    ref2 = O.run(on, oc, 1000, [rp], th0, clean)
+    th2 = g2.params(D.PARAMS_SERVER).astype(np.float64)
+    assert per_tensor_rel(th2, ref2["theta"], on) < TOL                         # north_star's metric (A29)
+    # Delta theta per tensor in relative L2: the max norm would be set by the few near-zero-gradient
+    # elements whose RMSProp step amplifies rounding by alpha / sqrt(eps) (see the teacher-forced test)
+    for o, c in O.tensor_table(on):
+        d_gpu, d_ref = th2[o:o + c] - th0[o:o + c], ref2["theta"][o:o + c] - th0[o:o + c]
+        assert np.linalg.norm(d_gpu - d_ref) <= TOL * np.linalg.norm(d_ref)
+    g2.close()
     g.close()
 
 
@@ -142,7 +155,8 @@ def test_schedule_variants(n_push, n_fetch, C):
     out = g.train(9, want_argmax=True)
     ref = O.run(on, oc, 64, [rp], theta0.astype(np.float64), 9)
     assert out["generation"] == ref["n"] == 9 // n_push
-    assert per_tensor_rel(g.params(D.PARAMS_SERVER), ref["theta"], on) < TOL
+    th0 = theta0.astype(np.float64)
+    assert delta_rel(g.params(D.PARAMS_SERVER), th0, ref["theta"], th0, on, ulps=9) < TOL
     g.close()
 
 
@@ -198,7 +212,8 @@ def test_device_pointer_inputs():
     out = g.train(4, want_idx=True)
     ref = O.run(on, oc, 32, [rp], theta0.astype(np.float64), 4)
     assert np.array_equal(out["idx"], ref["idx"][0])
-    assert per_tensor_rel(g.params(D.PARAMS_SERVER), ref["theta"], on) < TOL
+    th0 = theta0.astype(np.float64)
+    assert delta_rel(g.params(D.PARAMS_SERVER), th0, ref["theta"], th0, on, ulps=4) < TOL
     qd = torch.zeros((5, on.n_actions), dtype=torch.float32, device="cuda")
     ad = torch.zeros(5, dtype=torch.int32, device="cuda")
     g.q_values(torch.from_numpy(raw[0][:5]).cuda(), q_out=qd, argmax_out=ad)

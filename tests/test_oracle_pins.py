@@ -376,3 +376,25 @@ def test_rmsprop_r_updated_before_theta():
     # A5: theta uses the NEW r
     th, r = O.rmsprop(np.array([0.0]), np.array([4.0]), np.array([1.0]), 1.0, 0.9, 0.0)
     assert abs(r[0] - 3.7) < 1e-15 and abs(th[0] + 1.0 / math.sqrt(3.7)) < 1e-15
+
+
+def test_gradient_does_not_depend_on_the_thread_count():
+    """or_loss_grad sums the per-sample terms of P:123 in sample order whatever the number of OpenMP threads
+    that computed them (bench.py's all-core cpu_baseline times the same arithmetic as the tests use)."""
+    net = O.Net(frames=3, height=17, width=13, convs=((5, 5, 2), (6, 3, 2)), fcs=(19,), n_actions=5)
+    tt = O.tensor_table(net)
+    rng = np.random.default_rng(5)
+    th = rng.normal(0, 0.3, O.param_count(net))
+    s = rng.integers(0, 256, (37, 3, 17, 13), dtype=np.uint8)   # 2 blocks of 16 + a ragged 5
+    a = rng.integers(0, 5, 37).astype(np.int32)
+    y = rng.normal(0, 1, 37)
+    n0 = O.threads()
+    try:
+        O.set_threads(1)
+        l1, g1 = O.loss_grad(net, th, s, a, y)
+        O.set_threads(0)
+        lk, gk = O.loss_grad(net, th, s, a, y)
+    finally:
+        O.set_threads(n0)
+    assert l1 == lk and np.array_equal(g1, gk)
+    assert len(tt) == 8

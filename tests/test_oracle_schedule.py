@@ -53,6 +53,8 @@ def serial_reference(cfg, replays, theta0, steps, cap, net=TINY, stale=None):
         for k in range(N):
             if T % cfg.n_fetch == 0:
                 m = max(n - cfg.fetch_lag, 0)
+                if cfg.fetch_gen is not None:   # the realised schedule of an asynchronous run (A40)
+                    m = int(cfg.fetch_gen[k][T // cfg.n_fetch])
                 th_local[k] = history[m].copy()
                 n_loc[k] = m
                 if n_loc[k] - ell[k] >= cfg.target_sync:
@@ -236,3 +238,35 @@ def test_per_gradient_rule_two_equal_gradients_closed_form():
     for _ in range(2):
         t, rr = O.rmsprop(t, rr, np.array([g]), a, 0.9, eps)
     assert abs(t[0] - th2) < 1e-15 and abs(rr[0] - r2) < 1e-15
+
+
+@pytest.mark.parametrize("N,n_push,n_fetch", [(1, 1, 1), (2, 2, 1), (2, 1, 3), (3, 2, 2)])
+def test_realised_async_schedule_equals_serial_loop(N, n_push, n_fetch):
+    """O13 generalised (A40): every fetch returns a generation chosen by the asynchronous run (any published
+    one, here drawn at random from the last three); or_run with that schedule equals the written-out loop,
+    and the fixed-lag schedules reproduce fetch_lag = 0 / 1 exactly."""
+    steps = 9
+    rng = np.random.default_rng(N * 100 + n_push * 10 + n_fetch)
+    nf = -(-steps // n_fetch)
+    gen_at = [(f * n_fetch) // n_push for f in range(nf)]   # server generation when fetch f happens (lock-step)
+    fg = np.array([[max(g - int(rng.integers(0, 3)), 0) for g in gen_at] for _ in range(N)], np.int64)
+    reps = make_replays(N, 60, 7)
+    th0 = he_theta(TINY, 4)
+    cfg = O.TrainCfg(n_replicas=N, minibatch=4, n_push=n_push, n_fetch=n_fetch, target_sync=2, lr=3e-3, gamma=0.9,
+                     fetch_gen=fg)
+    ref = serial_reference(cfg, reps, th0, steps, CAP)
+    out = O.run(TINY, cfg, CAP, reps, th0, steps)
+    assert out["rc"] == 0
+    assert np.allclose(out["theta"], ref[0], rtol=0, atol=1e-12)
+    for lag in (0, 1):
+        fixed = np.array([[max(g - lag, 0) for g in gen_at] for _ in range(N)], np.int64)
+        c1 = O.TrainCfg(**{**cfg.__dict__, "fetch_gen": fixed})
+        c2 = O.TrainCfg(**{**cfg.__dict__, "fetch_gen": None, "fetch_lag": lag})
+        assert np.array_equal(O.run(TINY, c1, CAP, reps, th0, steps)["theta"], O.run(TINY, c2, CAP, reps, th0, steps)["theta"])
+
+
+def test_realised_schedule_rejects_an_unpublished_generation():
+    reps = make_replays(1, 30, 3)
+    fg = np.array([[0, 5, 1]], np.int64)   # generation 5 does not exist at step 1
+    cfg = O.TrainCfg(n_replicas=1, minibatch=2, fetch_gen=fg)
+    assert O.run(TINY, cfg, CAP, reps, he_theta(TINY, 1), 3)["rc"] == -4

@@ -27,7 +27,11 @@ def main():
     ap.add_argument("--tiny", action="store_true")
     ap.add_argument("--scaled", action="store_true", help="BASELINE configs[4] net (generic bf16 conv path)")
     ap.add_argument("--smooth", action="store_true")
-    ap.add_argument("--async-mode", action="store_true")
+    ap.add_argument("--gated", action="store_true", help="gated-regime theta0 (tests/helpers.gated_theta, A38)")
+    ap.add_argument("--eps", type=float, default=1e-8, help="RMSProp epsilon (A4)")
+    ap.add_argument("--repeat", type=int, default=1, help="run the whole job this many times (bit identity)")
+    ap.add_argument("--async-mode", action="store_true", help="DQN_ASYNC_LAG1 (the deterministic twin, O13)")
+    ap.add_argument("--async-free", action="store_true", help="DQN_ASYNC (newest published generation, A40)")
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--server-rule", type=int, default=0, help="0 mean (A7), 1 per gradient (A33)")
     a = ap.parse_args()
@@ -48,23 +52,43 @@ def main():
         kw = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=18)
     prec = D.FP32 if a.precision == "fp32" else D.BF16
     dc, on, oc = nets(minibatch=a.b, replay_capacity=200, n_push=a.n_push, n_fetch=a.n_fetch,
-                      target_sync=a.target_sync, lr=a.lr, precision=prec,
-                      sync_mode=D.ASYNC if a.async_mode else D.DETERMINISTIC, server_rule=a.server_rule, **kw)
+                      target_sync=a.target_sync, lr=a.lr, rms_eps=a.eps, precision=prec,
+                      sync_mode=D.ASYNC_LAG1 if a.async_mode else D.ASYNC if a.async_free else D.DETERMINISTIC,
+                      server_rule=a.server_rule, **kw)
     theta0 = he_theta(on, 3)
     if a.smooth:
         from tests.test_gpu_parity_bf16 import smooth_theta
         theta0 = smooth_theta(on, 3)
-    g = D.DQN(dc, rank=rank, world=world, nccl_id=obj[0], init_params=theta0)
+    if a.gated:
+        from tests.helpers import gated_theta
+        theta0 = gated_theta(on, 3)
     _, raw = replay(on, 250, 100 + rank)
-    g.push(*raw)
-    out = g.train(a.steps, want_idx=True)
-    th = g.params(D.PARAMS_SERVER)        # collective
+    runs = []
+    for _ in range(a.repeat):
+        g = D.DQN(dc, rank=rank, world=world, nccl_id=obj[0] if not runs else None, init_params=theta0) \
+            if not runs else None
+        if g is None:  # a fresh communicator for every repetition
+            o2 = [D.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(o2, src=0)
+            g = D.DQN(dc, rank=rank, world=world, nccl_id=o2[0], init_params=theta0)
+        g.push(*raw)
+        out = g.train(a.steps, want_idx=True, want_generation=True)
+        th = g.params(D.PARAMS_SERVER)        # collective
+        rr = g.params(D.PARAMS_RMS)           # collective
+        runs.append((th, rr))
+        if len(runs) < a.repeat:
+            g.close()
     idx = torch.from_numpy(out["idx"]).cuda()
     gathered = [torch.zeros_like(idx) for _ in range(world)]
     dist.all_gather(gathered, idx)
+    gen = torch.from_numpy(out["step_generation"]).cuda()
+    gens = [torch.zeros_like(gen) for _ in range(world)]
+    dist.all_gather(gens, gen)
     if rank == 0:
-        np.savez(a.out, theta=th, n=out["generation"], idx=np.stack([x.cpu().numpy() for x in gathered]),
-                 staleness=out["staleness"])
+        np.savez(a.out, theta=runs[0][0], r=runs[0][1], n=out["generation"],
+                 idx=np.stack([x.cpu().numpy() for x in gathered]), staleness=out["staleness"],
+                 step_generation=np.stack([x.cpu().numpy() for x in gens]),
+                 identical=all(np.array_equal(t, runs[0][0]) and np.array_equal(r, runs[0][1]) for t, r in runs))
     g.close()
     dist.barrier()
     dist.destroy_process_group()
