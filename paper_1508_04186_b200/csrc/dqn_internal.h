@@ -3,6 +3,7 @@
 // nothing here is shared with oracle/.
 #pragma once
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (types only; the encode entry point is fetched from the driver at run time)
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -367,6 +368,82 @@ void launch_gpack(const float* theta, __nv_bfloat16* dst, long long img_off, con
                   cudaStream_t st);
 void init_conv_kernel_attrs();
 unsigned long long gconv_error();
+// warp-specialised persistent TMA GEMM (kernels_tma.cu): the large-batch FC layers. Operand maps are 2-D
+// bf16 tensors read in 64-column boxes with the 128-byte swizzle (make_tmap_bf16): a K-major operand's box is
+// [128 or BN rows][64 k], an MN-major one's [64 k][64 mn]. Epilogues as TcGemmArgs (TC_EPI_*).
+constexpr int kTgMaxStages = 8;
+struct TGemmArgs {
+  CUtensorMap ta[2], tb[2];        // per group
+  int M, N, K;
+  int kper, splits;                // K per split (a multiple of 64 when splits > 1), split count
+  int BN;                          // n-tile: multiple of 16 (K-major B) or of 64 (MN-major B), <= 256
+  int a_mn, b_mn, groups, stages;
+  int epi, store;
+  float* C[2];
+  long long ldc;
+  float* partial;
+  __nv_bfloat16* out_bf16;
+  const __nv_bfloat16* mask;
+  long long ldo;
+  int hwc_HW, hwc_C;
+  int hwc_Wo, hwc_Ws;              // hwc_Ws > 0: the NHWC dZ in the input-grid geometry (row y * Ws + x, not
+  long long ldo_out;               //   y * Wo + x), per-sample stride ldo_out (TCONV backward)
+  // TC_EPI_CONV_FWD (implicit-GEMM convolution over "virtual rows"): row m = img * Hs*Ws + y * Ws + x of the
+  // input grid; K chunk c = (tap t, 64-channel block cb), A box at row m0 + (t / Tw) * Ws + t % Tw; rows with
+  // y >= Ho or x >= Wo are computed and discarded
+  int Ws, HsWs, Tw, Cblk, Ho, Wo;
+  const float* bias[2];
+  __nv_bfloat16* cout[2];          // next layer's s2d grid (s_next > 0) or the canonical (C,H,W) flatten
+  float scale;                     // 1/255 on layer 1 (integer-valued bf16 pixels), else 1
+  int s_next;
+};
+constexpr int TC_EPI_CONV_FWD = 3;
+// ---- TMA implicit-GEMM convolutions with tap windows (kernels_tma.cu). The A source is a 2-D bf16 tensor of
+// "virtual rows" (row = img * Hs*Ws + y * Ws + x of a layer's input grid, 64-channel blocks); ONE TMA box of
+// R = 128 (or 64) + maxshift rows per channel block feeds every tap: tap t is the same window read from row
+// shift(t) = (t / Tw) * Ws + t % Tw on (128-byte-swizzled descriptors stay valid under whole-row shifts).
+//   TCONV_FWD   : D[row][n] = sum_t sum_c X[row + shift(t)][c] W_t[n][c]; B = packed forward weights, resident
+//   TCONV_DGRAD : D[row][c] = sum_t sum_n dZ[row - shift(t)][n] W_t[n][c] (dZ in the layer's input-grid geometry,
+//                 zero outside the Ho x Wo outputs); B = packed data-gradient weights, resident; epilogue
+//                 x [X > 0] (ReLU') and inverse space-to-depth into the previous layer's dZ (same geometry)
+//   TCONV_WGRAD : D[(t, c)][n] = sum_rows X[row + shift(t)][c] dZ[row][n] over a K range of rows (MN-major
+//                 operands, two 64-row (t, c-block) halves per M tile, plus one all-ones half giving db);
+//                 per-range partials, reduced in range order by gconv_wreduce (deterministic)
+enum { TCONV_FWD = 0, TCONV_DGRAD = 1, TCONV_WGRAD = 2 };
+struct TConvArgs {
+  CUtensorMap ta[2];               // the A source rows per group: box {64, R}
+  CUtensorMap tb[2];               // FWD / DGRAD: packed weights [BN][T*64*Cblk] (box {64, BN}); WGRAD: dZ rows (box {64, 64})
+  int mode, groups;
+  int M;                           // FWD / DGRAD: rows (b * Hs*Ws); WGRAD: T * Cs (+ the ones rows)
+  int BN;                          // MMA N: FWD N, DGRAD Cs, WGRAD 64
+  int T, Tw, Ws, HsWs, Cblk;       // taps, tap width, grid width, grid pixels, 64-channel blocks of A
+  int R, maxshift;                 // window rows, largest tap shift
+  int stages;
+  // FWD epilogue
+  int Ho, Wo, N, s_next;
+  float scale;
+  const float* bias[2];
+  __nv_bfloat16* cout[2];
+  // DGRAD epilogue
+  const __nv_bfloat16* xmask;      // layer input activation [rows][Cs] (post-ReLU: the mask of ReLU')
+  __nv_bfloat16* dzprev;           // previous layer's dZ, input-grid geometry [b * prevHsWs][Cp]
+  int s, Cp, prevWs, prevHsWs, Cs;
+  // WGRAD: K rows = b * Hs*Ws split into ranges of kpr chunks of 64 rows
+  long long krows;
+  int kpr, ranges, TCs, Nout;
+  float* partial;                  // [ranges][TCs][Nout]
+  float* partial_db;               // [ranges][Nout]
+};
+bool init_tconv_kernel_attrs();
+size_t tconv_smem(const TConvArgs& a);  // 0: does not fit
+void launch_tconv(const TConvArgs& a, int num_sms, cudaStream_t st);
+void launch_gconv_wreduce(const GConvWgradArgs& a, cudaStream_t st);
+// layer 1 of the generic path: sample (a1) and gather + convert (a2) every s / s' slot of the step into the
+// bf16 s2d grid [b][21][21][64] per group, which the TMA convolution reads
+void launch_gather_s2d(const GConvFwdArgs& a, __nv_bfloat16* x1_0, __nv_bfloat16* x1_1, int groups, cudaStream_t st);
+bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld, int box_rows);
+void launch_tgemm(const TGemmArgs& a, int num_sms, cudaStream_t st);
+bool init_tma_kernel_attrs();  // false: the kernel cannot get its shared memory (the older GEMMs are used)
 // pipelined tcgen05 GEMM (generic path FC layers): K split into chunks of 64 (kper % 64 == 0)
 void launch_gemm_pipe(const TcGemmArgs& a, int groups, cudaStream_t st);
 void launch_fc_reduce(const TcGemmArgs& a, int groups, cudaStream_t st);
@@ -436,6 +513,8 @@ void launch_tc_gemm(const TcGemmArgs& a, int groups, cudaStream_t st);
 // one launch: the tiles of GEMM p0, the tiles of GEMM p1 (single split, group 0 each), then the
 // cross-sample TD-head finish (head_finish.cuh) — the bf16 path's whole FC backward
 void launch_tc_pair_with_head(const TcGemmArgs& p0, const TcGemmArgs& p1, const HeadArgs& head, cudaStream_t st);
+// the whole K of both GEMMs fits tc_pair's shared-memory staging (else: gemm_pipe x 2 + head_finish_warp)
+bool tc_pair_fits(const TcGemmArgs& p0, const TcGemmArgs& p1);
 void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st, bool with_reduce = true);
 
 }  // namespace dqn

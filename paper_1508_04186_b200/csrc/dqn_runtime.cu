@@ -76,6 +76,18 @@ struct dqn_ctx {
     __nv_bfloat16* dz = nullptr;            // output gradient [b][Ho][Wo][N]
   } gl[kMaxConv];
   int2* pack_map = nullptr;                 // [pack_n]: packed slots of each canonical conv parameter
+  // the FC layers on the warp-specialised TMA GEMM (kernels_tma.cu; DQN_TGEMM=0: the older tcgen05 GEMMs)
+  bool use_tgemm = false;
+  TGemmArgs tg_fwd{}, tg_dw{}, tg_dx{};
+  // the conv forward on the same TMA GEMM (implicit GEMM over virtual rows); layer 1 reads a bf16 s2d grid
+  // gathered from the replay by gather_s2d_kernel (x1[g], [b][441][64])
+  bool use_tconv = false;
+  TConvArgs tc_fwd[kMaxConv]{}, tc_dgrad[kMaxConv]{}, tc_wgrad[kMaxConv]{};
+  GConvWgradArgs tc_wred[kMaxConv]{};
+  __nv_bfloat16* x1[2] = {};
+  __nv_bfloat16* dzp[kMaxConv] = {};          // dZ of every conv layer in its input-grid geometry (zero borders)
+  float* tc_part = nullptr;
+  float* tc_part_db = nullptr;
   long long pack_n = 0, gpack_off = -1;
   float* gw_partial = nullptr;
   float* gw_partial_db = nullptr;
@@ -294,7 +306,7 @@ static const char* gpath_unsupported(const NetShape& net, const dqn_config* c) {
     if (L.N % 64 != 0) return "DQN_BF16: filters of convs after the first must be a multiple of 64";
   }
   const FcShape& F = net.fc[0];
-  if (F.D % 16 != 0 || F.H % 16 != 0 || F.H > 512) return "DQN_BF16: FC sizes must be multiples of 16 (units <= 512)";
+  if (F.D % 16 != 0 || F.H % 16 != 0 || F.H > 4096) return "DQN_BF16: FC sizes must be multiples of 16 (units <= 4096)";
   if (c->minibatch % 16 != 0 || c->minibatch > 512) return "DQN_BF16 needs minibatch % 16 == 0 and <= 512";
   return nullptr;
 }
@@ -329,11 +341,8 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
     const bool mnih = is_mnih_stack(c);
     if (mnih) {
       if (c->minibatch % 16 != 0 || c->minibatch > 256) { *why = "DQN_BF16 needs minibatch % 16 == 0 and <= 256"; return DQN_EINVAL; }
-      if (c->fc_units[0] % 16 != 0 || c->fc_units[0] > 1024) { *why = "DQN_BF16 needs fc units % 16 == 0"; return DQN_EINVAL; }
-      // the FC dX GEMM (tc_pair) stages its whole K = fc units of W and dH in shared memory (200 KB budget)
-      if ((128LL + c->minibatch) * c->fc_units[0] * 2 > 200 * 1024) {
-        *why = "DQN_BF16 (Mnih stack): (128 + minibatch) * fc_units * 2 bytes must fit 200 KB (FC dX staging)";
-        return DQN_EINVAL;
+      if (c->fc_units[0] % 16 != 0 || c->fc_units[0] > 4096) {
+        *why = "DQN_BF16 needs fc units % 16 == 0 and <= 4096"; return DQN_EINVAL;
       }
       return DQN_OK;
     }
@@ -415,6 +424,12 @@ static void free_all(dqn_ctx* c) {
       if (p) cudaFree(p);
   }
   if (c->gw_partial) cudaFree(c->gw_partial);
+  for (auto* x : c->x1)
+    if (x) cudaFree(x);
+  for (auto* x : c->dzp)
+    if (x) cudaFree(x);
+  if (c->tc_part) cudaFree(c->tc_part);
+  if (c->tc_part_db) cudaFree(c->tc_part_db);
   if (c->gw_partial_db) cudaFree(c->gw_partial_db);
   for (int i = 0; i < 2; ++i) {
     if (c->h_stage[i]) cudaFreeHost(c->h_stage[i]);
@@ -560,6 +575,124 @@ static int setup_fused_comm(dqn_ctx* ctx) {
   return DQN_OK;
 }
 
+// The FC layers (a5, a7) on the warp-specialised TMA GEMM: forward split-K partials (the TD head reduces
+// them), dW into G, dX (x ReLU mask) into the last conv layer's NHWC dZ. Tensor maps are built once here (the
+// buffers never move); any refusal leaves the older tcgen05 GEMMs in place.
+static void setup_tgemm_fc(dqn_ctx* ctx) {
+  const char* e = getenv("DQN_TGEMM");
+  if ((e && atoi(e) == 0) || !init_tma_kernel_attrs()) return;
+  const FcShape& F = ctx->net.fc[0];
+  const int b = ctx->cfg.minibatch, D = F.D, H = F.H;
+  const int sp = ctx->fc_splits, kper = (((D + 63) / 64 + sp - 1) / sp) * 64;
+  if ((sp - 1) * kper >= D) return;  // an empty split
+  const __nv_bfloat16* W[2] = {ctx->theta_local_bf16 + F.w_off, ctx->theta_hat_bf16 + F.w_off};
+  const dqn_ctx::GLayer& GL = ctx->gl[ctx->net.n_conv - 1];
+  bool ok = true;
+  TGemmArgs& f = ctx->tg_fwd;  // h^T [H][b] = W [H][D] a2^T, K-major operands
+  f.M = H; f.N = b; f.K = D; f.kper = kper; f.splits = sp; f.BN = std::min(128, (b + 15) / 16 * 16);
+  f.a_mn = 0; f.b_mn = 0; f.groups = 2; f.epi = TC_EPI_FC_FWD; f.partial = ctx->fc_partial;
+  for (int g = 0; g < 2; ++g) {
+    ok = ok && make_tmap_bf16(&f.ta[g], W[g], H, D, D, 128);
+    ok = ok && make_tmap_bf16(&f.tb[g], ctx->a2_bf16 + (long long)g * b * D, b, D, D, f.BN);
+  }
+  TGemmArgs& w = ctx->tg_dw;  // dW [H][D] = dH^T a2: both operands MN-major over K = b
+  w.M = H; w.N = D; w.K = b; w.kper = b; w.splits = 1; w.BN = 64;
+  w.a_mn = 1; w.b_mn = 1; w.groups = 1; w.epi = TC_EPI_ACCUM; w.store = ctx->cfg.n_push == 1;
+  w.C[0] = ctx->grad + F.w_off; w.ldc = D;
+  ok = ok && make_tmap_bf16(&w.ta[0], ctx->dh_bf16, b, H, H, 64);
+  ok = ok && make_tmap_bf16(&w.tb[0], ctx->a2_bf16, b, D, D, 64);
+  TGemmArgs& x = ctx->tg_dx;  // dZ [b][D] = [a2 > 0] dH W: A = W MN-major over K = H, B = dH K-major
+  x.M = D; x.N = b; x.K = H; x.kper = H; x.splits = 1; x.BN = 64;
+  x.a_mn = 1; x.b_mn = 0; x.groups = 1; x.epi = TC_EPI_MASK_T;
+  x.out_bf16 = GL.dz; x.mask = ctx->a2_bf16; x.ldo = D; x.hwc_HW = GL.Ho * GL.Wo; x.hwc_C = GL.N;
+  ok = ok && make_tmap_bf16(&x.ta[0], W[0], H, D, D, 64);
+  ok = ok && make_tmap_bf16(&x.tb[0], ctx->dh_bf16, b, H, H, x.BN);
+  ctx->use_tgemm = ok;
+  if (!ok || ((e = getenv("DQN_TCONV")) && atoi(e) == 0) || !init_tconv_kernel_attrs()) return;
+  // every conv layer on the TMA tap-window kernel (kernels_tma.cu): forward (theta on s, theta^ on s'), data
+  // gradient of every layer but the first, weight gradient (+ db) as per-range partials reduced in order
+  const NetShape& net = ctx->net;
+  const int nl = net.n_conv;
+  for (int g = 0; g < 2; ++g)
+    if (dalloc(ctx, &ctx->x1[g], (long long)b * 441 * 64)) return;
+  long long max_part = 0, max_db = 0;
+  for (int i = 0; i < nl && ok; ++i) {
+    const ConvShape& L = net.conv[i];
+    const dqn_ctx::GLayer& G = ctx->gl[i];
+    const int T = G.Th * G.Tw, K = T * G.Cs, HsWs = G.Hs * G.Ws, maxshift = (G.Th - 1) * G.Ws + (G.Tw - 1);
+    const long long rows = (long long)b * HsWs;
+    if (G.Cs % 64 != 0 || L.N % 16 != 0 || L.N > 256 || (i > 0 && L.N % 64 != 0) || 128 + maxshift > 256) {
+      ok = false;
+      break;
+    }
+    if (dalloc(ctx, &ctx->dzp[i], rows * L.N)) return;
+    if (cudaMemset(ctx->dzp[i], 0, sizeof(__nv_bfloat16) * rows * L.N) != cudaSuccess) return;
+    const __nv_bfloat16* x[2] = {i == 0 ? ctx->x1[0] : G.x[0], i == 0 ? ctx->x1[1] : G.x[1]};
+    // forward
+    TConvArgs& f = ctx->tc_fwd[i];
+    f.mode = TCONV_FWD; f.groups = 2; f.M = (int)rows; f.BN = L.N;
+    f.T = T; f.Tw = G.Tw; f.Ws = G.Ws; f.HsWs = HsWs; f.Cblk = G.Cs / 64; f.maxshift = maxshift; f.R = 128 + maxshift;
+    f.Ho = G.Ho; f.Wo = G.Wo; f.N = L.N; f.s_next = i + 1 < nl ? ctx->gl[i + 1].s : 0;
+    f.scale = i == 0 ? 1.0f / 255.0f : 1.0f;
+    const __nv_bfloat16* wpk[2] = {ctx->theta_local_bf16 + ctx->gpack_off + G.fwd_pack,
+                                   ctx->theta_hat_bf16 + ctx->gpack_off + G.fwd_pack};
+    for (int g = 0; g < 2; ++g) {
+      ok = ok && make_tmap_bf16(&f.ta[g], x[g], rows, G.Cs, G.Cs, f.R);
+      ok = ok && make_tmap_bf16(&f.tb[g], wpk[g], L.N, K, K, L.N);
+      f.bias[g] = (g ? ctx->theta_hat : ctx->theta_local) + L.b_off;
+      f.cout[g] = i + 1 < nl ? ctx->gl[i + 1].x[g] : ctx->a2_bf16 + (long long)g * b * F.D;
+    }
+    ok = ok && tconv_smem(f) > 0;
+    // weight gradient: M = (tap, c') rows + the all-ones block (db), K = rows split into ranges
+    TConvArgs& w = ctx->tc_wgrad[i];
+    w.mode = TCONV_WGRAD; w.groups = 1; w.TCs = K; w.M = K + 64; w.BN = 64;
+    w.T = T; w.Tw = G.Tw; w.Ws = G.Ws; w.HsWs = HsWs; w.Cblk = G.Cs / 64; w.maxshift = maxshift; w.R = 64 + maxshift;
+    w.krows = rows; w.Nout = L.N;
+    const long long chunks = (rows + 63) / 64;
+    const int m_tiles = (w.M + 127) / 128;
+    w.ranges = (int)std::max<long long>(1, std::min<long long>(chunks, (2LL * ctx->num_sms + m_tiles - 1) / m_tiles));
+    w.kpr = (int)((chunks + w.ranges - 1) / w.ranges);
+    w.ranges = (int)((chunks + w.kpr - 1) / w.kpr);
+    ok = ok && L.N <= 64 && make_tmap_bf16(&w.ta[0], x[0], rows, G.Cs, G.Cs, w.R);
+    ok = ok && make_tmap_bf16(&w.tb[0], ctx->dzp[i], rows, L.N, L.N, 64);
+    ok = ok && tconv_smem(w) > 0;
+    max_part = std::max(max_part, (long long)w.ranges * K * L.N);
+    max_db = std::max(max_db, (long long)w.ranges * L.N);
+    GConvWgradArgs& r = ctx->tc_wred[i];
+    r.Th = G.Th; r.Tw = G.Tw; r.Cs = G.Cs; r.N = L.N; r.b = w.ranges; r.ipc = 1; r.first = i == 0;
+    r.w_canon = G.w_canon; r.w_off = L.w_off; r.w_nstride = (long long)L.C * L.k * L.k; r.b_off = L.b_off;
+    r.grad = ctx->grad; r.store = ctx->cfg.n_push == 1;
+    // data gradient (layers after the first): A = this layer's dZ, B = the packed data-gradient weights
+    if (i > 0) {
+      TConvArgs& d = ctx->tc_dgrad[i];
+      const dqn_ctx::GLayer& GP = ctx->gl[i - 1];
+      d.mode = TCONV_DGRAD; d.groups = 1; d.M = (int)rows; d.BN = G.Cs;
+      d.T = T; d.Tw = G.Tw; d.Ws = G.Ws; d.HsWs = HsWs; d.Cblk = L.N / 64; d.maxshift = maxshift;
+      d.R = 128 + maxshift;
+      d.xmask = G.x[0]; d.s = G.s; d.Cp = G.Cs / (G.s * G.s); d.Cs = G.Cs;
+      d.prevWs = GP.Ws; d.prevHsWs = GP.Hs * GP.Ws;
+      ok = ok && G.Cs <= 256 && make_tmap_bf16(&d.ta[0], ctx->dzp[i], rows, L.N, L.N, d.R);
+      ok = ok && make_tmap_bf16(&d.tb[0], ctx->theta_local_bf16 + ctx->gpack_off + G.dg_pack, G.Cs, T * L.N,
+                                T * L.N, G.Cs);
+      ok = ok && tconv_smem(d) > 0;
+    }
+  }
+  if (ok) {
+    ok = !dalloc(ctx, &ctx->tc_part, max_part) && !dalloc(ctx, &ctx->tc_part_db, max_db);
+    for (int i = 0; i < nl && ok; ++i) {
+      ctx->tc_wgrad[i].partial = ctx->tc_part; ctx->tc_wgrad[i].partial_db = ctx->tc_part_db;
+      ctx->tc_wred[i].partial = ctx->tc_part; ctx->tc_wred[i].partial_db = ctx->tc_part_db;
+      if (i > 0) ctx->tc_dgrad[i].dzprev = ctx->dzp[i - 1];
+    }
+    // FC dX writes the last conv layer's dZ in its input-grid geometry
+    const dqn_ctx::GLayer& GL2 = ctx->gl[nl - 1];
+    ctx->tg_dx.out_bf16 = ctx->dzp[nl - 1];
+    ctx->tg_dx.hwc_Wo = GL2.Wo; ctx->tg_dx.hwc_Ws = GL2.Ws;
+    ctx->tg_dx.ldo_out = (long long)GL2.Hs * GL2.Ws * GL2.N;
+  }
+  ctx->use_tconv = ok;
+}
+
 // Generic bf16 conv path (kernels_conv.cu): layer geometry, packed-weight maps, buffers.
 static int setup_gpath(dqn_ctx* ctx) {
   const NetShape& net = ctx->net;
@@ -654,6 +787,7 @@ static int setup_gpath(dqn_ctx* ctx) {
   if ((rc = dalloc(ctx, &ctx->q_stage_s2d, (long long)b * kMnihSlot))) return rc;
   if ((rc = dalloc(ctx, &ctx->gw_partial, max_part))) return rc;
   if ((rc = dalloc(ctx, &ctx->gw_partial_db, max_db))) return rc;
+  setup_tgemm_fc(ctx);
   return DQN_OK;
 }
 
@@ -785,6 +919,7 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   if (ctx->gpath && (rc = setup_gpath(ctx))) return rc;
   if (ctx->bf16 && !ctx->gpath) {
     init_bf16_kernel_attrs();
+    init_conv_kernel_attrs();  // gemm_pipe: the FC backward of FC layers too wide for tc_pair
     const int H = net.fc[0].H;
     ctx->fc_splits = 18;  // K = 2592 = 18 x 144
     ctx->img_off = ctx->P_pad;
@@ -1360,11 +1495,20 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   gx.M = F.D; gx.N = b; gx.K = F.H; gx.BN = b <= 32 ? 16 : 64; gx.kper = F.H; gx.splits = 1;
   gx.epi = TC_EPI_MASK_T; gx.out_bf16 = ctx->dz2_bf16; gx.mask = ctx->a2_bf16; gx.ldo = F.D;
   gx.pre_a = 1; gx.pre_b = 0;  // W is published by the previous step's update; dH by the predecessor
-  PB("fc1_bwd_head_finish", 1);
   gw.st_id = gx.st_id = ST_FC_BWD;
   gw.st_ph = ST_P3; gx.st_ph = ST_P4;
-  launch_tc_pair_with_head(gw, gx, h, st);
-  PE();
+  if (tc_pair_fits(gw, gx)) {
+    PB("fc1_bwd_head_finish", 1);
+    launch_tc_pair_with_head(gw, gx, h, st);
+    PE();
+  } else {  // wide FC layers: K-pipelined GEMMs (any fc), then the head finish
+    gw.BN = 64; gx.BN = 64;
+    PB("fc1_bwd_head_finish", 3);
+    launch_gemm_pipe(gw, 1, st);
+    launch_gemm_pipe(gx, 1, st);
+    launch_head_finish_warp(h, st);
+    PE();
+  }
   // a8/a9 conv backward
   BwdConvArgs ba{};
   ba.ring_s = ctx->ring_s; ba.slot_stride = ctx->slot_stride; ba.idx = ctx->idx; ba.a1_save = ctx->a1_save; ba.dz2 = ctx->dz2_bf16;
@@ -1471,8 +1615,15 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     PE();
   }
   // a1-a4s: sample + gather (layer 1) and every conv forward, s with theta and s' with theta^
-  PB("conv_fwd", nl);
-  for (int i = 0; i < nl; ++i) {
+  PB("conv_fwd", ctx->use_tconv ? nl + 1 : nl);
+  if (ctx->use_tconv) {
+    GConvFwdArgs ga{};
+    ga.ring[0] = ctx->ring_s; ga.ring[1] = ctx->ring_sn; ga.slot_stride = ctx->slot_stride;
+    ga.idx = ctx->idx; ga.ctr = ctx->ctr; ga.seed = c.seed; ga.rank = (unsigned)ctx->rank; ga.b = b;
+    launch_gather_s2d(ga, ctx->x1[0], ctx->x1[1], 2, st);
+    for (int i = 0; i < nl; ++i) launch_tconv(ctx->tc_fwd[i], ctx->num_sms, st);
+  }
+  for (int i = 0; i < nl && !ctx->use_tconv; ++i) {
     const ConvShape& L = net.conv[i];
     const dqn_ctx::GLayer& G = ctx->gl[i];
     GConvFwdArgs a{};
@@ -1499,7 +1650,8 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   gf.M = F.H; gf.N = b; gf.K = F.D; gf.BN = std::min(b, 128); gf.kper = F.D / ctx->fc_splits; gf.splits = ctx->fc_splits;
   gf.epi = TC_EPI_FC_FWD; gf.partial = ctx->fc_partial;
   PB("fc1_fwd", 1);
-  launch_gemm_pipe(gf, 2, st);
+  if (ctx->use_tgemm) launch_tgemm(ctx->tg_fwd, ctx->num_sms, st);
+  else launch_gemm_pipe(gf, 2, st);
   PE();
   // a6 head
   HeadArgs h{};
@@ -1537,12 +1689,31 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   // one launch: the FC dW and dX tiles plus the head finish CTAs run side by side (tc_pair); the
   // whole K (= b and H <= 512) is staged at once, which the 200 KB budget allows at BN = 64
   gx.pre_a = 1; gx.pre_b = 0; gw.pre_a = 0; gw.pre_b = 1;
-  PB("fc1_bwd_head_finish", 1);
-  launch_tc_pair_with_head(gw, gx, h, st);
-  PE();
+  if (ctx->use_tgemm) {  // the warp-specialised TMA GEMMs, then the head finish
+    PB("fc1_bwd_head_finish", 3);
+    launch_tgemm(ctx->tg_dw, ctx->num_sms, st);
+    launch_tgemm(ctx->tg_dx, ctx->num_sms, st);
+    launch_head_finish_warp(h, st);
+    PE();
+  } else if (tc_pair_fits(gw, gx)) {
+    PB("fc1_bwd_head_finish", 1);
+    launch_tc_pair_with_head(gw, gx, h, st);
+    PE();
+  } else {  // FC widths whose whole K does not fit tc_pair's staging: K-pipelined GEMMs, then the head finish
+    PB("fc1_bwd_head_finish", 3);
+    launch_gemm_pipe(gw, 1, st);
+    launch_gemm_pipe(gx, 1, st);
+    launch_head_finish_warp(h, st);
+    PE();
+  }
   // a8/a9: per layer, top down: wgrad (+ range reduction into G), then dgrad into the layer below
   PB("conv_bwd", 3 * nl - 1);
-  for (int i = nl - 1; i >= 0; --i) {
+  for (int i = nl - 1; i >= 0 && ctx->use_tconv; --i) {
+    launch_tconv(ctx->tc_wgrad[i], ctx->num_sms, st);
+    launch_gconv_wreduce(ctx->tc_wred[i], st);
+    if (i > 0) launch_tconv(ctx->tc_dgrad[i], ctx->num_sms, st);
+  }
+  for (int i = nl - 1; i >= 0 && !ctx->use_tconv; --i) {
     const ConvShape& L = net.conv[i];
     const dqn_ctx::GLayer& G = ctx->gl[i];
     GConvWgradArgs w{};
@@ -1996,7 +2167,7 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
   }
   if (hc.bad_input & 0x80000000u)
     return set_err(ctx, DQN_ECUDA, "fused server round: peer barrier timed out (ranks out of step?)");
-  if (ctx->gpath && gconv_error())
+  if (ctx->bf16 && gconv_error())
     return set_err(ctx, DQN_ECUDA, "generic conv kernel: an MMA completion was never signalled (bounded wait expired)");
   if (hc.T != (unsigned long long)ctx->T)
     return set_err(ctx, DQN_ECUDA, "device step counters diverged from the host schedule");

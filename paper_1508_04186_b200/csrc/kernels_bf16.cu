@@ -24,7 +24,6 @@
 #include "wimg.cuh"
 #include "philox.cuh"
 #include "sm100.cuh"
-#include "stage.cuh"
 
 namespace dqn {
 using namespace dqn_sm100;
@@ -361,16 +360,29 @@ __host__ __device__ __forceinline__ bool tc_mask_fits(const TcGemmArgs& a) {
   return (long long)(128 + a.BN) * a.kper * 2 + (long long)a.BN * 256 <= 200 * 1024;
 }
 
-// B (BN rows x KC) into [kc][n][8] (K-major) or [n/8][k][8] (MN-major), 16-byte async copies (stage.cuh)
+// B (BN rows x KC) into [kc][n][8] (K-major) or [n/8][k][8] (MN-major), 16-byte async copies
 __device__ __forceinline__ void stage_b_operand(const TcGemmArgs& a, const __nv_bfloat16* Bg, uint8_t* sB, int n0,
                                                 int k0, int KC, int kch) {
-  const int N = a.N;
-  if (!a.b_mn)
-    stage_kmajor(sB, Bg + (long long)n0 * a.ldb + k0, a.ldb, a.BN, kch, kch, [&](int r) { return n0 + r < N; },
-                 threadIdx.x, blockDim.x);
-  else
-    stage_mnmajor(sB, Bg + (long long)k0 * a.ldb + n0, a.ldb, a.BN / 8, KC, KC,
-                  [&](int gi) { return n0 + 8 * gi < N; }, threadIdx.x, blockDim.x);
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  const int bn = a.BN;
+  if (!a.b_mn) {
+    for (int e = threadIdx.x; e < bn * kch; e += blockDim.x) {
+      const int r = e / kch, c = e % kch;
+      const int n = n0 + r;
+      uint8_t* d = sB + (c * bn + r) * 16;
+      if (n < a.N) cp_async16(d, Bg + (long long)n * a.ldb + k0 + 8 * c);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  } else {
+    const int ng = bn / 8;
+    for (int e = threadIdx.x; e < ng * KC; e += blockDim.x) {
+      const int gi = e % ng, k = e / ng;
+      const int n = n0 + 8 * gi;
+      uint8_t* d = sB + (gi * KC + k) * 16;
+      if (n < a.N) cp_async16(d, Bg + (long long)(k0 + k) * a.ldb + n);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  }
 }
 
 __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int split, int g, uint8_t* smem,
@@ -416,13 +428,23 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
     }
   }
   if (!a.pre_a) { pdl_sync(); st_stamp(a.st_id, 1); }
-  const int M = a.M;
-  if (!a.a_mn)  // K-major: smem [kc][row][8]
-    stage_kmajor(sA, Ag + (long long)m0 * a.lda + k0, a.lda, 128, kch, kch, [&](int r) { return m0 + r < M; },
-                 threadIdx.x, blockDim.x);
-  else          // MN-major: smem [row/8][k][8]
-    stage_mnmajor(sA, Ag + (long long)k0 * a.lda + m0, a.lda, 16, KC, KC, [&](int gi) { return m0 + 8 * gi < M; },
-                  threadIdx.x, blockDim.x);
+  if (!a.a_mn) {  // K-major: smem [kc][row][8]
+    for (int e = threadIdx.x; e < 128 * kch; e += blockDim.x) {
+      const int r = e / kch, c = e % kch;
+      const int m = m0 + r;
+      uint8_t* d = sA + (c * 128 + r) * 16;
+      if (m < a.M) cp_async16(d, Ag + (long long)m * a.lda + k0 + 8 * c);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  } else {        // MN-major: smem [row/8][k][8]
+    for (int e = threadIdx.x; e < 16 * KC; e += blockDim.x) {
+      const int gi = e % 16, k = e / 16;
+      const int m = m0 + 8 * gi;
+      uint8_t* d = sA + (gi * KC + k) * 16;
+      if (m < a.M) cp_async16(d, Ag + (long long)(k0 + k) * a.lda + m);
+      else *reinterpret_cast<uint4*>(d) = z4;
+    }
+  }
   const int bn = a.BN;
   // operands produced by the immediate predecessor are staged after the PDL wait (pre_a / pre_b flags)
   if (a.pre_a && !a.pre_b) { pdl_sync(); st_stamp(a.st_id, 1); }
@@ -602,6 +624,10 @@ static size_t tc_smem(const TcGemmArgs& a) {
   if (a.epi == TC_EPI_MASK_T && tc_mask_fits(a)) smem += (size_t)a.BN * 128 * 2;  // the mask tile
   if (a.epi == TC_EPI_ACCUM) smem = std::max(smem, (size_t)128 * (a.BN + 4) * 4);  // epilogue tile
   return smem;
+}
+
+bool tc_pair_fits(const TcGemmArgs& p0, const TcGemmArgs& p1) {
+  return std::max(tc_smem(p0), tc_smem(p1)) <= (size_t)200 * 1024;
 }
 
 void launch_tc_pair_with_head(const TcGemmArgs& p0, const TcGemmArgs& p1, const HeadArgs& head, cudaStream_t st) {

@@ -30,7 +30,6 @@
 #include "pdl.cuh"
 #include "philox.cuh"
 #include "sm100.cuh"
-#include "stage.cuh"
 #include "step_trace.cuh"
 
 namespace dqn {
@@ -228,7 +227,10 @@ __global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
       for (int kc = 0; kc < 8; ++kc) *reinterpret_cast<uint4*>(sA + (kc * 128 + tid) * 16) = make_uint4(0, 0, 0, 0);
     }
     // B: N rows x 8 chunks of the packed [N][K] weights
-    stage_kmajor(sB, W + (long long)c * KCH, K, a.N, 8, 8, [](int) { return true; }, tid, 128);
+    for (int e = tid; e < a.N * 8; e += 128) {
+      const int n = e >> 3, kc = e & 7;
+      cp_async16(sB + (kc * a.N + n) * 16, W + (long long)n * K + c * KCH + 8 * kc);
+    }
     cp_async_commit();
   };
   for (int c = 0; c < NS - 1; ++c) {  // prologue: chunks 0 .. NS-2 in flight
@@ -350,7 +352,10 @@ __global__ void __launch_bounds__(128) gconv_dgrad_kernel(GConvDgradArgs a) {
 #pragma unroll
       for (int kc = 0; kc < 8; ++kc) *reinterpret_cast<uint4*>(sA + (kc * 128 + tid) * 16) = make_uint4(0, 0, 0, 0);
     }
-    stage_kmajor(sB, a.wpkT + (long long)c * KCH, KT, a.Cs, 8, 8, [](int) { return true; }, tid, 128);
+    for (int e = tid; e < a.Cs * 8; e += 128) {
+      const int n = e >> 3, kc = e & 7;
+      cp_async16(sB + (kc * a.Cs + n) * 16, a.wpkT + (long long)n * KT + c * KCH + 8 * kc);
+    }
     cp_async_commit();
   };
   for (int c = 0; c < NS - 1; ++c) {
@@ -613,6 +618,12 @@ bool gconv_wgrad_fits(int N, int first, int ipc, int HoWo) {
   return gconv_wgrad_smem(N, first, ipc, HoWo) <= g_wgrad_smem_cap;
 }
 
+void launch_gconv_wreduce(const GConvWgradArgs& a, cudaStream_t st) {
+  const long long n = (long long)a.Th * a.Tw * a.Cs * a.N + a.N;
+  launch_pdl(gconv_wreduce_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, st, a);
+  gconv_debug("gconv_wreduce", st);
+}
+
 void launch_gconv_wgrad(const GConvWgradArgs& a, cudaStream_t st) {
   const int T = a.Th * a.Tw, MK = T * a.Cs;
   const int ranges = (a.b + a.ipc - 1) / a.ipc;
@@ -681,19 +692,37 @@ __global__ void __launch_bounds__(128) gemm_pipe_kernel(TcGemmArgs a) {
     uint8_t* sA = smem + buf * SB;
     uint8_t* sB = sA + A_BYTES;
     const int kb = k0 + c * KCH, klen = min(KCH, KC - c * KCH);  // the last chunk may be short
-    const int M = a.M, N = a.N;
-    if (!a.a_mn)  // [kc][128][8]
-      stage_kmajor(sA, Ag + (long long)m0 * a.lda + kb, a.lda, 128, 8, (klen + 7) / 8,
-                   [&](int r) { return m0 + r < M; }, tid, 128);
-    else          // [16][64 k][8]
-      stage_mnmajor(sA, Ag + (long long)kb * a.lda + m0, a.lda, 16, KCH, klen,
-                    [&](int gi) { return m0 + 8 * gi < M; }, tid, 128);
-    if (!a.b_mn)  // [kc][bn][8]
-      stage_kmajor(sB, Bg + (long long)n0 * a.ldb + kb, a.ldb, bn, 8, (klen + 7) / 8,
-                   [&](int r) { return n0 + r < N; }, tid, 128);
-    else          // [bn/8][64 k][8]
-      stage_mnmajor(sB, Bg + (long long)kb * a.ldb + n0, a.ldb, bn / 8, KCH, klen,
-                    [&](int gi) { return n0 + 8 * gi < N; }, tid, 128);
+    if (!a.a_mn) {  // [kc][128][8]
+      for (int e = tid; e < 128 * 8; e += 128) {
+        const int r = e >> 3, kc = e & 7, m = m0 + r;
+        uint8_t* d = sA + (kc * 128 + r) * 16;
+        if (m < a.M && 8 * kc < klen) cp_async16(d, Ag + (long long)m * a.lda + kb + 8 * kc);
+        else *reinterpret_cast<uint4*>(d) = z4;
+      }
+    } else {        // [16][64 k][8]
+      for (int e = tid; e < 16 * KCH; e += 128) {
+        const int gi = e & 15, k = e >> 4, m = m0 + 8 * gi;
+        uint8_t* d = sA + (gi * KCH + k) * 16;
+        if (m < a.M && k < klen) cp_async16(d, Ag + (long long)(kb + k) * a.lda + m);
+        else *reinterpret_cast<uint4*>(d) = z4;
+      }
+    }
+    if (!a.b_mn) {  // [kc][bn][8]
+      for (int e = tid; e < bn * 8; e += 128) {
+        const int r = e >> 3, kc = e & 7, n = n0 + r;
+        uint8_t* d = sB + (kc * bn + r) * 16;
+        if (n < a.N && 8 * kc < klen) cp_async16(d, Bg + (long long)n * a.ldb + kb + 8 * kc);
+        else *reinterpret_cast<uint4*>(d) = z4;
+      }
+    } else {        // [bn/8][64 k][8]
+      const int ng = bn / 8;
+      for (int e = tid; e < ng * KCH; e += 128) {
+        const int gi = e % ng, k = e / ng, n = n0 + 8 * gi;
+        uint8_t* d = sB + (gi * KCH + k) * 16;
+        if (n < a.N && k < klen) cp_async16(d, Bg + (long long)(kb + k) * a.ldb + n);
+        else *reinterpret_cast<uint4*>(d) = z4;
+      }
+    }
     cp_async_commit();
   };
   for (int c = 0; c < NS - 1; ++c) {

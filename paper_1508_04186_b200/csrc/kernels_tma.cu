@@ -1,0 +1,651 @@
+// kernels_tma.cu — warp-specialised, persistent tcgen05 GEMM fed by TMA (the FC layers of the large-batch
+// configurations, a5 / a7: BASELINE.json configs[3] and [4]).
+//
+//   D[m][n] = sum_k A(m, k) B(n, k), one 128 x BN output tile per (group, m-tile, n-tile, k-split);
+//   A and B are 2-D bf16 tensors read by TMA (cp.async.bulk.tensor) in 64-element boxes with the 128-byte
+//   swizzle, i.e. directly in the UMMA SW128 canonical layouts: K-major boxes [rows][64 k] or MN-major
+//   boxes [64 k][64 mn] (two / BN/64 of them per stage).
+//
+// Roles (192 threads): warp 0 = TMA producer (one thread), warp 1 = MMA issuer (one thread; it also owns the
+// TMEM allocation), warps 2..5 = epilogue (128 threads = the 128 TMEM lanes: warp w reads lanes 32 (w % 4) ..).
+// A ring of `stages` shared-memory stages (full / empty mbarriers) and TWO TMEM accumulators (tfull / tempty):
+// the epilogue of tile i overlaps the MMAs of tile i + 1, and a persistent CTA walks tiles
+// blockIdx.x, blockIdx.x + gridDim.x, ...
+//
+// Epilogues (TcGemmArgs semantics, kernels_bf16.cu):
+//   TC_EPI_FC_FWD : partial[g][split][n][m] = D            (split-K partials; the TD head reduces them)
+//   TC_EPI_ACCUM  : C[g][m * ldc + n] = D (store) or += D   (FC dW into G)
+//   TC_EPI_MASK_T : out[n * ldo + m'] = mask[n * ldo + m] > 0 ? D : 0, m' = NHWC remap (FC dX, ReLU')
+#include <cuda.h>  // CUtensorMap and the encode entry point's types (fetched from the driver at run time)
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "dqn_internal.h"
+#include "pdl.cuh"
+#include "philox.cuh"
+#include "sm100.cuh"
+
+namespace dqn {
+using namespace dqn_sm100;
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn f = nullptr;
+  if (!f) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return f;
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// UMMA shared-memory descriptor with the 128-byte swizzle (layout type 2, Blackwell version 1)
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ bool bf16_gt0(unsigned short h) { return (h & 0x8000u) == 0 && h != 0; }
+
+constexpr int TG_THREADS = 192;
+constexpr int TG_A_BYTES = 128 * 64 * 2;  // one A stage: 128 rows x 64 k (or 64 k x 2 x 64 m)
+
+}  // namespace
+
+// DQN_SYNC_DEBUG=1 (with DQN_NO_GRAPH=1): synchronise after every launch of this file and name the first
+// kernel that faults
+static void sync_debug(const char* what, cudaStream_t st) {
+  static const int on = getenv("DQN_SYNC_DEBUG") ? atoi(getenv("DQN_SYNC_DEBUG")) : 0;
+  if (!on) return;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  fprintf(stderr, "[sync debug] %s: %s\n", what, cudaGetErrorString(e));
+  if (e != cudaSuccess) exit(3);
+}
+
+// A 2-D bf16 tensor [rows][cols] (cols contiguous, row pitch ld elements) read in boxes of box_rows x 64
+// columns with the 128-byte swizzle. Returns false when the driver entry point is missing or refuses.
+bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld, int box_rows) {
+  EncodeTiledFn f = encode_fn();
+  if (!f || (ld * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+__global__ void __launch_bounds__(TG_THREADS, 2) tgemm_kernel(const __grid_constant__ TGemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kTgMaxStages], empty[kTgMaxStages], tfull[2], tempty[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = a.stages, BN = a.BN;
+  const int B_BYTES = BN * 64 * 2, STAGE = TG_A_BYTES + B_BYTES;
+  const uint32_t tcols = BN <= 16 ? 32 : BN <= 32 ? 64 : BN <= 64 ? 128 : BN <= 128 ? 256 : 512;  // 2 accumulators
+  const int m_tiles = (a.M + 127) / 128, n_tiles = (a.N + BN - 1) / BN;
+  const int tiles = m_tiles * n_tiles * a.splits * a.groups;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&tbase, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_sync();  // operands come from the immediate predecessor; outputs may still be read by it
+  auto decode = [&](int t, int& g, int& split, int& m0, int& n0) {
+    const int mt = t % m_tiles;
+    t /= m_tiles;
+    const int nt = t % n_tiles;
+    t /= n_tiles;
+    split = t % a.splits;
+    g = t / a.splits;
+    m0 = mt * 128;
+    n0 = nt * BN;
+  };
+  auto n_chunks = [&](int split) { return (min(a.kper, a.K - split * a.kper) + 63) / 64; };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int g, split, m0, n0;
+        decode(t, g, split, m0, n0);
+        const int nch = n_chunks(split);
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          uint8_t* sA = smem + s * STAGE;
+          uint8_t* sB = sA + TG_A_BYTES;
+          mbar_arrive_expect_tx(&full[s], STAGE);
+          const int kb = split * a.kper + c * 64;
+          if (a.epi == TC_EPI_CONV_FWD) {  // tap t, channel block cb: the same rows shifted by the tap
+            const int tp = c / a.Cblk, cb = c % a.Cblk;
+            tma_load_2d(sA, &a.ta[g], cb * 64, m0 + (tp / a.Tw) * a.Ws + tp % a.Tw, &full[s]);
+          } else if (!a.a_mn) {
+            tma_load_2d(sA, &a.ta[g], kb, m0, &full[s]);
+          } else {
+            tma_load_2d(sA, &a.ta[g], m0, kb, &full[s]);
+            tma_load_2d(sA + 8192, &a.ta[g], m0 + 64, kb, &full[s]);
+          }
+          if (!a.b_mn) {
+            tma_load_2d(sB, &a.tb[g], kb, n0, &full[s]);
+          } else {
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, &a.tb[g], n0 + 64 * j, kb, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      const uint32_t idesc = make_idesc_bf16(128, BN, a.a_mn, a.b_mn);
+      int it = 0, tl = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        int g, split, m0, n0;
+        decode(t, g, split, m0, n0);
+        const int nch = n_chunks(split);
+        const int buf = tl & 1;
+        mbar_wait(&tempty[buf], ((tl >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(buf * BN);
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int s = it % S;
+          mbar_wait(&full[s], (it / S) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + TG_A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            // K-major: +32 B per K step inside the swizzled 128-B rows; MN-major: +16 rows of 128 B
+            const uint64_t ad = a.a_mn ? desc_sw128(sa + kk * 2048, 8192, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t bd = a.b_mn ? desc_sw128(sb + kk * 2048, 8192, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
+            mma_bf16(d, ad, bd, idesc, (c > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else {  // ---- epilogue: thread = one row (TMEM lane) of the tile
+    const int q = warp & 3;
+    int tl = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+      int g, split, m0, n0;
+      decode(t, g, split, m0, n0);
+      const int buf = tl & 1;
+      mbar_wait(&tfull[buf], (tl >> 1) & 1);
+      tc_fence_after();
+      const int m = m0 + 32 * q + lane;
+      const uint32_t trow = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(trow + c, v);  // warp-collective
+        if (m >= a.M) continue;
+        if (a.epi == TC_EPI_CONV_FWD) {  // bias + ReLU (x 1/255 on layer 1) into the next layer's grid
+          const int img = m / a.HsWs, pq = m - img * a.HsWs, oy = pq / a.Ws, ox = pq - oy * a.Ws;
+          if (oy >= a.Ho || ox >= a.Wo || img >= a.M / a.HsWs) continue;
+          const float* bias = a.bias[g];
+          uint32_t o[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(fmaxf(fmaf(v[i], a.scale, __ldg(bias + c + i)), 0.0f),
+                                                            fmaxf(fmaf(v[i + 1], a.scale, __ldg(bias + c + i + 1)), 0.0f));
+            o[i >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          const int Nn = a.N, HoWo = a.Ho * a.Wo;
+          if (a.s_next == 0) {  // canonical (C,H,W) flatten: out[img][n*HoWo + p]
+            __nv_bfloat16* dst = a.cout[g] + (long long)img * Nn * HoWo + (long long)oy * a.Wo + ox;
+            const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(o);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) dst[(long long)(c + i) * HoWo] = hv[i];
+          } else {  // next grid (s2d by s_next): pixel (oy/s, ox/s), channel (iy*s + ix)*N + n
+            const int sn = a.s_next, Hn = a.Ho / sn, Wn = a.Wo / sn, Cn = Nn * sn * sn;
+            const int py = oy / sn, px = ox / sn, qq = (oy % sn) * sn + (ox % sn);
+            if (py < Hn && px < Wn) {
+              uint4* dst = reinterpret_cast<uint4*>(a.cout[g] + (((long long)img * Hn + py) * Wn + px) * Cn + qq * Nn + c);
+              dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+              dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+            }
+          }
+        } else if (a.epi == TC_EPI_FC_FWD) {
+          float* p = a.partial + ((long long)g * a.splits + split) * (long long)a.N * a.M + m;
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (n0 + c + i < a.N) p[(long long)(n0 + c + i) * a.M] = v[i];
+        } else if (a.epi == TC_EPI_ACCUM) {
+          float* crow = a.C[g] + (long long)m * a.ldc + n0 + c;
+          if (n0 + c + 16 <= a.N && a.store) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(crow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)  // (unrolled: v[] must stay in registers)
+              if (n0 + c + i < a.N) crow[i] = a.store ? v[i] : crow[i] + v[i];
+          }
+        } else {  // TC_EPI_MASK_T: all 16 mask loads in flight before the (possibly aliasing) stores
+          long long om = m;
+          if (a.hwc_HW) {
+            const int pp = m % a.hwc_HW, cc = m / a.hwc_HW;
+            om = a.hwc_Ws ? ((long long)(pp / a.hwc_Wo) * a.hwc_Ws + pp % a.hwc_Wo) * a.hwc_C + cc
+                          : (long long)pp * a.hwc_C + cc;
+          }
+          const long long ldo_out = a.ldo_out ? a.ldo_out : a.ldo;
+          unsigned short mk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = n0 + c + i;
+            mk[i] = n < a.N ? __ldg(reinterpret_cast<const unsigned short*>(a.mask) + (long long)n * a.ldo + m) : 0;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = n0 + c + i;
+            if (n < a.N) a.out_bf16[(long long)n * ldo_out + om] = __float2bfloat16_rn(bf16_gt0(mk[i]) ? v[i] : 0.0f);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, tcols);
+}
+
+// CTAs per SM (1: one persistent CTA with the deepest ring; 2: two CTAs with half the ring each, so that one
+// CTA's TMA latency overlaps the other's MMAs and epilogue on small GEMMs) and the stage count that fits
+static int tg_ctas_per_sm(int BN) {
+  static const int env = getenv("DQN_TG_CTAS") ? atoi(getenv("DQN_TG_CTAS")) : 0;
+  if (env >= 1 && env <= 2) return env;
+  return BN <= 128 ? 2 : 1;
+}
+
+// ================================================================== TMA implicit-GEMM convolutions (TConvArgs)
+namespace {
+constexpr int TC_THREADS = 192;
+__device__ __forceinline__ int tap_shift(const TConvArgs& a, int t) { return (t / a.Tw) * a.Ws + t % a.Tw; }
+__host__ __device__ __forceinline__ int win_bytes(int rows) { return (rows * 128 + 1023) / 1024 * 1024; }
+// the (t, c-block) pair of 64-row M block mb of the weight gradient; mb * 64 >= TCs: the all-ones block
+__device__ __forceinline__ void wg_block(const TConvArgs& a, int mb, int& t, int& cb) {
+  t = mb / a.Cblk;
+  cb = mb % a.Cblk;
+}
+}  // namespace
+
+// smem: FWD / DGRAD: [resident B: T*Cblk chunks x BN rows x 128 B][stages x window of R rows]
+//       WGRAD: [stages x (2 windows of R rows + a dZ tile of 64 x 128 B)][ones tile 64 x 128 B]
+__host__ __device__ __forceinline__ int tconv_stage_bytes(const TConvArgs& a) {
+  return a.mode == TCONV_WGRAD ? 2 * win_bytes(a.R) + 8192 : win_bytes(a.R);
+}
+__host__ __device__ __forceinline__ int tconv_fixed_bytes(const TConvArgs& a) {
+  return a.mode == TCONV_WGRAD ? 8192 : a.T * a.Cblk * a.BN * 128;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_constant__ TConvArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kTgMaxStages], empty[kTgMaxStages], bfull, tfull[2], tempty[2];
+  __shared__ uint32_t tbase;
+  __shared__ uint32_t s_aoff[32];  // FWD / DGRAD: tap row offsets in the window (16-byte units)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = a.stages, BN = a.BN, SB = tconv_stage_bytes(a);
+  const bool wg = a.mode == TCONV_WGRAD;
+  // FWD / DGRAD: resident B first, then the ring; WGRAD: the ring first, then the ones tile ABOVE it (the
+  // second MN half of an A tile is addressed as half 0 + LBO, so the ones block must lie above every window)
+  uint8_t* fixed = wg ? smem + S * SB : smem;
+  uint8_t* ring = wg ? smem : smem + tconv_fixed_bytes(a);
+  const uint32_t tcols = BN <= 16 ? 32 : BN <= 32 ? 64 : BN <= 64 ? 128 : BN <= 128 ? 256 : 512;
+  // work split: FWD / DGRAD tiles of 128 rows, CTA c serving group c % groups (its resident weights);
+  // WGRAD tiles (m-tile, K range)
+  const int m_tiles = (a.M + 127) / 128;
+  const int g = wg ? 0 : (int)(blockIdx.x % a.groups);
+  const int cta = wg ? blockIdx.x : blockIdx.x / a.groups;
+  const int ctas = wg ? gridDim.x : (gridDim.x - g + a.groups - 1) / a.groups;
+  const int tiles = wg ? m_tiles * a.ranges : m_tiles;
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    mbar_init(&bfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (wg) {  // the all-ones operand block (db = sum over rows of dZ); every element equal, so unswizzled
+    for (int e = tid; e < 8192 / 16; e += blockDim.x)
+      reinterpret_cast<uint4*>(fixed)[e] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    fence_async_smem();
+  }
+  if (warp == 1) tmem_alloc(&tbase, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_sync();
+  auto chunks_of = [&](int r) {  // WGRAD: 64-row chunks of K range r
+    const long long r0 = (long long)r * a.kpr * 64;
+    const long long rows = min((long long)a.kpr * 64, a.krows - r0);
+    return (int)((rows + 63) / 64);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      if (!wg) {
+        mbar_arrive_expect_tx(&bfull, (uint32_t)(a.T * a.Cblk * BN * 128));
+        for (int ch = 0; ch < a.T * a.Cblk; ++ch) tma_load_2d(fixed + ch * BN * 128, &a.tb[g], ch * 64, 0, &bfull);
+      }
+      int it = 0;
+      for (int tl = cta; tl < tiles; tl += ctas) {
+        if (!wg) {
+          const int m0 = tl * 128, row0 = a.mode == TCONV_FWD ? m0 : m0 - a.maxshift;
+          for (int cb = 0; cb < a.Cblk; ++cb, ++it) {
+            const int st = it % S;
+            mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[st], (uint32_t)(a.R * 128));
+            tma_load_2d(ring + st * SB, &a.ta[g], cb * 64, row0, &full[st]);
+          }
+        } else {
+          const int mt = tl % m_tiles, r = tl / m_tiles, nch = chunks_of(r);
+          int cbs[2], ncb = 0;
+          for (int h = 0; h < 2; ++h) {
+            const int mb = 2 * mt + h;
+            if (mb * 64 >= a.TCs) continue;
+            int t, cb;
+            wg_block(a, mb, t, cb);
+            if (ncb == 0 || cbs[0] != cb) cbs[ncb++] = cb;
+          }
+          for (int c = 0; c < nch; ++c, ++it) {
+            const int st = it % S;
+            const int p0 = (int)((long long)r * a.kpr * 64 + c * 64);
+            mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[st], (uint32_t)(ncb * a.R * 128 + 8192));
+            uint8_t* sb = ring + st * SB;
+            for (int w = 0; w < ncb; ++w) tma_load_2d(sb + w * win_bytes(a.R), &a.ta[0], cbs[w] * 64, p0, &full[st]);
+            tma_load_2d(sb + 2 * win_bytes(a.R), &a.tb[0], 0, p0, &full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      if (!wg) mbar_wait(&bfull, 0);
+      for (int t = 0; t < a.T; ++t)  // row offset of tap t in the window, in 16-byte descriptor units
+        s_aoff[t] = (uint32_t)((a.mode == TCONV_FWD ? tap_shift(a, t) : a.maxshift - tap_shift(a, t)) * 8);
+      const uint32_t idesc = wg ? make_idesc_bf16(128, BN, 1, 1) : make_idesc_bf16(128, BN, 0, 0);
+      const uint32_t fx = smem_u32(fixed);
+      int it = 0, tl_local = 0;
+      for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
+        const int buf = tl_local & 1;
+        mbar_wait(&tempty[buf], ((tl_local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(buf * BN);
+        if (!wg) {
+          for (int cb = 0; cb < a.Cblk; ++cb, ++it) {
+            const int st = it % S;
+            mbar_wait(&full[st], (it / S) & 1);
+            tc_fence_after();
+            // descriptors advance by adding to the 14-bit start-address field (16-byte units); every tap is the
+            // same window read s_aoff[t] rows later, every K step 32 bytes later
+            const uint64_t a0 = desc_sw128(smem_u32(ring + st * SB), 16, 1024);
+            const uint64_t b0 = desc_sw128(fx, 16, 1024) + (uint64_t)(cb * BN * 8);
+            for (int t = 0; t < a.T; ++t) {
+              const uint64_t at = a0 + s_aoff[t], bt = b0 + (uint64_t)(t * a.Cblk * BN * 8);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16(d, at + 2 * kk, bt + 2 * kk, idesc, (cb > 0 || t > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&empty[st]);
+          }
+        } else {
+          const int mt = tl % m_tiles, r = tl / m_tiles, nch = chunks_of(r);
+          // the two 64-row halves of the A tile: a (t, cb) window read from row shift(t), or the ones block
+          int cbs[2], ncb = 0, hoff[2];
+          bool ones[2];
+          for (int h = 0; h < 2; ++h) {
+            const int mb = 2 * mt + h;
+            ones[h] = mb * 64 >= a.TCs;
+            if (ones[h]) continue;
+            int t, cb;
+            wg_block(a, mb, t, cb);
+            if (ncb == 0 || cbs[0] != cb) cbs[ncb++] = cb;
+            hoff[h] = (cbs[0] == cb ? 0 : win_bytes(a.R)) + tap_shift(a, t) * 128;
+          }
+          for (int c = 0; c < nch; ++c, ++it) {
+            const int st = it % S;
+            mbar_wait(&full[st], (it / S) & 1);
+            tc_fence_after();
+            const uint32_t sb = smem_u32(ring + st * SB);
+            const uint32_t h0 = ones[0] ? fx : sb + hoff[0];
+            const uint32_t h1 = ones[1] ? fx : sb + hoff[1];
+            // 64-wide MN groups: half 1 at half 0 + lbo (both halves the ones block: lbo 0 - never past it)
+            const uint32_t lbo = h1 > h0 ? h1 - h0 : 0u;
+            const uint32_t bt = sb + 2 * win_bytes(a.R);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16(d, desc_sw128(h0 + kk * 2048, lbo, 1024), desc_sw128(bt + kk * 2048, 8192, 1024), idesc,
+                       (c > 0 || kk > 0) ? 1u : 0u);
+            mma_commit(&empty[st]);
+          }
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else {  // ---- epilogue: thread = one row (TMEM lane) of the tile
+    const int q = warp & 3;
+    int tl_local = 0;
+    for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
+      const int buf = tl_local & 1;
+      mbar_wait(&tfull[buf], (tl_local >> 1) & 1);
+      tc_fence_after();
+      const int mt = wg ? tl % m_tiles : tl, r = wg ? tl / m_tiles : 0;
+      const int m = mt * 128 + 32 * q + lane;
+      const uint32_t trow = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(trow + c, v);  // warp-collective
+        if (a.mode == TCONV_FWD) {
+          if (m >= a.M) continue;
+          const int img = m / a.HsWs, pq = m - img * a.HsWs, oy = pq / a.Ws, ox = pq - oy * a.Ws;
+          if (oy >= a.Ho || ox >= a.Wo) continue;
+          const float* bias = a.bias[g];
+          uint32_t o[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(fmaxf(fmaf(v[i], a.scale, __ldg(bias + c + i)), 0.0f),
+                                                            fmaxf(fmaf(v[i + 1], a.scale, __ldg(bias + c + i + 1)), 0.0f));
+            o[i >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          const int Nn = a.N, HoWo = a.Ho * a.Wo;
+          if (a.s_next == 0) {  // canonical (C,H,W) flatten: out[img][n*HoWo + p]
+            __nv_bfloat16* dst = a.cout[g] + (long long)img * Nn * HoWo + (long long)oy * a.Wo + ox;
+            const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(o);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) dst[(long long)(c + i) * HoWo] = hv[i];
+          } else {  // next grid (s2d by s_next): pixel (oy/s, ox/s), channel (iy*s + ix)*N + n
+            const int sn = a.s_next, Hn = a.Ho / sn, Wn = a.Wo / sn, Cn = Nn * sn * sn;
+            const int py = oy / sn, px = ox / sn, qq = (oy % sn) * sn + (ox % sn);
+            if (py < Hn && px < Wn) {
+              uint4* dst = reinterpret_cast<uint4*>(a.cout[g] + (((long long)img * Hn + py) * Wn + px) * Cn + qq * Nn + c);
+              dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+              dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+            }
+          }
+        } else if (a.mode == TCONV_DGRAD) {  // x [X > 0], inverse space-to-depth into the previous dZ
+          if (m >= a.M) continue;
+          const int img = m / a.HsWs, pq = m - img * a.HsWs, py = pq / a.Ws, px = pq - py * a.Ws;
+          const uint4* xm = reinterpret_cast<const uint4*>(a.xmask + (long long)m * a.Cs + c);
+          const uint4 mk0 = __ldg(xm), mk1 = __ldg(xm + 1);
+          const uint32_t mw[8] = {mk0.x, mk0.y, mk0.z, mk0.w, mk1.x, mk1.y, mk1.z, mk1.w};
+          uint32_t o[8];
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(bf16_gt0(mw[h] & 0xFFFFu) ? v[2 * h] : 0.0f,
+                                                            bf16_gt0(mw[h] >> 16) ? v[2 * h + 1] : 0.0f);
+            o[h] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          const int qq = c / a.Cp, cc = c - qq * a.Cp, iy = qq / a.s, ix = qq - iy * a.s;
+          const long long row = (long long)img * a.prevHsWs + (long long)(py * a.s + iy) * a.prevWs + (px * a.s + ix);
+          uint4* dst = reinterpret_cast<uint4*>(a.dzprev + row * a.Cp + cc);
+          dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+          dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        } else {  // TCONV_WGRAD: per-range partials of dW (rows (t, c)) and of db (the first ones row)
+          if ((m < a.TCs || m == a.TCs) && c < a.Nout) {  // Nout % 16 == 0: whole 16-column groups
+            float* p = m < a.TCs ? a.partial + ((long long)r * a.TCs + m) * a.Nout + c : a.partial_db + (long long)r * a.Nout + c;
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, tcols);
+}
+
+bool init_tconv_kernel_attrs() {
+  const bool ok = cudaFuncSetAttribute(tconv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) ==
+                  cudaSuccess;
+  cudaGetLastError();
+  return ok;
+}
+
+// the deepest ring that fits 219 KB next to the resident weights (>= 2 stages), 0: does not fit
+size_t tconv_smem(const TConvArgs& a0) {
+  const int fixed = tconv_fixed_bytes(a0), sb = tconv_stage_bytes(a0);
+  const int st = std::min(kTgMaxStages, (219 * 1024 - 1024 - fixed) / sb);
+  if (st < 2) return 0;
+  return (size_t)fixed + (size_t)st * sb + 1024;
+}
+
+void launch_tconv(const TConvArgs& a0, int num_sms, cudaStream_t st) {
+  TConvArgs a = a0;
+  const int fixed = tconv_fixed_bytes(a), sb = tconv_stage_bytes(a);
+  a.stages = std::min(kTgMaxStages, (219 * 1024 - 1024 - fixed) / sb);
+  const int m_tiles = (a.M + 127) / 128;
+  const long long tiles = a.mode == TCONV_WGRAD ? (long long)m_tiles * a.ranges : (long long)m_tiles * a.groups;
+  int grid = (int)std::min<long long>(tiles, num_sms);
+  if (a.mode != TCONV_WGRAD) grid -= grid % a.groups;  // whole CTA sets per group
+  launch_pdl(tconv_kernel, dim3(grid), dim3(TC_THREADS), tconv_smem(a), st, a);
+  sync_debug(a.mode == TCONV_FWD ? "tconv fwd" : a.mode == TCONV_DGRAD ? "tconv dgrad" : "tconv wgrad", st);
+}
+
+// ---- layer 1 of the generic path: a1 (Philox sample) + a2 (gather, u8 -> exact bf16) into [b][441][64]
+// One CTA per (image, group); thread e handles 16 bytes = one frame's 16 s2d channels of one pixel of the
+// frame-major slot [frame][441 px][16] and writes them as 16 bf16 at [px][frame*16 ..]. The first CTA row also
+// bulk-prefetches the slot the same image index samples next step (the sampler is counter-based).
+__global__ void __launch_bounds__(224) gather_s2d_kernel(GConvFwdArgs a, __nv_bfloat16* x0, __nv_bfloat16* x1) {
+  const int img = blockIdx.x, g = blockIdx.y;
+  pdl_sync();  // the ring (pushes) and the replay size come from earlier launches; x is read by the previous step
+  long long slot;
+  if (a.ctr) {
+    const unsigned long long T = a.ctr->T;
+    slot = sample_slot(a.seed, a.rank, T, (unsigned)img, a.ctr->ring_size);  // a1
+    if (g == 0 && threadIdx.x == 0) {
+      if (a.idx) a.idx[img] = (int)slot;
+      const long long nxt = sample_slot(a.seed, a.rank, T + 1, (unsigned)img, a.ctr->ring_size);
+      bulk_prefetch_l2(a.ring[0] + nxt * a.slot_stride, 28224);
+      bulk_prefetch_l2(a.ring[1] + nxt * a.slot_stride, 28224);
+    }
+  } else {
+    slot = img;
+  }
+  const uint4* src = reinterpret_cast<const uint4*>(a.ring[g] + slot * a.slot_stride);
+  __nv_bfloat16* dst = (g ? x1 : x0) + (long long)img * 441 * 64;
+  // thread = one pixel: its 4 frames' 16-byte vectors (coalesced per frame plane across the warp) become one
+  // contiguous 128-byte row of 64 bf16 channels
+  for (int px = threadIdx.x; px < 441; px += blockDim.x) {
+    uint4 w[4];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) w[f] = __ldg(src + f * 441 + px);
+    uint4* d = reinterpret_cast<uint4*>(dst + (long long)px * 64);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const uint32_t ws[4] = {w[f].x, w[f].y, w[f].z, w[f].w};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {  // 4 bytes -> 4 exact bf16 (0..255 are exact)
+          const uint32_t b = ws[2 * h + q];
+          const __nv_bfloat162 lo = __floats2bfloat162_rn((float)(b & 0xFFu), (float)((b >> 8) & 0xFFu));
+          const __nv_bfloat162 hi = __floats2bfloat162_rn((float)((b >> 16) & 0xFFu), (float)(b >> 24));
+          o[2 * q] = *reinterpret_cast<const uint32_t*>(&lo);
+          o[2 * q + 1] = *reinterpret_cast<const uint32_t*>(&hi);
+        }
+        d[2 * f + h] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+}
+
+void launch_gather_s2d(const GConvFwdArgs& a, __nv_bfloat16* x1_0, __nv_bfloat16* x1_1, int groups, cudaStream_t st) {
+  launch_pdl(gather_s2d_kernel, dim3(a.b, groups), dim3(224), 0, st, a, x1_0, x1_1);
+  sync_debug("gather_s2d", st);
+}
+
+int tgemm_stages(int BN) {
+  const int stage = TG_A_BYTES + BN * 64 * 2;
+  const int budget = tg_ctas_per_sm(BN) == 2 ? 100 * 1024 : 200 * 1024;
+  return std::max(2, std::min(kTgMaxStages, budget / stage));
+}
+
+size_t tgemm_smem(int BN) { return (size_t)tgemm_stages(BN) * (TG_A_BYTES + BN * 64 * 2) + 1024; }
+
+bool init_tma_kernel_attrs() {
+  const bool ok = cudaFuncSetAttribute(tgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024 + 1024) == cudaSuccess;  // every ring fits 200 KB
+  cudaGetLastError();
+  return ok;
+}
+
+void launch_tgemm(const TGemmArgs& a0, int num_sms, cudaStream_t st) {
+  TGemmArgs a = a0;
+  a.stages = tgemm_stages(a.BN);
+  const long long tiles = (long long)((a.M + 127) / 128) * ((a.N + a.BN - 1) / a.BN) * a.splits * a.groups;
+  const int grid = (int)std::min<long long>(tiles, (long long)num_sms * tg_ctas_per_sm(a.BN));
+  launch_pdl(tgemm_kernel, dim3(grid), dim3(TG_THREADS), tgemm_smem(a.BN), st, a);
+  sync_debug("tgemm", st);
+}
+
+}  // namespace dqn

@@ -161,12 +161,3 @@ def test_fused_reduce_update_path():
     ref = O.run(on, oc, 1000, [rp], theta0.astype(np.float64), 5)
     th0 = theta0.astype(np.float64)
     assert delta_rel(th, th0, ref["theta"], th0, on, ulps=5) < TOL
-
-
-def test_fc_too_wide_for_the_dx_staging_is_rejected():
-    """(128 + b) * fc * 2 bytes must fit the FC dX GEMM's 200 KB shared-memory staging: DQN_EINVAL at create
-    (nothing is launched), not a failed launch inside the step graph."""
-    dc, _, _ = nets(minibatch=32, replay_capacity=100, precision=D.BF16, fcs=(1024,))
-    with pytest.raises(D.DqnError) as e:
-        D.DQN(dc)
-    assert e.value.code == D.EINVAL

@@ -42,8 +42,10 @@ def make(dc, on, n_items, seed, theta_seed, r_scale=1.0, out_std=0.5):
     return g, rp, raw, theta0.astype(np.float64)
 
 
-CASES = [(dict(), 32), (dict(), 256), (dict(fcs=(128,)), 32), (dict(fcs=(512,)), 32), (SCALED, 32), (SCALED, 512)]
-IDS = ["mnih-b32", "mnih-b256", "mnih-fc128", "mnih-fc512", "scaled-b32", "scaled-b512"]
+CASES = [(dict(), 32), (dict(), 256), (dict(fcs=(128,)), 32), (dict(fcs=(512,)), 32), (dict(fcs=(2048,)), 32),
+         (SCALED, 32), (SCALED, 512), (dict(SCALED, fcs=(1024,)), 32), (dict(SCALED, fcs=(2048,)), 64)]
+IDS = ["mnih-b32", "mnih-b256", "mnih-fc128", "mnih-fc512", "mnih-fc2048", "scaled-b32", "scaled-b512",
+       "scaled-fc1024", "scaled-fc2048"]  # fc > 512: the FC backward on the K-pipelined GEMM (BJ.c5's sweep)
 
 
 @pytest.mark.parametrize("kw,b", CASES, ids=IDS)
