@@ -433,6 +433,7 @@ struct TConvArgs {
   int kpr, ranges, TCs, Nout;
   float* partial;                  // [ranges][TCs][Nout]
   float* partial_db;               // [ranges][Nout]
+  int dbg;                         // probe only (tools/probe_tconv): 1 skip epilogue stores, 2 skip MMAs
 };
 bool init_tconv_kernel_attrs();
 size_t tconv_smem(const TConvArgs& a);  // 0: does not fit

@@ -48,12 +48,75 @@ EncodeTiledFn encode_fn() {
   return f;
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// ---- warp-uniform issue: the producer and MMA roles run on a WHOLE warp with warp-uniform values, and the
+// one-thread instructions (TMA, MMA, commit, expect-tx) carry their own elect.sync inside the asm. Issued from
+// under `if (lane == 0)` instead, every tcgen05.mma / TMA operand goes through a per-lane R2UR loop
+// (measured: ~110 cycles per MMA, ~1800 cycles per 16-MMA convolution tile of pure issue overhead).
+__device__ __forceinline__ void mma_bf16_w(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+      "{ .reg .pred e, q; elect.sync _|e, 0xffffffff; setp.ne.b32 q, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q; }" ::"r"(d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_w(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4]; }" ::"r"(
           smem_u32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_w(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1; }" ::"r"(smem_u32(bar)), "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+      "@e mbarrier.arrive.shared::cta.b64 _, [%0]; }" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ unsigned g_spin_ns = 0;     // probe knob: back-off of the single-thread waits
+__device__ unsigned g_epi_spin_ns = 64;
+// spin on mbarrier.test_wait (never suspends: the pipelines here hand off every few hundred cycles, and a
+// suspended try_wait was measured to add ~1 us per hand-off on short convolution tiles)
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  while (true) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) break;
+    if (g_spin_ns) __nanosleep(g_spin_ns);
+  }
+}
+// the epilogue warps' wait: one lane polls (with a short back-off), the warp then proceeds together, so eight
+// waiting warps do not flood the shared-memory pipe the producer and MMA threads hand off through
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t done;
+    while (true) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(smem_u32(bar)), "r"(parity)
+          : "memory");
+      if (done) break;
+      __nanosleep(g_epi_spin_ns);
+    }
+  }
+  __syncwarp();
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -140,7 +203,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2) tgemm_kernel(const __grid_const
   auto n_chunks = [&](int split) { return (min(a.kper, a.K - split * a.kper) + 63) / 64; };
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
+    {  // ---- TMA producer (whole warp, warp-uniform; one elected lane issues)
       int it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         int g, split, m0, n0;
@@ -148,30 +211,27 @@ __global__ void __launch_bounds__(TG_THREADS, 2) tgemm_kernel(const __grid_const
         const int nch = n_chunks(split);
         for (int c = 0; c < nch; ++c, ++it) {
           const int s = it % S;
-          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          mbar_spin(&empty[s], ((it / S) & 1) ^ 1);
           uint8_t* sA = smem + s * STAGE;
           uint8_t* sB = sA + TG_A_BYTES;
-          mbar_arrive_expect_tx(&full[s], STAGE);
+          mbar_expect_tx_w(&full[s], STAGE);
           const int kb = split * a.kper + c * 64;
-          if (a.epi == TC_EPI_CONV_FWD) {  // tap t, channel block cb: the same rows shifted by the tap
-            const int tp = c / a.Cblk, cb = c % a.Cblk;
-            tma_load_2d(sA, &a.ta[g], cb * 64, m0 + (tp / a.Tw) * a.Ws + tp % a.Tw, &full[s]);
-          } else if (!a.a_mn) {
-            tma_load_2d(sA, &a.ta[g], kb, m0, &full[s]);
+          if (!a.a_mn) {
+            tma_load_2d_w(sA, &a.ta[g], kb, m0, &full[s]);
           } else {
-            tma_load_2d(sA, &a.ta[g], m0, kb, &full[s]);
-            tma_load_2d(sA + 8192, &a.ta[g], m0 + 64, kb, &full[s]);
+            tma_load_2d_w(sA, &a.ta[g], m0, kb, &full[s]);
+            tma_load_2d_w(sA + 8192, &a.ta[g], m0 + 64, kb, &full[s]);
           }
           if (!a.b_mn) {
-            tma_load_2d(sB, &a.tb[g], kb, n0, &full[s]);
+            tma_load_2d_w(sB, &a.tb[g], kb, n0, &full[s]);
           } else {
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, &a.tb[g], n0 + 64 * j, kb, &full[s]);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d_w(sB + j * 8192, &a.tb[g], n0 + 64 * j, kb, &full[s]);
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    {  // ---- MMA issuer (whole warp, warp-uniform; one elected lane issues)
       const uint32_t idesc = make_idesc_bf16(128, BN, a.a_mn, a.b_mn);
       int it = 0, tl = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
@@ -179,24 +239,24 @@ __global__ void __launch_bounds__(TG_THREADS, 2) tgemm_kernel(const __grid_const
         decode(t, g, split, m0, n0);
         const int nch = n_chunks(split);
         const int buf = tl & 1;
-        mbar_wait(&tempty[buf], ((tl >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
+        mbar_spin(&tempty[buf], ((tl >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
         tc_fence_after();
         const uint32_t d = tbase + (uint32_t)(buf * BN);
         for (int c = 0; c < nch; ++c, ++it) {
           const int s = it % S;
-          mbar_wait(&full[s], (it / S) & 1);
-          tc_fence_after();
+          mbar_spin(&full[s], (it / S) & 1);
+          // (TMA data: async proxy to async proxy, ordered by the mbarrier; no tcgen05 fence)
           const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + TG_A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             // K-major: +32 B per K step inside the swizzled 128-B rows; MN-major: +16 rows of 128 B
             const uint64_t ad = a.a_mn ? desc_sw128(sa + kk * 2048, 8192, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t bd = a.b_mn ? desc_sw128(sb + kk * 2048, 8192, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
-            mma_bf16(d, ad, bd, idesc, (c > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16_w(d, ad, bd, idesc, (c > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+          mma_commit_w(&empty[s]);  // the stage is free once these MMAs have read it
         }
-        mma_commit(&tfull[buf]);
+        mma_commit_w(&tfull[buf]);
       }
     }
   } else {  // ---- epilogue: thread = one row (TMEM lane) of the tile
@@ -206,41 +266,33 @@ __global__ void __launch_bounds__(TG_THREADS, 2) tgemm_kernel(const __grid_const
       int g, split, m0, n0;
       decode(t, g, split, m0, n0);
       const int buf = tl & 1;
-      mbar_wait(&tfull[buf], (tl >> 1) & 1);
-      tc_fence_after();
       const int m = m0 + 32 * q + lane;
+      // TC_EPI_MASK_T: the ReLU mask of the next 16 columns is always in flight (the first batch before the
+      // accumulator wait, so it overlaps the mainloop)
+      unsigned short mkn[16];
+      auto load_mask = [&](int c0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int n = n0 + c0 + i;
+          mkn[i] = (n < a.N && m < a.M) ? __ldg(reinterpret_cast<const unsigned short*>(a.mask) + (long long)n * a.ldo + m)
+                                        : (unsigned short)0;
+        }
+      };
+      if (a.epi == TC_EPI_MASK_T) load_mask(0);
+      mbar_wait_warp(&tfull[buf], (tl >> 1) & 1);
+      tc_fence_after();
       const uint32_t trow = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tmem_ld16(trow + c, v);  // warp-collective
+        unsigned short mk[16];
+        if (a.epi == TC_EPI_MASK_T) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) mk[i] = mkn[i];
+          if (c + 16 < BN) load_mask(c + 16);
+        }
         if (m >= a.M) continue;
-        if (a.epi == TC_EPI_CONV_FWD) {  // bias + ReLU (x 1/255 on layer 1) into the next layer's grid
-          const int img = m / a.HsWs, pq = m - img * a.HsWs, oy = pq / a.Ws, ox = pq - oy * a.Ws;
-          if (oy >= a.Ho || ox >= a.Wo || img >= a.M / a.HsWs) continue;
-          const float* bias = a.bias[g];
-          uint32_t o[8];
-#pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(fmaxf(fmaf(v[i], a.scale, __ldg(bias + c + i)), 0.0f),
-                                                            fmaxf(fmaf(v[i + 1], a.scale, __ldg(bias + c + i + 1)), 0.0f));
-            o[i >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
-          }
-          const int Nn = a.N, HoWo = a.Ho * a.Wo;
-          if (a.s_next == 0) {  // canonical (C,H,W) flatten: out[img][n*HoWo + p]
-            __nv_bfloat16* dst = a.cout[g] + (long long)img * Nn * HoWo + (long long)oy * a.Wo + ox;
-            const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(o);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) dst[(long long)(c + i) * HoWo] = hv[i];
-          } else {  // next grid (s2d by s_next): pixel (oy/s, ox/s), channel (iy*s + ix)*N + n
-            const int sn = a.s_next, Hn = a.Ho / sn, Wn = a.Wo / sn, Cn = Nn * sn * sn;
-            const int py = oy / sn, px = ox / sn, qq = (oy % sn) * sn + (ox % sn);
-            if (py < Hn && px < Wn) {
-              uint4* dst = reinterpret_cast<uint4*>(a.cout[g] + (((long long)img * Hn + py) * Wn + px) * Cn + qq * Nn + c);
-              dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-              dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
-            }
-          }
-        } else if (a.epi == TC_EPI_FC_FWD) {
+        if (a.epi == TC_EPI_FC_FWD) {
           float* p = a.partial + ((long long)g * a.splits + split) * (long long)a.N * a.M + m;
 #pragma unroll
           for (int i = 0; i < 16; ++i)
@@ -264,12 +316,6 @@ __global__ void __launch_bounds__(TG_THREADS, 2) tgemm_kernel(const __grid_const
                           : (long long)pp * a.hwc_C + cc;
           }
           const long long ldo_out = a.ldo_out ? a.ldo_out : a.ldo;
-          unsigned short mk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int n = n0 + c + i;
-            mk[i] = n < a.N ? __ldg(reinterpret_cast<const unsigned short*>(a.mask) + (long long)n * a.ldo + m) : 0;
-          }
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int n = n0 + c + i;
@@ -297,7 +343,14 @@ static int tg_ctas_per_sm(int BN) {
 
 // ================================================================== TMA implicit-GEMM convolutions (TConvArgs)
 namespace {
-constexpr int TC_THREADS = 192;
+constexpr int kMaxAcc = 8;
+__host__ __device__ __forceinline__ int acc_buffers(int BN) {
+  int nb = 512 / (BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256);
+  return nb > kMaxAcc ? kMaxAcc : nb;
+}
+constexpr int TC_NMMA = 4;        // MMA-issuing warps: issue cost (~100 cycles per tcgen05.mma with its operand
+                                  // broadcast) exceeds a small-N MMA's execution, so 4 warps issue for alternate tiles
+constexpr int TC_THREADS = 32 * (1 + TC_NMMA + 8);  // producer warp, MMA warps, 8 epilogue warps (2 per TMEM quadrant)
 __device__ __forceinline__ int tap_shift(const TConvArgs& a, int t) { return (t / a.Tw) * a.Ws + t % a.Tw; }
 __host__ __device__ __forceinline__ int win_bytes(int rows) { return (rows * 128 + 1023) / 1024 * 1024; }
 // the (t, c-block) pair of 64-row M block mb of the weight gradient; mb * 64 >= TCs: the all-ones block
@@ -319,9 +372,8 @@ __host__ __device__ __forceinline__ int tconv_fixed_bytes(const TConvArgs& a) {
 __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_constant__ TConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kTgMaxStages], empty[kTgMaxStages], bfull, tfull[2], tempty[2];
+  __shared__ uint64_t full[kTgMaxStages], empty[kTgMaxStages], bfull, tfull[kMaxAcc], tempty[kMaxAcc];
   __shared__ uint32_t tbase;
-  __shared__ uint32_t s_aoff[32];  // FWD / DGRAD: tap row offsets in the window (16-byte units)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = a.stages, BN = a.BN, SB = tconv_stage_bytes(a);
   const bool wg = a.mode == TCONV_WGRAD;
@@ -329,7 +381,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
   // second MN half of an A tile is addressed as half 0 + LBO, so the ones block must lie above every window)
   uint8_t* fixed = wg ? smem + S * SB : smem;
   uint8_t* ring = wg ? smem : smem + tconv_fixed_bytes(a);
-  const uint32_t tcols = BN <= 16 ? 32 : BN <= 32 ? 64 : BN <= 64 ? 128 : BN <= 128 ? 256 : 512;
+  // NB TMEM accumulators (as many as 512 columns hold, at most kMaxAcc): the MMA warp runs up to NB tiles ahead
+  // of the epilogue, which hides the commit -> epilogue -> release round trip of short tiles
+  const int NB = acc_buffers(BN);
+  const uint32_t tcols = 512;
   // work split: FWD / DGRAD tiles of 128 rows, CTA c serving group c % groups (its resident weights);
   // WGRAD tiles (m-tile, K range)
   const int m_tiles = (a.M + 127) / 128;
@@ -343,9 +398,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
       mbar_init(&empty[st], 1);
     }
     mbar_init(&bfull, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], 8);
     }
     fence_mbar_init();
   }
@@ -355,10 +410,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
     fence_async_smem();
   }
   if (warp == 1) tmem_alloc(&tbase, tcols);
+  // MMA warps (FWD / DGRAD): up to TC_NMMA, each owning a sub-ring of Sw stages and every nmma-th tile, so that
+  // each stage barrier is always consumed in order (a warp running a whole ring lap ahead of another would
+  // otherwise alias an mbarrier phase); WGRAD's long K loops keep one MMA warp and the whole ring
+  int nmma = wg ? 1 : min(min(TC_NMMA, NB), S / a.Cblk);
+  if (nmma < 1) nmma = 1;
+  const int Sw = wg ? S : S / nmma;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) reinterpret_cast<long long*>(a.partial)[193] = clock64();
   pdl_sync();
+  if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) reinterpret_cast<long long*>(a.partial)[194] = clock64();
   auto chunks_of = [&](int r) {  // WGRAD: 64-row chunks of K range r
     const long long r0 = (long long)r * a.kpr * 64;
     const long long rows = min((long long)a.kpr * 64, a.krows - r0);
@@ -366,20 +429,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
   };
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
+    {  // ---- TMA producer (whole warp, warp-uniform; one elected lane issues)
       if (!wg) {
-        mbar_arrive_expect_tx(&bfull, (uint32_t)(a.T * a.Cblk * BN * 128));
-        for (int ch = 0; ch < a.T * a.Cblk; ++ch) tma_load_2d(fixed + ch * BN * 128, &a.tb[g], ch * 64, 0, &bfull);
+        mbar_expect_tx_w(&bfull, (uint32_t)(a.T * a.Cblk * BN * 128));
+        for (int ch = 0; ch < a.T * a.Cblk; ++ch) tma_load_2d_w(fixed + ch * BN * 128, &a.tb[g], ch * 64, 0, &bfull);
       }
-      int it = 0;
-      for (int tl = cta; tl < tiles; tl += ctas) {
+      int it = 0, tl_local = 0;
+      for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
         if (!wg) {
           const int m0 = tl * 128, row0 = a.mode == TCONV_FWD ? m0 : m0 - a.maxshift;
+          // the stages of MMA warp w's k-th tile: its own sub-ring of Sw stages (consumed in order by that warp)
+          const int w = tl_local % nmma, k = tl_local / nmma;
           for (int cb = 0; cb < a.Cblk; ++cb, ++it) {
-            const int st = it % S;
-            mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[st], (uint32_t)(a.R * 128));
-            tma_load_2d(ring + st * SB, &a.ta[g], cb * 64, row0, &full[st]);
+            const int q = k * a.Cblk + cb, st = w * Sw + q % Sw, ph = (q / Sw) & 1;
+            mbar_spin(&empty[st], ph ^ 1);
+            if (a.dbg & 4) {
+              mbar_arrive_w(&full[st]);
+            } else {
+              mbar_expect_tx_w(&full[st], (uint32_t)(a.R * 128));
+              tma_load_2d_w(ring + st * SB, &a.ta[g], cb * 64, row0, &full[st]);
+            }
+            if ((a.dbg & 64) && blockIdx.x == 0 && it < 64 && lane == 0) reinterpret_cast<long long*>(a.partial)[it] = clock64();
           }
         } else {
           const int mt = tl % m_tiles, r = tl / m_tiles, nch = chunks_of(r);
@@ -394,44 +464,55 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
           for (int c = 0; c < nch; ++c, ++it) {
             const int st = it % S;
             const int p0 = (int)((long long)r * a.kpr * 64 + c * 64);
-            mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[st], (uint32_t)(ncb * a.R * 128 + 8192));
+            mbar_spin(&empty[st], ((it / S) & 1) ^ 1);
+            mbar_expect_tx_w(&full[st], (uint32_t)(ncb * a.R * 128 + 8192));
             uint8_t* sb = ring + st * SB;
-            for (int w = 0; w < ncb; ++w) tma_load_2d(sb + w * win_bytes(a.R), &a.ta[0], cbs[w] * 64, p0, &full[st]);
-            tma_load_2d(sb + 2 * win_bytes(a.R), &a.tb[0], 0, p0, &full[st]);
+            for (int w = 0; w < ncb; ++w) tma_load_2d_w(sb + w * win_bytes(a.R), &a.ta[0], cbs[w] * 64, p0, &full[st]);
+            tma_load_2d_w(sb + 2 * win_bytes(a.R), &a.tb[0], 0, p0, &full[st]);
           }
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
-      if (!wg) mbar_wait(&bfull, 0);
-      for (int t = 0; t < a.T; ++t)  // row offset of tap t in the window, in 16-byte descriptor units
-        s_aoff[t] = (uint32_t)((a.mode == TCONV_FWD ? tap_shift(a, t) : a.maxshift - tap_shift(a, t)) * 8);
+  } else if (warp <= TC_NMMA) {
+    const int j = warp - 1;
+    if (j < nmma) {  // ---- MMA issuer j: local tiles j, j + nmma, ... (whole warp, warp-uniform; one lane issues)
+      if (!wg) mbar_spin(&bfull, 0);
+      const bool fwd = a.mode == TCONV_FWD;
+      const int Th = a.T / a.Tw;
+      const uint32_t ring_u = smem_u32(ring);
       const uint32_t idesc = wg ? make_idesc_bf16(128, BN, 1, 1) : make_idesc_bf16(128, BN, 0, 0);
       const uint32_t fx = smem_u32(fixed);
       int it = 0, tl_local = 0;
       for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
-        const int buf = tl_local & 1;
-        mbar_wait(&tempty[buf], ((tl_local >> 1) & 1) ^ 1);
+        if (tl_local % nmma != j) {  // another MMA warp's tile: only its stages are counted
+          it += wg ? chunks_of(tl / m_tiles) : a.Cblk;
+          continue;
+        }
+        const int buf = tl_local % NB;
+        if (!(a.dbg & 128)) mbar_spin(&tempty[buf], ((tl_local / NB) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tbase + (uint32_t)(buf * BN);
         if (!wg) {
+          const int k = tl_local / nmma;
           for (int cb = 0; cb < a.Cblk; ++cb, ++it) {
-            const int st = it % S;
-            mbar_wait(&full[st], (it / S) & 1);
-            tc_fence_after();
+            const int q = k * a.Cblk + cb, st = j * Sw + q % Sw;
+            mbar_spin(&full[st], (q / Sw) & 1);
+            // (TMA data: async proxy to async proxy, ordered by the mbarrier; no tcgen05 fence)
             // descriptors advance by adding to the 14-bit start-address field (16-byte units); every tap is the
-            // same window read s_aoff[t] rows later, every K step 32 bytes later
-            const uint64_t a0 = desc_sw128(smem_u32(ring + st * SB), 16, 1024);
+            // same window read shift(t) rows later (fwd; maxshift - shift(t) for dgrad), every K step 32 bytes
+            // later. Pure loop-counter arithmetic, so the operands stay in uniform registers (no per-MMA R2UR)
+            const uint64_t a0 = desc_sw128(ring_u + (uint32_t)(st * SB), 16, 1024);
             const uint64_t b0 = desc_sw128(fx, 16, 1024) + (uint64_t)(cb * BN * 8);
-            for (int t = 0; t < a.T; ++t) {
-              const uint64_t at = a0 + s_aoff[t], bt = b0 + (uint64_t)(t * a.Cblk * BN * 8);
+            for (int ty = 0, t = 0; ty < Th; ++ty)
+              for (int tx = 0; tx < a.Tw; ++tx, ++t) {
+                const int sh = ty * a.Ws + tx, off = fwd ? sh : a.maxshift - sh;
+                const uint64_t at = a0 + (uint64_t)(off * 8), bt = b0 + (uint64_t)((t * a.Cblk) * BN * 8);
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                mma_bf16(d, at + 2 * kk, bt + 2 * kk, idesc, (cb > 0 || t > 0 || kk > 0) ? 1u : 0u);
-            }
-            mma_commit(&empty[st]);
+                for (int kk = 0; kk < 4; ++kk)
+                  if (!(a.dbg & 2)) mma_bf16_w(d, at + 2 * kk, bt + 2 * kk, idesc, (cb > 0 || t > 0 || kk > 0) ? 1u : 0u);
+              }
+            if (a.dbg & 8) mbar_arrive_w(&empty[st]);
+            else mma_commit_w(&empty[st]);
           }
         } else {
           const int mt = tl % m_tiles, r = tl / m_tiles, nch = chunks_of(r);
@@ -449,8 +530,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
           }
           for (int c = 0; c < nch; ++c, ++it) {
             const int st = it % S;
-            mbar_wait(&full[st], (it / S) & 1);
-            tc_fence_after();
+            mbar_spin(&full[st], (it / S) & 1);
+            // (TMA data: async proxy to async proxy, ordered by the mbarrier; no tcgen05 fence)
             const uint32_t sb = smem_u32(ring + st * SB);
             const uint32_t h0 = ones[0] ? fx : sb + hoff[0];
             const uint32_t h1 = ones[1] ? fx : sb + hoff[1];
@@ -459,27 +540,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
             const uint32_t bt = sb + 2 * win_bytes(a.R);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16(d, desc_sw128(h0 + kk * 2048, lbo, 1024), desc_sw128(bt + kk * 2048, 8192, 1024), idesc,
-                       (c > 0 || kk > 0) ? 1u : 0u);
-            mma_commit(&empty[st]);
+              mma_bf16_w(d, desc_sw128(h0 + kk * 2048, lbo, 1024), desc_sw128(bt + kk * 2048, 8192, 1024), idesc,
+                         (c > 0 || kk > 0) ? 1u : 0u);
+            mma_commit_w(&empty[st]);
           }
         }
-        mma_commit(&tfull[buf]);
+        if (a.dbg & 8) mbar_arrive_w(&tfull[buf]);
+        else mma_commit_w(&tfull[buf]);
+        if ((a.dbg & 64) && blockIdx.x == 0 && tl_local < 64 && lane == 0) reinterpret_cast<long long*>(a.partial)[64 + tl_local] = clock64();
       }
     }
-  } else {  // ---- epilogue: thread = one row (TMEM lane) of the tile
-    const int q = warp & 3;
+  } else if (!(a.dbg & 128)) {  // ---- epilogue: thread = one row (TMEM lane) of the tile, half of its columns
+    const int q = warp & 3, half = (warp - 1 - TC_NMMA) >> 2, c_lo = half * (BN / 2), c_hi = c_lo + BN / 2;
     int tl_local = 0;
     for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
-      const int buf = tl_local & 1;
-      mbar_wait(&tfull[buf], (tl_local >> 1) & 1);
+      const int buf = tl_local % NB;
+      mbar_wait_warp(&tfull[buf], (tl_local / NB) & 1);
       tc_fence_after();
       const int mt = wg ? tl % m_tiles : tl, r = wg ? tl / m_tiles : 0;
       const int m = mt * 128 + 32 * q + lane;
       const uint32_t trow = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
-      for (int c = 0; c < BN; c += 16) {
+      for (int c = c_lo; c < c_hi; c += 16) {
         float v[16];
+        if (a.dbg & 16) continue;
         tmem_ld16(trow + c, v);  // warp-collective
+        if (a.dbg & 1) continue;
         if (a.mode == TCONV_FWD) {
           if (m >= a.M) continue;
           const int img = m / a.HsWs, pq = m - img * a.HsWs, oy = pq / a.Ws, ox = pq - oy * a.Ws;
@@ -536,8 +621,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
+      if ((a.dbg & 64) && blockIdx.x == 0 && tid == 64 && tl_local < 64) reinterpret_cast<long long*>(a.partial)[128 + tl_local] = clock64();
     }
   }
+  if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) reinterpret_cast<long long*>(a.partial)[192] = clock64();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tbase, tcols);
