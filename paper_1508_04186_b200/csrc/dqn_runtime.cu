@@ -88,6 +88,11 @@ struct dqn_ctx {
   __nv_bfloat16* dzp[kMaxConv] = {};          // dZ of every conv layer in its input-grid geometry (zero borders)
   float* tc_part = nullptr;
   float* tc_part_db = nullptr;
+  // N = 1, n_push = 1 on the TMA kernels: the head finish and the RMSProp update of the FC / output-layer
+  // parameters run on a side stream (graph branch) next to the FC dX and the conv backward
+  bool split_update = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_dw = nullptr, ev_join = nullptr;
   long long pack_n = 0, gpack_off = -1;
   float* gw_partial = nullptr;
   float* gw_partial_db = nullptr;
@@ -424,6 +429,9 @@ static void free_all(dqn_ctx* c) {
       if (p) cudaFree(p);
   }
   if (c->gw_partial) cudaFree(c->gw_partial);
+  if (c->side) cudaStreamDestroy(c->side);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_dw, c->ev_join})
+    if (e) cudaEventDestroy(e);
   for (auto* x : c->x1)
     if (x) cudaFree(x);
   for (auto* x : c->dzp)
@@ -608,6 +616,13 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
   ok = ok && make_tmap_bf16(&x.ta[0], W[0], H, D, D, 64);
   ok = ok && make_tmap_bf16(&x.tb[0], ctx->dh_bf16, b, H, H, x.BN);
   ctx->use_tgemm = ok;
+  if (ok && ctx->world == 1 && ctx->cfg.n_push == 1 && ctx->alias_local && !ctx->async && F.w_off % 4 == 0 &&
+      !((e = getenv("DQN_SPLIT_UPDATE")) && atoi(e) == 0) &&
+      cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) == cudaSuccess &&
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+      cudaEventCreateWithFlags(&ctx->ev_dw, cudaEventDisableTiming) == cudaSuccess &&
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) == cudaSuccess)
+    ctx->split_update = true;
   if (!ok || ((e = getenv("DQN_TCONV")) && atoi(e) == 0) || !init_tconv_kernel_attrs()) return;
   // every conv layer on the TMA tap-window kernel (kernels_tma.cu): forward (theta on s, theta^ on s'), data
   // gradient of every layer but the first, weight gradient (+ db) as per-range partials reduced in order
@@ -1689,7 +1704,25 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   // one launch: the FC dW and dX tiles plus the head finish CTAs run side by side (tc_pair); the
   // whole K (= b and H <= 512) is staged at once, which the 200 KB budget allows at BN = 64
   gx.pre_a = 1; gx.pre_b = 0; gw.pre_a = 0; gw.pre_b = 1;
-  if (ctx->use_tgemm) {  // the warp-specialised TMA GEMMs, then the head finish
+  const long long fc0 = F.w_off;  // the non-conv parameters [fc0, P_pad): FC weight and bias, output layer
+  if (ctx->use_tgemm && ctx->split_update && push) {
+    // side branch: head finish (dW_o, db_o, db_fc, loss, T + 1) next to the FC dW / dX, then the RMSProp update
+    // of the non-conv parameters next to the conv backward; joined at the end of the step
+    PB("fc1_bwd_head_finish", 2);
+    CK(cudaEventRecord(ctx->ev_fork, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    launch_head_finish_warp(h, ctx->side);
+    launch_tgemm(ctx->tg_dw, ctx->num_sms, st);
+    launch_tgemm(ctx->tg_dx, ctx->num_sms, st);  // reads the FC weight the side update is about to write
+    CK(cudaEventRecord(ctx->ev_dw, st));
+    PE();
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_dw, 0));
+    launch_rmsprop(ctx->theta_master + fc0, ctx->rms + fc0, ctx->grad + fc0, ctx->P_pad - fc0, (float)c.n_push,
+                   (float)c.lr, (float)c.rms_decay, (float)(1.0 - c.rms_decay), (float)c.rms_eps, nullptr,
+                   ctx->theta_local_bf16 + fc0, ctx->ctr, 1, ctx->side, -1, 0, 0,
+                   ctx->grad_snap ? ctx->grad_snap + fc0 : nullptr);
+    CK(cudaEventRecord(ctx->ev_join, ctx->side));
+  } else if (ctx->use_tgemm) {  // the warp-specialised TMA GEMMs, then the head finish
     PB("fc1_bwd_head_finish", 3);
     launch_tgemm(ctx->tg_dw, ctx->num_sms, st);
     launch_tgemm(ctx->tg_dx, ctx->num_sms, st);
@@ -1753,6 +1786,12 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
                      (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, st);
+      PE();
+    } else if (ctx->use_tgemm && ctx->split_update) {  // the conv parameters here, the rest on the side branch
+      PB("rmsprop_update", 1);
+      launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, fc0, div, (float)c.lr, rho, omr, (float)c.rms_eps,
+                     nullptr, ctx->theta_local_bf16, ctx->ctr, 1, st, -1, 0, 0, ctx->grad_snap);
+      CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
       PE();
     } else {
       PB("rmsprop_update", 1);

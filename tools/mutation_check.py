@@ -31,13 +31,17 @@ MUTATIONS = {
                              "const float d_lo = v[16 * q + 2 * h];"),
                             (B16, "const float d_hi = a_hi > 0.0f ? v[16 * q + 2 * h + 1] : 0.0f;",
                              "const float d_hi = v[16 * q + 2 * h + 1];")], [G + "test_gated_one_step[mnih-b32]"]),
-    "gconv_dgrad_relu_mask_even_channels": ([(CSRC + "kernels_conv.cu",
-                                              "o[h] = pack2(bf16_pos(mw[h] & 0xFFFFu) ? v[2 * h] : 0.0f,",
-                                              "o[h] = pack2(v[2 * h],")], [G + "test_gated_one_step[scaled-b32]"]),
-    "gconv_dgrad_relu_mask": ([(CSRC + "kernels_conv.cu",
-                                "o[h] = pack2(bf16_pos(mw[h] & 0xFFFFu) ? v[2 * h] : 0.0f, "
-                                "bf16_pos(mw[h] >> 16) ? v[2 * h + 1] : 0.0f);",
-                                "o[h] = pack2(v[2 * h], v[2 * h + 1]);")], [G + "test_gated_one_step[scaled-b32]"]),
+    "tconv_dgrad_relu_mask": ([(CSRC + "kernels_tma.cu",
+                                "const __nv_bfloat162 h2 = __floats2bfloat162_rn(bf16_gt0(mw[h] & 0xFFFFu) ? v[2 * h] : 0.0f,\n"
+                                "                                                            bf16_gt0(mw[h] >> 16) ? v[2 * h + 1] : 0.0f);",
+                                "const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);")],
+                              [G + "test_gated_one_step[scaled-b32]"]),
+    "tgemm_fc_dX_relu_mask": ([(CSRC + "kernels_tma.cu", "__float2bfloat16_rn(bf16_gt0(mk[i]) ? v[i] : 0.0f)",
+                                "__float2bfloat16_rn(v[i])")], [G + "test_gated_one_step[scaled-b32]"]),
+    "tconv_wgrad_tap_shift_dropped": ([(CSRC + "kernels_tma.cu",
+                                        "hoff[h] = (cbs[0] == cb ? 0 : win_bytes(a.R)) + tap_shift(a, t) * 128;",
+                                        "hoff[h] = (cbs[0] == cb ? 0 : win_bytes(a.R));")],
+                                      [G + "test_gated_one_step[scaled-b32]"]),
     "error_clip_one_sided": ([(CSRC + "kernels_head.cu", "dc = fminf(fmaxf(dc, -h.clip), h.clip);",
                                "dc = fminf(dc, h.clip);")], [G + "test_gated_error_clip[mnih]"]),
     "terminal_select_dropped": ([(CSRC + "kernels_head.cu", "const float y = term ? r : r + h.gamma * best;",
