@@ -131,6 +131,11 @@ typedef struct {
   /* optional caller-owned HOST output (NULL = not wanted); valid when k <= 4096 */
   int64_t* step_generation;  /* [k] generation n_local of the theta each step of the call used: the
                                 realised fetch schedule (A40; in DQN_ASYNC it depends on timing)       */
+  /* output: the paper's Fig. 3 quantities per replica step, from the most recent
+     dqn_profile_steps call on this context (-1 before any): T = gradient computation (sampling,
+     forward, TD head, backward), tau = the parameter update, and the communication regions
+     (push, fetch, the fused server round, target refresh)                                              */
+  double grad_ms, update_ms, comm_ms;
 } dqn_step_stats;
 
 /* Per-region device time of the replica step (diagnostic; dqn_profile_steps). */
@@ -177,8 +182,12 @@ int dqn_push_transitions(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_
  * (collective: every rank passes the same k). Per step T: fetch when
  * T % n_fetch == 0 (then refresh theta^ when n - l >= C); sample b slots
  * uniformly with replacement; targets with theta^; gradient at the fetched
- * theta; accumulate; when (T+1) % n_push == 0 reduce-scatter the gradient to
- * the shard owners, each applies RMSProp to its shard, n += 1.
+ * theta; accumulate; when (T+1) % n_push == 0 every shard owner sums the N
+ * replicas' gradient slices of its shard in rank order, applies RMSProp to its
+ * shard and n += 1. At world > 1 that round is ONE kernel over NVLink peer memory
+ * (DQN_DETERMINISTIC with n_fetch = 1: push, update and the delivery of the new
+ * theta to every replica); otherwise an NCCL reduce-scatter, the update and an
+ * NCCL all-gather (bf16 records on DQN_BF16), on a second stream in DQN_ASYNC*.
  * stats may be NULL. DQN_EEMPTY if the replay memory is empty (nothing run);
  * DQN_ENONFINITE if any round so far produced a non-finite mean gradient. */
 int dqn_train_steps(dqn_ctx* ctx, int64_t k, dqn_step_stats* stats);

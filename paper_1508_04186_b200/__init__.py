@@ -52,7 +52,8 @@ class _Stats(C.Structure):
     _fields_ = [("loss_mean", C.c_double), ("generation", C.c_int64), ("steps_done", C.c_int64),
                 ("device_ms", C.c_float), ("nonfinite_elems", C.c_int64), ("sampled_idx", C.c_void_p),
                 ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p), ("kernel_launches", C.c_int64),
-                ("staleness_hist", C.c_int64 * 32), ("step_generation", C.c_void_p)]
+                ("staleness_hist", C.c_int64 * 32), ("step_generation", C.c_void_p), ("grad_ms", C.c_double),
+                ("update_ms", C.c_double), ("comm_ms", C.c_double)]
 
 
 class _CollectStats(C.Structure):
@@ -259,7 +260,7 @@ class DQN:
         out = dict(loss_mean=st.loss_mean, generation=st.generation, steps_done=st.steps_done,
                    device_ms=st.device_ms, nonfinite_elems=st.nonfinite_elems, idx=idx, argmax=am, loss=lp,
                    kernel_launches=st.kernel_launches, staleness=np.array(st.staleness_hist[:], np.int64), rc=rc,
-                   step_generation=sg)
+                   step_generation=sg, grad_ms=st.grad_ms, update_ms=st.update_ms, comm_ms=st.comm_ms)
         self._check(rc)
         return out
 

@@ -193,6 +193,7 @@ struct dqn_ctx {
   bool use_graphs = true;
   bool step_trace = false;  // DQN_TRACE_STEP=1
   int num_sms = 148;
+  double prof_grad_ms = -1.0, prof_update_ms = -1.0, prof_comm_ms = -1.0;  // last dqn_profile_steps (T, tau, comm)
   bool early_update = true; // N = 1 bf16: FC / output-layer RMSProp inside the conv backward launch (DQN_EARLY_UPDATE=0: off)
   bool keep_grad = false;
   bool alias_local = false;
@@ -665,7 +666,8 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
     w.krows = rows; w.Nout = L.N;
     const long long chunks = (rows + 63) / 64;
     const int m_tiles = (w.M + 127) / 128;
-    w.ranges = (int)std::max<long long>(1, std::min<long long>(chunks, (2LL * ctx->num_sms + m_tiles - 1) / m_tiles));
+    (void)m_tiles;  // every M tile of a K range shares its staged chunks: one range per CTA
+    w.ranges = (int)std::max<long long>(1, std::min<long long>(chunks, ctx->num_sms));
     w.kpr = (int)((chunks + w.ranges - 1) / w.ranges);
     w.ranges = (int)((chunks + w.kpr - 1) / w.kpr);
     ok = ok && L.N <= 64 && make_tmap_bf16(&w.ta[0], x[0], rows, G.Cs, G.Cs, w.R);
@@ -2054,6 +2056,19 @@ extern "C" int dqn_profile_steps(dqn_ctx* ctx, int64_t k, dqn_region_time* out, 
     }
   }
   if (n_regions) *n_regions = (int32_t)names.size();
+  {  // the paper's Fig. 3 split: gradient time T, update time tau, communication
+    double gm = 0.0, um = 0.0, cm = 0.0;
+    for (size_t i = 0; i < names.size(); ++i) {
+      const double us = tot[i] / cnt[i] * cnt[i] / (double)std::max<long long>(1, k);  // per step
+      const std::string& n = names[i];
+      if (n == "rmsprop_update" || n == "reduce_update") um += us;
+      else if (n == "push_reduce_scatter" || n == "fetch_all_gather" || n == "fetch_copy" || n == "target_refresh" ||
+               n == "server_round_fused" || n == "server_round_acquire")
+        cm += us;
+      else gm += us;
+    }
+    ctx->prof_grad_ms = gm / 1e3; ctx->prof_update_ms = um / 1e3; ctx->prof_comm_ms = cm / 1e3;
+  }
   for (size_t i = 0; i < names.size() && out && (int32_t)i < cap; ++i) {
     std::memset(out[i].name, 0, sizeof(out[i].name));
     std::strncpy(out[i].name, names[i].c_str(), sizeof(out[i].name) - 1);
@@ -2224,6 +2239,9 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
         stats->step_generation[t - T0] =
             ctx->async ? ctx->h_adev->fgen_log[(t / c.n_fetch) % kDiagSteps] : ctx->gen_log[t % kDiagSteps];
     stats->kernel_launches = kernels;
+    stats->grad_ms = ctx->prof_grad_ms;
+    stats->update_ms = ctx->prof_update_ms;
+    stats->comm_ms = ctx->prof_comm_ms;
     double lm = 0.0;
     for (float l : loss) lm += l;
     stats->loss_mean = loss.empty() ? 0.0 : lm / (double)loss.size();

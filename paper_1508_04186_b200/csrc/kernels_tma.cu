@@ -410,12 +410,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
     fence_async_smem();
   }
   if (warp == 1) tmem_alloc(&tbase, tcols);
-  // MMA warps (FWD / DGRAD): up to TC_NMMA, each owning a sub-ring of Sw stages and every nmma-th tile, so that
-  // each stage barrier is always consumed in order (a warp running a whole ring lap ahead of another would
-  // otherwise alias an mbarrier phase); WGRAD's long K loops keep one MMA warp and the whole ring
-  int nmma = wg ? 1 : min(min(TC_NMMA, NB), S / a.Cblk);
+  // MMA warps: up to TC_NMMA, each owning a sub-ring of Sw stages and every nmma-th tile, so that each stage
+  // barrier is always consumed in order (a warp running a whole ring lap ahead of another would otherwise alias
+  // an mbarrier phase); WGRAD keeps at least 3 stages per warp for its long K loops
+  int nmma = wg ? min(min(TC_NMMA, NB), S / 3) : min(min(TC_NMMA, NB), S / a.Cblk);
   if (nmma < 1) nmma = 1;
-  const int Sw = wg ? S : S / nmma;
+  const int Sw = S / nmma;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -435,6 +435,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
         for (int ch = 0; ch < a.T * a.Cblk; ++ch) tma_load_2d_w(fixed + ch * BN * 128, &a.tb[g], ch * 64, 0, &bfull);
       }
       int it = 0, tl_local = 0;
+      int wq[TC_NMMA] = {0, 0, 0, 0};  // WGRAD: chunks issued to each MMA warp's sub-ring
       for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
         if (!wg) {
           const int m0 = tl * 128, row0 = a.mode == TCONV_FWD ? m0 : m0 - a.maxshift;
@@ -461,10 +462,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
             wg_block(a, mb, t, cb);
             if (ncb == 0 || cbs[0] != cb) cbs[ncb++] = cb;
           }
+          // warp w's own sub-ring: its chunks counted over its tiles only (the tiles of a CTA are dealt to the MMA
+          // warps round-robin, local tile k to warp k % nmma)
+          const int w = tl_local % nmma;
           for (int c = 0; c < nch; ++c, ++it) {
-            const int st = it % S;
+            const int q = wq[w]++, st = w * Sw + q % Sw;
             const int p0 = (int)((long long)r * a.kpr * 64 + c * 64);
-            mbar_spin(&empty[st], ((it / S) & 1) ^ 1);
+            mbar_spin(&empty[st], ((q / Sw) & 1) ^ 1);
             mbar_expect_tx_w(&full[st], (uint32_t)(ncb * a.R * 128 + 8192));
             uint8_t* sb = ring + st * SB;
             for (int w = 0; w < ncb; ++w) tma_load_2d_w(sb + w * win_bytes(a.R), &a.ta[0], cbs[w] * 64, p0, &full[st]);
@@ -482,7 +486,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
       const uint32_t ring_u = smem_u32(ring);
       const uint32_t idesc = wg ? make_idesc_bf16(128, BN, 1, 1) : make_idesc_bf16(128, BN, 0, 0);
       const uint32_t fx = smem_u32(fixed);
-      int it = 0, tl_local = 0;
+      int it = 0, tl_local = 0, qj = 0;
       for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
         if (tl_local % nmma != j) {  // another MMA warp's tile: only its stages are counted
           it += wg ? chunks_of(tl / m_tiles) : a.Cblk;
@@ -529,8 +533,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
             hoff[h] = (cbs[0] == cb ? 0 : win_bytes(a.R)) + tap_shift(a, t) * 128;
           }
           for (int c = 0; c < nch; ++c, ++it) {
-            const int st = it % S;
-            mbar_spin(&full[st], (it / S) & 1);
+            const int q = qj++, st = j * Sw + q % Sw;
+            mbar_spin(&full[st], (q / Sw) & 1);
             // (TMA data: async proxy to async proxy, ordered by the mbarrier; no tcgen05 fence)
             const uint32_t sb = smem_u32(ring + st * SB);
             const uint32_t h0 = ones[0] ? fx : sb + hoff[0];
@@ -630,15 +634,141 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
   if (warp == 1) tmem_dealloc(tbase, tcols);
 }
 
+
+// ---- TCONV_WGRAD: one CTA per K range; every 64-row chunk (the Cblk X windows + the dZ tile) is staged ONCE and
+// feeds every M tile of dW (tap, c-block pairs + the all-ones db block), each M tile its own TMEM accumulator;
+// MMA warp j issues the M tiles j, j + nmma, ... of every chunk (a stage is released when all of them committed)
+__host__ __device__ __forceinline__ int twg_stage_bytes(const TConvArgs& a) { return a.Cblk * win_bytes(a.R) + 8192; }
+
+__global__ void __launch_bounds__(TC_THREADS, 1) twgrad_kernel(const __grid_constant__ TConvArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kTgMaxStages], empty[kTgMaxStages], tfull, tempty;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = a.stages, SB = twg_stage_bytes(a);
+  uint8_t* ring = smem;
+  uint8_t* ones = smem + S * SB;  // above every window: the LBO of an A tile's second half stays positive
+  const int m_tiles = (a.M + 127) / 128;
+  const int nmma = m_tiles < TC_NMMA ? m_tiles : TC_NMMA;
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], nmma);
+    }
+    mbar_init(&tfull, nmma);
+    mbar_init(&tempty, 8);
+    fence_mbar_init();
+  }
+  for (int e = tid; e < 8192 / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(ones)[e] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  fence_async_smem();
+  if (warp == 1) tmem_alloc(&tbase, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_sync();
+  auto chunks_of = [&](int r) {
+    const long long r0 = (long long)r * a.kpr * 64;
+    const long long rows = min((long long)a.kpr * 64, a.krows - r0);
+    return (int)((rows + 63) / 64);
+  };
+  if (warp == 0) {  // ---- TMA producer (whole warp; one elected lane issues)
+    int it = 0;
+    for (int r = blockIdx.x; r < a.ranges; r += gridDim.x) {
+      const int nch = chunks_of(r);
+      for (int c = 0; c < nch; ++c, ++it) {
+        const int st = it % S;
+        const int p0 = (int)((long long)r * a.kpr * 64 + c * 64);
+        mbar_spin(&empty[st], ((it / S) & 1) ^ 1);
+        mbar_expect_tx_w(&full[st], (uint32_t)(a.Cblk * a.R * 128 + 8192));
+        uint8_t* sb = ring + st * SB;
+        for (int cb = 0; cb < a.Cblk; ++cb) tma_load_2d_w(sb + cb * win_bytes(a.R), &a.ta[0], cb * 64, p0, &full[st]);
+        tma_load_2d_w(sb + a.Cblk * win_bytes(a.R), &a.tb[0], 0, p0, &full[st]);
+      }
+    }
+  } else if (warp <= TC_NMMA) {
+    const int j = warp - 1;
+    if (j < nmma) {  // ---- MMA warp j: M tiles j, j + nmma, ... of every chunk
+      const uint32_t idesc = make_idesc_bf16(128, 64, 1, 1);
+      const uint32_t ring_u = smem_u32(ring), ones_u = smem_u32(ones);
+      int it = 0, rl = 0;
+      for (int r = blockIdx.x; r < a.ranges; r += gridDim.x, ++rl) {
+        mbar_spin(&tempty, (rl & 1) ^ 1);
+        tc_fence_after();
+        const int nch = chunks_of(r);
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int st = it % S;
+          mbar_spin(&full[st], (it / S) & 1);
+          const uint32_t sb = ring_u + (uint32_t)(st * SB);
+          const uint32_t bt = sb + (uint32_t)(a.Cblk * win_bytes(a.R));
+          for (int mt = j; mt < m_tiles; mt += nmma) {
+            uint32_t h[2];
+            for (int hh = 0; hh < 2; ++hh) {
+              const int mb = 2 * mt + hh;
+              if (mb * 64 >= a.TCs) {
+                h[hh] = ones_u;
+              } else {
+                const int t = mb / a.Cblk, cb = mb - t * a.Cblk;
+                h[hh] = sb + (uint32_t)(cb * win_bytes(a.R) + ((t / a.Tw) * a.Ws + t % a.Tw) * 128);
+              }
+            }
+            const uint32_t lbo = h[1] > h[0] ? h[1] - h[0] : 0u;
+            const uint32_t d = tbase + (uint32_t)(mt * 64);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16_w(d, desc_sw128(h[0] + kk * 2048, lbo, 1024), desc_sw128(bt + kk * 2048, 8192, 1024), idesc,
+                         (c > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit_w(&empty[st]);
+        }
+        mma_commit_w(&tfull);
+      }
+    }
+  } else {  // ---- epilogue: 8 warps, thread = one row of each M tile, half of the 64 columns
+    const int q = warp & 3, half = (warp - 1 - TC_NMMA) >> 2;
+    int rl = 0;
+    for (int r = blockIdx.x; r < a.ranges; r += gridDim.x, ++rl) {
+      mbar_wait_warp(&tfull, rl & 1);
+      tc_fence_after();
+      for (int mt = 0; mt < m_tiles; ++mt) {
+        const int m = mt * 128 + 32 * q + lane;
+        for (int c = half * 32; c < half * 32 + 32; c += 16) {
+          float v[16];
+          tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(mt * 64 + c), v);
+          if ((m < a.TCs || m == a.TCs) && c < a.Nout) {
+            float* p = m < a.TCs ? a.partial + ((long long)r * a.TCs + m) * a.Nout + c : a.partial_db + (long long)r * a.Nout + c;
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
 bool init_tconv_kernel_attrs() {
   const bool ok = cudaFuncSetAttribute(tconv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) ==
-                  cudaSuccess;
+                      cudaSuccess &&
+                  cudaFuncSetAttribute(twgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) ==
+                      cudaSuccess;
   cudaGetLastError();
   return ok;
 }
 
 // the deepest ring that fits 219 KB next to the resident weights (>= 2 stages), 0: does not fit
 size_t tconv_smem(const TConvArgs& a0) {
+  if (a0.mode == TCONV_WGRAD) {
+    const int sb = twg_stage_bytes(a0), st = std::min(kTgMaxStages, (219 * 1024 - 1024 - 8192) / sb);
+    if (st < 2 || (a0.M + 127) / 128 * 64 > 512) return 0;
+    return (size_t)st * sb + 8192 + 1024;
+  }
   const int fixed = tconv_fixed_bytes(a0), sb = tconv_stage_bytes(a0);
   const int st = std::min(kTgMaxStages, (219 * 1024 - 1024 - fixed) / sb);
   if (st < 2) return 0;
@@ -647,6 +777,12 @@ size_t tconv_smem(const TConvArgs& a0) {
 
 void launch_tconv(const TConvArgs& a0, int num_sms, cudaStream_t st) {
   TConvArgs a = a0;
+  if (a.mode == TCONV_WGRAD) {
+    a.stages = std::min(kTgMaxStages, (219 * 1024 - 1024 - 8192) / twg_stage_bytes(a));
+    launch_pdl(twgrad_kernel, dim3((unsigned)std::min(a.ranges, num_sms)), dim3(TC_THREADS), tconv_smem(a), st, a);
+    sync_debug("tconv wgrad", st);
+    return;
+  }
   const int fixed = tconv_fixed_bytes(a), sb = tconv_stage_bytes(a);
   a.stages = std::min(kTgMaxStages, (219 * 1024 - 1024 - fixed) / sb);
   const int m_tiles = (a.M + 127) / 128;

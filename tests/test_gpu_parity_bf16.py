@@ -161,3 +161,18 @@ def test_fused_reduce_update_path():
     ref = O.run(on, oc, 1000, [rp], theta0.astype(np.float64), 5)
     th0 = theta0.astype(np.float64)
     assert delta_rel(th, th0, ref["theta"], th0, on, ulps=5) < TOL
+
+
+def test_fig3_timing_fields():
+    """dqn_step_stats carries the paper's Fig. 3 split from the last dqn_profile_steps: gradient
+    time T, update time tau and communication, per replica step (-1 before any profile)."""
+    dc, on, _ = nets(minibatch=32, replay_capacity=300, precision=D.BF16)
+    g, _, _ = make(dc, on, he_theta(on, 4), 300, 8)
+    out = g.train(2)
+    assert out["grad_ms"] == -1.0 and out["update_ms"] == -1.0
+    regions = g.profile(4)
+    out = g.train(2)
+    assert out["grad_ms"] > 0 and out["update_ms"] > 0 and out["comm_ms"] >= 0
+    tot = sum(r["avg_us"] * r["steps"] for r in regions) / 4 / 1e3
+    assert abs(out["grad_ms"] + out["update_ms"] + out["comm_ms"] - tot) <= 1e-6 + 1e-6 * tot
+    g.close()
