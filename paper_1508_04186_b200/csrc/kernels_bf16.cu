@@ -179,7 +179,7 @@ static_assert(FWD_SU8 + mnih::SLOT <= FWD_SMEM, "u8 staging inside the kernel's 
 
 __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar, bar_ld;
+  __shared__ uint64_t bar, bar2, bar_ld;
   __shared__ uint32_t tbase;
   const int j = blockIdx.x, g = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     long long slot = j;
     if (a.ctr) slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)j, a.ctr->ring_size);  // a1
     if (g == 0 && a.idx) a.idx[j] = (int)slot;
-    mbar_init(&bar, 1);
+    mbar_init(&bar, 4);   // conv1: one commit per issuing warp
+    mbar_init(&bar2, 4);  // conv2: likewise
     mbar_init(&bar_ld, 1);
     fence_mbar_init();
     // a2 gather: the whole u8 state in one TMA bulk copy (28,224 contiguous bytes of the ring slot)
@@ -247,21 +248,24 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   tc_fence_after();
   st_stamp(ST_P1, 0);
   const uint32_t tmem = tbase;
-  // ---- conv1: 4 M-tiles x 4 taps x 4 K-steps, M = 128, N = 16
-  if (threadIdx.x == 0) {
+  // ---- conv1: 4 M-tiles x 4 taps x 4 K-steps, M = 128, N = 16; warp w issues M-tile w (warp-uniform issue:
+  // 16 MMAs per warp instead of 64 from one thread)
+  static_assert(mnih::M1_TILES == 4, "one conv1 M-tile per warp");
+  {
+    const int mt = warp;
     const uint32_t idesc = make_idesc_bf16(128, mnih::C1, 0, 0);
     const uint32_t xb = smem_u32(sX), wb = smem_u32(sW1);
-    for (int mt = 0; mt < mnih::M1_TILES; ++mt)
-      for (int t = 0; t < 4; ++t)
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = make_desc(xb + (2 * kk) * mnih::X_ALLOC * 16 + (mt * 128 + mnih::tap_shift1(t)) * 16,
-                                        mnih::X_ALLOC * 16, 128);
-          const uint64_t bd = make_desc(wb + (t * 8 + 2 * kk) * mnih::C1 * 16, mnih::C1 * 16, 128);
-          mma_bf16(tmem + mt * mnih::C1, ad, bd, idesc, (t | kk) != 0);
-        }
-    mma_commit(&bar);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t ad = make_desc(xb + (2 * kk) * mnih::X_ALLOC * 16 + (mt * 128 + mnih::tap_shift1(t)) * 16,
+                                      mnih::X_ALLOC * 16, 128);
+        const uint64_t bd = make_desc(wb + (t * 8 + 2 * kk) * mnih::C1 * 16, mnih::C1 * 16, 128);
+        mma_bf16_w(tmem + mt * mnih::C1, ad, bd, idesc, (t | kk) != 0);
+      }
+    mma_commit_w(&bar);
   }
-  __syncwarp();
   mbar_wait(&bar, 0);
   tc_fence_after();
   st_stamp(ST_P1, 1);
@@ -296,18 +300,20 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   __syncthreads();
   tc_fence_after();
   st_stamp(ST_P1, 2);
-  // ---- conv2: 1 M-tile x 4 taps x 4 K-steps, M = 128, N = 32
-  if (threadIdx.x == 0) {
+  // ---- conv2: 1 M-tile x 4 taps x 4 K-steps, M = 128, N = 32; warp w issues tap w into its own
+  // accumulator (columns 32 w: conv1's, all read above), the epilogue sums the four in tap order
+  {
+    const int t = warp;
     const uint32_t idesc = make_idesc_bf16(128, mnih::C2, 0, 0);
     const uint32_t ab = smem_u32(sA1), wb = smem_u32(sW2);
-    for (int t = 0; t < 4; ++t)
-      for (int kk = 0; kk < 4; ++kk) {
-        const uint64_t ad = make_desc(ab + (2 * kk) * mnih::A1_ALLOC * 16 + mnih::tap_shift2(t) * 16,
-                                      mnih::A1_ALLOC * 16, 128);
-        const uint64_t bd = make_desc(wb + (t * 8 + 2 * kk) * mnih::C2 * 16, mnih::C2 * 16, 128);
-        mma_bf16(tmem + 64, ad, bd, idesc, (t | kk) != 0);
-      }
-    mma_commit(&bar);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint64_t ad = make_desc(ab + (2 * kk) * mnih::A1_ALLOC * 16 + mnih::tap_shift2(t) * 16,
+                                    mnih::A1_ALLOC * 16, 128);
+      const uint64_t bd = make_desc(wb + (t * 8 + 2 * kk) * mnih::C2 * 16, mnih::C2 * 16, 128);
+      mma_bf16_w(tmem + 32 * t, ad, bd, idesc, kk != 0);
+    }
+    mma_commit_w(&bar2);
   }
   // save conv1's activation (group 0) for the backward while conv2 runs
   if (g == 0 && a.a1_save) {
@@ -315,8 +321,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     uint4* dst = reinterpret_cast<uint4*>(a.a1_save + (long long)j * 8 * mnih::A1_ALLOC * 16);
     for (int v = threadIdx.x; v < 8 * mnih::A1_ALLOC; v += blockDim.x) dst[v] = src[v];
   }
-  __syncwarp();
-  mbar_wait(&bar, 1);
+  mbar_wait(&bar2, 0);
   st_stamp(ST_P2, 0);
   tc_fence_after();
   // ---- conv2 epilogue: + b2, ReLU, bf16, canonical flatten d = c*81 + oy*9 + ox
@@ -328,8 +333,14 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     __nv_bfloat16* out = a.a2 + ((long long)g * a.n + j) * mnih::D + oy * 9 + ox;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 64 + 16 * h, v);
+      float v[16], u[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 16 * h, v);
+#pragma unroll
+      for (int t = 1; t < 4; ++t) {
+        tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 32 * t + 16 * h, u);
+#pragma unroll
+        for (int n = 0; n < 16; ++n) v[n] += u[n];
+      }
       if (ok) {
 #pragma unroll
         for (int n = 0; n < 16; ++n) {
@@ -458,17 +469,16 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
   const bool ph = a.st_ph && tile == 0 && split == 0 && g == 0;  // DQN_TRACE_STEP phase stamps
   if (ph) st_stamp_here(a.st_ph, 0);
   const uint32_t tmem = tbase;
-  if (threadIdx.x == 0) {
+  if (warp == 0) {  // warp-uniform issue (one elected lane), not a per-lane R2UR loop under threadIdx.x == 0
     const uint32_t idesc = make_idesc_bf16(128, bn, a.a_mn, a.b_mn);
     const uint32_t ab = smem_u32(sA), bb = smem_u32(sB);
     for (int kk = 0; kk < KC / 16; ++kk) {
       const uint64_t ad = a.a_mn ? make_desc(ab + kk * 256, 128, KC * 16) : make_desc(ab + kk * 2 * 128 * 16, 128 * 16, 128);
       const uint64_t bd = a.b_mn ? make_desc(bb + kk * 256, 128, KC * 16) : make_desc(bb + kk * 2 * bn * 16, bn * 16, 128);
-      mma_bf16(tmem, ad, bd, idesc, kk > 0);
+      mma_bf16_w(tmem, ad, bd, idesc, kk > 0);
     }
-    mma_commit(&bar);
+    mma_commit_w(&bar);
   }
-  __syncwarp();
   mbar_wait(&bar, 0);
   tc_fence_after();
   if (ph) st_stamp_here(a.st_ph, 1);
@@ -696,7 +706,7 @@ __device__ void rms_tail(const ReduceUpdateArgs& u, int cta, int ctas);
 
 __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, ReduceUpdateArgs u) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar_w;
   __shared__ uint32_t tbase;
   __shared__ float s_db1[16], s_db2[32];
   const int j = blockIdx.x;
@@ -712,7 +722,8 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
   uint8_t* sDZ1 = smem + BWD_SDZ1;
   uint8_t* sW2 = smem + BWD_SW2;
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&bar, 2);    // conv2 dX: one commit per issuing warp (2)
+    mbar_init(&bar_w, 6);  // conv2 dW (2 warps) + conv1 dW (4 warps)
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(&tbase, 256);
@@ -822,30 +833,37 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
     for (int r = DZ2_OFF; r < DZ2_OFF + mnih::M2V; ++r) s += __bfloat162float(col[r * 8]);
     s_db2[lane] = s;
   }
-  // TMEM columns: [0,32) conv1 dW (2 tiles x 16), [32,96) conv2 dW (2 tiles x 32), [128,192) conv2 dX
-  if (threadIdx.x == 0) {
+  // TMEM columns: [0,32) conv1 dW (2 tiles x 16, K half 0), [32,96) conv2 dW (2 tiles x 32), [128,192) and
+  // [192,256) conv2 dX (taps 0-1, 2-3), then [128,160) conv1 dW K half 1. Warp-uniform issue spread over the
+  // four warps: warps 0-1 conv2 dW M-tile w, warps 2-3 conv2 dX tap pair w - 2 (summed in the dZ1 epilogue).
+  {
     const uint32_t xa = smem_u32(sA1), dz2 = smem_u32(sDZ2), w2 = smem_u32(sW2);
-    // conv2 dW: M = (t pair, c'') via 16 planes, K = m' (6 steps), N = 32 (B MN-major: dZ2 planes)
-    const uint32_t id_dw2 = make_idesc_bf16(128, 32, 1, 1);
-    for (int mt = 0; mt < 2; ++mt)
+    if (warp < 2) {
+      // conv2 dW: M = (t pair, c'') via 16 planes, K = m' (6 steps), N = 32 (B MN-major: dZ2 planes)
+      const uint32_t id_dw2 = make_idesc_bf16(128, 32, 1, 1);
+      const int mt = warp, sh = mt * 10;  // taps (0,1) -> shifts 0,1 ; taps (2,3) -> 10,11
+#pragma unroll
       for (int kk = 0; kk < BWD_ROWS2 / 16; ++kk) {
-        const int sh = mt * 10;  // taps (0,1) -> shifts 0,1 ; taps (2,3) -> 10,11
         const uint64_t ad = make_desc(xa + (sh + 16 * kk) * 16, 128, mnih::A1_ALLOC * 16);
         const uint64_t bd = make_desc(dz2 + (DZ2_OFF + 16 * kk) * 16, 128, DZ2_ALLOC * 16);
-        mma_bf16(tmem + 32 + 32 * mt, ad, bd, id_dw2, kk > 0);
+        mma_bf16_w(tmem + 32 + 32 * mt, ad, bd, id_dw2, kk > 0);
       }
-    // conv2 dX: M = s2d pixel rows (100 -> 128), K = n2 (2 steps per tap), N = 64 (c'')
-    const uint32_t id_dx = make_idesc_bf16(128, 64, 0, 0);
-    for (int t = 0; t < 4; ++t)
-      for (int kk = 0; kk < 2; ++kk) {
+      mma_commit_w(&bar_w);
+    } else {
+      // conv2 dX: M = s2d pixel rows (100 -> 128), K = n2 (2 steps per tap), N = 64 (c'')
+      const uint32_t id_dx = make_idesc_bf16(128, 64, 0, 0);
+      const int tp = warp - 2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = 2 * tp + (q >> 1), kk = q & 1;
         const uint64_t ad = make_desc(dz2 + (2 * kk) * DZ2_ALLOC * 16 + (DZ2_OFF - mnih::tap_shift2(t)) * 16,
                                       DZ2_ALLOC * 16, 128);
         const uint64_t bd = make_desc(w2 + ((t * 4 + 2 * kk) * 64) * 16, 64 * 16, 128);
-        mma_bf16(tmem + 128, ad, bd, id_dx, (t | kk) != 0);
+        mma_bf16_w(tmem + 128 + 64 * tp, ad, bd, id_dx, q != 0);
       }
-    mma_commit(&bar);
+      mma_commit_w(&bar);
+    }
   }
-  __syncwarp();
   mbar_wait(&bar, 0);
   tc_fence_after();
   st_stamp(ST_P6, 1);
@@ -854,7 +872,13 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
     const int p = 32 * warp + lane;  // s2d(2) pixel row of conv2's input
     float v[64];
 #pragma unroll
-    for (int c = 0; c < 64; c += 16) tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 128 + c, v + c);
+    for (int c = 0; c < 64; c += 16) {
+      float u[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 128 + c, v + c);
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 192 + c, u);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[c + i] += u[i];
+    }
     if (p < mnih::A1_PIX) {
       const int py = p / 10, px = p % 10;
 #pragma unroll
@@ -882,18 +906,21 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
   __syncthreads();
   tc_fence_after();
   st_stamp(ST_P6, 2);
-  if (threadIdx.x == 0) {
-    // conv1 dW: M = (t pair, c') via 16 X planes, K = m1 (27 steps), N = 16 (B MN-major: dZ1 planes)
+  {
+    // conv1 dW: M = (t pair, c') via 16 X planes, K = m1 (27 steps), N = 16 (B MN-major: dZ1 planes);
+    // warp w: M-tile w & 1, K half w >> 1 (steps [0,14) into columns 16 mt, [14,27) into 128 + 16 mt)
     const uint32_t xb = smem_u32(sX), dz1 = smem_u32(sDZ1);
     const uint32_t id_dw1 = make_idesc_bf16(128, 16, 1, 1);
-    for (int mt = 0; mt < 2; ++mt)
-      for (int kk = 0; kk < BWD_ROWS1 / 16; ++kk) {
-        const int sh = mt * mnih::X_W;  // taps (0,1) -> 0,1 ; (2,3) -> 21,22
-        const uint64_t ad = make_desc(xb + (sh + 16 * kk) * 16, 128, mnih::X_ALLOC * 16);
-        const uint64_t bd = make_desc(dz1 + (16 * kk) * 16, 128, BWD_ROWS1 * 16);
-        mma_bf16(tmem + 16 * mt, ad, bd, id_dw1, kk > 0);
-      }
-    mma_commit(&bar);
+    const int mt = warp & 1, kh = warp >> 1;
+    const int sh = mt * mnih::X_W;  // taps (0,1) -> 0,1 ; (2,3) -> 21,22
+    constexpr int KS = BWD_ROWS1 / 16, KH = (KS + 1) / 2;
+    const int k0 = kh * KH, k1 = kh ? KS : KH;
+    for (int kk = k0; kk < k1; ++kk) {
+      const uint64_t ad = make_desc(xb + (sh + 16 * kk) * 16, 128, mnih::X_ALLOC * 16);
+      const uint64_t bd = make_desc(dz1 + (16 * kk) * 16, 128, BWD_ROWS1 * 16);
+      mma_bf16_w(tmem + 128 * kh + 16 * mt, ad, bd, id_dw1, kk > k0);
+    }
+    mma_commit_w(&bar_w);
   }
   // db1 from the dZ1 planes while conv1 dW runs: all 128 threads, channel n = tid % 16 over the
   // row slice tid / 16 (8 slices of rows), then the 8 slice sums in slice order (deterministic)
@@ -914,7 +941,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
   }
   __syncwarp();
   st_stamp(ST_P7, 0);
-  mbar_wait(&bar, 1);
+  mbar_wait(&bar_w, 0);
   tc_fence_after();
   st_stamp(ST_P7, 1);
   // ---- per-image partials: row = (t, c) of the tile, columns = output channels
@@ -924,6 +951,9 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
     for (int mt = 0; mt < 2; ++mt) {
       float v[32];
       tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 16 * mt, v);
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 128 + 16 * mt, v + 16);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] += v[16 + i];
       float* d1 = part + (mt * 128 + r) * 16;
 #pragma unroll
       for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(d1 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);

@@ -52,19 +52,7 @@ EncodeTiledFn encode_fn() {
 // one-thread instructions (TMA, MMA, commit, expect-tx) carry their own elect.sync inside the asm. Issued from
 // under `if (lane == 0)` instead, every tcgen05.mma / TMA operand goes through a per-lane R2UR loop
 // (measured: ~110 cycles per MMA, ~1800 cycles per 16-MMA convolution tile of pure issue overhead).
-__device__ __forceinline__ void mma_bf16_w(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{ .reg .pred e, q; elect.sync _|e, 0xffffffff; setp.ne.b32 q, %4, 0;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q; }" ::"r"(d),
-      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
-  asm volatile(
-      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(smem_u32(bar))
-      : "memory");
-}
+// mma_bf16_w / mma_commit_w live in sm100.cuh (the per-image kernels use them too).
 __device__ __forceinline__ void tma_load_2d_w(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"

@@ -123,6 +123,22 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Warp-uniform variants: called by a WHOLE warp with warp-uniform operands, one lane elected inside the asm.
+// Issued from under `if (threadIdx.x == 0)` instead, every operand goes through a per-lane R2UR loop
+// (~110 cycles per MMA measured on the convolution tiles, kernels_tma.cu).
+__device__ __forceinline__ void mma_bf16_w(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred e, q; elect.sync _|e, 0xffffffff; setp.ne.b32 q, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q; }" ::"r"(d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(smem_u32(bar))
+      : "memory");
+}
 // TMEM -> registers: warp w (w%4) reads lanes 32*(w%4) .. +31, 8 / 16 consecutive columns.
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t r[8];
