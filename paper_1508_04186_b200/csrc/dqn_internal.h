@@ -442,6 +442,10 @@ void launch_gconv_wreduce(const GConvWgradArgs& a, cudaStream_t st);
 // layer 1 of the generic path: sample (a1) and gather + convert (a2) every s / s' slot of the step into the
 // bf16 s2d grid [b][21][21][64] per group, which the TMA convolution reads
 void launch_gather_s2d(const GConvFwdArgs& a, __nv_bfloat16* x1_0, __nv_bfloat16* x1_1, int groups, cudaStream_t st);
+// canonical (C,H,W)-flattened images [b][C*Ho*Wo] -> input-grid geometry [b][Hs*Ws][C] (borders untouched)
+bool chw_to_hwc_fits(int C, int Ho, int Wo);
+void launch_chw_to_hwc(const __nv_bfloat16* src, __nv_bfloat16* dst, int b, int C, int Ho, int Wo, int Ws, int HsWs,
+                       cudaStream_t st);
 bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld, int box_rows);
 void launch_tgemm(const TGemmArgs& a, int num_sms, cudaStream_t st);
 bool init_tma_kernel_attrs();  // false: the kernel cannot get its shared memory (the older GEMMs are used)

@@ -86,6 +86,7 @@ struct dqn_ctx {
   GConvWgradArgs tc_wred[kMaxConv]{};
   __nv_bfloat16* x1[2] = {};
   __nv_bfloat16* dzp[kMaxConv] = {};          // dZ of every conv layer in its input-grid geometry (zero borders)
+  __nv_bfloat16* dx_canon = nullptr;          // FC dX (masked) in the canonical flatten [b][D], before chw_to_hwc
   float* tc_part = nullptr;
   float* tc_part_db = nullptr;
   // N = 1, n_push = 1 on the TMA kernels: the head finish and the RMSProp update of the FC / output-layer
@@ -701,11 +702,18 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
       ctx->tc_wred[i].partial = ctx->tc_part; ctx->tc_wred[i].partial_db = ctx->tc_part_db;
       if (i > 0) ctx->tc_dgrad[i].dzprev = ctx->dzp[i - 1];
     }
-    // FC dX writes the last conv layer's dZ in its input-grid geometry
+    // FC dX writes the last conv layer's dZ: coalesced into the canonical flatten, then chw_to_hwc permutes it
+    // into the layer's input-grid geometry (a direct NHWC store from the GEMM epilogue is a 2-byte scatter with a
+    // C-element stride across the warp: measured 33 us at BJ.configs[4])
     const dqn_ctx::GLayer& GL2 = ctx->gl[nl - 1];
-    ctx->tg_dx.out_bf16 = ctx->dzp[nl - 1];
-    ctx->tg_dx.hwc_Wo = GL2.Wo; ctx->tg_dx.hwc_Ws = GL2.Ws;
-    ctx->tg_dx.ldo_out = (long long)GL2.Hs * GL2.Ws * GL2.N;
+    if (chw_to_hwc_fits(GL2.N, GL2.Ho, GL2.Wo) && !dalloc(ctx, &ctx->dx_canon, (long long)b * F.D)) {
+      ctx->tg_dx.out_bf16 = ctx->dx_canon;
+      ctx->tg_dx.hwc_HW = 0;
+    } else {
+      ctx->tg_dx.out_bf16 = ctx->dzp[nl - 1];
+      ctx->tg_dx.hwc_Wo = GL2.Wo; ctx->tg_dx.hwc_Ws = GL2.Ws;
+      ctx->tg_dx.ldo_out = (long long)GL2.Hs * GL2.Ws * GL2.N;
+    }
   }
   ctx->use_tconv = ok;
 }
@@ -1591,6 +1599,14 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
 // gpack (conv weights of theta -> packed images), conv forward per layer (both groups), FC forward
 // (split-K), TD head, FC dW + dX (+ReLU mask, NHWC) + head finish, per layer wgrad (+ range
 // reduction into G) and dgrad, the update. Kernels: kernels_conv.cu, kernels_bf16.cu (tc_gemm).
+// the FC dX's permutation into the last conv layer's input-grid geometry (when it does not store NHWC itself)
+static void launch_dx_hwc(dqn_ctx* ctx, cudaStream_t st) {
+  if (!ctx->dx_canon) return;
+  const dqn_ctx::GLayer& G = ctx->gl[ctx->net.n_conv - 1];
+  launch_chw_to_hwc(ctx->dx_canon, ctx->dzp[ctx->net.n_conv - 1], ctx->cfg.minibatch, G.N, G.Ho, G.Wo, G.Ws,
+                    G.Hs * G.Ws, st);
+}
+
 static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   const NetShape& net = ctx->net;
   const dqn_config& c = ctx->cfg;
@@ -1710,13 +1726,14 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   if (ctx->use_tgemm && ctx->split_update && push) {
     // side branch: head finish (dW_o, db_o, db_fc, loss, T + 1) next to the FC dW / dX, then the RMSProp update
     // of the non-conv parameters next to the conv backward; joined at the end of the step
-    PB("fc1_bwd_head_finish", 2);
+    PB("fc1_bwd_head_finish", 2 + (ctx->dx_canon ? 1 : 0));
     CK(cudaEventRecord(ctx->ev_fork, st));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     launch_head_finish_warp(h, ctx->side);
     launch_tgemm(ctx->tg_dw, ctx->num_sms, st);
     launch_tgemm(ctx->tg_dx, ctx->num_sms, st);  // reads the FC weight the side update is about to write
     CK(cudaEventRecord(ctx->ev_dw, st));
+    launch_dx_hwc(ctx, st);
     PE();
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_dw, 0));
     launch_rmsprop(ctx->theta_master + fc0, ctx->rms + fc0, ctx->grad + fc0, ctx->P_pad - fc0, (float)c.n_push,
@@ -1725,9 +1742,10 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
                    ctx->grad_snap ? ctx->grad_snap + fc0 : nullptr);
     CK(cudaEventRecord(ctx->ev_join, ctx->side));
   } else if (ctx->use_tgemm) {  // the warp-specialised TMA GEMMs, then the head finish
-    PB("fc1_bwd_head_finish", 3);
+    PB("fc1_bwd_head_finish", 3 + (ctx->dx_canon ? 1 : 0));
     launch_tgemm(ctx->tg_dw, ctx->num_sms, st);
     launch_tgemm(ctx->tg_dx, ctx->num_sms, st);
+    launch_dx_hwc(ctx, st);
     launch_head_finish_warp(h, st);
     PE();
   } else if (tc_pair_fits(gw, gx)) {

@@ -785,54 +785,107 @@ void launch_tconv(const TConvArgs& a0, int num_sms, cudaStream_t st) {
 // One CTA per (image, group); thread e handles 16 bytes = one frame's 16 s2d channels of one pixel of the
 // frame-major slot [frame][441 px][16] and writes them as 16 bf16 at [px][frame*16 ..]. The first CTA row also
 // bulk-prefetches the slot the same image index samples next step (the sampler is counter-based).
-__global__ void __launch_bounds__(224) gather_s2d_kernel(GConvFwdArgs a, __nv_bfloat16* x0, __nv_bfloat16* x1) {
+// a2 gather + expansion: one CTA per (image, group). The 28,224-byte u8 slot arrives in shared memory by one
+// TMA bulk copy, 256 threads expand it into the 441 x 128-byte bf16 rows of the conv1 input grid (thread = one
+// 16-byte output chunk: 8 u8 of one frame plane -> 8 exact bf16), and one TMA bulk store writes the image's
+// 56,448 contiguous bytes: every global access is a full-line bulk transfer, none is a 16-byte scattered store.
+constexpr int GATHER_THREADS = 256, GATHER_SLOT = 441 * 64, GATHER_OUT = 441 * 128;
+constexpr int GATHER_SMEM = GATHER_SLOT + GATHER_OUT + 16;
+__global__ void __launch_bounds__(GATHER_THREADS) gather_s2d_kernel(GConvFwdArgs a, __nv_bfloat16* x0,
+                                                                     __nv_bfloat16* x1) {
+  extern __shared__ __align__(128) uint8_t gsm[];
+  uint8_t* sU8 = gsm;
+  uint8_t* sOut = gsm + GATHER_SLOT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + GATHER_SLOT + GATHER_OUT);
   const int img = blockIdx.x, g = blockIdx.y;
   pdl_sync();  // the ring (pushes) and the replay size come from earlier launches; x is read by the previous step
-  long long slot;
-  if (a.ctr) {
-    const unsigned long long T = a.ctr->T;
-    slot = sample_slot(a.seed, a.rank, T, (unsigned)img, a.ctr->ring_size);  // a1
-    if (g == 0 && threadIdx.x == 0) {
-      if (a.idx) a.idx[img] = (int)slot;
-      const long long nxt = sample_slot(a.seed, a.rank, T + 1, (unsigned)img, a.ctr->ring_size);
-      bulk_prefetch_l2(a.ring[0] + nxt * a.slot_stride, 28224);
-      bulk_prefetch_l2(a.ring[1] + nxt * a.slot_stride, 28224);
-    }
-  } else {
-    slot = img;
-  }
-  const uint4* src = reinterpret_cast<const uint4*>(a.ring[g] + slot * a.slot_stride);
-  __nv_bfloat16* dst = (g ? x1 : x0) + (long long)img * 441 * 64;
-  // thread = one pixel: its 4 frames' 16-byte vectors (coalesced per frame plane across the warp) become one
-  // contiguous 128-byte row of 64 bf16 channels
-  for (int px = threadIdx.x; px < 441; px += blockDim.x) {
-    uint4 w[4];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) w[f] = __ldg(src + f * 441 + px);
-    uint4* d = reinterpret_cast<uint4*>(dst + (long long)px * 64);
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      const uint32_t ws[4] = {w[f].x, w[f].y, w[f].z, w[f].w};
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t o[4];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {  // 4 bytes -> 4 exact bf16 (0..255 are exact)
-          const uint32_t b = ws[2 * h + q];
-          const __nv_bfloat162 lo = __floats2bfloat162_rn((float)(b & 0xFFu), (float)((b >> 8) & 0xFFu));
-          const __nv_bfloat162 hi = __floats2bfloat162_rn((float)((b >> 16) & 0xFFu), (float)(b >> 24));
-          o[2 * q] = *reinterpret_cast<const uint32_t*>(&lo);
-          o[2 * q + 1] = *reinterpret_cast<const uint32_t*>(&hi);
-        }
-        d[2 * f + h] = make_uint4(o[0], o[1], o[2], o[3]);
+  if (threadIdx.x == 0) {
+    long long slot = img;
+    if (a.ctr) {
+      const unsigned long long T = a.ctr->T;
+      slot = sample_slot(a.seed, a.rank, T, (unsigned)img, a.ctr->ring_size);  // a1
+      if (g == 0) {
+        if (a.idx) a.idx[img] = (int)slot;
+        // the sampler is counter-based: step T+1's slot is known now; warm L2 and the TLB for it
+        const long long nxt = sample_slot(a.seed, a.rank, T + 1, (unsigned)img, a.ctr->ring_size);
+        bulk_prefetch_l2(a.ring[0] + nxt * a.slot_stride, GATHER_SLOT);
+        bulk_prefetch_l2(a.ring[1] + nxt * a.slot_stride, GATHER_SLOT);
       }
     }
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, GATHER_SLOT);
+    bulk_g2s(sU8, a.ring[g] + slot * a.slot_stride, GATHER_SLOT, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // output chunk c = (pixel px, frame f, half h): bf16 channels 8 (2 f + h) .. +7 of pixel px = bytes
+  // 8 h .. 8 h + 7 of pixel px's 16-byte vector in frame plane f (slot layout [f][441][16])
+  for (int c = threadIdx.x; c < 441 * 8; c += GATHER_THREADS) {
+    const int px = c >> 3, f = (c >> 1) & 3, h = c & 1;
+    const uint2 w = *reinterpret_cast<const uint2*>(sU8 + f * 441 * 16 + px * 16 + h * 8);
+    const uint32_t ws[2] = {w.x, w.y};
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {  // 4 bytes -> 4 exact bf16 (0..255 are exact)
+      const uint32_t v = ws[q];
+      const __nv_bfloat162 lo = __floats2bfloat162_rn((float)(v & 0xFFu), (float)((v >> 8) & 0xFFu));
+      const __nv_bfloat162 hi = __floats2bfloat162_rn((float)((v >> 16) & 0xFFu), (float)(v >> 24));
+      o[2 * q] = *reinterpret_cast<const uint32_t*>(&lo);
+      o[2 * q + 1] = *reinterpret_cast<const uint32_t*>(&hi);
+    }
+    *reinterpret_cast<uint4*>(sOut + c * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store (async proxy)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __nv_bfloat16* dst = (g ? x1 : x0) + (long long)img * 441 * 64;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(sOut)),
+                 "r"((uint32_t)GATHER_OUT)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory stays live until read
   }
 }
 
 void launch_gather_s2d(const GConvFwdArgs& a, __nv_bfloat16* x1_0, __nv_bfloat16* x1_1, int groups, cudaStream_t st) {
-  launch_pdl(gather_s2d_kernel, dim3(a.b, groups), dim3(224), 0, st, a, x1_0, x1_1);
+  launch_pdl(gather_s2d_kernel, dim3(a.b, groups), dim3(GATHER_THREADS), GATHER_SMEM, st, a, x1_0, x1_1);
   sync_debug("gather_s2d", st);
+}
+
+// FC dX, second half: the tgemm epilogue wrote dZ of the last conv layer (ReLU mask applied) in the canonical
+// (C,H,W) flatten with coalesced stores; this permutes each image into the layer's input-grid geometry
+// [py * Ws + px][C] (the zero border is never written). One CTA per image, the image staged in shared memory.
+__global__ void __launch_bounds__(256) chw_to_hwc_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, int C, int Ho,
+                                                         int Wo, int Ws, int HsWs) {
+  extern __shared__ __align__(16) uint8_t csm[];
+  __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(csm);
+  const int img = blockIdx.x, HoWo = Ho * Wo, n = C * HoWo;
+  pdl_sync();  // src is the immediate predecessor's output; dst may still be read by the previous step
+  const __nv_bfloat16* s = src + (long long)img * n;
+  for (int e = threadIdx.x; e < n / 8; e += blockDim.x)
+    reinterpret_cast<uint4*>(sx)[e] = __ldg(reinterpret_cast<const uint4*>(s) + e);
+  __syncthreads();
+  const int c8n = C / 8;
+  for (int e = threadIdx.x; e < HoWo * c8n; e += blockDim.x) {
+    const int p = e / c8n, c0 = (e - p * c8n) * 8;
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      o[j] = (uint32_t)__bfloat16_as_ushort(sx[(c0 + 2 * j) * HoWo + p]) |
+             ((uint32_t)__bfloat16_as_ushort(sx[(c0 + 2 * j + 1) * HoWo + p]) << 16);
+    const int oy = p / Wo, ox = p - oy * Wo;
+    *reinterpret_cast<uint4*>(dst + ((long long)img * HsWs + (long long)oy * Ws + ox) * C + c0) =
+        make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+bool chw_to_hwc_fits(int C, int Ho, int Wo) { return C % 8 == 0 && (C * Ho * Wo) % 8 == 0 && C * Ho * Wo * 2 <= 48 * 1024; }
+
+void launch_chw_to_hwc(const __nv_bfloat16* src, __nv_bfloat16* dst, int b, int C, int Ho, int Wo, int Ws, int HsWs,
+                       cudaStream_t st) {
+  launch_pdl(chw_to_hwc_kernel, dim3(b), dim3(256), (size_t)C * Ho * Wo * 2, st, src, dst, C, Ho, Wo, Ws, HsWs);
+  sync_debug("chw_to_hwc", st);
 }
 
 int tgemm_stages(int BN) {
@@ -845,7 +898,9 @@ size_t tgemm_smem(int BN) { return (size_t)tgemm_stages(BN) * (TG_A_BYTES + BN *
 
 bool init_tma_kernel_attrs() {
   const bool ok = cudaFuncSetAttribute(tgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       200 * 1024 + 1024) == cudaSuccess;  // every ring fits 200 KB
+                                       200 * 1024 + 1024) == cudaSuccess &&  // every ring fits 200 KB
+                  cudaFuncSetAttribute(gather_s2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GATHER_SMEM) ==
+                      cudaSuccess;
   cudaGetLastError();
   return ok;
 }
