@@ -22,7 +22,10 @@ constexpr int HS_AMAX = 32;
 constexpr int HS_MAX_SPLITS = kHeadMaxSplits;
 
 // dynamic smem: h [H] | h' [H] | W^_o [A][H] | W_o[a_j] [H]
-__global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
+// CH: FC split-K partials in flight per thread and group (all of them at small b, where the head is on the
+// latency-bound critical path; 8 at large b, where 4 CTAs per SM need the register budget)
+template <int CH, int MINB>
+__global__ void __launch_bounds__(HS_THREADS, MINB) head_sample_kernel(HeadArgs h) {
   extern __shared__ float4 sm4[];
   const int H = h.H, A = h.A, j = blockIdx.x;
   float* s_h0 = reinterpret_cast<float*>(sm4);  // [H]
@@ -49,18 +52,25 @@ __global__ void __launch_bounds__(HS_THREADS) head_sample_kernel(HeadArgs h) {
   if (h.fc_partial) {
     const int ns = h.fc_splits;
     for (int u = threadIdx.x; u < H; u += HS_THREADS) {
-      float pv[2][HS_MAX_SPLITS];  // every split of both groups in flight at once
+      // the splits of both groups, CH at a time in flight, summed in split order (zeros past ns are exact)
+      float s2[2] = {0.0f, 0.0f};
+      for (int s0 = 0; s0 < ns; s0 += CH) {
+        float pv[2][CH];
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        const float* p = h.fc_partial + (long long)g * ns * h.fc_split_stride + (long long)j * H + u;
+        for (int g = 0; g < 2; ++g) {
+          const float* p = h.fc_partial + (long long)g * ns * h.fc_split_stride + (long long)j * H + u;
 #pragma unroll
-        for (int sp = 0; sp < HS_MAX_SPLITS; ++sp) pv[g][sp] = sp < ns ? __ldcg(p + (long long)sp * h.fc_split_stride) : 0.0f;
+          for (int k = 0; k < CH; ++k)
+            pv[g][k] = s0 + k < ns ? __ldcg(p + (long long)(s0 + k) * h.fc_split_stride) : 0.0f;
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int k = 0; k < CH; ++k) s2[g] += pv[g][k];
       }
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
-        float s = 0.0f;
-#pragma unroll
-        for (int sp = 0; sp < HS_MAX_SPLITS; ++sp) s += pv[g][sp];  // split order (zeros past ns are exact)
+        const float s = s2[g];
         const float v = fmaxf(s + __ldg(h.fc_bias[g] + u), 0.0f);
         (g ? s_h1 : s_h0)[u] = v;
         h.act_out[g][(long long)j * H + u] = v;
@@ -139,12 +149,16 @@ size_t head_smem_bytes(int A, int H, int b) {
 
 void init_head_kernel_attrs() {
   // the 227 KB opt-in limit includes the kernel's static shared memory
-  cudaFuncSetAttribute(head_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+  cudaFuncSetAttribute(head_sample_kernel<HS_MAX_SPLITS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+  cudaFuncSetAttribute(head_sample_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
   cudaGetLastError();  // an attribute refusal only limits the largest head; validate_cfg bounds it
 }
 
 void launch_head_f32(const HeadArgs& h, cudaStream_t st, bool with_finish) {
-  launch_pdl(head_sample_kernel, dim3(h.b), dim3(HS_THREADS), head_smem_bytes(h.A, h.H, h.b), st, h);
+  if (h.b <= 128)
+    launch_pdl(head_sample_kernel<HS_MAX_SPLITS, 1>, dim3(h.b), dim3(HS_THREADS), head_smem_bytes(h.A, h.H, h.b), st, h);
+  else
+    launch_pdl(head_sample_kernel<8, 4>, dim3(h.b), dim3(HS_THREADS), head_smem_bytes(h.A, h.H, h.b), st, h);
   if (!with_finish) return;  // the bf16 path runs the finish inside its fused FC-backward launch
   const int n = h.A * h.H + h.A + h.H + 1;
   launch_pdl(head_finish_kernel, dim3((n + 255) / 256), dim3(256), 0, st, h);

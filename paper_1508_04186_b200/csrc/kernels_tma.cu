@@ -787,16 +787,15 @@ void launch_tconv(const TConvArgs& a0, int num_sms, cudaStream_t st) {
 // bulk-prefetches the slot the same image index samples next step (the sampler is counter-based).
 // a2 gather + expansion: one CTA per (image, group). The 28,224-byte u8 slot arrives in shared memory by one
 // TMA bulk copy, 256 threads expand it into the 441 x 128-byte bf16 rows of the conv1 input grid (thread = one
-// 16-byte output chunk: 8 u8 of one frame plane -> 8 exact bf16), and one TMA bulk store writes the image's
-// 56,448 contiguous bytes: every global access is a full-line bulk transfer, none is a 16-byte scattered store.
-constexpr int GATHER_THREADS = 256, GATHER_SLOT = 441 * 64, GATHER_OUT = 441 * 128;
-constexpr int GATHER_SMEM = GATHER_SLOT + GATHER_OUT + 16;
+// 16-byte output chunk: 8 u8 of one frame plane -> 8 exact bf16; a warp stores 512 contiguous bytes). 28 KB of
+// shared memory per CTA keeps ~7 CTAs per SM, i.e. the whole b = 512 x 2 gather resident in one wave.
+constexpr int GATHER_THREADS = 256, GATHER_SLOT = 441 * 64;
+constexpr int GATHER_SMEM = GATHER_SLOT + 16;
 __global__ void __launch_bounds__(GATHER_THREADS) gather_s2d_kernel(GConvFwdArgs a, __nv_bfloat16* x0,
                                                                      __nv_bfloat16* x1) {
   extern __shared__ __align__(128) uint8_t gsm[];
   uint8_t* sU8 = gsm;
-  uint8_t* sOut = gsm + GATHER_SLOT;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + GATHER_SLOT + GATHER_OUT);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + GATHER_SLOT);
   const int img = blockIdx.x, g = blockIdx.y;
   pdl_sync();  // the ring (pushes) and the replay size come from earlier launches; x is read by the previous step
   if (threadIdx.x == 0) {
@@ -819,6 +818,7 @@ __global__ void __launch_bounds__(GATHER_THREADS) gather_s2d_kernel(GConvFwdArgs
   }
   __syncthreads();
   mbar_wait(bar, 0);
+  uint4* dst = reinterpret_cast<uint4*>((g ? x1 : x0) + (long long)img * 441 * 64);
   // output chunk c = (pixel px, frame f, half h): bf16 channels 8 (2 f + h) .. +7 of pixel px = bytes
   // 8 h .. 8 h + 7 of pixel px's 16-byte vector in frame plane f (slot layout [f][441][16])
   for (int c = threadIdx.x; c < 441 * 8; c += GATHER_THREADS) {
@@ -834,17 +834,7 @@ __global__ void __launch_bounds__(GATHER_THREADS) gather_s2d_kernel(GConvFwdArgs
       o[2 * q] = *reinterpret_cast<const uint32_t*>(&lo);
       o[2 * q + 1] = *reinterpret_cast<const uint32_t*>(&hi);
     }
-    *reinterpret_cast<uint4*>(sOut + c * 16) = make_uint4(o[0], o[1], o[2], o[3]);
-  }
-  fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store (async proxy)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __nv_bfloat16* dst = (g ? x1 : x0) + (long long)img * 441 * 64;
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(sOut)),
-                 "r"((uint32_t)GATHER_OUT)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // shared memory stays live until read
+    dst[c] = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
