@@ -1010,19 +1010,42 @@ __device__ __forceinline__ float bwd_part_sum(int e, const BwdConvArgs& a) {
 }
 
 // Sum the per-image partials in image order (deterministic) and scatter into G's canonical layout.
+// Large b: warp w of the CTA sums images [64 w, 64 w + 64) of 32 consecutive entries in image order (two rounds
+// of 32 loads in flight instead of b / 32 serial rounds), then the CTA adds the warps' subtotals in warp order:
+// a fixed two-level order, deterministic run to run. One warp per CTA (b <= 64) is the plain image order.
 __global__ void bwd_reduce_kernel(BwdConvArgs a) {
+  __shared__ float s_sub[4][32];
   st_stamp(ST_BWD_REDUCE, 0);
   pdl_sync();
   st_stamp(ST_BWD_REDUCE, 1);
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= BWD_PART) return;
-  a.grad[bwd_part_dst(e, a)] += bwd_part_sum(e, a);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  const int per = (a.n + nw - 1) / nw, i_lo = w * per, i_hi = min(a.n, i_lo + per);
+  float s = 0.0f;
+  if (e < BWD_PART) {
+    for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+      float v[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = i0 + k < i_hi ? __ldcg(a.partial + (long long)(i0 + k) * BWD_PART + e) : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (i0 + k < i_hi) s += v[k];
+    }
+  }
+  s_sub[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && e < BWD_PART) {
+    float t = s_sub[0][lane];
+    for (int q = 1; q < nw; ++q) t += s_sub[q][lane];
+    a.grad[bwd_part_dst(e, a)] += e < BWD_PART_W1 ? t * (1.0f / 255.0f) : t;
+  }
   st_stamp(ST_BWD_REDUCE, 2);
 }
 
 void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st, bool with_reduce) {
   launch_pdl(bwd_conv_bf16_kernel, dim3(a.n), dim3(128), BWD_SMEM, st, a, ReduceUpdateArgs{});
-  if (with_reduce) launch_pdl(bwd_reduce_kernel, dim3(cdiv(BWD_PART, 128)), dim3(128), 0, st, a);
+  const int nw = std::min(4, std::max(1, (a.n + 63) / 64));  // warps (image groups of >= 64) per 32 entries
+  if (with_reduce) launch_pdl(bwd_reduce_kernel, dim3(cdiv(BWD_PART, 32)), dim3(32 * nw), 0, st, a);
 }
 
 // N = 1, n_push = 1: the image-order reduction of the conv partials fused into the RMSProp update
