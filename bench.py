@@ -359,6 +359,8 @@ def main():
                     help="override the hidden FC width of the config's net (model-size sweep, SURVEY §8(d) BJ.c5)")
     ap.add_argument("--dedup", action="store_true",
                     help="frame-deduplicated replay (F+1 frames per slot; G-pong stacks slide by one frame)")
+    ap.add_argument("--prio-alpha", type=float, default=0.0,
+                    help="prioritized replay variant (NEXT-4, A41): alpha in {1, 0.5}; 0 = uniform (default)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
@@ -399,7 +401,8 @@ def main():
     for p in ([prec] if prec is not None else [D.BF16, D.FP32]):
         cfg = D.Config(**net, minibatch=b, replay_capacity=args.replay, target_sync=C["C"], precision=p,
                        lr=2.5e-4, gamma=0.99, n_push=C["n_push"], n_fetch=C["n_fetch"],
-                       sync_mode=D.ASYNC if C["async"] else D.DETERMINISTIC, replay_dedup=int(args.dedup))
+                       sync_mode=D.ASYNC if C["async"] else D.DETERMINISTIC, replay_dedup=int(args.dedup),
+                       replay_prio_alpha=args.prio_alpha, replay_prio_eps=0.01 if args.prio_alpha else 0.0)
         try:
             dqn = D.DQN(cfg, rank=rank, world=world, nccl_id=nccl_id, stream=stream.cuda_stream)
             break
@@ -538,6 +541,7 @@ def main():
                                                                       if args.fc is not None else ""),
                    "net": net_name(net), "minibatch_per_replica": b,
                    "replay_per_replica": args.replay, "replay_dedup": bool(args.dedup),
+                   "replay_sampling": (f"prioritized, alpha {args.prio_alpha} (A41)" if args.prio_alpha else "uniform"),
                    "target_sync_C": C["C"] if C["C"] < 2**40 else None,
                    "n_push": C["n_push"], "n_fetch": C["n_fetch"],
                    "sync_mode": "async (a fetch takes the newest published generation)" if C["async"] else "deterministic",

@@ -111,6 +111,13 @@ typedef struct {
                                           it into a snapshot that dqn_get_params(DQN_PARAMS_GRAD) returns.
                                           Diagnostic; the step's kernels, launch configuration and
                                           arithmetic are otherwise unchanged (it adds one store per element) */
+  double replay_prio_alpha;            /* prioritized replay (NEXT-4, "emphasize transitions from which we
+                                          can learn the most"; rule = DESIGN.md A41): 0 = uniform sampling (a1,
+                                          default); 1 or 0.5 = draw slot i with probability p_i / sum p, p_i =
+                                          (|delta_i| + replay_prio_eps)^alpha written after the step that sampled
+                                          it, stored transitions entering with the largest p so far; b stratified
+                                          draws per step from a 32-ary fp32 sum tree. Not with dqn_collect */
+  double replay_prio_eps;              /* eps_p >= 0 of the priority                                           */
 } dqn_config;
 
 typedef struct {
@@ -136,6 +143,8 @@ typedef struct {
      forward, TD head, backward), tau = the parameter update, and the communication regions
      (push, fetch, the fused server round, target refresh)                                              */
   double grad_ms, update_ms, comm_ms;
+  /* optional caller-owned HOST output (NULL = not wanted); valid when k <= 4096 */
+  float* td_error;           /* [k][b] delta_j = Q(phi_j, a_j; theta) - y_j, unclipped (A27)            */
 } dqn_step_stats;
 
 /* Per-region device time of the replica step (diagnostic; dqn_profile_steps). */
@@ -250,6 +259,12 @@ int dqn_env_stacks(dqn_ctx* ctx, uint8_t* out, int64_t cap_bytes);
 
 /* Replay occupancy: total pushes so far and min(count, capacity). */
 int dqn_replay_size(const dqn_ctx* ctx, int64_t* count, int64_t* size);
+
+/* Prioritized replay (cfg.replay_prio_alpha != 0; NEXT-4, A41): the replay_capacity leaf priorities
+ * p_i (0 = never stored) into out[cap >= replay_capacity] and the sum-tree total into *total (either may
+ * be NULL; host or device pointers). Synchronises the context stream. DQN_EINVAL without prioritized
+ * replay or with a short buffer. */
+int dqn_get_priorities(dqn_ctx* ctx, float* out, int64_t cap, float* total);
 
 /* Last error message of this context ("" if none); with ctx == NULL, the message of the
  * last failed dqn_create on the calling thread. Never NULL. */

@@ -45,7 +45,8 @@ class _Config(C.Structure):
                 ("n_push", C.c_int32), ("n_fetch", C.c_int32), ("target_sync", C.c_int64),
                 ("precision", C.c_int32), ("sync_mode", C.c_int32), ("seed", C.c_uint64),
                 ("init_std", C.c_double), ("init_seed", C.c_uint64), ("init_params", C.c_void_p),
-                ("server_rule", C.c_int32), ("replay_dedup", C.c_int32), ("keep_grad", C.c_int32)]
+                ("server_rule", C.c_int32), ("replay_dedup", C.c_int32), ("keep_grad", C.c_int32),
+                ("replay_prio_alpha", C.c_double), ("replay_prio_eps", C.c_double)]
 
 
 class _Stats(C.Structure):
@@ -53,7 +54,7 @@ class _Stats(C.Structure):
                 ("device_ms", C.c_float), ("nonfinite_elems", C.c_int64), ("sampled_idx", C.c_void_p),
                 ("target_argmax", C.c_void_p), ("loss_per_step", C.c_void_p), ("kernel_launches", C.c_int64),
                 ("staleness_hist", C.c_int64 * 32), ("step_generation", C.c_void_p), ("grad_ms", C.c_double),
-                ("update_ms", C.c_double), ("comm_ms", C.c_double)]
+                ("update_ms", C.c_double), ("comm_ms", C.c_double), ("td_error", C.c_void_p)]
 
 
 class _CollectStats(C.Structure):
@@ -92,6 +93,8 @@ class Config:
     server_rule: int = 0   # SERVER_MEAN (A7) | SERVER_PER_GRADIENT (A33)
     replay_dedup: int = 0  # 1: F+1 frames per slot (s' = s shifted by one frame + a new frame)
     keep_grad: int = 0     # 1: the update kernels also store the pushed gradient (DQN_PARAMS_GRAD)
+    replay_prio_alpha: float = 0.0  # prioritized replay (A41): 0 = uniform, 1 or 0.5
+    replay_prio_eps: float = 0.0
 
     def to_c(self, init_ptr: Optional[int] = None) -> _Config:
         c = _Config()
@@ -104,7 +107,7 @@ class Config:
             c.fc_units[i] = u
         for name in ("n_actions", "minibatch", "gamma", "lr", "rms_decay", "rms_eps", "err_clip", "replay_capacity",
                      "n_push", "n_fetch", "target_sync", "precision", "sync_mode", "seed", "init_std", "init_seed",
-                     "server_rule", "replay_dedup", "keep_grad"):
+                     "server_rule", "replay_dedup", "keep_grad", "replay_prio_alpha", "replay_prio_eps"):
             setattr(c, name, getattr(self, name))
         c.init_params = init_ptr
         return c
@@ -138,6 +141,7 @@ def lib() -> C.CDLL:
         L.dqn_profile_steps.argtypes = [P, C.c_int64, C.POINTER(_RegionTime), C.c_int32, C.POINTER(C.c_int32)]
         L.dqn_get_params.argtypes = [P, C.c_int, P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
         L.dqn_replay_size.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.dqn_get_priorities.argtypes = [P, P, C.c_int64, P]
         L.dqn_last_error.restype = C.c_char_p
         L.dqn_last_error.argtypes = [P]
         L.dqn_destroy.argtypes = [P]
@@ -149,7 +153,7 @@ def lib() -> C.CDLL:
 
 EXPORTED = ("dqn_param_count", "dqn_nccl_id_bytes", "dqn_nccl_unique_id", "dqn_create", "dqn_push_transitions",
             "dqn_train_steps", "dqn_profile_steps", "dqn_q_values", "dqn_get_params", "dqn_replay_size", "dqn_last_error",
-            "dqn_destroy", "dqn_collect", "dqn_env_stacks", "dqn_store_and_train")
+            "dqn_destroy", "dqn_collect", "dqn_env_stacks", "dqn_store_and_train", "dqn_get_priorities")
 
 
 def param_count(cfg: Config) -> int:
@@ -232,7 +236,7 @@ class DQN:
         self._check(lib().dqn_push_transitions(self._h, n, ps, pa, pr, pn, pt))
 
     def train(self, k: int, want_idx: bool = False, want_argmax: bool = False, want_loss: bool = False,
-              store=None, want_generation: bool = False) -> dict:
+              store=None, want_generation: bool = False, want_delta: bool = False) -> dict:
         """k replica steps (dqn_train_steps); with store = (s, a, r, s_next, term) of k transitions, Alg. 1's
         loop instead: transition i is stored, then step i runs (dqn_store_and_train)."""
         st = _Stats()
@@ -241,6 +245,8 @@ class DQN:
         am = np.zeros((k, b), np.int32) if want_argmax else None
         lp = np.zeros(k, np.float32) if want_loss else None
         sg = np.zeros(k, np.int64) if want_generation else None
+        dl = np.zeros((k, b), np.float32) if want_delta else None
+        st.td_error = dl.ctypes.data if dl is not None else None
         st.step_generation = sg.ctypes.data if sg is not None else None
         st.sampled_idx = idx.ctypes.data if idx is not None else None
         st.target_argmax = am.ctypes.data if am is not None else None
@@ -260,7 +266,7 @@ class DQN:
         out = dict(loss_mean=st.loss_mean, generation=st.generation, steps_done=st.steps_done,
                    device_ms=st.device_ms, nonfinite_elems=st.nonfinite_elems, idx=idx, argmax=am, loss=lp,
                    kernel_launches=st.kernel_launches, staleness=np.array(st.staleness_hist[:], np.int64), rc=rc,
-                   step_generation=sg, grad_ms=st.grad_ms, update_ms=st.update_ms, comm_ms=st.comm_ms)
+                   step_generation=sg, grad_ms=st.grad_ms, update_ms=st.update_ms, comm_ms=st.comm_ms, delta=dl)
         self._check(rc)
         return out
 
@@ -319,6 +325,13 @@ class DQN:
         g = C.c_uint64()
         self._check(lib().dqn_get_params(self._h, which, None, 0, C.byref(n), C.byref(g)))
         return int(g.value)
+
+    def priorities(self) -> Tuple[np.ndarray, float]:
+        """Prioritized replay (A41): the leaf priorities [replay_capacity] and the sum-tree total."""
+        out = np.zeros(self.cfg.replay_capacity, np.float32)
+        tot = np.zeros(1, np.float32)
+        self._check(lib().dqn_get_priorities(self._h, out.ctypes.data, out.size, tot.ctypes.data))
+        return out, float(tot[0])
 
     def replay_size(self) -> Tuple[int, int]:
         c, s = C.c_int64(), C.c_int64()

@@ -92,6 +92,7 @@ struct HeadArgs {
   float* s_dq;                // [b]
   int* s_act;                 // [b]
   float* s_loss;              // [b]
+  float* s_delta;             // [b] delta_j (unclipped TD error; the prioritized replay's update reads it)
   const float* theta;         // live theta (fp32, canonical)
   const float* theta_hat;     // target theta^ (fp32, canonical)
   long long w_off, b_off;     // output layer
@@ -110,6 +111,15 @@ struct HeadArgs {
   float* diag_loss;           // [kDiagSteps]
   int* diag_idx;              // [kDiagSteps][b]
   int* diag_amax;             // [kDiagSteps][b]
+  float* diag_delta;          // [kDiagSteps][b] delta_j per step (dqn_step_stats.td_error)
+};
+
+// prioritized replay (NEXT-4, A41): 32-ary fp32 sum tree, level l at node + off[l], level K = the root
+constexpr int kPrioMaxLevels = 6;  // 32^6 slots
+struct PrioTree {
+  float* node;
+  long long off[kPrioMaxLevels + 1];
+  int K;
 };
 
 // ------------------------------------------------------------------ launchers
@@ -252,6 +262,7 @@ struct FwdConvArgs {
   long long img_off;               // conv weight image (wimg.cuh) inside theta[g]
   long long slot_stride;           // bytes between replay slots (28,224, or 35,280 with frame dedup)
   int late;                        // 1: sample + gather after the PDL wait (the predecessor wrote the ring)
+  const int* idx_in;               // prioritized replay: the slots prio_sample_kernel drew (nullptr: a1's sampler)
 };
 // dqn_store_and_train on the bf16 Mnih path: Alg. 1's Store as the first kernel of every step of the
 // replayed step graph. The graph is fixed, so the chunk of transitions and its position come from here
@@ -330,6 +341,7 @@ struct GConvFwdArgs {
   const DevCounters* ctr;          // layer 1: sampler state (nullptr: image j = slot j)
   unsigned long long seed;
   unsigned rank;
+  const int* idx_in;               // layer 1, prioritized replay: the drawn slots (nullptr: a1's sampler)
   int first;                       // 1: layer 1 (u8 input, 1/255 folded into the epilogue)
   long long slot_stride;           // layer 1: bytes between replay slots (frame-major s2d)
   int b, Hs, Ws, Cs, Th, Tw, Ho, Wo, N;
@@ -441,6 +453,12 @@ void launch_tconv(const TConvArgs& a, int num_sms, cudaStream_t st);
 void launch_gconv_wreduce(const GConvWgradArgs& a, cudaStream_t st);
 // layer 1 of the generic path: sample (a1) and gather + convert (a2) every s / s' slot of the step into the
 // bf16 s2d grid [b][21][21][64] per group, which the TMA convolution reads
+void launch_prio_sample(const PrioTree& t, int b, unsigned long long seed, unsigned rank, const DevCounters* ctr,
+                        int* idx, cudaStream_t st);
+void launch_prio_update(const PrioTree& t, int b, const int* idx, const float* delta, int alpha_half, float eps,
+                        float* maxp, cudaStream_t st);
+void launch_prio_push(const PrioTree& t, long long cap, long long first, long long m, const float* maxp,
+                      cudaStream_t st);
 void launch_gather_s2d(const GConvFwdArgs& a, __nv_bfloat16* x1_0, __nv_bfloat16* x1_1, int groups, cudaStream_t st);
 // canonical (C,H,W)-flattened images [b][C*Ho*Wo] -> input-grid geometry [b][Hs*Ws][C] (borders untouched)
 bool chw_to_hwc_fits(int C, int Ho, int Wo);

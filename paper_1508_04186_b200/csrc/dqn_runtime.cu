@@ -176,6 +176,14 @@ struct dqn_ctx {
   // dqn_store_and_train on the bf16 Mnih path: the Store runs inside the step graphs (variant bit 16)
   StoreCtl* store_ctl = nullptr;
   bool graph_store = false;
+  // prioritized replay (NEXT-4, A41; cfg.replay_prio_alpha != 0)
+  bool prio = false;
+  int prio_alpha_half = 0;
+  float prio_eps = 0.0f;
+  PrioTree ptree{};
+  float* prio_maxp = nullptr;                 // the largest priority written so far (1 initially)
+  float* head_delta = nullptr;                // [b] delta_j of the step (TD head -> prio_update)
+  float* diag_delta = nullptr;                // [kDiagSteps][b]
   bool store_chunks_ready = false;
   // multi-step graphs: kChunkLog lengths 2^0..2^(kChunkLog-1) of consecutive same-variant steps,
   // so the programmatic (PDL) edges also span step boundaries (a graph boundary serialises)
@@ -330,6 +338,13 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   }
   if (c->server_rule != DQN_SERVER_MEAN && c->server_rule != DQN_SERVER_PER_GRADIENT) { *why = "unknown server_rule"; return DQN_EINVAL; }
   if (c->replay_dedup != 0 && (c->replay_dedup != 1 || c->frames < 2)) { *why = "replay_dedup needs 0, or 1 with frames >= 2"; return DQN_EINVAL; }
+  if (!(c->replay_prio_alpha == 0.0 || c->replay_prio_alpha == 0.5 || c->replay_prio_alpha == 1.0) ||
+      !(c->replay_prio_eps >= 0.0 && std::isfinite(c->replay_prio_eps))) {
+    *why = "replay_prio_alpha must be 0, 0.5 or 1 and replay_prio_eps finite >= 0 (A41)"; return DQN_EINVAL;
+  }
+  if (c->replay_prio_alpha != 0.0 && c->replay_capacity > (1LL << 30)) {
+    *why = "prioritized replay: capacity <= 2^30"; return DQN_EINVAL;
+  }
   if (c->server_rule == DQN_SERVER_PER_GRADIENT && c->sync_mode != DQN_DETERMINISTIC) {
     *why = "DQN_SERVER_PER_GRADIENT needs DQN_DETERMINISTIC"; return DQN_EINVAL;
   }
@@ -414,7 +429,7 @@ static void free_all(dqn_ctx* c) {
                   c->diag_idx, c->diag_amax, c->head_dq, c->head_act, c->head_loss, c->q_stage, c->q_out, c->q_amax, c->d_stage,
                   c->theta_local_bf16, c->theta_hat_bf16, c->a2_bf16, c->a1_save,
                   c->dh_bf16, c->dz2_bf16, c->fc_partial, c->tc_counters, c->bwd_partial, c->q_stage_s2d,
-                  c->store_ctl};
+                  c->store_ctl, c->ptree.node, c->prio_maxp, c->head_delta, c->diag_delta, c->dx_canon};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& G : c->gl) {
@@ -932,6 +947,29 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
   if ((rc = dalloc(ctx, &ctx->head_dq, b))) return rc;
   if ((rc = dalloc(ctx, &ctx->head_act, b))) return rc;
   if ((rc = dalloc(ctx, &ctx->head_loss, b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->head_delta, b))) return rc;
+  if ((rc = dalloc(ctx, &ctx->diag_delta, (long long)kDiagSteps * b))) return rc;
+  if (cfg->replay_prio_alpha != 0.0) {  // the 32-ary sum tree: 32^K leaves (0 = never stored), K levels above
+    ctx->prio = true;
+    ctx->prio_alpha_half = cfg->replay_prio_alpha == 0.5;
+    ctx->prio_eps = (float)cfg->replay_prio_eps;
+    int K = 1;
+    long long L = 32;
+    while (L < ctx->cap) { L *= 32; ++K; }
+    ctx->ptree.K = K;
+    long long off = 0;
+    for (int l = 0; l <= K; ++l) {
+      ctx->ptree.off[l] = off;
+      off += L;
+      L /= 32;
+    }
+    if ((rc = dalloc(ctx, &ctx->ptree.node, off))) return rc;
+    CK(cudaMemsetAsync(ctx->ptree.node, 0, sizeof(float) * off, ctx->stream));
+    if ((rc = dalloc(ctx, &ctx->prio_maxp, 1))) return rc;
+    const float one = 1.0f;
+    CK(cudaMemcpyAsync(ctx->prio_maxp, &one, sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   if ((rc = dalloc(ctx, &ctx->ctr, 1))) return rc;
   CK(cudaMemsetAsync(ctx->ctr, 0, sizeof(DevCounters), ctx->stream));
   if ((rc = dalloc(ctx, &ctx->diag_loss, kDiagSteps))) return rc;
@@ -1100,6 +1138,8 @@ static void push_ring(dqn_ctx* ctx, long long i0, long long m, const uint8_t* s,
     launch_push_canonical(ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->count, 0,
                           i0, m, ctx->net.state_bytes, s, a, r, sn, t, ctx->stream, size_out, size, ctx->slot_stride,
                           ctx->dedup);
+  // prioritized replay: the stored slots enter with the largest priority so far (A41)
+  if (ctx->prio) launch_prio_push(ctx->ptree, ctx->cap, (ctx->count + i0) % ctx->cap, m, ctx->prio_maxp, ctx->stream);
 }
 
 
@@ -1237,6 +1277,21 @@ static void prof_end(dqn_ctx* ctx) {
 #define PB(name, k) prof_begin(ctx, name, k)
 #define PE() prof_end(ctx)
 
+// prioritized replay (A41): the draws of step T (before the forward) and the priority update after the TD head
+static void enqueue_prio_sample(dqn_ctx* ctx, cudaStream_t st) {
+  PB("prio_sample", 1);
+  launch_prio_sample(ctx->ptree, ctx->cfg.minibatch, ctx->cfg.seed, (unsigned)ctx->rank, ctx->ctr, ctx->idx, st);
+  PE();
+}
+static void enqueue_prio_update(dqn_ctx* ctx, cudaStream_t st) {
+  if (!ctx->prio) return;
+  PB("prio_update", 1);
+  launch_prio_update(ctx->ptree, ctx->cfg.minibatch, ctx->idx, ctx->head_delta, ctx->prio_alpha_half, ctx->prio_eps,
+                     ctx->prio_maxp, st);
+  PE();
+}
+
+
 // a13 on the bf16 path over NCCL: pack this rank's record, one all-gather, unpack every rank's record into
 // the working copies (fp32 entries outside the FC weight, bf16 everywhere + the conv weight image)
 static int enqueue_fetch_bf16(dqn_ctx* ctx, cudaStream_t st, float* dst, __nv_bfloat16* dst_bf16) {
@@ -1280,7 +1335,8 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   }
   // a1 sample
   PB("sample", 1);
-  launch_sample(ctx->idx, b, c.seed, (unsigned)ctx->rank, ctx->ctr, st);
+  if (ctx->prio) launch_prio_sample(ctx->ptree, b, c.seed, (unsigned)ctx->rank, ctx->ctr, ctx->idx, st);
+  else launch_sample(ctx->idx, b, c.seed, (unsigned)ctx->rank, ctx->ctr, st);
   PE();
   // a2-a4 convolutions, theta on s and theta^ on s' in one launch per layer
   ImgSrc src0{};
@@ -1335,9 +1391,11 @@ static int enqueue_step_f32(dqn_ctx* ctx, bool fetch, bool refresh, bool push) {
   h.dH = net.n_fc > 0 ? ctx->dz_fc[net.n_fc - 1] : ctx->dz_conv[net.n_conv - 1];
   h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
   h.s_dq = ctx->head_dq; h.s_act = ctx->head_act; h.s_loss = ctx->head_loss;
+  h.s_delta = ctx->head_delta; h.diag_delta = ctx->diag_delta;
   PB("head_td", 2);
   launch_head_f32(h, st);
   PE();
+  enqueue_prio_update(ctx, st);
   // a7 hidden FC backward
   for (int l = net.n_fc - 1; l >= 0; --l) {
     const FcShape& F = net.fc[l];
@@ -1466,6 +1524,11 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   fa.img_off = ctx->img_off;
   fa.slot_stride = ctx->slot_stride;
   fa.late = store ? 1 : 0;
+  if (ctx->prio) {  // the draws come from the sum tree: the forward waits for them (A41)
+    enqueue_prio_sample(ctx, st);
+    fa.idx_in = ctx->idx;
+    fa.late = 1;
+  }
   PB("conv_fwd", 1);
   launch_fwd_conv_bf16(fa, 2, st);
   PE();
@@ -1500,9 +1563,11 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   h.st_id = ST_HEAD;
   h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
   h.s_dq = ctx->head_dq; h.s_act = ctx->head_act; h.s_loss = ctx->head_loss;
+  h.s_delta = ctx->head_delta; h.diag_delta = ctx->diag_delta;
   PB("head_sample", 1);
   launch_head_f32(h, st, /*with_finish=*/false);
   PE();
+  enqueue_prio_update(ctx, st);
   // a7 FC backward: dW[h][d] += sum_j dH[j][h] a2[j][d]  and  dz2[j][d] = [a2 > 0] sum_h dH[j][h] W[h][d]
   TcGemmArgs gw{};
   gw.A[0] = ctx->dh_bf16; gw.lda = F.H; gw.a_mn = 1;
@@ -1648,11 +1713,13 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     PE();
   }
   // a1-a4s: sample + gather (layer 1) and every conv forward, s with theta and s' with theta^
+  if (ctx->prio) enqueue_prio_sample(ctx, st);  // the draws from the sum tree (A41), read by layer 1
   PB("conv_fwd", ctx->use_tconv ? nl + 1 : nl);
   if (ctx->use_tconv) {
     GConvFwdArgs ga{};
     ga.ring[0] = ctx->ring_s; ga.ring[1] = ctx->ring_sn; ga.slot_stride = ctx->slot_stride;
     ga.idx = ctx->idx; ga.ctr = ctx->ctr; ga.seed = c.seed; ga.rank = (unsigned)ctx->rank; ga.b = b;
+    ga.idx_in = ctx->prio ? ctx->idx : nullptr;
     launch_gather_s2d(ga, ctx->x1[0], ctx->x1[1], 2, st);
     for (int i = 0; i < nl; ++i) launch_tconv(ctx->tc_fwd[i], ctx->num_sms, st);
   }
@@ -1664,6 +1731,7 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     if (i == 0) {
       a.ring[0] = ctx->ring_s; a.ring[1] = ctx->ring_sn; a.slot_stride = ctx->slot_stride;
       a.idx = ctx->idx; a.ctr = ctx->ctr; a.seed = c.seed; a.rank = (unsigned)ctx->rank;
+      a.idx_in = ctx->prio ? ctx->idx : nullptr;
     } else {
       a.x[0] = G.x[0]; a.x[1] = G.x[1];
     }
@@ -1702,9 +1770,11 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   h.act_out[0] = ctx->act_fc[0][0]; h.act_out[1] = ctx->act_fc[0][1];
   h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
   h.s_dq = ctx->head_dq; h.s_act = ctx->head_act; h.s_loss = ctx->head_loss;
+  h.s_delta = ctx->head_delta; h.diag_delta = ctx->diag_delta;
   PB("head_sample", 1);
   launch_head_f32(h, st, false);
   PE();
+  enqueue_prio_update(ctx, st);
   // a7: FC dW (plain store at n_push = 1) + FC dX (x ReLU mask, into the last conv's NHWC dZ)
   const dqn_ctx::GLayer& GL = ctx->gl[nl - 1];
   TcGemmArgs gw{};
@@ -2132,7 +2202,7 @@ extern "C" int dqn_store_and_train(dqn_ctx* ctx, int64_t k, const uint8_t* s, co
   // graphs (store_step_kernel), so the steps keep their PDL overlap; otherwise one ring kernel plus a
   // one-step graph per iteration (DQN_GRAPH_STORE=0 forces the latter)
   const char* gs = getenv("DQN_GRAPH_STORE");
-  if (!ctx->store_ctl && ctx->bf16 && !ctx->gpath && !(gs && atoi(gs) == 0)) {
+  if (!ctx->store_ctl && ctx->bf16 && !ctx->gpath && !ctx->prio && !(gs && atoi(gs) == 0)) {
     int rc0 = dalloc(ctx, &ctx->store_ctl, 1);
     if (rc0) return rc0;
     ctx->graph_store = true;
@@ -2168,6 +2238,11 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
       for (long long s = 0; s < k; ++s)
         CK(cudaMemcpyAsync(stats->target_argmax + s * c.minibatch,
                            ctx->diag_amax + ((T0 + s) % kDiagSteps) * c.minibatch, sizeof(int) * c.minibatch,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    if (stats && stats->td_error)
+      for (long long s = 0; s < k; ++s)
+        CK(cudaMemcpyAsync(stats->td_error + s * c.minibatch,
+                           ctx->diag_delta + ((T0 + s) % kDiagSteps) * c.minibatch, sizeof(float) * c.minibatch,
                            cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -2379,6 +2454,7 @@ extern "C" int dqn_collect(dqn_ctx* ctx, int32_t n_envs, int32_t grid, int64_t s
   const NetShape& net = ctx->net;
   const int F = net.F, H = net.Hin;
   if (net.A != 4) return set_err(ctx, DQN_EINVAL, "dqn_collect: the Snake game needs n_actions == 4");
+  if (ctx->prio) return set_err(ctx, DQN_EINVAL, "dqn_collect stores without priorities: not with replay_prio_alpha");
   if (net.Hin != net.Win || grid < 4 || grid > 32 || H % grid != 0 || ((long long)H * H) % 16 != 0)
     return set_err(ctx, DQN_EINVAL, "dqn_collect: needs square frames, 4 <= grid <= 32, height % grid == 0, H*H % 16 == 0");
   if (n_envs < 1 || n_envs > ctx->cfg.minibatch || n_envs > ctx->cap || steps < 0 || !(epsilon >= 0.0 && epsilon <= 1.0))
@@ -2591,6 +2667,21 @@ extern "C" int dqn_get_params(dqn_ctx* ctx, int which, float* out, int64_t cap, 
     return DQN_OK;
   }
   CK(cudaMemcpyAsync(out, src, sizeof(float) * ctx->P, kind, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DQN_OK;
+}
+
+extern "C" int dqn_get_priorities(dqn_ctx* ctx, float* out, int64_t cap, float* total) {
+  if (!ctx) return DQN_EINVAL;
+  if (ctx->poisoned) return DQN_ESTATE;
+  if (!ctx->prio) return set_err(ctx, DQN_EINVAL, "priorities exist only with replay_prio_alpha != 0");
+  if (out && cap < ctx->cap) return set_err(ctx, DQN_EINVAL, "output buffer smaller than replay_capacity");
+  if (out)
+    CK(cudaMemcpyAsync(out, ctx->ptree.node, sizeof(float) * ctx->cap,
+                       is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+  if (total)
+    CK(cudaMemcpyAsync(total, ctx->ptree.node + ctx->ptree.off[ctx->ptree.K], sizeof(float),
+                       is_device_ptr(total) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return DQN_OK;
 }

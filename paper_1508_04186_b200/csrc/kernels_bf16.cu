@@ -197,8 +197,9 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   }
   if (threadIdx.x == 0) {
     long long slot = j;
-    if (a.ctr) slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)j, a.ctr->ring_size);  // a1
-    if (g == 0 && a.idx) a.idx[j] = (int)slot;
+    if (a.idx_in) slot = a.idx_in[j];  // prioritized replay (A41): drawn by the predecessor (a.late = 1)
+    else if (a.ctr) slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)j, a.ctr->ring_size);  // a1
+    if (g == 0 && a.idx && !a.idx_in) a.idx[j] = (int)slot;
     mbar_init(&bar, 4);   // conv1: one commit per issuing warp
     mbar_init(&bar2, 4);  // conv2: likewise
     mbar_init(&bar_ld, 1);
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     // the sampler is counter-based: step T+1's slot is known now. Prefetch it into L2 so that the
     // next step's gather is an L2 hit with a warm TLB (a random 28 KB slot of a 56 GB ring
     // otherwise costs a page walk); harmless if a push changes the ring size before T+1.
-    if (a.ctr) {
+    if (a.ctr && !a.idx_in) {
       const long long nxt = sample_slot(a.seed, a.rank, a.ctr->T + 1, (unsigned)j, a.ctr->ring_size);
       bulk_prefetch_l2(a.ring[g] + nxt * a.slot_stride, mnih::SLOT);
     }

@@ -190,7 +190,9 @@ __global__ void __launch_bounds__(128) gconv_fwd_kernel(GConvFwdArgs a) {
   if (row_ok) {
     if (a.first) {
       long long slot;
-      if (a.ctr) {
+      if (a.idx_in) {
+        slot = a.idx_in[img];  // prioritized replay (A41)
+      } else if (a.ctr) {
         slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)img, a.ctr->ring_size);  // a1
         if (g == 0 && oy == 0 && ox == 0 && a.idx) a.idx[img] = (int)slot;
       } else {

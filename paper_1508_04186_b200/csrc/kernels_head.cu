@@ -120,9 +120,11 @@ __global__ void __launch_bounds__(HS_THREADS, MINB) head_sample_kernel(HeadArgs 
       h.s_dq[j] = dq;
       h.s_act[j] = act;
       h.s_loss[j] = 0.5f * delta * delta;
+      h.s_delta[j] = delta;
       const int dslot = (int)(h.ctr->T % kDiagSteps);
       h.diag_idx[(long long)dslot * h.b + j] = slot;
       h.diag_amax[(long long)dslot * h.b + j] = barg;
+      h.diag_delta[(long long)dslot * h.b + j] = delta;
     }
   }
   __syncthreads();

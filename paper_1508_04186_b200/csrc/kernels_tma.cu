@@ -800,7 +800,9 @@ __global__ void __launch_bounds__(GATHER_THREADS) gather_s2d_kernel(GConvFwdArgs
   pdl_sync();  // the ring (pushes) and the replay size come from earlier launches; x is read by the previous step
   if (threadIdx.x == 0) {
     long long slot = img;
-    if (a.ctr) {
+    if (a.idx_in) {
+      slot = a.idx_in[img];  // prioritized replay (A41): drawn by the predecessor
+    } else if (a.ctr) {
       const unsigned long long T = a.ctr->T;
       slot = sample_slot(a.seed, a.rank, T, (unsigned)img, a.ctr->ring_size);  // a1
       if (g == 0) {

@@ -63,6 +63,15 @@ MUTATIONS = {
         CSRC + "kernels_comm.cu", "const long long m = forced >= 0 ? forced : (long long)g;",
         "const long long m = forced >= 0 ? forced : (long long)g - (g > 0 ? 1 : 0);")],
         ["tests/test_gpu_async.py::test_async_free_running_fp32_equals_its_realised_schedule[4-1-2-0]"]),
+    "prio_sqrt_dropped": ([(CSRC + "kernels_prio.cu", "    if (alpha_half) p = __fsqrt_rn(p);\n", "")],
+                          ["tests/test_gpu_prio.py::test_prioritized_replay_teacher_forced[fp32-a05]"]),
+    "prio_duplicate_first_wins": ([(CSRC + "kernels_prio.cu",
+                                    "for (int k = j + 1; k < b && !later; ++k) later = idx[k] == i;",
+                                    "for (int k = 0; k < j && !later; ++k) later = idx[k] == i;")],
+                                  ["tests/test_gpu_prio.py::test_prioritized_replay_teacher_forced[fp32-a1]"]),
+    "prio_not_stratified": ([(CSRC + "kernels_prio.cu", "float r = __fmul_rn(__fadd_rn((float)j, u), __fdiv_rn(S, (float)b));",
+                              "float r = __fmul_rn(u, S);")],
+                            ["tests/test_gpu_prio.py::test_prioritized_replay_teacher_forced[fp32-a1]"]),
 }
 
 
