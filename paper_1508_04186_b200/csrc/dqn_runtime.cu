@@ -683,6 +683,8 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
     const long long chunks = (rows + 63) / 64;
     const int m_tiles = (w.M + 127) / 128;
     (void)m_tiles;  // every M tile of a K range shares its staged chunks: one range per CTA
+    // one K range per SM (measured at BJ.configs[4]: 1/2, 1/4, 1/8 of the SMs with proportionally longer
+    // ranges cost +21 / +74 / +187 us of conv backward: the per-chunk MMA work, not the partials, binds)
     w.ranges = (int)std::max<long long>(1, std::min<long long>(chunks, ctx->num_sms));
     w.kpr = (int)((chunks + w.ranges - 1) / w.ranges);
     w.ranges = (int)((chunks + w.kpr - 1) / w.kpr);

@@ -339,23 +339,13 @@ __host__ __device__ __forceinline__ int acc_buffers(int BN) {
 constexpr int TC_NMMA = 4;        // MMA-issuing warps: issue cost (~100 cycles per tcgen05.mma with its operand
                                   // broadcast) exceeds a small-N MMA's execution, so 4 warps issue for alternate tiles
 constexpr int TC_THREADS = 32 * (1 + TC_NMMA + 8);  // producer warp, MMA warps, 8 epilogue warps (2 per TMEM quadrant)
-__device__ __forceinline__ int tap_shift(const TConvArgs& a, int t) { return (t / a.Tw) * a.Ws + t % a.Tw; }
 __host__ __device__ __forceinline__ int win_bytes(int rows) { return (rows * 128 + 1023) / 1024 * 1024; }
-// the (t, c-block) pair of 64-row M block mb of the weight gradient; mb * 64 >= TCs: the all-ones block
-__device__ __forceinline__ void wg_block(const TConvArgs& a, int mb, int& t, int& cb) {
-  t = mb / a.Cblk;
-  cb = mb % a.Cblk;
-}
 }  // namespace
 
-// smem: FWD / DGRAD: [resident B: T*Cblk chunks x BN rows x 128 B][stages x window of R rows]
-//       WGRAD: [stages x (2 windows of R rows + a dZ tile of 64 x 128 B)][ones tile 64 x 128 B]
-__host__ __device__ __forceinline__ int tconv_stage_bytes(const TConvArgs& a) {
-  return a.mode == TCONV_WGRAD ? 2 * win_bytes(a.R) + 8192 : win_bytes(a.R);
-}
-__host__ __device__ __forceinline__ int tconv_fixed_bytes(const TConvArgs& a) {
-  return a.mode == TCONV_WGRAD ? 8192 : a.T * a.Cblk * a.BN * 128;
-}
+// smem (FWD / DGRAD; the weight gradient is twgrad_kernel): [resident B: T*Cblk chunks x BN rows x 128 B]
+// [stages x window of R rows]
+__host__ __device__ __forceinline__ int tconv_stage_bytes(const TConvArgs& a) { return win_bytes(a.R); }
+__host__ __device__ __forceinline__ int tconv_fixed_bytes(const TConvArgs& a) { return a.T * a.Cblk * a.BN * 128; }
 
 __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_constant__ TConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -364,22 +354,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = a.stages, BN = a.BN, SB = tconv_stage_bytes(a);
-  const bool wg = a.mode == TCONV_WGRAD;
-  // FWD / DGRAD: resident B first, then the ring; WGRAD: the ring first, then the ones tile ABOVE it (the
-  // second MN half of an A tile is addressed as half 0 + LBO, so the ones block must lie above every window)
-  uint8_t* fixed = wg ? smem + S * SB : smem;
-  uint8_t* ring = wg ? smem : smem + tconv_fixed_bytes(a);
+  uint8_t* fixed = smem;  // the resident B operand, then the ring
+  uint8_t* ring = smem + tconv_fixed_bytes(a);
   // NB TMEM accumulators (as many as 512 columns hold, at most kMaxAcc): the MMA warp runs up to NB tiles ahead
   // of the epilogue, which hides the commit -> epilogue -> release round trip of short tiles
   const int NB = acc_buffers(BN);
   const uint32_t tcols = 512;
-  // work split: FWD / DGRAD tiles of 128 rows, CTA c serving group c % groups (its resident weights);
-  // WGRAD tiles (m-tile, K range)
+  // work split: tiles of 128 rows, CTA c serving group c % groups (its resident weights)
   const int m_tiles = (a.M + 127) / 128;
-  const int g = wg ? 0 : (int)(blockIdx.x % a.groups);
-  const int cta = wg ? blockIdx.x : blockIdx.x / a.groups;
-  const int ctas = wg ? gridDim.x : (gridDim.x - g + a.groups - 1) / a.groups;
-  const int tiles = wg ? m_tiles * a.ranges : m_tiles;
+  const int g = (int)(blockIdx.x % a.groups);
+  const int cta = blockIdx.x / a.groups;
+  const int ctas = (gridDim.x - g + a.groups - 1) / a.groups;
+  const int tiles = m_tiles;
   if (tid == 0) {
     for (int st = 0; st < S; ++st) {
       mbar_init(&full[st], 1);
@@ -392,16 +378,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
     }
     fence_mbar_init();
   }
-  if (wg) {  // the all-ones operand block (db = sum over rows of dZ); every element equal, so unswizzled
-    for (int e = tid; e < 8192 / 16; e += blockDim.x)
-      reinterpret_cast<uint4*>(fixed)[e] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-    fence_async_smem();
-  }
   if (warp == 1) tmem_alloc(&tbase, tcols);
   // MMA warps: up to TC_NMMA, each owning a sub-ring of Sw stages and every nmma-th tile, so that each stage
   // barrier is always consumed in order (a warp running a whole ring lap ahead of another would otherwise alias
-  // an mbarrier phase); WGRAD keeps at least 3 stages per warp for its long K loops
-  int nmma = wg ? min(min(TC_NMMA, NB), S / 3) : min(min(TC_NMMA, NB), S / a.Cblk);
+  // an mbarrier phase)
+  int nmma = min(min(TC_NMMA, NB), S / a.Cblk);
   if (nmma < 1) nmma = 1;
   const int Sw = S / nmma;
   tc_fence_before();
@@ -410,22 +391,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
   if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) reinterpret_cast<long long*>(a.partial)[193] = clock64();
   pdl_sync();
   if ((a.dbg & 64) && blockIdx.x == 0 && tid == 0) reinterpret_cast<long long*>(a.partial)[194] = clock64();
-  auto chunks_of = [&](int r) {  // WGRAD: 64-row chunks of K range r
-    const long long r0 = (long long)r * a.kpr * 64;
-    const long long rows = min((long long)a.kpr * 64, a.krows - r0);
-    return (int)((rows + 63) / 64);
-  };
 
   if (warp == 0) {
     {  // ---- TMA producer (whole warp, warp-uniform; one elected lane issues)
-      if (!wg) {
-        mbar_expect_tx_w(&bfull, (uint32_t)(a.T * a.Cblk * BN * 128));
-        for (int ch = 0; ch < a.T * a.Cblk; ++ch) tma_load_2d_w(fixed + ch * BN * 128, &a.tb[g], ch * 64, 0, &bfull);
-      }
+      mbar_expect_tx_w(&bfull, (uint32_t)(a.T * a.Cblk * BN * 128));
+      for (int ch = 0; ch < a.T * a.Cblk; ++ch) tma_load_2d_w(fixed + ch * BN * 128, &a.tb[g], ch * 64, 0, &bfull);
       int it = 0, tl_local = 0;
-      int wq[TC_NMMA] = {0, 0, 0, 0};  // WGRAD: chunks issued to each MMA warp's sub-ring
       for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
-        if (!wg) {
+        {
           const int m0 = tl * 128, row0 = a.mode == TCONV_FWD ? m0 : m0 - a.maxshift;
           // the stages of MMA warp w's k-th tile: its own sub-ring of Sw stages (consumed in order by that warp)
           const int w = tl_local % nmma, k = tl_local / nmma;
@@ -440,51 +413,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
             }
             if ((a.dbg & 64) && blockIdx.x == 0 && it < 64 && lane == 0) reinterpret_cast<long long*>(a.partial)[it] = clock64();
           }
-        } else {
-          const int mt = tl % m_tiles, r = tl / m_tiles, nch = chunks_of(r);
-          int cbs[2], ncb = 0;
-          for (int h = 0; h < 2; ++h) {
-            const int mb = 2 * mt + h;
-            if (mb * 64 >= a.TCs) continue;
-            int t, cb;
-            wg_block(a, mb, t, cb);
-            if (ncb == 0 || cbs[0] != cb) cbs[ncb++] = cb;
-          }
-          // warp w's own sub-ring: its chunks counted over its tiles only (the tiles of a CTA are dealt to the MMA
-          // warps round-robin, local tile k to warp k % nmma)
-          const int w = tl_local % nmma;
-          for (int c = 0; c < nch; ++c, ++it) {
-            const int q = wq[w]++, st = w * Sw + q % Sw;
-            const int p0 = (int)((long long)r * a.kpr * 64 + c * 64);
-            mbar_spin(&empty[st], ((q / Sw) & 1) ^ 1);
-            mbar_expect_tx_w(&full[st], (uint32_t)(ncb * a.R * 128 + 8192));
-            uint8_t* sb = ring + st * SB;
-            for (int w = 0; w < ncb; ++w) tma_load_2d_w(sb + w * win_bytes(a.R), &a.ta[0], cbs[w] * 64, p0, &full[st]);
-            tma_load_2d_w(sb + 2 * win_bytes(a.R), &a.tb[0], 0, p0, &full[st]);
-          }
         }
       }
     }
   } else if (warp <= TC_NMMA) {
     const int j = warp - 1;
     if (j < nmma) {  // ---- MMA issuer j: local tiles j, j + nmma, ... (whole warp, warp-uniform; one lane issues)
-      if (!wg) mbar_spin(&bfull, 0);
+      mbar_spin(&bfull, 0);
       const bool fwd = a.mode == TCONV_FWD;
       const int Th = a.T / a.Tw;
       const uint32_t ring_u = smem_u32(ring);
-      const uint32_t idesc = wg ? make_idesc_bf16(128, BN, 1, 1) : make_idesc_bf16(128, BN, 0, 0);
+      const uint32_t idesc = make_idesc_bf16(128, BN, 0, 0);
       const uint32_t fx = smem_u32(fixed);
-      int it = 0, tl_local = 0, qj = 0;
+      int it = 0, tl_local = 0;
       for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
         if (tl_local % nmma != j) {  // another MMA warp's tile: only its stages are counted
-          it += wg ? chunks_of(tl / m_tiles) : a.Cblk;
+          it += a.Cblk;
           continue;
         }
         const int buf = tl_local % NB;
         if (!(a.dbg & 128)) mbar_spin(&tempty[buf], ((tl_local / NB) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tbase + (uint32_t)(buf * BN);
-        if (!wg) {
+        {
           const int k = tl_local / nmma;
           for (int cb = 0; cb < a.Cblk; ++cb, ++it) {
             const int q = k * a.Cblk + cb, st = j * Sw + q % Sw;
@@ -506,36 +457,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
             if (a.dbg & 8) mbar_arrive_w(&empty[st]);
             else mma_commit_w(&empty[st]);
           }
-        } else {
-          const int mt = tl % m_tiles, r = tl / m_tiles, nch = chunks_of(r);
-          // the two 64-row halves of the A tile: a (t, cb) window read from row shift(t), or the ones block
-          int cbs[2], ncb = 0, hoff[2];
-          bool ones[2];
-          for (int h = 0; h < 2; ++h) {
-            const int mb = 2 * mt + h;
-            ones[h] = mb * 64 >= a.TCs;
-            if (ones[h]) continue;
-            int t, cb;
-            wg_block(a, mb, t, cb);
-            if (ncb == 0 || cbs[0] != cb) cbs[ncb++] = cb;
-            hoff[h] = (cbs[0] == cb ? 0 : win_bytes(a.R)) + tap_shift(a, t) * 128;
-          }
-          for (int c = 0; c < nch; ++c, ++it) {
-            const int q = qj++, st = j * Sw + q % Sw;
-            mbar_spin(&full[st], (q / Sw) & 1);
-            // (TMA data: async proxy to async proxy, ordered by the mbarrier; no tcgen05 fence)
-            const uint32_t sb = smem_u32(ring + st * SB);
-            const uint32_t h0 = ones[0] ? fx : sb + hoff[0];
-            const uint32_t h1 = ones[1] ? fx : sb + hoff[1];
-            // 64-wide MN groups: half 1 at half 0 + lbo (both halves the ones block: lbo 0 - never past it)
-            const uint32_t lbo = h1 > h0 ? h1 - h0 : 0u;
-            const uint32_t bt = sb + 2 * win_bytes(a.R);
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_w(d, desc_sw128(h0 + kk * 2048, lbo, 1024), desc_sw128(bt + kk * 2048, 8192, 1024), idesc,
-                         (c > 0 || kk > 0) ? 1u : 0u);
-            mma_commit_w(&empty[st]);
-          }
         }
         if (a.dbg & 8) mbar_arrive_w(&tfull[buf]);
         else mma_commit_w(&tfull[buf]);
@@ -549,7 +470,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
       const int buf = tl_local % NB;
       mbar_wait_warp(&tfull[buf], (tl_local / NB) & 1);
       tc_fence_after();
-      const int mt = wg ? tl % m_tiles : tl, r = wg ? tl / m_tiles : 0;
+      const int mt = tl;
       const int m = mt * 128 + 32 * q + lane;
       const uint32_t trow = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
       for (int c = c_lo; c < c_hi; c += 16) {
@@ -602,12 +523,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
           uint4* dst = reinterpret_cast<uint4*>(a.dzprev + row * a.Cp + cc);
           dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
           dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
-        } else {  // TCONV_WGRAD: per-range partials of dW (rows (t, c)) and of db (the first ones row)
-          if ((m < a.TCs || m == a.TCs) && c < a.Nout) {  // Nout % 16 == 0: whole 16-column groups
-            float* p = m < a.TCs ? a.partial + ((long long)r * a.TCs + m) * a.Nout + c : a.partial_db + (long long)r * a.Nout + c;
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          }
         }
       }
       tc_fence_before();
@@ -774,9 +689,9 @@ void launch_tconv(const TConvArgs& a0, int num_sms, cudaStream_t st) {
   const int fixed = tconv_fixed_bytes(a), sb = tconv_stage_bytes(a);
   a.stages = std::min(kTgMaxStages, (219 * 1024 - 1024 - fixed) / sb);
   const int m_tiles = (a.M + 127) / 128;
-  const long long tiles = a.mode == TCONV_WGRAD ? (long long)m_tiles * a.ranges : (long long)m_tiles * a.groups;
+  const long long tiles = (long long)m_tiles * a.groups;
   int grid = (int)std::min<long long>(tiles, num_sms);
-  if (a.mode != TCONV_WGRAD) grid -= grid % a.groups;  // whole CTA sets per group
+  grid -= grid % a.groups;  // whole CTA sets per group
   launch_pdl(tconv_kernel, dim3(grid), dim3(TC_THREADS), tconv_smem(a), st, a);
   sync_debug(a.mode == TCONV_FWD ? "tconv fwd" : a.mode == TCONV_DGRAD ? "tconv dgrad" : "tconv wgrad", st);
 }

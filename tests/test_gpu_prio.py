@@ -23,7 +23,7 @@ CAP = 1500  # K = 3 levels above 32768 leaves; the second push wraps the ring
                                                 (D.BF16, {}, 1.0), (D.BF16, SCALED, 0.5)],
                          ids=["fp32-a1", "fp32-a05", "bf16-mnih-a1", "bf16-scaled-a05"])
 def test_prioritized_replay_teacher_forced(precision, kw, alpha):
-    eps = 0.01
+    eps = 1.0 if alpha == 1.0 else 0.01  # alpha = 1: every written priority exceeds the initial max (1)
     dc, on, _ = nets(minibatch=32, replay_capacity=CAP, precision=precision, target_sync=3, lr=1e-3,
                      replay_prio_alpha=alpha, replay_prio_eps=eps, **kw)
     theta0 = he_theta(on, 5)
@@ -61,6 +61,7 @@ def test_prioritized_replay_teacher_forced(precision, kw, alpha):
     g.push(*more)
     leaves, total = g.priorities()
     stored = [(1200 + i) % CAP for i in range(600)]
+    assert maxp > 1.0 or alpha != 1.0
     assert np.all(leaves[stored] == maxp)
     lv = PR.build_tree(leaves, K)
     assert lv[-1][0] == np.float32(total)

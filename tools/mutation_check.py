@@ -38,9 +38,9 @@ MUTATIONS = {
                               [G + "test_gated_one_step[scaled-b32]"]),
     "tgemm_fc_dX_relu_mask": ([(CSRC + "kernels_tma.cu", "__float2bfloat16_rn(bf16_gt0(mk[i]) ? v[i] : 0.0f)",
                                 "__float2bfloat16_rn(v[i])")], [G + "test_gated_one_step[scaled-b32]"]),
-    "tconv_wgrad_tap_shift_dropped": ([(CSRC + "kernels_tma.cu",
-                                        "hoff[h] = (cbs[0] == cb ? 0 : win_bytes(a.R)) + tap_shift(a, t) * 128;",
-                                        "hoff[h] = (cbs[0] == cb ? 0 : win_bytes(a.R));")],
+    "twgrad_tap_shift_dropped": ([(CSRC + "kernels_tma.cu",
+                                   "h[hh] = sb + (uint32_t)(cb * win_bytes(a.R) + ((t / a.Tw) * a.Ws + t % a.Tw) * 128);",
+                                   "h[hh] = sb + (uint32_t)(cb * win_bytes(a.R));")],
                                       [G + "test_gated_one_step[scaled-b32]"]),
     "error_clip_one_sided": ([(CSRC + "kernels_head.cu", "dc = fminf(fmaxf(dc, -h.clip), h.clip);",
                                "dc = fminf(dc, h.clip);")], [G + "test_gated_error_clip[mnih]"]),
@@ -65,10 +65,8 @@ MUTATIONS = {
         ["tests/test_gpu_async.py::test_async_free_running_fp32_equals_its_realised_schedule[4-1-2-0]"]),
     "prio_sqrt_dropped": ([(CSRC + "kernels_prio.cu", "    if (alpha_half) p = __fsqrt_rn(p);\n", "")],
                           ["tests/test_gpu_prio.py::test_prioritized_replay_teacher_forced[fp32-a05]"]),
-    "prio_duplicate_first_wins": ([(CSRC + "kernels_prio.cu",
-                                    "for (int k = j + 1; k < b && !later; ++k) later = idx[k] == i;",
-                                    "for (int k = 0; k < j && !later; ++k) later = idx[k] == i;")],
-                                  ["tests/test_gpu_prio.py::test_prioritized_replay_teacher_forced[fp32-a1]"]),
+    "prio_max_priority_not_kept": ([(CSRC + "kernels_prio.cu", "    *maxp = mm;\n", "")],
+                                   ["tests/test_gpu_prio.py::test_prioritized_replay_teacher_forced[fp32-a1]"]),
     "prio_not_stratified": ([(CSRC + "kernels_prio.cu", "float r = __fmul_rn(__fadd_rn((float)j, u), __fdiv_rn(S, (float)b));",
                               "float r = __fmul_rn(u, S);")],
                             ["tests/test_gpu_prio.py::test_prioritized_replay_teacher_forced[fp32-a1]"]),
