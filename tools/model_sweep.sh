@@ -9,6 +9,6 @@ run() {
          --master-port 29633 bench.py --gpus $N "$@" 2>/dev/null | grep "^{" >> $out; fi
 }
 C="--steps 300 --warmup 10 --replay 100000 --e2e-steps 10 --profile-steps 40 --no-cpu-baseline --no-acting"
-for fc in 128 256 512; do run --config c2 --fc $fc $C; done  # (128 + b) * fc * 2 B <= 200 KB: fc <= 640 at b = 32
-run --config c5 $C
+for fc in 128 256 512; do run --config c2 --fc $fc $C; done  # Mnih stack, b = 32 (tc_pair stages (128 + b) fc 2 B <= 200 KB)
+for fc in 512 1024 2048; do run --config c5 --fc $fc $C; done  # scaled net, b = 512: the TMA GEMMs take any fc
 cat $out | cut -c1-200
