@@ -58,8 +58,11 @@ enum { DQN_DETERMINISTIC = 0, /* lock-step: a fetch returns the current server t
 /* how a push round combines the N workers' gradients (Alg. 2)
  *   MEAN         : one RMSProp application of the mean of the N*n_push gradients, n += 1 (A7)
  *   PER_GRADIENT : Alg. 2 literally - each worker's gradient (mean of its n_push) applied in turn
- *                  in rank order, one RMSProp application and n += 1 each (A33). N > 1 needs the
- *                  fused server round (DQN_DETERMINISTIC, n_fetch = 1); DQN_ASYNC is rejected. */
+ *                  in rank order, one RMSProp application and n += 1 each (A33). N > 1: the fused
+ *                  server round (DQN_DETERMINISTIC, n_fetch = 1), or DQN_ASYNC / DQN_ASYNC_LAG1, where
+ *                  the round's all-to-all delivers every worker's slice into the owner's inbox on the
+ *                  comm stream (only whole rounds are published: fetched generations are multiples
+ *                  of N). DQN_DETERMINISTIC with n_fetch > 1 is rejected. */
 enum { DQN_SERVER_MEAN = 0, DQN_SERVER_PER_GRADIENT = 1 };
 
 /* which parameter vector dqn_get_params returns */

@@ -222,13 +222,19 @@ struct AsyncCopy {
   float* hat;                      // theta^ (copied too when the fetch refreshes, A10)
   __nv_bfloat16* hatb;
   long long n32, n16;              // fp32 / bf16 elements
+  long long npr;                   // generations per round (1, or N with the per-gradient rule): slot = m / npr % 3
 };
 // fetch f: pick the generation (forced >= 0: that one, the lag-1 twin; else the newest published), decide
 // the refresh (n - l >= C), log it; then copy it into the working buffers
 void launch_async_pick(AsyncDev* d, long long forced, long long C, long long f, cudaStream_t st);
 void launch_async_copy(const AsyncDev* d, const AsyncCopy& c, cudaStream_t st);
-// comm stream, after round k's theta is in pub[(k+1) % 3]: staleness of the round's steps, then publish k + 1
-void launch_async_publish(AsyncDev* d, long long k, int n_push, int n_fetch, unsigned delay_ns, cudaStream_t st);
+// comm stream, after round k = n0 / npr's theta is in pub[(k+1) % 3]: staleness of the round's steps (n0 minus
+// the generation each used), then publish generation n0 + npr
+void launch_async_publish(AsyncDev* d, long long n0, long long npr, int n_push, int n_fetch, unsigned delay_ns,
+                          cudaStream_t st);
+// A33 over NCCL (DQN_ASYNC*): theta, r of the owned shard updated by the inbox's world gradients in rank order
+void launch_rmsprop_per_gradient(float* theta, float* r, const float* inbox, int world, long long shard, float n_push,
+                                 float lr, float rho, float omr, float eps, DevCounters* ctr, cudaStream_t st);
 
 // a13 over NCCL on the bf16 path: the per-rank record of one all-gather (kernels_comm.cu)
 struct FetchRecord {

@@ -46,7 +46,7 @@ struct dqn_ctx {
   float* g_shard = nullptr;       // [shard] reduce-scatter output (world > 1)
   float* theta_local = nullptr;   // [P_pad] fetched theta (may alias theta_master)
   float* theta_hat = nullptr;     // [P_pad] target theta^
-  float* grad_snap = nullptr;     // [P_pad] optional copy of the last step's gradient (DQN_KEEP_GRAD)
+  float* grad_snap = nullptr;     // [P_pad] optional copy of the last pushed gradient (cfg.keep_grad)
   float* gather_tmp = nullptr;    // [P_pad] for get_params(SERVER/RMS) with world > 1
   // activations: conv layer c -> act_conv[c][g] [b][N*Ho*Wo]; hidden fc l -> act_fc[l][g] [b][H]
   float* act_conv[kMaxConv][2] = {};
@@ -104,6 +104,8 @@ struct dqn_ctx {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_grad = nullptr, ev_pub[3] = {}, ev_send[2] = {};
   float* g_send[2] = {};                          // [P_pad] gradient handed to round k, by k % 2
+  float* inbox = nullptr;                         // [world][shard] DQN_ASYNC* + per-gradient rule: every worker's
+                                                  // slice of this rank's shard, applied one by one (A33)
   float* theta_pub[3] = {};                       // [P_pad] published server theta, by generation % 3
   __nv_bfloat16* theta_pub_bf16[3] = {};
   AsyncDev* adev = nullptr;                       // device generation flag, fetch log, staleness histogram
@@ -345,9 +347,6 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
   if (c->replay_prio_alpha != 0.0 && c->replay_capacity > (1LL << 30)) {
     *why = "prioritized replay: capacity <= 2^30"; return DQN_EINVAL;
   }
-  if (c->server_rule == DQN_SERVER_PER_GRADIENT && c->sync_mode != DQN_DETERMINISTIC) {
-    *why = "DQN_SERVER_PER_GRADIENT needs DQN_DETERMINISTIC"; return DQN_EINVAL;
-  }
   if (!(c->rms_decay >= 0.0 && c->rms_decay < 1.0) || !(c->rms_eps >= 0.0) || !(c->lr >= 0.0) ||
       !std::isfinite(c->gamma) || !(c->err_clip >= 0.0)) {
     *why = "invalid hyper-parameter"; return DQN_EINVAL;
@@ -429,7 +428,7 @@ static void free_all(dqn_ctx* c) {
                   c->diag_idx, c->diag_amax, c->head_dq, c->head_act, c->head_loss, c->q_stage, c->q_out, c->q_amax, c->d_stage,
                   c->theta_local_bf16, c->theta_hat_bf16, c->a2_bf16, c->a1_save,
                   c->dh_bf16, c->dz2_bf16, c->fc_partial, c->tc_counters, c->bwd_partial, c->q_stage_s2d,
-                  c->store_ctl, c->ptree.node, c->prio_maxp, c->head_delta, c->diag_delta, c->dx_canon};
+                  c->store_ctl, c->ptree.node, c->prio_maxp, c->head_delta, c->diag_delta, c->dx_canon, c->inbox};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& G : c->gl) {
@@ -608,7 +607,9 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
   if ((e && atoi(e) == 0) || !init_tma_kernel_attrs()) return;
   const FcShape& F = ctx->net.fc[0];
   const int b = ctx->cfg.minibatch, D = F.D, H = F.H;
-  const int sp = ctx->fc_splits, kper = (((D + 63) / 64 + sp - 1) / sp) * 64;
+  const char* es = getenv("DQN_TG_FWD_SPLITS");  // probe knob (<= fc_splits: the partial buffer's size)
+  const int sp = es ? std::max(1, std::min(ctx->fc_splits, atoi(es))) : ctx->fc_splits;
+  const int kper = (((D + 63) / 64 + sp - 1) / sp) * 64;
   if ((sp - 1) * kper >= D) return;  // an empty split
   const __nv_bfloat16* W[2] = {ctx->theta_local_bf16 + F.w_off, ctx->theta_hat_bf16 + F.w_off};
   const dqn_ctx::GLayer& GL = ctx->gl[ctx->net.n_conv - 1];
@@ -1049,6 +1050,9 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
       if ((rc = dalloc(ctx, &ctx->g_send[i], ctx->P_pad))) return rc;
       CK(cudaEventRecord(ctx->ev_send[i], ctx->stream));
     }
+    if (cfg->server_rule == DQN_SERVER_PER_GRADIENT && world > 1 &&
+        (rc = dalloc(ctx, &ctx->inbox, (long long)world * ctx->shard)))
+      return rc;
     if ((rc = dalloc(ctx, &ctx->adev, 1))) return rc;
     CK(cudaMemsetAsync(ctx->adev, 0, sizeof(AsyncDev), ctx->stream));
     CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_adev), sizeof(AsyncDev), cudaHostAllocDefault));
@@ -1076,8 +1080,9 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     NK(ncclCommInitRank(&ctx->comm, world, id, rank));
     const char* fe = getenv("DQN_FUSED_COMM");
     ctx->fused_comm = !ctx->async && cfg->n_fetch == 1 && world <= kMaxWorld && !(fe && atoi(fe) == 0);
-    if (cfg->server_rule == DQN_SERVER_PER_GRADIENT && !ctx->fused_comm)
-      return set_err(ctx, DQN_EINVAL, "DQN_SERVER_PER_GRADIENT with N > 1 needs the fused server round (n_fetch = 1)");
+    if (cfg->server_rule == DQN_SERVER_PER_GRADIENT && !ctx->fused_comm && !ctx->async)
+      return set_err(ctx, DQN_EINVAL, "DQN_SERVER_PER_GRADIENT with N > 1: the fused server round (deterministic, "
+                                      "n_fetch = 1) or DQN_ASYNC*");
     if (ctx->fused_comm && (rc = setup_fused_comm(ctx))) return rc;
     if (ctx->bf16 && !ctx->fused_comm) {
       FetchRecord& f = ctx->frec;
@@ -1559,7 +1564,8 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   h.idx = ctx->idx; h.ring_a = ctx->ring_a; h.ring_r = ctx->ring_r; h.ring_term = ctx->ring_t;
   h.gamma = (float)c.gamma; h.clip = (float)c.err_clip;
   h.grad = ctx->grad; h.dH = ctx->dz_fc[0]; h.dH_bf16 = ctx->dh_bf16;
-  h.fc_partial = ctx->fc_partial; h.fc_splits = gf.splits; h.fc_split_stride = (long long)gf.N * gf.M;
+  h.fc_partial = ctx->fc_partial; h.fc_split_stride = (long long)gf.N * gf.M;
+  h.fc_splits = ctx->use_tgemm ? ctx->tg_fwd.splits : gf.splits;
   h.fc_bias[0] = ctx->theta_local + F.b_off; h.fc_bias[1] = ctx->theta_hat + F.b_off;
   h.act_out[0] = ctx->act_fc[0][0]; h.act_out[1] = ctx->act_fc[0][1];
   h.st_id = ST_HEAD;
@@ -1767,7 +1773,8 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   h.idx = ctx->idx; h.ring_a = ctx->ring_a; h.ring_r = ctx->ring_r; h.ring_term = ctx->ring_t;
   h.gamma = (float)c.gamma; h.clip = (float)c.err_clip;
   h.grad = ctx->grad; h.dH = ctx->dz_fc[0]; h.dH_bf16 = ctx->dh_bf16;
-  h.fc_partial = ctx->fc_partial; h.fc_splits = gf.splits; h.fc_split_stride = (long long)gf.N * gf.M;
+  h.fc_partial = ctx->fc_partial; h.fc_split_stride = (long long)gf.N * gf.M;
+  h.fc_splits = ctx->use_tgemm ? ctx->tg_fwd.splits : gf.splits;
   h.fc_bias[0] = ctx->theta_local + F.b_off; h.fc_bias[1] = ctx->theta_hat + F.b_off;
   h.act_out[0] = ctx->act_fc[0][0]; h.act_out[1] = ctx->act_fc[0][1];
   h.ctr = ctx->ctr; h.diag_loss = ctx->diag_loss; h.diag_idx = ctx->diag_idx; h.diag_amax = ctx->diag_amax;
@@ -1967,9 +1974,10 @@ static void schedule(dqn_ctx* ctx, bool* fetch, bool* refresh, bool* push) {
 // takes the newest published generation without waiting; the lag-1 twin waits for generation n - 1
 static int async_fetch(dqn_ctx* ctx) {
   long long forced = -1;
-  if (ctx->async_lag1) {
-    forced = std::max(ctx->n - 1, 0LL);
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_pub[forced % 3], 0));
+  const long long npr = ctx->n_per_round;  // generations per round: 1, or N with the per-gradient rule
+  if (ctx->async_lag1) {  // the previous round's result
+    forced = std::max(ctx->n - npr, 0LL);
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_pub[(forced / npr) % 3], 0));
   }
   launch_async_pick(ctx->adev, forced, ctx->cfg.target_sync, ctx->n_fetches, ctx->stream);
   AsyncCopy cp{};
@@ -1980,19 +1988,23 @@ static int async_fetch(dqn_ctx* ctx) {
   cp.th = ctx->theta_local; cp.thb = ctx->theta_local_bf16;
   cp.hat = ctx->theta_hat; cp.hatb = ctx->theta_hat_bf16;
   cp.n32 = ctx->P_pad; cp.n16 = ctx->bf16 ? ctx->P_bf16 : 0;
+  cp.npr = npr;
   launch_async_copy(ctx->adev, cp, ctx->stream);
   ctx->n_fetches += 1;
   CK(cudaGetLastError());
   return DQN_OK;
 }
 
-// asynchronous push of round k = n: hand the accumulated gradient to the comm stream, which runs the whole
-// server round (reduce-scatter, RMSProp on the owned shard, all-gather into theta_pub[(k + 1) % 3], publish)
-// while the replica keeps stepping. All NCCL traffic of this mode lives on the comm stream, in rank order.
+// asynchronous push of round k (server generation n = k * npr before it): hand the accumulated gradient to the
+// comm stream, which runs the whole server round (reduce-scatter, RMSProp on the owned shard, all-gather into
+// theta_pub[(k + 1) % 3], publish generation n + npr) while the replica keeps stepping. With the per-gradient
+// rule (A33) the reduce-scatter becomes an all-to-all into the owner's inbox and the owner applies the N
+// workers' gradients one by one in rank order (npr = N generations per round). All NCCL traffic of this mode
+// lives on the comm stream, in rank order.
 static int async_push(dqn_ctx* ctx) {
   const dqn_config& c = ctx->cfg;
   cudaStream_t cs = ctx->comm_stream;
-  const long long k = ctx->n;
+  const long long n0 = ctx->n, k = n0 / ctx->n_per_round;
   float* gs = ctx->g_send[k % 2];
   // g_send[k % 2] is read by round k - 2 until that round ends (so the comm stream lags by two rounds at most)
   CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_send[k % 2], 0));
@@ -2006,9 +2018,20 @@ static int async_push(dqn_ctx* ctx) {
   const float rho = (float)c.rms_decay, omr = (float)(1.0 - c.rms_decay);
   const int s = (int)((k + 1) % 3);
   if (ctx->world > 1) {
-    NK(ncclReduceScatter(gs, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, cs));
-    launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
-                   (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, cs);
+    if (ctx->inbox) {  // A33: worker p's slice of every owner's shard to that owner, applied in rank order
+      NK(ncclGroupStart());
+      for (int p = 0; p < ctx->world; ++p) {
+        NK(ncclSend(gs + (long long)p * ctx->shard, (size_t)ctx->shard, ncclFloat, p, ctx->comm, cs));
+        NK(ncclRecv(ctx->inbox + (long long)p * ctx->shard, (size_t)ctx->shard, ncclFloat, p, ctx->comm, cs));
+      }
+      NK(ncclGroupEnd());
+      launch_rmsprop_per_gradient(ctx->theta_master, ctx->rms, ctx->inbox, ctx->world, ctx->shard, (float)c.n_push,
+                                  (float)c.lr, rho, omr, (float)c.rms_eps, ctx->ctr, cs);
+    } else {
+      NK(ncclReduceScatter(gs, ctx->g_shard, (size_t)ctx->shard, ncclFloat, ncclSum, ctx->comm, cs));
+      launch_rmsprop(ctx->theta_master, ctx->rms, ctx->g_shard, ctx->shard, div, (float)c.lr, rho, omr,
+                     (float)c.rms_eps, nullptr, nullptr, ctx->ctr, 0, cs);
+    }
     if (ctx->fetch_bf16) {  // a13 in bf16 (+ the fp32 entries outside the FC weight)
       int rc = enqueue_fetch_bf16(ctx, cs, ctx->theta_pub[s], ctx->theta_pub_bf16[s]);
       if (rc) return rc;
@@ -2022,7 +2045,7 @@ static int async_push(dqn_ctx* ctx) {
   if (ctx->bf16 && !ctx->fetch_bf16)
     launch_f32_to_bf16(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->P_pad, cs, ctx->img_off, ctx->w1_off, ctx->w2_off);
   if (ctx->gpath) launch_gpack(ctx->theta_pub[s], ctx->theta_pub_bf16[s], ctx->gpack_off, ctx->pack_map, ctx->pack_n, cs);
-  launch_async_publish(ctx->adev, k, c.n_push, c.n_fetch, ctx->async_delay_ns, cs);
+  launch_async_publish(ctx->adev, n0, ctx->n_per_round, c.n_push, c.n_fetch, ctx->async_delay_ns, cs);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_pub[s], cs));
   CK(cudaEventRecord(ctx->ev_send[k % 2], cs));

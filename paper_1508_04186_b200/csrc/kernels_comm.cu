@@ -280,7 +280,7 @@ __global__ void async_pick_kernel(AsyncDev* d, long long forced, long long C, lo
 
 __global__ void async_copy_kernel(const AsyncDev* d, AsyncCopy c) {
   const long long m = *(volatile const long long*)&d->fetch_gen;
-  const int slot = (int)(m % 3), refresh = *(volatile const int*)&d->do_refresh;
+  const int slot = (int)((m / c.npr) % 3), refresh = *(volatile const int*)&d->do_refresh;
   const float4* s4 = reinterpret_cast<const float4*>(c.pub[slot]);
   const long long stride = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (long long i = t0; i < c.n32 / 4; i += stride) {
@@ -302,7 +302,9 @@ __global__ void async_copy_kernel(const AsyncDev* d, AsyncCopy c) {
   }
 }
 
-__global__ void async_publish_kernel(AsyncDev* d, long long k, int n_push, int n_fetch, unsigned delay_ns) {
+__global__ void async_publish_kernel(AsyncDev* d, long long n0, long long npr, int n_push, int n_fetch,
+                                     unsigned delay_ns) {
+  const long long k = n0 / npr;  // the round
   if (threadIdx.x == 0) {
     if (delay_ns) {  // DQN_ASYNC_DELAY_US (diagnostic): a slow server, so that fetches see stale generations
       const unsigned long long t0 = gtimer();
@@ -312,11 +314,11 @@ __global__ void async_publish_kernel(AsyncDev* d, long long k, int n_push, int n
     // A25: every replica step t of round k used the generation of its last fetch f = t / n_fetch
     for (long long t = k * n_push; t < (k + 1) * n_push; ++t) {
       const long long base = d->fgen_log[(t / n_fetch) % kDiagSteps];
-      const long long st = k - base;
+      const long long st = n0 - base;
       d->hist[st < 31 ? (st < 0 ? 0 : st) : 31] += 1;
     }
-    // theta_pub[(k + 1) % 3] was written by this stream's earlier kernels: release generation k + 1
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&d->pub_gen), "l"((unsigned long long)(k + 1)) : "memory");
+    // theta_pub[(k + 1) % 3] was written by this stream's earlier kernels: release generation n0 + npr
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&d->pub_gen), "l"((unsigned long long)(n0 + npr)) : "memory");
   }
 }
 
@@ -327,8 +329,48 @@ void launch_async_copy(const AsyncDev* d, const AsyncCopy& c, cudaStream_t st) {
   const long long n = std::max(c.n32 / 4, c.n16 / 8);
   async_copy_kernel<<<(int)std::min<long long>((n + 255) / 256, 148 * 4), 256, 0, st>>>(d, c);
 }
-void launch_async_publish(AsyncDev* d, long long k, int n_push, int n_fetch, unsigned delay_ns, cudaStream_t st) {
-  async_publish_kernel<<<1, 32, 0, st>>>(d, k, n_push, n_fetch, delay_ns);
+void launch_async_publish(AsyncDev* d, long long n0, long long npr, int n_push, int n_fetch, unsigned delay_ns,
+                          cudaStream_t st) {
+  async_publish_kernel<<<1, 32, 0, st>>>(d, n0, npr, n_push, n_fetch, delay_ns);
+}
+
+// A33 in the asynchronous mode: worker p's gradient slice (the mean of its n_push accumulated gradients, A8) is
+// applied to the owned shard as its own RMSProp step, p = 0 .. N-1 in rank order (Alg. 2); the same
+// per-element arithmetic as rmsprop_kernel and the fused round's per-gradient branch (A4, A5, A24)
+__global__ void rmsprop_per_gradient_kernel(float* __restrict__ theta, float* __restrict__ r,
+                                            const float* __restrict__ inbox, int world, long long shard, float inv_np,
+                                            float lr, float rho, float omr, float eps, DevCounters* ctr) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= shard / 4) return;
+  float4 t4 = reinterpret_cast<const float4*>(theta)[i];
+  float4 r4 = reinterpret_cast<const float4*>(r)[i];
+  float tv[4] = {t4.x, t4.y, t4.z, t4.w}, rv[4] = {r4.x, r4.y, r4.z, r4.w};
+  unsigned bad = 0;
+  for (int p = 0; p < world; ++p) {
+    const float4 g4 = __ldcg(reinterpret_cast<const float4*>(inbox + (long long)p * shard) + i);
+    const float gp[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float gb = gp[q] * inv_np;
+      if (isfinite(gb)) {
+        const float rr = rho * rv[q] + omr * gb * gb;
+        rv[q] = rr;
+        tv[q] = tv[q] - lr * gb * rsqrtf(rr + eps);
+      } else {
+        ++bad;
+      }
+    }
+  }
+  reinterpret_cast<float4*>(theta)[i] = make_float4(tv[0], tv[1], tv[2], tv[3]);
+  reinterpret_cast<float4*>(r)[i] = make_float4(rv[0], rv[1], rv[2], rv[3]);
+  if (bad) atomicAdd(&ctr->nonfinite, bad);
+}
+
+void launch_rmsprop_per_gradient(float* theta, float* r, const float* inbox, int world, long long shard, float n_push,
+                                 float lr, float rho, float omr, float eps, DevCounters* ctr, cudaStream_t st) {
+  const long long n4 = shard / 4;
+  rmsprop_per_gradient_kernel<<<(unsigned)std::max<long long>(1, (n4 + 255) / 256), 256, 0, st>>>(
+      theta, r, inbox, world, shard, 1.0f / n_push, lr, rho, omr, eps, ctr);
 }
 
 DQN_STEP_TRACE_HOST(comm)

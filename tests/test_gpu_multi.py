@@ -131,6 +131,30 @@ def test_two_replicas_async_free_running_equals_realised_schedule(tmp_path):
     assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 1e-5
 
 
+@pytest.mark.parametrize("mode", ["--async-free", "--async-mode"])
+def test_two_replicas_async_per_gradient_rule(tmp_path, mode):
+    """NEXT-2 in the asynchronous modes (A33 + A40): the round's reduce-scatter becomes an all-to-all into each
+    owner's inbox and the owner applies worker 0's gradient, then worker 1's (n += 2 per round), while the
+    replicas keep stepping; the oracle (server_rule = 1) replays the realised schedule (free-running) or the
+    lag-one-round twin. Staleness counts generations: multiples of N here."""
+    if n_gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    env = {"DQN_ASYNC_DELAY_US": "200"} if mode == "--async-free" else None
+    res = run_ranks(2, tmp_path, "--tiny", "--n-push", "2", "--n-fetch", "1", "--target-sync", "3", "--steps", "10",
+                    mode, "--server-rule", "1", env=env)
+    dc, on, oc = nets(minibatch=16, replay_capacity=200, n_push=2, n_fetch=1, target_sync=3, lr=1e-3, **TINY_KW)
+    oc.n_replicas = 2
+    oc.server_rule = 1
+    oc.fetch_gen = res["step_generation"]  # n_fetch = 1: one fetch per step
+    assert np.all(res["step_generation"] % 2 == 0)  # only whole rounds are published
+    reps = [replay(on, 250, 100 + k)[0] for k in range(2)]
+    th0 = he_theta(on, 3).astype(np.float64)
+    ref = O.run(on, oc, 200, reps, th0, 10)
+    assert ref["rc"] == 0 and int(res["n"]) == ref["n"] == 10
+    assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
+    assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 1e-5
+
+
 @pytest.mark.parametrize("world", [4, 8])
 def test_many_replicas_fp32_match_oracle(tmp_path, world):
     """N = 4 / 8 (skipped on smaller boxes): the fused server round (NEXT-1) with every rank owning

@@ -265,6 +265,24 @@ def test_realised_async_schedule_equals_serial_loop(N, n_push, n_fetch):
         assert np.array_equal(O.run(TINY, c1, CAP, reps, th0, steps)["theta"], O.run(TINY, c2, CAP, reps, th0, steps)["theta"])
 
 
+@pytest.mark.parametrize("N,n_push", [(2, 2), (3, 1)])
+def test_realised_async_schedule_per_gradient_rule_equals_serial_loop(N, n_push):
+    """A33 + A40 (the asynchronous per-gradient mode): rounds publish only whole rounds (generations k N), every
+    fetch takes one of the last three published; or_run equals the written-out loop."""
+    steps = 8
+    rng = np.random.default_rng(N * 10 + n_push)
+    rounds_at = [T // n_push for T in range(steps)]      # rounds completed when fetch T happens (n_fetch = 1)
+    fg = np.array([[max(r - int(rng.integers(0, 3)), 0) * N for r in rounds_at] for _ in range(N)], np.int64)
+    reps = make_replays(N, 60, 9)
+    th0 = he_theta(TINY, 5)
+    cfg = O.TrainCfg(n_replicas=N, minibatch=4, n_push=n_push, n_fetch=1, target_sync=3, lr=3e-3, gamma=0.9,
+                     fetch_gen=fg, server_rule=1)
+    ref = serial_reference(cfg, reps, th0, steps, CAP)
+    out = O.run(TINY, cfg, CAP, reps, th0, steps)
+    assert out["rc"] == 0 and out["n"] == (steps // n_push) * N
+    assert np.allclose(out["theta"], ref[0], rtol=0, atol=1e-12)
+
+
 def test_realised_schedule_rejects_an_unpublished_generation():
     reps = make_replays(1, 30, 3)
     fg = np.array([[0, 5, 1]], np.int64)   # generation 5 does not exist at step 1
