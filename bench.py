@@ -121,15 +121,20 @@ def conv_param_count(net=MNIH) -> int:
 
 
 def region_traffic(name: str, dtype: str, net=MNIH):
-    """DRAM bytes (read + write) per launch of a region's kernels, from the committed `ncu --set full`
-    capture of this round (profiles/r1_traffic.json), or None when not captured."""
-    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if dtype != "bf16" or net != MNIH or not os.path.exists(p) or name not in REGION_KERNELS:  # Mnih kernels only
+    """DRAM bytes (read + write) of one step's launches of a region's kernels, from the committed `ncu --set
+    full` captures of this round (profiles/r2_traffic.json, tools/traffic_json.py): per kernel on the Mnih
+    path, per region on the generic path (the scaled net); None when not captured."""
+    p = os.path.join(ROOT, "profiles", "r2_traffic.json")
+    if dtype != "bf16" or not os.path.exists(p):
         return None
     with open(p) as f:
         t = json.load(f)
-    ks = [k for k in REGION_KERNELS[name] if k in t]  # the kernels of the region that ran in the capture
-    return sum((t[k]["dram_read_MB"] + t[k]["dram_write_MB"]) * 1e6 for k in ks) if ks else None
+    if net == MNIH and name in REGION_KERNELS:
+        ks = [k for k in REGION_KERNELS[name] if k in t["mnih"]]  # the kernels of the region that ran in the capture
+        return sum((t["mnih"][k]["dram_read_MB"] + t["mnih"][k]["dram_write_MB"]) * 1e6 for k in ks) if ks else None
+    if net == SCALED and name in t["scaled"]["regions"]:
+        return t["scaled"]["regions"][name]["bytes"]
+    return None
 
 
 def roofline(regions, b, net, world, dtype, profile_steps):
