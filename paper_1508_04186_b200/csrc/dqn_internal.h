@@ -373,8 +373,9 @@ struct GConvWgradArgs {
   long long slot_stride;
   const __nv_bfloat16* dz;         // [b][Ho][Wo][N]
   int b, Hs, Ws, Cs, Th, Tw, Ho, Wo, N, ipc;  // ipc: images per CTA (K range)
-  float* partial;                  // [ranges][Th*Tw*Cs][N]
+  float* partial;                  // [ranges][Th*Tw*Cs][N], or [ranges][N][Th*Tw*Cs] with part_cm
   float* partial_db;               // [ranges][N]
+  int part_cm;                     // 1: partials column-major per range (twgrad_kernel's coalesced epilogue)
   const int* w_canon;              // per dW row (tap, c'): canonical offset at n = 0 (-1: none)
   long long w_off, w_nstride, b_off;
   float* grad;

@@ -697,7 +697,7 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
     GConvWgradArgs& r = ctx->tc_wred[i];
     r.Th = G.Th; r.Tw = G.Tw; r.Cs = G.Cs; r.N = L.N; r.b = w.ranges; r.ipc = 1; r.first = i == 0;
     r.w_canon = G.w_canon; r.w_off = L.w_off; r.w_nstride = (long long)L.C * L.k * L.k; r.b_off = L.b_off;
-    r.grad = ctx->grad; r.store = ctx->cfg.n_push == 1;
+    r.grad = ctx->grad; r.store = ctx->cfg.n_push == 1; r.part_cm = 1;
     // data gradient (layers after the first): A = this layer's dZ, B = the packed data-gradient weights
     if (i > 0) {
       TConvArgs& d = ctx->tc_dgrad[i];

@@ -585,6 +585,7 @@ __global__ void __launch_bounds__(256) gconv_wreduce_kernel(GConvWgradArgs a) {
   const int nr = (a.b + a.ipc - 1) / a.ipc, per = (nr + 7) / 8;
   const int q0 = grp * per, q1 = min(nr, q0 + per);
   float s = 0.0f;
+  // part_cm: e enumerates (n, row) with the row fastest, the column-major partials' order (coalesced reads)
   if (e < total) {
     if (e < nw)
       for (int q = q0; q < q1; ++q) s += a.partial[(long long)q * nw + e];
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(256) gconv_wreduce_kernel(GConvWgradArgs a) {
   for (int g = 0; g < 8; ++g) t += red[g][el];
   long long dst;
   if (e < nw) {
-    const int row = (int)(e / a.N), n = (int)(e % a.N);
+    const int row = a.part_cm ? (int)(e % MK) : (int)(e / a.N), n = a.part_cm ? (int)(e / MK) : (int)(e % a.N);
     if (a.first) t *= 1.0f / 255.0f;
     if (a.w_canon[row] < 0) return;
     dst = a.w_off + (long long)n * a.w_nstride + a.w_canon[row];

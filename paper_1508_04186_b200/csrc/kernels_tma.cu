@@ -639,8 +639,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) twgrad_kernel(const __grid_cons
         for (int c = half * 32; c < half * 32 + 32; c += 16) {
           float v[16];
           tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(mt * 64 + c), v);
-          if ((m < a.TCs || m == a.TCs) && c < a.Nout) {
-            float* p = m < a.TCs ? a.partial + ((long long)r * a.TCs + m) * a.Nout + c : a.partial_db + (long long)r * a.Nout + c;
+          if (c >= a.Nout) continue;
+          if (m < a.TCs) {  // column-major [r][n][m]: a warp's 32 rows are 128 contiguous bytes per column
+            float* p = a.partial + ((long long)r * a.Nout + c) * a.TCs + m;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) p[(long long)i * a.TCs] = v[i];
+          } else if (m == a.TCs) {  // the all-ones row: db
+            float* p = a.partial_db + (long long)r * a.Nout + c;
 #pragma unroll
             for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
           }
