@@ -429,6 +429,27 @@ constexpr int TC_EPI_CONV_FWD = 3;
 //                 operands, two 64-row (t, c-block) halves per M tile, plus one all-ones half giving db);
 //                 per-range partials, reduced in range order by gconv_wreduce (deterministic)
 enum { TCONV_FWD = 0, TCONV_DGRAD = 1, TCONV_WGRAD = 2 };
+// n / d for a divisor fixed at launch (the epilogues' row -> (image, y, x) decompositions): one multiply-high,
+// an add and a shift instead of a ~20-instruction integer division (Granlund-Montgomery; exact for all 32-bit n)
+struct FastDiv {
+  uint32_t d, m, s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0u, 0u};
+  if (d <= 1) return f;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.m = (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+  f.s = l - 1;
+  return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fdiv(const FastDiv& f, uint32_t n) {
+  if (f.d <= 1) return n;
+  const uint32_t t = __umulhi(n, f.m);
+  return (t + ((n - t) >> 1)) >> f.s;
+}
+#endif
 struct TConvArgs {
   CUtensorMap ta[2];               // the A source rows per group: box {64, R}
   CUtensorMap tb[2];               // FWD / DGRAD: packed weights [BN][T*64*Cblk] (box {64, BN}); WGRAD: dZ rows (box {64, 64})
@@ -453,6 +474,7 @@ struct TConvArgs {
   float* partial;                  // [ranges][TCs][Nout]
   float* partial_db;               // [ranges][Nout]
   int dbg;                         // probe only (tools/probe_tconv): 1 skip epilogue stores, 2 skip MMAs
+  FastDiv fd_hsws, fd_ws, fd_sn, fd_cp, fd_s;  // set by launch_tconv from HsWs, Ws, s_next, Cp, s
 };
 bool init_tconv_kernel_attrs();
 size_t tconv_smem(const TConvArgs& a);  // 0: does not fit

@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kTgMaxStages], empty[kTgMaxStages], bfull, tfull[kMaxAcc], tempty[kMaxAcc];
   __shared__ uint32_t tbase;
+  __shared__ __align__(16) float smem_bias[256];  // FWD: the layer's bias (BN <= 256)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = a.stages, BN = a.BN, SB = tconv_stage_bytes(a);
   uint8_t* fixed = smem;  // the resident B operand, then the ring
@@ -465,6 +466,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
     }
   } else if (!(a.dbg & 128)) {  // ---- epilogue: thread = one row (TMEM lane) of the tile, half of its columns
     const int q = warp & 3, half = (warp - 1 - TC_NMMA) >> 2, c_lo = half * (BN / 2), c_hi = c_lo + BN / 2;
+    // per-thread constants of the epilogue: the next grid's shape (FWD) and the bias in shared memory (the
+    // per-element address math and the bias loads were ~30 % of the forward's stall samples)
+    const int Nn = a.N, HoWo = a.Ho * a.Wo;
+    const int sn = a.s_next > 0 ? a.s_next : 1, Hn = a.Ho / sn, Wn = a.Wo / sn, Cn = Nn * sn * sn;
+    const float* s_bias = smem_bias;
+    if (a.mode == TCONV_FWD) {  // the 8 epilogue warps stage the bias (after the PDL wait: the update wrote it)
+      for (int e = tid - 32 * (1 + TC_NMMA); e < BN; e += 256) smem_bias[e] = __ldg(a.bias[g] + e);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
     int tl_local = 0;
     for (int tl = cta; tl < tiles; tl += ctas, ++tl_local) {
       const int buf = tl_local % NB;
@@ -472,6 +482,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
       tc_fence_after();
       const int mt = tl;
       const int m = mt * 128 + 32 * q + lane;
+      // row m -> (image, y, x) of the grid, once per tile
+      const int img = (int)fdiv(a.fd_hsws, (uint32_t)m), pq = m - img * a.HsWs;
+      const int yy = (int)fdiv(a.fd_ws, (uint32_t)pq), xx = pq - yy * a.Ws;
       const uint32_t trow = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
       for (int c = c_lo; c < c_hi; c += 16) {
         float v[16];
@@ -480,25 +493,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
         if (a.dbg & 1) continue;
         if (a.mode == TCONV_FWD) {
           if (m >= a.M) continue;
-          const int img = m / a.HsWs, pq = m - img * a.HsWs, oy = pq / a.Ws, ox = pq - oy * a.Ws;
+          const int oy = yy, ox = xx;
           if (oy >= a.Ho || ox >= a.Wo) continue;
-          const float* bias = a.bias[g];
+          float bz[16];
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(s_bias + c + i);
+            bz[i] = b4.x; bz[i + 1] = b4.y; bz[i + 2] = b4.z; bz[i + 3] = b4.w;
+          }
           uint32_t o[8];
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(fmaxf(fmaf(v[i], a.scale, __ldg(bias + c + i)), 0.0f),
-                                                            fmaxf(fmaf(v[i + 1], a.scale, __ldg(bias + c + i + 1)), 0.0f));
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(fmaxf(fmaf(v[i], a.scale, bz[i]), 0.0f),
+                                                            fmaxf(fmaf(v[i + 1], a.scale, bz[i + 1]), 0.0f));
             o[i >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
           }
-          const int Nn = a.N, HoWo = a.Ho * a.Wo;
           if (a.s_next == 0) {  // canonical (C,H,W) flatten: out[img][n*HoWo + p]
             __nv_bfloat16* dst = a.cout[g] + (long long)img * Nn * HoWo + (long long)oy * a.Wo + ox;
             const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(o);
 #pragma unroll
             for (int i = 0; i < 16; ++i) dst[(long long)(c + i) * HoWo] = hv[i];
           } else {  // next grid (s2d by s_next): pixel (oy/s, ox/s), channel (iy*s + ix)*N + n
-            const int sn = a.s_next, Hn = a.Ho / sn, Wn = a.Wo / sn, Cn = Nn * sn * sn;
-            const int py = oy / sn, px = ox / sn, qq = (oy % sn) * sn + (ox % sn);
+            const int py = (int)fdiv(a.fd_sn, (uint32_t)oy), px = (int)fdiv(a.fd_sn, (uint32_t)ox);
+            const int qq = (oy - py * sn) * sn + (ox - px * sn);
             if (py < Hn && px < Wn) {
               uint4* dst = reinterpret_cast<uint4*>(a.cout[g] + (((long long)img * Hn + py) * Wn + px) * Cn + qq * Nn + c);
               dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
@@ -507,7 +524,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
           }
         } else if (a.mode == TCONV_DGRAD) {  // x [X > 0], inverse space-to-depth into the previous dZ
           if (m >= a.M) continue;
-          const int img = m / a.HsWs, pq = m - img * a.HsWs, py = pq / a.Ws, px = pq - py * a.Ws;
+          const int py = yy, px = xx;
           const uint4* xm = reinterpret_cast<const uint4*>(a.xmask + (long long)m * a.Cs + c);
           const uint4 mk0 = __ldg(xm), mk1 = __ldg(xm + 1);
           const uint32_t mw[8] = {mk0.x, mk0.y, mk0.z, mk0.w, mk1.x, mk1.y, mk1.z, mk1.w};
@@ -518,7 +535,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tconv_kernel(const __grid_const
                                                             bf16_gt0(mw[h] >> 16) ? v[2 * h + 1] : 0.0f);
             o[h] = *reinterpret_cast<const uint32_t*>(&h2);
           }
-          const int qq = c / a.Cp, cc = c - qq * a.Cp, iy = qq / a.s, ix = qq - iy * a.s;
+          const int qq = (int)fdiv(a.fd_cp, (uint32_t)c), cc = c - qq * a.Cp;
+          const int iy = (int)fdiv(a.fd_s, (uint32_t)qq), ix = qq - iy * a.s;
           const long long row = (long long)img * a.prevHsWs + (long long)(py * a.s + iy) * a.prevWs + (px * a.s + ix);
           uint4* dst = reinterpret_cast<uint4*>(a.dzprev + row * a.Cp + cc);
           dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
@@ -693,6 +711,11 @@ void launch_tconv(const TConvArgs& a0, int num_sms, cudaStream_t st) {
   }
   const int fixed = tconv_fixed_bytes(a), sb = tconv_stage_bytes(a);
   a.stages = std::min(kTgMaxStages, (219 * 1024 - 1024 - fixed) / sb);
+  a.fd_hsws = make_fastdiv((uint32_t)a.HsWs);
+  a.fd_ws = make_fastdiv((uint32_t)a.Ws);
+  a.fd_sn = make_fastdiv((uint32_t)(a.s_next > 0 ? a.s_next : 1));
+  a.fd_cp = make_fastdiv((uint32_t)(a.Cp > 0 ? a.Cp : 1));
+  a.fd_s = make_fastdiv((uint32_t)(a.s > 0 ? a.s : 1));
   const int m_tiles = (a.M + 127) / 128;
   const long long tiles = (long long)m_tiles * a.groups;
   int grid = (int)std::min<long long>(tiles, num_sms);
