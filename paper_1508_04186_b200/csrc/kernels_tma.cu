@@ -613,6 +613,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) twgrad_kernel(const __grid_cons
     if (j < nmma) {  // ---- MMA warp j: M tiles j, j + nmma, ... of every chunk
       const uint32_t idesc = make_idesc_bf16(128, 64, 1, 1);
       const uint32_t ring_u = smem_u32(ring), ones_u = smem_u32(ones);
+      // this warp's (at most 2: M <= 8 tiles, nmma = min(tiles, 4)) M tiles: the stage offsets of their two
+      // 64-row halves, a (t, cb) window read from row shift(t), or -1 for the ones block; fixed for the kernel
+      int off[2][2], nmt = 0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int mt = j + k * nmma;
+        if (mt < m_tiles) nmt = k + 1;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int mb = 2 * mt + hh;
+          if (mt >= m_tiles || mb * 64 >= a.TCs) {
+            off[k][hh] = -1;
+            continue;
+          }
+          const int t = mb / a.Cblk, cb = mb - t * a.Cblk;
+          off[k][hh] = cb * win_bytes(a.R) + ((t / a.Tw) * a.Ws + t % a.Tw) * 128;
+        }
+      }
       int it = 0, rl = 0;
       for (int r = blockIdx.x; r < a.ranges; r += gridDim.x, ++rl) {
         mbar_spin(&tempty, (rl & 1) ^ 1);
@@ -623,22 +641,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) twgrad_kernel(const __grid_cons
           mbar_spin(&full[st], (it / S) & 1);
           const uint32_t sb = ring_u + (uint32_t)(st * SB);
           const uint32_t bt = sb + (uint32_t)(a.Cblk * win_bytes(a.R));
-          for (int mt = j; mt < m_tiles; mt += nmma) {
-            uint32_t h[2];
-            for (int hh = 0; hh < 2; ++hh) {
-              const int mb = 2 * mt + hh;
-              if (mb * 64 >= a.TCs) {
-                h[hh] = ones_u;
-              } else {
-                const int t = mb / a.Cblk, cb = mb - t * a.Cblk;
-                h[hh] = sb + (uint32_t)(cb * win_bytes(a.R) + ((t / a.Tw) * a.Ws + t % a.Tw) * 128);
-              }
-            }
-            const uint32_t lbo = h[1] > h[0] ? h[1] - h[0] : 0u;
-            const uint32_t d = tbase + (uint32_t)(mt * 64);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (k >= nmt) break;
+            const uint32_t h0 = off[k][0] < 0 ? ones_u : sb + (uint32_t)off[k][0];
+            const uint32_t h1 = off[k][1] < 0 ? ones_u : sb + (uint32_t)off[k][1];
+            const uint32_t lbo = h1 > h0 ? h1 - h0 : 0u;  // both halves the ones block: 0, never past it
+            const uint32_t d = tbase + (uint32_t)((j + k * nmma) * 64);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16_w(d, desc_sw128(h[0] + kk * 2048, lbo, 1024), desc_sw128(bt + kk * 2048, 8192, 1024), idesc,
+              mma_bf16_w(d, desc_sw128(h0 + kk * 2048, lbo, 1024), desc_sw128(bt + kk * 2048, 8192, 1024), idesc,
                          (c > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit_w(&empty[st]);

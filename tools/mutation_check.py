@@ -39,8 +39,8 @@ MUTATIONS = {
     "tgemm_fc_dX_relu_mask": ([(CSRC + "kernels_tma.cu", "__float2bfloat16_rn(bf16_gt0(mk[i]) ? v[i] : 0.0f)",
                                 "__float2bfloat16_rn(v[i])")], [G + "test_gated_one_step[scaled-b32]"]),
     "twgrad_tap_shift_dropped": ([(CSRC + "kernels_tma.cu",
-                                   "h[hh] = sb + (uint32_t)(cb * win_bytes(a.R) + ((t / a.Tw) * a.Ws + t % a.Tw) * 128);",
-                                   "h[hh] = sb + (uint32_t)(cb * win_bytes(a.R));")],
+                                   "off[k][hh] = cb * win_bytes(a.R) + ((t / a.Tw) * a.Ws + t % a.Tw) * 128;",
+                                   "off[k][hh] = cb * win_bytes(a.R);")],
                                       [G + "test_gated_one_step[scaled-b32]"]),
     "error_clip_one_sided": ([(CSRC + "kernels_head.cu", "dc = fminf(fmaxf(dc, -h.clip), h.clip);",
                                "dc = fminf(dc, h.clip);")], [G + "test_gated_error_clip[mnih]"]),
