@@ -134,10 +134,13 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
                            long long state_bytes, const uint8_t* s, const int32_t* a, const float* r,
                            const uint8_t* sn, const uint8_t* t, cudaStream_t st, long long* ring_size_out = nullptr,
                            long long ring_size = 0, long long stride = 0, int dedup = 0);
+// pack_map (generic path, N = 1): also write the updated conv parameters i < pack_n into their packed slots
+// pub_bf16[pack_off + map[i].x / .y] (what gpack_kernel does at the start of a step)
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
                     cudaStream_t st, long long img_off = -1,
-                    long long w1_off = 0, long long w2_off = 0, float* g_snap = nullptr);
+                    long long w1_off = 0, long long w2_off = 0, float* g_snap = nullptr,
+                    const int2* pack_map = nullptr, long long pack_n = 0, long long pack_off = 0);
 void launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t st, long long img_off = -1,
                         long long w1_off = 0, long long w2_off = 0);
 void launch_bf16_to_f32(const __nv_bfloat16* src, float* dst, long long n, cudaStream_t st);

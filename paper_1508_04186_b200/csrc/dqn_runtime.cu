@@ -607,8 +607,8 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
   if ((e && atoi(e) == 0) || !init_tma_kernel_attrs()) return;
   const FcShape& F = ctx->net.fc[0];
   const int b = ctx->cfg.minibatch, D = F.D, H = F.H;
-  const char* es = getenv("DQN_TG_FWD_SPLITS");  // probe knob (<= fc_splits: the partial buffer's size)
-  const int sp = es ? std::max(1, std::min(ctx->fc_splits, atoi(es))) : ctx->fc_splits;
+  // the head's split count (A/B at BJ.configs[4]: 7 splits 210.2, 4: 211.4, 2: 214.3 us/step)
+  const int sp = ctx->fc_splits;
   const int kper = (((D + 63) / 64 + sp - 1) / sp) * 64;
   if ((sp - 1) * kper >= D) return;  // an empty split
   const __nv_bfloat16* W[2] = {ctx->theta_local_bf16 + F.w_off, ctx->theta_hat_bf16 + F.w_off};
@@ -1707,9 +1707,14 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     }
   }
   // packed conv weights of the working theta (changed by every update)
-  PB("gpack", 1);
-  launch_gpack(ctx->theta_local, ctx->theta_local_bf16, ctx->gpack_off, ctx->pack_map, ctx->pack_n, st);
-  PE();
+  // N = 1 (deterministic): the update of the previous step wrote the packed images with theta (rmsprop pack_map);
+  // otherwise theta_local arrived from the server round / fetch and is packed here
+  const bool pack_in_update = ctx->world == 1 && !ctx->async;
+  if (!pack_in_update) {
+    PB("gpack", 1);
+    launch_gpack(ctx->theta_local, ctx->theta_local_bf16, ctx->gpack_off, ctx->pack_map, ctx->pack_n, st);
+    PE();
+  }
   if (refresh) {  // a14: theta^ <- theta, packed images included
     PB("target_refresh", 0);
     if (ctx->fused_comm)
@@ -1889,14 +1894,15 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
     } else if (ctx->use_tgemm && ctx->split_update) {  // the conv parameters here, the rest on the side branch
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, fc0, div, (float)c.lr, rho, omr, (float)c.rms_eps,
-                     nullptr, ctx->theta_local_bf16, ctx->ctr, 1, st, -1, 0, 0, ctx->grad_snap);
+                     nullptr, ctx->theta_local_bf16, ctx->ctr, 1, st, -1, 0, 0, ctx->grad_snap, ctx->pack_map,
+                     ctx->pack_n, ctx->gpack_off);
       CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
       PE();
     } else {
       PB("rmsprop_update", 1);
       launch_rmsprop(ctx->theta_master, ctx->rms, ctx->grad, ctx->P_pad, div, (float)c.lr, rho, omr,
                      (float)c.rms_eps, nullptr, ctx->alias_local ? ctx->theta_local_bf16 : nullptr, ctx->ctr, 1, st, -1, 0,
-                     0, ctx->grad_snap);
+                     0, ctx->grad_snap, ctx->alias_local ? ctx->pack_map : nullptr, ctx->pack_n, ctx->gpack_off);
       PE();
     }
   }

@@ -123,7 +123,8 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
 __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r, float* __restrict__ g, long long n,
                                float inv_div, float lr, float rho, float omr, float eps, float* __restrict__ pub_f32,
                                __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr, int zero_g, long long img_off,
-                               long long w1_off, long long w2_off, float* __restrict__ g_snap) {
+                               long long w1_off, long long w2_off, float* __restrict__ g_snap,
+                               const int2* __restrict__ pack_map, long long pack_n, long long pack_off) {
   st_stamp(ST_UPDATE, 0);
   pdl_sync();
   st_stamp(ST_UPDATE, 1);
@@ -159,6 +160,17 @@ __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r,
     o.x = *reinterpret_cast<uint32_t*>(&lo);
     o.y = *reinterpret_cast<uint32_t*>(&hi);
     reinterpret_cast<uint2*>(pub_bf16)[i] = o;
+    if (pack_map && 4 * i < pack_n) {  // the generic path's packed conv images (gpack_kernel, fused at N = 1)
+      const float tq[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (4 * i + q >= pack_n) break;
+        const int2 d = pack_map[4 * i + q];
+        const __nv_bfloat16 v = __float2bfloat16_rn(tq[q]);
+        if (d.x >= 0) pub_bf16[pack_off + d.x] = v;
+        if (d.y >= 0) pub_bf16[pack_off + d.y] = v;
+      }
+    }
     if (img_off >= 0 && 4 * i + 3 >= min(w1_off, w2_off) && 4 * i < max(w1_off, w2_off) + kW2Elems) {
       const float tq[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
@@ -174,10 +186,11 @@ __global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r,
 
 void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, float lr, float rho, float omr,
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
-                    cudaStream_t st, long long img_off, long long w1_off, long long w2_off, float* g_snap) {
+                    cudaStream_t st, long long img_off, long long w1_off, long long w2_off, float* g_snap,
+                    const int2* pack_map, long long pack_n, long long pack_off) {
   const int blocks = (int)((n / 4 + 255) / 256);
   launch_pdl(rmsprop_kernel, dim3(blocks < 1 ? 1 : blocks), dim3(256), 0, st, theta, r, g, n, 1.0f / div, lr, rho, omr,
-             eps, pub_f32, pub_bf16, ctr, zero_g, img_off, w1_off, w2_off, g_snap);
+             eps, pub_f32, pub_bf16, ctr, zero_g, img_off, w1_off, w2_off, g_snap, pack_map, pack_n, pack_off);
 }
 
 

@@ -1,0 +1,7 @@
+# after the gpack fusion: generic-path parity + the FC-forward split A/B at BJ.configs[4]
+timeout 900 python -m pytest -q -x -m gpu tests/test_gpu_parity_gated.py tests/test_gpu_parity_gconv.py tests/test_gpu_full_size.py tests/test_gpu_replay_dedup.py 2>&1 | tail -2
+for sp in 7 4 2; do
+  DQN_TG_FWD_SPLITS=$sp timeout 300 python bench.py --config c5 --steps 50 --warmup 5 --no-cpu-baseline --no-acting > gpurun_out/c5_sp$sp.json 2>/dev/null
+  python -c "
+import json; d=json.loads([l for l in open('gpurun_out/c5_sp$sp.json') if l.startswith('{')][0]); r=d.get('regions_us',{}); print('splits $sp', round(d['value']), round(d['ms_per_step']*1e3,1), r.get('fc1_fwd'), r.get('head_sample'), r.get('gpack'), r.get('conv_bwd'))"
+done
