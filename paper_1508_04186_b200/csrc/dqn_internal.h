@@ -410,16 +410,9 @@ struct TGemmArgs {
   int hwc_HW, hwc_C;
   int hwc_Wo, hwc_Ws;              // hwc_Ws > 0: the NHWC dZ in the input-grid geometry (row y * Ws + x, not
   long long ldo_out;               //   y * Wo + x), per-sample stride ldo_out (TCONV backward)
-  // TC_EPI_CONV_FWD (implicit-GEMM convolution over "virtual rows"): row m = img * Hs*Ws + y * Ws + x of the
-  // input grid; K chunk c = (tap t, 64-channel block cb), A box at row m0 + (t / Tw) * Ws + t % Tw; rows with
-  // y >= Ho or x >= Wo are computed and discarded
-  int Ws, HsWs, Tw, Cblk, Ho, Wo;
-  const float* bias[2];
-  __nv_bfloat16* cout[2];          // next layer's s2d grid (s_next > 0) or the canonical (C,H,W) flatten
-  float scale;                     // 1/255 on layer 1 (integer-valued bf16 pixels), else 1
-  int s_next;
 };
-constexpr int TC_EPI_CONV_FWD = 3;
+// tgemm only: C[g][n * ldc + m] = D (store) or += D, the transposed ACCUM (lanes = consecutive m: coalesced)
+constexpr int TC_EPI_ACCUM_T = 4;
 // ---- TMA implicit-GEMM convolutions with tap windows (kernels_tma.cu). The A source is a 2-D bf16 tensor of
 // "virtual rows" (row = img * Hs*Ws + y * Ws + x of a layer's input grid, 64-channel blocks); ONE TMA box of
 // R = 128 (or 64) + maxshift rows per channel block feeds every tap: tap t is the same window read from row

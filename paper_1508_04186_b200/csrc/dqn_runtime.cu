@@ -621,12 +621,12 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
     ok = ok && make_tmap_bf16(&f.ta[g], W[g], H, D, D, 128);
     ok = ok && make_tmap_bf16(&f.tb[g], ctx->a2_bf16 + (long long)g * b * D, b, D, D, f.BN);
   }
-  TGemmArgs& w = ctx->tg_dw;  // dW [H][D] = dH^T a2: both operands MN-major over K = b
-  w.M = H; w.N = D; w.K = b; w.kper = b; w.splits = 1; w.BN = 64;
-  w.a_mn = 1; w.b_mn = 1; w.groups = 1; w.epi = TC_EPI_ACCUM; w.store = ctx->cfg.n_push == 1;
+  TGemmArgs& w = ctx->tg_dw;  // dW^T [D][H] = a2^T dH: both operands MN-major over K = b, stored transposed into
+  w.M = D; w.N = H; w.K = b; w.kper = b; w.splits = 1; w.BN = 64;  // G's [H][D] (lanes along d: coalesced)
+  w.a_mn = 1; w.b_mn = 1; w.groups = 1; w.epi = TC_EPI_ACCUM_T; w.store = ctx->cfg.n_push == 1;
   w.C[0] = ctx->grad + F.w_off; w.ldc = D;
-  ok = ok && make_tmap_bf16(&w.ta[0], ctx->dh_bf16, b, H, H, 64);
-  ok = ok && make_tmap_bf16(&w.tb[0], ctx->a2_bf16, b, D, D, 64);
+  ok = ok && make_tmap_bf16(&w.ta[0], ctx->a2_bf16, b, D, D, 64);
+  ok = ok && make_tmap_bf16(&w.tb[0], ctx->dh_bf16, b, H, H, 64);
   TGemmArgs& x = ctx->tg_dx;  // dZ [b][D] = [a2 > 0] dH W: A = W MN-major over K = H, B = dH K-major
   x.M = D; x.N = b; x.K = H; x.kper = H; x.splits = 1; x.BN = 64;
   x.a_mn = 1; x.b_mn = 0; x.groups = 1; x.epi = TC_EPI_MASK_T;

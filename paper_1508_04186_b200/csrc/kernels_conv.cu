@@ -586,11 +586,17 @@ __global__ void __launch_bounds__(256) gconv_wreduce_kernel(GConvWgradArgs a) {
   const int q0 = grp * per, q1 = min(nr, q0 + per);
   float s = 0.0f;
   // part_cm: e enumerates (n, row) with the row fastest, the column-major partials' order (coalesced reads)
-  if (e < total) {
-    if (e < nw)
-      for (int q = q0; q < q1; ++q) s += a.partial[(long long)q * nw + e];
-    else
-      for (int q = q0; q < q1; ++q) s += a.partial_db[(long long)q * a.N + (e - nw)];
+  if (e < total) {  // 8 loads in flight per round, summed in range order
+    const float* src = e < nw ? a.partial + e : a.partial_db + (e - nw);
+    const long long stride = e < nw ? nw : a.N;
+    for (int q = q0; q < q1; q += 8) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = q + k < q1 ? __ldcg(src + (long long)(q + k) * stride) : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (q + k < q1) s += v[k];
+    }
   }
   __shared__ float red[8][32];
   red[grp][el] = s;

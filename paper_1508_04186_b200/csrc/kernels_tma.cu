@@ -16,6 +16,7 @@
 //   TC_EPI_FC_FWD : partial[g][split][n][m] = D            (split-K partials; the TD head reduces them)
 //   TC_EPI_ACCUM  : C[g][m * ldc + n] = D (store) or += D   (FC dW into G)
 //   TC_EPI_MASK_T : out[n * ldo + m'] = mask[n * ldo + m] > 0 ? D : 0, m' = NHWC remap (FC dX, ReLU')
+//   TC_EPI_ACCUM_T: C[g][n * ldc + m] = D or += D                  (FC dW computed as dW^T: coalesced stores)
 #include <cuda.h>  // CUtensorMap and the encode entry point's types (fetched from the driver at run time)
 
 #include <algorithm>
@@ -295,6 +296,16 @@ __global__ void __launch_bounds__(TG_THREADS, 2) tgemm_kernel(const __grid_const
 #pragma unroll
             for (int i = 0; i < 16; ++i)  // (unrolled: v[] must stay in registers)
               if (n0 + c + i < a.N) crow[i] = a.store ? v[i] : crow[i] + v[i];
+          }
+        } else if (a.epi == TC_EPI_ACCUM_T) {  // C[n][m]: the warp's 32 rows are 128 contiguous bytes per column
+          float* ccol = a.C[g] + m;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = n0 + c + i;
+            if (n < a.N) {
+              float* p = ccol + (long long)n * a.ldc;
+              *p = a.store ? v[i] : *p + v[i];
+            }
           }
         } else {  // TC_EPI_MASK_T: all 16 mask loads in flight before the (possibly aliasing) stores
           long long om = m;
