@@ -7,7 +7,8 @@ import pytest
 
 import paper_1508_04186_b200 as D
 import synth
-from tests.helpers import he_theta, nets
+from oracle import oracle as O
+from tests.helpers import delta_rel, gated_theta, he_theta, nets
 
 pytestmark = pytest.mark.gpu
 TINY_KW = dict(frames=3, height=17, width=13, convs=((5, 5, 2), (6, 3, 2)), fcs=(19,), n_actions=5)
@@ -60,3 +61,27 @@ def test_dedup_rejects_unshifted_stacks(device_push):
     assert e.value.code == D.EINVAL
     assert g.replay_size() == (0, 0)  # nothing stored
     g.close()
+
+
+@pytest.mark.parametrize("precision,kw", [(D.FP32, TINY_KW), (D.BF16, {})], ids=["fp32-tiny", "bf16-mnih"])
+def test_dedup_matches_the_oracle(precision, kw):
+    """The deduplicated replay against the oracle (which stores full stacks): the same transitions, so the
+    same sampled slots (bit-exact) and theta after k steps within the path's bar (fp32 1e-5; bf16 in the gated
+    regime, A38, 2e-2)."""
+    steps = 4
+    lr = 1e-3 if precision == D.FP32 else 1e-5
+    eps = 1e-8 if precision == D.FP32 else 1e-2
+    dc, on, oc = nets(minibatch=32, replay_capacity=150, precision=precision, target_sync=2, lr=lr, rms_eps=eps,
+                      replay_dedup=1, **kw)
+    th0 = he_theta(on, 3) if precision == D.FP32 else gated_theta(on, 3)
+    data = synth.g_pong(200, on.frames, on.height, on.width, on.n_actions, 11)  # wraps the 150-slot ring
+    g = D.DQN(dc, init_params=th0)
+    g.push(*data)
+    out = g.train(steps, want_idx=True)
+    th = g.params(D.PARAMS_SERVER)
+    g.close()
+    s, a, r, sn, t = data
+    ref = O.run(on, oc, 150, [O.Replay(s, a, r.astype(np.float64), sn, t)], th0.astype(np.float64), steps)
+    assert np.array_equal(out["idx"], ref["idx"][0].astype(np.int32))
+    tol = 1e-5 if precision == D.FP32 else 2e-2
+    assert delta_rel(th, th0, ref["theta"], th0, on, ulps=steps) < tol
