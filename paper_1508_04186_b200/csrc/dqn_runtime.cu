@@ -87,8 +87,12 @@ struct dqn_ctx {
   __nv_bfloat16* x1[2] = {};
   __nv_bfloat16* dzp[kMaxConv] = {};          // dZ of every conv layer in its input-grid geometry (zero borders)
   __nv_bfloat16* dx_canon = nullptr;          // FC dX (masked) in the canonical flatten [b][D], before chw_to_hwc
-  float* tc_part = nullptr;
+  float* tc_part = nullptr;                   // every layer's weight-gradient partials, each at its own offset
   float* tc_part_db = nullptr;
+  // conv backward on two graph branches: the data-gradient chain (dgrad L-1 .. 1, then wgrad 0) on the main
+  // stream, the weight gradients (+ range reductions) of layers L-1 .. 1 on bside, each after its dZ is ready
+  cudaStream_t bside = nullptr;
+  cudaEvent_t ev_bdz[kMaxConv] = {}, ev_bjoin = nullptr;
   // N = 1, n_push = 1 on the TMA kernels: the head finish and the RMSProp update of the FC / output-layer
   // parameters run on a side stream (graph branch) next to the FC dX and the conv backward
   bool split_update = false;
@@ -453,6 +457,10 @@ static void free_all(dqn_ctx* c) {
   for (auto* x : c->dzp)
     if (x) cudaFree(x);
   if (c->tc_part) cudaFree(c->tc_part);
+  if (c->bside) cudaStreamDestroy(c->bside);
+  for (cudaEvent_t e : c->ev_bdz)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_bjoin) cudaEventDestroy(c->ev_bjoin);
   if (c->tc_part_db) cudaFree(c->tc_part_db);
   if (c->gw_partial_db) cudaFree(c->gw_partial_db);
   for (int i = 0; i < 2; ++i) {
@@ -692,8 +700,8 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
     ok = ok && L.N <= 64 && make_tmap_bf16(&w.ta[0], x[0], rows, G.Cs, G.Cs, w.R);
     ok = ok && make_tmap_bf16(&w.tb[0], ctx->dzp[i], rows, L.N, L.N, 64);
     ok = ok && tconv_smem(w) > 0;
-    max_part = std::max(max_part, (long long)w.ranges * K * L.N);
-    max_db = std::max(max_db, (long long)w.ranges * L.N);
+    max_part += (long long)w.ranges * K * L.N;  // per-layer regions: two layers' weight gradients may overlap
+    max_db += (long long)w.ranges * L.N;
     GConvWgradArgs& r = ctx->tc_wred[i];
     r.Th = G.Th; r.Tw = G.Tw; r.Cs = G.Cs; r.N = L.N; r.b = w.ranges; r.ipc = 1; r.first = i == 0;
     r.w_canon = G.w_canon; r.w_off = L.w_off; r.w_nstride = (long long)L.C * L.k * L.k; r.b_off = L.b_off;
@@ -715,10 +723,25 @@ static void setup_tgemm_fc(dqn_ctx* ctx) {
   }
   if (ok) {
     ok = !dalloc(ctx, &ctx->tc_part, max_part) && !dalloc(ctx, &ctx->tc_part_db, max_db);
+    long long po = 0, pdo = 0;
     for (int i = 0; i < nl && ok; ++i) {
-      ctx->tc_wgrad[i].partial = ctx->tc_part; ctx->tc_wgrad[i].partial_db = ctx->tc_part_db;
-      ctx->tc_wred[i].partial = ctx->tc_part; ctx->tc_wred[i].partial_db = ctx->tc_part_db;
+      TConvArgs& w = ctx->tc_wgrad[i];
+      w.partial = ctx->tc_part + po; w.partial_db = ctx->tc_part_db + pdo;
+      ctx->tc_wred[i].partial = w.partial; ctx->tc_wred[i].partial_db = w.partial_db;
+      po += (long long)w.ranges * w.TCs * w.Nout;
+      pdo += (long long)w.ranges * w.Nout;
       if (i > 0) ctx->tc_dgrad[i].dzprev = ctx->dzp[i - 1];
+    }
+    const char* cb = getenv("DQN_CONC_BWD");
+    if (ok && nl >= 2 && !(cb && atoi(cb) == 0) &&
+        cudaStreamCreateWithFlags(&ctx->bside, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaEventCreateWithFlags(&ctx->ev_bjoin, cudaEventDisableTiming) == cudaSuccess) {
+      for (int i = 0; i < nl; ++i)
+        if (cudaEventCreateWithFlags(&ctx->ev_bdz[i], cudaEventDisableTiming) != cudaSuccess) {
+          cudaStreamDestroy(ctx->bside);
+          ctx->bside = nullptr;
+          break;
+        }
     }
     // FC dX writes the last conv layer's dZ: coalesced into the canonical flatten, then chw_to_hwc permutes it
     // into the layer's input-grid geometry (a direct NHWC store from the GEMM epilogue is a 2-byte scatter with a
@@ -1845,7 +1868,23 @@ static int enqueue_step_gpath(dqn_ctx* ctx, bool fetch, bool refresh, bool push)
   }
   // a8/a9: per layer, top down: wgrad (+ range reduction into G), then dgrad into the layer below
   PB("conv_bwd", 3 * nl - 1);
-  for (int i = nl - 1; i >= 0 && ctx->use_tconv; --i) {
+  if (ctx->use_tconv && ctx->bside) {
+    // the data-gradient chain on the main stream; layer i's weight gradient on bside as soon as dZ_i exists, so it
+    // fills the SMs the chain's tails leave idle (they read dZ_i and the layer input, write their own partials
+    // and G's conv rows; joined before the update)
+    for (int i = nl - 1; i >= 1; --i) {
+      CK(cudaEventRecord(ctx->ev_bdz[i], st));  // dZ_i complete (FC dX or the data gradient of layer i + 1)
+      CK(cudaStreamWaitEvent(ctx->bside, ctx->ev_bdz[i], 0));
+      launch_tconv(ctx->tc_wgrad[i], ctx->num_sms, ctx->bside);
+      launch_gconv_wreduce(ctx->tc_wred[i], ctx->bside);
+      launch_tconv(ctx->tc_dgrad[i], ctx->num_sms, st);
+    }
+    launch_tconv(ctx->tc_wgrad[0], ctx->num_sms, st);
+    launch_gconv_wreduce(ctx->tc_wred[0], st);
+    CK(cudaEventRecord(ctx->ev_bjoin, ctx->bside));
+    CK(cudaStreamWaitEvent(st, ctx->ev_bjoin, 0));
+  }
+  for (int i = nl - 1; i >= 0 && ctx->use_tconv && !ctx->bside; --i) {
     launch_tconv(ctx->tc_wgrad[i], ctx->num_sms, st);
     launch_gconv_wreduce(ctx->tc_wred[i], st);
     if (i > 0) launch_tconv(ctx->tc_dgrad[i], ctx->num_sms, st);
