@@ -74,8 +74,7 @@ __device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
       "@e mbarrier.arrive.shared::cta.b64 _, [%0]; }" ::"r"(smem_u32(bar))
       : "memory");
 }
-__device__ unsigned g_spin_ns = 0;     // probe knob: back-off of the single-thread waits
-__device__ unsigned g_epi_spin_ns = 64;
+constexpr unsigned kEpiSpinNs = 64;  // back-off of the epilogue warps' polling lane (the producer / MMA spin freely)
 // spin on mbarrier.test_wait (never suspends: the pipelines here hand off every few hundred cycles, and a
 // suspended try_wait was measured to add ~1 us per hand-off on short convolution tiles)
 __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
@@ -87,7 +86,6 @@ __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
     if (done) break;
-    if (g_spin_ns) __nanosleep(g_spin_ns);
   }
 }
 // the epilogue warps' wait: one lane polls (with a short back-off), the warp then proceeds together, so eight
@@ -102,7 +100,7 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
           : "r"(smem_u32(bar)), "r"(parity)
           : "memory");
       if (done) break;
-      __nanosleep(g_epi_spin_ns);
+      __nanosleep(kEpiSpinNs);
     }
   }
   __syncwarp();

@@ -59,8 +59,6 @@ int main(int argc, char** argv) {
     fprintf(stderr, "setup failed\n");
     return 1;
   }
-  if (getenv("TC_SPIN")) { unsigned v = atoi(getenv("TC_SPIN")); cudaMemcpyToSymbol(g_spin_ns, &v, 4); }
-  if (getenv("TC_ESPIN")) { unsigned v = atoi(getenv("TC_ESPIN")); cudaMemcpyToSymbol(g_epi_spin_ns, &v, 4); }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   launch_tconv(f, sms, 0);
