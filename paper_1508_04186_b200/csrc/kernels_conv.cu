@@ -802,36 +802,51 @@ void launch_gemm_pipe(const TcGemmArgs& a, int groups, cudaStream_t st) {
 // ------------------------------------------------------------------ TD head finish, one warp per element
 // The cross-sample sums of head_finish.cuh for large b: lane l sums samples j = l, l+32, ... in
 // ascending order, then the 32 lane sums combine in a fixed shuffle tree (deterministic).
+// The cross-sample sums of the TD head (head_finish.cuh's elements) with a warp per 32 consecutive outputs:
+//   dW_o[a][u0 .. u0+31] : warp (a, u0) walks the samples in ascending j; only samples with a_j = a contribute
+//                          (a warp-uniform branch), and their rows h_j[u0 .. u0+31] are one coalesced 128-byte load
+//   db_fc[u0 .. u0+31]   : warp u0, every sample, the same coalesced rows of dH
+//   db_o[a], loss, T + 1 : one warp each, lanes over the samples, butterfly (fixed order)
+// (a warp per output element reading h_j[u] for 32 samples at once touched 32 lines per load)
 __global__ void __launch_bounds__(256) head_finish_warp_kernel(HeadArgs h) {
   pdl_sync();
   const int lane = threadIdx.x & 31;
-  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int H = h.H, A = h.A;
-  if (e >= A * H + A + H + 1) return;
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int H = h.H, A = h.A, UB = (H + 31) / 32;
   const float* h0 = h.fc_partial ? h.act_out[0] : h.act[0];
-  float s = 0.0f;
-  if (e < A * H) {
-    const int a = e / H, u = e % H;
-    for (int j = lane; j < h.b; j += 32)
-      if (h.s_act[j] == a) s = fmaf(h.s_dq[j], h0[(long long)j * H + u], s);
-  } else if (e < A * H + A) {
-    const int a = e - A * H;
-    for (int j = lane; j < h.b; j += 32)
-      if (h.s_act[j] == a) s += h.s_dq[j];
-  } else if (e < A * H + A + H) {
+  if (w < A * UB) {  // dW_o rows
+    const int a = w / UB, u = (w % UB) * 32 + lane;
+    float s = 0.0f;
+    for (int j = 0; j < h.b; ++j)
+      if (__ldg(h.s_act + j) == a && u < H) s = fmaf(h.s_dq[j], h0[(long long)j * H + u], s);
+    if (u < H) h.grad[h.w_off + (long long)a * H + u] += s;
+    return;
+  }
+  const int w2 = w - A * UB;
+  if (w2 < UB) {  // db of the previous FC layer
     if (!h.prev_is_fc) return;
-    const int u = e - A * H - A;
-    for (int j = lane; j < h.b; j += 32) s += h.dH[(long long)j * H + u];
-  } else {
+    const int u = w2 * 32 + lane;
+    if (u >= H) return;
+    float s = 0.0f;
+    for (int j = 0; j < h.b; ++j) s += h.dH[(long long)j * H + u];
+    h.grad[h.prev_b_off + u] += s;
+    return;
+  }
+  const int w3 = w2 - UB;
+  if (w3 > A) return;
+  float s = 0.0f;
+  if (w3 < A) {  // db_o[a]
+    for (int j = lane; j < h.b; j += 32)
+      if (h.s_act[j] == w3) s += h.s_dq[j];
+  } else {  // the loss
     for (int j = lane; j < h.b; j += 32) s += h.s_loss[j];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane != 0) return;
-  if (e < A * H) h.grad[h.w_off + e] += s;
-  else if (e < A * H + A) h.grad[h.b_off + (e - A * H)] += s;
-  else if (e < A * H + A + H) h.grad[h.prev_b_off + (e - A * H - A)] += s;
-  else {
+  if (w3 < A) {
+    h.grad[h.b_off + w3] += s;
+  } else {
     const unsigned long long T = h.ctr->T;
     h.diag_loss[T % kDiagSteps] = s / (float)h.b;
     h.ctr->T = T + 1;  // this step is complete for the sampler
@@ -839,8 +854,8 @@ __global__ void __launch_bounds__(256) head_finish_warp_kernel(HeadArgs h) {
 }
 
 void launch_head_finish_warp(const HeadArgs& h, cudaStream_t st) {
-  const int n = h.A * h.H + h.A + h.H + 1;
-  launch_pdl(head_finish_warp_kernel, dim3((n + 7) / 8), dim3(256), 0, st, h);
+  const int UB = (h.H + 31) / 32, warps = h.A * UB + UB + h.A + 1;
+  launch_pdl(head_finish_warp_kernel, dim3((warps + 7) / 8), dim3(256), 0, st, h);
   gconv_debug("head_finish_warp", st);
 }
 
