@@ -802,60 +802,107 @@ void launch_gemm_pipe(const TcGemmArgs& a, int groups, cudaStream_t st) {
 // ------------------------------------------------------------------ TD head finish, one warp per element
 // The cross-sample sums of head_finish.cuh for large b: lane l sums samples j = l, l+32, ... in
 // ascending order, then the 32 lane sums combine in a fixed shuffle tree (deterministic).
-// The cross-sample sums of the TD head (head_finish.cuh's elements) with a warp per 32 consecutive outputs:
-//   dW_o[a][u0 .. u0+31] : warp (a, u0) walks the samples in ascending j; only samples with a_j = a contribute
-//                          (a warp-uniform branch), and their rows h_j[u0 .. u0+31] are one coalesced 128-byte load
-//   db_fc[u0 .. u0+31]   : warp u0, every sample, the same coalesced rows of dH
-//   db_o[a], loss, T + 1 : one warp each, lanes over the samples, butterfly (fixed order)
+// The cross-sample sums of the TD head (head_finish.cuh's elements), coalesced over 32 consecutive outputs:
+//   dW_o[a][u0 .. u0+31] : a warp per (a, u0) walks the samples in ascending j; the samples with a_j = a (found
+//                          with ballots over the actions staged in shared memory) are batched 8 at a time, so 8
+//                          coalesced 128-byte row loads h_j[u0 .. u0+31] are in flight; summed in j order
+//   db_fc[u0 .. u0+31]   : a CTA per u0: warp k sums samples [k b/8, (k+1) b/8) of dH with 8 loads in flight,
+//                          then the 8 partial sums are added in warp order
+//   db_o[a], loss, T + 1 : the last CTA, a warp per output, lanes over the samples, butterfly (fixed order)
 // (a warp per output element reading h_j[u] for 32 samples at once touched 32 lines per load)
 __global__ void __launch_bounds__(256) head_finish_warp_kernel(HeadArgs h) {
+  extern __shared__ float hf_sm[];  // [b] dQ_j | [b] a_j
+  __shared__ float s_part[8][32];
+  float* s_dq = hf_sm;
+  int* s_act = reinterpret_cast<int*>(hf_sm + h.b);
   pdl_sync();
-  const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int H = h.H, A = h.A, UB = (H + 31) / 32;
+  for (int j = threadIdx.x; j < h.b; j += blockDim.x) {
+    s_dq[j] = h.s_dq[j];
+    s_act[j] = h.s_act[j];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int H = h.H, A = h.A, UB = (H + 31) / 32, cw = (A * UB + 7) / 8;  // CTAs of dW_o warps
   const float* h0 = h.fc_partial ? h.act_out[0] : h.act[0];
-  if (w < A * UB) {  // dW_o rows
-    const int a = w / UB, u = (w % UB) * 32 + lane;
+  if ((int)blockIdx.x < cw) {  // dW_o rows
+    const int w = blockIdx.x * 8 + warp;
+    if (w >= A * UB) return;
+    const int a = w / UB, u = (w % UB) * 32 + lane, uc = u < H ? u : H - 1;
     float s = 0.0f;
-    for (int j = 0; j < h.b; ++j)
-      if (__ldg(h.s_act + j) == a && u < H) s = fmaf(h.s_dq[j], h0[(long long)j * H + u], s);
+    int js[8], n = 0;
+    auto flush = [&]() {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = k < n ? h0[(long long)js[k] * H + uc] : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < n) s = fmaf(s_dq[js[k]], v[k], s);
+      n = 0;
+    };
+    for (int j0 = 0; j0 < h.b; j0 += 32) {
+      unsigned m = __ballot_sync(0xffffffffu, j0 + lane < h.b && s_act[j0 + lane] == a);
+      while (m) {
+        const int j = j0 + __ffs(m) - 1;
+        m &= m - 1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k == n) js[k] = j;
+        if (++n == 8) flush();
+      }
+    }
+    if (n) flush();
     if (u < H) h.grad[h.w_off + (long long)a * H + u] += s;
     return;
   }
-  const int w2 = w - A * UB;
-  if (w2 < UB) {  // db of the previous FC layer
+  const int cb = (int)blockIdx.x - cw;
+  if (cb < UB) {  // db of the previous FC layer, u block cb
     if (!h.prev_is_fc) return;
-    const int u = w2 * 32 + lane;
-    if (u >= H) return;
+    const int u = cb * 32 + lane, uc = u < H ? u : H - 1;
+    const int per = (h.b + 7) / 8, j_lo = warp * per, j_hi = min(h.b, j_lo + per);
     float s = 0.0f;
-    for (int j = 0; j < h.b; ++j) s += h.dH[(long long)j * H + u];
-    h.grad[h.prev_b_off + u] += s;
+    for (int j0 = j_lo; j0 < j_hi; j0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = j0 + k < j_hi ? h.dH[(long long)(j0 + k) * H + uc] : 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (j0 + k < j_hi) s += v[k];
+    }
+    s_part[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && u < H) {
+      float t = s_part[0][lane];
+      for (int k = 1; k < 8; ++k) t += s_part[k][lane];
+      h.grad[h.prev_b_off + u] += t;
+    }
     return;
   }
-  const int w3 = w2 - UB;
-  if (w3 > A) return;
-  float s = 0.0f;
-  if (w3 < A) {  // db_o[a]
-    for (int j = lane; j < h.b; j += 32)
-      if (h.s_act[j] == w3) s += h.s_dq[j];
-  } else {  // the loss
-    for (int j = lane; j < h.b; j += 32) s += h.s_loss[j];
-  }
+  // the last CTA: db_o[a] for a < A, then the loss (warp per output, outputs strided over the 8 warps)
+  for (int o = warp; o <= A; o += 8) {
+    float s = 0.0f;
+    if (o < A) {
+      for (int j = lane; j < h.b; j += 32)
+        if (s_act[j] == o) s += s_dq[j];
+    } else {
+      for (int j = lane; j < h.b; j += 32) s += h.s_loss[j];
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane != 0) return;
-  if (w3 < A) {
-    h.grad[h.b_off + w3] += s;
-  } else {
-    const unsigned long long T = h.ctr->T;
-    h.diag_loss[T % kDiagSteps] = s / (float)h.b;
-    h.ctr->T = T + 1;  // this step is complete for the sampler
+    for (int q = 16; q > 0; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
+    if (lane == 0) {
+      if (o < A) {
+        h.grad[h.b_off + o] += s;
+      } else {
+        const unsigned long long T = h.ctr->T;
+        h.diag_loss[T % kDiagSteps] = s / (float)h.b;
+        h.ctr->T = T + 1;  // this step is complete for the sampler
+      }
+    }
   }
 }
 
 void launch_head_finish_warp(const HeadArgs& h, cudaStream_t st) {
-  const int UB = (h.H + 31) / 32, warps = h.A * UB + UB + h.A + 1;
-  launch_pdl(head_finish_warp_kernel, dim3((warps + 7) / 8), dim3(256), 0, st, h);
+  const int UB = (h.H + 31) / 32, ctas = (h.A * UB + 7) / 8 + UB + 1;
+  launch_pdl(head_finish_warp_kernel, dim3(ctas), dim3(256), (size_t)h.b * 8, st, h);
   gconv_debug("head_finish_warp", st);
 }
 

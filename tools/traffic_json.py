@@ -42,8 +42,14 @@ def scaled(path):
     ls = launches(path)
     starts = [i for i, l in enumerate(ls) if l["kernel"] == "gather_s2d_kernel"]
     i0 = starts[0]
-    i1 = starts[1] if len(starts) > 1 else len(ls)
-    step = ls[i0:i1]
+    # one step from a gather to the next; with a single gather in the capture, the launches before it are the
+    # previous step's tail and complete the cycle (the capture holds at least one step's worth of launches)
+    if len(starts) > 1:
+        step = ls[i0:starts[1]]
+    else:  # the capture's last launches repeat its first ones (the next step began): count them once
+        names = [l["kernel"] for l in ls]
+        k = max((k for k in range(i0 + 1) if names[:k] == names[len(names) - k:]), default=0)
+        step = ls[i0:] + ls[k:i0]
     reg = {}
     seen_head = False
     tg = 0
