@@ -24,7 +24,10 @@ constexpr int HS_MAX_SPLITS = kHeadMaxSplits;
 // dynamic smem: h [H] | h' [H] | W^_o [A][H] | W_o[a_j] [H]
 // CH: FC split-K partials in flight per thread and group (all of them at small b, where the head is on the
 // latency-bound critical path; 8 at large b, where 4 CTAs per SM need the register budget)
-template <int CH, int MINB>
+// MC > 1: the CTAs of a cluster of MC share one read of theta^'s output layer: the cluster's first CTA issues a
+// TMA bulk copy multicast into every member's shared memory (one L2 read instead of MC; the layer is the same
+// for every sample)
+template <int CH, int MINB, int MC>
 __global__ void __launch_bounds__(HS_THREADS, MINB) head_sample_kernel(HeadArgs h) {
   extern __shared__ float4 sm4[];
   const int H = h.H, A = h.A, j = blockIdx.x;
@@ -42,7 +45,30 @@ __global__ void __launch_bounds__(HS_THREADS, MINB) head_sample_kernel(HeadArgs 
   const int act = __ldg(h.ring_a + slot);
   const float r = __ldg(h.ring_r + slot);
   const uint8_t term = __ldg(h.ring_term + slot);
-  for (int e = threadIdx.x; e < A * H; e += HS_THREADS) s_wt[e] = __ldg(h.theta_hat + h.w_off + e);
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (MC > 1) {
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+    const uint32_t bytes = (uint32_t)(A * H * 4);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    }
+    // every member's barrier is initialised and armed before the multicast can complete on it
+    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (rank == 0 && threadIdx.x == 0) {
+      const uint16_t mask = (uint16_t)((1u << MC) - 1);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+          "%4;" ::"r"((uint32_t)__cvta_generic_to_shared(s_wt)),
+          "l"(h.theta_hat + h.w_off), "r"(bytes), "r"(bar), "h"(mask)
+          : "memory");
+    }
+  } else {
+    for (int e = threadIdx.x; e < A * H; e += HS_THREADS) s_wt[e] = __ldg(h.theta_hat + h.w_off + e);
+  }
   for (int u = threadIdx.x; u < H; u += HS_THREADS) s_wa[u] = __ldg(h.theta + h.w_off + (long long)act * H + u);
   if (threadIdx.x < A) s_bt[threadIdx.x] = __ldg(h.theta_hat + h.b_off + threadIdx.x);
   if (threadIdx.x == 0) s_qa_b = __ldg(h.theta + h.b_off + act);
@@ -81,6 +107,15 @@ __global__ void __launch_bounds__(HS_THREADS, MINB) head_sample_kernel(HeadArgs 
       s_h0[u] = __ldg(h.act[0] + (long long)j * H + u);
       s_h1[u] = __ldg(h.act[1] + (long long)j * H + u);
     }
+  }
+  if (MC > 1) {  // theta^'s output layer has landed (phase 0 of this CTA's barrier)
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(bar)
+                   : "memory");
   }
   __syncthreads();
   // ---- Q'(s'_j; theta^) for every action (warp per action) and Q(s_j; theta)_{a_j}
@@ -151,16 +186,20 @@ size_t head_smem_bytes(int A, int H, int b) {
 
 void init_head_kernel_attrs() {
   // the 227 KB opt-in limit includes the kernel's static shared memory
-  cudaFuncSetAttribute(head_sample_kernel<HS_MAX_SPLITS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-  cudaFuncSetAttribute(head_sample_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+  cudaFuncSetAttribute(head_sample_kernel<HS_MAX_SPLITS, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+  cudaFuncSetAttribute(head_sample_kernel<8, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+  cudaFuncSetAttribute(head_sample_kernel<8, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
   cudaGetLastError();  // an attribute refusal only limits the largest head; validate_cfg bounds it
 }
 
 void launch_head_f32(const HeadArgs& h, cudaStream_t st, bool with_finish) {
+  const size_t smem = head_smem_bytes(h.A, h.H, h.b);
   if (h.b <= 128)
-    launch_pdl(head_sample_kernel<HS_MAX_SPLITS, 1>, dim3(h.b), dim3(HS_THREADS), head_smem_bytes(h.A, h.H, h.b), st, h);
+    launch_pdl(head_sample_kernel<HS_MAX_SPLITS, 1, 1>, dim3(h.b), dim3(HS_THREADS), smem, st, h);
+  else if (h.b % 4 == 0 && h.w_off % 4 == 0 && (h.A * h.H) % 4 == 0)  // 16-byte bulk copies
+    launch_pdl_cluster(head_sample_kernel<8, 4, 4>, dim3(h.b), dim3(HS_THREADS), smem, 4, st, h);
   else
-    launch_pdl(head_sample_kernel<8, 4>, dim3(h.b), dim3(HS_THREADS), head_smem_bytes(h.A, h.H, h.b), st, h);
+    launch_pdl(head_sample_kernel<8, 4, 1>, dim3(h.b), dim3(HS_THREADS), smem, st, h);
   if (!with_finish) return;  // the bf16 path runs the finish inside its fused FC-backward launch
   const int n = h.A * h.H + h.A + h.H + 1;
   launch_pdl(head_finish_kernel, dim3((n + 255) / 256), dim3(256), 0, st, h);
