@@ -166,6 +166,11 @@ struct dqn_ctx {
   uint8_t* d_stage = nullptr;  // push_chunk transitions (~4 MB), allocated at create
   uint8_t* h_stage[2] = {};
   cudaEvent_t ev_stage[2] = {};
+  // dqn_store_and_train with host buffers: sub-chunks alternate between the two halves of d_stage, copied on
+  // copy_stream while the previous sub-chunk's steps run (ev_copied: the half is filled, ev_consumed: its steps
+  // are done with it)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {}, ev_consumed[2] = {};
   int stage_flip = 0;
   long long push_chunk = 0;
   // pinned landing zone of dqn_train_steps' per-call outputs
@@ -458,6 +463,7 @@ static void free_all(dqn_ctx* c) {
     if (x) cudaFree(x);
   if (c->tc_part) cudaFree(c->tc_part);
   if (c->bside) cudaStreamDestroy(c->bside);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (cudaEvent_t e : c->ev_bdz)
     if (e) cudaEventDestroy(e);
   if (c->ev_bjoin) cudaEventDestroy(c->ev_bjoin);
@@ -466,6 +472,8 @@ static void free_all(dqn_ctx* c) {
   for (int i = 0; i < 2; ++i) {
     if (c->h_stage[i]) cudaFreeHost(c->h_stage[i]);
     if (c->ev_stage[i]) cudaEventDestroy(c->ev_stage[i]);
+    if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+    if (c->ev_consumed[i]) cudaEventDestroy(c->ev_consumed[i]);
   }
   if (c->h_out) cudaFreeHost(c->h_out);
   if (c->theta_local && !c->alias_local) cudaFree(c->theta_local);
@@ -893,10 +901,13 @@ static int create_impl(dqn_ctx* ctx, const dqn_config* cfg, int rank, int world,
     const long long sb = ctx->net.state_bytes;
     ctx->push_chunk = std::min<long long>(ctx->cap, std::max<long long>(1, (4LL << 20) / (2 * sb + 12)));
     const long long bytes = align16(2 * ctx->push_chunk * sb) + 3 * align16(4 * ctx->push_chunk);
-    if ((rc = dalloc(ctx, &ctx->d_stage, bytes))) return rc;
+    if ((rc = dalloc(ctx, &ctx->d_stage, bytes + 256))) return rc;  // (+ the two halves' alignment slack)
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
       CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage[i]), bytes, cudaHostAllocDefault));
       CK(cudaEventCreateWithFlags(&ctx->ev_stage[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_copied[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_consumed[i], cudaEventDisableTiming));
     }
     CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_out), sizeof(dqn_ctx::HostOut), cudaHostAllocDefault));
   }
@@ -1232,6 +1243,34 @@ static int push_impl(dqn_ctx* ctx, int64_t n, const uint8_t* s, const int32_t* a
           return set_err(ctx, DQN_EINVAL, "replay_dedup: s' is not s shifted by one frame at item " + std::to_string(i));
     }
     // chunk layout (host pinned and device): s [m][sb] | s' [m][sb] | a [m] i32 | r [m] f32 | term [m] u8
+    if (steps && ctx->copy_stream && ctx->push_chunk >= 2) {  // (two halves of >= 1 item each)
+      // Alg. 1's loop: sub-chunks of the caller's transitions are copied (DMA when pinned; the call synchronises
+      // before returning) into alternate halves of d_stage on copy_stream, overlapping the previous sub-chunk's
+      // steps on the context stream
+      const long long sc = std::max<long long>(1, std::min<long long>(16, ctx->push_chunk / 2));
+      const long long half = align16(2 * sc * sb) + 3 * align16(4 * sc);
+      int buf = 0;
+      for (long long i0 = first; i0 < n; i0 += sc, buf ^= 1) {
+        const long long m = std::min(sc, n - i0);
+        const long long o_sn = m * sb, o_a = align16(2 * m * sb), o_r = o_a + align16(4 * m), o_t = o_r + align16(4 * m);
+        uint8_t* d = ctx->d_stage + buf * half;
+        cudaStream_t cs = ctx->copy_stream;
+        CK(cudaStreamWaitEvent(cs, ctx->ev_consumed[buf], 0));  // the steps of two sub-chunks back are done with it
+        CK(cudaMemcpyAsync(d, s + i0 * sb, m * sb, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(d + o_sn, s_next + i0 * sb, m * sb, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(d + o_a, a + i0, m * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(d + o_r, r + i0, m * sizeof(float), cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(d + o_t, terminal + i0, m, cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(ctx->ev_copied[buf], cs));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[buf], 0));
+        int rc = store(i0, m, d, reinterpret_cast<const int32_t*>(d + o_a), reinterpret_cast<const float*>(d + o_r),
+                       d + o_sn, d + o_t);
+        if (rc) return rc;
+        CK(cudaEventRecord(ctx->ev_consumed[buf], ctx->stream));
+      }
+      ctx->count += n;
+      return DQN_OK;
+    }
     for (long long i0 = first; i0 < n; i0 += ctx->push_chunk) {
       const long long m = std::min(ctx->push_chunk, n - i0);
       const long long o_sn = m * sb, o_a = align16(2 * m * sb), o_r = o_a + align16(4 * m), o_t = o_r + align16(4 * m);
