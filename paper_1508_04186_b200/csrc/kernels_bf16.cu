@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, bar_w;
   __shared__ uint32_t tbase;
-  __shared__ float s_db1[16], s_db2[32];
+  __shared__ float s_db1[16], s_db2[32], s_db1_part[4][16];
   const int j = blockIdx.x;
   if (j >= a.n) {  // early-update CTAs (u.early): RMSProp of the non-conv parameters, off the critical path
     rms_tail(u, j - a.n, gridDim.x - a.n);
@@ -880,6 +880,9 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[c + i] += u[i];
     }
+    float dsum[16];  // db1 of this thread's pixel: its four sub-pixels' dZ1, per channel (bf16-rounded as stored)
+#pragma unroll
+    for (int n = 0; n < 16; ++n) dsum[n] = 0.0f;
     if (p < mnih::A1_PIX) {
       const int py = p / 10, px = p % 10;
 #pragma unroll
@@ -894,12 +897,27 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
           const float d_lo = a_lo > 0.0f ? v[16 * q + 2 * h] : 0.0f;
           const float d_hi = a_hi > 0.0f ? v[16 * q + 2 * h + 1] : 0.0f;
           o[h] = pack_bf16(d_lo, d_hi);
+          dsum[2 * h] += __uint_as_float(o[h] << 16);
+          dsum[2 * h + 1] += __uint_as_float(o[h] & 0xFFFF0000u);
         }
         const int y = 2 * py + (q >> 1), x = 2 * px + (q & 1);
         const int m1r = y * mnih::X_W + x;
         *reinterpret_cast<uint4*>(sDZ1 + (0 * BWD_ROWS1 + m1r) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
         *reinterpret_cast<uint4*>(sDZ1 + (1 * BWD_ROWS1 + m1r) * 16) = make_uint4(o[4], o[5], o[6], o[7]);
       }
+    }
+    // db1: the warp's 32 pixels by a shuffle butterfly per channel, then the 4 warps' sums in warp order
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) dsum[n] += __shfl_xor_sync(0xffffffffu, dsum[n], o2);
+    }
+    if (lane < 16) {
+      float vsel = dsum[0];
+#pragma unroll
+      for (int n = 1; n < 16; ++n)
+        if (lane == n) vsel = dsum[n];
+      s_db1_part[warp][lane] = vsel;
     }
   }
   fence_async_smem();
@@ -923,29 +941,16 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
     }
     mma_commit_w(&bar_w);
   }
-  // db1 from the dZ1 planes while conv1 dW runs: all 128 threads, channel n = tid % 16 over the
-  // row slice tid / 16 (8 slices of rows), then the 8 slice sums in slice order (deterministic)
-  __shared__ float s_db1_part[8][16];
-  {
-    const int n = threadIdx.x & 15, sl = threadIdx.x >> 4;
-    const __nv_bfloat16* colp = reinterpret_cast<const __nv_bfloat16*>(sDZ1 + (n >> 3) * BWD_ROWS1 * 16) + (n & 7);
-    float s = 0.0f;
-    for (int r = sl * 53; r < min(420, sl * 53 + 53); ++r) s += __bfloat162float(colp[r * 8]);
-    s_db1_part[sl][n] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < 16) {
-    float s = 0.0f;
-#pragma unroll
-    for (int sl = 0; sl < 8; ++sl) s += s_db1_part[sl][threadIdx.x];
-    s_db1[threadIdx.x] = s;
-  }
+  // db1 = the 4 warps' sums (computed in the dZ1 epilogue) in warp order (deterministic)
+  if (threadIdx.x < 16) s_db1[threadIdx.x] = ((s_db1_part[0][threadIdx.x] + s_db1_part[1][threadIdx.x]) +
+                                              s_db1_part[2][threadIdx.x]) + s_db1_part[3][threadIdx.x];
   __syncwarp();
   st_stamp(ST_P7, 0);
   mbar_wait(&bar_w, 0);
   tc_fence_after();
   st_stamp(ST_P7, 1);
-  // ---- per-image partials: row = (t, c) of the tile, columns = output channels
+  // ---- per-image partials, column-major: [n][row], row = (t, c) of the tile; a warp's 32 rows of one column are
+  // 128 contiguous bytes (row-major float4 rows touched 32 lines per store instruction)
   float* part = a.partial + (long long)j * BWD_PART;
   {
     const int r = 32 * warp + lane;  // M row within a tile
@@ -955,14 +960,12 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
       tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 128 + 16 * mt, v + 16);
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] += v[16 + i];
-      float* d1 = part + (mt * 128 + r) * 16;
 #pragma unroll
-      for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(d1 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      for (int i = 0; i < 16; ++i) part[i * 256 + mt * 128 + r] = v[i];
       tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 32 + 32 * mt, v);
       tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + 32 + 32 * mt + 16, v + 16);
-      float* d2 = part + BWD_PART_W1 + (mt * 128 + r) * 32;
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(d2 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      for (int i = 0; i < 32; ++i) part[BWD_PART_W1 + i * 256 + mt * 128 + r] = v[i];
     }
     if (threadIdx.x < 16) part[BWD_PART_W1 + BWD_PART_W2 + threadIdx.x] = s_db1[threadIdx.x];
     if (threadIdx.x < 32) part[BWD_PART_W1 + BWD_PART_W2 + 16 + threadIdx.x] = s_db2[threadIdx.x];
@@ -975,8 +978,8 @@ __global__ void __launch_bounds__(128) bwd_conv_bf16_kernel(BwdConvArgs a, Reduc
 
 // canonical theta index of per-image partial entry e (tap-permuted conv dW rows, then the biases)
 __device__ __forceinline__ long long bwd_part_dst(int e, const BwdConvArgs& a) {
-  if (e < BWD_PART_W1) {  // (mt*128 + r, n) with r -> tap t = 2*mt + r/64, c' = r%64
-    const int row = e / 16, n = e % 16;
+  if (e < BWD_PART_W1) {  // column-major (n, mt*128 + r) with r -> tap t = 2*mt + r/64, c' = r%64
+    const int row = e % 256, n = e / 256;
     const int t = 2 * (row / 128) + ((row % 128) >> 6), c = row & 63;
     const int f = c >> 4, iy = (c >> 2) & 3, ix = c & 3;
     const int ky = 4 * (t >> 1) + iy, kx = 4 * (t & 1) + ix;
@@ -984,7 +987,7 @@ __device__ __forceinline__ long long bwd_part_dst(int e, const BwdConvArgs& a) {
   }
   if (e < BWD_PART_W1 + BWD_PART_W2) {
     const int ee = e - BWD_PART_W1;
-    const int row = ee / 32, n = ee % 32;
+    const int row = ee % 256, n = ee / 256;
     const int t = 2 * (row / 128) + ((row % 128) >> 6), c2 = row & 63;
     const int q = c2 >> 4, c = c2 & 15;
     const int ky = 2 * (t >> 1) + (q >> 1), kx = 2 * (t & 1) + (q & 1);
