@@ -43,4 +43,37 @@ __device__ __forceinline__ void head_finish_elem(const HeadArgs& h, int e) {
   }
 }
 
+// dW_o[a][u] of a warp whose 32 lanes hold consecutive u of the same action a (H % 32 == 0): the samples with
+// a_j = a are found 32 at a time by a ballot over the staged actions and their h_j[u] loads go out 8 at a
+// time. The fmaf chain runs over the same samples in the same ascending order as head_finish_elem (bit-identical),
+// without one exposed load latency per matching sample.
+__device__ __forceinline__ float head_finish_dwo_warp(const HeadArgs& h, const float* h0, const int* s_act,
+                                                      const float* s_dq, int a, int u) {
+  const int lane = threadIdx.x & 31;
+  float s = 0.0f;
+  int js[8], nn = 0;
+  auto flush = [&]() {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = k < nn ? h0[(long long)js[k] * h.H + u] : 0.0f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < nn) s = fmaf(s_dq[js[k]], v[k], s);
+    nn = 0;
+  };
+  for (int j0 = 0; j0 < h.b; j0 += 32) {
+    unsigned m = __ballot_sync(0xffffffffu, j0 + lane < h.b && s_act[j0 + lane] == a);
+    while (m) {
+      const int j = j0 + __ffs(m) - 1;
+      m &= m - 1;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k == nn) js[k] = j;
+      if (++nn == 8) flush();
+    }
+  }
+  if (nn) flush();
+  return s;
+}
+
 }  // namespace dqn

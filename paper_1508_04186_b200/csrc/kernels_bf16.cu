@@ -622,9 +622,26 @@ __global__ void __launch_bounds__(128) tc_pair_kernel(TcPairArgs a) {
   } else {
     pdl_sync();  // the TD head's per-sample outputs come from the predecessor
     if (bx == a.tiles0 + a.tiles1) st_stamp_here(ST_P5, 0);
-    const int n = head_finish_elems(a.head);
-    for (int e = (bx - a.tiles0 - a.tiles1) * 128 + threadIdx.x; e < n; e += (gridDim.x - a.tiles0 - a.tiles1) * 128)
-      head_finish_elem(a.head, e);
+    const HeadArgs& h = a.head;
+    const int n = head_finish_elems(h);
+    // the samples' actions and dQ staged in shared memory (this CTA's operand area is unused)
+    int* s_act = reinterpret_cast<int*>(smem);
+    float* s_dq = reinterpret_cast<float*>(smem) + h.b;
+    for (int j = threadIdx.x; j < h.b; j += 128) {
+      s_act[j] = h.s_act[j];
+      s_dq[j] = h.s_dq[j];
+    }
+    __syncthreads();
+    const bool warp_rows = h.H % 32 == 0;  // a warp's 32 dW_o elements share one action
+    const float* h0 = h.fc_partial ? h.act_out[0] : h.act[0];
+    for (int e = (bx - a.tiles0 - a.tiles1) * 128 + threadIdx.x; e < n; e += (gridDim.x - a.tiles0 - a.tiles1) * 128) {
+      if (warp_rows && e - (threadIdx.x & 31) + 31 < h.A * h.H) {  // the whole warp in the dW_o rows
+        const int a_ = e / h.H, u = e % h.H;
+        h.grad[h.w_off + e] += head_finish_dwo_warp(h, h0, s_act, s_dq, a_, u);
+      } else {
+        head_finish_elem(h, e);
+      }
+    }
     if (bx == a.tiles0 + a.tiles1) st_stamp_here(ST_P5, 2);
   }
   st_stamp(ST_FC_BWD, 2);
