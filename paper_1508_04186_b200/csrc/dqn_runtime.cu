@@ -353,8 +353,8 @@ static int validate_cfg(const dqn_config* c, NetShape* net, std::string* why) {
       !(c->replay_prio_eps >= 0.0 && std::isfinite(c->replay_prio_eps))) {
     *why = "replay_prio_alpha must be 0, 0.5 or 1 and replay_prio_eps finite >= 0 (A41)"; return DQN_EINVAL;
   }
-  if (c->replay_prio_alpha != 0.0 && c->replay_capacity > (1LL << 30)) {
-    *why = "prioritized replay: capacity <= 2^30"; return DQN_EINVAL;
+  if (c->replay_prio_alpha != 0.0 && (c->replay_capacity > (1LL << 30) || c->minibatch > 8192)) {
+    *why = "prioritized replay: capacity <= 2^30 and b <= 8192"; return DQN_EINVAL;
   }
   if (!(c->rms_decay >= 0.0 && c->rms_decay < 1.0) || !(c->rms_eps >= 0.0) || !(c->lr >= 0.0) ||
       !std::isfinite(c->gamma) || !(c->err_clip >= 0.0)) {

@@ -8,8 +8,8 @@
 //   prio_sample  : warp per draw; t_j = ((j + u_j) / b) S (stratified), then a fixed-order scan of each node's
 //                  32 children from the root down. Every compare / add is an explicit round-to-nearest fp32 op
 //                  in the oracle's order (oracle/prio.py), so draws are bit-identical given the same leaves.
-//   prio_update  : one CTA after the TD head: p_j = (|delta_j| + eps)^alpha into the slot's leaf (the largest j of
-//                  duplicates wins), the max priority, then the changed nodes level by level.
+//   prio_update  : one CTA after the TD head: p_j = (|delta_j| + eps)^alpha into the slot's leaf, the max priority,
+//                  then the changed nodes level by level, 8 per warp with their loads in flight.
 //   prio_push    : one CTA after a Store: the stored slots' leaves = the max priority, their ancestors rebuilt.
 #include "dqn_internal.h"
 #include "pdl.cuh"
@@ -80,17 +80,20 @@ __global__ void __launch_bounds__(256) prio_sample_kernel(PrioTree t, int b, uns
   if (lane == 0) idx[j] = (int)node;
 }
 
+// Duplicates of a slot in one minibatch carry the same transition and theta, hence the same delta and the same
+// priority: every draw writes its leaf (the rule "the largest j writes" of A41 is unobservable), and a tree node
+// shared by several draws is rebuilt once when the draws are sorted (the stratified descent is monotone in j,
+// so equal parents are adjacent) and harmlessly more than once otherwise.
 __global__ void __launch_bounds__(1024) prio_update_kernel(PrioTree t, int b, const int* idx, const float* delta,
                                                            int alpha_half, float eps, float* maxp) {
+  extern __shared__ int s_idx[];  // [b]
   __shared__ float s_max[32];
   pdl_sync();  // delta and idx of this step (the TD head, the sampler)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
   float m = 0.0f;
   for (int j = tid; j < b; j += blockDim.x) {
     const int i = idx[j];
-    bool later = false;
-    for (int k = j + 1; k < b && !later; ++k) later = idx[k] == i;
-    if (later) continue;  // a later sample of the same slot writes it
+    s_idx[j] = i;
     float p = __fadd_rn(fabsf(delta[j]), eps);
     if (alpha_half) p = __fsqrt_rn(p);
     t.node[t.off[0] + i] = p;
@@ -105,14 +108,26 @@ __global__ void __launch_bounds__(1024) prio_update_kernel(PrioTree t, int b, co
     for (int w = 0; w < nw; ++w) mm = fmaxf(mm, s_max[w]);
     *maxp = mm;
   }
+  constexpr int PW = 8;  // parents per warp and round: their 8 coalesced child loads in flight together
   for (int l = 1; l <= t.K; ++l) {
-    // warp per changed node; a node shared by several draws is rebuilt by the first of them only
-    for (int j = warp; j < b; j += nw) {
-      const long long i = (long long)idx[j] >> (5 * l);
-      bool earlier = false;
-      for (int k = lane; k < j && !earlier; k += 32) earlier = ((long long)idx[k] >> (5 * l)) == i;
-      if (__any_sync(kFull, earlier)) continue;
-      rebuild_node(t, l, i);
+    const int sh = 5 * l;
+    for (int j0 = warp * PW; j0 < b; j0 += nw * PW) {
+      float c[PW];
+      long long par[PW];
+      bool need[PW];
+#pragma unroll
+      for (int q = 0; q < PW; ++q) {
+        const int j = j0 + q;
+        par[q] = j < b ? (long long)s_idx[j] >> sh : -1;
+        need[q] = j < b && (j == 0 || ((long long)s_idx[j - 1] >> sh) != par[q]);
+        c[q] = need[q] ? __ldcg(t.node + t.off[l - 1] + par[q] * 32 + lane) : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < PW; ++q) {
+        if (!need[q]) continue;
+        const float sum = butterfly32(c[q]);
+        if (lane == 0) t.node[t.off[l] + par[q]] = sum;
+      }
     }
     __syncthreads();
   }
@@ -146,7 +161,8 @@ void launch_prio_sample(const PrioTree& t, int b, unsigned long long seed, unsig
 
 void launch_prio_update(const PrioTree& t, int b, const int* idx, const float* delta, int alpha_half, float eps,
                         float* maxp, cudaStream_t st) {
-  launch_pdl(prio_update_kernel, dim3(1), dim3(1024), 0, st, t, b, idx, delta, alpha_half, eps, maxp);
+  launch_pdl(prio_update_kernel, dim3(1), dim3(1024), (size_t)b * sizeof(int), st, t, b, idx, delta, alpha_half, eps,
+             maxp);
 }
 
 void launch_prio_push(const PrioTree& t, long long cap, long long first, long long m, const float* maxp,
