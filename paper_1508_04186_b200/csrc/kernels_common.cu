@@ -2,6 +2,8 @@
 //   a1  sampler (counter-based Philox4x32-10, integer-only index mapping)
 //   push path (validation + FIFO ring writes, "Store experience" of Alg. 1)
 //   a12 fused RMSProp shard update of Alg. 2
+#include <algorithm>
+
 #include "dqn_internal.h"
 #include "pdl.cuh"
 #include "philox.cuh"
@@ -120,64 +122,97 @@ void launch_push_canonical(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring_a, f
 // front, there is no loop-carried latency and no fence. The round counter n is
 // mirrored by the host (deterministic schedule); non-finite elements are counted
 // (sticky) with one atomic per offending thread.
-__global__ void rmsprop_kernel(float* __restrict__ theta, float* __restrict__ r, float* __restrict__ g, long long n,
-                               float inv_div, float lr, float rho, float omr, float eps, float* __restrict__ pub_f32,
-                               __nv_bfloat16* __restrict__ pub_bf16, DevCounters* ctr, int zero_g, long long img_off,
-                               long long w1_off, long long w2_off, float* __restrict__ g_snap,
-                               const int2* __restrict__ pack_map, long long pack_n, long long pack_off) {
-  st_stamp(ST_UPDATE, 0);
-  pdl_sync();
-  st_stamp(ST_UPDATE, 1);
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n / 4) return;
-  const float4 g4 = reinterpret_cast<const float4*>(g)[i];
-  float4 t4 = reinterpret_cast<const float4*>(theta)[i];
-  float4 r4 = reinterpret_cast<const float4*>(r)[i];
-  if (zero_g) reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (g_snap) reinterpret_cast<float4*>(g_snap)[i] = g4;  // cfg.keep_grad (diagnostic)
+struct RmsArgs {
+  float* theta;
+  float* r;
+  float* g;
+  long long n;
+  float inv_div, lr, rho, omr, eps;
+  float* pub_f32;
+  __nv_bfloat16* pub_bf16;
+  int zero_g;
+  long long img_off, w1_off, w2_off;
+  float* g_snap;
+  const int2* pack_map;
+  long long pack_n, pack_off;
+};
+
+// one float4 of the update (loads done by the caller); returns the non-finite count
+__device__ __forceinline__ unsigned rmsprop_vec(const RmsArgs& u, long long i, float4 g4, float4 t4, float4 r4) {
+  if (u.zero_g) reinterpret_cast<float4*>(u.g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (u.g_snap) reinterpret_cast<float4*>(u.g_snap)[i] = g4;  // cfg.keep_grad (diagnostic)
   float tv[4] = {t4.x, t4.y, t4.z, t4.w};
   float rv[4] = {r4.x, r4.y, r4.z, r4.w};
   const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
   unsigned bad = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const float gb = gv[q] * inv_div;  // mean over N * n_push gradients (A7, A8)
+    const float gb = gv[q] * u.inv_div;  // mean over N * n_push gradients (A7, A8)
     if (isfinite(gb)) {
-      const float rr = rho * rv[q] + omr * gb * gb;
+      const float rr = u.rho * rv[q] + u.omr * gb * gb;
       rv[q] = rr;
-      tv[q] = tv[q] - lr * gb * rsqrtf(rr + eps);
+      tv[q] = tv[q] - u.lr * gb * rsqrtf(rr + u.eps);
     } else {
       ++bad;
     }
   }
   t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);
-  reinterpret_cast<float4*>(theta)[i] = t4;
-  reinterpret_cast<float4*>(r)[i] = make_float4(rv[0], rv[1], rv[2], rv[3]);
-  if (pub_f32) reinterpret_cast<float4*>(pub_f32)[i] = t4;
-  if (pub_bf16) {
+  reinterpret_cast<float4*>(u.theta)[i] = t4;
+  reinterpret_cast<float4*>(u.r)[i] = make_float4(rv[0], rv[1], rv[2], rv[3]);
+  if (u.pub_f32) reinterpret_cast<float4*>(u.pub_f32)[i] = t4;
+  if (u.pub_bf16) {
     uint2 o;
     __nv_bfloat162 lo = __floats2bfloat162_rn(t4.x, t4.y), hi = __floats2bfloat162_rn(t4.z, t4.w);
     o.x = *reinterpret_cast<uint32_t*>(&lo);
     o.y = *reinterpret_cast<uint32_t*>(&hi);
-    reinterpret_cast<uint2*>(pub_bf16)[i] = o;
-    if (pack_map && 4 * i < pack_n) {  // the generic path's packed conv images (gpack_kernel, fused at N = 1)
+    reinterpret_cast<uint2*>(u.pub_bf16)[i] = o;
+    if (u.pack_map && 4 * i < u.pack_n) {  // the generic path's packed conv images (gpack_kernel, fused at N = 1)
       const float tq[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (4 * i + q >= pack_n) break;
-        const int2 d = pack_map[4 * i + q];
+        if (4 * i + q >= u.pack_n) break;
+        const int2 d = u.pack_map[4 * i + q];
         const __nv_bfloat16 v = __float2bfloat16_rn(tq[q]);
-        if (d.x >= 0) pub_bf16[pack_off + d.x] = v;
-        if (d.y >= 0) pub_bf16[pack_off + d.y] = v;
+        if (d.x >= 0) u.pub_bf16[u.pack_off + d.x] = v;
+        if (d.y >= 0) u.pub_bf16[u.pack_off + d.y] = v;
       }
     }
-    if (img_off >= 0 && 4 * i + 3 >= min(w1_off, w2_off) && 4 * i < max(w1_off, w2_off) + kW2Elems) {
+    if (u.img_off >= 0 && 4 * i + 3 >= min(u.w1_off, u.w2_off) && 4 * i < max(u.w1_off, u.w2_off) + kW2Elems) {
       const float tq[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int sl = wimg_slot(4 * i + q, w1_off, w2_off);
-        if (sl >= 0) pub_bf16[img_off + sl] = __float2bfloat16_rn(tq[q]);
+        const int sl = wimg_slot(4 * i + q, u.w1_off, u.w2_off);
+        if (sl >= 0) u.pub_bf16[u.img_off + sl] = __float2bfloat16_rn(tq[q]);
       }
+    }
+  }
+  return bad;
+}
+
+// grid-stride over the float4s, RMS_VECS of them per thread and round with all their loads issued first (large
+// vectors run on a few waves of resident threads instead of one thread per float4)
+constexpr int RMS_VECS = 4;
+__global__ void __launch_bounds__(256) rmsprop_kernel(RmsArgs u, DevCounters* ctr) {
+  st_stamp(ST_UPDATE, 0);
+  pdl_sync();
+  st_stamp(ST_UPDATE, 1);
+  const long long n4 = u.n / 4, stride = (long long)gridDim.x * blockDim.x;
+  unsigned bad = 0;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += stride * RMS_VECS) {
+    float4 g4[RMS_VECS], t4[RMS_VECS], r4[RMS_VECS];
+#pragma unroll
+    for (int k = 0; k < RMS_VECS; ++k) {
+      const long long i = i0 + k * stride;
+      if (i < n4) {
+        g4[k] = reinterpret_cast<const float4*>(u.g)[i];
+        t4[k] = reinterpret_cast<const float4*>(u.theta)[i];
+        r4[k] = reinterpret_cast<const float4*>(u.r)[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < RMS_VECS; ++k) {
+      const long long i = i0 + k * stride;
+      if (i < n4) bad += rmsprop_vec(u, i, g4[k], t4[k], r4[k]);
     }
   }
   if (bad) atomicAdd(&ctr->nonfinite, bad);
@@ -188,9 +223,11 @@ void launch_rmsprop(float* theta, float* r, float* g, long long n, float div, fl
                     float eps, float* pub_f32, __nv_bfloat16* pub_bf16, DevCounters* ctr, int zero_g,
                     cudaStream_t st, long long img_off, long long w1_off, long long w2_off, float* g_snap,
                     const int2* pack_map, long long pack_n, long long pack_off) {
-  const int blocks = (int)((n / 4 + 255) / 256);
-  launch_pdl(rmsprop_kernel, dim3(blocks < 1 ? 1 : blocks), dim3(256), 0, st, theta, r, g, n, 1.0f / div, lr, rho, omr,
-             eps, pub_f32, pub_bf16, ctr, zero_g, img_off, w1_off, w2_off, g_snap, pack_map, pack_n, pack_off);
+  // one float4 per thread up to 4 resident waves of 256-thread CTAs, a grid-stride loop beyond
+  const long long blocks = std::min<long long>((n / 4 + 255) / 256, 4LL * 148);
+  const RmsArgs u{theta, r, g, n, 1.0f / div, lr, rho, omr, eps, pub_f32, pub_bf16, zero_g, img_off, w1_off, w2_off,
+                  g_snap, pack_map, pack_n, pack_off};
+  launch_pdl(rmsprop_kernel, dim3((unsigned)(blocks < 1 ? 1 : blocks)), dim3(256), 0, st, u, ctr);
 }
 
 
