@@ -36,7 +36,7 @@ def run(conc_bwd, split_update, b):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("b", [32, 512])
+@pytest.mark.parametrize("b", [32, 144, 512])
 def test_graph_branches_are_bit_identical(b):
     ref = run(0, 0, b)
     for conc, split in ((1, 1), (1, 0), (0, 1)):

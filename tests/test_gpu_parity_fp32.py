@@ -58,9 +58,11 @@ def test_sampled_indices_bit_exact_with_wraparound():
     g.close()
 
 
-@pytest.mark.parametrize("kw", [dict(), TINY_KW], ids=["mnih", "tiny"])
-def test_first_step_gradient(kw):
-    dc, on, oc = nets(minibatch=32, replay_capacity=1000, **kw)
+@pytest.mark.parametrize("kw,b", [(dict(), 32), (TINY_KW, 32), (dict(), 1), (dict(), 37), (TINY_KW, 37)],
+                         ids=["mnih", "tiny", "mnih-b1", "mnih-b37", "tiny-b37"])
+def test_first_step_gradient(kw, b):
+    """b = 1 (a single sample) and b = 37 (a 32-sample tile plus a ragged 5) as well as the configs' 32."""
+    dc, on, oc = nets(minibatch=b, replay_capacity=1000, **kw)
     g, theta0, rp = make(dc, on, 300, 21)
     g.train(1)
     grad = g.params(D.PARAMS_GRAD)

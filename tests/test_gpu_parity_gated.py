@@ -43,9 +43,13 @@ def make(dc, on, n_items, seed, theta_seed, r_scale=1.0, out_std=0.5):
 
 
 CASES = [(dict(), 32), (dict(), 256), (dict(fcs=(128,)), 32), (dict(fcs=(512,)), 32), (dict(fcs=(2048,)), 32),
-         (SCALED, 32), (SCALED, 512), (dict(SCALED, fcs=(1024,)), 32), (dict(SCALED, fcs=(2048,)), 64)]
+         (SCALED, 32), (SCALED, 512), (dict(SCALED, fcs=(1024,)), 32), (dict(SCALED, fcs=(2048,)), 64),
+         (dict(), 16), (dict(), 80), (dict(), 144), (SCALED, 16), (SCALED, 144)]
 IDS = ["mnih-b32", "mnih-b256", "mnih-fc128", "mnih-fc512", "mnih-fc2048", "scaled-b32", "scaled-b512",
-       "scaled-fc1024", "scaled-fc2048"]  # fc > 512: the FC backward on the K-pipelined GEMM (BJ.c5's sweep)
+       "scaled-fc1024", "scaled-fc2048",  # fc > 512: the FC backward on the K-pipelined GEMM (BJ.c5's sweep)
+       # ragged minibatches: half a 32-sample head tile; 80 = 2.5 head tiles; 144 = one 128-row GEMM M tile plus
+       # a 16-row tail (and the cluster-multicast TD head, b > 128)
+       "mnih-b16", "mnih-b80", "mnih-b144", "scaled-b16", "scaled-b144"]
 
 
 @pytest.mark.parametrize("kw,b", CASES, ids=IDS)

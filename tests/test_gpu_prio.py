@@ -19,12 +19,15 @@ SCALED = dict(convs=((32, 8, 4), (64, 4, 2), (64, 3, 1)), fcs=(512,), n_actions=
 CAP = 1500  # K = 3 levels above 32768 leaves; the second push wraps the ring
 
 
-@pytest.mark.parametrize("precision,kw,alpha", [(D.FP32, TINY_KW, 1.0), (D.FP32, TINY_KW, 0.5),
-                                                (D.BF16, {}, 1.0), (D.BF16, SCALED, 0.5)],
-                         ids=["fp32-a1", "fp32-a05", "bf16-mnih-a1", "bf16-scaled-a05"])
-def test_prioritized_replay_teacher_forced(precision, kw, alpha):
+@pytest.mark.parametrize("precision,kw,alpha,b", [(D.FP32, TINY_KW, 1.0, 32), (D.FP32, TINY_KW, 0.5, 32),
+                                                  (D.BF16, {}, 1.0, 32), (D.BF16, SCALED, 0.5, 32),
+                                                  (D.FP32, TINY_KW, 0.5, 37), (D.BF16, {}, 1.0, 144)],
+                         ids=["fp32-a1", "fp32-a05", "bf16-mnih-a1", "bf16-scaled-a05", "fp32-a05-b37",
+                              "bf16-mnih-a1-b144"])
+def test_prioritized_replay_teacher_forced(precision, kw, alpha, b):
+    """b = 37 and 144: strata that are not a multiple of the 32-draw warp scan (a ragged last warp)."""
     eps = 1.0 if alpha == 1.0 else 0.01  # alpha = 1: every written priority exceeds the initial max (1)
-    dc, on, _ = nets(minibatch=32, replay_capacity=CAP, precision=precision, target_sync=3, lr=1e-3,
+    dc, on, _ = nets(minibatch=b, replay_capacity=CAP, precision=precision, target_sync=3, lr=1e-3,
                      replay_prio_alpha=alpha, replay_prio_eps=eps, **kw)
     theta0 = he_theta(on, 5)
     g = D.DQN(dc, init_params=theta0)
