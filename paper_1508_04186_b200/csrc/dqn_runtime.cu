@@ -2390,8 +2390,8 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
     if (cudaMemcpy(t, ctx->sra.trace, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
       // intervals: barrier A, work, release (block 0); first block start -> last release;
       // block 0 release -> next step past pdl_sync; acquire spin
-      double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      int n = 0;
+      double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, sc[4] = {0, 0, 0, 0};
+      int n = 0, nc = 0;
       for (int r = 0; r < 63; ++r) {  // skip the newest slot (its next-step stamps are not there yet)
         const unsigned long long* q = t + r * 16;
         if (!q[0] || q[3] <= q[0] || !q[7] || q[6] < q[3] || q[4] == ~0ull) continue;
@@ -2399,6 +2399,10 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
         s[3] += (double)(q[5] - q[4]); s[4] += (double)(q[6] - q[3]); s[5] += (double)(q[7] - q[6]);
         if (q[8] && q[10]) {  // the next step's first kernel (bf16): entry, gather landed, past pdl_sync
           s[6] += (double)q[8] - (double)q[5]; s[7] += (double)(q[9] - q[8]); s[8] += (double)(q[10] - q[9]);
+        }
+        if (q[13] && q[14] && q[14] != ~0ull) {  // spread of barrier A over the blocks; conv blocks' work and release
+          sc[0] += (double)q[14] - (double)q[1]; sc[1] += (double)q[13] - (double)q[1];
+          if (q[11] && q[12]) { sc[2] += (double)q[12] - (double)q[1]; sc[3] += (double)q[11] - (double)q[1]; ++nc; }
         }
         ++n;
       }
@@ -2415,6 +2419,10 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
                 " all blocks %.2f us; release -> next kernel %.2f us; acquire %.2f us\n",
                 ctx->rank, n, s[0] / n / 1e3, s[1] / n / 1e3, s[2] / n / 1e3, s[3] / n / 1e3, s[4] / n / 1e3,
                 s[5] / n / 1e3);
+      if (n)
+        fprintf(stderr, "[dqn rank %d] relative to block 0 past barrier A: first / last block past it %.2f / %.2f us;"
+                " conv blocks' work done %.2f us, conv release %.2f us (%d rounds)\n", ctx->rank, sc[0] / n / 1e3,
+                sc[1] / n / 1e3, nc ? sc[2] / nc / 1e3 : 0.0, nc ? sc[3] / nc / 1e3 : 0.0, nc);
       if (n && ctx->bf16)
         fprintf(stderr, "[dqn rank %d] next fwd: entry - last round block %.2f us, gather %.2f us, expand+pdl_sync %.2f us\n",
                 ctx->rank, s[6] / n / 1e3, s[7] / n / 1e3, s[8] / n / 1e3);

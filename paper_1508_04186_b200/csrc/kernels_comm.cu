@@ -55,7 +55,10 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   const unsigned long long T = a.ctr->T;
   const unsigned long long round_idx = T / (unsigned long long)a.n_push;
   TRACE(0);
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[((round_idx + 1) % 64) * 16 + 4] = ~0ull;
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    a.trace[((round_idx + 1) % 64) * 16 + 4] = ~0ull;
+    a.trace[((round_idx + 1) % 64) * 16 + 14] = ~0ull;
+  }
   if (a.trace && threadIdx.x == 0) atomicMin(a.trace + (round_idx % 64) * 16 + 4, gtimer());
   // ---- barrier A
   if (threadIdx.x == 0) {
@@ -67,6 +70,10 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   }
   __syncthreads();
   TRACE(1);
+  if (a.trace && threadIdx.x == 0) {  // 13 / 14: last / first block past barrier A
+    atomicMax(a.trace + (round_idx % 64) * 16 + 13, gtimer());
+    atomicMin(a.trace + (round_idx % 64) * 16 + 14, gtimer());
+  }
   // ---- reduce (rank order) + RMSProp + deliver, 16-byte vectors, grid-stride over the owned shard
   const long long n4 = a.shard / 4;
   const long long base = (long long)a.rank * a.shard;
@@ -150,12 +157,14 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   // every peer (done_c), so the next step's conv forward can start before this round ends
   const unsigned long long nb_c = (unsigned long long)((a.conv4 + blockDim.x - 1) / blockDim.x);
   if (threadIdx.x == 0 && blockIdx.x < nb_c) {
+    if (a.trace) atomicMax(a.trace + (round_idx % 64) * 16 + 12, gtimer());  // 12: last conv block's work done
     unsigned long long old;
     asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(a.my_join_c), "l"(1ull) : "memory");
     if (old == round_idx * nb_c - 1) {
       fence_acq_rel_sys();
       for (int p = 0; p < a.world; ++p)
         asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(a.done_c[p]), "l"(1ull) : "memory");
+      if (a.trace) a.trace[(round_idx % 64) * 16 + 11] = gtimer();  // 11: conv parameters released
     }
   }
   if (threadIdx.x == 0) {
