@@ -189,6 +189,7 @@ struct ServerRoundArgs {
   long long conv4;
   unsigned long long* done_c[kMaxWorld];        // every rank's conv-release counter
   unsigned long long* my_join_c;                // local join counter of the conv blocks
+  int conv_per_block = 256;                     // conv-prefix float4s per block (1..256)
 };
 void launch_server_round(const ServerRoundArgs& a, cudaStream_t st);
 // the acquire half of the round's second barrier, run at the start of the next step
@@ -252,7 +253,7 @@ void launch_fetch_pack(const float* master, const FetchRecord& f, uint8_t* send,
 void launch_fetch_unpack(const uint8_t* recv, const FetchRecord& f, float* theta, __nv_bfloat16* theta_bf16,
                          cudaStream_t st);
 void launch_widen_range(const __nv_bfloat16* src, float* dst, long long lo, long long hi, cudaStream_t st);
-int server_round_blocks(long long shard);
+int server_round_blocks(long long shard, long long conv4, int conv_per_block);
 
 // bf16 tensor-core path, Mnih-2013 net (kernels_bf16.cu)
 struct FwdConvArgs {

@@ -603,6 +603,7 @@ static int setup_fused_comm(dqn_ctx* ctx) {
     ctx->acq.done_c = ctx->done + 2;
     ctx->acq.n_c = (int)std::min<long long>(N, (kBwdPart + ctx->shard - 1) / ctx->shard);
     ctx->acq.conv_first = 1;
+    a.conv_per_block = 64;  // the conv prefix's scattered weight-image stores spread over 4x more blocks (DESIGN 6a)
   }
   const char* tr = getenv("DQN_TRACE_COMM");
   if (tr && atoi(tr)) {

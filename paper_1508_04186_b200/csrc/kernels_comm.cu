@@ -78,7 +78,18 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   const long long n4 = a.shard / 4;
   const long long base = (long long)a.rank * a.shard;
   unsigned bad = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+  // one float4 per thread; with a conv prefix (conv4 > 0) its float4s are spread conv_per_block per block over the
+  // first nb_c blocks (the weight image's scattered peer stores then come from nb_c SMs instead of conv4 / 256),
+  // the rest of those blocks and all later blocks take the remaining float4s in order
+  const int cpb = a.conv_per_block;
+  const long long nb_c = (a.conv4 + cpb - 1) / cpb;
+  long long i;
+  if ((long long)blockIdx.x < nb_c)
+    i = (int)threadIdx.x < cpb ? (blockIdx.x * (long long)cpb + threadIdx.x < a.conv4 ? blockIdx.x * (long long)cpb + threadIdx.x : n4)
+                               : a.conv4 + blockIdx.x * (long long)(256 - cpb) + (threadIdx.x - cpb);
+  else
+    i = a.conv4 + nb_c * (256 - cpb) + (blockIdx.x - nb_c) * 256LL + threadIdx.x;
+  if (i < n4) {
     // all N peer loads in flight at once (NVLink latency ~1-2 us), then summed in rank order
     float4 v[kMaxWorld];
 #pragma unroll
@@ -155,12 +166,11 @@ __global__ void __launch_bounds__(256) server_round_kernel(ServerRoundArgs a) {
   // conv-first delivery: the blocks holding conv parameters (the first nb_c blocks of the owner(s) of
   // the canonical prefix) first join their own counter; the last of them releases the conv weights to
   // every peer (done_c), so the next step's conv forward can start before this round ends
-  const unsigned long long nb_c = (unsigned long long)((a.conv4 + blockDim.x - 1) / blockDim.x);
-  if (threadIdx.x == 0 && blockIdx.x < nb_c) {
+  if (threadIdx.x == 0 && (long long)blockIdx.x < nb_c) {
     if (a.trace) atomicMax(a.trace + (round_idx % 64) * 16 + 12, gtimer());  // 12: last conv block's work done
     unsigned long long old;
     asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(a.my_join_c), "l"(1ull) : "memory");
-    if (old == round_idx * nb_c - 1) {
+    if (old == round_idx * (unsigned long long)nb_c - 1) {
       fence_acq_rel_sys();
       for (int p = 0; p < a.world; ++p)
         asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(a.done_c[p]), "l"(1ull) : "memory");
@@ -192,14 +202,17 @@ void launch_fused_round_acquire(const FusedAcquire& f, cudaStream_t st) {
   launch_pdl(fused_round_acquire_kernel, dim3(148), dim3(256), 0, st, f);
 }
 
-// one 16-byte vector per thread (no cross-block waits inside the kernel, so no residency bound)
-int server_round_blocks(long long shard) {
-  const long long b = (shard / 4 + 255) / 256;
+// one 16-byte vector per thread (no cross-block waits inside the kernel, so no residency bound); the conv prefix
+// spread cpb per block over the first blocks
+int server_round_blocks(long long shard, long long conv4, int cpb) {
+  const long long n4 = shard / 4, nb_c = (conv4 + cpb - 1) / cpb;
+  const long long rest = std::max(0LL, n4 - conv4 - nb_c * (256 - cpb));
+  const long long b = nb_c + (rest + 255) / 256;
   return (int)(b < 1 ? 1 : b);
 }
 
 void launch_server_round(const ServerRoundArgs& a, cudaStream_t st) {
-  launch_pdl(server_round_kernel, dim3(server_round_blocks(a.shard)), dim3(256), 0, st, a);
+  launch_pdl(server_round_kernel, dim3(server_round_blocks(a.shard, a.conv4, a.conv_per_block)), dim3(256), 0, st, a);
 }
 
 // ---- NCCL fetch on the bf16 path (a13, n_fetch > 1 or DQN_ASYNC): one all-gather of a per-rank record
