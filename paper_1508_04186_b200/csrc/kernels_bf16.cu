@@ -1031,11 +1031,11 @@ __device__ __forceinline__ float bwd_part_sum(int e, const BwdConvArgs& a) {
 }
 
 // Sum the per-image partials in image order (deterministic) and scatter into G's canonical layout.
-// Large b: warp w of the CTA sums images [64 w, 64 w + 64) of 32 consecutive entries in image order (two rounds
+// Large b: warp w of the CTA sums images [32 w, 32 w + 32) of 32 consecutive entries in image order (one round
 // of 32 loads in flight instead of b / 32 serial rounds), then the CTA adds the warps' subtotals in warp order:
-// a fixed two-level order, deterministic run to run. One warp per CTA (b <= 64) is the plain image order.
+// a fixed two-level order, deterministic run to run. One warp per CTA (b <= 32) is the plain image order.
 __global__ void bwd_reduce_kernel(BwdConvArgs a) {
-  __shared__ float s_sub[4][32];
+  __shared__ float s_sub[8][32];
   st_stamp(ST_BWD_REDUCE, 0);
   pdl_sync();
   st_stamp(ST_BWD_REDUCE, 1);
@@ -1065,7 +1065,9 @@ __global__ void bwd_reduce_kernel(BwdConvArgs a) {
 
 void launch_bwd_conv_bf16(const BwdConvArgs& a, cudaStream_t st, bool with_reduce) {
   launch_pdl(bwd_conv_bf16_kernel, dim3(a.n), dim3(128), BWD_SMEM, st, a, ReduceUpdateArgs{});
-  const int nw = std::min(4, std::max(1, (a.n + 63) / 64));  // warps (image groups of >= 64) per 32 entries
+  // warps per 32 entries: image groups of 32, one batch of 32 loads in flight per thread (BJ.configs[3], b = 256:
+  // 84.6 -> 82.0 us/step against groups of 64, which took two dependent batches; groups of 16 measured no better)
+  const int nw = std::min(8, std::max(1, (a.n + 31) / 32));
   if (with_reduce) launch_pdl(bwd_reduce_kernel, dim3(cdiv(BWD_PART, 32)), dim3(32 * nw), 0, st, a);
 }
 
