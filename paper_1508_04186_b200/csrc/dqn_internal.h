@@ -328,6 +328,7 @@ struct TcGemmArgs {
   int store;                // TC_EPI_ACCUM: 1 = C = D (C known to be zero / overwritten), 0 = C += D
   int hwc_HW, hwc_C;        // TC_EPI_MASK_T: write feature m = c*HW + p to p*C + c (NHWC dZ), 0: off
   FusedAcquire acq;         // conv-first delivery (acq.conv_first): the FC forward acquires the round
+  int bulk_accum;           // TC_EPI_ACCUM: rows go out as bulk (reduce-)copies from shared memory
 };
 enum { TC_EPI_ACCUM = 0, TC_EPI_FC_FWD = 1, TC_EPI_MASK_T = 2 };
 struct BwdConvArgs {

@@ -1648,6 +1648,11 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   gw.epi = TC_EPI_ACCUM; gw.C[0] = ctx->grad + F.w_off; gw.ldc = F.D;
   gw.pre_a = 0; gw.pre_b = 1;  // dH comes from the predecessor (head_sample), a2 from the conv forward
   gw.store = c.n_push == 1;     // n_push = 1: this step's gradient is the whole accumulator (A8)
+  {  // n_push > 1: the tile rows go out as bulk fp32 reduce-adds (BJ.configs[3]: 82.3 -> 81.0 us/step); at
+     // n_push = 1 the plain stores measured the same either way (32.4-33.6 vs 33.0-33.1 us/step), so they stay
+    const char* ba = getenv("DQN_BULK_ACCUM");
+    gw.bulk_accum = ba ? atoi(ba) : c.n_push > 1;
+  }
   TcGemmArgs gx{};
   gx.A[0] = ctx->theta_local_bf16 + F.w_off; gx.lda = F.D; gx.a_mn = 1;
   gx.B[0] = ctx->dh_bf16; gx.ldb = F.H; gx.b_mn = 0;

@@ -513,9 +513,19 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
 #pragma unroll
       for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(row + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     }
-    __syncthreads();
     const int nv = bn / 4;
     const bool vec = (a.ldc % 4) == 0 && ((reinterpret_cast<uintptr_t>(a.C[g]) & 15) == 0);
+    const int ncols = min(bn, a.N - n0);
+    if (a.bulk_accum && vec && ncols % 4 == 0) {
+      // one bulk transfer per tile row: C += row (or C = row) done by the TMA unit at L2, fp32 add with RN
+      // (the same rounding as the register path below), no load round trip through the SM
+      fence_async_smem();
+      __syncthreads();
+      const int r = threadIdx.x;
+      if (m0 + r < a.M) bulk_s2g_f32(a.C[g] + (long long)(m0 + r) * a.ldc + n0, sD + r * ld, (uint32_t)ncols * 4, !a.store);
+      goto epi_done;
+    }
+    __syncthreads();
     constexpr int BATCH = 12;  // loads of a batch are all issued before any store (C may alias nothing else,
                                // but the compiler cannot know that)
     for (int e0 = threadIdx.x; e0 < 128 * nv; e0 += 128 * BATCH) {
@@ -587,6 +597,7 @@ __device__ __forceinline__ void tc_gemm_tile(const TcGemmArgs& a, int tile, int 
       }
     }
   }
+epi_done:
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 256);

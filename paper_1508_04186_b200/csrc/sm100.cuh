@@ -44,6 +44,18 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// one contiguous shared -> global bulk transfer (16-byte aligned, size a multiple of 16), plain store or fp32
+// reduce-add (RN, done at L2); waits until the transfer is complete
+__device__ __forceinline__ void bulk_s2g_f32(float* dst, const float* src, uint32_t bytes, bool add) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(src);
+  if (add)
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst), "r"(s), "r"(bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(s), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // expect `bytes` of async-proxy traffic on the barrier and arrive once
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
