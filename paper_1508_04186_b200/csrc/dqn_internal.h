@@ -273,6 +273,9 @@ struct FwdConvArgs {
   long long slot_stride;           // bytes between replay slots (28,224, or 35,280 with frame dedup)
   int late;                        // 1: sample + gather after the PDL wait (the predecessor wrote the ring)
   const int* idx_in;               // prioritized replay: the slots prio_sample_kernel drew (nullptr: a1's sampler)
+  const struct StoreCtl* store_ctl; // non-null (with late = 0): the predecessor is this step's in-graph Store; the
+  long long cap;                   // replay size and the stored slot come from StoreCtl, and only a CTA that drew
+                                   // the slot being stored waits for the Store before its gather
 };
 // dqn_store_and_train on the bf16 Mnih path: Alg. 1's Store as the first kernel of every step of the
 // replayed step graph. The graph is fixed, so the chunk of transitions and its position come from here

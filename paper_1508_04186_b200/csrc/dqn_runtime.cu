@@ -1594,6 +1594,15 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   fa.img_off = ctx->img_off;
   fa.slot_stride = ctx->slot_stride;
   fa.late = store ? 1 : 0;
+  {  // N = 1 Store steps: the gather of every slot but the one being stored overlaps the Store (the slot draw
+     // needs only StoreCtl and T, both older than the Store)
+    const char* eg = getenv("DQN_STORE_EARLY_GATHER");
+    if (store && ctx->world == 1 && !ctx->dedup && !ctx->prio && !(eg && atoi(eg) == 0)) {
+      fa.late = 0;
+      fa.store_ctl = ctx->store_ctl;
+      fa.cap = ctx->cap;
+    }
+  }
   if (ctx->prio) {  // the draws come from the sum tree: the forward waits for them (A41)
     enqueue_prio_sample(ctx, st);
     fa.idx_in = ctx->idx;

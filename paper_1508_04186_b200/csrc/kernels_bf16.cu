@@ -82,6 +82,9 @@ __global__ void push_s2d_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring
 // read the ring) completed; the conv forward that follows samples and gathers after its own PDL wait.
 __global__ void store_step_kernel(StoreArgs a) {
   pdl_wait();
+  // the successor may launch now: the previous step is complete, and the forward reads this kernel's writes only
+  // after its own griddepcontrol.wait (a CTA that drew the slot being stored waits before its gather)
+  pdl_trigger();
   const StoreCtl c = *a.ctl;
   const long long i = (long long)a.ctr->T - c.base;
   const long long slot = (c.count0 + i) % a.cap;
@@ -107,7 +110,6 @@ __global__ void store_step_kernel(StoreArgs a) {
     a.ring_t[slot] = c.t[i] ? 1 : 0;
     a.ctr->ring_size = c.count0 + i + 1 < a.cap ? c.count0 + i + 1 : a.cap;
   }
-  pdl_trigger();
 }
 
 void launch_store_step(const StoreArgs& a, cudaStream_t st) {
@@ -196,9 +198,20 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tr[8]));
   }
   if (threadIdx.x == 0) {
-    long long slot = j;
-    if (a.idx_in) slot = a.idx_in[j];  // prioritized replay (A41): drawn by the predecessor (a.late = 1)
-    else if (a.ctr) slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)j, a.ctr->ring_size);  // a1
+    long long slot = j, size = 0;
+    if (a.idx_in) {
+      slot = a.idx_in[j];  // prioritized replay (A41): drawn by the predecessor (a.late = 1)
+    } else if (a.store_ctl) {
+      // this step's Store (the predecessor) puts item T - base into slot (count0 + T - base) mod cap and makes the
+      // replay size min(cap, count0 + T - base + 1): the draw needs neither the Store's writes nor its size store
+      const unsigned long long T = a.ctr->T;
+      const long long i = (long long)T - a.store_ctl->base, n_new = a.store_ctl->count0 + i + 1;
+      size = n_new < a.cap ? n_new : a.cap;
+      slot = sample_slot(a.seed, a.rank, T, (unsigned)j, size);  // a1
+      if (slot == (a.store_ctl->count0 + i) % a.cap) pdl_wait();  // drew the slot being stored: wait for it
+    } else if (a.ctr) {
+      slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)j, a.ctr->ring_size);  // a1
+    }
     if (g == 0 && a.idx && !a.idx_in) a.idx[j] = (int)slot;
     mbar_init(&bar, 4);   // conv1: one commit per issuing warp
     mbar_init(&bar2, 4);  // conv2: likewise
@@ -211,7 +224,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     // next step's gather is an L2 hit with a warm TLB (a random 28 KB slot of a 56 GB ring
     // otherwise costs a page walk); harmless if a push changes the ring size before T+1.
     if (a.ctr && !a.idx_in) {
-      const long long nxt = sample_slot(a.seed, a.rank, a.ctr->T + 1, (unsigned)j, a.ctr->ring_size);
+      const long long nxt = sample_slot(a.seed, a.rank, a.ctr->T + 1, (unsigned)j, a.store_ctl ? size : a.ctr->ring_size);
       bulk_prefetch_l2(a.ring[g] + nxt * a.slot_stride, mnih::SLOT);
     }
   }
