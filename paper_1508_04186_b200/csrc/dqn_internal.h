@@ -256,27 +256,6 @@ void launch_widen_range(const __nv_bfloat16* src, float* dst, long long lo, long
 int server_round_blocks(long long shard, long long conv4, int conv_per_block);
 
 // bf16 tensor-core path, Mnih-2013 net (kernels_bf16.cu)
-struct FwdConvArgs {
-  const uint8_t* ring[2];          // s / s' rings (s2d) or a staging buffer (ctr == nullptr: image j = slot j)
-  const __nv_bfloat16* theta[2];   // canonical bf16 parameters (theta, theta^)
-  const float* theta_f32[2];       // canonical fp32 parameters (biases)
-  long long w1_off, b1_off, w2_off, b2_off;
-  int* idx;                        // out (group 0) [n]
-  const DevCounters* ctr;
-  unsigned long long seed;
-  unsigned rank;
-  int n;
-  __nv_bfloat16* a2;               // [groups*n][2592]
-  uint8_t* a1_save;                // [n][8][144][16] or nullptr
-  FusedAcquire acq;                // NEXT-1: the previous round's deliveries (acq.done == nullptr: none)
-  long long img_off;               // conv weight image (wimg.cuh) inside theta[g]
-  long long slot_stride;           // bytes between replay slots (28,224, or 35,280 with frame dedup)
-  int late;                        // 1: sample + gather after the PDL wait (the predecessor wrote the ring)
-  const int* idx_in;               // prioritized replay: the slots prio_sample_kernel drew (nullptr: a1's sampler)
-  const struct StoreCtl* store_ctl; // non-null (with late = 0): the predecessor is this step's in-graph Store; the
-  long long cap;                   // replay size and the stored slot come from StoreCtl, and only a CTA that drew
-                                   // the slot being stored waits for the Store before its gather
-};
 // dqn_store_and_train on the bf16 Mnih path: Alg. 1's Store as the first kernel of every step of the
 // replayed step graph. The graph is fixed, so the chunk of transitions and its position come from here
 // (written by store_ctl_kernel before the chunk's graphs): step T stores item T - base of the chunk into
@@ -300,6 +279,31 @@ struct StoreArgs {
   int dedup;
   const StoreCtl* ctl;
   DevCounters* ctr;
+};
+struct FwdConvArgs {
+  const uint8_t* ring[2];          // s / s' rings (s2d) or a staging buffer (ctr == nullptr: image j = slot j)
+  const __nv_bfloat16* theta[2];   // canonical bf16 parameters (theta, theta^)
+  const float* theta_f32[2];       // canonical fp32 parameters (biases)
+  long long w1_off, b1_off, w2_off, b2_off;
+  int* idx;                        // out (group 0) [n]
+  const DevCounters* ctr;
+  unsigned long long seed;
+  unsigned rank;
+  int n;
+  __nv_bfloat16* a2;               // [groups*n][2592]
+  uint8_t* a1_save;                // [n][8][144][16] or nullptr
+  FusedAcquire acq;                // NEXT-1: the previous round's deliveries (acq.done == nullptr: none)
+  long long img_off;               // conv weight image (wimg.cuh) inside theta[g]
+  long long slot_stride;           // bytes between replay slots (28,224, or 35,280 with frame dedup)
+  int late;                        // 1: sample + gather after the PDL wait (the predecessor wrote the ring)
+  const int* idx_in;               // prioritized replay: the slots prio_sample_kernel drew (nullptr: a1's sampler)
+  // store_fused (N = 1 dqn_store_and_train): this step's Alg. 1 Store runs in the extra CTA columns x < 14 after the
+  // PDL wait, image j in column j + 14; the draws use the replay size the Store makes (StoreCtl, T), and only a CTA
+  // that drew the slot being stored waits (store_flag >= T + 1) before its gather
+  int store_fused;
+  StoreArgs store;
+  unsigned long long* store_flag;
+  unsigned* store_join;            // the Store CTAs' join counter (monotone)
 };
 void launch_store_step(const StoreArgs& a, cudaStream_t st);
 void launch_store_ctl(StoreCtl* ctl, const uint8_t* s, const uint8_t* sn, const int32_t* a, const float* r,

@@ -186,6 +186,7 @@ struct dqn_ctx {
   long long graph_kernels[16] = {};
   // dqn_store_and_train on the bf16 Mnih path: the Store runs inside the step graphs (variant bit 16)
   StoreCtl* store_ctl = nullptr;
+  unsigned long long* store_flag = nullptr;  // the forward's fused Store: T + 1 once step T's item is in the ring
   bool graph_store = false;
   // prioritized replay (NEXT-4, A41; cfg.replay_prio_alpha != 0)
   bool prio = false;
@@ -437,7 +438,7 @@ static void free_all(dqn_ctx* c) {
                   c->diag_idx, c->diag_amax, c->head_dq, c->head_act, c->head_loss, c->q_stage, c->q_out, c->q_amax, c->d_stage,
                   c->theta_local_bf16, c->theta_hat_bf16, c->a2_bf16, c->a1_save,
                   c->dh_bf16, c->dz2_bf16, c->fc_partial, c->tc_counters, c->bwd_partial, c->q_stage_s2d,
-                  c->store_ctl, c->ptree.node, c->prio_maxp, c->head_delta, c->diag_delta, c->dx_canon, c->inbox};
+                  c->store_ctl, c->store_flag, c->ptree.node, c->prio_maxp, c->head_delta, c->diag_delta, c->dx_canon, c->inbox};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& G : c->gl) {
@@ -1549,9 +1550,14 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   const ConvShape& L1 = net.conv[0];
   const ConvShape& L2 = net.conv[1];
   cudaStream_t st = ctx->stream;
-  if (store) {  // Alg. 1 "Store" of this iteration's transition (dqn_store_and_train), then the step
-    StoreArgs sa{ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->slot_stride,
-                 ctx->dedup ? 1 : 0, ctx->store_ctl, ctx->ctr};
+  const StoreArgs sa{ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->slot_stride,
+                     ctx->dedup ? 1 : 0, ctx->store_ctl, ctx->ctr};
+  // N = 1: the Store runs inside the conv forward (its extra CTA), so the forward keeps its PDL overlap with the
+  // previous step's update and only a draw of the slot being stored waits for it (DQN_STORE_IN_FWD=0: own kernel)
+  const char* sf = getenv("DQN_STORE_IN_FWD");
+  const bool store_fused = store && ctx->world == 1 && !ctx->dedup && !ctx->prio && ctx->store_flag &&
+                           !(sf && atoi(sf) == 0);
+  if (store && !store_fused) {  // Alg. 1 "Store" of this iteration's transition (dqn_store_and_train), then the step
     PB("store", 1);
     launch_store_step(sa, st);
     PE();
@@ -1593,15 +1599,12 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   fa.acq = ctx->acq;
   fa.img_off = ctx->img_off;
   fa.slot_stride = ctx->slot_stride;
-  fa.late = store ? 1 : 0;
-  {  // N = 1 Store steps: the gather of every slot but the one being stored overlaps the Store (the slot draw
-     // needs only StoreCtl and T, both older than the Store)
-    const char* eg = getenv("DQN_STORE_EARLY_GATHER");
-    if (store && ctx->world == 1 && !ctx->dedup && !ctx->prio && !(eg && atoi(eg) == 0)) {
-      fa.late = 0;
-      fa.store_ctl = ctx->store_ctl;
-      fa.cap = ctx->cap;
-    }
+  fa.late = store && !store_fused ? 1 : 0;
+  if (store_fused) {
+    fa.store_fused = 1;
+    fa.store = sa;
+    fa.store_flag = ctx->store_flag;
+    fa.store_join = reinterpret_cast<unsigned*>(ctx->store_flag + 1);
   }
   if (ctx->prio) {  // the draws come from the sum tree: the forward waits for them (A41)
     enqueue_prio_sample(ctx, st);
@@ -2329,6 +2332,8 @@ extern "C" int dqn_store_and_train(dqn_ctx* ctx, int64_t k, const uint8_t* s, co
   if (!ctx->store_ctl && ctx->bf16 && !ctx->gpath && !ctx->prio && !(gs && atoi(gs) == 0)) {
     int rc0 = dalloc(ctx, &ctx->store_ctl, 1);
     if (rc0) return rc0;
+    if ((rc0 = dalloc(ctx, &ctx->store_flag, 2))) return rc0;  // monotone T + 1 of the last fused Store | join
+    CK(cudaMemsetAsync(ctx->store_flag, 0, 2 * sizeof(unsigned long long), ctx->stream));
     ctx->graph_store = true;
   }
   const long long T0 = ctx->T;
@@ -2444,6 +2449,8 @@ static int finish_steps(dqn_ctx* ctx, long long T0, long long k, long long kerne
       fflush(stderr);
     }
   }
+  if (hc.bad_input & 0x40000000u)
+    return set_err(ctx, DQN_ECUDA, "fused Store: a forward CTA's wait for the stored slot timed out");
   if (hc.bad_input & 0x80000000u)
     return set_err(ctx, DQN_ECUDA, "fused server round: peer barrier timed out (ranks out of step?)");
   if (ctx->bf16 && gconv_error())

@@ -80,16 +80,9 @@ __global__ void push_s2d_kernel(uint8_t* ring_s, uint8_t* ring_sn, int32_t* ring
 // Alg. 1 "Store" inside the step graph (dqn_store_and_train): step T writes item T - base of the chunk
 // (StoreCtl) into its ring slot exactly as push_s2d_kernel does, after the previous step's kernels (which
 // read the ring) completed; the conv forward that follows samples and gathers after its own PDL wait.
-__global__ void store_step_kernel(StoreArgs a) {
-  pdl_wait();
-  // the successor may launch now: the previous step is complete, and the forward reads this kernel's writes only
-  // after its own griddepcontrol.wait (a CTA that drew the slot being stored waits before its gather)
-  pdl_trigger();
-  const StoreCtl c = *a.ctl;
-  const long long i = (long long)a.ctr->T - c.base;
-  const long long slot = (c.count0 + i) % a.cap;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;  // (frame, pixel)
-  if (v < mnih::X_PIX * 4) {
+// one (frame, pixel) 16-byte piece v of item i of the chunk into ring slot `slot` (s and, unless deduplicated, s')
+__device__ __forceinline__ void store_piece(const StoreArgs& a, const StoreCtl& c, long long i, long long slot, int v) {
+  {
     const int f = v / mnih::X_PIX, p = v % mnih::X_PIX;
     const int py = p / 21, px = p % 21;
 #pragma unroll
@@ -104,11 +97,51 @@ __global__ void store_step_kernel(StoreArgs a) {
       *reinterpret_cast<uint4*>((which ? a.ring_sn : a.ring_s) + slot * a.stride + f * 7056 + p * 16) = o;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.ring_a[slot] = c.a[i];
-    a.ring_r[slot] = c.r[i];
-    a.ring_t[slot] = c.t[i] ? 1 : 0;
-    a.ctr->ring_size = c.count0 + i + 1 < a.cap ? c.count0 + i + 1 : a.cap;
+}
+
+// the item's action, reward, terminal flag and the new replay size (one thread)
+__device__ __forceinline__ void store_scalars(const StoreArgs& a, const StoreCtl& c, long long i, long long slot) {
+  a.ring_a[slot] = c.a[i];
+  a.ring_r[slot] = c.r[i];
+  a.ring_t[slot] = c.t[i] ? 1 : 0;
+  a.ctr->ring_size = c.count0 + i + 1 < a.cap ? c.count0 + i + 1 : a.cap;
+}
+
+__global__ void store_step_kernel(StoreArgs a) {
+  pdl_wait();
+  // the successor may launch now: the previous step is complete, and the forward reads this kernel's writes only
+  // after its own griddepcontrol.wait
+  pdl_trigger();
+  const StoreCtl c = *a.ctl;
+  const long long i = (long long)a.ctr->T - c.base;
+  const long long slot = (c.count0 + i) % a.cap;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;  // (frame, pixel)
+  if (v < mnih::X_PIX * 4) store_piece(a, c, i, slot, v);
+  if (blockIdx.x == 0 && threadIdx.x == 0) store_scalars(a, c, i, slot);
+}
+
+// the same Store as the forward's extra CTA (store_fused): after the PDL wait (the previous step, whose kernels
+// read the ring, is complete), then a gpu-scope release of T + 1 for the CTAs that drew this slot
+constexpr int kStoreCtas = (mnih::X_PIX * 4 + 127) / 128;  // one 16-byte piece per thread of 128-thread CTAs
+
+__device__ __forceinline__ void store_in_forward(const FwdConvArgs& fa) {
+  const StoreArgs& a = fa.store;
+  pdl_wait();
+  const StoreCtl c = *a.ctl;
+  const unsigned long long T = a.ctr->T;
+  const long long i = (long long)T - c.base;
+  const long long slot = (c.count0 + i) % a.cap;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < mnih::X_PIX * 4) store_piece(a, c, i, slot, v);
+  if (v == 0) store_scalars(a, c, i, slot);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // the last of the kStoreCtas CTAs to join releases T + 1
+    __threadfence();
+    const unsigned old = atomicAdd(fa.store_join, 1u);
+    if ((old + 1) % kStoreCtas == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(fa.store_flag), "l"(T + 1) : "memory");
+    }
   }
 }
 
@@ -183,7 +216,11 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, bar2, bar_ld;
   __shared__ uint32_t tbase;
-  const int j = blockIdx.x, g = blockIdx.y;
+  if (a.store_fused && blockIdx.x < kStoreCtas) {  // Alg. 1's Store of this step (group 0's extra CTAs)
+    if (blockIdx.y == 0) store_in_forward(a);
+    return;
+  }
+  const int j = blockIdx.x - (a.store_fused ? kStoreCtas : 0), g = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   st_stamp(ST_FWD, 0);
   uint8_t* sX = smem + FWD_SX;
@@ -201,14 +238,25 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     long long slot = j, size = 0;
     if (a.idx_in) {
       slot = a.idx_in[j];  // prioritized replay (A41): drawn by the predecessor (a.late = 1)
-    } else if (a.store_ctl) {
-      // this step's Store (the predecessor) puts item T - base into slot (count0 + T - base) mod cap and makes the
+    } else if (a.store_fused) {
+      // this step's Store (CTA column 0) puts item T - base into slot (count0 + T - base) mod cap and makes the
       // replay size min(cap, count0 + T - base + 1): the draw needs neither the Store's writes nor its size store
       const unsigned long long T = a.ctr->T;
-      const long long i = (long long)T - a.store_ctl->base, n_new = a.store_ctl->count0 + i + 1;
-      size = n_new < a.cap ? n_new : a.cap;
+      const StoreCtl* c = a.store.ctl;
+      const long long i = (long long)T - c->base, n_new = c->count0 + i + 1;
+      size = n_new < a.store.cap ? n_new : a.store.cap;
       slot = sample_slot(a.seed, a.rank, T, (unsigned)j, size);  // a1
-      if (slot == (a.store_ctl->count0 + i) % a.cap) pdl_wait();  // drew the slot being stored: wait for it
+      if (slot == (c->count0 + i) % a.store.cap) {  // drew the slot being stored: wait for the Store's release
+        long long spin = 0;
+        for (;;) {
+          unsigned long long v;
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.store_flag) : "memory");
+          if (v >= T + 1) break;
+          __nanosleep(32);
+          if (++spin > (1LL << 26)) { atomicOr(&a.store.ctr->bad_input, 0x40000000u); break; }
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy stores before the TMA read
+      }
     } else if (a.ctr) {
       slot = sample_slot(a.seed, a.rank, a.ctr->T, (unsigned)j, a.ctr->ring_size);  // a1
     }
@@ -224,7 +272,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
     // next step's gather is an L2 hit with a warm TLB (a random 28 KB slot of a 56 GB ring
     // otherwise costs a page walk); harmless if a push changes the ring size before T+1.
     if (a.ctr && !a.idx_in) {
-      const long long nxt = sample_slot(a.seed, a.rank, a.ctr->T + 1, (unsigned)j, a.store_ctl ? size : a.ctr->ring_size);
+      const long long nxt = sample_slot(a.seed, a.rank, a.ctr->T + 1, (unsigned)j, a.store_fused ? size : a.ctr->ring_size);
       bulk_prefetch_l2(a.ring[g] + nxt * a.slot_stride, mnih::SLOT);
     }
   }
@@ -371,7 +419,7 @@ __global__ void __launch_bounds__(128) fwd_conv_bf16_kernel(FwdConvArgs a) {
 }
 
 void launch_fwd_conv_bf16(const FwdConvArgs& a, int groups, cudaStream_t st) {
-  dim3 grid(a.n, groups);
+  dim3 grid(a.n + (a.store_fused ? kStoreCtas : 0), groups);
   launch_pdl(fwd_conv_bf16_kernel, grid, dim3(128), FWD_SMEM, st, a);
 }
 
