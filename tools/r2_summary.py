@@ -31,10 +31,13 @@ rows = [("n1", "BJ.configs[1]: Mnih, b = 32, 1M-slot replay, C = 1000", 1),
         ("c5_n4", "BJ.configs[4], fused round", 4),
         ("c2_prio", "BJ.configs[1] + prioritized replay (A41)", 1)]
 print("# Round 2 profiles — B200 (sm_100a)\n")
-print("All numbers come from one 4-GPU `gpurun` box at the end of the round (`tools/final_r2.sh`): the GPU suite")
-print("with test ids, smoke, the bench lines, the reference arm, the model-size sweep at N = 1 and 4, and (one GPU)")
-print("the ncu launch lists and one `ncu --set full` step of the Mnih and generic paths. Every ncu pass ran after")
-print("the same command exited 0 without ncu. Clocks: see each line's `clocks` (1965 MHz, no throttle reason).\n")
+print("The numbers come from `gpurun` boxes at the end of the round. `tools/final_r2.sh` on one 4-GPU box produced the")
+print("reference arm, the sweep, and the ncu launch lists and captures. Every ncu pass ran after the same command had")
+print("exited 0 without ncu. Lines whose code changed afterwards were re-measured on later boxes:")
+print("* BJ.configs[2] (`tools/final_r2_round.sh`);")
+print("* BJ.configs[3] and the GPU suite (`tools/final_r2_last.sh`);")
+print("* BJ.configs[1] at N = 1 and a 2-GPU suite (`tools/final_r2_n1.sh`).")
+print("Clocks: see each line's `clocks` (1965 MHz, no throttle reason).\n")
 print("## Bench lines (`bench.py`, device-timed, max over ranks)\n")
 print("| file | workload | N | transitions/s | µs/step | e2e | dominant region | bound, fraction | step tensor / HBM |")
 print("|---|---|---|---|---|---|---|---|---|")
