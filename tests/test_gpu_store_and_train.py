@@ -20,11 +20,14 @@ def _cuda():
     yield
 
 
-@pytest.mark.parametrize("prec,device_inputs,cap", [(D.FP32, False, 64), (D.BF16, False, 64), (D.BF16, True, 64),
-                                                      (D.BF16, False, 40)])
-def test_store_and_train_equals_alternating_calls(prec, device_inputs, cap):
+@pytest.mark.parametrize("prec,device_inputs,cap,b", [(D.FP32, False, 64, 8), (D.BF16, False, 64, 16),
+                                                        (D.BF16, True, 64, 16), (D.BF16, False, 40, 16),
+                                                        (D.BF16, False, 300, 256)])
+def test_store_and_train_equals_alternating_calls(prec, device_inputs, cap, b):
+    """b = 256: 256 image CTAs per group beside the forward's 14 Store CTAs; with 34-45 items in the replay
+    nearly every step has draws of the slot being stored (they wait for the Store's release)."""
     import torch
-    b, k, pre = 16 if prec == D.BF16 else 8, 12, 33
+    k, pre = 12, 33
     dc, on, _ = nets(minibatch=b, replay_capacity=cap, precision=prec, lr=1e-4)
     theta0 = he_theta(on, 5)
     _, raw = replay(on, pre + k, 9)
