@@ -1552,11 +1552,11 @@ static int enqueue_step_bf16(dqn_ctx* ctx, bool fetch, bool refresh, bool push, 
   cudaStream_t st = ctx->stream;
   const StoreArgs sa{ctx->ring_s, ctx->ring_sn, ctx->ring_a, ctx->ring_r, ctx->ring_t, ctx->cap, ctx->slot_stride,
                      ctx->dedup ? 1 : 0, ctx->store_ctl, ctx->ctr};
-  // N = 1: the Store runs inside the conv forward (its extra CTA), so the forward keeps its PDL overlap with the
-  // previous step's update and only a draw of the slot being stored waits for it (DQN_STORE_IN_FWD=0: own kernel)
+  // N = 1 or the fused server round: the Store runs inside the conv forward (its extra CTAs), so the forward keeps
+  // its PDL overlap with the previous kernel and only a draw of the slot being stored waits for it (DQN_STORE_IN_FWD=0: own kernel)
   const char* sf = getenv("DQN_STORE_IN_FWD");
-  const bool store_fused = store && ctx->world == 1 && !ctx->dedup && !ctx->prio && ctx->store_flag &&
-                           !(sf && atoi(sf) == 0);
+  const bool store_fused = store && (ctx->world == 1 || ctx->fused_comm) && !ctx->dedup && !ctx->prio &&
+                           ctx->store_flag && !(sf && atoi(sf) == 0);
   if (store && !store_fused) {  // Alg. 1 "Store" of this iteration's transition (dqn_store_and_train), then the step
     PB("store", 1);
     launch_store_step(sa, st);

@@ -203,3 +203,14 @@ def test_two_replicas_per_gradient_rule(tmp_path, n_push):
     assert int(res["n"]) == ref["n"] == 2 * (6 // n_push)
     assert np.array_equal(res["idx"], ref["idx"].astype(np.int32))
     assert delta_rel(res["theta"], th0, ref["theta"], th0, on, ulps=ref["n"]) < 1e-5
+
+
+@pytest.mark.parametrize("env", [{}, {"DQN_STORE_IN_FWD": "0"}], ids=["store-in-forward", "store-kernel"])
+def test_two_replicas_store_and_train_equals_alternating_calls(tmp_path, env):
+    """Alg. 1's loop at N = 2 on the bf16 Mnih path with the fused server round: one dqn_store_and_train call
+    equals alternating push(1) + train(1) calls bit for bit on every rank (indices, losses, server theta)."""
+    if n_gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_ranks(2, tmp_path, "--precision", "bf16", "--b", "32", "--store", "10", "--lr", "1e-4", env=env,
+                    tag="store")
+    assert bool(res["identical"])

@@ -34,6 +34,9 @@ def main():
     ap.add_argument("--async-free", action="store_true", help="DQN_ASYNC (newest published generation, A40)")
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--server-rule", type=int, default=0, help="0 mean (A7), 1 per gradient (A33)")
+    ap.add_argument("--store", type=int, default=0,
+                    help="Alg. 1's loop: push 33 items, then this many store+step iterations, once as alternating "
+                         "push(1) + train(1) calls and once as one dqn_store_and_train call (bit identity)")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -63,6 +66,9 @@ def main():
         from tests.helpers import gated_theta
         theta0 = gated_theta(on, 3)
     _, raw = replay(on, 250, 100 + rank)
+    if a.store:
+        store_mode(a, D, dc, theta0, raw, rank, world, obj[0], dist)
+        return
     runs = []
     for _ in range(a.repeat):
         g = D.DQN(dc, rank=rank, world=world, nccl_id=obj[0] if not runs else None, init_params=theta0) \
@@ -90,6 +96,43 @@ def main():
                  step_generation=np.stack([x.cpu().numpy() for x in gens]),
                  identical=all(np.array_equal(t, runs[0][0]) and np.array_equal(r, runs[0][1]) for t, r in runs))
     g.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def store_mode(a, D, dc, theta0, raw, rank, world, nccl_id, dist):
+    import torch
+    head = tuple(x[:33] for x in raw)
+    tail = tuple(x[33:33 + a.store] for x in raw)
+    res = []
+    for how in ("alternating", "store_and_train"):
+        if how == "alternating":
+            uid = nccl_id
+        else:
+            o2 = [D.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(o2, src=0)
+            uid = o2[0]
+        g = D.DQN(dc, rank=rank, world=world, nccl_id=uid, init_params=theta0)
+        g.push(*head)
+        if how == "alternating":
+            idx, loss = [], []
+            for i in range(a.store):
+                g.push(*(x[i:i + 1] for x in tail))
+                o = g.train(1, want_idx=True, want_loss=True)
+                idx.append(o["idx"][0])
+                loss.append(o["loss"][0])
+            idx, loss = np.stack(idx), np.array(loss, np.float32)
+        else:
+            o = g.train(a.store, want_idx=True, want_loss=True, store=tail)
+            idx, loss = o["idx"], o["loss"]
+        th = g.params(D.PARAMS_SERVER)  # collective
+        res.append((idx, loss, th))
+        g.close()
+    same = all(np.array_equal(x, y) for x, y in zip(res[0], res[1]))
+    flag = torch.tensor([1 if same else 0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        np.savez(a.out, identical=bool(flag.item()), theta=res[1][2])
     dist.barrier()
     dist.destroy_process_group()
 
