@@ -34,7 +34,7 @@ print("# Round 2 profiles — B200 (sm_100a)\n")
 print("The numbers come from `gpurun` boxes at the end of the round. `tools/final_r2.sh` on one 4-GPU box produced the")
 print("reference arm, the sweep, and the ncu launch lists and captures. Every ncu pass ran after the same command had")
 print("exited 0 without ncu. Lines whose code changed afterwards were re-measured on later boxes:")
-print("* BJ.configs[2] (`tools/final_r2_round.sh`);")
+print("* BJ.configs[2] (`tools/final_r2_round.sh`, then `tools/final_r2_multi.sh`);")
 print("* BJ.configs[3] and the GPU suite (`tools/final_r2_last.sh`);")
 print("* BJ.configs[1] at N = 1 and a 2-GPU suite (`tools/final_r2_n1.sh`).")
 print("Clocks: see each line's `clocks` (1965 MHz, no throttle reason).\n")
