@@ -120,7 +120,7 @@ __global__ void store_step_kernel(StoreArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) store_scalars(a, c, i, slot);
 }
 
-// the same Store as the forward's extra CTA (store_fused): after the PDL wait (the previous step, whose kernels
+// the same Store in the forward's extra CTAs (store_fused): after the PDL wait (the previous step, whose kernels
 // read the ring, is complete), then a gpu-scope release of T + 1 for the CTAs that drew this slot
 constexpr int kStoreCtas = (mnih::X_PIX * 4 + 127) / 128;  // one 16-byte piece per thread of 128-thread CTAs
 
